@@ -1,0 +1,425 @@
+"""Benchmark of the RAFEM hot path on B200.
+
+Metric (BASELINE.json): accepted RAFEM time steps per second of a full
+simulation.  Workload (configs[1], "the paper's larger workload"): the
+mesh-B analog generate_box_mesh(20, 20, 21) (8,400 nodes, 43,320 tets,
+16,800 dofs), the full 900 s simulated ablation (96 accepted steps, 214
+corrector passes), GMRES/PCG with Jacobi at tol 1e-10.
+
+One bench step = one full 900 s simulation.
+  value : native device loop (rafem_simulate), mesh and state in HBM.
+  e2e   : the reference-shaped public API (run_simulation -> assemble_global
+          -> solve) with host numpy buffers crossing the boundary every pass.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference algorithm's CPU restatement
+(oracle/rafem_oracle.py, a bit-exact numpy port of rafem 0.1.0, pinned
+against the reference's golden vectors) on the host cores; each of its
+steps is a window of 8 accepted steps of one continuing simulation.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MESH_B = (20, 20, 21)
+TOTAL_TIME = 900.0
+METRIC = "time-steps/s (full 900 s RAFEM simulation, mesh-B analog)"
+REF_WINDOW = 8
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--backend", default="pcg", choices=["pcg", "gmres"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c3", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")),
+            int(os.environ.get("WORLD_SIZE", "1")))
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+
+class ClockSampler:
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as exc:  # noqa: BLE001
+            self.nv = None
+            self.err = str(exc)
+
+    _NAMES = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+              0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
+              0x2: "applications_clocks_setting", 0x100: "display_clock_setting"}
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self._NAMES.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle restatement of the reference; never the measured product)
+
+def cpu_sample(max_steps: int, threads_env: dict) -> dict:
+    """Time the oracle port on this host in a subprocess (BLAS threads set)."""
+    code = (
+        "import sys,json,time; sys.path.insert(0, %r)\n"
+        "from oracle import rafem_oracle as O\n"
+        "m = O.box_mesh(*%r)\n"
+        "t0 = time.perf_counter()\n"
+        "r = O.run(m, {0: O.OMaterial()}, O.OSim(total_time=%r), keep_fields=False, max_steps=%d)\n"
+        "w = time.perf_counter() - t0\n"
+        "print(json.dumps({'steps': r.accepted_steps, 'wall_s': w, 'passes': r.corrector_passes}))\n"
+    ) % (ROOT, MESH_B, TOTAL_TIME, max_steps)
+    env = dict(os.environ, **threads_env)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         timeout=900)
+    if out.returncode != 0:
+        raise RuntimeError(out.stderr[-2000:])
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    from oracle import rafem_oracle as O
+    cores = os.cpu_count() or 1
+    mesh = O.box_mesh(*MESH_B)
+    # one continuing simulation, advanced REF_WINDOW accepted steps per bench step
+    state = {"run": None}
+
+    def gen():
+        while True:
+            for rec in _oracle_steps(O, mesh):
+                yield rec
+
+    it = gen()
+
+    def window():
+        t0 = time.perf_counter()
+        for _ in range(REF_WINDOW):
+            next(it)
+        return time.perf_counter() - t0
+
+    for _ in range(args.warmup):
+        window()
+    times = [window() for _ in range(args.steps)]
+    total = sum(times)
+    value = REF_WINDOW * args.steps / total
+    del state
+    line = {
+        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (generated Kuhn box mesh; reference physics defaults)",
+        "impl": "reference",
+        "config": {"workload": "rafem-B900", "mesh": "generate_box_mesh(20,20,21)", "dofs": 16800,
+                   "total_time_s": TOTAL_TIME, "solver": "gmres(30)+jacobi tol 1e-10 (reference)",
+                   "step": f"{REF_WINDOW} accepted time steps of one continuing simulation"},
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} windows x {REF_WINDOW} accepted steps after "
+                                   f"{args.warmup} warm-up windows (bit-exact numpy port of rafem 0.1.0)"},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _oracle_steps(O, mesh):
+    """Generator over accepted steps of the oracle's time loop (fem.py:554-644)."""
+    cfg = O.OSim(total_time=TOTAL_TIME)
+    N = mesh.node_count
+    geom = O.geometry(mesh)
+    T = np.full(N, cfg.initial_temp)
+    V = np.zeros(N)
+    T_prev = T.copy()
+    t, dt_cur, dt_prev, step = 0.0, cfg.dt_init, cfg.dt_init, 0
+    mats = {0: O.OMaterial()}
+    while t < cfg.total_time:
+        remaining = cfg.total_time - t
+        last = dt_cur >= remaining
+        dt = remaining if last else dt_cur
+        t_it = T + (dt / dt_prev) * (T - T_prev) if step >= 1 else T.copy()
+        v_it = V.copy()
+        x_old = np.empty(2 * N)
+        x_old[0::2], x_old[1::2] = v_it, t_it
+        ok, used = False, 0
+        for it_ in range(1, cfg.max_corrector_iters + 1):
+            used = it_
+            s = O.assemble(mesh, mats, cfg.applied_voltage, cfg.boundary_temp, t_it, v_it, T, dt, geom=geom)
+            x_new, st = O.gmres(s.row_ptr, s.col_idx, s.vals, s.rhs.copy(), x0=x_old.copy(),
+                                restart_m=30, tol=cfg.tolerance, precondition="jacobi")
+            if not st.converged:
+                break
+            delta = float(np.max(np.abs(x_new - x_old) / np.maximum(1.0, np.abs(x_old))))
+            v_it, t_it = x_new[0::2].copy(), x_new[1::2].copy()
+            x_old = x_new
+            if delta < cfg.corrector_tol:
+                ok = True
+                break
+        if not ok:
+            dt_cur = max(dt * 0.5, cfg.dt_min)
+            continue
+        T_prev, T, V = T, t_it, v_it
+        dt_prev = dt
+        t = cfg.total_time if last else t + dt
+        step += 1
+        dt_cur = min(dt * 1.5, cfg.dt_max) if used <= 5 else (max(dt * 0.75, cfg.dt_min) if used >= 20 else dt)
+        yield step
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def pcg_iter_bytes(N, S):
+    """Algorithmic HBM bytes of one fused PCG iteration on the paired layout.
+
+    SpMV: 20 B per slot (int32 column + (V,T) double2) + 4(N+1) row_ptr.
+    Vectors, 16 B per node each: SpMV phase reads z, p_old; writes p, q;
+    update phase reads x, p, r, q, minv; writes x, r, z  -> 12 x 16N.
+    """
+    return 20 * S + 4 * (N + 1) + 12 * 16 * N
+
+
+def gmres_iter_bytes(N, S, k_avg):
+    """GMRES(m) CGS2 step k: SpMV + 2 passes over k+1 basis vectors + updates."""
+    n = 2 * N
+    return 20 * S + 4 * (N + 1) + 16 * N + (32 * (k_avg + 1) + 56) * n
+
+
+def run_ours(args):
+    import torch
+    rank, local, world = dist_env()
+    os.environ["RAFEM_DEVICE"] = str(local)
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://")
+    from paper_2409_13036_b200 import _native as nat
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh, run_simulation
+    from paper_2409_13036_b200.timeloop import DeviceRun
+
+    peaks = {}
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        peaks = json.load(open(pk))
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+
+    mesh = generate_box_mesh(*MESH_B)
+    mat = MaterialParams.default()
+    cfg = SimConfig(total_time=TOTAL_TIME, solver=SolverConfig(backend=args.backend, precondition="jacobi"))
+    runner = DeviceRun(mesh, mat)
+    stream = torch.cuda.ExternalStream(nat.lib().rafem_stream(nat.context()))
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MB > L2
+
+    def one(record):
+        recs, summ = runner.run(cfg, record_fields=record)
+        return summ
+
+    for _ in range(args.warmup):
+        one(False)
+    launches0 = nat.kernel_launches()
+    times, summs = [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            if world > 1:
+                import torch.distributed as dist
+                dist.barrier()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            summs.append(one(False))
+            ev1.record(stream)
+            ev1.synchronize()
+            times.append(ev0.elapsed_time(ev1))
+            torch.cuda.synchronize()
+    launches = nat.kernel_launches() - launches0
+    total_ms = float(sum(times))
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    steps_per_run = summs[0].accepted_steps
+    value = world * args.steps * steps_per_run / (total_ms / 1e3)
+
+    # roofline of the dominant kernel (the persistent Krylov solve)
+    S, N = runner.dm.slots, runner.dm.node_count
+    iters = sum(s.total_solver_iterations for s in summs)
+    passes = sum(s.passes for s in summs)
+    solve_ms = sum(s.solve_ms for s in summs)
+    asm_ms = sum(s.assemble_ms for s in summs)
+    if args.backend == "pcg":
+        bytes_total = iters * pcg_iter_bytes(N, S) + passes * (20 * S + 4 * (N + 1) + 6 * 16 * N)
+    else:
+        bytes_total = iters * gmres_iter_bytes(N, S, 15) + passes * (20 * S + 4 * (N + 1) + 48 * N)
+    achieved = bytes_total / (solve_ms / 1e3) / 1e9 if solve_ms > 0 else 0.0
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None,
+                "kernel": f"{args.backend}_kernel<2,true,false> (persistent cooperative solve)",
+                "launches": passes, "avg_launch_us": 1e3 * solve_ms / max(passes, 1),
+                "share_of_step": solve_ms / total_ms if world == 1 else None,
+                "peak_source": peak_src,
+                "note": "paper-scale mesh: working set ~5 MB lives in L2; kernel is barrier-latency bound"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (generated Kuhn box mesh; reference physics defaults)",
+        "config": {"workload": "rafem-B900", "mesh": "generate_box_mesh(20,20,21)", "dofs": 2 * N,
+                   "slots": S, "total_time_s": TOTAL_TIME, "accepted_steps_per_run": steps_per_run,
+                   "corrector_passes_per_run": summs[0].passes,
+                   "solver_iterations_per_run": summs[0].total_solver_iterations,
+                   "solver": f"{args.backend}+jacobi tol 1e-10", "parallelism": f"replicas x{world}",
+                   "step": "one full 900 s simulation", "l2": "flushed (256 MB write) between timed steps",
+                   "assemble_ms_per_run": asm_ms / args.steps, "solve_ms_per_run": solve_ms / args.steps},
+        "roofline": roofline,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+
+    if rank == 0 and not args.no_e2e:
+        line["e2e"] = e2e_leg(mesh, mat, args, run_simulation, SimConfig, SolverConfig, world)
+    if rank == 0 and not args.no_c3:
+        try:
+            line["spmv_c3"] = c3_leg(hbm_peak, peak_src)
+        except Exception as exc:  # noqa: BLE001
+            line["spmv_c3"] = {"error": str(exc)[:300]}
+    if rank == 0 and not args.no_cpu:
+        try:
+            smp = cpu_sample(24, {"OPENBLAS_NUM_THREADS": "1", "OMP_NUM_THREADS": "1"})
+            line["cpu_baseline"] = {"value": smp["steps"] / smp["wall_s"], "unit": "steps/s", "cores": 1,
+                                    "kind": "port",
+                                    "sample": f"first {smp['steps']} accepted steps of the same 900 s run "
+                                              f"({smp['passes']} passes, {smp['wall_s']:.1f} s), bit-exact "
+                                              "numpy port of rafem 0.1.0, GMRES(30)+Jacobi 1e-10, 1 BLAS thread"}
+        except Exception as exc:  # noqa: BLE001
+            line["cpu_baseline"] = {"error": str(exc)[:300]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def e2e_leg(mesh, mat, args, run_simulation, SimConfig, SolverConfig, world):
+    """Same metric through the public plug-in API with host buffers each pass."""
+    cfg = SimConfig(total_time=TOTAL_TIME, solver=SolverConfig(backend=args.backend, precondition="jacobi"))
+    run_simulation(mesh, mat, cfg)  # warm (mesh upload + symbolic phase cached)
+    reps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        summ = run_simulation(mesh, mat, cfg)
+    wall = time.perf_counter() - t0
+    N = mesh.node_count
+    passes = summ.total_corrector_iters
+    # per pass: H2D t_iter, v_iter, t_prev (3N f64) + b, x0 (2 x 2N f64); D2H rhs + x (2 x 2N f64)
+    h2d = passes * 8 * (3 * N + 4 * N)
+    d2h = passes * 8 * (4 * N) + passes * 16
+    return {"value": summ.accepted_steps * reps / wall, "unit": "steps/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "reps": reps,
+            "path": "run_simulation -> assemble_global -> solve (host numpy in/out every pass)"}
+
+
+def c3_leg(hbm_peak, peak_src):
+    """1M-dof roofline study (configs[2]): SpMV and cold PCG solve on the device."""
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, assemble_global, generate_box_mesh, solve
+    mesh = generate_box_mesh(80, 80, 79)
+    n = mesh.node_count
+    t = np.full(n, 37.0)
+    s = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, np.zeros(n), t, 0.5)
+    h = s.device
+    import ctypes as C
+    from paper_2409_13036_b200 import _native as nat
+    ms = C.c_double()
+    nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 50, C.byref(ms)), "spmv bench")
+    S, N = h.mesh.slots, n
+    b_paired = 20 * S + 4 * (N + 1) + 16 * N + 16 * N
+    b_csr = 12 * (2 * S) + 4 * (2 * N + 1) + 8 * 2 * N + 8 * 2 * N
+    ach = b_paired / (ms.value / 1e3) / 1e9
+    x0 = np.empty(2 * n)
+    x0[0::2], x0[1::2] = 0.0, 37.0
+    x, st = solve(s.matrix, s.rhs, x0=x0, config=SolverConfig(backend="pcg", precondition="jacobi"))
+    it_bytes = pcg_iter_bytes(N, S)
+    solve_ach = st.iterations * it_bytes / (st.device_ms / 1e3) / 1e9 if st.device_ms else 0.0
+    return {"workload": "generate_box_mesh(80,80,79) cold system, 1,011,200 dofs",
+            "spmv": {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                     "frac_of_8TBs": ach / 8000.0, "us_per_launch": 1e3 * ms.value,
+                     "bytes_per_launch": b_paired, "layout": "node-paired CSR (int32 col + double2 per slot)",
+                     "csr_equivalent_bytes": b_csr, "csr_equivalent_GBs": b_csr / (ms.value / 1e3) / 1e9,
+                     "peak_source": peak_src},
+            "pcg_cold_solve": {"iterations": st.iterations, "device_ms": st.device_ms,
+                               "us_per_iteration": 1e3 * st.device_ms / max(st.iterations, 1),
+                               "achieved_GBs": solve_ach, "frac": solve_ach / hbm_peak,
+                               "final_relative_residual": st.final_relative_residual}}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,200 @@
+/*
+ * rafem_b200.h — C ABI of the B200-native RAFEM hot path (librafem_b200.so).
+ *
+ * The reference (rafem 0.1.0, /root/reference/pkg/src/rafem) is pure
+ * Python; its plugin seam is two module globals that corrector_step
+ * calls (fem.py:47-48, 492, 501):
+ *
+ *     assemble_global(mesh, material, config, t_iter, v_iter, t_prev, dt,
+ *                     apply_constraints=True, equilibrate=True, threads=None)
+ *                                                       (fem.py:325-336)
+ *     solve(a, b, x0=None, config=None, session=None, tracer=None,
+ *           trace_step=-1, trace_corrector_iter=-1)     (solver.py:580-589)
+ *
+ * plus the sparse kernels they rest on, spmv (sparse.py:205-219) and
+ * coo_to_csr (sparse.py:164-197).  These entry points are what a ctypes
+ * binding of that seam needs (see INTEGRATION.md for the binding).
+ * All pointers are HOST pointers unless a name ends in _dev.  Every call
+ * is synchronous with respect to the host unless stated otherwise.
+ *
+ * Status codes map onto the reference's exception taxonomy:
+ *   RAFEM_OK              0
+ *   RAFEM_ERR_BREAKDOWN   1  -> rafem.solver.GmresBreakdownError (solver.py:73, 522)
+ *   RAFEM_ERR_INVALID     2  -> ValueError (solver.py:173-181, 399-417; fem.py:354-358)
+ *   RAFEM_ERR_PHYSICS     3  -> rafem.fem.PhysicsRangeError (fem.py:272-278)
+ *   RAFEM_ERR_UNSUPPORTED 4  -> NotImplementedError (e.g. pattern too dense)
+ *   RAFEM_ERR_STEP_FAILURE 5 -> rafem.fem.StepFailureError (fem.py:76-82, 629-631)
+ *   RAFEM_ERR_CUDA       -1  -> RuntimeError(rafem_last_error(ctx))
+ */
+#ifndef RAFEM_B200_H
+#define RAFEM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RAFEM_OK 0
+#define RAFEM_ERR_BREAKDOWN 1
+#define RAFEM_ERR_INVALID 2
+#define RAFEM_ERR_PHYSICS 3
+#define RAFEM_ERR_UNSUPPORTED 4
+#define RAFEM_ERR_STEP_FAILURE 5
+#define RAFEM_ERR_CUDA (-1)
+
+/* Krylov method (solver.py:50 lists the reference backends; only its
+ * iterative one is on the device path, plus PCG for SPD FEM systems). */
+#define RAFEM_METHOD_GMRES 0
+#define RAFEM_METHOD_PCG 1
+
+#define RAFEM_PRECOND_NONE 0
+#define RAFEM_PRECOND_JACOBI 1
+
+/* Dirichlet kind per interleaved dof (fem.py:403-413). */
+#define RAFEM_DOF_FREE 0
+#define RAFEM_DOF_APPLIED_VOLTAGE 1 /* 2*electrode_pos      -> config.applied_voltage */
+#define RAFEM_DOF_ZERO 2            /* 2*electrode_neg      -> 0.0                    */
+#define RAFEM_DOF_BOUNDARY_TEMP 3   /* 2*outer_boundary + 1 -> config.boundary_temp   */
+
+typedef struct rafem_ctx rafem_ctx;
+typedef struct rafem_mesh rafem_mesh;     /* mesh + symbolic pattern + geometry, on device  */
+typedef struct rafem_system rafem_system; /* one assembled corrector-pass system, on device */
+typedef struct rafem_matrix rafem_matrix; /* a general CSR uploaded from the host            */
+
+/* SolverConfig (solver.py:81-110) restricted to the iterative path. */
+typedef struct {
+    int32_t method;          /* RAFEM_METHOD_*                                   */
+    int32_t restart_m;       /* GMRES(m) restart length, >= 1                    */
+    double tolerance;        /* relative residual target, in (0, 1)              */
+    int64_t max_total_iters; /* <= 0 means 10 * n (solver.py:411)                */
+    int32_t precondition;    /* RAFEM_PRECOND_*                                  */
+    int32_t grid_ctas;       /* 0 = auto; otherwise persistent-kernel CTA count  */
+} rafem_solver_params;
+
+/* SolveStats (solver.py:113-130). */
+typedef struct {
+    int64_t iterations;          /* inner steps (Arnoldi / CG iterations)          */
+    int64_t restarts;            /* cycles - 1                                     */
+    double final_relative_residual; /* last TRUE residual ||b-Ax||/||b||           */
+    int32_t converged;
+    int32_t stagnated;
+    int64_t cycles;              /* entries of cycle_lens                          */
+    int64_t history_len;         /* total history entries (may exceed hist_cap)    */
+    double device_ms;            /* CUDA-event time of the solve kernel            */
+} rafem_solve_stats;
+
+typedef struct {
+    double dt;                 /* > 0 (fem.py:354-355)                          */
+    double applied_voltage;    /* SimConfig.applied_voltage (fem.py:131)        */
+    double boundary_temp;      /* SimConfig.boundary_temp (fem.py:132)          */
+    int32_t apply_constraints; /* fem.py:333                                    */
+    int32_t equilibrate;       /* fem.py:334                                    */
+} rafem_assemble_params;
+
+/* SimConfig (fem.py:121-147) for the native time loop. */
+typedef struct {
+    double total_time, dt_init, dt_min, dt_max, corrector_tol;
+    int32_t max_corrector_iters;
+    int32_t record_fields;     /* 1: copy every accepted (V,T) dof vector out    */
+    double applied_voltage, boundary_temp, initial_temp;
+    int64_t max_steps;         /* <= 0: run to total_time; else stop after n     */
+    rafem_solver_params solver;
+} rafem_sim_params;
+
+/* SimulationSummary (fem.py:543-551). */
+typedef struct {
+    int64_t accepted_steps, total_corrector_iters, total_solver_iterations, dt_halvings;
+    int64_t passes;            /* corrector passes (assembly + solve pairs)      */
+    double final_time;
+    int32_t status;            /* RAFEM_OK, or the error that aborted the run    */
+    int32_t failed_step;       /* step index of a StepFailureError, else -1      */
+    double failed_dt;
+    double wall_ms;            /* host wall clock of the whole loop              */
+    double assemble_ms, solve_ms; /* CUDA-event sums per region                  */
+    int64_t bad_element;       /* PhysicsRangeError element, else -1             */
+} rafem_sim_summary;
+
+/* ---- context ----------------------------------------------------------- */
+int rafem_ctx_create(int device, rafem_ctx** out);
+void rafem_ctx_destroy(rafem_ctx* ctx);
+const char* rafem_last_error(const rafem_ctx* ctx);
+int rafem_device_info(rafem_ctx* ctx, int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor,
+                      int64_t* total_mem);
+/* launches of the library's own kernels since ctx creation */
+int64_t rafem_kernel_launches(const rafem_ctx* ctx);
+/* the cudaStream_t every library call runs on (for external CUDA events) */
+void* rafem_stream(const rafem_ctx* ctx);
+
+/* ---- sparse.py ----------------------------------------------------------- */
+/* spmv (sparse.py:205-219): y = A x, each row summed left to right over its
+ * stored entries with separately rounded products — bit-identical to the
+ * reference's bincount route. */
+int rafem_spmv(rafem_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row_ptr,
+               const int64_t* col_idx, const double* vals, const double* x, double* y);
+
+/* coo_to_csr (sparse.py:164-197): stable device sort by (row, col), runs
+ * summed first-to-last from 0.0.  Outputs must hold nnz_in entries;
+ * *nnz_out receives the compressed count. */
+int rafem_coo_to_csr(rafem_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz_in,
+                     const int64_t* rows, const int64_t* cols, const double* vals,
+                     int64_t* row_ptr_out, int64_t* col_idx_out, double* vals_out,
+                     int64_t* nnz_out);
+
+/* ---- general CSR solve (solver.py:580-636 with a host CsrMatrix) --------- */
+int rafem_matrix_create(rafem_ctx* ctx, int64_t nrows, int64_t nnz, const int64_t* row_ptr,
+                        const int64_t* col_idx, const double* vals, rafem_matrix** out);
+void rafem_matrix_destroy(rafem_matrix* a);
+int rafem_matrix_solve(rafem_matrix* a, const double* b, const double* x0 /* nullable */,
+                       const rafem_solver_params* p, double* x_out, rafem_solve_stats* st,
+                       double* hist, int64_t hist_cap, int64_t* cycle_lens, int64_t cycle_cap);
+
+/* ---- mesh, assembly (fem.py:212-430) -------------------------------------- */
+/* Symbolic phase, once per mesh: node pattern, incidence lists, slot map and
+ * element geometry, all on device.  tets are 0-based node ids; region_index
+ * maps each tet to a row of the per-region tables (k, rho_c, sigma0, alpha,
+ * t_ref; fem.py:85-118).  dof_kind: 2N RAFEM_DOF_* codes. */
+int rafem_mesh_create(rafem_ctx* ctx, int64_t n_nodes, const double* nodes, int64_t n_tets,
+                      const int64_t* tets, const int32_t* region_index, int32_t n_regions,
+                      const double* k, const double* rho_c, const double* sigma0,
+                      const double* alpha, const double* t_ref, const uint8_t* dof_kind,
+                      rafem_mesh** out);
+void rafem_mesh_destroy(rafem_mesh* mesh);
+/* node-pattern size (slots); the dof CSR has 2*slots entries */
+int64_t rafem_mesh_slots(const rafem_mesh* mesh);
+/* node-level pattern: row_ptr (N+1), col (slots) */
+int rafem_mesh_pattern(rafem_mesh* mesh, int64_t* node_row_ptr, int32_t* node_col);
+
+int rafem_system_create(rafem_mesh* mesh, rafem_system** out);
+void rafem_system_destroy(rafem_system* sys);
+/* assemble_global (fem.py:325-430) into sys; fields are host arrays of N.
+ * On RAFEM_ERR_PHYSICS, *bad_element holds the lowest offending element. */
+int rafem_assemble(rafem_system* sys, const double* t_iter, const double* v_iter,
+                   const double* t_prev, const rafem_assemble_params* p, double* scale_out,
+                   int64_t* bad_element);
+/* dof-order values (2*slots, CsrMatrix.vals order) and rhs (2N) to host */
+int rafem_system_download(rafem_system* sys, double* vals_out, double* rhs_out);
+/* solve the device-resident system; b == NULL uses the assembled rhs */
+int rafem_system_solve(rafem_system* sys, const double* b, const double* x0,
+                       const rafem_solver_params* p, double* x_out, rafem_solve_stats* st,
+                       double* hist, int64_t hist_cap, int64_t* cycle_lens, int64_t cycle_cap);
+/* y = A x on the device-resident system (dof vectors, host) */
+int rafem_system_spmv(rafem_system* sys, const double* x, double* y);
+/* device-only SpMV timing: `reps` back-to-back launches of the standalone
+ * SpMV kernel on a device-resident x, mean CUDA-event ms per launch */
+int rafem_system_spmv_bench(rafem_system* sys, int32_t reps, double* ms_per_launch);
+
+/* ---- native time loop (fem.py:554-644 around the device path) ------------ */
+/* Runs run_simulation's adaptive predictor-corrector loop with mesh, system,
+ * iterates and solver state resident in HBM; one 32-byte status read per
+ * corrector pass.  If p->record_fields, rec_x must hold rec_cap * 2N doubles
+ * (interleaved V/T per accepted step).  rec_* arrays may be NULL if rec_cap
+ * is 0. */
+int rafem_simulate(rafem_system* sys, const rafem_sim_params* p, rafem_sim_summary* out,
+                   int64_t rec_cap, int64_t* rec_step, double* rec_time, double* rec_dt,
+                   int32_t* rec_iters, double* rec_x);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RAFEM_B200_H */

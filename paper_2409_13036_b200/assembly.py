@@ -1,0 +1,316 @@
+"""Assembly plug-in: ``assemble_global`` on the B200.
+
+Mirrors rafem/fem.py's configuration types (``RegionMaterial``,
+``MaterialParams``, ``SimConfig``: fem.py:85-147), ``PhysicsRangeError``
+(fem.py:72-73), ``AssembledSystem`` (fem.py:299-303) and the signature and
+semantics of ``assemble_global`` (fem.py:325-430).  The symbolic work
+(pattern, incidence lists, slot map, geometry) happens once per mesh on
+the device and is cached; each call is one H2D of the three fields plus
+four kernels, and the returned matrix stays in HBM.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .csr import DeviceCsrMatrix
+from .krylov import SolverConfig
+
+__all__ = [
+    "AssembledSystem", "MaterialParams", "PhysicsRangeError", "RegionMaterial", "SimConfig",
+    "assemble_global", "device_mesh",
+]
+
+
+class PhysicsRangeError(RuntimeError):
+    """A material law left its admissible range (fem.py:72-73)."""
+
+
+@dataclass
+class RegionMaterial:
+    k: float = 0.5e-3
+    rho_c: float = 3.6e-3
+    sigma0: float = 0.2e-3
+    alpha: float = 0.02
+    t_ref: float = 37.0
+
+    def __post_init__(self):
+        if self.k <= 0.0 or self.rho_c <= 0.0 or self.sigma0 <= 0.0:
+            raise ValueError("k, rho_c and sigma0 must be positive")
+
+
+@dataclass
+class MaterialParams:
+    regions: dict = field(default_factory=lambda: {0: RegionMaterial()})
+
+    @classmethod
+    def default(cls) -> "MaterialParams":
+        return cls()
+
+    def for_region(self, tag: int) -> RegionMaterial:
+        try:
+            return self.regions[tag]
+        except KeyError:
+            raise KeyError(f"no material defined for region tag {tag}") from None
+
+
+@dataclass
+class SimConfig:
+    total_time: float = 900.0
+    dt_init: float = 0.5
+    dt_min: float = 1e-6
+    dt_max: float = 10.0
+    corrector_tol: float = 1e-4
+    max_corrector_iters: int = 50
+    applied_voltage: float = 25.0
+    boundary_temp: float = 37.0
+    initial_temp: float = 37.0
+    threads: int = 1
+    solver: SolverConfig = field(default_factory=SolverConfig)
+
+    def __post_init__(self):
+        if self.total_time <= 0.0:
+            raise ValueError("total_time must be positive")
+        if not (0.0 < self.dt_min <= self.dt_init <= self.dt_max):
+            raise ValueError("need 0 < dt_min <= dt_init <= dt_max")
+        if self.corrector_tol <= 0.0:
+            raise ValueError("corrector_tol must be positive")
+        if self.max_corrector_iters < 1:
+            raise ValueError("max_corrector_iters must be at least 1")
+        if self.threads < 1:
+            raise ValueError("threads must be at least 1")
+
+
+# ---------------------------------------------------------------------------
+# device handles
+
+def _region_tables(mesh, material):
+    """Region tag -> row index and per-region coefficient tables (fem.py:212-226)."""
+    tags, index = np.unique(mesh.regions, return_inverse=True)
+    mats = [material.for_region(int(t)) for t in tags]  # KeyError like the reference
+    tab = {name: np.ascontiguousarray([getattr(m, name) for m in mats], dtype=np.float64)
+           for name in ("k", "rho_c", "sigma0", "alpha", "t_ref")}
+    return np.ascontiguousarray(index, dtype=np.int32), tab
+
+
+def _dof_kinds(mesh):
+    """Dirichlet kind per interleaved dof (fem.py:403-413)."""
+    kind = np.zeros(2 * mesh.node_count, dtype=np.uint8)
+    kind[2 * mesh.node_sets["electrode_pos"]] = nat.DOF_APPLIED_VOLTAGE
+    kind[2 * mesh.node_sets["electrode_neg"]] = nat.DOF_ZERO
+    kind[2 * mesh.node_sets["outer_boundary"] + 1] = nat.DOF_BOUNDARY_TEMP
+    return kind
+
+
+class DeviceMesh:
+    """Mesh + symbolic pattern + geometry resident on the device."""
+
+    def __init__(self, mesh, material):
+        self.node_count = int(mesh.nodes.shape[0])
+        self.tet_count = int(mesh.tets.shape[0])
+        region_index, tab = _region_tables(mesh, material)
+        self.regions_tags = np.unique(mesh.regions)
+        kind = _dof_kinds(mesh)
+        nodes = np.ascontiguousarray(mesh.nodes, dtype=np.float64)
+        tets = np.ascontiguousarray(mesh.tets, dtype=np.int64)
+        h = C.c_void_p()
+        L = nat.lib()
+        rc = L.rafem_mesh_create(nat.context(), self.node_count, nat.ptr(nodes), self.tet_count,
+                                 nat.ptr(tets), nat.ptr(region_index), len(tab["k"]),
+                                 nat.ptr(tab["k"]), nat.ptr(tab["rho_c"]), nat.ptr(tab["sigma0"]),
+                                 nat.ptr(tab["alpha"]), nat.ptr(tab["t_ref"]), nat.ptr(kind),
+                                 C.byref(h))
+        nat.check(rc, "mesh setup")
+        self.handle = h
+        self._finalizer = weakref.finalize(self, L.rafem_mesh_destroy, h)
+        self.slots = int(L.rafem_mesh_slots(h))
+        self._pattern = None
+        self._pool: list = []
+
+    def node_pattern(self):
+        if self._pattern is None:
+            rp = np.empty(self.node_count + 1, dtype=np.int64)
+            col = np.empty(max(self.slots, 1), dtype=np.int32)
+            nat.check(nat.lib().rafem_mesh_pattern(self.handle, nat.ptr(rp), nat.ptr(col)), "pattern")
+            self._pattern = (rp, col[: self.slots].astype(np.int64))
+        return self._pattern
+
+    @property
+    def dof_row_ptr(self):
+        if not hasattr(self, "_dof_rp"):
+            rp, _ = self.node_pattern()
+            deg = np.diff(rp)
+            out = np.empty(2 * self.node_count + 1, dtype=np.int64)
+            out[0] = 0
+            out[1::2] = 2 * rp[:-1] + deg      # end of row 2i
+            out[2::2] = 2 * rp[1:]             # end of row 2i+1
+            self._dof_rp = out
+        return self._dof_rp
+
+    @property
+    def dof_col_idx(self):
+        if not hasattr(self, "_dof_ci"):
+            rp, col = self.node_pattern()
+            deg = np.diff(rp)
+            node = np.repeat(np.arange(self.node_count), deg)
+            pos = np.arange(self.slots) - rp[node]                 # offset within the node row
+            out = np.empty(2 * self.slots, dtype=np.int64)
+            out[2 * rp[node] + pos] = 2 * col                       # V row: cols 2j
+            out[2 * rp[node] + deg[node] + pos] = 2 * col + 1       # T row: cols 2j+1
+            self._dof_ci = out
+        return self._dof_ci
+
+    def acquire_system(self):
+        if self._pool:
+            return self._pool.pop()
+        h = C.c_void_p()
+        nat.check(nat.lib().rafem_system_create(self.handle, C.byref(h)), "system alloc")
+        return h
+
+    def release_system(self, h):
+        if len(self._pool) < 4:
+            self._pool.append(h)
+        else:
+            nat.lib().rafem_system_destroy(h)
+
+    def __del__(self):
+        try:
+            for h in self._pool:
+                nat.lib().rafem_system_destroy(h)
+            self._pool = []
+        except Exception:
+            pass
+
+
+class SystemHandle:
+    """One assembled system in HBM; returned to its mesh's pool when dropped."""
+
+    def __init__(self, mesh: DeviceMesh):
+        self.mesh = mesh
+        self.handle = mesh.acquire_system()
+        self.scale = 1.0
+        self._rhs = None
+
+    def __del__(self):
+        try:
+            self.mesh.release_system(self.handle)
+        except Exception:
+            pass
+
+    def download_vals(self):
+        out = np.empty(2 * self.mesh.slots)
+        nat.check(nat.lib().rafem_system_download(self.handle, nat.ptr(out), None), "download")
+        return out
+
+    def rhs(self):
+        if self._rhs is None:
+            out = np.empty(2 * self.mesh.node_count)
+            nat.check(nat.lib().rafem_system_download(self.handle, None, nat.ptr(out)), "download")
+            self._rhs = out
+        return self._rhs
+
+    def spmv(self, x):
+        y = np.empty(2 * self.mesh.node_count)
+        nat.check(nat.lib().rafem_system_spmv(self.handle, nat.ptr(x), nat.ptr(y)), "spmv")
+        return y
+
+    def solve(self, b, x0, params, x_out, st, hist, cyc):
+        return nat.lib().rafem_system_solve(self.handle, nat.ptr(b), nat.ptr(x0), C.byref(params),
+                                            nat.ptr(x_out), C.byref(st), nat.ptr(hist), hist.size,
+                                            nat.ptr(cyc), cyc.size)
+
+
+_MESH_CACHE: dict = {}
+
+
+def _material_key(mesh, material):
+    tags = np.unique(mesh.regions)
+    rows = []
+    for t in tags:
+        m = material.for_region(int(t))
+        rows.append((int(t), m.k, m.rho_c, m.sigma0, m.alpha, m.t_ref))
+    return tuple(rows)
+
+
+def device_mesh(mesh, material) -> DeviceMesh:
+    """Cached device mesh for (mesh object, material values)."""
+    key = (id(mesh), _material_key(mesh, material))
+    hit = _MESH_CACHE.get(key)
+    if hit is not None:
+        ref, nodes_id, tets_id, dm = hit
+        if ref() is mesh and nodes_id == id(mesh.nodes) and tets_id == id(mesh.tets):
+            return dm
+    dm = DeviceMesh(mesh, material)
+    try:
+        ref = weakref.ref(mesh, lambda _r, k=key: _MESH_CACHE.pop(k, None))
+    except TypeError:  # not weak-referenceable: keep a strong ref
+        ref = (lambda m=mesh: m)
+    _MESH_CACHE[key] = (ref, id(mesh.nodes), id(mesh.tets), dm)
+    return dm
+
+
+class AssembledSystem:
+    """(matrix, rhs, voltage_row_scale) of fem.py:299-303; rhs is read from HBM on first use."""
+
+    def __init__(self, handle: SystemHandle):
+        self._h = handle
+        self.matrix = DeviceCsrMatrix(handle)
+        self.voltage_row_scale = handle.scale
+
+    @property
+    def rhs(self):
+        return self._h.rhs()
+
+    @property
+    def device(self) -> SystemHandle:
+        return self._h
+
+
+def assemble_global(mesh, material, config, t_iter, v_iter, t_prev, dt, apply_constraints=True,
+                    equilibrate=True, threads=None) -> AssembledSystem:
+    """Interleaved 2N x 2N system for one corrector pass (fem.py:325-430).
+
+    ``threads`` is validated and otherwise ignored: the device fill is
+    bit-identical for any launch configuration, which is the property the
+    reference's thread count guarantees (fem.py:343-346).
+    """
+    if dt <= 0.0:
+        raise ValueError("dt must be positive")
+    threads = config.threads if threads is None else threads
+    if threads < 1:
+        raise ValueError("threads must be at least 1")
+    n = int(mesh.nodes.shape[0])
+    t_iter = np.ascontiguousarray(t_iter, dtype=np.float64)
+    v_iter = np.ascontiguousarray(v_iter, dtype=np.float64)
+    t_prev = np.ascontiguousarray(t_prev, dtype=np.float64)
+    for arr in (t_iter, v_iter, t_prev):
+        if arr.shape != (n,):
+            raise ValueError("field length does not match the mesh node count")
+    dm = device_mesh(mesh, material)
+    h = SystemHandle(dm)
+    p = nat.AssembleParams()
+    p.dt = float(dt)
+    p.applied_voltage = float(config.applied_voltage)
+    p.boundary_temp = float(config.boundary_temp)
+    p.apply_constraints = 1 if apply_constraints else 0
+    p.equilibrate = 1 if equilibrate else 0
+    scale = C.c_double()
+    bad = C.c_int64(-1)
+    rc = nat.lib().rafem_assemble(h.handle, nat.ptr(t_iter), nat.ptr(v_iter), nat.ptr(t_prev),
+                                  C.byref(p), C.byref(scale), C.byref(bad))
+    if rc == nat.ERR_PHYSICS:
+        e = int(bad.value)
+        tets = mesh.tets[e]
+        tbar = float(np.mean(t_iter[tets]))
+        rm = material.for_region(int(mesh.regions[e]))
+        sigma = rm.sigma0 * (1.0 + rm.alpha * (tbar - rm.t_ref))
+        raise PhysicsRangeError(
+            f"sigma(T) = {sigma:.3g} S/mm <= 0 in element {e} (mean T {tbar:.3g})")
+    nat.check(rc, "assemble")
+    h.scale = float(scale.value)
+    return AssembledSystem(h)

@@ -1,0 +1,694 @@
+// capi.cu — the extern "C" boundary of librafem_b200 (include/rafem_b200.h)
+// and the native time loop (rafem_simulate).
+#include "common.cuh"
+#include "internal.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+using namespace rafem;
+
+int rafem_fail(rafem_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+int rafem_fail_cuda(rafem_ctx* ctx, cudaError_t e, const char* what, const char* file, int line) {
+    char buf[512];
+    std::snprintf(buf, sizeof(buf), "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
+                  cudaGetErrorString(e), what, file, line);
+    if (ctx) ctx->err = buf;
+    return RAFEM_ERR_CUDA;
+}
+
+namespace rafem {
+
+int ensure(rafem_ctx* ctx, DevBuf& b, size_t bytes) {
+    if (b.bytes >= bytes && b.p) return RAFEM_OK;
+    if (b.p) {
+        RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        cudaFree(b.p);
+        b.p = nullptr;
+        b.bytes = 0;
+    }
+    const size_t want = std::max<size_t>(bytes, 256);
+    RF_CUDA_TRY(ctx, cudaMalloc(&b.p, want));
+    b.bytes = want;
+    return RAFEM_OK;
+}
+
+void* pinned(rafem_ctx* ctx, size_t bytes) {
+    if (ctx->pin_bytes >= bytes && ctx->pin) return ctx->pin;
+    if (ctx->pin) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaFreeHost(ctx->pin);
+        ctx->pin = nullptr;
+        ctx->pin_bytes = 0;
+    }
+    const size_t want = std::max<size_t>(bytes, 1 << 16);
+    if (cudaMallocHost(&ctx->pin, want) != cudaSuccess) {
+        ctx->pin = nullptr;
+        return nullptr;
+    }
+    ctx->pin_bytes = want;
+    return ctx->pin;
+}
+
+}  // namespace rafem
+
+namespace {
+
+// host -> device through the pinned staging buffer (async wrt the host
+// only up to the final stream sync the callers do)
+int upload(rafem_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return RAFEM_OK;
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return RAFEM_OK;
+}
+
+void fill_stats(const KResult& r, float ms, rafem_solve_stats* st) {
+    st->iterations = r.iterations;
+    st->restarts = r.restarts;
+    st->final_relative_residual = r.final_rel;
+    st->converged = r.converged;
+    st->stagnated = r.stagnated;
+    st->cycles = r.cycles;
+    st->history_len = r.hist_len;
+    st->device_ms = ms;
+}
+
+int check_params(rafem_ctx* ctx, const rafem_solver_params* p) {
+    if (!p) return rafem_fail(ctx, RAFEM_ERR_INVALID, "solver params missing");
+    if (p->method != RAFEM_METHOD_GMRES && p->method != RAFEM_METHOD_PCG)
+        return rafem_fail(ctx, RAFEM_ERR_INVALID, "unknown Krylov method");
+    if (p->restart_m < 1) return rafem_fail(ctx, RAFEM_ERR_INVALID, "restart_m must be at least 1");
+    if (!(p->tolerance > 0.0 && p->tolerance < 1.0))
+        return rafem_fail(ctx, RAFEM_ERR_INVALID, "tolerance must lie in (0, 1)");
+    return RAFEM_OK;
+}
+
+MatView system_view(rafem_system* s) {
+    MatView A;
+    A.rp = s->mesh->rp;
+    A.col = s->mesh->col;
+    A.val = s->val2;
+    A.ngroups = s->mesh->N;
+    A.W = 2;
+    A.slots = s->mesh->slots;
+    return A;
+}
+
+// device layout of sys->status
+struct SysStatus {
+    PassStatus pass;
+    int flag;  // zero-diagonal flag of the Jacobi setup
+    int pad;
+};
+
+SysStatus* sys_status(rafem_system* s) { return reinterpret_cast<SysStatus*>(s->status); }
+
+// solve on a matrix view with host b/x0/x; shared by system and matrix paths
+int solve_common(rafem_ctx* ctx, const MatView& A, double* b_dev, bool b_is_host, const double* b,
+                 const double* x0, const rafem_solver_params* p, double* x_out, rafem_solve_stats* st,
+                 double* hist, int64_t hist_cap, int64_t* cycle_lens, int64_t cycle_cap, double* minv,
+                 double* xbuf, SysStatus* dstat) {
+    const int n = A.ngroups * A.W;
+    if (int rc = check_params(ctx, p)) return rc;
+    if (b_is_host && b) {
+        if (int rc = upload(ctx, b_dev, b, sizeof(double) * n)) return rc;
+    }
+    const double* x0_dev = nullptr;
+    if (x0) {
+        if (int rc = upload(ctx, xbuf, x0, sizeof(double) * n)) return rc;
+        x0_dev = xbuf;
+    }
+    int* flag = &dstat->flag;
+    if (p->precondition == RAFEM_PRECOND_JACOBI) {
+        if (int rc = jacobi_minv(ctx, A, minv, flag)) return rc;
+    } else {
+        RF_CUDA_TRY(ctx, cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+    }
+    if (int rc = krylov_solve(ctx, A, b_dev, x0_dev, xbuf, minv, *p, &dstat->pass.solve, flag, ctx->ev0, ctx->ev1))
+        return rc;
+    KResult r;
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(&r, &dstat->pass.solve, sizeof(r), cudaMemcpyDeviceToHost, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(x_out, xbuf, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    if (st) fill_stats(r, ms, st);
+    if (int rc = krylov_read_history(ctx, r, hist, hist_cap, reinterpret_cast<long long*>(cycle_lens), cycle_cap))
+        return rc;
+    if (r.status == RAFEM_ERR_INVALID)
+        return rafem_fail(ctx, RAFEM_ERR_INVALID, "Jacobi preconditioning requires a zero-free diagonal");
+    if (r.status == RAFEM_ERR_BREAKDOWN) {
+        char buf[256];
+        std::snprintf(buf, sizeof(buf), "Arnoldi breakdown with relative residual %.3e above tolerance %.3e",
+                      r.final_rel, p->tolerance);
+        if (p->method == RAFEM_METHOD_PCG)
+            std::snprintf(buf, sizeof(buf), "CG breakdown (operator not SPD under the preconditioner), "
+                          "relative residual %.3e", r.final_rel);
+        return rafem_fail(ctx, RAFEM_ERR_BREAKDOWN, buf);
+    }
+    return RAFEM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rafem_ctx_create(int device, rafem_ctx** out) {
+    if (!out) return RAFEM_ERR_INVALID;
+    *out = nullptr;
+    rafem_ctx* ctx = new rafem_ctx();
+    ctx->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        int rc = rafem_fail_cuda(ctx, e, "cudaSetDevice", __FILE__, __LINE__);
+        *out = ctx;  // keep the message readable
+        return rc;
+    }
+    cudaDeviceProp prop;
+    RF_CUDA_TRY(ctx, cudaGetDeviceProperties(&prop, device));
+    ctx->sm_count = prop.multiProcessorCount;
+    ctx->cc_major = prop.major;
+    ctx->cc_minor = prop.minor;
+    ctx->total_mem = (long long)prop.totalGlobalMem;
+    if (!prop.cooperativeLaunch) {
+        *out = ctx;
+        return rafem_fail(ctx, RAFEM_ERR_UNSUPPORTED, "device lacks cooperative launch");
+    }
+    RF_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    RF_CUDA_TRY(ctx, cudaEventCreate(&ctx->ev0));
+    RF_CUDA_TRY(ctx, cudaEventCreate(&ctx->ev1));
+    RF_CUDA_TRY(ctx, cudaEventCreate(&ctx->ev2));
+    ensure(ctx, ctx->ws_res, 4096);
+    *out = ctx;
+    return RAFEM_OK;
+}
+
+void rafem_ctx_destroy(rafem_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (DevBuf* b : {&ctx->ws_basis, &ctx->ws_vec, &ctx->ws_partial, &ctx->ws_hess, &ctx->ws_hist,
+                      &ctx->ws_cyc, &ctx->ws_part, &ctx->ws_res})
+        if (b->p) cudaFree(b->p);
+    if (ctx->pin) cudaFreeHost(ctx->pin);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->ev2) cudaEventDestroy(ctx->ev2);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char* rafem_last_error(const rafem_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+int rafem_device_info(rafem_ctx* ctx, int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor,
+                      int64_t* total_mem) {
+    if (!ctx) return RAFEM_ERR_INVALID;
+    if (sm_count) *sm_count = ctx->sm_count;
+    if (cc_major) *cc_major = ctx->cc_major;
+    if (cc_minor) *cc_minor = ctx->cc_minor;
+    if (total_mem) *total_mem = ctx->total_mem;
+    return RAFEM_OK;
+}
+
+int64_t rafem_kernel_launches(const rafem_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+void* rafem_stream(const rafem_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+// ---- sparse ---------------------------------------------------------------
+
+int rafem_spmv(rafem_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* row_ptr,
+               const int64_t* col_idx, const double* vals, const double* x, double* y) {
+    if (!ctx) return RAFEM_ERR_INVALID;
+    if (nrows < 0 || ncols < 0 || nnz < 0) return rafem_fail(ctx, RAFEM_ERR_INVALID, "negative size");
+    if (nrows >= (1LL << 31) || ncols >= (1LL << 31) || nnz >= (1LL << 31))
+        return rafem_fail(ctx, RAFEM_ERR_UNSUPPORTED, "spmv: sizes must fit in int32");
+    if (nrows == 0) return RAFEM_OK;
+    std::vector<int> rp(nrows + 1), ci(nnz);
+    for (int64_t i = 0; i <= nrows; ++i) rp[i] = (int)row_ptr[i];
+    for (int64_t k = 0; k < nnz; ++k) ci[k] = (int)col_idx[k];
+    int *drp = nullptr, *dci = nullptr;
+    double *dv = nullptr, *dx = nullptr, *dy = nullptr;
+    auto cleanup = [&]() { cudaFree(drp); cudaFree(dci); cudaFree(dv); cudaFree(dx); cudaFree(dy); };
+    cudaError_t e;
+#define RF_S(x) do { e = (x); if (e != cudaSuccess) { cleanup(); return rafem_fail_cuda(ctx, e, #x, __FILE__, __LINE__); } } while (0)
+    RF_S(cudaMalloc(&drp, sizeof(int) * (nrows + 1)));
+    RF_S(cudaMalloc(&dci, sizeof(int) * std::max<int64_t>(nnz, 1)));
+    RF_S(cudaMalloc(&dv, sizeof(double) * std::max<int64_t>(nnz, 1)));
+    RF_S(cudaMalloc(&dx, sizeof(double) * std::max<int64_t>(ncols, 1)));
+    RF_S(cudaMalloc(&dy, sizeof(double) * nrows));
+    RF_S(cudaMemcpyAsync(drp, rp.data(), sizeof(int) * (nrows + 1), cudaMemcpyHostToDevice, ctx->stream));
+    if (nnz) {
+        RF_S(cudaMemcpyAsync(dci, ci.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice, ctx->stream));
+        RF_S(cudaMemcpyAsync(dv, vals, sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    if (ncols) RF_S(cudaMemcpyAsync(dx, x, sizeof(double) * ncols, cudaMemcpyHostToDevice, ctx->stream));
+    MatView A{drp, dci, dv, (int)nrows, 1, nnz};
+    if (int rc = spmv_launch(ctx, A, dx, dy)) { cleanup(); return rc; }
+    RF_S(cudaMemcpyAsync(y, dy, sizeof(double) * nrows, cudaMemcpyDeviceToHost, ctx->stream));
+    RF_S(cudaStreamSynchronize(ctx->stream));
+#undef RF_S
+    cleanup();
+    return RAFEM_OK;
+}
+
+int rafem_coo_to_csr(rafem_ctx* ctx, int64_t nrows, int64_t ncols, int64_t nnz_in, const int64_t* rows,
+                     const int64_t* cols, const double* vals, int64_t* row_ptr_out, int64_t* col_idx_out,
+                     double* vals_out, int64_t* nnz_out) {
+    if (!ctx) return RAFEM_ERR_INVALID;
+    return coo_to_csr_device(ctx, nrows, ncols, nnz_in, rows, cols, vals, row_ptr_out, col_idx_out, vals_out,
+                             nnz_out);
+}
+
+// ---- general matrix ---------------------------------------------------------
+
+int rafem_matrix_create(rafem_ctx* ctx, int64_t nrows, int64_t nnz, const int64_t* row_ptr,
+                        const int64_t* col_idx, const double* vals, rafem_matrix** out) {
+    if (!ctx || !out) return RAFEM_ERR_INVALID;
+    *out = nullptr;
+    if (nrows < 0 || nnz < 0) return rafem_fail(ctx, RAFEM_ERR_INVALID, "negative size");
+    if (nrows >= (1LL << 31) || nnz >= (1LL << 31))
+        return rafem_fail(ctx, RAFEM_ERR_UNSUPPORTED, "matrix sizes must fit in int32");
+    rafem_matrix* a = new rafem_matrix();
+    a->ctx = ctx;
+    a->n = (int)nrows;
+    a->nnz = nnz;
+    std::vector<int> rp(nrows + 1), ci(nnz);
+    for (int64_t i = 0; i <= nrows; ++i) rp[i] = (int)row_ptr[i];
+    for (int64_t k = 0; k < nnz; ++k) ci[k] = (int)col_idx[k];
+    cudaError_t e;
+#define RF_M(x) do { e = (x); if (e != cudaSuccess) { rafem_matrix_destroy(a); return rafem_fail_cuda(ctx, e, #x, __FILE__, __LINE__); } } while (0)
+    RF_M(cudaMalloc(&a->rp, sizeof(int) * (nrows + 1)));
+    RF_M(cudaMalloc(&a->col, sizeof(int) * std::max<int64_t>(nnz, 1)));
+    RF_M(cudaMalloc(&a->val, sizeof(double) * std::max<int64_t>(nnz, 1)));
+    RF_M(cudaMalloc(&a->minv, sizeof(double) * (3 * (size_t)std::max<int64_t>(nrows, 1) + 64)));
+    RF_M(cudaMemcpyAsync(a->rp, rp.data(), sizeof(int) * (nrows + 1), cudaMemcpyHostToDevice, ctx->stream));
+    if (nnz) {
+        RF_M(cudaMemcpyAsync(a->col, ci.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice, ctx->stream));
+        RF_M(cudaMemcpyAsync(a->val, vals, sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    RF_M(cudaStreamSynchronize(ctx->stream));
+#undef RF_M
+    *out = a;
+    return RAFEM_OK;
+}
+
+void rafem_matrix_destroy(rafem_matrix* a) {
+    if (!a) return;
+    cudaFree(a->rp);
+    cudaFree(a->col);
+    cudaFree(a->val);
+    cudaFree(a->minv);
+    delete a;
+}
+
+int rafem_matrix_solve(rafem_matrix* a, const double* b, const double* x0, const rafem_solver_params* p,
+                       double* x_out, rafem_solve_stats* st, double* hist, int64_t hist_cap,
+                       int64_t* cycle_lens, int64_t cycle_cap) {
+    if (!a) return RAFEM_ERR_INVALID;
+    rafem_ctx* ctx = a->ctx;
+    const int n = a->n;
+    if (n == 0) {
+        if (st) std::memset(st, 0, sizeof(*st)), st->converged = 1;
+        return RAFEM_OK;
+    }
+    // minv buffer doubles as b and x staging: [minv | b | x | status]
+    double* minv = a->minv;
+    double* bdev = a->minv + n;
+    double* xdev = a->minv + 2 * (size_t)n;
+    if (int rc = ensure(ctx, ctx->ws_res, sizeof(SysStatus) + 256)) return rc;
+    SysStatus* ds = static_cast<SysStatus*>(ctx->ws_res.p);
+    MatView A{a->rp, a->col, a->val, n, 1, a->nnz};
+    return solve_common(ctx, A, bdev, true, b, x0, p, x_out, st, hist, hist_cap, cycle_lens, cycle_cap, minv, xdev, ds);
+}
+
+// ---- mesh / system -----------------------------------------------------------
+
+int rafem_mesh_create(rafem_ctx* ctx, int64_t n_nodes, const double* nodes, int64_t n_tets, const int64_t* tets,
+                      const int32_t* region_index, int32_t n_regions, const double* k, const double* rho_c,
+                      const double* sigma0, const double* alpha, const double* t_ref, const uint8_t* dof_kind,
+                      rafem_mesh** out) {
+    if (!ctx || !out) return RAFEM_ERR_INVALID;
+    *out = nullptr;
+    if (n_nodes < 0 || n_tets < 0 || n_regions < 1) return rafem_fail(ctx, RAFEM_ERR_INVALID, "bad mesh sizes");
+    if (n_nodes >= (1LL << 30) || n_tets >= (1LL << 30))
+        return rafem_fail(ctx, RAFEM_ERR_UNSUPPORTED, "mesh too large for 30-bit element ids");
+    std::vector<int> t32(4 * (size_t)n_tets);
+    for (int64_t i = 0; i < 4 * n_tets; ++i) {
+        if (tets[i] < 0 || tets[i] >= n_nodes) return rafem_fail(ctx, RAFEM_ERR_INVALID, "tet references a node out of range");
+        t32[i] = (int)tets[i];
+    }
+    std::vector<int> reg(n_tets, 0);
+    if (region_index)
+        for (int64_t e = 0; e < n_tets; ++e) {
+            if (region_index[e] < 0 || region_index[e] >= n_regions) return rafem_fail(ctx, RAFEM_ERR_INVALID, "region index out of range");
+            reg[e] = region_index[e];
+        }
+    std::vector<double> tab(5 * (size_t)n_regions);
+    for (int r = 0; r < n_regions; ++r) {
+        tab[r] = k[r];
+        tab[n_regions + r] = rho_c[r];
+        tab[2 * n_regions + r] = sigma0[r];
+        tab[3 * n_regions + r] = alpha[r];
+        tab[4 * n_regions + r] = t_ref[r];
+    }
+    rafem_mesh* m = new rafem_mesh();
+    m->ctx = ctx;
+    m->N = (int)n_nodes;
+    m->M = (int)n_tets;
+    m->nreg = n_regions;
+    cudaError_t e;
+#define RF_MS(x) do { e = (x); if (e != cudaSuccess) { rafem_mesh_destroy(m); return rafem_fail_cuda(ctx, e, #x, __FILE__, __LINE__); } } while (0)
+    const size_t N = std::max<int64_t>(n_nodes, 1), M = std::max<int64_t>(n_tets, 1);
+    RF_MS(cudaMalloc(&m->nodes, sizeof(double) * 3 * N));
+    RF_MS(cudaMalloc(&m->tets, sizeof(int) * 4 * M));
+    RF_MS(cudaMalloc(&m->region, sizeof(int) * M));
+    RF_MS(cudaMalloc(&m->regtab, sizeof(double) * 5 * n_regions));
+    RF_MS(cudaMalloc(&m->kind, 2 * N));
+    RF_MS(cudaMemcpy(m->nodes, nodes, sizeof(double) * 3 * n_nodes, cudaMemcpyHostToDevice));
+    RF_MS(cudaMemcpy(m->tets, t32.data(), sizeof(int) * 4 * n_tets, cudaMemcpyHostToDevice));
+    RF_MS(cudaMemcpy(m->region, reg.data(), sizeof(int) * n_tets, cudaMemcpyHostToDevice));
+    RF_MS(cudaMemcpy(m->regtab, tab.data(), sizeof(double) * 5 * n_regions, cudaMemcpyHostToDevice));
+    RF_MS(cudaMemcpy(m->kind, dof_kind, 2 * n_nodes, cudaMemcpyHostToDevice));
+#undef RF_MS
+    if (int rc = mesh_symbolic(m)) {
+        rafem_mesh_destroy(m);
+        return rc;
+    }
+    if (int rc = mesh_geometry(m)) {
+        rafem_mesh_destroy(m);
+        return rc;
+    }
+    cudaError_t se = cudaStreamSynchronize(ctx->stream);
+    if (se != cudaSuccess) {
+        rafem_mesh_destroy(m);
+        return rafem_fail_cuda(ctx, se, "mesh setup", __FILE__, __LINE__);
+    }
+    *out = m;
+    return RAFEM_OK;
+}
+
+void rafem_mesh_destroy(rafem_mesh* m) {
+    if (!m) return;
+    for (void* p : {(void*)m->nodes, (void*)m->tets, (void*)m->region, (void*)m->regtab, (void*)m->kind,
+                    (void*)m->rp, (void*)m->col, (void*)m->diag, (void*)m->inc_ptr, (void*)m->inc_ea,
+                    (void*)m->inc_slot, (void*)m->base, (void*)m->grad, (void*)m->vol})
+        if (p) cudaFree(p);
+    delete m;
+}
+
+int64_t rafem_mesh_slots(const rafem_mesh* m) { return m ? m->slots : -1; }
+
+int rafem_mesh_pattern(rafem_mesh* m, int64_t* node_row_ptr, int32_t* node_col) {
+    if (!m) return RAFEM_ERR_INVALID;
+    rafem_ctx* ctx = m->ctx;
+    std::vector<int> rp(m->N + 1);
+    RF_CUDA_TRY(ctx, cudaMemcpy(rp.data(), m->rp, sizeof(int) * (m->N + 1), cudaMemcpyDeviceToHost));
+    for (int i = 0; i <= m->N; ++i) node_row_ptr[i] = rp[i];
+    if (m->slots) RF_CUDA_TRY(ctx, cudaMemcpy(node_col, m->col, sizeof(int) * m->slots, cudaMemcpyDeviceToHost));
+    return RAFEM_OK;
+}
+
+int rafem_system_create(rafem_mesh* m, rafem_system** out) {
+    if (!m || !out) return RAFEM_ERR_INVALID;
+    *out = nullptr;
+    rafem_ctx* ctx = m->ctx;
+    rafem_system* s = new rafem_system();
+    s->mesh = m;
+    const size_t N = std::max(m->N, 1), M = std::max(m->M, 1), S = std::max<long long>(m->slots, 1);
+    cudaError_t e;
+#define RF_SS(x) do { e = (x); if (e != cudaSuccess) { rafem_system_destroy(s); return rafem_fail_cuda(ctx, e, #x, __FILE__, __LINE__); } } while (0)
+    RF_SS(cudaMalloc(&s->val2, sizeof(double) * 2 * S));
+    RF_SS(cudaMalloc(&s->rhs, sizeof(double) * 2 * N));
+    RF_SS(cudaMalloc(&s->sigma, sizeof(double) * M));
+    RF_SS(cudaMalloc(&s->load, sizeof(double) * 4 * M));
+    RF_SS(cudaMalloc(&s->diagpart, sizeof(double) * 2 * N));
+    RF_SS(cudaMalloc(&s->minv, sizeof(double) * 2 * N));
+    RF_SS(cudaMalloc(&s->xin, sizeof(double) * (3 * N + 2 * S)));  // host inputs / dof expansion
+    RF_SS(cudaMalloc(&s->status, 1024));
+    RF_SS(cudaMalloc(&s->xs, sizeof(double) * 6 * 2 * N));
+    RF_SS(cudaMemset(s->status, 0, 1024));
+#undef RF_SS
+    *out = s;
+    return RAFEM_OK;
+}
+
+void rafem_system_destroy(rafem_system* s) {
+    if (!s) return;
+    for (void* p : {(void*)s->val2, (void*)s->rhs, (void*)s->sigma, (void*)s->load, (void*)s->diagpart,
+                    (void*)s->minv, (void*)s->xin, (void*)s->status, (void*)s->xs})
+        if (p) cudaFree(p);
+    delete s;
+}
+
+int rafem_assemble(rafem_system* s, const double* t_iter, const double* v_iter, const double* t_prev,
+                   const rafem_assemble_params* p, double* scale_out, int64_t* bad_element) {
+    if (!s || !p) return RAFEM_ERR_INVALID;
+    rafem_mesh* m = s->mesh;
+    rafem_ctx* ctx = m->ctx;
+    if (!(p->dt > 0.0)) return rafem_fail(ctx, RAFEM_ERR_INVALID, "dt must be positive");
+    const int N = m->N;
+    double* pin = static_cast<double*>(pinned(ctx, sizeof(double) * 3 * (size_t)std::max(N, 1)));
+    if (!pin) return rafem_fail(ctx, RAFEM_ERR_CUDA, "pinned staging allocation failed");
+    std::memcpy(pin, t_iter, sizeof(double) * N);
+    std::memcpy(pin + N, v_iter, sizeof(double) * N);
+    std::memcpy(pin + 2 * (size_t)N, t_prev, sizeof(double) * N);
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(s->xin, pin, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, ctx->stream));
+    SysStatus* ds = sys_status(s);
+    if (int rc = assemble_launch(s, s->xin, 1, s->xin + N, 1, s->xin + 2 * (size_t)N, 1, *p, &ds->pass.scale,
+                                 &ds->pass.bad_element))
+        return rc;
+    PassStatus hs;
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, &ds->pass, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    s->scale = hs.scale;
+    if (scale_out) *scale_out = hs.scale;
+    if (bad_element) *bad_element = hs.bad_element;
+    if (hs.bad_element >= 0) {
+        char buf[128];
+        std::snprintf(buf, sizeof(buf), "sigma(T) <= 0 in element %lld", hs.bad_element);
+        return rafem_fail(ctx, RAFEM_ERR_PHYSICS, buf);
+    }
+    return RAFEM_OK;
+}
+
+int rafem_system_download(rafem_system* s, double* vals_out, double* rhs_out) {
+    if (!s) return RAFEM_ERR_INVALID;
+    rafem_ctx* ctx = s->mesh->ctx;
+    const int N = s->mesh->N;
+    if (vals_out && s->mesh->slots) {
+        double* scratch = s->xin;  // 2*slots fits in xin (3N + 2S)
+        if (int rc = expand_dof_vals(s, scratch)) return rc;
+        RF_CUDA_TRY(ctx, cudaMemcpyAsync(vals_out, scratch, sizeof(double) * 2 * s->mesh->slots, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    if (rhs_out) RF_CUDA_TRY(ctx, cudaMemcpyAsync(rhs_out, s->rhs, sizeof(double) * 2 * N, cudaMemcpyDeviceToHost, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return RAFEM_OK;
+}
+
+int rafem_system_solve(rafem_system* s, const double* b, const double* x0, const rafem_solver_params* p,
+                       double* x_out, rafem_solve_stats* st, double* hist, int64_t hist_cap, int64_t* cycle_lens,
+                       int64_t cycle_cap) {
+    if (!s) return RAFEM_ERR_INVALID;
+    rafem_ctx* ctx = s->mesh->ctx;
+    const size_t n2 = 2 * (size_t)s->mesh->N;
+    double* bdev = b ? s->xs + 4 * n2 : s->rhs;
+    double* xdev = s->xs + 5 * n2;
+    return solve_common(ctx, system_view(s), bdev, b != nullptr, b, x0, p, x_out, st, hist, hist_cap, cycle_lens,
+                        cycle_cap, s->minv, xdev, sys_status(s));
+}
+
+int rafem_system_spmv(rafem_system* s, const double* x, double* y) {
+    if (!s) return RAFEM_ERR_INVALID;
+    rafem_ctx* ctx = s->mesh->ctx;
+    const size_t n2 = 2 * (size_t)s->mesh->N;
+    double* dx = s->xs + 4 * n2;
+    double* dy = s->xs + 5 * n2;
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(dx, x, sizeof(double) * n2, cudaMemcpyHostToDevice, ctx->stream));
+    if (int rc = spmv_launch(ctx, system_view(s), dx, dy)) return rc;
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(y, dy, sizeof(double) * n2, cudaMemcpyDeviceToHost, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return RAFEM_OK;
+}
+
+int rafem_system_spmv_bench(rafem_system* s, int32_t reps, double* ms_per_launch) {
+    if (!s || reps < 1) return RAFEM_ERR_INVALID;
+    rafem_ctx* ctx = s->mesh->ctx;
+    const size_t n2 = 2 * (size_t)s->mesh->N;
+    double* dx = s->xs + 4 * n2;
+    double* dy = s->xs + 5 * n2;
+    if (int rc = fill_initial(ctx, dx, s->mesh->N, 1.25)) return rc;
+    const MatView A = system_view(s);
+    if (int rc = spmv_launch(ctx, A, dx, dy)) return rc;  // warm-up
+    RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+    for (int r = 0; r < reps; ++r)
+        if (int rc = spmv_launch(ctx, A, dx, dy)) return rc;
+    RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
+    float ms = 0.f;
+    RF_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    *ms_per_launch = ms / reps;
+    return RAFEM_OK;
+}
+
+// ---- native time loop -------------------------------------------------------
+// run_simulation (fem.py:554-644) + corrector_step (fem.py:463-540) with all
+// vectors resident in HBM; the host only reads a 96-byte PassStatus per
+// corrector pass to take the same control decisions the reference takes.
+
+int rafem_simulate(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary* out, int64_t rec_cap,
+                   int64_t* rec_step, double* rec_time, double* rec_dt, int32_t* rec_iters, double* rec_x) {
+    if (!s || !p || !out) return RAFEM_ERR_INVALID;
+    rafem_mesh* m = s->mesh;
+    rafem_ctx* ctx = m->ctx;
+    std::memset(out, 0, sizeof(*out));
+    out->failed_step = -1;
+    out->bad_element = -1;
+    if (int rc = check_params(ctx, &p->solver)) return rc;
+    if (!(p->total_time > 0.0) || !(p->dt_min > 0.0 && p->dt_min <= p->dt_init && p->dt_init <= p->dt_max) ||
+        !(p->corrector_tol > 0.0) || p->max_corrector_iters < 1)
+        return rafem_fail(ctx, RAFEM_ERR_INVALID, "invalid SimConfig");
+    const auto t_wall = std::chrono::steady_clock::now();
+    const int N = m->N;
+    const size_t n2 = 2 * (size_t)N;
+    cudaStream_t st = ctx->stream;
+    double* xacc = s->xs;            // accepted (V, T)
+    double* xprev = s->xs + n2;      // accepted one step earlier
+    double* xit = s->xs + 2 * n2;    // current iterate (x_old)
+    double* xnew = s->xs + 3 * n2;   // solve output
+    if (int rc = fill_initial(ctx, xacc, N, p->initial_temp)) return rc;
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(xprev, xacc, sizeof(double) * n2, cudaMemcpyDeviceToDevice, st));
+    SysStatus* ds = sys_status(s);
+    const MatView A = system_view(s);
+    const bool pre = p->solver.precondition == RAFEM_PRECOND_JACOBI;
+    rafem_assemble_params ap{};
+    ap.applied_voltage = p->applied_voltage;
+    ap.boundary_temp = p->boundary_temp;
+    ap.apply_constraints = 1;
+    ap.equilibrate = 1;
+
+    double t = 0.0, dt_state = p->dt_init, dt_prev = p->dt_init;
+    long long step = 0, passes = 0, total_corr = 0, total_inner = 0, halvings = 0;
+    double asm_ms = 0.0, sol_ms = 0.0;
+    int status = RAFEM_OK;
+    while (t < p->total_time) {
+        if (p->max_steps > 0 && step >= p->max_steps) break;
+        const double remaining = p->total_time - t;
+        const bool final_step = dt_state >= remaining;
+        const double dt = final_step ? remaining : dt_state;
+        if (int rc = predictor_launch(ctx, xit, xacc, xprev, N, (int)step, dt / dt_prev)) return rc;
+        bool converged = false;
+        int iters = 0;
+        for (int it = 1; it <= p->max_corrector_iters; ++it) {
+            iters = it;
+            ++passes;
+            ap.dt = dt;
+            RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+            if (int rc = assemble_launch(s, xit + 1, 2, xit, 2, xacc + 1, 2, ap, &ds->pass.scale, &ds->pass.bad_element))
+                return rc;
+            if (pre) {
+                if (int rc = jacobi_minv(ctx, A, s->minv, &ds->flag)) return rc;
+            } else {
+                RF_CUDA_TRY(ctx, cudaMemsetAsync(&ds->flag, 0, sizeof(int), st));
+            }
+            if (int rc = krylov_solve(ctx, A, s->rhs, xit, xnew, s->minv, p->solver, &ds->pass.solve, &ds->flag,
+                                      ctx->ev1, ctx->ev2))
+                return rc;
+            if (int rc = vec_delta_launch(ctx, xnew, xit, (int)n2, &ds->pass.delta)) return rc;
+            PassStatus hs;
+            RF_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, &ds->pass, sizeof(hs), cudaMemcpyDeviceToHost, st));
+            RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+            float a_ms = 0.f, s_ms = 0.f;
+            cudaEventElapsedTime(&a_ms, ctx->ev0, ctx->ev1);
+            cudaEventElapsedTime(&s_ms, ctx->ev1, ctx->ev2);
+            asm_ms += a_ms;
+            sol_ms += s_ms;
+            if (hs.bad_element >= 0) {  // PhysicsRangeError aborts the run (fem.py:274)
+                out->bad_element = hs.bad_element;
+                status = RAFEM_ERR_PHYSICS;
+                break;
+            }
+            if (hs.solve.status == RAFEM_ERR_INVALID) {  // ValueError aborts the run
+                status = RAFEM_ERR_INVALID;
+                ctx->err = "Jacobi preconditioning requires a zero-free diagonal";
+                break;
+            }
+            if (hs.solve.status == RAFEM_ERR_BREAKDOWN) break;  // SolverError -> step failure (fem.py:511-515)
+            total_inner += hs.solve.iterations;
+            if (!hs.solve.converged) break;                   // fem.py:517-524
+            std::swap(xit, xnew);                              // x_old = x_new (fem.py:529-530)
+            if (hs.delta < p->corrector_tol) {
+                converged = true;
+                break;
+            }
+        }
+        if (status != RAFEM_OK) break;
+        total_corr += iters;
+        if (converged) {
+            // rotate: prev <- acc <- iterate   (fem.py:604-607)
+            double* old_prev = xprev;
+            xprev = xacc;
+            xacc = xit;
+            xit = old_prev;
+            dt_prev = dt;
+            t = final_step ? p->total_time : t + dt;
+            if (step < rec_cap) {
+                if (rec_step) rec_step[step] = step;
+                if (rec_time) rec_time[step] = t;
+                if (rec_dt) rec_dt[step] = dt;
+                if (rec_iters) rec_iters[step] = iters;
+                if (p->record_fields && rec_x)
+                    RF_CUDA_TRY(ctx, cudaMemcpyAsync(rec_x + (size_t)step * n2, xacc, sizeof(double) * n2,
+                                                     cudaMemcpyDeviceToHost, st));
+            }
+            ++step;
+            if (iters <= 5)
+                dt_state = std::min(dt * 1.5, p->dt_max);
+            else if (iters >= 20)
+                dt_state = std::max(dt * 0.75, p->dt_min);
+            else
+                dt_state = dt;
+        } else {
+            if (dt <= p->dt_min) {  // StepFailureError (fem.py:629-631)
+                status = RAFEM_ERR_STEP_FAILURE;
+                out->failed_step = (int)step;
+                out->failed_dt = dt;
+                break;
+            }
+            dt_state = std::max(dt * 0.5, p->dt_min);
+            ++halvings;
+        }
+    }
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    // keep the final accepted state at the front of xs for callers
+    if (xacc != s->xs) RF_CUDA_TRY(ctx, cudaMemcpy(s->xs, xacc, sizeof(double) * n2, cudaMemcpyDeviceToDevice));
+    out->accepted_steps = step;
+    out->total_corrector_iters = total_corr;
+    out->total_solver_iterations = total_inner;
+    out->dt_halvings = halvings;
+    out->passes = passes;
+    out->final_time = t;
+    out->status = status;
+    out->assemble_ms = asm_ms;
+    out->solve_ms = sol_ms;
+    out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_wall).count();
+    if (status == RAFEM_ERR_PHYSICS) {
+        char buf[128];
+        std::snprintf(buf, sizeof(buf), "sigma(T) <= 0 in element %lld", (long long)out->bad_element);
+        return rafem_fail(ctx, status, buf);
+    }
+    if (status == RAFEM_ERR_STEP_FAILURE) {
+        char buf[160];
+        std::snprintf(buf, sizeof(buf), "step %d failed to converge with dt already at the floor (%g s)",
+                      out->failed_step, out->failed_dt);
+        return rafem_fail(ctx, status, buf);
+    }
+    return status;
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+// common.cuh — shared device helpers for librafem_b200 (sm_100a).
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cg = cooperative_groups;
+
+#define RF_DEV __device__ __forceinline__
+
+namespace rafem {
+
+// Exact IEEE-754 ops.  FMA contraction would change the rounding of the
+// reference's numpy expressions (each numpy op rounds separately), so
+// every accumulation that must be bit-stable spells its ops explicitly.
+RF_DEV double mul(double a, double b) { return __dmul_rn(a, b); }
+RF_DEV double add(double a, double b) { return __dadd_rn(a, b); }
+RF_DEV double sub(double a, double b) { return __dsub_rn(a, b); }
+
+constexpr int kWarp = 32;
+
+// Streaming (evict-first) loads for matrix data that is read once per
+// sweep, so the gathered vector keeps its place in L2.
+RF_DEV double ld_stream(const double* p) { return __ldcs(p); }
+RF_DEV double2 ld_stream(const double2* p) { return __ldcs(p); }
+RF_DEV int ld_stream(const int* p) { return __ldcs(p); }
+
+// Deterministic warp sum: fixed xor-butterfly, so every lane ends with
+// the same bits and the result depends only on the lane values.
+RF_DEV double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = add(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+RF_DEV double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Block-wide deterministic sum of NV values per thread.  Result valid in
+// all threads.  `red` must hold NV * 32 doubles of shared memory.
+template <int NV>
+RF_DEV void block_sum(double (&v)[NV], double* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+    __syncthreads();  // protect `red` from a previous use
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) red[i * 32 + wid] = v[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        double s = (lane < nw) ? red[i * 32 + lane] : 0.0;
+        v[i] = warp_sum(s);
+    }
+}
+
+RF_DEV double block_max(double v, double* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_max(v);
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    double s = (lane < nw) ? red[lane] : 0.0;
+    return warp_max(s);
+}
+
+// Sum of partial[0..G) (one per CTA) in a fixed order, by one warp.
+// Every CTA that calls this sees identical bits.
+RF_DEV double reduce_partials_warp(const double* partial, int G) {
+    const int lane = threadIdx.x & 31;
+    double s = 0.0;
+    for (int c = lane; c < G; c += 32) s = add(s, __ldcg(partial + c));
+    return warp_sum(s);
+}
+
+}  // namespace rafem
+
+// Host-side error plumbing shared by the .cu translation units.
+#define RF_CUDA_TRY(ctx, expr)                                                   \
+    do {                                                                         \
+        cudaError_t _e = (expr);                                                 \
+        if (_e != cudaSuccess) return rafem_fail_cuda((ctx), _e, #expr, __FILE__, __LINE__); \
+    } while (0)

@@ -1,0 +1,163 @@
+// internal.hpp — host-side structures shared by the librafem_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/rafem_b200.h"
+
+namespace rafem {
+
+// Result block a Krylov kernel leaves in device memory (read back by the
+// host API, or inspected on device by the native time loop).
+struct KResult {
+    long long iterations;
+    long long restarts;
+    long long cycles;
+    long long hist_len;
+    double final_rel;
+    int converged;
+    int stagnated;
+    int status;  // RAFEM_OK / RAFEM_ERR_BREAKDOWN / RAFEM_ERR_INVALID
+    int pad;
+};
+
+// Per-pass status the native loop reads back (one small D2H per pass).
+struct PassStatus {
+    KResult solve;
+    double delta;          // corrector delta max|dx|/max(1,|x_old|)
+    long long bad_element; // PhysicsRangeError element or -1
+    double scale;          // voltage_row_scale of the pass
+};
+
+// Matrix view consumed by the Krylov and SpMV kernels.  W = dofs per row
+// group: 1 for a general CSR (one row per group), 2 for the FEM node
+// pattern (rows 2i and 2i+1 share node i's columns; one double2 per slot).
+struct MatView {
+    const int* rp;      // ngroups + 1
+    const int* col;     // slots, GROUP (node) indices
+    const double* val;  // W doubles per slot
+    int ngroups;
+    int W;
+    long long slots;
+};
+
+// Growable device scratch owned by a context.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace rafem
+
+struct rafem_ctx {
+    int device = 0;
+    int sm_count = 0;
+    int cc_major = 0, cc_minor = 0;
+    long long total_mem = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+    std::string err;
+    long long launches = 0;
+    // solver workspace (grown on demand)
+    rafem::DevBuf ws_basis, ws_vec, ws_partial, ws_hess, ws_hist, ws_cyc, ws_part, ws_res;
+    // host pinned staging
+    void* pin = nullptr;
+    size_t pin_bytes = 0;
+    int coop_occ_gmres[2][2] = {{0, 0}, {0, 0}};
+};
+
+struct rafem_matrix {
+    rafem_ctx* ctx = nullptr;
+    int n = 0;
+    long long nnz = 0;
+    int* rp = nullptr;
+    int* col = nullptr;
+    double* val = nullptr;
+    double* minv = nullptr;
+};
+
+struct rafem_mesh {
+    rafem_ctx* ctx = nullptr;
+    int N = 0, M = 0;
+    long long slots = 0;
+    int maxdeg = 0;     // max slots per node row
+    int maxinc = 0;     // max incident tets per node
+    // inputs
+    double* nodes = nullptr;  // N x 3
+    int* tets = nullptr;      // M x 4
+    int* region = nullptr;    // M
+    int nreg = 0;
+    double* regtab = nullptr; // 5 x nreg: k, rho_c, sigma0, alpha, t_ref
+    uint8_t* kind = nullptr;  // 2N dof kinds
+    // symbolic pattern
+    int* rp = nullptr;        // N + 1
+    int* col = nullptr;       // slots
+    int* diag = nullptr;      // N: slot offset of the diagonal within its row
+    int* inc_ptr = nullptr;   // N + 1
+    unsigned* inc_ea = nullptr;   // 4M: tet | (local index << 30)
+    unsigned* inc_slot = nullptr; // 4M: 4 x uint8 row offsets of the tet's nodes
+    // geometry (constant per mesh)
+    double* base = nullptr;   // M x 10: vol * grad_a . grad_b, symmetric packed
+    double* grad = nullptr;   // M x 12
+    double* vol = nullptr;    // M
+};
+
+struct rafem_system {
+    rafem_mesh* mesh = nullptr;
+    double* val2 = nullptr;   // slots x 2 (V, T)
+    double* rhs = nullptr;    // 2N
+    double* sigma = nullptr;  // M
+    double* load = nullptr;   // M x 4 T-rhs element contributions
+    double* diagpart = nullptr; // 2 x G partial diag sums
+    double* minv = nullptr;   // 2N
+    double* xin = nullptr;    // 3N staging for host inputs / 2N iterate buffers
+    double* status = nullptr; // device PassStatus + scratch
+    double scale = 1.0;
+    // native-loop state
+    double* xs = nullptr;     // 5 x 2N dof vectors
+};
+
+// error helpers (capi.cu)
+int rafem_fail(rafem_ctx* ctx, int code, const std::string& msg);
+int rafem_fail_cuda(rafem_ctx* ctx, cudaError_t e, const char* what, const char* file, int line);
+
+namespace rafem {
+
+// krylov.cu
+int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const double* x0_dev,
+                 double* x_dev, const double* minv_dev, const rafem_solver_params& p,
+                 KResult* res_dev, int* flag_dev, cudaEvent_t ev_start = nullptr,
+                 cudaEvent_t ev_stop = nullptr);
+int jacobi_minv(rafem_ctx* ctx, const MatView& A, double* minv_dev, int* flag_dev);
+int krylov_read_history(rafem_ctx* ctx, const KResult& r, double* hist, long long hist_cap,
+                        long long* cyc, long long cyc_cap);
+int spmv_launch(rafem_ctx* ctx, const MatView& A, const double* x_dev, double* y_dev);
+int vec_delta_launch(rafem_ctx* ctx, const double* xn, const double* xo, int n, double* out_dev);
+
+// assembly.cu
+int mesh_symbolic(rafem_mesh* m);
+int mesh_geometry(rafem_mesh* m);
+int assemble_launch(rafem_system* s, const double* t_it, int ts, const double* v_it, int vs,
+                    const double* t_prev, int ps, const rafem_assemble_params& p,
+                    double* scale_dev, long long* bad_dev);
+int expand_dof_vals(rafem_system* s, double* out_dev);
+int predictor_launch(rafem_ctx* ctx, double* x_it, const double* x_acc, const double* x_prev,
+                     int N, int step, double ratio);
+int fill_initial(rafem_ctx* ctx, double* x, int N, double t0);
+
+// sparse.cu
+int scan_ints(rafem_ctx* ctx, const int* in, int* out, int n);
+int coo_to_csr_device(rafem_ctx* ctx, long long nrows, long long ncols, long long nnz,
+                      const int64_t* rows, const int64_t* cols, const double* vals,
+                      int64_t* row_ptr_out, int64_t* col_idx_out, double* vals_out,
+                      int64_t* nnz_out);
+
+// grow a device buffer to at least `bytes`
+int ensure(rafem_ctx* ctx, DevBuf& b, size_t bytes);
+void* pinned(rafem_ctx* ctx, size_t bytes);
+
+}  // namespace rafem

@@ -1,0 +1,889 @@
+// krylov.cu — persistent-kernel Krylov solvers and SpMV for sm_100a.
+//
+// Reference semantics: solver.py:381-531 (restarted GMRES(m), Givens LSQ,
+// right Jacobi, true-residual restarts, stagnation latch, breakdown rules)
+// and sparse.py:205-219 (SpMV, per-row left-to-right sums).
+//
+// One cooperative launch runs a whole solve: every CTA owns a contiguous
+// block of row groups (balanced by slots + rows), keeps its share of every
+// vector, and meets the others only at grid barriers around the scalar
+// reductions.  Reductions are deterministic: per-thread partial sums in a
+// fixed order, a fixed xor-butterfly per warp, per-CTA partials in global
+// memory, and every CTA re-reduces the G partials in the same fixed order,
+// so all CTAs take identical control decisions and results are bitwise
+// reproducible run to run.
+#include "common.cuh"
+#include "internal.hpp"
+
+#include <algorithm>
+#include <cmath>
+
+namespace rafem {
+
+constexpr int KT = 512;  // threads per CTA of the persistent kernels
+
+struct KArgs {
+    MatView A;
+    const int* gpart;  // G + 1 group partition
+    long long ldv;     // basis row stride
+    const double* b;
+    double* x;
+    const double* minv;
+    double* V;  // GMRES basis, (m + 1) x ldv
+    double* w0;
+    double* w1;
+    double* r;
+    double* z;
+    double* p0;
+    double* p1;
+    double* q;
+    double* partial;  // 2 x (m + 2) x G
+    double* hess;     // per-CTA Hessenberg scratch when it does not fit in smem
+    long long hess_stride;
+    int m;
+    double tol;
+    long long cap;
+    double* hist;
+    long long hist_cap;
+    long long* cyc;
+    long long cyc_cap;
+    KResult* res;
+    const int* flag;  // nonzero: zero diagonal under Jacobi -> ValueError
+};
+
+// ---------------------------------------------------------------------------
+// SpMV over this CTA's row groups.  Each group's rows are summed left to
+// right over the stored slots with separately rounded products: exactly
+// the reference's bincount order (sparse.py:217-218), so y is bit-identical.
+
+template <bool STREAM>
+RF_DEV int ldcol(const int* p) {
+    return STREAM ? __ldcs(p) : __ldg(p);
+}
+template <bool STREAM>
+RF_DEV double ldval(const double* p) {
+    return STREAM ? __ldcs(p) : __ldg(p);
+}
+template <bool STREAM>
+RF_DEV double2 ldval2(const double2* p) {
+    return STREAM ? __ldcs(p) : __ldg(p);
+}
+
+template <int W, bool STREAM, class Src, class Epi>
+RF_DEV void spmv_groups(const MatView& A, int g0, int g1, const Src& src, Epi&& epi) {
+    for (int g = g0 + threadIdx.x; g < g1; g += blockDim.x) {
+        const int s0 = __ldg(A.rp + g), s1 = __ldg(A.rp + g + 1);
+        if constexpr (W == 1) {
+            double acc = 0.0;
+            for (int s = s0; s < s1; ++s)
+                acc = add(acc, mul(ldval<STREAM>(A.val + s), src.at(ldcol<STREAM>(A.col + s))));
+            double y[1] = {acc};
+            epi(g, y);
+        } else {
+            const double2* v2 = reinterpret_cast<const double2*>(A.val);
+            double av = 0.0, at = 0.0;
+            for (int s = s0; s < s1; ++s) {
+                const int c = ldcol<STREAM>(A.col + s);
+                const double2 a2 = ldval2<STREAM>(v2 + s);
+                const double2 xx = src.at2(c);
+                av = add(av, mul(a2.x, xx.x));
+                at = add(at, mul(a2.y, xx.y));
+            }
+            double y[2] = {av, at};
+            epi(g, y);
+        }
+    }
+}
+
+// Operand sources: the SpMV input is formed on the fly from vectors that
+// are final after the previous grid barrier, which saves a barrier per
+// Krylov step.
+struct SrcPlain {
+    const double* x;
+    RF_DEV double at(int j) const { return __ldcg(x + j); }
+    RF_DEV double2 at2(int c) const { return __ldcg(reinterpret_cast<const double2*>(x) + c); }
+};
+
+// GMRES: z_j = minv_j * (s_j * c), where v_k = s * c is the next basis
+// vector (c = 1/beta or 1/h_{k,k-1}); owners store the same bits in V[k].
+template <bool PRE>
+struct SrcBasis {
+    const double* s;
+    double c;
+    const double* minv;
+    RF_DEV double at(int j) const {
+        double v = mul(__ldcg(s + j), c);
+        return PRE ? mul(v, __ldg(minv + j)) : v;
+    }
+    RF_DEV double2 at2(int cc) const {
+        double2 sv = __ldcg(reinterpret_cast<const double2*>(s) + cc);
+        double2 v = make_double2(mul(sv.x, c), mul(sv.y, c));
+        if (PRE) {
+            double2 mv = __ldg(reinterpret_cast<const double2*>(minv) + cc);
+            v.x = mul(v.x, mv.x);
+            v.y = mul(v.y, mv.y);
+        }
+        return v;
+    }
+};
+
+// PCG: p_j = z_j + beta * pold_j (first step: p = z).
+struct SrcCg {
+    const double* z;
+    const double* po;
+    double beta;
+    int first;
+    RF_DEV double at(int j) const {
+        double zj = __ldcg(z + j);
+        return first ? zj : add(zj, mul(beta, __ldcg(po + j)));
+    }
+    RF_DEV double2 at2(int c) const {
+        double2 zz = __ldcg(reinterpret_cast<const double2*>(z) + c);
+        if (first) return zz;
+        double2 pp = __ldcg(reinterpret_cast<const double2*>(po) + c);
+        return make_double2(add(zz.x, mul(beta, pp.x)), add(zz.y, mul(beta, pp.y)));
+    }
+};
+
+// ---------------------------------------------------------------------------
+// reduction plumbing
+
+// Publish nv (<= 8) block-reduced values as this CTA's partials.
+template <int NV>
+RF_DEV void publish(double (&v)[NV], int nv, double* P, int base, int G, double* red) {
+    block_sum<NV>(v, red);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+            if (j < nv) P[(long long)(base + j) * G + blockIdx.x] = v[j];
+    }
+}
+
+// After a grid barrier: reduce nv coefficient rows of P into co[] (all CTAs).
+RF_DEV void gather(const double* P, int nv, int G, double* co) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int i = wid; i < nv; i += nw) {
+        double s = reduce_partials_warp(P + (long long)i * G, G);
+        if (lane == 0) co[i] = s;
+    }
+    __syncthreads();
+}
+
+// Per-CTA dots v_i . w for i < nv over dofs [lo, hi), published into P.
+RF_DEV void multidot(const double* V, long long ldv, int nv, const double* w, int lo, int hi,
+                     double* P, int G, double* red) {
+    for (int i0 = 0; i0 < nv; i0 += 8) {
+        double acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+        const int cnt = min(8, nv - i0);
+        for (int e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+            const double we = w[e];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j < cnt) acc[j] = add(acc[j], mul(__ldcg(V + (long long)(i0 + j) * ldv + e), we));
+        }
+        publish<8>(acc, cnt, P, i0, G, red);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// GMRES(m) — solver.py:381-531, with classical Gram-Schmidt applied twice
+// (CGS2) in place of the reference's modified Gram-Schmidt: the same
+// Arnoldi basis to working precision, but 3 grid barriers per step instead
+// of k + 2 dependent reductions.
+
+template <int W, bool PRE, bool STREAM>
+__global__ void __launch_bounds__(KT, 1) gmres_kernel(KArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) double dyn[];
+    __shared__ double red[32 * 8];
+    __shared__ double sc[4];
+    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
+    const int g0 = a.gpart[cta], g1 = a.gpart[cta + 1];
+    const int lo = W * g0, hi = W * g1;
+    const int m = a.m;
+    const long long ldv = a.ldv;
+    double* H = a.hess ? a.hess + (long long)cta * a.hess_stride : dyn;  // col-major (m+1) x m
+    double* cs = H + (long long)(m + 1) * m;
+    double* sn = cs + m;
+    double* gg = sn + m;      // m + 1
+    double* yy = gg + m + 1;  // m
+    double* co = yy + m;      // m + 2
+    const long long pstride = (long long)(m + 2) * G;
+    int par = 0;
+
+    if (*a.flag) {
+        if (cta == 0 && tid == 0) {
+            a.res->status = RAFEM_ERR_INVALID;
+            a.res->converged = 0;
+            a.res->iterations = 0;
+        }
+        return;
+    }
+
+    // ||b||  (solver.py:421)
+    {
+        double v[1] = {0.0};
+        for (int e = lo + tid; e < hi; e += bd) {
+            const double be = a.b[e];
+            v[0] = add(v[0], mul(be, be));
+        }
+        publish<1>(v, 1, a.partial + par * pstride, 0, G, red);
+        grid.sync();
+        gather(a.partial + par * pstride, 1, G, co);
+        par ^= 1;
+    }
+    const double bnorm = sqrt(co[0]);
+    if (bnorm == 0.0) {  // zero data: zero solution (solver.py:422-425)
+        for (int e = lo + tid; e < hi; e += bd) a.x[e] = 0.0;
+        if (cta == 0 && tid == 0) {
+            a.res->iterations = 0;
+            a.res->restarts = 0;
+            a.res->cycles = 0;
+            a.res->hist_len = 0;
+            a.res->final_rel = 0.0;
+            a.res->converged = 1;
+            a.res->stagnated = 0;
+            a.res->status = RAFEM_OK;
+        }
+        return;
+    }
+
+    const MatView A = a.A;
+    // r = b - A x, returns ||r|| / ||b||   (solver.py:438-439, 517-518)
+    auto true_residual = [&]() -> double {
+        double v[1] = {0.0};
+        spmv_groups<W, STREAM>(A, g0, g1, SrcPlain{a.x}, [&](int g, const double* y) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                const int e = W * g + w;
+                const double re = sub(a.b[e], y[w]);
+                a.r[e] = re;
+                v[0] = add(v[0], mul(re, re));
+            }
+        });
+        publish<1>(v, 1, a.partial + par * pstride, 0, G, red);
+        grid.sync();
+        gather(a.partial + par * pstride, 1, G, co);
+        par ^= 1;
+        return sqrt(co[0]) / bnorm;
+    };
+
+    long long total = 0, cycles = 0, hlen = 0;
+    int weak = 0;
+    bool latched = false, have_prev = false, converged = false;
+    double prev_start = 0.0, rel = INFINITY;
+    int status = RAFEM_OK;
+    const double tiny = 2.2250738585072014e-308;  // np.finfo(float64).tiny
+
+    while (true) {
+        rel = true_residual();
+        if (have_prev) {  // stagnation bookkeeping (solver.py:440-447)
+            if (rel > (1.0 - 1e-3) * prev_start) {
+                if (++weak >= 3) latched = true;
+            } else {
+                weak = 0;
+            }
+            have_prev = false;
+        }
+        if (rel <= a.tol) {
+            converged = true;
+            break;
+        }
+        if (total >= a.cap) break;
+
+        const double cycle_start = rel;
+        const double beta = rel * bnorm;
+        if (tid == 0) {
+            for (int i = 0; i <= m; ++i) gg[i] = 0.0;
+            gg[0] = beta;
+        }
+        const double* src = a.r;
+        double src_scale = 1.0 / beta;
+        int used = 0;
+        bool broke = false, dead = false;
+        const long long hstart = hlen;
+
+        for (int k = 0; k < m; ++k) {
+            double* wk = (k & 1) ? a.w1 : a.w0;
+            double* Vk = a.V + (long long)k * ldv;
+            // v_k (own rows) and w = A (M^-1 v_k)       (solver.py:469-470)
+            for (int e = lo + tid; e < hi; e += bd) Vk[e] = mul(src[e], src_scale);
+            if (a.minv) {
+                spmv_groups<W, STREAM>(A, g0, g1, SrcBasis<PRE>{src, src_scale, a.minv},
+                                       [&](int g, const double* y) {
+#pragma unroll
+                                           for (int w = 0; w < W; ++w) wk[W * g + w] = y[w];
+                                       });
+            } else {
+                spmv_groups<W, STREAM>(A, g0, g1, SrcBasis<false>{src, src_scale, nullptr},
+                                       [&](int g, const double* y) {
+#pragma unroll
+                                           for (int w = 0; w < W; ++w) wk[W * g + w] = y[w];
+                                       });
+            }
+            __syncthreads();
+            // CGS pass 1: h_i = v_i . w
+            double* P = a.partial + par * pstride;
+            multidot(a.V, ldv, k + 1, wk, lo, hi, P, G, red);
+            grid.sync();
+            gather(P, k + 1, G, co);
+            par ^= 1;
+            if (tid == 0)
+                for (int i = 0; i <= k; ++i) H[(long long)k * (m + 1) + i] = co[i];
+            // w -= sum h_i v_i ; CGS pass 2: c_i = v_i . w
+            for (int e = lo + tid; e < hi; e += bd) {
+                double acc = wk[e];
+                for (int i = 0; i <= k; ++i) acc = sub(acc, mul(co[i], __ldcg(a.V + (long long)i * ldv + e)));
+                wk[e] = acc;
+            }
+            P = a.partial + par * pstride;
+            multidot(a.V, ldv, k + 1, wk, lo, hi, P, G, red);
+            grid.sync();
+            gather(P, k + 1, G, co);
+            par ^= 1;
+            if (tid == 0)
+                for (int i = 0; i <= k; ++i) H[(long long)k * (m + 1) + i] = add(H[(long long)k * (m + 1) + i], co[i]);
+            // w -= sum c_i v_i ; ||w||
+            {
+                double v[1] = {0.0};
+                for (int e = lo + tid; e < hi; e += bd) {
+                    double acc = wk[e];
+                    for (int i = 0; i <= k; ++i)
+                        acc = sub(acc, mul(co[i], __ldcg(a.V + (long long)i * ldv + e)));
+                    wk[e] = acc;
+                    v[0] = add(v[0], mul(acc, acc));
+                }
+                P = a.partial + par * pstride;
+                publish<1>(v, 1, P, 0, G, red);
+                grid.sync();
+                gather(P, 1, G, co);
+                par ^= 1;
+            }
+            const double hk1 = sqrt(co[0]);
+            total += 1;
+            // Givens update of column k (solver.py:478-496), one thread per CTA
+            if (tid == 0) {
+                double* hc = H + (long long)k * (m + 1);
+                hc[k + 1] = hk1;
+                for (int i = 0; i < k; ++i) {
+                    const double t = add(mul(cs[i], hc[i]), mul(sn[i], hc[i + 1]));
+                    hc[i + 1] = add(mul(-sn[i], hc[i]), mul(cs[i], hc[i + 1]));
+                    hc[i] = t;
+                }
+                const double rad = hypot(hc[k], hc[k + 1]);
+                double est = 0.0;
+                int isdead = 0;
+                if (rad == 0.0) {
+                    isdead = 1;
+                } else {
+                    cs[k] = hc[k] / rad;
+                    sn[k] = hc[k + 1] / rad;
+                    hc[k] = rad;
+                    hc[k + 1] = 0.0;
+                    gg[k + 1] = mul(-sn[k], gg[k]);
+                    gg[k] = mul(cs[k], gg[k]);
+                    est = fabs(gg[k + 1]) / bnorm;
+                    if (cta == 0 && hlen < a.hist_cap) a.hist[hlen] = est;
+                }
+                sc[0] = isdead;
+                sc[1] = est;
+            }
+            __syncthreads();
+            if (sc[0] != 0.0) {  // column added nothing (solver.py:483-487)
+                dead = true;
+                used = k;
+                break;
+            }
+            used = k + 1;
+            const double est = sc[1];
+            ++hlen;
+            if (hk1 < tiny) {  // breakdown (solver.py:497-499)
+                broke = true;
+                break;
+            }
+            src = wk;
+            src_scale = 1.0 / hk1;
+            if (est <= a.tol || total >= a.cap) break;
+        }
+
+        if (used > 0) {  // y = R^-1 g ; x += M^-1 (V y)   (solver.py:504-511)
+            if (tid == 0) {
+                for (int i = used - 1; i >= 0; --i) {
+                    double d = 0.0;
+                    for (int j = i + 1; j < used; ++j) d = add(d, mul(H[(long long)j * (m + 1) + i], yy[j]));
+                    yy[i] = sub(gg[i], d) / H[(long long)i * (m + 1) + i];
+                }
+            }
+            __syncthreads();
+            for (int e = lo + tid; e < hi; e += bd) {
+                double u = 0.0;
+                for (int i = 0; i < used; ++i) u = add(u, mul(__ldcg(a.V + (long long)i * ldv + e), yy[i]));
+                if (PRE) u = mul(a.minv[e], u);
+                a.x[e] = add(a.x[e], u);
+            }
+        }
+        if (cta == 0 && tid == 0 && cycles < a.cyc_cap) a.cyc[cycles] = hlen - hstart;
+        ++cycles;
+        have_prev = true;
+        prev_start = cycle_start;
+        grid.sync();  // x final everywhere before the next SpMV
+
+        if (broke || dead) {  // solver.py:516-524
+            rel = true_residual();
+            if (rel <= a.tol) {
+                converged = true;
+            } else {
+                status = RAFEM_ERR_BREAKDOWN;
+            }
+            break;
+        }
+    }
+
+    if (cta == 0 && tid == 0) {
+        a.res->iterations = total;
+        a.res->restarts = cycles > 0 ? cycles - 1 : 0;
+        a.res->cycles = cycles;
+        a.res->hist_len = hlen;
+        a.res->final_rel = rel;
+        a.res->converged = converged ? 1 : 0;
+        a.res->stagnated = (latched && !converged) ? 1 : 0;
+        a.res->status = status;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Jacobi-preconditioned CG with two grid barriers per iteration (p is
+// formed on the fly inside the SpMV gather).  Not in the reference (which
+// ships GMRES only); used for the SPD FEM systems under its own backend
+// name.  Converged only when the TRUE residual meets the tolerance: a
+// recursive-residual exit re-enters at the top with r = b - A x and
+// restarts the recurrence if needed (mirrors solver.py:437-450).
+
+template <int W, bool PRE, bool STREAM>
+__global__ void __launch_bounds__(KT, 1) pcg_kernel(KArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red[32 * 8];
+    __shared__ double co[8];
+    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
+    const int g0 = a.gpart[cta], g1 = a.gpart[cta + 1];
+    const int lo = W * g0, hi = W * g1;
+    const long long pstride = 8LL * G;
+    int par = 0;
+
+    if (*a.flag) {
+        if (cta == 0 && tid == 0) {
+            a.res->status = RAFEM_ERR_INVALID;
+            a.res->converged = 0;
+            a.res->iterations = 0;
+        }
+        return;
+    }
+    {
+        double v[1] = {0.0};
+        for (int e = lo + tid; e < hi; e += bd) {
+            const double be = a.b[e];
+            v[0] = add(v[0], mul(be, be));
+        }
+        publish<1>(v, 1, a.partial + par * pstride, 0, G, red);
+        grid.sync();
+        gather(a.partial + par * pstride, 1, G, co);
+        par ^= 1;
+    }
+    const double bnorm = sqrt(co[0]);
+    if (bnorm == 0.0) {
+        for (int e = lo + tid; e < hi; e += bd) a.x[e] = 0.0;
+        if (cta == 0 && tid == 0) {
+            a.res->iterations = 0;
+            a.res->restarts = 0;
+            a.res->cycles = 0;
+            a.res->hist_len = 0;
+            a.res->final_rel = 0.0;
+            a.res->converged = 1;
+            a.res->stagnated = 0;
+            a.res->status = RAFEM_OK;
+        }
+        return;
+    }
+    const MatView A = a.A;
+    long long total = 0, cycles = 0, hlen = 0;
+    bool converged = false;
+    double rel = INFINITY;
+    int status = RAFEM_OK;
+
+    while (true) {
+        double rz, rr;
+        {  // r = b - A x ; z = M^-1 r ; (r.z, r.r)
+            double v[2] = {0.0, 0.0};
+            spmv_groups<W, STREAM>(A, g0, g1, SrcPlain{a.x}, [&](int g, const double* y) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    const int e = W * g + w;
+                    const double re = sub(a.b[e], y[w]);
+                    const double ze = PRE ? mul(a.minv[e], re) : re;
+                    a.r[e] = re;
+                    a.z[e] = ze;
+                    v[0] = add(v[0], mul(re, ze));
+                    v[1] = add(v[1], mul(re, re));
+                }
+            });
+            double* P = a.partial + par * pstride;
+            publish<2>(v, 2, P, 0, G, red);
+            grid.sync();
+            gather(P, 2, G, co);
+            par ^= 1;
+            rz = co[0];
+            rr = co[1];
+        }
+        rel = sqrt(rr) / bnorm;
+        if (rel <= a.tol) {
+            converged = true;
+            break;
+        }
+        if (total >= a.cap) break;
+        if (!(rz > 0.0) || !isfinite(rz)) {  // not SPD under this preconditioner
+            status = RAFEM_ERR_BREAKDOWN;
+            break;
+        }
+        const long long hstart = hlen;
+        double beta = 0.0;
+        int first = 1, pc = 0;
+        while (true) {
+            double* pn = pc ? a.p1 : a.p0;
+            const double* po = pc ? a.p0 : a.p1;
+            double pq;
+            {  // q = A p, p = z + beta p_old formed in the gather; p.q
+                double v[1] = {0.0};
+                const SrcCg src{a.z, po, beta, first};
+                spmv_groups<W, STREAM>(A, g0, g1, src, [&](int g, const double* y) {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) {
+                        const int e = W * g + w;
+                        const double pe = src.at(e);
+                        pn[e] = pe;
+                        a.q[e] = y[w];
+                        v[0] = add(v[0], mul(pe, y[w]));
+                    }
+                });
+                double* P = a.partial + par * pstride;
+                publish<1>(v, 1, P, 0, G, red);
+                grid.sync();
+                gather(P, 1, G, co);
+                par ^= 1;
+                pq = co[0];
+            }
+            if (!(pq > 0.0) || !isfinite(pq)) {
+                status = RAFEM_ERR_BREAKDOWN;
+                break;
+            }
+            const double alpha = rz / pq;
+            double rzn;
+            {  // x += alpha p ; r -= alpha q ; z = M^-1 r ; (r.z, r.r)
+                double v[2] = {0.0, 0.0};
+                for (int e = lo + tid; e < hi; e += bd) {
+                    a.x[e] = add(a.x[e], mul(alpha, pn[e]));
+                    const double re = sub(a.r[e], mul(alpha, a.q[e]));
+                    const double ze = PRE ? mul(a.minv[e], re) : re;
+                    a.r[e] = re;
+                    a.z[e] = ze;
+                    v[0] = add(v[0], mul(re, ze));
+                    v[1] = add(v[1], mul(re, re));
+                }
+                double* P = a.partial + par * pstride;
+                publish<2>(v, 2, P, 0, G, red);
+                grid.sync();
+                gather(P, 2, G, co);
+                par ^= 1;
+                rzn = co[0];
+                rr = co[1];
+            }
+            ++total;
+            const double est = sqrt(rr) / bnorm;
+            if (cta == 0 && tid == 0 && hlen < a.hist_cap) a.hist[hlen] = est;
+            ++hlen;
+            if (est <= a.tol || total >= a.cap) break;
+            if (!(rzn > 0.0) || !isfinite(rzn)) {
+                status = RAFEM_ERR_BREAKDOWN;
+                break;
+            }
+            beta = rzn / rz;
+            rz = rzn;
+            first = 0;
+            pc ^= 1;
+        }
+        if (cta == 0 && tid == 0 && cycles < a.cyc_cap) a.cyc[cycles] = hlen - hstart;
+        ++cycles;
+        if (status != RAFEM_OK) break;
+    }
+    if (cta == 0 && tid == 0) {
+        a.res->iterations = total;
+        a.res->restarts = cycles > 0 ? cycles - 1 : 0;
+        a.res->cycles = cycles;
+        a.res->hist_len = hlen;
+        a.res->final_rel = rel;
+        a.res->converged = converged ? 1 : 0;
+        a.res->stagnated = 0;
+        a.res->status = status;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// helper kernels
+
+// Balanced partition of row groups: CTA c starts at the first group whose
+// weight prefix (slots + groups) reaches c/G of the total.
+__global__ void partition_kernel(const int* rp, int ngroups, int G, int* gpart) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c > G) return;
+    if (c == 0) {
+        gpart[0] = 0;
+        return;
+    }
+    if (c == G) {
+        gpart[G] = ngroups;
+        return;
+    }
+    const long long total = (long long)rp[ngroups] + ngroups;
+    const long long target = (total * c + G - 1) / G;
+    int lo = 0, hi = ngroups;  // first g with rp[g] + g >= target
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((long long)rp[mid] + mid >= target)
+            hi = mid;
+        else
+            lo = mid + 1;
+    }
+    gpart[c] = lo;
+}
+
+// minv = 1 / stored diagonal (solver.py:413-418, sparse.py:121-128).
+template <int W>
+__global__ void jacobi_kernel(MatView A, double* minv, int* flag) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= A.ngroups) return;
+    double d[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) d[w] = 0.0;
+    for (int s = A.rp[g]; s < A.rp[g + 1]; ++s) {
+        if (A.col[s] == g) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) d[w] = A.val[(long long)s * W + w];
+        }
+    }
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        if (d[w] == 0.0) atomicOr(flag, 1);
+        minv[W * g + w] = 1.0 / d[w];
+    }
+}
+
+template <int W, bool STREAM>
+__global__ void __launch_bounds__(256) spmv_kernel(MatView A, const double* __restrict__ x,
+                                                   double* __restrict__ y) {
+    const int g0 = blockIdx.x * blockDim.x;
+    const int g1 = min(A.ngroups, g0 + (int)blockDim.x);
+    spmv_groups<W, STREAM>(A, g0, g1, SrcPlain{x}, [&](int g, const double* yy) {
+        if (W == 1) {
+            y[g] = yy[0];
+        } else {
+            reinterpret_cast<double2*>(y)[g] = make_double2(yy[0], yy[1]);
+        }
+    });
+}
+
+// delta = max |xn - xo| / max(1, |xo|)  (fem.py:527-528); nonnegative
+// doubles order like their bit patterns, so an integer atomicMax is an
+// exact, order-independent max.
+__global__ void delta_kernel(const double* xn, const double* xo, int n, unsigned long long* out) {
+    __shared__ double red[32];
+    double v = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double o = xo[i];
+        const double d = fabs(sub(xn[i], o)) / fmax(1.0, fabs(o));
+        v = (d > v || d != d) ? d : v;
+    }
+    v = block_max(v, red);
+    if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(v));
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+
+static int kernel_grid(rafem_ctx* ctx, const void* fn, size_t smem, int want) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, KT, smem) != cudaSuccess || occ < 1)
+        return 0;
+    const int gmax = occ * ctx->sm_count;
+    return std::max(1, std::min(want, gmax));
+}
+
+int jacobi_minv(rafem_ctx* ctx, const MatView& A, double* minv_dev, int* flag_dev) {
+    RF_CUDA_TRY(ctx, cudaMemsetAsync(flag_dev, 0, sizeof(int), ctx->stream));
+    const int blocks = (A.ngroups + 255) / 256;
+    if (blocks > 0) {
+        if (A.W == 1)
+            jacobi_kernel<1><<<blocks, 256, 0, ctx->stream>>>(A, minv_dev, flag_dev);
+        else
+            jacobi_kernel<2><<<blocks, 256, 0, ctx->stream>>>(A, minv_dev, flag_dev);
+        ctx->launches++;
+        RF_CUDA_TRY(ctx, cudaGetLastError());
+    }
+    return RAFEM_OK;
+}
+
+int spmv_launch(rafem_ctx* ctx, const MatView& A, const double* x_dev, double* y_dev) {
+    const int blocks = (A.ngroups + 255) / 256;
+    if (blocks == 0) return RAFEM_OK;
+    const bool stream = A.slots * (4 + 8LL * A.W) > (48LL << 20);
+    if (A.W == 1) {
+        if (stream)
+            spmv_kernel<1, true><<<blocks, 256, 0, ctx->stream>>>(A, x_dev, y_dev);
+        else
+            spmv_kernel<1, false><<<blocks, 256, 0, ctx->stream>>>(A, x_dev, y_dev);
+    } else {
+        if (stream)
+            spmv_kernel<2, true><<<blocks, 256, 0, ctx->stream>>>(A, x_dev, y_dev);
+        else
+            spmv_kernel<2, false><<<blocks, 256, 0, ctx->stream>>>(A, x_dev, y_dev);
+    }
+    ctx->launches++;
+    RF_CUDA_TRY(ctx, cudaGetLastError());
+    return RAFEM_OK;
+}
+
+int vec_delta_launch(rafem_ctx* ctx, const double* xn, const double* xo, int n, double* out_dev) {
+    RF_CUDA_TRY(ctx, cudaMemsetAsync(out_dev, 0, sizeof(double), ctx->stream));
+    const int blocks = std::max(1, std::min((n + 255) / 256, ctx->sm_count * 4));
+    delta_kernel<<<blocks, 256, 0, ctx->stream>>>(xn, xo, n, reinterpret_cast<unsigned long long*>(out_dev));
+    ctx->launches++;
+    RF_CUDA_TRY(ctx, cudaGetLastError());
+    return RAFEM_OK;
+}
+
+template <int W, bool PRE, bool STREAM>
+static const void* pick_kernel(int method) {
+    return method == RAFEM_METHOD_PCG ? (const void*)pcg_kernel<W, PRE, STREAM>
+                                      : (const void*)gmres_kernel<W, PRE, STREAM>;
+}
+
+static const void* select_kernel(int method, int W, bool pre, bool stream) {
+    if (W == 1) {
+        if (pre) return stream ? pick_kernel<1, true, true>(method) : pick_kernel<1, true, false>(method);
+        return stream ? pick_kernel<1, false, true>(method) : pick_kernel<1, false, false>(method);
+    }
+    if (pre) return stream ? pick_kernel<2, true, true>(method) : pick_kernel<2, true, false>(method);
+    return stream ? pick_kernel<2, false, true>(method) : pick_kernel<2, false, false>(method);
+}
+
+int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const double* x0_dev,
+                 double* x_dev, const double* minv_dev, const rafem_solver_params& p,
+                 KResult* res_dev, int* flag_dev, cudaEvent_t ev_start, cudaEvent_t ev_stop) {
+    const int n = A.ngroups * A.W;
+    const bool gm = p.method != RAFEM_METHOD_PCG;
+    const int m = gm ? p.restart_m : 1;
+    const bool pre = p.precondition == RAFEM_PRECOND_JACOBI;
+    const bool stream = A.slots * (4 + 8LL * A.W) > (48LL << 20);
+    const void* fn = select_kernel(p.method, A.W, pre, stream);
+
+    // x starts at x0 (or zero); the kernel never touches x before the first
+    // true-residual test, so an exact x0 comes back bitwise (solver.py:448-450)
+    if (x0_dev) {
+        if (x0_dev != x_dev)
+            RF_CUDA_TRY(ctx, cudaMemcpyAsync(x_dev, x0_dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
+        RF_CUDA_TRY(ctx, cudaMemsetAsync(x_dev, 0, sizeof(double) * n, ctx->stream));
+    }
+
+    // persistent grid size: enough CTAs to cover the rows, at most one wave
+    const long long hess_doubles = gm ? (long long)(m + 1) * m + 4LL * m + 4 : 0;
+    size_t smem = 0;
+    bool hess_global = false;
+    if (gm) {
+        if (hess_doubles * 8 <= 160 * 1024) {
+            smem = (size_t)hess_doubles * 8;
+        } else {
+            hess_global = true;
+        }
+    }
+    if (smem > 48 * 1024)
+        RF_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int want = p.grid_ctas > 0 ? p.grid_ctas : (int)std::max<long long>(1, (n + 511) / 512);
+    want = std::min(want, std::max(1, A.ngroups));
+    const int G = kernel_grid(ctx, fn, smem, want);
+    if (G < 1) return rafem_fail(ctx, RAFEM_ERR_CUDA, "cannot size the cooperative solver grid");
+
+    // workspace
+    const long long ldv = ((long long)n + 31) / 32 * 32;
+    if (gm) {
+        if (int rc = ensure(ctx, ctx->ws_basis, sizeof(double) * (size_t)(m + 1) * ldv)) return rc;
+    }
+    if (int rc = ensure(ctx, ctx->ws_vec, sizeof(double) * (size_t)7 * ldv)) return rc;
+    if (int rc = ensure(ctx, ctx->ws_partial, sizeof(double) * (size_t)2 * (std::max(m, 6) + 2) * G)) return rc;
+    if (hess_global) {
+        if (int rc = ensure(ctx, ctx->ws_hess, sizeof(double) * (size_t)hess_doubles * G)) return rc;
+    }
+    const long long hist_cap = std::min<long long>(p.max_total_iters > 0 ? p.max_total_iters : 10LL * n, 1LL << 20) + 1;
+    const long long cyc_cap = hist_cap;
+    if (int rc = ensure(ctx, ctx->ws_hist, sizeof(double) * (size_t)hist_cap)) return rc;
+    if (int rc = ensure(ctx, ctx->ws_cyc, sizeof(long long) * (size_t)cyc_cap)) return rc;
+    if (int rc = ensure(ctx, ctx->ws_part, sizeof(int) * (size_t)(G + 1))) return rc;
+
+    int* gpart = static_cast<int*>(ctx->ws_part.p);
+    partition_kernel<<<(G + 1 + 127) / 128, 128, 0, ctx->stream>>>(A.rp, A.ngroups, G, gpart);
+    ctx->launches++;
+    RF_CUDA_TRY(ctx, cudaGetLastError());
+
+    double* vec = static_cast<double*>(ctx->ws_vec.p);
+    KArgs a{};
+    a.A = A;
+    a.gpart = gpart;
+    a.ldv = ldv;
+    a.b = b_dev;
+    a.x = x_dev;
+    a.minv = pre ? minv_dev : nullptr;
+    a.V = gm ? static_cast<double*>(ctx->ws_basis.p) : nullptr;
+    a.w0 = vec;
+    a.w1 = vec + ldv;
+    a.r = vec + 2 * ldv;
+    a.z = vec + 3 * ldv;
+    a.p0 = vec + 4 * ldv;
+    a.p1 = vec + 5 * ldv;
+    a.q = vec + 6 * ldv;
+    a.partial = static_cast<double*>(ctx->ws_partial.p);
+    a.hess = hess_global ? static_cast<double*>(ctx->ws_hess.p) : nullptr;
+    a.hess_stride = hess_doubles;
+    a.m = m;
+    a.tol = p.tolerance;
+    a.cap = p.max_total_iters > 0 ? p.max_total_iters : 10LL * n;
+    a.hist = static_cast<double*>(ctx->ws_hist.p);
+    a.hist_cap = hist_cap;
+    a.cyc = static_cast<long long*>(ctx->ws_cyc.p);
+    a.cyc_cap = cyc_cap;
+    a.res = res_dev;
+    a.flag = flag_dev;
+    void* args[] = {&a};
+    if (ev_start) RF_CUDA_TRY(ctx, cudaEventRecord(ev_start, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fn, dim3(G), dim3(KT), args, smem, ctx->stream));
+    if (ev_stop) RF_CUDA_TRY(ctx, cudaEventRecord(ev_stop, ctx->stream));
+    ctx->launches++;
+    return RAFEM_OK;
+}
+
+int krylov_read_history(rafem_ctx* ctx, const KResult& r, double* hist, long long hist_cap,
+                        long long* cyc, long long cyc_cap) {
+    if (hist && hist_cap > 0 && r.hist_len > 0) {
+        const long long nh = std::min<long long>(std::min<long long>(r.hist_len, hist_cap),
+                                                 (long long)(ctx->ws_hist.bytes / sizeof(double)));
+        RF_CUDA_TRY(ctx, cudaMemcpyAsync(hist, ctx->ws_hist.p, sizeof(double) * nh, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    if (cyc && cyc_cap > 0 && r.cycles > 0) {
+        const long long nc = std::min<long long>(std::min<long long>(r.cycles, cyc_cap),
+                                                 (long long)(ctx->ws_cyc.bytes / sizeof(long long)));
+        RF_CUDA_TRY(ctx, cudaMemcpyAsync(cyc, ctx->ws_cyc.p, sizeof(long long) * nc, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return RAFEM_OK;
+}
+
+}  // namespace rafem

@@ -1,0 +1,253 @@
+"""GPU parity: device assembly and full simulations vs oracle/golden.
+
+Bars: pattern bitwise; values within the reference's own
+assembly tolerances (single tet <= 1e-14, boxes rtol 1e-12 —
+test_fem.py:134-198); scale equal; per-solve residual <= 1e-10; full runs
+with an identical trajectory, final-step field error <= 1e-6 vs the
+reference at 1e-10, every step <= 1e-6 vs the reference at 1e-12 when run
+at 1e-12, and PSNR above the 1e-5 noise control (metrics.py:47-76).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import rafem_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def single_tet():
+    from paper_2409_13036_b200 import TetMesh
+    return TetMesh(np.array([[0.0, 0, 0], [1.0, 0, 0], [0.0, 1, 0], [0.0, 0, 1]]),
+                   np.array([[0, 1, 2, 3]]), np.zeros(1, dtype=np.int64),
+                   {"outer_boundary": np.array([2]), "electrode_pos": np.array([0]),
+                    "electrode_neg": np.array([1])})
+
+
+def mesh_for(name, d):
+    from paper_2409_13036_b200 import generate_box_mesh
+    return single_tet() if name == "tet" else generate_box_mesh(*map(int, d[f"{name}_dims"]))
+
+
+@pytest.mark.parametrize("name", ["tet", "b333", "b435", "b666", "A"])
+def test_assembly_vs_golden(name):
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, assemble_global
+    d = golden("assembly")
+    mesh = mesh_for(name, d)
+    t, v, tp = d[f"{name}_t"], d[f"{name}_v"], d[f"{name}_tp"]
+    for tag, kw in (("full", {}), ("raw", dict(apply_constraints=False)),
+                    ("noeq", dict(equilibrate=False))):
+        s = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, v, tp, 0.5, **kw)
+        assert np.array_equal(s.matrix.row_ptr, d[f"{name}_{tag}_row_ptr"])
+        assert np.array_equal(s.matrix.col_idx, d[f"{name}_{tag}_col_idx"])
+        assert s.voltage_row_scale == float(d[f"{name}_{tag}_scale"])
+        ref_v, ref_b = d[f"{name}_{tag}_vals"], d[f"{name}_{tag}_rhs"]
+        if name == "tet":
+            assert np.max(np.abs(s.matrix.vals - ref_v)) <= 1e-14
+            assert np.max(np.abs(s.rhs - ref_b)) <= 1e-14
+        else:
+            assert np.allclose(s.matrix.vals, ref_v, rtol=1e-12, atol=1e-15)
+            assert np.allclose(s.rhs, ref_b, rtol=1e-12, atol=1e-11)
+        # explicit zeros and unit diagonals of the elimination are exact
+        assert np.array_equal(s.matrix.vals == 0.0, ref_v == 0.0)
+        assert np.array_equal(s.matrix.vals == 1.0, ref_v == 1.0)
+    cold = assemble_global(mesh, MaterialParams.default(), SimConfig(), np.full(mesh.node_count, 37.0),
+                           np.zeros(mesh.node_count), np.full(mesh.node_count, 37.0), 0.5)
+    assert np.allclose(cold.matrix.vals, d[f"{name}_cold_vals"], rtol=1e-12, atol=1e-15)
+    assert np.allclose(cold.rhs, d[f"{name}_cold_rhs"], rtol=1e-12, atol=1e-11)
+
+
+def test_two_regions_vs_golden():
+    from paper_2409_13036_b200 import (MaterialParams, RegionMaterial, SimConfig, assemble_global,
+                                       generate_box_mesh)
+    d = golden("assembly")
+    mesh = generate_box_mesh(4, 3, 5)
+    mesh.regions = d["reg2_regions"].copy()
+    mat = MaterialParams({0: RegionMaterial(), 1: RegionMaterial(k=0.9e-3, rho_c=2.5e-3,
+                                                                  sigma0=0.35e-3, alpha=0.01)})
+    s = assemble_global(mesh, mat, SimConfig(), d["reg2_t"], d["reg2_v"], d["reg2_t"], 0.25)
+    assert np.allclose(s.matrix.vals, d["reg2_vals"], rtol=1e-12, atol=1e-15)
+    assert np.allclose(s.rhs, d["reg2_rhs"], rtol=1e-12, atol=1e-11)
+
+
+def test_assembly_deterministic_pattern_invariant_and_errors():
+    from paper_2409_13036_b200 import (MaterialParams, PhysicsRangeError, SimConfig, assemble_global,
+                                       generate_box_mesh)
+    mesh = generate_box_mesh(6, 5, 7)
+    n = mesh.node_count
+    rng = np.random.default_rng(11)
+    t, v, tp = rng.uniform(37, 60, n), rng.uniform(0, 25, n), rng.uniform(37, 60, n)
+    a = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, v, tp, 0.5, threads=1)
+    b = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, v, tp, 0.5, threads=7)
+    assert np.array_equal(a.matrix.vals, b.matrix.vals) and np.array_equal(a.rhs, b.rhs)
+    c = assemble_global(mesh, MaterialParams.default(), SimConfig(), np.full(n, 37.0), np.zeros(n),
+                        np.full(n, 37.0), 0.125)
+    assert np.array_equal(a.matrix.row_ptr, c.matrix.row_ptr)
+    assert np.array_equal(a.matrix.col_idx, c.matrix.col_idx)
+    # equilibration: power of two that balances the diagonal blocks
+    raw = assemble_global(mesh, MaterialParams.default(), SimConfig(), np.full(n, 37.0), np.zeros(n),
+                          np.full(n, 37.0), 0.5, apply_constraints=False)
+    sc = raw.voltage_row_scale
+    assert math.log2(sc) == round(math.log2(sc))
+    dg = raw.matrix.diagonal()
+    assert 0.5 <= dg[1::2].sum() / dg[0::2].sum() <= 2.0
+    with pytest.raises(PhysicsRangeError, match="element"):
+        assemble_global(mesh, MaterialParams.default(), SimConfig(), np.full(n, -20.0), np.zeros(n),
+                        np.full(n, 37.0), 0.5)
+    with pytest.raises(ValueError):
+        assemble_global(mesh, MaterialParams.default(), SimConfig(), t, v, tp, 0.0)
+    mesh2 = generate_box_mesh(2, 2, 2)
+    mesh2.regions[:] = 5
+    with pytest.raises(KeyError, match="region tag 5"):
+        assemble_global(mesh2, MaterialParams.default(), SimConfig(), np.full(8, 37.0), np.zeros(8),
+                        np.full(8, 37.0), 0.5)
+
+
+def test_device_matrix_solves_like_host_copy():
+    from paper_2409_13036_b200 import (CsrMatrix, MaterialParams, SimConfig, SolverConfig, assemble_global,
+                                       generate_box_mesh, solve, spmv)
+    mesh = generate_box_mesh(9, 8, 10)
+    n = mesh.node_count
+    rng = np.random.default_rng(2409)
+    s = assemble_global(mesh, MaterialParams.default(), SimConfig(), 37 + rng.uniform(0, 30, n),
+                        rng.uniform(0, 25, n), np.full(n, 37.0), 0.5)
+    host = CsrMatrix(s.matrix.nrows, s.matrix.ncols, s.matrix.row_ptr, s.matrix.col_idx, s.matrix.vals)
+    x = rng.standard_normal(2 * n)
+    assert np.array_equal(spmv(s.matrix, x), spmv(host, x))
+    for backend in ("gmres", "pcg"):
+        cfg = SolverConfig(backend=backend, precondition="jacobi")
+        xd, sd = solve(s.matrix, s.rhs, config=cfg)
+        xh, sh = solve(host, s.rhs, config=cfg)
+        res = np.linalg.norm(s.rhs - O.matvec(host.row_ptr, host.col_idx, host.vals, xd)) / np.linalg.norm(s.rhs)
+        assert sd.converged and res <= 1e-10
+        assert np.max(np.abs(xd - xh)) <= 1e-8 * np.max(np.abs(xh))
+
+
+# ---------------------------------------------------------------- full runs
+
+def _rel_inf(x, ref):
+    return float(np.max(np.abs(x - ref)) / np.max(np.abs(ref)))
+
+
+def _compare_run(records, d, field_tol, every_step):
+    assert len(records) == len(d["time"])
+    assert np.array_equal([r.time for r in records], d["time"])
+    assert np.array_equal([r.dt for r in records], d["dt"])
+    assert np.array_equal([r.corrector_iters for r in records], d["corrector_iters"])
+    worst = 0.0
+    kept = list(d["kept"])
+    idx = range(len(kept)) if every_step else [len(kept) - 1]
+    for i in idx:
+        rec = records[kept[i]]
+        worst = max(worst, _rel_inf(rec.T, d["T"][i]), _rel_inf(rec.V, d["V"][i]))
+    assert worst <= field_tol, worst
+    peak_t = float(np.max(np.abs(d["T"])))
+    peak_v = float(np.max(np.abs(d["V"])))
+    for i in idx:
+        rec = records[kept[i]]
+        assert O.psnr(d["T"][i], rec.T, peak_t) > 20 * (math.log10(peak_t) - math.log10(1e-5))
+        assert O.psnr(d["V"][i], rec.V, peak_v) > 20 * (math.log10(peak_v) - math.log10(1e-5))
+    return worst
+
+
+@pytest.mark.parametrize("backend", ["gmres", "pcg"])
+def test_host_loop_A40_vs_reference(backend):
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh, run_simulation
+    recs = []
+    cfg = SimConfig(total_time=40.0, solver=SolverConfig(backend=backend, precondition="jacobi"))
+    run_simulation(generate_box_mesh(15, 15, 16), MaterialParams.default(), cfg, sink=recs.append)
+    _compare_run(recs, golden("run_A40_1e-10"), 1e-6, every_step=False)
+
+
+@pytest.mark.parametrize("backend", ["gmres", "pcg"])
+def test_native_loop_A40_tight_every_step(backend):
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh, simulate_device
+    cfg = SimConfig(total_time=40.0, solver=SolverConfig(backend=backend, precondition="jacobi",
+                                                         tolerance=1e-12))
+    recs, _ = simulate_device(generate_box_mesh(15, 15, 16), MaterialParams.default(), cfg)
+    _compare_run(recs, golden("run_A40_1e-12"), 1e-6, every_step=True)
+
+
+@pytest.mark.parametrize("backend", ["gmres", "pcg"])
+def test_native_loop_B900_vs_reference(backend):
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh, simulate_device
+    mesh = generate_box_mesh(20, 20, 21)
+    cfg = SimConfig(total_time=900.0, solver=SolverConfig(backend=backend, precondition="jacobi"))
+    recs, summ = simulate_device(mesh, MaterialParams.default(), cfg)
+    d = golden("run_B900_1e-10")
+    _compare_run(recs, d, 1e-6, every_step=False)
+    assert summ.accepted_steps == 96 and summ.passes == int(d["summary"][1])
+    cfg12 = SimConfig(total_time=900.0, solver=SolverConfig(backend=backend, precondition="jacobi",
+                                                            tolerance=1e-12))
+    recs12, _ = simulate_device(mesh, MaterialParams.default(), cfg12)
+    _compare_run(recs12, golden("run_B900_1e-12"), 1e-6, every_step=True)
+
+
+def test_native_and_host_loops_agree_and_are_deterministic():
+    from paper_2409_13036_b200 import (MaterialParams, SimConfig, SolverConfig, generate_box_mesh,
+                                       run_simulation, simulate_device)
+    mesh = generate_box_mesh(6, 6, 6)
+    cfg = SimConfig(total_time=30.0, solver=SolverConfig(backend="gmres", precondition="jacobi"))
+    r1, _ = simulate_device(mesh, MaterialParams.default(), cfg)
+    r2, _ = simulate_device(mesh, MaterialParams.default(), cfg)
+    hl = []
+    run_simulation(mesh, MaterialParams.default(), cfg, sink=hl.append)
+    assert len(r1) == len(r2) == len(hl)
+    for a, b, c in zip(r1, r2, hl):
+        assert np.array_equal(a.T, b.T) and np.array_equal(a.V, b.V)
+        assert (a.time, a.dt, a.corrector_iters) == (c.time, c.dt, c.corrector_iters)
+        assert np.array_equal(a.T, c.T) and np.array_equal(a.V, c.V)
+
+
+def test_zero_drive_is_exact_and_max_principle():
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh, simulate_device
+    mesh = generate_box_mesh(5, 5, 5)
+    for backend in ("gmres", "pcg"):
+        idle = SimConfig(total_time=10.0, applied_voltage=0.0,
+                         solver=SolverConfig(backend=backend, precondition="jacobi"))
+        recs, _ = simulate_device(mesh, MaterialParams.default(), idle)
+        for r in recs:
+            assert np.max(np.abs(r.T - 37.0)) <= 1e-10 and np.max(np.abs(r.V)) <= 1e-12
+        live = SimConfig(total_time=10.0, solver=SolverConfig(backend=backend, precondition="jacobi"))
+        recs, _ = simulate_device(mesh, MaterialParams.default(), live)
+        assert min(r.V.min() for r in recs) >= -1e-9 and max(r.V.max() for r in recs) <= 25 + 1e-9
+
+
+def test_time_loop_failure_semantics():
+    from paper_2409_13036_b200 import (MaterialParams, RegionMaterial, SimConfig, SolverConfig,
+                                       StepFailureError, corrector_step, generate_box_mesh, initial_state,
+                                       run_simulation, simulate_device)
+    mesh = generate_box_mesh(3, 3, 3)
+    g = SolverConfig(backend="gmres")
+    recs = []
+    seen = []
+
+    def hook(step, attempt):
+        seen.append((step, attempt))
+        return step == 1 and attempt == 0
+
+    summ = run_simulation(mesh, MaterialParams.default(), SimConfig(total_time=3.0, solver=g),
+                          sink=recs.append, fault_hook=hook)
+    assert summ.dt_halvings == 1 and recs[1].dt == 0.75 * 0.5 and recs[-1].time == 3.0
+    attempts = []
+    with pytest.raises(StepFailureError):
+        run_simulation(mesh, MaterialParams.default(),
+                       SimConfig(dt_init=4e-6, dt_min=1e-6, total_time=1.0, solver=g),
+                       fault_hook=lambda s, a: attempts.append((s, a)) or True)
+    assert attempts == [(0, 0), (0, 1), (0, 2)]
+    out = corrector_step(mesh, MaterialParams.default(), SimConfig(max_corrector_iters=1, solver=g),
+                         initial_state(mesh, SimConfig()), 0.5)
+    assert not out.converged and out.iterations == 1 and out.cause == "corrector iteration cap reached"
+    hot = MaterialParams({0: RegionMaterial(alpha=0.4)})
+    cfg = SimConfig(total_time=10.0, dt_init=10.0, dt_max=10.0, applied_voltage=500.0, solver=g)
+    out = corrector_step(mesh, hot, cfg, initial_state(mesh, cfg), 10.0)
+    assert not out.converged and out.iterations == 50
+    # the native loop reproduces the small-mesh golden run exactly in trajectory
+    d = golden("run_b333_6s")
+    recs, _ = simulate_device(mesh, MaterialParams.default(),
+                              SimConfig(total_time=6.0, solver=SolverConfig(backend="gmres",
+                                                                            precondition="jacobi")))
+    assert [r.dt for r in recs] == list(d["dt"]) and [r.time for r in recs] == list(d["time"])
