@@ -98,6 +98,7 @@ MatView system_view(rafem_system* s) {
     A.ngroups = s->mesh->N;
     A.W = 2;
     A.slots = s->mesh->slots;
+    A.pattern_id = s->mesh->id;
     return A;
 }
 
@@ -197,6 +198,7 @@ void rafem_ctx_destroy(rafem_ctx* ctx) {
                       &ctx->ws_cyc, &ctx->ws_part, &ctx->ws_res})
         if (b->p) cudaFree(b->p);
     if (ctx->pin) cudaFreeHost(ctx->pin);
+    for (auto& e : ctx->part_cache) cudaFree(e.gpart);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->ev2) cudaEventDestroy(ctx->ev2);
@@ -358,7 +360,9 @@ int rafem_mesh_create(rafem_ctx* ctx, int64_t n_nodes, const double* nodes, int6
         tab[4 * n_regions + r] = t_ref[r];
     }
     rafem_mesh* m = new rafem_mesh();
+    static unsigned long long next_id = 1;
     m->ctx = ctx;
+    m->id = next_id++;
     m->N = (int)n_nodes;
     m->M = (int)n_tets;
     m->nreg = n_regions;

@@ -43,6 +43,15 @@ struct MatView {
     int ngroups;
     int W;
     long long slots;
+    unsigned long long pattern_id = 0;  // nonzero: partitions may be cached
+};
+
+struct PartCacheEntry {
+    unsigned long long pattern_id;
+    const int* rp;
+    int G;
+    int* gpart;
+    size_t max_slice;
 };
 
 // Growable device scratch owned by a context.
@@ -67,7 +76,9 @@ struct rafem_ctx {
     // host pinned staging
     void* pin = nullptr;
     size_t pin_bytes = 0;
-    int coop_occ_gmres[2][2] = {{0, 0}, {0, 0}};
+    std::vector<rafem::PartCacheEntry> part_cache;
+    int last_mode = -1;  // 1: cluster-resident solve, 0: grid-wide cooperative solve
+    int last_ctas = 0;
 };
 
 struct rafem_matrix {
@@ -86,6 +97,7 @@ struct rafem_mesh {
     long long slots = 0;
     int maxdeg = 0;     // max slots per node row
     int maxinc = 0;     // max incident tets per node
+    unsigned long long id = 0;  // unique per mesh (partition cache key)
     // inputs
     double* nodes = nullptr;  // N x 3
     int* tets = nullptr;      // M x 4

@@ -4,11 +4,21 @@
 // right Jacobi, true-residual restarts, stagnation latch, breakdown rules)
 // and sparse.py:205-219 (SpMV, per-row left-to-right sums).
 //
-// One cooperative launch runs a whole solve: every CTA owns a contiguous
-// block of row groups (balanced by slots + rows), keeps its share of every
-// vector, and meets the others only at grid barriers around the scalar
-// reductions.  Reductions are deterministic: per-thread partial sums in a
-// fixed order, a fixed xor-butterfly per warp, per-CTA partials in global
+// One launch runs a whole solve.  Every CTA owns a contiguous block of row
+// groups (balanced by slots + rows), keeps its share of every vector, and
+// meets the others only at barriers around the scalar reductions.  Two
+// execution modes share the same solver bodies:
+//
+//   * cluster mode (paper-scale systems): ONE thread-block cluster of up to
+//     16 CTAs.  Each CTA copies its matrix slice into shared memory once and
+//     the barriers are hardware cluster barriers (~0.2 us), so a Krylov
+//     iteration costs a few microseconds with no HBM matrix traffic.
+//   * grid mode (large systems): a cooperative launch of one CTA per SM
+//     with grid-wide barriers; matrix slots stream from HBM with
+//     evict-first loads while the gathered vectors stay in L2.
+//
+// Reductions are deterministic in both modes: per-thread partial sums in
+// a fixed order, a fixed xor-butterfly per warp, per-CTA partials in global
 // memory, and every CTA re-reduces the G partials in the same fixed order,
 // so all CTAs take identical control decisions and results are bitwise
 // reproducible run to run.
@@ -17,10 +27,14 @@
 
 #include <algorithm>
 #include <cmath>
+#include <vector>
 
 namespace rafem {
 
-constexpr int KT = 512;  // threads per CTA of the persistent kernels
+constexpr int KT = 512;        // threads per CTA of the persistent kernels
+constexpr int KTC = 640;      // cluster-mode PCG: one thread per row group at paper scale
+constexpr int kMaxCluster = 16;
+constexpr size_t kSmemBudget = 220 * 1024;
 
 struct KArgs {
     MatView A;
@@ -40,6 +54,7 @@ struct KArgs {
     double* partial;  // 2 x (m + 2) x G
     double* hess;     // per-CTA Hessenberg scratch when it does not fit in smem
     long long hess_stride;
+    long long hess_smem;  // doubles of Hessenberg scratch at the head of dynamic smem
     int m;
     double tol;
     long long cap;
@@ -52,42 +67,89 @@ struct KArgs {
 };
 
 // ---------------------------------------------------------------------------
+// execution modes
+
+struct GridMode {
+    static constexpr bool kCluster = false;
+    RF_DEV static void sync() { cg::this_grid().sync(); }
+};
+struct ClusterMode {
+    static constexpr bool kCluster = true;
+    RF_DEV static void sync() { cg::this_cluster().sync(); }
+};
+
+// Row access: global (read-only / streaming loads) or this CTA's slice in
+// shared memory (rp rebased to the CTA's first group).
+template <int W, bool SMEM, bool STREAM>
+struct Rows {
+    const int* rp;
+    const int* col;
+    const double* val;
+    int gbase;
+    RF_DEV int start(int g) const { return SMEM ? rp[g - gbase] : __ldg(rp + g); }
+    RF_DEV int column(int s) const { return SMEM ? col[s] : (STREAM ? __ldcs(col + s) : __ldg(col + s)); }
+    RF_DEV double value1(int s) const { return SMEM ? val[s] : (STREAM ? __ldcs(val + s) : __ldg(val + s)); }
+    RF_DEV double2 value2(int s) const {
+        const double2* p = reinterpret_cast<const double2*>(val) + s;
+        return SMEM ? *p : (STREAM ? __ldcs(p) : __ldg(p));
+    }
+};
+
+// ---------------------------------------------------------------------------
 // SpMV over this CTA's row groups.  Each group's rows are summed left to
 // right over the stored slots with separately rounded products: exactly
 // the reference's bincount order (sparse.py:217-218), so y is bit-identical.
+// Slots are processed in chunks of 8 whose column/value loads and operand
+// gathers are all issued before the (sequential) accumulation, so a row
+// costs one gather latency per chunk instead of one per slot.
 
-template <bool STREAM>
-RF_DEV int ldcol(const int* p) {
-    return STREAM ? __ldcs(p) : __ldg(p);
-}
-template <bool STREAM>
-RF_DEV double ldval(const double* p) {
-    return STREAM ? __ldcs(p) : __ldg(p);
-}
-template <bool STREAM>
-RF_DEV double2 ldval2(const double2* p) {
-    return STREAM ? __ldcs(p) : __ldg(p);
-}
+constexpr int kChunk = 8;   // scalar rows
+constexpr int kChunk2 = 4;  // paired rows (two double2 per slot in flight)
 
-template <int W, bool STREAM, class Src, class Epi>
-RF_DEV void spmv_groups(const MatView& A, int g0, int g1, const Src& src, Epi&& epi) {
+template <int W, class R, class Src, class Epi>
+RF_DEV void spmv_groups(const R& rows, int g0, int g1, const Src& src, Epi&& epi) {
     for (int g = g0 + threadIdx.x; g < g1; g += blockDim.x) {
-        const int s0 = __ldg(A.rp + g), s1 = __ldg(A.rp + g + 1);
+        const int s0 = rows.start(g), s1 = rows.start(g + 1);
         if constexpr (W == 1) {
             double acc = 0.0;
-            for (int s = s0; s < s1; ++s)
-                acc = add(acc, mul(ldval<STREAM>(A.val + s), src.at(ldcol<STREAM>(A.col + s))));
+            for (int s = s0; s < s1; s += kChunk) {
+                int c[kChunk];
+                double a[kChunk], xv[kChunk];
+#pragma unroll
+                for (int j = 0; j < kChunk; ++j)
+                    if (s + j < s1) {
+                        c[j] = rows.column(s + j);
+                        a[j] = rows.value1(s + j);
+                    }
+#pragma unroll
+                for (int j = 0; j < kChunk; ++j)
+                    if (s + j < s1) xv[j] = src.at(c[j]);
+#pragma unroll
+                for (int j = 0; j < kChunk; ++j)
+                    if (s + j < s1) acc = add(acc, mul(a[j], xv[j]));
+            }
             double y[1] = {acc};
             epi(g, y);
         } else {
-            const double2* v2 = reinterpret_cast<const double2*>(A.val);
             double av = 0.0, at = 0.0;
-            for (int s = s0; s < s1; ++s) {
-                const int c = ldcol<STREAM>(A.col + s);
-                const double2 a2 = ldval2<STREAM>(v2 + s);
-                const double2 xx = src.at2(c);
-                av = add(av, mul(a2.x, xx.x));
-                at = add(at, mul(a2.y, xx.y));
+            for (int s = s0; s < s1; s += kChunk2) {
+                int c[kChunk2];
+                double2 a[kChunk2], xv[kChunk2];
+#pragma unroll
+                for (int j = 0; j < kChunk2; ++j)
+                    if (s + j < s1) {
+                        c[j] = rows.column(s + j);
+                        a[j] = rows.value2(s + j);
+                    }
+#pragma unroll
+                for (int j = 0; j < kChunk2; ++j)
+                    if (s + j < s1) xv[j] = src.at2(c[j]);
+#pragma unroll
+                for (int j = 0; j < kChunk2; ++j)
+                    if (s + j < s1) {
+                        av = add(av, mul(a[j].x, xv[j].x));
+                        at = add(at, mul(a[j].y, xv[j].y));
+                    }
             }
             double y[2] = {av, at};
             epi(g, y);
@@ -96,12 +158,11 @@ RF_DEV void spmv_groups(const MatView& A, int g0, int g1, const Src& src, Epi&& 
 }
 
 // Operand sources: the SpMV input is formed on the fly from vectors that
-// are final after the previous grid barrier, which saves a barrier per
-// Krylov step.
+// are final after the previous barrier, which saves a barrier per step.
 struct SrcPlain {
     const double* x;
-    RF_DEV double at(int j) const { return __ldcg(x + j); }
-    RF_DEV double2 at2(int c) const { return __ldcg(reinterpret_cast<const double2*>(x) + c); }
+    RF_DEV double at(int j) const { return __ldca(x + j); }
+    RF_DEV double2 at2(int c) const { return __ldca(reinterpret_cast<const double2*>(x) + c); }
 };
 
 // GMRES: z_j = minv_j * (s_j * c), where v_k = s * c is the next basis
@@ -112,11 +173,11 @@ struct SrcBasis {
     double c;
     const double* minv;
     RF_DEV double at(int j) const {
-        double v = mul(__ldcg(s + j), c);
+        double v = mul(__ldca(s + j), c);
         return PRE ? mul(v, __ldg(minv + j)) : v;
     }
     RF_DEV double2 at2(int cc) const {
-        double2 sv = __ldcg(reinterpret_cast<const double2*>(s) + cc);
+        double2 sv = __ldca(reinterpret_cast<const double2*>(s) + cc);
         double2 v = make_double2(mul(sv.x, c), mul(sv.y, c));
         if (PRE) {
             double2 mv = __ldg(reinterpret_cast<const double2*>(minv) + cc);
@@ -134,13 +195,13 @@ struct SrcCg {
     double beta;
     int first;
     RF_DEV double at(int j) const {
-        double zj = __ldcg(z + j);
-        return first ? zj : add(zj, mul(beta, __ldcg(po + j)));
+        double zj = __ldca(z + j);
+        return first ? zj : add(zj, mul(beta, __ldca(po + j)));
     }
     RF_DEV double2 at2(int c) const {
-        double2 zz = __ldcg(reinterpret_cast<const double2*>(z) + c);
+        double2 zz = __ldca(reinterpret_cast<const double2*>(z) + c);
         if (first) return zz;
-        double2 pp = __ldcg(reinterpret_cast<const double2*>(po) + c);
+        double2 pp = __ldca(reinterpret_cast<const double2*>(po) + c);
         return make_double2(add(zz.x, mul(beta, pp.x)), add(zz.y, mul(beta, pp.y)));
     }
 };
@@ -148,7 +209,6 @@ struct SrcCg {
 // ---------------------------------------------------------------------------
 // reduction plumbing
 
-// Publish nv (<= 8) block-reduced values as this CTA's partials.
 template <int NV>
 RF_DEV void publish(double (&v)[NV], int nv, double* P, int base, int G, double* red) {
     block_sum<NV>(v, red);
@@ -159,7 +219,7 @@ RF_DEV void publish(double (&v)[NV], int nv, double* P, int base, int G, double*
     }
 }
 
-// After a grid barrier: reduce nv coefficient rows of P into co[] (all CTAs).
+// After a barrier: reduce nv coefficient rows of P into co[] (all CTAs).
 RF_DEV void gather(const double* P, int nv, int G, double* co) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int i = wid; i < nv; i += nw) {
@@ -181,22 +241,77 @@ RF_DEV void multidot(const double* V, long long ldv, int nv, const double* w, in
             const double we = w[e];
 #pragma unroll
             for (int j = 0; j < 8; ++j)
-                if (j < cnt) acc[j] = add(acc[j], mul(__ldcg(V + (long long)(i0 + j) * ldv + e), we));
+                if (j < cnt) acc[j] = add(acc[j], mul(__ldca(V + (long long)(i0 + j) * ldv + e), we));
         }
         publish<8>(acc, cnt, P, i0, G, red);
     }
 }
 
+// Cluster mode: copy this CTA's slice of the matrix into shared memory
+// (16-byte vector loads; the slice is constant for the whole solve).
+template <int W>
+RF_DEV void stage_slice(const MatView& A, int g0, int g1, double* sval, int* scol, int* srp) {
+    const int s0 = __ldg(A.rp + g0), s1 = __ldg(A.rp + g1);
+    const int ns = s1 - s0;
+    for (int g = g0 + threadIdx.x; g <= g1; g += blockDim.x) srp[g - g0] = __ldg(A.rp + g) - s0;
+    if (W == 2) {
+        const double2* src = reinterpret_cast<const double2*>(A.val) + s0;
+        double2* dst = reinterpret_cast<double2*>(sval);
+        for (int s = threadIdx.x; s < ns; s += blockDim.x) dst[s] = __ldg(src + s);
+    } else {
+        for (int s = threadIdx.x; s < ns; s += blockDim.x) sval[s] = __ldg(A.val + s0 + s);
+    }
+    for (int s = threadIdx.x; s < ns; s += blockDim.x) scol[s] = __ldg(A.col + s0 + s);
+    __syncthreads();
+}
+
+RF_DEV void write_result(KResult* res, long long total, long long cycles, long long hlen, double rel,
+                         bool converged, bool stagnated, int status) {
+    res->iterations = total;
+    res->restarts = cycles > 0 ? cycles - 1 : 0;
+    res->cycles = cycles;
+    res->hist_len = hlen;
+    res->final_rel = rel;
+    res->converged = converged ? 1 : 0;
+    res->stagnated = stagnated ? 1 : 0;
+    res->status = status;
+}
+
+// Shared prologue: invalid flag check and ||b|| (solver.py:413-425).
+// Returns bnorm, or a negative value when the kernel must stop.
+template <class Mode>
+RF_DEV double prologue(const KArgs& a, int lo, int hi, double* co, double* red, int& par, long long pstride) {
+    if (*a.flag) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) write_result(a.res, 0, 0, 0, INFINITY, false, false, RAFEM_ERR_INVALID);
+        return -1.0;
+    }
+    const int G = gridDim.x;
+    double v[1] = {0.0};
+    for (int e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+        const double be = a.b[e];
+        v[0] = add(v[0], mul(be, be));
+    }
+    publish<1>(v, 1, a.partial + par * pstride, 0, G, red);
+    Mode::sync();
+    gather(a.partial + par * pstride, 1, G, co);
+    par ^= 1;
+    const double bnorm = sqrt(co[0]);
+    if (bnorm == 0.0) {  // zero data: zero solution (solver.py:422-425)
+        for (int e = lo + threadIdx.x; e < hi; e += blockDim.x) a.x[e] = 0.0;
+        if (blockIdx.x == 0 && threadIdx.x == 0) write_result(a.res, 0, 0, 0, 0.0, true, false, RAFEM_OK);
+        return -1.0;
+    }
+    return bnorm;
+}
+
 // ---------------------------------------------------------------------------
 // GMRES(m) — solver.py:381-531, with classical Gram-Schmidt applied twice
 // (CGS2) in place of the reference's modified Gram-Schmidt: the same
-// Arnoldi basis to working precision, but 3 grid barriers per step instead
-// of k + 2 dependent reductions.
+// Arnoldi basis to working precision, but 3 barriers per step instead of
+// k + 2 dependent reductions.
 
-template <int W, bool PRE, bool STREAM>
-__global__ void __launch_bounds__(KT, 1) gmres_kernel(KArgs a) {
-    cg::grid_group grid = cg::this_grid();
-    extern __shared__ __align__(16) double dyn[];
+template <int W, bool PRE, class Mode, class R>
+RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
     __shared__ double red[32 * 8];
     __shared__ double sc[4];
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
@@ -213,48 +328,13 @@ __global__ void __launch_bounds__(KT, 1) gmres_kernel(KArgs a) {
     const long long pstride = (long long)(m + 2) * G;
     int par = 0;
 
-    if (*a.flag) {
-        if (cta == 0 && tid == 0) {
-            a.res->status = RAFEM_ERR_INVALID;
-            a.res->converged = 0;
-            a.res->iterations = 0;
-        }
-        return;
-    }
+    const double bnorm = prologue<Mode>(a, lo, hi, co, red, par, pstride);
+    if (bnorm < 0.0) return;
 
-    // ||b||  (solver.py:421)
-    {
-        double v[1] = {0.0};
-        for (int e = lo + tid; e < hi; e += bd) {
-            const double be = a.b[e];
-            v[0] = add(v[0], mul(be, be));
-        }
-        publish<1>(v, 1, a.partial + par * pstride, 0, G, red);
-        grid.sync();
-        gather(a.partial + par * pstride, 1, G, co);
-        par ^= 1;
-    }
-    const double bnorm = sqrt(co[0]);
-    if (bnorm == 0.0) {  // zero data: zero solution (solver.py:422-425)
-        for (int e = lo + tid; e < hi; e += bd) a.x[e] = 0.0;
-        if (cta == 0 && tid == 0) {
-            a.res->iterations = 0;
-            a.res->restarts = 0;
-            a.res->cycles = 0;
-            a.res->hist_len = 0;
-            a.res->final_rel = 0.0;
-            a.res->converged = 1;
-            a.res->stagnated = 0;
-            a.res->status = RAFEM_OK;
-        }
-        return;
-    }
-
-    const MatView A = a.A;
     // r = b - A x, returns ||r|| / ||b||   (solver.py:438-439, 517-518)
     auto true_residual = [&]() -> double {
         double v[1] = {0.0};
-        spmv_groups<W, STREAM>(A, g0, g1, SrcPlain{a.x}, [&](int g, const double* y) {
+        spmv_groups<W>(rows, g0, g1, SrcPlain{a.x}, [&](int g, const double* y) {
 #pragma unroll
             for (int w = 0; w < W; ++w) {
                 const int e = W * g + w;
@@ -264,7 +344,7 @@ __global__ void __launch_bounds__(KT, 1) gmres_kernel(KArgs a) {
             }
         });
         publish<1>(v, 1, a.partial + par * pstride, 0, G, red);
-        grid.sync();
+        Mode::sync();
         gather(a.partial + par * pstride, 1, G, co);
         par ^= 1;
         return sqrt(co[0]) / bnorm;
@@ -310,24 +390,15 @@ __global__ void __launch_bounds__(KT, 1) gmres_kernel(KArgs a) {
             double* Vk = a.V + (long long)k * ldv;
             // v_k (own rows) and w = A (M^-1 v_k)       (solver.py:469-470)
             for (int e = lo + tid; e < hi; e += bd) Vk[e] = mul(src[e], src_scale);
-            if (a.minv) {
-                spmv_groups<W, STREAM>(A, g0, g1, SrcBasis<PRE>{src, src_scale, a.minv},
-                                       [&](int g, const double* y) {
+            spmv_groups<W>(rows, g0, g1, SrcBasis<PRE>{src, src_scale, a.minv}, [&](int g, const double* y) {
 #pragma unroll
-                                           for (int w = 0; w < W; ++w) wk[W * g + w] = y[w];
-                                       });
-            } else {
-                spmv_groups<W, STREAM>(A, g0, g1, SrcBasis<false>{src, src_scale, nullptr},
-                                       [&](int g, const double* y) {
-#pragma unroll
-                                           for (int w = 0; w < W; ++w) wk[W * g + w] = y[w];
-                                       });
-            }
+                for (int w = 0; w < W; ++w) wk[W * g + w] = y[w];
+            });
             __syncthreads();
             // CGS pass 1: h_i = v_i . w
             double* P = a.partial + par * pstride;
             multidot(a.V, ldv, k + 1, wk, lo, hi, P, G, red);
-            grid.sync();
+            Mode::sync();
             gather(P, k + 1, G, co);
             par ^= 1;
             if (tid == 0)
@@ -335,12 +406,12 @@ __global__ void __launch_bounds__(KT, 1) gmres_kernel(KArgs a) {
             // w -= sum h_i v_i ; CGS pass 2: c_i = v_i . w
             for (int e = lo + tid; e < hi; e += bd) {
                 double acc = wk[e];
-                for (int i = 0; i <= k; ++i) acc = sub(acc, mul(co[i], __ldcg(a.V + (long long)i * ldv + e)));
+                for (int i = 0; i <= k; ++i) acc = sub(acc, mul(co[i], __ldca(a.V + (long long)i * ldv + e)));
                 wk[e] = acc;
             }
             P = a.partial + par * pstride;
             multidot(a.V, ldv, k + 1, wk, lo, hi, P, G, red);
-            grid.sync();
+            Mode::sync();
             gather(P, k + 1, G, co);
             par ^= 1;
             if (tid == 0)
@@ -351,13 +422,13 @@ __global__ void __launch_bounds__(KT, 1) gmres_kernel(KArgs a) {
                 for (int e = lo + tid; e < hi; e += bd) {
                     double acc = wk[e];
                     for (int i = 0; i <= k; ++i)
-                        acc = sub(acc, mul(co[i], __ldcg(a.V + (long long)i * ldv + e)));
+                        acc = sub(acc, mul(co[i], __ldca(a.V + (long long)i * ldv + e)));
                     wk[e] = acc;
                     v[0] = add(v[0], mul(acc, acc));
                 }
                 P = a.partial + par * pstride;
                 publish<1>(v, 1, P, 0, G, red);
-                grid.sync();
+                Mode::sync();
                 gather(P, 1, G, co);
                 par ^= 1;
             }
@@ -419,7 +490,7 @@ __global__ void __launch_bounds__(KT, 1) gmres_kernel(KArgs a) {
             __syncthreads();
             for (int e = lo + tid; e < hi; e += bd) {
                 double u = 0.0;
-                for (int i = 0; i < used; ++i) u = add(u, mul(__ldcg(a.V + (long long)i * ldv + e), yy[i]));
+                for (int i = 0; i < used; ++i) u = add(u, mul(__ldca(a.V + (long long)i * ldv + e), yy[i]));
                 if (PRE) u = mul(a.minv[e], u);
                 a.x[e] = add(a.x[e], u);
             }
@@ -428,7 +499,7 @@ __global__ void __launch_bounds__(KT, 1) gmres_kernel(KArgs a) {
         ++cycles;
         have_prev = true;
         prev_start = cycle_start;
-        grid.sync();  // x final everywhere before the next SpMV
+        Mode::sync();  // x final everywhere before the next SpMV
 
         if (broke || dead) {  // solver.py:516-524
             rel = true_residual();
@@ -440,30 +511,19 @@ __global__ void __launch_bounds__(KT, 1) gmres_kernel(KArgs a) {
             break;
         }
     }
-
-    if (cta == 0 && tid == 0) {
-        a.res->iterations = total;
-        a.res->restarts = cycles > 0 ? cycles - 1 : 0;
-        a.res->cycles = cycles;
-        a.res->hist_len = hlen;
-        a.res->final_rel = rel;
-        a.res->converged = converged ? 1 : 0;
-        a.res->stagnated = (latched && !converged) ? 1 : 0;
-        a.res->status = status;
-    }
+    if (cta == 0 && tid == 0) write_result(a.res, total, cycles, hlen, rel, converged, latched && !converged, status);
 }
 
 // ---------------------------------------------------------------------------
-// Jacobi-preconditioned CG with two grid barriers per iteration (p is
-// formed on the fly inside the SpMV gather).  Not in the reference (which
-// ships GMRES only); used for the SPD FEM systems under its own backend
-// name.  Converged only when the TRUE residual meets the tolerance: a
-// recursive-residual exit re-enters at the top with r = b - A x and
-// restarts the recurrence if needed (mirrors solver.py:437-450).
+// Jacobi-preconditioned CG with two barriers per iteration (p is formed on
+// the fly inside the SpMV gather).  Not in the reference (which ships GMRES
+// only); used for the SPD FEM systems under its own backend name.
+// Converged only when the TRUE residual meets the tolerance: a recursive-
+// residual exit re-enters at the top with r = b - A x and restarts the
+// recurrence if needed (mirrors solver.py:437-450).
 
-template <int W, bool PRE, bool STREAM>
-__global__ void __launch_bounds__(KT, 1) pcg_kernel(KArgs a) {
-    cg::grid_group grid = cg::this_grid();
+template <int W, bool PRE, class Mode, class R>
+RF_DEV void pcg_body(const KArgs& a, const R& rows) {
     __shared__ double red[32 * 8];
     __shared__ double co[8];
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
@@ -472,41 +532,8 @@ __global__ void __launch_bounds__(KT, 1) pcg_kernel(KArgs a) {
     const long long pstride = 8LL * G;
     int par = 0;
 
-    if (*a.flag) {
-        if (cta == 0 && tid == 0) {
-            a.res->status = RAFEM_ERR_INVALID;
-            a.res->converged = 0;
-            a.res->iterations = 0;
-        }
-        return;
-    }
-    {
-        double v[1] = {0.0};
-        for (int e = lo + tid; e < hi; e += bd) {
-            const double be = a.b[e];
-            v[0] = add(v[0], mul(be, be));
-        }
-        publish<1>(v, 1, a.partial + par * pstride, 0, G, red);
-        grid.sync();
-        gather(a.partial + par * pstride, 1, G, co);
-        par ^= 1;
-    }
-    const double bnorm = sqrt(co[0]);
-    if (bnorm == 0.0) {
-        for (int e = lo + tid; e < hi; e += bd) a.x[e] = 0.0;
-        if (cta == 0 && tid == 0) {
-            a.res->iterations = 0;
-            a.res->restarts = 0;
-            a.res->cycles = 0;
-            a.res->hist_len = 0;
-            a.res->final_rel = 0.0;
-            a.res->converged = 1;
-            a.res->stagnated = 0;
-            a.res->status = RAFEM_OK;
-        }
-        return;
-    }
-    const MatView A = a.A;
+    const double bnorm = prologue<Mode>(a, lo, hi, co, red, par, pstride);
+    if (bnorm < 0.0) return;
     long long total = 0, cycles = 0, hlen = 0;
     bool converged = false;
     double rel = INFINITY;
@@ -516,7 +543,7 @@ __global__ void __launch_bounds__(KT, 1) pcg_kernel(KArgs a) {
         double rz, rr;
         {  // r = b - A x ; z = M^-1 r ; (r.z, r.r)
             double v[2] = {0.0, 0.0};
-            spmv_groups<W, STREAM>(A, g0, g1, SrcPlain{a.x}, [&](int g, const double* y) {
+            spmv_groups<W>(rows, g0, g1, SrcPlain{a.x}, [&](int g, const double* y) {
 #pragma unroll
                 for (int w = 0; w < W; ++w) {
                     const int e = W * g + w;
@@ -530,7 +557,7 @@ __global__ void __launch_bounds__(KT, 1) pcg_kernel(KArgs a) {
             });
             double* P = a.partial + par * pstride;
             publish<2>(v, 2, P, 0, G, red);
-            grid.sync();
+            Mode::sync();
             gather(P, 2, G, co);
             par ^= 1;
             rz = co[0];
@@ -556,7 +583,7 @@ __global__ void __launch_bounds__(KT, 1) pcg_kernel(KArgs a) {
             {  // q = A p, p = z + beta p_old formed in the gather; p.q
                 double v[1] = {0.0};
                 const SrcCg src{a.z, po, beta, first};
-                spmv_groups<W, STREAM>(A, g0, g1, src, [&](int g, const double* y) {
+                spmv_groups<W>(rows, g0, g1, src, [&](int g, const double* y) {
 #pragma unroll
                     for (int w = 0; w < W; ++w) {
                         const int e = W * g + w;
@@ -568,7 +595,7 @@ __global__ void __launch_bounds__(KT, 1) pcg_kernel(KArgs a) {
                 });
                 double* P = a.partial + par * pstride;
                 publish<1>(v, 1, P, 0, G, red);
-                grid.sync();
+                Mode::sync();
                 gather(P, 1, G, co);
                 par ^= 1;
                 pq = co[0];
@@ -592,7 +619,7 @@ __global__ void __launch_bounds__(KT, 1) pcg_kernel(KArgs a) {
                 }
                 double* P = a.partial + par * pstride;
                 publish<2>(v, 2, P, 0, G, red);
-                grid.sync();
+                Mode::sync();
                 gather(P, 2, G, co);
                 par ^= 1;
                 rzn = co[0];
@@ -616,20 +643,50 @@ __global__ void __launch_bounds__(KT, 1) pcg_kernel(KArgs a) {
         ++cycles;
         if (status != RAFEM_OK) break;
     }
-    if (cta == 0 && tid == 0) {
-        a.res->iterations = total;
-        a.res->restarts = cycles > 0 ? cycles - 1 : 0;
-        a.res->cycles = cycles;
-        a.res->hist_len = hlen;
-        a.res->final_rel = rel;
-        a.res->converged = converged ? 1 : 0;
-        a.res->stagnated = 0;
-        a.res->status = status;
-    }
+    if (cta == 0 && tid == 0) write_result(a.res, total, cycles, hlen, rel, converged, false, status);
 }
 
 // ---------------------------------------------------------------------------
-// helper kernels
+// kernels
+
+template <int W, bool PRE, bool STREAM>
+__global__ void __launch_bounds__(KT, 1) gmres_grid_kernel(KArgs a) {
+    extern __shared__ __align__(16) double dyn[];
+    const Rows<W, false, STREAM> rows{a.A.rp, a.A.col, a.A.val, 0};
+    gmres_body<W, PRE, GridMode>(a, rows, dyn);
+}
+
+template <int W, bool PRE, bool STREAM>
+__global__ void __launch_bounds__(KT, 1) pcg_grid_kernel(KArgs a) {
+    const Rows<W, false, STREAM> rows{a.A.rp, a.A.col, a.A.val, 0};
+    pcg_body<W, PRE, GridMode>(a, rows);
+}
+
+// cluster mode: dynamic smem = [Hessenberg scratch | value slice | column slice | rp slice]
+template <int W>
+RF_DEV Rows<W, true, false> cluster_rows(const KArgs& a, double* dyn) {
+    const int g0 = a.gpart[blockIdx.x], g1 = a.gpart[blockIdx.x + 1];
+    const int ns = __ldg(a.A.rp + g1) - __ldg(a.A.rp + g0);
+    double* sval = dyn + a.hess_smem;
+    int* scol = reinterpret_cast<int*>(sval + (long long)W * ns);
+    int* srp = scol + ((ns + 3) & ~3);
+    stage_slice<W>(a.A, g0, g1, sval, scol, srp);
+    return Rows<W, true, false>{srp, scol, sval, g0};
+}
+
+template <int W, bool PRE>
+__global__ void __launch_bounds__(KT, 1) gmres_cluster_kernel(KArgs a) {
+    extern __shared__ __align__(16) double dyn[];
+    const auto rows = cluster_rows<W>(a, dyn);
+    gmres_body<W, PRE, ClusterMode>(a, rows, dyn);
+}
+
+template <int W, bool PRE>
+__global__ void __launch_bounds__(KTC, 1) pcg_cluster_kernel(KArgs a) {
+    extern __shared__ __align__(16) double dyn[];
+    const auto rows = cluster_rows<W>(a, dyn);
+    pcg_body<W, PRE, ClusterMode>(a, rows);
+}
 
 // Balanced partition of row groups: CTA c starts at the first group whose
 // weight prefix (slots + groups) reaches c/G of the total.
@@ -683,7 +740,8 @@ __global__ void __launch_bounds__(256) spmv_kernel(MatView A, const double* __re
                                                    double* __restrict__ y) {
     const int g0 = blockIdx.x * blockDim.x;
     const int g1 = min(A.ngroups, g0 + (int)blockDim.x);
-    spmv_groups<W, STREAM>(A, g0, g1, SrcPlain{x}, [&](int g, const double* yy) {
+    const Rows<W, false, STREAM> rows{A.rp, A.col, A.val, 0};
+    spmv_groups<W>(rows, g0, g1, SrcPlain{x}, [&](int g, const double* yy) {
         if (W == 1) {
             y[g] = yy[0];
         } else {
@@ -710,14 +768,6 @@ __global__ void delta_kernel(const double* xn, const double* xo, int n, unsigned
 // ---------------------------------------------------------------------------
 // host launchers
 
-static int kernel_grid(rafem_ctx* ctx, const void* fn, size_t smem, int want) {
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, KT, smem) != cudaSuccess || occ < 1)
-        return 0;
-    const int gmax = occ * ctx->sm_count;
-    return std::max(1, std::min(want, gmax));
-}
-
 int jacobi_minv(rafem_ctx* ctx, const MatView& A, double* minv_dev, int* flag_dev) {
     RF_CUDA_TRY(ctx, cudaMemsetAsync(flag_dev, 0, sizeof(int), ctx->stream));
     const int blocks = (A.ngroups + 255) / 256;
@@ -732,10 +782,12 @@ int jacobi_minv(rafem_ctx* ctx, const MatView& A, double* minv_dev, int* flag_de
     return RAFEM_OK;
 }
 
+static bool streams_matrix(const MatView& A) { return A.slots * (4 + 8LL * A.W) > (48LL << 20); }
+
 int spmv_launch(rafem_ctx* ctx, const MatView& A, const double* x_dev, double* y_dev) {
     const int blocks = (A.ngroups + 255) / 256;
     if (blocks == 0) return RAFEM_OK;
-    const bool stream = A.slots * (4 + 8LL * A.W) > (48LL << 20);
+    const bool stream = streams_matrix(A);
     if (A.W == 1) {
         if (stream)
             spmv_kernel<1, true><<<blocks, 256, 0, ctx->stream>>>(A, x_dev, y_dev);
@@ -761,19 +813,69 @@ int vec_delta_launch(rafem_ctx* ctx, const double* xn, const double* xo, int n, 
     return RAFEM_OK;
 }
 
-template <int W, bool PRE, bool STREAM>
-static const void* pick_kernel(int method) {
-    return method == RAFEM_METHOD_PCG ? (const void*)pcg_kernel<W, PRE, STREAM>
-                                      : (const void*)gmres_kernel<W, PRE, STREAM>;
+template <int W, bool PRE>
+static const void* grid_kernel(bool gmres, bool stream) {
+    if (gmres) return stream ? (const void*)gmres_grid_kernel<W, PRE, true> : (const void*)gmres_grid_kernel<W, PRE, false>;
+    return stream ? (const void*)pcg_grid_kernel<W, PRE, true> : (const void*)pcg_grid_kernel<W, PRE, false>;
+}
+template <int W, bool PRE>
+static const void* cluster_kernel(bool gmres) {
+    return gmres ? (const void*)gmres_cluster_kernel<W, PRE> : (const void*)pcg_cluster_kernel<W, PRE>;
+}
+static const void* select_grid(bool gmres, int W, bool pre, bool stream) {
+    if (W == 1) return pre ? grid_kernel<1, true>(gmres, stream) : grid_kernel<1, false>(gmres, stream);
+    return pre ? grid_kernel<2, true>(gmres, stream) : grid_kernel<2, false>(gmres, stream);
+}
+static const void* select_cluster(bool gmres, int W, bool pre) {
+    if (W == 1) return pre ? cluster_kernel<1, true>(gmres) : cluster_kernel<1, false>(gmres);
+    return pre ? cluster_kernel<2, true>(gmres) : cluster_kernel<2, false>(gmres);
 }
 
-static const void* select_kernel(int method, int W, bool pre, bool stream) {
-    if (W == 1) {
-        if (pre) return stream ? pick_kernel<1, true, true>(method) : pick_kernel<1, true, false>(method);
-        return stream ? pick_kernel<1, false, true>(method) : pick_kernel<1, false, false>(method);
+// Partition for G CTAs (device) and, for the cluster path, the largest
+// per-CTA slice in bytes (host).  Cached per pattern id.
+struct PartInfo {
+    int* gpart = nullptr;
+    size_t max_slice = 0;
+};
+
+static int partition(rafem_ctx* ctx, const MatView& A, int G, bool need_slice, PartInfo& out) {
+    // cache hit?
+    for (auto& e : ctx->part_cache) {
+        if (A.pattern_id && e.pattern_id == A.pattern_id && e.G == G && e.rp == A.rp) {
+            out.gpart = e.gpart;
+            out.max_slice = e.max_slice;
+            return RAFEM_OK;
+        }
     }
-    if (pre) return stream ? pick_kernel<2, true, true>(method) : pick_kernel<2, true, false>(method);
-    return stream ? pick_kernel<2, false, true>(method) : pick_kernel<2, false, false>(method);
+    int* gpart = nullptr;
+    if (A.pattern_id) {
+        RF_CUDA_TRY(ctx, cudaMalloc(&gpart, sizeof(int) * (G + 1)));
+    } else {
+        if (int rc = ensure(ctx, ctx->ws_part, sizeof(int) * (size_t)(G + 1))) return rc;
+        gpart = static_cast<int*>(ctx->ws_part.p);
+    }
+    partition_kernel<<<(G + 1 + 127) / 128, 128, 0, ctx->stream>>>(A.rp, A.ngroups, G, gpart);
+    ctx->launches++;
+    RF_CUDA_TRY(ctx, cudaGetLastError());
+    size_t max_slice = 0;
+    if (need_slice) {
+        std::vector<int> hp(G + 1), hr(G + 1);
+        RF_CUDA_TRY(ctx, cudaMemcpyAsync(hp.data(), gpart, sizeof(int) * (G + 1), cudaMemcpyDeviceToHost, ctx->stream));
+        RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        for (int c = 0; c <= G; ++c)
+            RF_CUDA_TRY(ctx, cudaMemcpyAsync(&hr[c], A.rp + hp[c], sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        for (int c = 0; c < G; ++c) {
+            const size_t ns = (size_t)(hr[c + 1] - hr[c]);
+            const size_t ng = (size_t)(hp[c + 1] - hp[c]);
+            const size_t bytes = ns * 8 * A.W + ((ns + 3) & ~(size_t)3) * 4 + (ng + 1) * 4;
+            max_slice = std::max(max_slice, bytes);
+        }
+    }
+    if (A.pattern_id) ctx->part_cache.push_back({A.pattern_id, A.rp, G, gpart, max_slice});
+    out.gpart = gpart;
+    out.max_slice = max_slice;
+    return RAFEM_OK;
 }
 
 int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const double* x0_dev,
@@ -783,8 +885,7 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     const bool gm = p.method != RAFEM_METHOD_PCG;
     const int m = gm ? p.restart_m : 1;
     const bool pre = p.precondition == RAFEM_PRECOND_JACOBI;
-    const bool stream = A.slots * (4 + 8LL * A.W) > (48LL << 20);
-    const void* fn = select_kernel(p.method, A.W, pre, stream);
+    const bool stream = streams_matrix(A);
 
     // x starts at x0 (or zero); the kernel never touches x before the first
     // true-residual test, so an exact x0 comes back bitwise (solver.py:448-450)
@@ -795,25 +896,64 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
         RF_CUDA_TRY(ctx, cudaMemsetAsync(x_dev, 0, sizeof(double) * n, ctx->stream));
     }
 
-    // persistent grid size: enough CTAs to cover the rows, at most one wave
-    const long long hess_doubles = gm ? (long long)(m + 1) * m + 4LL * m + 4 : 0;
+    const long long hess_doubles = gm ? (long long)(m + 1) * m + 5LL * m + 4 : 0;
+    const size_t hess_bytes = (size_t)hess_doubles * 8;
+
+    // ---- choose the execution mode
+    const void* fn = nullptr;
     size_t smem = 0;
-    bool hess_global = false;
-    if (gm) {
-        if (hess_doubles * 8 <= 160 * 1024) {
-            smem = (size_t)hess_doubles * 8;
+    bool cluster = false, hess_global = false;
+    PartInfo part;
+    int G = 0;
+    const bool try_cluster = p.grid_ctas <= 0 && A.slots * (4 + 8LL * A.W) <= (long long)kMaxCluster * (200 << 10);
+    if (try_cluster) {
+        int C = (int)std::min<long long>(kMaxCluster, std::max<long long>(1, (A.ngroups + 255) / 256));
+        if (int rc = partition(ctx, A, C, true, part)) return rc;
+        const size_t need = (size_t)((hess_doubles + 1) / 2 * 2) * 8 + part.max_slice;
+        if (need <= kSmemBudget) {
+            fn = select_cluster(gm, A.W, pre);
+            RF_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            RF_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(C);
+            cfg.blockDim = dim3(gm ? KT : KTC);
+            cfg.dynamicSmemBytes = need;
+            cfg.stream = ctx->stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = C;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) == cudaSuccess && nclusters >= 1) {
+                cluster = true;
+                smem = need;
+                G = C;
+            }
+            cudaGetLastError();
+        }
+    }
+    if (!cluster) {
+        fn = select_grid(gm, A.W, pre, stream);
+        if (hess_bytes <= 160 * 1024) {
+            smem = hess_bytes;
         } else {
             hess_global = true;
         }
+        if (smem > 48 * 1024)
+            RF_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 0;
+        RF_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, KT, smem));
+        if (occ < 1) return rafem_fail(ctx, RAFEM_ERR_CUDA, "cannot size the cooperative solver grid");
+        int want = p.grid_ctas > 0 ? p.grid_ctas : (int)std::max<long long>(1, ((long long)n + 511) / 512);
+        want = std::min(want, std::max(1, A.ngroups));
+        G = std::max(1, std::min(want, occ * ctx->sm_count));
+        if (int rc = partition(ctx, A, G, false, part)) return rc;
     }
-    if (smem > 48 * 1024)
-        RF_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int want = p.grid_ctas > 0 ? p.grid_ctas : (int)std::max<long long>(1, (n + 511) / 512);
-    want = std::min(want, std::max(1, A.ngroups));
-    const int G = kernel_grid(ctx, fn, smem, want);
-    if (G < 1) return rafem_fail(ctx, RAFEM_ERR_CUDA, "cannot size the cooperative solver grid");
 
-    // workspace
+    // ---- workspace
     const long long ldv = ((long long)n + 31) / 32 * 32;
     if (gm) {
         if (int rc = ensure(ctx, ctx->ws_basis, sizeof(double) * (size_t)(m + 1) * ldv)) return rc;
@@ -827,17 +967,11 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     const long long cyc_cap = hist_cap;
     if (int rc = ensure(ctx, ctx->ws_hist, sizeof(double) * (size_t)hist_cap)) return rc;
     if (int rc = ensure(ctx, ctx->ws_cyc, sizeof(long long) * (size_t)cyc_cap)) return rc;
-    if (int rc = ensure(ctx, ctx->ws_part, sizeof(int) * (size_t)(G + 1))) return rc;
-
-    int* gpart = static_cast<int*>(ctx->ws_part.p);
-    partition_kernel<<<(G + 1 + 127) / 128, 128, 0, ctx->stream>>>(A.rp, A.ngroups, G, gpart);
-    ctx->launches++;
-    RF_CUDA_TRY(ctx, cudaGetLastError());
 
     double* vec = static_cast<double*>(ctx->ws_vec.p);
     KArgs a{};
     a.A = A;
-    a.gpart = gpart;
+    a.gpart = part.gpart;
     a.ldv = ldv;
     a.b = b_dev;
     a.x = x_dev;
@@ -853,6 +987,7 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     a.partial = static_cast<double*>(ctx->ws_partial.p);
     a.hess = hess_global ? static_cast<double*>(ctx->ws_hess.p) : nullptr;
     a.hess_stride = hess_doubles;
+    a.hess_smem = (cluster && gm) ? (hess_doubles + 1) / 2 * 2 : 0;  // keep the slice 16-B aligned
     a.m = m;
     a.tol = p.tolerance;
     a.cap = p.max_total_iters > 0 ? p.max_total_iters : 10LL * n;
@@ -862,10 +997,30 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     a.cyc_cap = cyc_cap;
     a.res = res_dev;
     a.flag = flag_dev;
+    if (cluster) smem = (size_t)a.hess_smem * 8 + part.max_slice;
     void* args[] = {&a};
     if (ev_start) RF_CUDA_TRY(ctx, cudaEventRecord(ev_start, ctx->stream));
-    RF_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fn, dim3(G), dim3(KT), args, smem, ctx->stream));
+    if (cluster) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(G);
+        cfg.blockDim = dim3(gm ? KT : KTC);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = G;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        RF_CUDA_TRY(ctx, cudaLaunchKernelExC(&cfg, fn, args));
+        ctx->last_mode = 1;
+    } else {
+        RF_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fn, dim3(G), dim3(KT), args, smem, ctx->stream));
+        ctx->last_mode = 0;
+    }
     if (ev_stop) RF_CUDA_TRY(ctx, cudaEventRecord(ev_stop, ctx->stream));
+    ctx->last_ctas = G;
     ctx->launches++;
     return RAFEM_OK;
 }
