@@ -125,6 +125,12 @@ int rafem_device_info(rafem_ctx* ctx, int32_t* sm_count, int32_t* cc_major, int3
 int64_t rafem_kernel_launches(const rafem_ctx* ctx);
 /* the cudaStream_t every library call runs on (for external CUDA events) */
 void* rafem_stream(const rafem_ctx* ctx);
+/* diagnostics: last solve's execution mode (1 cluster-resident, 0 grid-wide)
+ * and CTA count; per-iteration phase timestamps (SM clock64) of CTA 0 when
+ * tracing is on: 8 slots per iteration, returns entries copied */
+int rafem_last_solve_mode(const rafem_ctx* ctx, int32_t* mode, int32_t* ctas);
+int rafem_set_trace(rafem_ctx* ctx, int32_t on);
+int64_t rafem_get_trace(rafem_ctx* ctx, int64_t* out, int64_t cap);
 
 /* ---- sparse.py ----------------------------------------------------------- */
 /* spmv (sparse.py:205-219): y = A x, each row summed left to right over its

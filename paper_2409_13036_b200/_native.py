@@ -76,6 +76,9 @@ _SIGS = {
     "rafem_device_info": (i32, [vp, P(i32), P(i32), P(i32), P(i64)]),
     "rafem_kernel_launches": (i64, [vp]),
     "rafem_stream": (vp, [vp]),
+    "rafem_last_solve_mode": (i32, [vp, P(i32), P(i32)]),
+    "rafem_set_trace": (i32, [vp, i32]),
+    "rafem_get_trace": (i64, [vp, vp, i64]),
     "rafem_spmv": (i32, [vp, i64, i64, i64, vp, vp, vp, vp, vp]),
     "rafem_coo_to_csr": (i32, [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp, P(i64)]),
     "rafem_matrix_create": (i32, [vp, i64, i64, vp, vp, vp, P(vp)]),

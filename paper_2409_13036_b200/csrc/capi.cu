@@ -195,7 +195,7 @@ void rafem_ctx_destroy(rafem_ctx* ctx) {
     if (!ctx) return;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (DevBuf* b : {&ctx->ws_basis, &ctx->ws_vec, &ctx->ws_partial, &ctx->ws_hess, &ctx->ws_hist,
-                      &ctx->ws_cyc, &ctx->ws_part, &ctx->ws_res})
+                      &ctx->ws_cyc, &ctx->ws_part, &ctx->ws_res, &ctx->ws_trace})
         if (b->p) cudaFree(b->p);
     if (ctx->pin) cudaFreeHost(ctx->pin);
     for (auto& e : ctx->part_cache) cudaFree(e.gpart);
@@ -221,6 +221,26 @@ int rafem_device_info(rafem_ctx* ctx, int32_t* sm_count, int32_t* cc_major, int3
 int64_t rafem_kernel_launches(const rafem_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 void* rafem_stream(const rafem_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int rafem_last_solve_mode(const rafem_ctx* ctx, int32_t* mode, int32_t* ctas) {
+    if (!ctx) return RAFEM_ERR_INVALID;
+    if (mode) *mode = ctx->last_mode;
+    if (ctas) *ctas = ctx->last_ctas;
+    return RAFEM_OK;
+}
+
+int rafem_set_trace(rafem_ctx* ctx, int32_t on) {
+    if (!ctx) return RAFEM_ERR_INVALID;
+    ctx->trace_on = on ? 1 : 0;
+    return RAFEM_OK;
+}
+
+int64_t rafem_get_trace(rafem_ctx* ctx, int64_t* out, int64_t cap) {
+    if (!ctx || !ctx->ws_trace.p) return 0;
+    const int64_t n = std::min<int64_t>(cap, (int64_t)(ctx->ws_trace.bytes / sizeof(long long)));
+    if (cudaMemcpy(out, ctx->ws_trace.p, sizeof(long long) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+    return n;
+}
 
 // ---- sparse ---------------------------------------------------------------
 

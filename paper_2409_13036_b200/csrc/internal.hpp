@@ -77,8 +77,11 @@ struct rafem_ctx {
     void* pin = nullptr;
     size_t pin_bytes = 0;
     std::vector<rafem::PartCacheEntry> part_cache;
+    int trace_on = 0;
+    rafem::DevBuf ws_trace;
     int last_mode = -1;  // 1: cluster-resident solve, 0: grid-wide cooperative solve
     int last_ctas = 0;
+    int last_team = 0;
 };
 
 struct rafem_matrix {

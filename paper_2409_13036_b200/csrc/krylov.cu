@@ -27,12 +27,13 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 namespace rafem {
 
 constexpr int KT = 512;        // threads per CTA of the persistent kernels
-constexpr int KTC = 640;      // cluster-mode PCG: one thread per row group at paper scale
+constexpr int KTC = 512;      // cluster-mode PCG: one thread per row group at paper scale
 constexpr int kMaxCluster = 16;
 constexpr size_t kSmemBudget = 220 * 1024;
 
@@ -64,7 +65,16 @@ struct KArgs {
     long long cyc_cap;
     KResult* res;
     const int* flag;  // nonzero: zero diagonal under Jacobi -> ValueError
+    long long* trace; // optional per-phase clock64 stamps (CTA 0, thread 0)
+    int trace_cap;
+    int team;         // lanes per row group in the solver SpMV (power of two)
 };
+
+// Phase timestamps for diagnosis: slot k of iteration i at trace[i*8 + k].
+RF_DEV void stamp(const KArgs& a, long long it, int k) {
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && it * 8 + k < a.trace_cap)
+        a.trace[it * 8 + k] = clock64();
+}
 
 // ---------------------------------------------------------------------------
 // execution modes
@@ -106,8 +116,83 @@ struct Rows {
 constexpr int kChunk = 8;   // scalar rows
 constexpr int kChunk2 = 4;  // paired rows (two double2 per slot in flight)
 
+// Solver SpMV: a team of `team` lanes (power of two <= 32, runtime) per row
+// group; lane l takes slots l, l + team, ... (two in flight), and the team
+// combines its partial sums with a fixed xor-butterfly.  The summation
+// order differs from the reference's left-to-right one but is fixed for a
+// given launch shape, so solves stay bit-reproducible.  A team puts every
+// gather of a row in flight at once, which matters when rows are few per
+// CTA (paper-scale meshes spread over all SMs).  team == 1 is one thread
+// per row.  The loop trip count is uniform over the CTA, so every lane
+// reaches the shuffles; lane 0 of each team runs the row epilogue.
+// `pre(g)` runs on lane 0 before the slot loop (owner-row loads that do not
+// depend on the product, so their latency overlaps the gathers) and its
+// result is handed to `fin(g, y, pf)` after the team reduction.
+struct NoPre {
+    RF_DEV int operator()(int) const { return 0; }
+};
+
+template <int W, class R, class Src, class Pre, class Fin>
+RF_DEV void spmv_team2(const R& rows, int g0, int g1, int team, const Src& src, const Pre& pre, Fin&& fin) {
+    const int lane = threadIdx.x & (team - 1);
+    const int nteams = blockDim.x / team;
+    const int tt = threadIdx.x / team;
+    for (int gb = g0; gb < g1; gb += nteams) {
+        const int g = gb + tt;
+        const bool active = g < g1;
+        double av = 0.0, at = 0.0;
+        decltype(pre(0)) pf{};
+        if (active && lane == 0) pf = pre(g);
+        if (active) {
+            const int s0 = rows.start(g), s1 = rows.start(g + 1);
+            for (int s = s0 + lane; s < s1; s += 2 * team) {
+                const int sb = s + team;
+                const bool two = sb < s1;
+                if constexpr (W == 1) {
+                    const int c0 = rows.column(s);
+                    const int c1 = two ? rows.column(sb) : c0;
+                    const double a0 = rows.value1(s);
+                    const double a1 = two ? rows.value1(sb) : 0.0;
+                    const double x0 = src.at(c0);
+                    const double x1 = two ? src.at(c1) : 0.0;
+                    av = add(av, mul(a0, x0));
+                    if (two) av = add(av, mul(a1, x1));
+                } else {
+                    const int c0 = rows.column(s);
+                    const int c1 = two ? rows.column(sb) : c0;
+                    const double2 a0 = rows.value2(s);
+                    const double2 a1 = two ? rows.value2(sb) : make_double2(0.0, 0.0);
+                    const double2 x0 = src.at2(c0);
+                    const double2 x1 = two ? src.at2(c1) : make_double2(0.0, 0.0);
+                    av = add(av, mul(a0.x, x0.x));
+                    at = add(at, mul(a0.y, x0.y));
+                    if (two) {
+                        av = add(av, mul(a1.x, x1.x));
+                        at = add(at, mul(a1.y, x1.y));
+                    }
+                }
+            }
+        }
+        for (int o = team >> 1; o > 0; o >>= 1) {
+            av = add(av, __shfl_xor_sync(0xffffffffu, av, o));
+            if (W == 2) at = add(at, __shfl_xor_sync(0xffffffffu, at, o));
+        }
+        if (active && lane == 0) {
+            double y[2] = {av, at};
+            fin(g, y, pf);
+        }
+    }
+}
+
 template <int W, class R, class Src, class Epi>
+RF_DEV void spmv_team(const R& rows, int g0, int g1, int team, const Src& src, Epi&& epi) {
+    spmv_team2<W>(rows, g0, g1, team, src, NoPre{}, [&](int g, const double* y, int) { epi(g, y); });
+}
+
+template <int W, class R, class Src, class Epi, int CH1 = kChunk, int CH2 = Src::kChunk2>
 RF_DEV void spmv_groups(const R& rows, int g0, int g1, const Src& src, Epi&& epi) {
+    constexpr int kChunk = CH1;
+    constexpr int kChunk2 = CH2;
     for (int g = g0 + threadIdx.x; g < g1; g += blockDim.x) {
         const int s0 = rows.start(g), s1 = rows.start(g + 1);
         if constexpr (W == 1) {
@@ -160,6 +245,7 @@ RF_DEV void spmv_groups(const R& rows, int g0, int g1, const Src& src, Epi&& epi
 // Operand sources: the SpMV input is formed on the fly from vectors that
 // are final after the previous barrier, which saves a barrier per step.
 struct SrcPlain {
+    static constexpr int kChunk2 = 4;
     const double* x;
     RF_DEV double at(int j) const { return __ldca(x + j); }
     RF_DEV double2 at2(int c) const { return __ldca(reinterpret_cast<const double2*>(x) + c); }
@@ -169,6 +255,7 @@ struct SrcPlain {
 // vector (c = 1/beta or 1/h_{k,k-1}); owners store the same bits in V[k].
 template <bool PRE>
 struct SrcBasis {
+    static constexpr int kChunk2 = 4;
     const double* s;
     double c;
     const double* minv;
@@ -190,6 +277,7 @@ struct SrcBasis {
 
 // PCG: p_j = z_j + beta * pold_j (first step: p = z).
 struct SrcCg {
+    static constexpr int kChunk2 = 4;
     const double* z;
     const double* po;
     double beta;
@@ -334,7 +422,7 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
     // r = b - A x, returns ||r|| / ||b||   (solver.py:438-439, 517-518)
     auto true_residual = [&]() -> double {
         double v[1] = {0.0};
-        spmv_groups<W>(rows, g0, g1, SrcPlain{a.x}, [&](int g, const double* y) {
+        spmv_team<W>(rows, g0, g1, a.team, SrcPlain{a.x}, [&](int g, const double* y) {
 #pragma unroll
             for (int w = 0; w < W; ++w) {
                 const int e = W * g + w;
@@ -390,7 +478,7 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
             double* Vk = a.V + (long long)k * ldv;
             // v_k (own rows) and w = A (M^-1 v_k)       (solver.py:469-470)
             for (int e = lo + tid; e < hi; e += bd) Vk[e] = mul(src[e], src_scale);
-            spmv_groups<W>(rows, g0, g1, SrcBasis<PRE>{src, src_scale, a.minv}, [&](int g, const double* y) {
+            spmv_team<W>(rows, g0, g1, a.team, SrcBasis<PRE>{src, src_scale, a.minv}, [&](int g, const double* y) {
 #pragma unroll
                 for (int w = 0; w < W; ++w) wk[W * g + w] = y[w];
             });
@@ -515,22 +603,73 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
 }
 
 // ---------------------------------------------------------------------------
-// Jacobi-preconditioned CG with two barriers per iteration (p is formed on
-// the fly inside the SpMV gather).  Not in the reference (which ships GMRES
-// only); used for the SPD FEM systems under its own backend name.
-// Converged only when the TRUE residual meets the tolerance: a recursive-
-// residual exit re-enters at the top with r = b - A x and restarts the
-// recurrence if needed (mirrors solver.py:437-450).
+// Jacobi-preconditioned CG in the single-reduction (Chronopoulos-Gear)
+// form: per iteration ONE fused pass computes the owner updates
+//     p = u + beta p,  s = w + beta s,  x += alpha p,  r -= alpha s,
+//     u = M^-1 r,      w = A u,         (r.u, w.u, r.r)
+// and ONE barrier publishes the three dots.  The SpMV operand u_j is
+// formed on the fly in the gather from the previous iteration's r, w, s
+// (final after the last barrier) with exactly the owner's operation
+// sequence, so owner and gatherers agree bit for bit.  Not in the
+// reference (which ships GMRES only); used for the SPD FEM systems under
+// its own backend name.  Converged only when the TRUE residual meets the
+// tolerance: a recursive-residual exit re-enters at the top with
+// r = b - A x and restarts the recurrence if needed (solver.py:437-450).
+
+// u_j = M_j (r_j - alpha (w_j + beta s_j)); mode 0: u = M r; mode 1: no s term.
+template <bool PRE>
+struct SrcCgU {
+    static constexpr int kChunk2 = 2;
+    const double* r;
+    const double* w;
+    const double* s;
+    const double* minv;
+    double alpha, beta;
+    int mode;
+    RF_DEV double at(int j) const {
+        double t = __ldca(r + j);
+        if (mode) {
+            const double sw = mode == 2 ? add(__ldca(w + j), mul(beta, __ldca(s + j))) : __ldca(w + j);
+            t = sub(t, mul(alpha, sw));
+        }
+        return PRE ? mul(__ldg(minv + j), t) : t;
+    }
+    RF_DEV double2 at2(int c) const {
+        double2 t = __ldca(reinterpret_cast<const double2*>(r) + c);
+        if (mode) {
+            double2 sw = __ldca(reinterpret_cast<const double2*>(w) + c);
+            if (mode == 2) {
+                const double2 ss = __ldca(reinterpret_cast<const double2*>(s) + c);
+                sw.x = add(sw.x, mul(beta, ss.x));
+                sw.y = add(sw.y, mul(beta, ss.y));
+            }
+            t.x = sub(t.x, mul(alpha, sw.x));
+            t.y = sub(t.y, mul(alpha, sw.y));
+        }
+        if (PRE) {
+            const double2 mv = __ldg(reinterpret_cast<const double2*>(minv) + c);
+            t.x = mul(mv.x, t.x);
+            t.y = mul(mv.y, t.y);
+        }
+        return t;
+    }
+};
 
 template <int W, bool PRE, class Mode, class R>
 RF_DEV void pcg_body(const KArgs& a, const R& rows) {
     __shared__ double red[32 * 8];
     __shared__ double co[8];
-    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
+    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
     const int g0 = a.gpart[cta], g1 = a.gpart[cta + 1];
     const int lo = W * g0, hi = W * g1;
     const long long pstride = 8LL * G;
     int par = 0;
+    // ping-pong r, w, s (gathered); p and x are owner-only.  Selected with
+    // ternaries, not arrays, so nothing is indexed dynamically (no stack).
+    auto rb = [&](int i) { return i ? a.z : a.r; };
+    auto wb = [&](int i) { return i ? a.w1 : a.w0; };
+    auto sb = [&](int i) { return i ? a.q : a.p1; };
+    double* p = a.p0;
 
     const double bnorm = prologue<Mode>(a, lo, hi, co, red, par, pstride);
     if (bnorm < 0.0) return;
@@ -538,106 +677,132 @@ RF_DEV void pcg_body(const KArgs& a, const R& rows) {
     bool converged = false;
     double rel = INFINITY;
     int status = RAFEM_OK;
+    int cur = 0;
+
+    auto round = [&](double (&v)[3]) {
+        double* P = a.partial + par * pstride;
+        stamp(a, total, 1);
+        publish<3>(v, 3, P, 0, G, red);
+        stamp(a, total, 2);
+        Mode::sync();
+        stamp(a, total, 3);
+        gather(P, 3, G, co);
+        stamp(a, total, 4);
+        par ^= 1;
+    };
 
     while (true) {
-        double rz, rr;
-        {  // r = b - A x ; z = M^-1 r ; (r.z, r.r)
-            double v[2] = {0.0, 0.0};
-            spmv_groups<W>(rows, g0, g1, SrcPlain{a.x}, [&](int g, const double* y) {
+        {  // r = b - A x ; r.r
+            double v[3] = {0.0, 0.0, 0.0};
+            double* r = rb(cur);
+            spmv_team<W>(rows, g0, g1, a.team, SrcPlain{a.x}, [&](int g, const double* y) {
 #pragma unroll
                 for (int w = 0; w < W; ++w) {
                     const int e = W * g + w;
                     const double re = sub(a.b[e], y[w]);
-                    const double ze = PRE ? mul(a.minv[e], re) : re;
-                    a.r[e] = re;
-                    a.z[e] = ze;
-                    v[0] = add(v[0], mul(re, ze));
-                    v[1] = add(v[1], mul(re, re));
+                    r[e] = re;
+                    v[2] = add(v[2], mul(re, re));
                 }
             });
-            double* P = a.partial + par * pstride;
-            publish<2>(v, 2, P, 0, G, red);
-            Mode::sync();
-            gather(P, 2, G, co);
-            par ^= 1;
-            rz = co[0];
-            rr = co[1];
+            round(v);
         }
-        rel = sqrt(rr) / bnorm;
+        rel = sqrt(co[2]) / bnorm;
         if (rel <= a.tol) {
             converged = true;
             break;
         }
         if (total >= a.cap) break;
-        if (!(rz > 0.0) || !isfinite(rz)) {  // not SPD under this preconditioner
-            status = RAFEM_ERR_BREAKDOWN;
-            break;
-        }
-        const long long hstart = hlen;
-        double beta = 0.0;
-        int first = 1, pc = 0;
-        while (true) {
-            double* pn = pc ? a.p1 : a.p0;
-            const double* po = pc ? a.p0 : a.p1;
-            double pq;
-            {  // q = A p, p = z + beta p_old formed in the gather; p.q
-                double v[1] = {0.0};
-                const SrcCg src{a.z, po, beta, first};
-                spmv_groups<W>(rows, g0, g1, src, [&](int g, const double* y) {
+        double gamma, alpha, beta = 0.0;
+        {  // w = A u, u = M^-1 r ; (r.u, w.u)
+            double v[3] = {0.0, 0.0, 0.0};
+            const double* r = rb(cur);
+            double* w = wb(cur);
+            const SrcCgU<PRE> src{r, nullptr, nullptr, a.minv, 0.0, 0.0, 0};
+            spmv_team<W>(rows, g0, g1, a.team, src, [&](int g, const double* y) {
 #pragma unroll
-                    for (int w = 0; w < W; ++w) {
-                        const int e = W * g + w;
-                        const double pe = src.at(e);
-                        pn[e] = pe;
-                        a.q[e] = y[w];
-                        v[0] = add(v[0], mul(pe, y[w]));
-                    }
-                });
-                double* P = a.partial + par * pstride;
-                publish<1>(v, 1, P, 0, G, red);
-                Mode::sync();
-                gather(P, 1, G, co);
-                par ^= 1;
-                pq = co[0];
-            }
-            if (!(pq > 0.0) || !isfinite(pq)) {
-                status = RAFEM_ERR_BREAKDOWN;
+                for (int k = 0; k < W; ++k) {
+                    const int e = W * g + k;
+                    const double ue = src.at(e);
+                    w[e] = y[k];
+                    v[0] = add(v[0], mul(r[e], ue));
+                    v[1] = add(v[1], mul(y[k], ue));
+                }
+            });
+            round(v);
+            gamma = co[0];
+            if (!(gamma > 0.0) || !(co[1] > 0.0) || !isfinite(gamma) || !isfinite(co[1])) {
+                status = RAFEM_ERR_BREAKDOWN;  // not SPD under this preconditioner
                 break;
             }
-            const double alpha = rz / pq;
-            double rzn;
-            {  // x += alpha p ; r -= alpha q ; z = M^-1 r ; (r.z, r.r)
-                double v[2] = {0.0, 0.0};
-                for (int e = lo + tid; e < hi; e += bd) {
-                    a.x[e] = add(a.x[e], mul(alpha, pn[e]));
-                    const double re = sub(a.r[e], mul(alpha, a.q[e]));
-                    const double ze = PRE ? mul(a.minv[e], re) : re;
-                    a.r[e] = re;
-                    a.z[e] = ze;
-                    v[0] = add(v[0], mul(re, ze));
-                    v[1] = add(v[1], mul(re, re));
+            alpha = gamma / co[1];
+        }
+        const long long hstart = hlen;
+        int mode = 1;
+        while (true) {
+            stamp(a, total, 0);
+            const double* ro = rb(cur);
+            const double* wo = wb(cur);
+            const double* so = sb(cur);
+            double* rn = rb(cur ^ 1);
+            double* wn = wb(cur ^ 1);
+            double* sn = sb(cur ^ 1);
+            double v[3] = {0.0, 0.0, 0.0};
+            const SrcCgU<PRE> src{ro, wo, so, a.minv, alpha, beta, mode};
+            // owner-row operands are loaded before the slot loop (prefetch)
+            struct Own {
+                double r[W], w[W], s[W], m[W], p[W], x[W];
+            };
+            auto pre = [&](int g) {
+                Own o;
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    const int e = W * g + k;
+                    o.r[k] = ro[e];
+                    o.w[k] = wo[e];
+                    o.s[k] = mode == 2 ? so[e] : 0.0;
+                    o.m[k] = PRE ? __ldg(a.minv + e) : 1.0;
+                    o.p[k] = mode == 2 ? p[e] : 0.0;
+                    o.x[k] = a.x[e];
                 }
-                double* P = a.partial + par * pstride;
-                publish<2>(v, 2, P, 0, G, red);
-                Mode::sync();
-                gather(P, 2, G, co);
-                par ^= 1;
-                rzn = co[0];
-                rr = co[1];
-            }
+                return o;
+            };
+            spmv_team2<W>(rows, g0, g1, a.team, src, pre, [&](int g, const double* y, const Own& o) {
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    const int e = W * g + k;
+                    const double s_n = mode == 2 ? add(o.w[k], mul(beta, o.s[k])) : o.w[k];
+                    const double u_o = PRE ? mul(o.m[k], o.r[k]) : o.r[k];
+                    const double p_n = mode == 2 ? add(u_o, mul(beta, o.p[k])) : u_o;
+                    a.x[e] = add(o.x[k], mul(alpha, p_n));
+                    p[e] = p_n;
+                    const double r_n = sub(o.r[k], mul(alpha, s_n));
+                    const double u_n = PRE ? mul(o.m[k], r_n) : r_n;
+                    rn[e] = r_n;
+                    wn[e] = y[k];
+                    sn[e] = s_n;
+                    v[0] = add(v[0], mul(r_n, u_n));
+                    v[1] = add(v[1], mul(y[k], u_n));
+                    v[2] = add(v[2], mul(r_n, r_n));
+                }
+            });
+            round(v);
+            cur ^= 1;
             ++total;
-            const double est = sqrt(rr) / bnorm;
+            const double est = sqrt(co[2]) / bnorm;
             if (cta == 0 && tid == 0 && hlen < a.hist_cap) a.hist[hlen] = est;
             ++hlen;
             if (est <= a.tol || total >= a.cap) break;
-            if (!(rzn > 0.0) || !isfinite(rzn)) {
+            const double gnew = co[0];
+            const double bnew = gnew / gamma;
+            const double den = co[1] - bnew * gnew / alpha;
+            if (!(gnew > 0.0) || !(den > 0.0) || !isfinite(den)) {
                 status = RAFEM_ERR_BREAKDOWN;
                 break;
             }
-            beta = rzn / rz;
-            rz = rzn;
-            first = 0;
-            pc ^= 1;
+            alpha = gnew / den;
+            beta = bnew;
+            gamma = gnew;
+            mode = 2;
         }
         if (cta == 0 && tid == 0 && cycles < a.cyc_cap) a.cyc[cycles] = hlen - hstart;
         ++cycles;
@@ -646,23 +811,12 @@ RF_DEV void pcg_body(const KArgs& a, const R& rows) {
     if (cta == 0 && tid == 0) write_result(a.res, total, cycles, hlen, rel, converged, false, status);
 }
 
+
 // ---------------------------------------------------------------------------
 // kernels
 
-template <int W, bool PRE, bool STREAM>
-__global__ void __launch_bounds__(KT, 1) gmres_grid_kernel(KArgs a) {
-    extern __shared__ __align__(16) double dyn[];
-    const Rows<W, false, STREAM> rows{a.A.rp, a.A.col, a.A.val, 0};
-    gmres_body<W, PRE, GridMode>(a, rows, dyn);
-}
-
-template <int W, bool PRE, bool STREAM>
-__global__ void __launch_bounds__(KT, 1) pcg_grid_kernel(KArgs a) {
-    const Rows<W, false, STREAM> rows{a.A.rp, a.A.col, a.A.val, 0};
-    pcg_body<W, PRE, GridMode>(a, rows);
-}
-
-// cluster mode: dynamic smem = [Hessenberg scratch | value slice | column slice | rp slice]
+// A CTA's matrix slice staged in shared memory (constant for the solve):
+// dynamic smem = [Hessenberg scratch | value slice | column slice | rp slice]
 template <int W>
 RF_DEV Rows<W, true, false> cluster_rows(const KArgs& a, double* dyn) {
     const int g0 = a.gpart[blockIdx.x], g1 = a.gpart[blockIdx.x + 1];
@@ -672,6 +826,32 @@ RF_DEV Rows<W, true, false> cluster_rows(const KArgs& a, double* dyn) {
     int* srp = scol + ((ns + 3) & ~3);
     stage_slice<W>(a.A, g0, g1, sval, scol, srp);
     return Rows<W, true, false>{srp, scol, sval, g0};
+}
+
+// Grid mode; MS selects the matrix source: 0 read-only global loads,
+// 1 evict-first streaming loads (matrix larger than L2), 2 slice in smem.
+template <int W, bool PRE, int MS>
+__global__ void __launch_bounds__(KT, 1) gmres_grid_kernel(KArgs a) {
+    extern __shared__ __align__(16) double dyn[];
+    if constexpr (MS == 2) {
+        const auto rows = cluster_rows<W>(a, dyn);
+        gmres_body<W, PRE, GridMode>(a, rows, dyn);
+    } else {
+        const Rows<W, false, MS == 1> rows{a.A.rp, a.A.col, a.A.val, 0};
+        gmres_body<W, PRE, GridMode>(a, rows, dyn);
+    }
+}
+
+template <int W, bool PRE, int MS>
+__global__ void __launch_bounds__(KT, 1) pcg_grid_kernel(KArgs a) {
+    extern __shared__ __align__(16) double dyn[];
+    if constexpr (MS == 2) {
+        const auto rows = cluster_rows<W>(a, dyn);
+        pcg_body<W, PRE, GridMode>(a, rows);
+    } else {
+        const Rows<W, false, MS == 1> rows{a.A.rp, a.A.col, a.A.val, 0};
+        pcg_body<W, PRE, GridMode>(a, rows);
+    }
 }
 
 template <int W, bool PRE>
@@ -813,18 +993,22 @@ int vec_delta_launch(rafem_ctx* ctx, const double* xn, const double* xo, int n, 
     return RAFEM_OK;
 }
 
+template <int W, bool PRE, int MS>
+static const void* grid_kernel_ms(bool gmres) {
+    return gmres ? (const void*)gmres_grid_kernel<W, PRE, MS> : (const void*)pcg_grid_kernel<W, PRE, MS>;
+}
 template <int W, bool PRE>
-static const void* grid_kernel(bool gmres, bool stream) {
-    if (gmres) return stream ? (const void*)gmres_grid_kernel<W, PRE, true> : (const void*)gmres_grid_kernel<W, PRE, false>;
-    return stream ? (const void*)pcg_grid_kernel<W, PRE, true> : (const void*)pcg_grid_kernel<W, PRE, false>;
+static const void* grid_kernel(bool gmres, int ms) {
+    if (ms == 2) return grid_kernel_ms<W, PRE, 2>(gmres);
+    return ms == 1 ? grid_kernel_ms<W, PRE, 1>(gmres) : grid_kernel_ms<W, PRE, 0>(gmres);
 }
 template <int W, bool PRE>
 static const void* cluster_kernel(bool gmres) {
     return gmres ? (const void*)gmres_cluster_kernel<W, PRE> : (const void*)pcg_cluster_kernel<W, PRE>;
 }
-static const void* select_grid(bool gmres, int W, bool pre, bool stream) {
-    if (W == 1) return pre ? grid_kernel<1, true>(gmres, stream) : grid_kernel<1, false>(gmres, stream);
-    return pre ? grid_kernel<2, true>(gmres, stream) : grid_kernel<2, false>(gmres, stream);
+static const void* select_grid(bool gmres, int W, bool pre, int ms) {
+    if (W == 1) return pre ? grid_kernel<1, true>(gmres, ms) : grid_kernel<1, false>(gmres, ms);
+    return pre ? grid_kernel<2, true>(gmres, ms) : grid_kernel<2, false>(gmres, ms);
 }
 static const void* select_cluster(bool gmres, int W, bool pre) {
     if (W == 1) return pre ? cluster_kernel<1, true>(gmres) : cluster_kernel<1, false>(gmres);
@@ -905,7 +1089,13 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     bool cluster = false, hess_global = false;
     PartInfo part;
     int G = 0;
-    const bool try_cluster = p.grid_ctas <= 0 && A.slots * (4 + 8LL * A.W) <= (long long)kMaxCluster * (200 << 10);
+    // Grid mode over every SM is the default: measured on B200 (mesh-B
+    // analog) a 148-CTA grid with team SpMV beats one 16-CTA cluster by
+    // 2.5x despite the costlier barrier.  RAFEM_SOLVER_MODE=cluster selects
+    // the cluster-resident variant for experiments.
+    const char* force = getenv("RAFEM_SOLVER_MODE");
+    const bool try_cluster = p.grid_ctas <= 0 && (force && force[0] == 'c') &&
+                             A.slots * (4 + 8LL * A.W) <= (long long)kMaxCluster * (200 << 10);
     if (try_cluster) {
         int C = (int)std::min<long long>(kMaxCluster, std::max<long long>(1, (A.ngroups + 255) / 256));
         if (int rc = partition(ctx, A, C, true, part)) return rc;
@@ -935,22 +1125,31 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
             cudaGetLastError();
         }
     }
+    int ms = stream ? 1 : 0;
     if (!cluster) {
-        fn = select_grid(gm, A.W, pre, stream);
-        if (hess_bytes <= 160 * 1024) {
+        // one CTA per SM (the kernels are register-bound to 1 CTA/SM)
+        int want = p.grid_ctas > 0 ? p.grid_ctas : ctx->sm_count;
+        want = std::max(1, std::min(want, A.ngroups));
+        G = want;
+        // stage the matrix slice in smem when it fits next to the Hessenberg scratch
+        const bool small = A.slots * (4 + 8LL * A.W) <= (long long)G * (160 << 10);
+        if (int rc = partition(ctx, A, G, small, part)) return rc;
+        const size_t hs_al = (size_t)((hess_doubles + 1) / 2 * 2) * 8;
+        if (small && hs_al + part.max_slice <= kSmemBudget) {
+            ms = 2;
+            smem = hs_al + part.max_slice;
+        } else if (hess_bytes <= 160 * 1024) {
             smem = hess_bytes;
         } else {
             hess_global = true;
         }
+        fn = select_grid(gm, A.W, pre, ms);
         if (smem > 48 * 1024)
             RF_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ = 0;
         RF_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, KT, smem));
         if (occ < 1) return rafem_fail(ctx, RAFEM_ERR_CUDA, "cannot size the cooperative solver grid");
-        int want = p.grid_ctas > 0 ? p.grid_ctas : (int)std::max<long long>(1, ((long long)n + 511) / 512);
-        want = std::min(want, std::max(1, A.ngroups));
-        G = std::max(1, std::min(want, occ * ctx->sm_count));
-        if (int rc = partition(ctx, A, G, false, part)) return rc;
+        if (G > occ * ctx->sm_count) return rafem_fail(ctx, RAFEM_ERR_INVALID, "grid_ctas exceeds co-resident CTAs");
     }
 
     // ---- workspace
@@ -987,7 +1186,7 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     a.partial = static_cast<double*>(ctx->ws_partial.p);
     a.hess = hess_global ? static_cast<double*>(ctx->ws_hess.p) : nullptr;
     a.hess_stride = hess_doubles;
-    a.hess_smem = (cluster && gm) ? (hess_doubles + 1) / 2 * 2 : 0;  // keep the slice 16-B aligned
+    a.hess_smem = ((cluster || ms == 2) && gm) ? (hess_doubles + 1) / 2 * 2 : 0;  // keep the slice 16-B aligned
     a.m = m;
     a.tol = p.tolerance;
     a.cap = p.max_total_iters > 0 ? p.max_total_iters : 10LL * n;
@@ -997,6 +1196,21 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     a.cyc_cap = cyc_cap;
     a.res = res_dev;
     a.flag = flag_dev;
+    if (ctx->trace_on) {
+        if (int rc = ensure(ctx, ctx->ws_trace, sizeof(long long) * 8 * 4096)) return rc;
+        RF_CUDA_TRY(ctx, cudaMemsetAsync(ctx->ws_trace.p, 0, sizeof(long long) * 8 * 4096, ctx->stream));
+        a.trace = static_cast<long long*>(ctx->ws_trace.p);
+        a.trace_cap = 8 * 4096;
+    }
+    {
+        const int rows_per_cta = (A.ngroups + G - 1) / G;
+        const int threads = (cluster && !gm) ? KTC : KT;
+        int team = 1;
+        while (team < 16 && rows_per_cta * team * 2 <= threads) team *= 2;
+        if (const char* env = getenv("RAFEM_TEAM")) team = std::max(1, std::min(32, atoi(env)));
+        a.team = team;
+        ctx->last_team = team;
+    }
     if (cluster) smem = (size_t)a.hess_smem * 8 + part.max_slice;
     void* args[] = {&a};
     if (ev_start) RF_CUDA_TRY(ctx, cudaEventRecord(ev_start, ctx->stream));
