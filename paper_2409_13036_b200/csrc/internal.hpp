@@ -79,6 +79,8 @@ struct rafem_ctx {
     std::vector<rafem::PartCacheEntry> part_cache;
     int trace_on = 0;
     rafem::DevBuf ws_trace;
+    rafem::DevBuf ws_flags;     // grid barrier / all-reduce slots
+    unsigned epoch = 0;         // per-launch flag epoch
     int last_mode = -1;  // 1: cluster-resident solve, 0: grid-wide cooperative solve
     int last_ctas = 0;
     int last_team = 0;

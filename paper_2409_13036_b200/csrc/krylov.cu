@@ -68,6 +68,8 @@ struct KArgs {
     long long* trace; // optional per-phase clock64 stamps (CTA 0, thread 0)
     int trace_cap;
     int team;         // lanes per row group in the solver SpMV (power of two)
+    unsigned long long* flags;  // 2 x G x 8 words of barrier/all-reduce slots
+    unsigned epoch;             // per-launch flag epoch (never 0)
 };
 
 // Phase timestamps for diagnosis: slot k of iteration i at trace[i*8 + k].
@@ -81,10 +83,12 @@ RF_DEV void stamp(const KArgs& a, long long it, int k) {
 
 struct GridMode {
     static constexpr bool kCluster = false;
+    static constexpr bool kFlags = false;  // LL flag all-reduce (measured slower: L2 hot spot)
     RF_DEV static void sync() { cg::this_grid().sync(); }
 };
 struct ClusterMode {
     static constexpr bool kCluster = true;
+    static constexpr bool kFlags = false;
     RF_DEV static void sync() { cg::this_cluster().sync(); }
 };
 
@@ -365,23 +369,152 @@ RF_DEV void write_result(KResult* res, long long total, long long cycles, long l
     res->status = status;
 }
 
+// ---------------------------------------------------------------------------
+// Grid-wide barrier + all-reduce without cooperative_groups.
+//
+// Each CTA owns a 64-byte slot per round parity.  For up to 3 values the
+// slot carries the CTA's block-reduced partials LL-style: every 8-byte
+// word holds half of a double in its low 32 bits and the round flag in the
+// high 32 bits, and 8-byte stores are single-copy atomic, so a reader that
+// sees the current flag in a word also sees its data.  One polling pass of
+// warp 0 over the G slots is therefore barrier and gather at once (one L2
+// round trip after the last CTA arrives, instead of barrier + gather).
+// Publication is release-ordered after the CTA's vector writes
+// (bar.sync then __threadfence by the publishing thread) and the poll is
+// followed by an acquire fence, so the next phase's gathers see every
+// CTA's vectors.  Flags are (launch epoch << 16 | round); slots alternate
+// parity, which suffices because a CTA can run at most one round ahead of
+// the slowest poller.  A spin cap traps instead of hanging the GPU.
+
+RF_DEV void st_relaxed(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+RF_DEV unsigned long long ld_relaxed(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+constexpr long long kSpinCap = 1LL << 31;
+
+template <class Mode>
+struct Sync {
+    const KArgs& a;
+    unsigned round = 0;
+
+    RF_DEV unsigned flag() const { return (a.epoch << 16) | (round & 0xffffu); }
+    RF_DEV unsigned long long* slot(int cta) const {
+        return a.flags + ((size_t)(round & 1u) * gridDim.x + cta) * 8;
+    }
+
+    // Block-reduce v, combine over all CTAs in a fixed order into co[0..nv).
+    template <int NV>
+    RF_DEV void reduce(double (&v)[NV], int nv, double* P, double* co, double* red) {
+        const int G = gridDim.x;
+        if constexpr (Mode::kCluster || !Mode::kFlags) {
+            publish<NV>(v, nv, P, 0, G, red);
+            Mode::sync();
+            gather(P, nv, G, co);
+            return;
+        } else {
+            static_assert(NV <= 3, "LL slots carry at most three values");
+            block_sum<NV>(v, red);
+            const unsigned f = flag();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                unsigned long long* s = slot(blockIdx.x);
+#pragma unroll
+                for (int j = 0; j < NV; ++j) {
+                    if (j < nv) {
+                        const unsigned long long bits = (unsigned long long)__double_as_longlong(v[j]);
+                        st_relaxed(s + 2 * j, ((unsigned long long)f << 32) | (bits & 0xffffffffULL));
+                        st_relaxed(s + 2 * j + 1, ((unsigned long long)f << 32) | (bits >> 32));
+                    }
+                }
+            }
+            if (threadIdx.x < 32) {
+                const int lane = threadIdx.x;
+                double acc[NV];
+#pragma unroll
+                for (int j = 0; j < NV; ++j) acc[j] = 0.0;
+                for (int c = lane; c < G; c += 32) {
+                    const unsigned long long* s = slot(c);
+                    unsigned long long w[2 * NV];
+                    long long spins = 0;
+                    bool ok;
+                    do {
+                        ok = true;
+#pragma unroll
+                        for (int k = 0; k < 2 * NV; ++k) {
+                            if (k < 2 * nv) {
+                                w[k] = ld_relaxed(s + k);
+                                ok = ok && (unsigned)(w[k] >> 32) == f;
+                            }
+                        }
+                        if (++spins > kSpinCap) asm volatile("trap;");
+                    } while (!ok);
+#pragma unroll
+                    for (int j = 0; j < NV; ++j)
+                        if (j < nv)
+                            acc[j] = add(acc[j], __longlong_as_double((long long)((w[2 * j] & 0xffffffffULL) |
+                                                                                  (w[2 * j + 1] << 32))));
+                }
+#pragma unroll
+                for (int j = 0; j < NV; ++j) acc[j] = warp_sum(acc[j]);
+                if (lane == 0)
+                    for (int j = 0; j < nv; ++j) co[j] = acc[j];
+                __threadfence();
+            }
+            __syncthreads();
+            ++round;
+        }
+    }
+
+    // Barrier only (vector visibility).
+    RF_DEV void barrier() {
+        if constexpr (Mode::kCluster || !Mode::kFlags) {
+            Mode::sync();
+        } else {
+            __syncthreads();
+            const unsigned f = flag();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                st_relaxed(slot(blockIdx.x) + 7, f);
+            }
+            if (threadIdx.x < 32) {
+                for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) {
+                    long long spins = 0;
+                    while ((unsigned)ld_relaxed(slot(c) + 7) != f)
+                        if (++spins > kSpinCap) asm volatile("trap;");
+                }
+                __threadfence();
+            }
+            __syncthreads();
+            ++round;
+        }
+    }
+
+    // Partials already stored in P by publish(); barrier then fixed-order gather.
+    RF_DEV void sync_gather(const double* P, int nv, double* co) {
+        barrier();
+        gather(P, nv, gridDim.x, co);
+    }
+};
+
 // Shared prologue: invalid flag check and ||b|| (solver.py:413-425).
 // Returns bnorm, or a negative value when the kernel must stop.
 template <class Mode>
-RF_DEV double prologue(const KArgs& a, int lo, int hi, double* co, double* red, int& par, long long pstride) {
+RF_DEV double prologue(const KArgs& a, Sync<Mode>& sy, int lo, int hi, double* co, double* red, int& par,
+                       long long pstride) {
     if (*a.flag) {
         if (blockIdx.x == 0 && threadIdx.x == 0) write_result(a.res, 0, 0, 0, INFINITY, false, false, RAFEM_ERR_INVALID);
         return -1.0;
     }
-    const int G = gridDim.x;
     double v[1] = {0.0};
     for (int e = lo + threadIdx.x; e < hi; e += blockDim.x) {
         const double be = a.b[e];
         v[0] = add(v[0], mul(be, be));
     }
-    publish<1>(v, 1, a.partial + par * pstride, 0, G, red);
-    Mode::sync();
-    gather(a.partial + par * pstride, 1, G, co);
+    sy.template reduce<1>(v, 1, a.partial + par * pstride, co, red);
     par ^= 1;
     const double bnorm = sqrt(co[0]);
     if (bnorm == 0.0) {  // zero data: zero solution (solver.py:422-425)
@@ -415,8 +548,9 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
     double* co = yy + m;      // m + 2
     const long long pstride = (long long)(m + 2) * G;
     int par = 0;
+    Sync<Mode> sy{a};
 
-    const double bnorm = prologue<Mode>(a, lo, hi, co, red, par, pstride);
+    const double bnorm = prologue<Mode>(a, sy, lo, hi, co, red, par, pstride);
     if (bnorm < 0.0) return;
 
     // r = b - A x, returns ||r|| / ||b||   (solver.py:438-439, 517-518)
@@ -431,9 +565,7 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
                 v[0] = add(v[0], mul(re, re));
             }
         });
-        publish<1>(v, 1, a.partial + par * pstride, 0, G, red);
-        Mode::sync();
-        gather(a.partial + par * pstride, 1, G, co);
+        sy.template reduce<1>(v, 1, a.partial + par * pstride, co, red);
         par ^= 1;
         return sqrt(co[0]) / bnorm;
     };
@@ -486,8 +618,7 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
             // CGS pass 1: h_i = v_i . w
             double* P = a.partial + par * pstride;
             multidot(a.V, ldv, k + 1, wk, lo, hi, P, G, red);
-            Mode::sync();
-            gather(P, k + 1, G, co);
+            sy.sync_gather(P, k + 1, co);
             par ^= 1;
             if (tid == 0)
                 for (int i = 0; i <= k; ++i) H[(long long)k * (m + 1) + i] = co[i];
@@ -499,8 +630,7 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
             }
             P = a.partial + par * pstride;
             multidot(a.V, ldv, k + 1, wk, lo, hi, P, G, red);
-            Mode::sync();
-            gather(P, k + 1, G, co);
+            sy.sync_gather(P, k + 1, co);
             par ^= 1;
             if (tid == 0)
                 for (int i = 0; i <= k; ++i) H[(long long)k * (m + 1) + i] = add(H[(long long)k * (m + 1) + i], co[i]);
@@ -515,9 +645,7 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
                     v[0] = add(v[0], mul(acc, acc));
                 }
                 P = a.partial + par * pstride;
-                publish<1>(v, 1, P, 0, G, red);
-                Mode::sync();
-                gather(P, 1, G, co);
+                sy.template reduce<1>(v, 1, P, co, red);
                 par ^= 1;
             }
             const double hk1 = sqrt(co[0]);
@@ -587,7 +715,7 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
         ++cycles;
         have_prev = true;
         prev_start = cycle_start;
-        Mode::sync();  // x final everywhere before the next SpMV
+        sy.barrier();  // x final everywhere before the next SpMV
 
         if (broke || dead) {  // solver.py:516-524
             rel = true_residual();
@@ -671,7 +799,8 @@ RF_DEV void pcg_body(const KArgs& a, const R& rows) {
     auto sb = [&](int i) { return i ? a.q : a.p1; };
     double* p = a.p0;
 
-    const double bnorm = prologue<Mode>(a, lo, hi, co, red, par, pstride);
+    Sync<Mode> sy{a};
+    const double bnorm = prologue<Mode>(a, sy, lo, hi, co, red, par, pstride);
     if (bnorm < 0.0) return;
     long long total = 0, cycles = 0, hlen = 0;
     bool converged = false;
@@ -682,11 +811,7 @@ RF_DEV void pcg_body(const KArgs& a, const R& rows) {
     auto round = [&](double (&v)[3]) {
         double* P = a.partial + par * pstride;
         stamp(a, total, 1);
-        publish<3>(v, 3, P, 0, G, red);
-        stamp(a, total, 2);
-        Mode::sync();
-        stamp(a, total, 3);
-        gather(P, 3, G, co);
+        sy.template reduce<3>(v, 3, P, co, red);
         stamp(a, total, 4);
         par ^= 1;
     };
@@ -1196,6 +1321,16 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     a.cyc_cap = cyc_cap;
     a.res = res_dev;
     a.flag = flag_dev;
+    {  // barrier / all-reduce slots: zeroed once, distinguished per launch by the epoch
+        const size_t fb = sizeof(unsigned long long) * 2 * 8 * (size_t)std::max(G, 1);
+        if (ctx->ws_flags.bytes < fb) {
+            if (int rc = ensure(ctx, ctx->ws_flags, fb)) return rc;
+            RF_CUDA_TRY(ctx, cudaMemsetAsync(ctx->ws_flags.p, 0, ctx->ws_flags.bytes, ctx->stream));
+        }
+        ctx->epoch = ctx->epoch % 0xffffu + 1;
+        a.flags = static_cast<unsigned long long*>(ctx->ws_flags.p);
+        a.epoch = ctx->epoch;
+    }
     if (ctx->trace_on) {
         if (int rc = ensure(ctx, ctx->ws_trace, sizeof(long long) * 8 * 4096)) return rc;
         RF_CUDA_TRY(ctx, cudaMemsetAsync(ctx->ws_trace.p, 0, sizeof(long long) * 8 * 4096, ctx->stream));

@@ -33,8 +33,9 @@ for dims in [(20, 20, 21), (15, 15, 16)]:
                         f"dev={st.device_ms*1e3:.0f}us -> {st.device_ms*1e3/max(st.iterations,1):.2f} us/it")
                 rows = tr[5:k - 1]
                 if backend == "pcg" and len(rows) > 2 and rows[0, 0] > 0:
-                    d = np.diff(rows[:, :5], axis=1).mean(axis=0) / 1.965e3
+                    sp = ((rows[:, 1] - rows[:, 0]).mean()) / 1.965e3
+                    rd = ((rows[:, 4] - rows[:, 1]).mean()) / 1.965e3
                     per = (rows[1:, 0] - rows[:-1, 0]).mean() / 1.965e3
-                    line += f" | spmv {d[0]:.2f} publish {d[1]:.2f} sync {d[2]:.2f} gather {d[3]:.2f} | iter {per:.2f} us"
+                    line += f" | spmv {sp:.2f} reduce {rd:.2f} | iter {per:.2f} us"
                 print(line, flush=True)
     L.rafem_set_trace(ctx, 0)
