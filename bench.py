@@ -392,6 +392,10 @@ def c3_leg(hbm_peak, peak_src):
     from paper_2409_13036_b200 import _native as nat
     ms = C.c_double()
     nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 50, C.byref(ms)), "spmv bench")
+    os.environ["RAFEM_NO_TMA_SPMV"] = "1"
+    ms_plain = C.c_double()
+    nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 50, C.byref(ms_plain)), "spmv bench")
+    del os.environ["RAFEM_NO_TMA_SPMV"]
     S, N = h.mesh.slots, n
     b_paired = 20 * S + 4 * (N + 1) + 16 * N + 16 * N
     b_csr = 12 * (2 * S) + 4 * (2 * N + 1) + 8 * 2 * N + 8 * 2 * N
@@ -405,6 +409,8 @@ def c3_leg(hbm_peak, peak_src):
             "spmv": {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
                      "frac_of_8TBs": ach / 8000.0, "us_per_launch": 1e3 * ms.value,
                      "bytes_per_launch": b_paired, "layout": "node-paired CSR (int32 col + double2 per slot)",
+                     "kernel": "spmv_tma_kernel (TMA bulk-staged slot tiles, left-to-right rows)",
+                     "thread_per_row_kernel_GBs": b_paired / (ms_plain.value / 1e3) / 1e9,
                      "csr_equivalent_bytes": b_csr, "csr_equivalent_GBs": b_csr / (ms.value / 1e3) / 1e9,
                      "peak_source": peak_src},
             "pcg_cold_solve": {"iterations": st.iterations, "device_ms": st.device_ms,

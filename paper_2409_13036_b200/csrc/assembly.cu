@@ -547,7 +547,7 @@ int mesh_symbolic(rafem_mesh* m) {
     RF_CUDA_TRY(ctx, cudaMemcpyAsync(&slots, m->rp + N, sizeof(int), cudaMemcpyDeviceToHost, st));
     RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
     m->slots = slots;
-    RF_CUDA_TRY(ctx, cudaMalloc(&m->col, sizeof(int) * (size_t)std::max(slots, 1)));
+    RF_CUDA_TRY(ctx, cudaMalloc(&m->col, sizeof(int) * ((size_t)std::max(slots, 1) + 8)));  // +8: 16-B TMA tail
     RF_CUDA_TRY(ctx, cudaMalloc(&m->diag, sizeof(int) * (size_t)std::max(N, 1)));
     if (N > 0) {
         adj_fill_kernel<<<(N + 127) / 128, 128, 0, st>>>(m->inc_ptr, m->inc_ea, m->tets, N, m->rp, m->col, m->diag, m->inc_slot);

@@ -99,6 +99,7 @@ MatView system_view(rafem_system* s) {
     A.W = 2;
     A.slots = s->mesh->slots;
     A.pattern_id = s->mesh->id;
+    A.maxdeg = s->mesh->maxdeg;
     return A;
 }
 

@@ -44,6 +44,7 @@ struct MatView {
     int W;
     long long slots;
     unsigned long long pattern_id = 0;  // nonzero: partitions may be cached
+    int maxdeg = 0;                     // max slots per row group (0: unknown)
 };
 
 struct PartCacheEntry {

@@ -1055,6 +1055,77 @@ __global__ void __launch_bounds__(256) spmv_kernel(MatView A, const double* __re
     });
 }
 
+// Bandwidth-bound SpMV for paired matrices larger than L2: each CTA walks
+// tiles of `tr` node rows; one elected thread streams a tile's contiguous
+// slot data (double2 values + int32 columns) into shared memory with 1-D
+// TMA bulk copies completing on an mbarrier, double-buffered so the next
+// tile's copy overlaps this tile's compute.  Threads then sum their row left
+// to right from shared memory (bit-identical to sparse.py:217-218) while the
+// x gathers hit L2.  The matrix never passes through registers on its way
+// in, and no thread waits on a column load before issuing its gathers.
+__global__ void __launch_bounds__(256, 1) spmv_tma_kernel(MatView A, const double* __restrict__ x,
+                                                          double* __restrict__ y, int tr, int valcap,
+                                                          int bufbytes) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ __align__(8) unsigned long long bar[2];
+    const int N = A.ngroups;
+    const int tiles = (N + tr - 1) / tr;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int t, int b) {
+        const int r0 = t * tr, r1 = min(N, r0 + tr);
+        const int s0 = __ldg(A.rp + r0), s1 = __ldg(A.rp + r1);
+        const int sa = s0 & ~3, se = (s1 + 3) & ~3;
+        unsigned char* base = sm + (size_t)b * bufbytes;
+        const unsigned vb = 16u * (unsigned)(s1 - s0), cb = 4u * (unsigned)(se - sa);
+        mbar_expect_tx(&bar[b], vb + cb);
+        if (vb) tma_load_1d(base, A.val + 2LL * s0, vb, &bar[b]);
+        if (cb) tma_load_1d(base + (size_t)valcap * 16, A.col + sa, cb, &bar[b]);
+    };
+    int i = 0;
+    if (threadIdx.x == 0 && (int)blockIdx.x < tiles) issue(blockIdx.x, 0);
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+        const int b = i & 1;
+        const int tn = t + gridDim.x;
+        if (threadIdx.x == 0 && tn < tiles) {
+            fence_proxy_async();  // earlier generic reads of buffer b^1 before the async overwrite
+            issue(tn, b ^ 1);
+        }
+        mbar_wait(&bar[b], (unsigned)(i >> 1) & 1u);
+        const int r0 = t * tr, r1 = min(N, r0 + tr);
+        const int s0 = __ldg(A.rp + r0);
+        const int sa = s0 & ~3;
+        const double2* sv = reinterpret_cast<const double2*>(sm + (size_t)b * bufbytes);
+        const int* sc = reinterpret_cast<const int*>(sm + (size_t)b * bufbytes + (size_t)valcap * 16);
+        for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+            const int a0 = __ldg(A.rp + r), a1 = __ldg(A.rp + r + 1);
+            double av = 0.0, at = 0.0;
+            for (int s = a0; s < a1; s += 4) {
+                double2 xv[4], vv[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (s + j < a1) {
+                        vv[j] = sv[s + j - s0];
+                        xv[j] = __ldg(x2 + sc[s + j - sa]);
+                    }
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (s + j < a1) {
+                        av = add(av, mul(vv[j].x, xv[j].x));
+                        at = add(at, mul(vv[j].y, xv[j].y));
+                    }
+            }
+            reinterpret_cast<double2*>(y)[r] = make_double2(av, at);
+        }
+        __syncthreads();
+    }
+}
+
 // delta = max |xn - xo| / max(1, |xo|)  (fem.py:527-528); nonnegative
 // doubles order like their bit patterns, so an integer atomicMax is an
 // exact, order-independent max.
@@ -1093,6 +1164,24 @@ int spmv_launch(rafem_ctx* ctx, const MatView& A, const double* x_dev, double* y
     const int blocks = (A.ngroups + 255) / 256;
     if (blocks == 0) return RAFEM_OK;
     const bool stream = streams_matrix(A);
+    const char* no_tma = getenv("RAFEM_NO_TMA_SPMV");
+    if (A.W == 2 && stream && A.maxdeg > 0 && !(no_tma && no_tma[0] == '1')) {
+        int tr = 256;
+        // per buffer: tr*maxdeg double2 values + (tr*maxdeg + 8) int32 columns, two buffers
+        auto buf_bytes = [&](int t) { return t * A.maxdeg * 16 + ((t * A.maxdeg + 8) * 4 + 15) / 16 * 16; };
+        while (tr > 32 && 2 * (size_t)buf_bytes(tr) > kSmemBudget) tr /= 2;
+        if (2 * (size_t)buf_bytes(tr) <= kSmemBudget) {
+            const int valcap = tr * A.maxdeg;
+            const size_t smem = 2 * (size_t)buf_bytes(tr);
+            RF_CUDA_TRY(ctx, cudaFuncSetAttribute(spmv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            const int tiles = (A.ngroups + tr - 1) / tr;
+            const int grid = std::min(tiles, ctx->sm_count);
+            spmv_tma_kernel<<<grid, 256, smem, ctx->stream>>>(A, x_dev, y_dev, tr, valcap, buf_bytes(tr));
+            ctx->launches++;
+            RF_CUDA_TRY(ctx, cudaGetLastError());
+            return RAFEM_OK;
+        }
+    }
     if (A.W == 1) {
         if (stream)
             spmv_kernel<1, true><<<blocks, 256, 0, ctx->stream>>>(A, x_dev, y_dev);

@@ -1,6 +1,6 @@
 #!/bin/bash
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
-timeout 300 python scripts/probe_trace.py grid ",4,8" > gpurun_out/probe.txt 2>&1
+timeout 300 python scripts/probe_trace.py grid "" > gpurun_out/probe.txt 2>&1
 timeout 600 python -m pytest tests -q -m gpu --timeout 300 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu --no-c3 > gpurun_out/bench.log 2>&1
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu > gpurun_out/bench.log 2>&1

@@ -217,3 +217,24 @@ def test_pcg_on_fem_systems_vs_oracle():
         xo, so = O.pcg(a.row_ptr, a.col_idx, a.vals, b, tol=1e-10)
         assert abs(st.iterations - so.iterations) <= max(3, 0.05 * so.iterations)
         assert rel_err(x, xo) < 1e-8
+
+
+def test_tma_spmv_bitwise_at_1M_dofs():
+    """configs[2] (1,011,200 dofs): the TMA-staged streaming SpMV is bit-exact."""
+    import os
+    from paper_2409_13036_b200 import (CsrMatrix, MaterialParams, SimConfig, assemble_global,
+                                       generate_box_mesh, spmv)
+    mesh = generate_box_mesh(80, 80, 79)
+    n = mesh.node_count
+    t = np.full(n, 37.0)
+    s = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, np.zeros(n), t, 0.5)
+    x = np.random.default_rng(5).standard_normal(2 * n)
+    y_dev = spmv(s.matrix, x)                       # streaming TMA kernel (matrix > 48 MB)
+    os.environ["RAFEM_NO_TMA_SPMV"] = "1"
+    try:
+        y_plain = spmv(s.matrix, x)                 # thread-per-row kernel
+    finally:
+        del os.environ["RAFEM_NO_TMA_SPMV"]
+    a = s.matrix
+    assert np.array_equal(y_dev, y_plain)
+    assert np.array_equal(y_dev, O.matvec(a.row_ptr, a.col_idx, a.vals, x))
