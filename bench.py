@@ -313,7 +313,8 @@ def run_ours(args):
     achieved = bytes_total / (solve_ms / 1e3) / 1e9 if solve_ms > 0 else 0.0
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": None,
-                "kernel": f"{args.backend}_kernel<2,true,false> (persistent cooperative solve)",
+                "kernel": ("simulate_kernel<true> (whole run, one cooperative launch); bytes = PCG iterations"
+                           if runner.last_mode == "fused-simulation" else f"{args.backend}_grid_kernel (persistent solve)"),
                 "launches": passes, "avg_launch_us": 1e3 * solve_ms / max(passes, 1),
                 "share_of_step": solve_ms / total_ms if world == 1 else None,
                 "peak_source": peak_src,
@@ -330,6 +331,7 @@ def run_ours(args):
                    "solver_iterations_per_run": summs[0].total_solver_iterations,
                    "solver": f"{args.backend}+jacobi tol 1e-10", "parallelism": f"replicas x{world}",
                    "step": "one full 900 s simulation", "l2": "flushed (256 MB write) between timed steps",
+                   "device_path": f"{runner.last_mode} ({runner.last_ctas} CTAs)",
                    "assemble_ms_per_run": asm_ms / args.steps, "solve_ms_per_run": solve_ms / args.steps},
         "roofline": roofline,
         "gpu_launches": int(launches),

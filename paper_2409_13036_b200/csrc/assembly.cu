@@ -20,6 +20,7 @@
 //      atomics, so every pass is bit-stable.
 //   3. equilibration scale from deterministic diagonal sums (fem.py:390-400).
 //   4. scale + symmetric Dirichlet elimination per row (fem.py:402-428).
+#include "assembly_dev.cuh"
 #include "common.cuh"
 #include "internal.hpp"
 
@@ -212,15 +213,6 @@ __global__ void adj_fill_kernel(const int* inc_ptr, const unsigned* inc_ea, cons
 // cofactors (column j of E^-1 is the cross product of the other two edges
 // over det), grad_0 = -(grad_1 + grad_2 + grad_3).
 
-RF_DEV int sym_index(int a, int b) {
-    // packed upper triangle of a symmetric 4x4: (0,0)(0,1)(0,2)(0,3)(1,1)(1,2)(1,3)(2,2)(2,3)(3,3)
-    if (a > b) {
-        const int t = a;
-        a = b;
-        b = t;
-    }
-    return a * 4 - (a * (a - 1)) / 2 + (b - a);
-}
 
 __global__ void geometry_kernel(const double* nodes, const int* tets, int M, double* base,
                                 double* grad, double* vol_out) {
@@ -273,116 +265,22 @@ __global__ void geometry_kernel(const double* nodes, const int* tets, int M, dou
 }
 
 // ---------------------------------------------------------------------------
-// numeric fill
+// numeric fill (device functions in assembly_dev.cuh)
 
-struct Regions {
-    const double* tab;  // 5 x nreg: k, rho_c, sigma0, alpha, t_ref
-    int nreg;
-};
-
-// 1. per element: sigma(Tbar) (fem.py:272-278), Joule load (fem.py:286-288),
-//    T-rhs load rho_c/dt M T_prev + f_joule (fem.py:317-321).
-__global__ void element_kernel(const int* tets, const int* region, Regions R, const double* grad,
-                               const double* volv, int M, const double* t_it, int ts,
-                               const double* v_it, int vs, const double* t_prev, int ps, double dt,
-                               double* sigma_out, double* load_out, unsigned long long* bad) {
+// 1. per element: sigma, the 16 (V, T) block contributions, T-rhs loads
+__global__ void element_kernel(AsmMesh m, AsmFields f, double2* contrib, double* load, unsigned long long* bad) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= M) return;
-    int nd[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) nd[a] = tets[4 * e + a];
-    const int rg = region[e];
-    const double sigma0 = R.tab[2 * R.nreg + rg], alpha = R.tab[3 * R.nreg + rg];
-    const double tref = R.tab[4 * R.nreg + rg];
-    const double rcdt = R.tab[1 * R.nreg + rg] / dt;
-    double tsum = 0.0;
-#pragma unroll
-    for (int a = 0; a < 4; ++a) tsum = add(tsum, t_it[(long long)ts * nd[a]]);
-    const double tbar = tsum / 4.0;
-    const double sigma = mul(sigma0, add(1.0, mul(alpha, sub(tbar, tref))));
-    if (sigma <= 0.0) atomicMin(bad, (unsigned long long)e);  // fem.py:274
-    sigma_out[e] = sigma;
-    const double vol = volv[e];
-    double gv[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const double va = v_it[(long long)vs * nd[a]];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) gv[d] = add(gv[d], mul(va, grad[12LL * e + 3 * a + d]));
-    }
-    const double gg = add(add(mul(gv[0], gv[0]), mul(gv[2], gv[2])), mul(gv[1], gv[1]));
-    const double fj = mul(mul(sigma, gg), vol) / 4.0;
-    double tp[4];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) tp[b] = t_prev[(long long)ps * nd[b]];
-    const double moff = mul(rcdt, mul(vol, 0.05));  // rho_c/dt * vol/20
-    const double mdia = mul(rcdt, mul(vol, 0.1));   // rho_c/dt * vol/10
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        double t[4];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) t[b] = mul(a == b ? mdia : moff, tp[b]);
-        const double mt = add(add(t[0], t[2]), add(t[1], t[3]));
-        load_out[4LL * e + a] = add(mt, fj);
-    }
+    if (e >= m.M) return;
+    if (element_tet(e, m, f, contrib, load)) atomicMin(bad, (unsigned long long)e);
 }
 
-// 2. slot fill, TEAM lanes per node row.
-template <int TEAM>
-__global__ void fill_kernel(const int* rp, const int* inc_ptr, const unsigned* inc_ea,
-                            const unsigned* inc_slot, const int* region, Regions R,
-                            const double* base, const double* volv, const double* sigma,
-                            const double* load, int N, double dt, double* val2, double* rhs,
-                            double* diag_raw, const int* diag) {
-    const int team = (blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
-    const int lane = threadIdx.x % TEAM;
-    if (team >= N) return;
-    const int i = team;
-    const int s0 = rp[i], deg = rp[i + 1] - s0;
-    const int p0 = inc_ptr[i], p1 = inc_ptr[i + 1];
-    const int dslot = diag[i];
-    for (int cb = 0; cb < deg; cb += TEAM) {
-        const int l = cb + lane;
-        double accV = 0.0, accT = 0.0;
-        for (int p = p0; p < p1; ++p) {
-            const unsigned offs = __ldg(inc_slot + p);
-            int b = -1;
-#pragma unroll
-            for (int bb = 0; bb < 4; ++bb)
-                if ((int)((offs >> (8 * bb)) & 255u) == l) b = bb;
-            if (b >= 0) {
-                const unsigned ea = __ldg(inc_ea + p);
-                const int e = (int)(ea & 0x3fffffffu), a = (int)(ea >> 30);
-                const double bab = __ldg(base + 10LL * e + sym_index(a, b));
-                accV = add(accV, mul(__ldg(sigma + e), bab));
-                const int rg = __ldg(region + e);
-                const double kk = R.tab[rg];
-                const double rcdt = R.tab[R.nreg + rg] / dt;
-                const double mass = mul(__ldg(volv + e), a == b ? 0.1 : 0.05);
-                accT = add(accT, add(mul(rcdt, mass), mul(kk, bab)));
-            }
-        }
-        if (l < deg) {
-            reinterpret_cast<double2*>(val2)[s0 + l] = make_double2(accV, accT);
-            if (l == dslot) {
-                diag_raw[2LL * i] = accV;
-                diag_raw[2LL * i + 1] = accT;
-            }
-        }
-    }
-    if (dslot < 0 && lane == 0) {
-        diag_raw[2LL * i] = 0.0;
-        diag_raw[2LL * i + 1] = 0.0;
-    }
-    if (lane == 0) {  // T rhs: sum of element loads in ascending element order
-        double r = 0.0;
-        for (int p = p0; p < p1; ++p) {
-            const unsigned ea = __ldg(inc_ea + p);
-            r = add(r, __ldg(load + 4LL * (ea & 0x3fffffffu) + (ea >> 30)));
-        }
-        rhs[2LL * i] = 0.0;
-        rhs[2LL * i + 1] = r;
-    }
+// 2. slot fill, one warp per node row
+__global__ void __launch_bounds__(256) fill_kernel(AsmMesh m, const double2* contrib, const double* load,
+                                                   double2* val2, double* rhs, double* diag_raw) {
+    __shared__ FillScratch ws[8];
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= m.N) return;  // whole warps exit together
+    fill_node_warp(i, m, contrib, load, val2 + __ldg(m.rp + i), rhs, diag_raw, ws[threadIdx.x >> 5]);
 }
 
 // 3. scale = 2^round(log2(sum diag_T / sum diag_V)) from a fixed-order
@@ -403,66 +301,12 @@ __global__ void __launch_bounds__(1024) equil_kernel(const double* diag_raw, int
     }
 }
 
-RF_DEV double dof_value(int kind, double applied, double btemp) {
-    return kind == RAFEM_DOF_APPLIED_VOLTAGE ? applied : (kind == RAFEM_DOF_BOUNDARY_TEMP ? btemp : 0.0);
-}
-
-// 4. voltage-row scaling and symmetric Dirichlet elimination, keeping the
-//    explicit zeros so the pattern is step-invariant (fem.py:398-428).
-template <int TEAM>
-__global__ void constrain_kernel(const int* rp, const int* col, const uint8_t* kind, int N,
-                                 const double* scale_p, int apply, double applied, double btemp,
-                                 double* val2, double* rhs) {
-    const int team = (blockIdx.x * blockDim.x + threadIdx.x) / TEAM;
-    const int lane = threadIdx.x % TEAM;
-    const unsigned mask = (TEAM == 32) ? 0xffffffffu : (0xffffu << (threadIdx.x & 16));
-    if (team >= N) return;  // whole teams exit together (N teams, TEAM | 32)
-    const int i = team;
-    const double scale = *scale_p;
-    const int s0 = rp[i], deg = rp[i + 1] - s0;
-    const int kV = apply ? kind[2LL * i] : 0, kT = apply ? kind[2LL * i + 1] : 0;
-    double mV = 0.0, mT = 0.0;  // moved-column sums, storage order (fem.py:419-424)
-    for (int cb = 0; cb < deg; cb += TEAM) {
-        const int l = cb + lane;
-        double termV = 0.0, termT = 0.0;
-        int movV = 0, movT = 0;
-        if (l < deg) {
-            const int j = col[s0 + l];
-            const int cV = apply ? kind[2LL * j] : 0, cT = apply ? kind[2LL * j + 1] : 0;
-            double2 v = reinterpret_cast<double2*>(val2)[s0 + l];
-            const double vs = mul(v.x, scale);
-            if (!kV && cV) {
-                movV = 1;
-                termV = mul(vs, dof_value(cV, applied, btemp));
-            }
-            if (!kT && cT) {
-                movT = 1;
-                termT = mul(v.y, dof_value(cT, applied, btemp));
-            }
-            double outV = vs, outT = v.y;
-            if (kV || cV) outV = (kV && j == i) ? 1.0 : 0.0;
-            if (kT || cT) outT = (kT && j == i) ? 1.0 : 0.0;
-            reinterpret_cast<double2*>(val2)[s0 + l] = make_double2(outV, outT);
-        }
-        for (int t = 0; t < TEAM; ++t) {
-            const double tv = __shfl_sync(mask, termV, t, TEAM);
-            const double tt = __shfl_sync(mask, termT, t, TEAM);
-            const int fv = __shfl_sync(mask, movV, t, TEAM);
-            const int ft = __shfl_sync(mask, movT, t, TEAM);
-            if (fv) mV = add(mV, tv);
-            if (ft) mT = add(mT, tt);
-        }
-    }
-    if (lane == 0) {
-        double rv = 0.0;  // V rhs is zero before constraints (fem.py:388, 400)
-        double rt = rhs[2LL * i + 1];
-        if (apply) {
-            rv = kV ? dof_value(kV, applied, btemp) : sub(rv, mV);
-            rt = kT ? dof_value(kT, applied, btemp) : sub(rt, mT);
-        }
-        rhs[2LL * i] = rv;
-        rhs[2LL * i + 1] = rt;
-    }
+// 4. voltage-row scaling and symmetric Dirichlet elimination, one warp per node row
+__global__ void __launch_bounds__(256) constrain_kernel(AsmMesh m, const double* scale_p, int apply, double applied,
+                                                        double btemp, double2* val2, double* rhs) {
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= m.N) return;
+    constrain_node_warp(i, m, *scale_p, apply, applied, btemp, val2 + __ldg(m.rp + i), rhs, nullptr, nullptr);
 }
 
 // dof-order values for CsrMatrix.vals: row 2i then row 2i+1 per node.
@@ -575,6 +419,27 @@ int mesh_geometry(rafem_mesh* m) {
     return RAFEM_OK;
 }
 
+AsmMesh asm_mesh(const rafem_mesh* m) {
+    AsmMesh a;
+    a.tets = m->tets;
+    a.region = m->region;
+    a.regtab = m->regtab;
+    a.nreg = m->nreg;
+    a.base = m->base;
+    a.grad = m->grad;
+    a.vol = m->vol;
+    a.rp = m->rp;
+    a.col = m->col;
+    a.diag = m->diag;
+    a.inc_ptr = m->inc_ptr;
+    a.inc_ea = m->inc_ea;
+    a.inc_slot = m->inc_slot;
+    a.kind = m->kind;
+    a.N = m->N;
+    a.M = m->M;
+    return a;
+}
+
 int assemble_launch(rafem_system* s, const double* t_it, int ts, const double* v_it, int vs,
                     const double* t_prev, int ps, const rafem_assemble_params& p,
                     double* scale_dev, long long* bad_dev) {
@@ -582,33 +447,22 @@ int assemble_launch(rafem_system* s, const double* t_it, int ts, const double* v
     rafem_ctx* ctx = m->ctx;
     cudaStream_t st = ctx->stream;
     const int N = m->N, M = m->M;
-    const Regions R{m->regtab, m->nreg};
+    const AsmMesh am = asm_mesh(m);
+    const AsmFields f{t_it, ts, v_it, vs, t_prev, ps, p.dt};
+    double2* contrib = reinterpret_cast<double2*>(s->contrib);
+    double2* val2 = reinterpret_cast<double2*>(s->val2);
     RF_CUDA_TRY(ctx, cudaMemsetAsync(bad_dev, 0xff, sizeof(long long), st));
     if (M > 0) {
-        element_kernel<<<(M + 127) / 128, 128, 0, st>>>(m->tets, m->region, R, m->grad, m->vol, M, t_it, ts,
-                                                        v_it, vs, t_prev, ps, p.dt, s->sigma, s->load,
+        element_kernel<<<(M + 127) / 128, 128, 0, st>>>(am, f, contrib, s->load,
                                                         reinterpret_cast<unsigned long long*>(bad_dev));
         ctx->launches++;
     }
     if (N > 0) {
-        const int team = m->maxdeg <= 16 ? 16 : 32;
-        const long long threads = (long long)N * team;
-        const int blocks = (int)((threads + 255) / 256);
-        if (team == 16) {
-            fill_kernel<16><<<blocks, 256, 0, st>>>(m->rp, m->inc_ptr, m->inc_ea, m->inc_slot, m->region, R, m->base,
-                                                    m->vol, s->sigma, s->load, N, p.dt, s->val2, s->rhs, s->diagpart, m->diag);
-        } else {
-            fill_kernel<32><<<blocks, 256, 0, st>>>(m->rp, m->inc_ptr, m->inc_ea, m->inc_slot, m->region, R, m->base,
-                                                    m->vol, s->sigma, s->load, N, p.dt, s->val2, s->rhs, s->diagpart, m->diag);
-        }
+        const int blocks = (int)(((long long)N * 32 + 255) / 256);
+        fill_kernel<<<blocks, 256, 0, st>>>(am, contrib, s->load, val2, s->rhs, s->diagpart);
         equil_kernel<<<1, 1024, 0, st>>>(s->diagpart, N, p.equilibrate, scale_dev);
-        if (team == 16) {
-            constrain_kernel<16><<<blocks, 256, 0, st>>>(m->rp, m->col, m->kind, N, scale_dev, p.apply_constraints,
-                                                         p.applied_voltage, p.boundary_temp, s->val2, s->rhs);
-        } else {
-            constrain_kernel<32><<<blocks, 256, 0, st>>>(m->rp, m->col, m->kind, N, scale_dev, p.apply_constraints,
-                                                         p.applied_voltage, p.boundary_temp, s->val2, s->rhs);
-        }
+        constrain_kernel<<<blocks, 256, 0, st>>>(am, scale_dev, p.apply_constraints, p.applied_voltage,
+                                                 p.boundary_temp, val2, s->rhs);
         ctx->launches += 3;
     } else {
         RF_CUDA_TRY(ctx, cudaMemcpyAsync(scale_dev, &s->scale, sizeof(double), cudaMemcpyHostToDevice, st));

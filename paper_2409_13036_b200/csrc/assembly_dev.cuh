@@ -1,0 +1,253 @@
+// assembly_dev.cuh — per-element and per-node-row assembly steps as device
+// functions, shared by the standalone assembly kernels (assembly.cu) and
+// the fused device-resident simulation kernel (simulate.cu).
+//
+// Arithmetic follows the reference expression by expression (fem.py:247-430)
+// with every operation rounded separately (no FMA contraction):
+//   sigma  = sigma0 * (1 + alpha * (Tbar - Tref))            fem.py:273
+//   K_sig  = sigma * (vol * grad_a.grad_b)                    fem.py:280-282
+//   T blk  = (rho_c/dt) * (vol * (1+d_ab)/20) + k * base       fem.py:283-284, 317
+//   load_a = sum_b (rho_c/dt) M_ab T_prev,b + sigma|gradV|^2 vol / 4   fem.py:286-288, 319-321
+// and the per-slot sums run over the node's incident elements in ascending
+// element order, which is the reference's duplicate-summation order.
+#pragma once
+
+#include "../../include/rafem_b200.h"
+#include "common.cuh"
+
+namespace rafem {
+
+struct AsmMesh {
+    const int* tets;      // M x 4
+    const int* region;    // M
+    const double* regtab; // 5 x nreg: k, rho_c, sigma0, alpha, t_ref
+    int nreg;
+    const double* base;   // M x 10 packed symmetric vol*grad.grad
+    const double* grad;   // M x 12
+    const double* vol;    // M
+    const int* rp;        // N + 1 node pattern
+    const int* col;       // slots
+    const int* diag;      // N diagonal offsets
+    const int* inc_ptr;   // N + 1
+    const unsigned* inc_ea;   // tet | local << 30, ascending tet per node
+    const unsigned* inc_slot; // 4 x uint8 row offsets
+    const uint8_t* kind;  // 2N dof kinds
+    int N, M;
+};
+
+// nodal fields with strides (host inputs are contiguous N-arrays; the device
+// loop reads the interleaved dof vectors directly)
+struct AsmFields {
+    const double* t;
+    int ts;
+    const double* v;
+    int vs;
+    const double* tp;
+    int ps;
+    double dt;
+};
+
+RF_DEV int sym_index(int a, int b) {
+    // packed upper triangle of a symmetric 4x4: (0,0)(0,1)(0,2)(0,3)(1,1)(1,2)(1,3)(2,2)(2,3)(3,3)
+    if (a > b) {
+        const int t = a;
+        a = b;
+        b = t;
+    }
+    return a * 4 - (a * (a - 1)) / 2 + (b - a);
+}
+
+// Element e: 16 (V, T) block contributions in (a, b) row-major order and the
+// four T-rhs loads.  Returns true when sigma(Tbar) <= 0 (PhysicsRangeError).
+RF_DEV bool element_tet(int e, const AsmMesh& m, const AsmFields& f, double2* contrib, double* load) {
+    int nd[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) nd[a] = __ldg(m.tets + 4 * e + a);
+    const int rg = __ldg(m.region + e);
+    const double kk = m.regtab[rg];
+    const double rcdt = m.regtab[m.nreg + rg] / f.dt;
+    const double sigma0 = m.regtab[2 * m.nreg + rg], alpha = m.regtab[3 * m.nreg + rg];
+    const double tref = m.regtab[4 * m.nreg + rg];
+    double tv[4], vv[4], tp[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        tv[a] = __ldcg(f.t + (long long)f.ts * nd[a]);
+        vv[a] = __ldcg(f.v + (long long)f.vs * nd[a]);
+        tp[a] = __ldcg(f.tp + (long long)f.ps * nd[a]);
+    }
+    double tsum = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) tsum = add(tsum, tv[a]);
+    const double tbar = tsum / 4.0;
+    const double sigma = mul(sigma0, add(1.0, mul(alpha, sub(tbar, tref))));
+    const double vol = __ldg(m.vol + e);
+    double b10[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) b10[k] = __ldg(m.base + 10LL * e + k);
+    const double mdia = mul(vol, 0.1), moff = mul(vol, 0.05);  // vol (1 + d_ab) / 20
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const double bab = b10[sym_index(a, b)];
+            const double mass = a == b ? mdia : moff;
+            contrib[16LL * e + 4 * a + b] = make_double2(mul(sigma, bab), add(mul(rcdt, mass), mul(kk, bab)));
+        }
+    double gv[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) gv[d] = add(gv[d], mul(vv[a], __ldg(m.grad + 12LL * e + 3 * a + d)));
+    const double gg = add(add(mul(gv[0], gv[0]), mul(gv[2], gv[2])), mul(gv[1], gv[1]));
+    const double fj = mul(mul(sigma, gg), vol) / 4.0;
+    const double mo = mul(rcdt, moff), md = mul(rcdt, mdia);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        double t[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) t[b] = mul(a == b ? md : mo, tp[b]);
+        load[4LL * e + a] = add(add(add(t[0], t[2]), add(t[1], t[3])), fj);
+    }
+    return sigma <= 0.0;  // fem.py:274
+}
+
+// Per-warp staging for one node row's incident elements.
+struct FillScratch {
+    double2 c[32][4];
+    unsigned off[32];
+    double ld[32];
+};
+
+// Node row i, one warp: lane l accumulates slot l.  The warp loads up to 32
+// incidence records and their element contributions in parallel, stages
+// them in shared memory, then every lane walks the incidences in ascending
+// element order adding the contributions that land on its column.
+// Writes raw (unscaled, unconstrained) slot values to out[l], the T rhs and
+// the raw diagonal (V, T).
+RF_DEV void fill_node_warp(int i, const AsmMesh& m, const double2* contrib, const double* load,
+                           double2* out, double* rhs, double* diag_raw, FillScratch& ws) {
+    const int lane = threadIdx.x & 31;
+    const int deg = __ldg(m.rp + i + 1) - __ldg(m.rp + i);
+    const int p0 = __ldg(m.inc_ptr + i), ninc = __ldg(m.inc_ptr + i + 1) - p0;
+    const int dslot = __ldg(m.diag + i);
+    for (int cb = 0; cb < deg; cb += 32) {
+        const int l = cb + lane;
+        double accV = 0.0, accT = 0.0, racc = 0.0;
+        for (int pc = 0; pc < ninc; pc += 32) {
+            const int p = pc + lane;
+            if (p < ninc) {
+                const unsigned ea = __ldg(m.inc_ea + p0 + p);
+                const unsigned e = ea & 0x3fffffffu, a = ea >> 30;
+                ws.off[lane] = __ldg(m.inc_slot + p0 + p);
+#pragma unroll
+                for (int b = 0; b < 4; ++b) ws.c[lane][b] = __ldcg(contrib + 16LL * e + 4 * a + b);
+                ws.ld[lane] = __ldcg(load + 4LL * e + a);
+            }
+            __syncwarp();
+            const int nq = min(32, ninc - pc);
+            for (int q = 0; q < nq; ++q) {
+                const unsigned offs = ws.off[q];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    if ((int)((offs >> (8 * b)) & 255u) == l) {
+                        const double2 c = ws.c[q][b];
+                        accV = add(accV, c.x);
+                        accT = add(accT, c.y);
+                    }
+                }
+                racc = add(racc, ws.ld[q]);
+            }
+            __syncwarp();
+        }
+        if (l < deg) {
+            out[l] = make_double2(accV, accT);
+            if (l == dslot) {
+                diag_raw[2LL * i] = accV;
+                diag_raw[2LL * i + 1] = accT;
+            }
+        }
+        if (cb == 0 && lane == 0) {
+            rhs[2LL * i] = 0.0;
+            rhs[2LL * i + 1] = racc;
+        }
+    }
+    if (dslot < 0 && lane == 0) {
+        diag_raw[2LL * i] = 0.0;
+        diag_raw[2LL * i + 1] = 0.0;
+    }
+}
+
+RF_DEV double dof_value(int kind, double applied, double btemp) {
+    return kind == RAFEM_DOF_APPLIED_VOLTAGE ? applied : (kind == RAFEM_DOF_BOUNDARY_TEMP ? btemp : 0.0);
+}
+
+// Node row i, one warp: voltage-row scaling and symmetric Dirichlet
+// elimination keeping the explicit zeros (fem.py:398-428), in place on the
+// row's slots; optional Jacobi inverse diagonal of the final row.
+RF_DEV void constrain_node_warp(int i, const AsmMesh& m, double scale, int apply, double applied, double btemp,
+                                double2* vals, double* rhs, double* minv, int* zero_diag) {
+    const int lane = threadIdx.x & 31;
+    const int s0 = __ldg(m.rp + i), deg = __ldg(m.rp + i + 1) - s0;
+    const int kV = apply ? m.kind[2LL * i] : 0, kT = apply ? m.kind[2LL * i + 1] : 0;
+    const int dslot = __ldg(m.diag + i);
+    double mV = 0.0, mT = 0.0;  // moved-column sums in storage order (fem.py:419-424)
+    double dV = 0.0, dT = 0.0;
+    for (int cb = 0; cb < deg; cb += 32) {
+        const int l = cb + lane;
+        double termV = 0.0, termT = 0.0;
+        int movV = 0, movT = 0;
+        if (l < deg) {
+            const int j = __ldg(m.col + s0 + l);
+            const int cV = apply ? m.kind[2LL * j] : 0, cT = apply ? m.kind[2LL * j + 1] : 0;
+            const double2 v = vals[l];
+            const double vs = mul(v.x, scale);
+            if (!kV && cV) {
+                movV = 1;
+                termV = mul(vs, dof_value(cV, applied, btemp));
+            }
+            if (!kT && cT) {
+                movT = 1;
+                termT = mul(v.y, dof_value(cT, applied, btemp));
+            }
+            double outV = vs, outT = v.y;
+            if (kV || cV) outV = (kV && j == i) ? 1.0 : 0.0;
+            if (kT || cT) outT = (kT && j == i) ? 1.0 : 0.0;
+            vals[l] = make_double2(outV, outT);
+            if (l == dslot) {
+                dV = outV;
+                dT = outT;
+            }
+        }
+        for (int t = 0; t < 32; ++t) {
+            const double tv = __shfl_sync(0xffffffffu, termV, t);
+            const double tt = __shfl_sync(0xffffffffu, termT, t);
+            const int fv = __shfl_sync(0xffffffffu, movV, t);
+            const int ft = __shfl_sync(0xffffffffu, movT, t);
+            if (fv) mV = add(mV, tv);
+            if (ft) mT = add(mT, tt);
+        }
+    }
+    if (minv && dslot >= 0) {
+        const int src = dslot & 31;
+        dV = __shfl_sync(0xffffffffu, dV, src);
+        dT = __shfl_sync(0xffffffffu, dT, src);
+    }
+    if (lane == 0) {
+        double rv = 0.0;  // V rhs is zero before constraints (fem.py:388, 400)
+        double rt = rhs[2LL * i + 1];
+        if (apply) {
+            rv = kV ? dof_value(kV, applied, btemp) : sub(rv, mV);
+            rt = kT ? dof_value(kT, applied, btemp) : sub(rt, mT);
+        }
+        rhs[2LL * i] = rv;
+        rhs[2LL * i + 1] = rt;
+        if (minv) {  // solver.py:413-418 on the final stored diagonal
+            if (dslot < 0) dV = dT = 0.0;
+            if (dV == 0.0 || dT == 0.0) atomicOr(zero_diag, 1);
+            minv[2LL * i] = 1.0 / dV;
+            minv[2LL * i + 1] = 1.0 / dT;
+        }
+    }
+}
+
+}  // namespace rafem

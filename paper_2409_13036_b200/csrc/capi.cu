@@ -196,7 +196,7 @@ void rafem_ctx_destroy(rafem_ctx* ctx) {
     if (!ctx) return;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (DevBuf* b : {&ctx->ws_basis, &ctx->ws_vec, &ctx->ws_partial, &ctx->ws_hess, &ctx->ws_hist,
-                      &ctx->ws_cyc, &ctx->ws_part, &ctx->ws_res, &ctx->ws_trace, &ctx->ws_flags})
+                      &ctx->ws_cyc, &ctx->ws_part, &ctx->ws_res, &ctx->ws_trace, &ctx->ws_flags, &ctx->ws_simout})
         if (b->p) cudaFree(b->p);
     if (ctx->pin) cudaFreeHost(ctx->pin);
     for (auto& e : ctx->part_cache) cudaFree(e.gpart);
@@ -450,7 +450,7 @@ int rafem_system_create(rafem_mesh* m, rafem_system** out) {
 #define RF_SS(x) do { e = (x); if (e != cudaSuccess) { rafem_system_destroy(s); return rafem_fail_cuda(ctx, e, #x, __FILE__, __LINE__); } } while (0)
     RF_SS(cudaMalloc(&s->val2, sizeof(double) * 2 * S));
     RF_SS(cudaMalloc(&s->rhs, sizeof(double) * 2 * N));
-    RF_SS(cudaMalloc(&s->sigma, sizeof(double) * M));
+    RF_SS(cudaMalloc(&s->contrib, sizeof(double) * 32 * M));
     RF_SS(cudaMalloc(&s->load, sizeof(double) * 4 * M));
     RF_SS(cudaMalloc(&s->diagpart, sizeof(double) * 2 * N));
     RF_SS(cudaMalloc(&s->minv, sizeof(double) * 2 * N));
@@ -465,7 +465,7 @@ int rafem_system_create(rafem_mesh* m, rafem_system** out) {
 
 void rafem_system_destroy(rafem_system* s) {
     if (!s) return;
-    for (void* p : {(void*)s->val2, (void*)s->rhs, (void*)s->sigma, (void*)s->load, (void*)s->diagpart,
+    for (void* p : {(void*)s->val2, (void*)s->rhs, (void*)s->contrib, (void*)s->load, (void*)s->diagpart,
                     (void*)s->minv, (void*)s->xin, (void*)s->status, (void*)s->xs})
         if (p) cudaFree(p);
     delete s;
@@ -582,6 +582,78 @@ int rafem_simulate(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary
     const int N = m->N;
     const size_t n2 = 2 * (size_t)N;
     cudaStream_t st = ctx->stream;
+
+    // Preferred path: the whole simulation in one persistent kernel (PCG).
+    const char* nofused = getenv("RAFEM_NO_FUSED");
+    if (p->solver.method == RAFEM_METHOD_PCG && !(nofused && nofused[0] == '1')) {
+        const long long cap = std::max<long long>(rec_cap, 0);
+        double* d_rx = nullptr;
+        double* d_rt = nullptr;
+        double* d_rd = nullptr;
+        int* d_ri = nullptr;
+        auto release = [&]() {
+            cudaFree(d_rx);
+            cudaFree(d_rt);
+            cudaFree(d_rd);
+            cudaFree(d_ri);
+        };
+        if (cap > 0) {
+            RF_CUDA_TRY(ctx, cudaMalloc(&d_rt, sizeof(double) * cap));
+            RF_CUDA_TRY(ctx, cudaMalloc(&d_rd, sizeof(double) * cap));
+            RF_CUDA_TRY(ctx, cudaMalloc(&d_ri, sizeof(int) * cap));
+            if (p->record_fields && rec_x) RF_CUDA_TRY(ctx, cudaMalloc(&d_rx, sizeof(double) * n2 * cap));
+        }
+        SimDevOut so{};
+        float kms = 0.f;
+        const int frc = simulate_fused(s, p, &so, d_rx, d_rt, d_rd, d_ri, cap, s->xs + 5 * n2, &kms);
+        if (frc == RAFEM_OK) {
+            const long long nrec = std::min<long long>(so.accepted, cap);
+            if (nrec > 0) {
+                std::vector<double> ht(nrec), hd(nrec);
+                std::vector<int> hi(nrec);
+                RF_CUDA_TRY(ctx, cudaMemcpy(ht.data(), d_rt, sizeof(double) * nrec, cudaMemcpyDeviceToHost));
+                RF_CUDA_TRY(ctx, cudaMemcpy(hd.data(), d_rd, sizeof(double) * nrec, cudaMemcpyDeviceToHost));
+                RF_CUDA_TRY(ctx, cudaMemcpy(hi.data(), d_ri, sizeof(int) * nrec, cudaMemcpyDeviceToHost));
+                for (long long k = 0; k < nrec; ++k) {
+                    if (rec_step) rec_step[k] = k;
+                    if (rec_time) rec_time[k] = ht[k];
+                    if (rec_dt) rec_dt[k] = hd[k];
+                    if (rec_iters) rec_iters[k] = hi[k];
+                }
+                if (d_rx) RF_CUDA_TRY(ctx, cudaMemcpy(rec_x, d_rx, sizeof(double) * n2 * nrec, cudaMemcpyDeviceToHost));
+            }
+            release();
+            out->accepted_steps = so.accepted;
+            out->total_corrector_iters = so.corr;
+            out->total_solver_iterations = so.inner;
+            out->dt_halvings = so.halvings;
+            out->passes = so.passes;
+            out->final_time = so.t;
+            out->status = so.status;
+            out->failed_step = so.failed_step;
+            out->failed_dt = so.failed_dt;
+            out->bad_element = so.bad;
+            out->assemble_ms = so.asm_ns * 1e-6;
+            out->solve_ms = so.solve_ns * 1e-6;
+            out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_wall).count();
+            if (so.status == RAFEM_ERR_PHYSICS) {
+                char buf[128];
+                std::snprintf(buf, sizeof(buf), "sigma(T) <= 0 in element %lld", (long long)so.bad);
+                return rafem_fail(ctx, so.status, buf);
+            }
+            if (so.status == RAFEM_ERR_STEP_FAILURE) {
+                char buf[160];
+                std::snprintf(buf, sizeof(buf), "step %d failed to converge with dt already at the floor (%g s)",
+                              so.failed_step, so.failed_dt);
+                return rafem_fail(ctx, so.status, buf);
+            }
+            if (so.status == RAFEM_ERR_INVALID)
+                return rafem_fail(ctx, so.status, "Jacobi preconditioning requires a zero-free diagonal");
+            return so.status;
+        }
+        release();
+        if (frc != RAFEM_ERR_UNSUPPORTED) return frc;
+    }
     double* xacc = s->xs;            // accepted (V, T)
     double* xprev = s->xs + n2;      // accepted one step earlier
     double* xit = s->xs + 2 * n2;    // current iterate (x_old)

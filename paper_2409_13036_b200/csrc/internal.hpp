@@ -33,6 +33,16 @@ struct PassStatus {
     double scale;          // voltage_row_scale of the pass
 };
 
+// Summary the fused simulation kernel leaves in device memory.
+struct SimDevOut {
+    long long accepted, corr, inner, halvings, passes;
+    double t;
+    int status, failed_step;
+    double failed_dt;
+    long long bad;
+    long long asm_ns, solve_ns;
+};
+
 // Matrix view consumed by the Krylov and SpMV kernels.  W = dofs per row
 // group: 1 for a general CSR (one row per group), 2 for the FEM node
 // pattern (rows 2i and 2i+1 share node i's columns; one double2 per slot).
@@ -81,6 +91,7 @@ struct rafem_ctx {
     int trace_on = 0;
     rafem::DevBuf ws_trace;
     rafem::DevBuf ws_flags;     // grid barrier / all-reduce slots
+    rafem::DevBuf ws_simout;    // fused simulation summary
     unsigned epoch = 0;         // per-launch flag epoch
     int last_mode = -1;  // 1: cluster-resident solve, 0: grid-wide cooperative solve
     int last_ctas = 0;
@@ -128,7 +139,7 @@ struct rafem_system {
     rafem_mesh* mesh = nullptr;
     double* val2 = nullptr;   // slots x 2 (V, T)
     double* rhs = nullptr;    // 2N
-    double* sigma = nullptr;  // M
+    double* contrib = nullptr; // M x 16 x (V, T) element block contributions
     double* load = nullptr;   // M x 4 T-rhs element contributions
     double* diagpart = nullptr; // 2 x G partial diag sums
     double* minv = nullptr;   // 2N
@@ -151,6 +162,11 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
                  KResult* res_dev, int* flag_dev, cudaEvent_t ev_start = nullptr,
                  cudaEvent_t ev_stop = nullptr);
 int jacobi_minv(rafem_ctx* ctx, const MatView& A, double* minv_dev, int* flag_dev);
+// fused device-resident simulation (krylov.cu + simulate_dev.cuh); returns
+// RAFEM_ERR_UNSUPPORTED when the system is not eligible (caller falls back)
+int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, double* rec_x_dev,
+                   double* rec_time_dev, double* rec_dt_dev, int* rec_iters_dev, long long rec_cap,
+                   double* final_x_dev, float* ms);
 int krylov_read_history(rafem_ctx* ctx, const KResult& r, double* hist, long long hist_cap,
                         long long* cyc, long long cyc_cap);
 int spmv_launch(rafem_ctx* ctx, const MatView& A, const double* x_dev, double* y_dev);
@@ -166,6 +182,8 @@ int expand_dof_vals(rafem_system* s, double* out_dev);
 int predictor_launch(rafem_ctx* ctx, double* x_it, const double* x_acc, const double* x_prev,
                      int N, int step, double ratio);
 int fill_initial(rafem_ctx* ctx, double* x, int N, double t0);
+struct AsmMesh;
+AsmMesh asm_mesh(const rafem_mesh* m);
 
 // sparse.cu
 int scan_ints(rafem_ctx* ctx, const int* in, int* out, int n);

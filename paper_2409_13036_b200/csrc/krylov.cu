@@ -22,6 +22,7 @@
 // memory, and every CTA re-reduces the G partials in the same fixed order,
 // so all CTAs take identical control decisions and results are bitwise
 // reproducible run to run.
+#include "assembly_dev.cuh"
 #include "common.cuh"
 #include "internal.hpp"
 
@@ -783,15 +784,22 @@ struct SrcCgU {
     }
 };
 
+// Uniform (identical in every CTA) outcome of one PCG solve.
+struct PcgOut {
+    long long total;
+    double rel;
+    int converged;
+    int status;
+};
+
+// The PCG iteration proper, after ||b|| is known.  `co`/`red` are the
+// caller's shared scratch; `par` its partial-buffer parity.
 template <int W, bool PRE, class Mode, class R>
-RF_DEV void pcg_body(const KArgs& a, const R& rows) {
-    __shared__ double red[32 * 8];
-    __shared__ double co[8];
+RF_DEV PcgOut pcg_core(const KArgs& a, const R& rows, Sync<Mode>& sy, double bnorm, double* co, double* red,
+                       int& par) {
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
     const int g0 = a.gpart[cta], g1 = a.gpart[cta + 1];
-    const int lo = W * g0, hi = W * g1;
     const long long pstride = 8LL * G;
-    int par = 0;
     // ping-pong r, w, s (gathered); p and x are owner-only.  Selected with
     // ternaries, not arrays, so nothing is indexed dynamically (no stack).
     auto rb = [&](int i) { return i ? a.z : a.r; };
@@ -799,9 +807,6 @@ RF_DEV void pcg_body(const KArgs& a, const R& rows) {
     auto sb = [&](int i) { return i ? a.q : a.p1; };
     double* p = a.p0;
 
-    Sync<Mode> sy{a};
-    const double bnorm = prologue<Mode>(a, sy, lo, hi, co, red, par, pstride);
-    if (bnorm < 0.0) return;
     long long total = 0, cycles = 0, hlen = 0;
     bool converged = false;
     double rel = INFINITY;
@@ -933,7 +938,20 @@ RF_DEV void pcg_body(const KArgs& a, const R& rows) {
         ++cycles;
         if (status != RAFEM_OK) break;
     }
-    if (cta == 0 && tid == 0) write_result(a.res, total, cycles, hlen, rel, converged, false, status);
+    if (a.res && cta == 0 && tid == 0) write_result(a.res, total, cycles, hlen, rel, converged, false, status);
+    return PcgOut{total, rel, converged ? 1 : 0, status};
+}
+
+template <int W, bool PRE, class Mode, class R>
+RF_DEV void pcg_body(const KArgs& a, const R& rows) {
+    __shared__ double red[32 * 8];
+    __shared__ double co[8];
+    const int g0 = a.gpart[blockIdx.x], g1 = a.gpart[blockIdx.x + 1];
+    int par = 0;
+    Sync<Mode> sy{a};
+    const double bnorm = prologue<Mode>(a, sy, W * g0, W * g1, co, red, par, 8LL * gridDim.x);
+    if (bnorm < 0.0) return;
+    pcg_core<W, PRE, Mode>(a, rows, sy, bnorm, co, red, par);
 }
 
 
@@ -1476,6 +1494,116 @@ int krylov_read_history(rafem_ctx* ctx, const KResult& r, double* hist, long lon
         RF_CUDA_TRY(ctx, cudaMemcpyAsync(cyc, ctx->ws_cyc.p, sizeof(long long) * nc, cudaMemcpyDeviceToHost, ctx->stream));
     }
     RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return RAFEM_OK;
+}
+
+}  // namespace rafem
+
+// ---------------------------------------------------------------------------
+// fused device-resident simulation (simulate_dev.cuh)
+
+#include "simulate_dev.cuh"
+
+namespace rafem {
+
+int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, double* rec_x_dev,
+                   double* rec_time_dev, double* rec_dt_dev, int* rec_iters_dev, long long rec_cap,
+                   double* final_x_dev, float* ms) {
+    rafem_mesh* mesh = s->mesh;
+    rafem_ctx* ctx = mesh->ctx;
+    const int N = mesh->N;
+    if (N == 0 || mesh->M == 0) return RAFEM_ERR_UNSUPPORTED;
+    MatView A;
+    A.rp = mesh->rp;
+    A.col = mesh->col;
+    A.val = s->val2;
+    A.ngroups = N;
+    A.W = 2;
+    A.slots = mesh->slots;
+    A.pattern_id = mesh->id;
+    A.maxdeg = mesh->maxdeg;
+    if (mesh->maxdeg > 32) return RAFEM_ERR_UNSUPPORTED;
+    const bool pre = p->solver.precondition == RAFEM_PRECOND_JACOBI;
+    const void* fn = pre ? (const void*)simulate_kernel<true> : (const void*)simulate_kernel<false>;
+    const int G = std::max(1, std::min(ctx->sm_count, N));
+    PartInfo part;
+    if (A.slots * 20LL > (long long)G * (150 << 10)) return RAFEM_ERR_UNSUPPORTED;
+    if (int rc = partition(ctx, A, G, true, part)) return rc;
+    cudaFuncAttributes fa;
+    RF_CUDA_TRY(ctx, cudaFuncGetAttributes(&fa, fn));
+    const size_t smem = part.max_slice;
+    if (smem + fa.sharedSizeBytes > 227 * 1024) return RAFEM_ERR_UNSUPPORTED;
+    RF_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    RF_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, KT, smem));
+    if (occ < 1 || G > occ * ctx->sm_count) return RAFEM_ERR_UNSUPPORTED;
+
+    const long long n2 = 2LL * N;
+    const long long ldv = (n2 + 31) / 32 * 32;
+    if (int rc = ensure(ctx, ctx->ws_vec, sizeof(double) * (size_t)7 * ldv)) return rc;
+    if (int rc = ensure(ctx, ctx->ws_partial, sizeof(double) * (size_t)2 * 8 * G)) return rc;
+    if (int rc = ensure(ctx, ctx->ws_simout, sizeof(SimDevOut))) return rc;
+    {
+        const size_t fb = sizeof(unsigned long long) * 2 * 8 * (size_t)G;
+        if (ctx->ws_flags.bytes < fb) {
+            if (int rc = ensure(ctx, ctx->ws_flags, fb)) return rc;
+            RF_CUDA_TRY(ctx, cudaMemsetAsync(ctx->ws_flags.p, 0, ctx->ws_flags.bytes, ctx->stream));
+        }
+        ctx->epoch = ctx->epoch % 0xffffu + 1;
+    }
+    double* vec = static_cast<double*>(ctx->ws_vec.p);
+    SimArgs S{};
+    KArgs& a = S.k;
+    a.A = A;
+    a.gpart = part.gpart;
+    a.ldv = ldv;
+    a.minv = pre ? s->minv : nullptr;
+    a.w0 = vec;
+    a.w1 = vec + ldv;
+    a.r = vec + 2 * ldv;
+    a.z = vec + 3 * ldv;
+    a.p0 = vec + 4 * ldv;
+    a.p1 = vec + 5 * ldv;
+    a.q = vec + 6 * ldv;
+    a.partial = static_cast<double*>(ctx->ws_partial.p);
+    a.m = 1;
+    a.tol = p->solver.tolerance;
+    a.cap = p->solver.max_total_iters > 0 ? p->solver.max_total_iters : 10LL * n2;
+    a.flags = static_cast<unsigned long long*>(ctx->ws_flags.p);
+    a.epoch = ctx->epoch;
+    {
+        const int rows_per_cta = (N + G - 1) / G;
+        int team = 1;
+        while (team < 16 && rows_per_cta * team * 2 <= KT) team *= 2;
+        if (const char* env = getenv("RAFEM_TEAM")) team = std::max(1, std::min(32, atoi(env)));
+        a.team = team;
+        ctx->last_team = team;
+    }
+    S.m = asm_mesh(mesh);
+    S.contrib = reinterpret_cast<double2*>(s->contrib);
+    S.load = s->load;
+    S.rhs = s->rhs;
+    S.diag_raw = s->diagpart;
+    S.xs = s->xs;
+    S.final_x = final_x_dev;
+    S.n2 = n2;
+    S.p = *p;
+    S.rec_x = rec_x_dev;
+    S.rec_time = rec_time_dev;
+    S.rec_dt = rec_dt_dev;
+    S.rec_iters = rec_iters_dev;
+    S.rec_cap = rec_cap;
+    S.out = static_cast<SimDevOut*>(ctx->ws_simout.p);
+    void* args[] = {&S};
+    RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fn, dim3(G), dim3(KT), args, smem, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+    ctx->launches++;
+    ctx->last_mode = 2;
+    ctx->last_ctas = G;
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(out, ctx->ws_simout.p, sizeof(SimDevOut), cudaMemcpyDeviceToHost, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ms) cudaEventElapsedTime(ms, ctx->ev0, ctx->ev1);
     return RAFEM_OK;
 }
 

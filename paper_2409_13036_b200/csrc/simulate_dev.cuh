@@ -1,0 +1,261 @@
+// simulate_dev.cuh — the whole adaptive RAFEM simulation in ONE persistent
+// cooperative kernel (included by krylov.cu; uses its solver internals).
+//
+// Reference: run_simulation (fem.py:554-644) around corrector_step
+// (fem.py:463-540), assemble_global (fem.py:325-430) and the Krylov solve.
+// Every CTA owns a contiguous block of node rows (the solver partition) and
+// a contiguous block of elements.  Per corrector pass:
+//   barrier -> element phase (own elements: sigma, 16 (V,T) contributions,
+//   T loads) -> max-reduce PhysicsRange flag -> fill own rows straight into
+//   the CTA's shared-memory matrix slice (warp per row, ascending element
+//   order) -> sum-reduce diagonal sums -> equilibration scale + Dirichlet
+//   elimination + Jacobi inverse diagonal on own rows -> reduce ||b||^2 and
+//   the zero-diagonal flag -> single-reduction PCG on the smem slice ->
+//   max-reduce the corrector delta.
+// The time-step control (predictor, acceptance, dt growth / shrink /
+// halving, StepFailure) is scalar logic every CTA evaluates on identical,
+// deterministically reduced values, so all CTAs take the same branches and
+// the host launches once per simulation.
+#pragma once
+
+namespace rafem {
+
+struct SimArgs {
+    KArgs k;  // solver workspace: partition, vectors, minv, partials, flags, team, tol, cap
+    AsmMesh m;
+    double2* contrib;  // M x 16
+    double* load;      // M x 4
+    double* rhs;       // 2N
+    double* diag_raw;  // 2N
+    double* xs;        // 4 x n2: working dof vectors
+    double* final_x;   // n2: last accepted state
+    long long n2;
+    rafem_sim_params p;
+    double* rec_x;  // device records (rec_cap x n2) or null
+    double* rec_time;
+    double* rec_dt;
+    int* rec_iters;
+    long long rec_cap;
+    SimDevOut* out;
+};
+
+// Max over CTAs of one nonnegative value (exact, order independent).
+template <class Mode>
+RF_DEV double reduce_max1(Sync<Mode>& sy, double v, double* P, double* red) {
+    __shared__ double res;
+    v = block_max(v, red);
+    if (threadIdx.x == 0) P[blockIdx.x] = v;
+    sy.barrier();
+    if (threadIdx.x < 32) {
+        double m = 0.0;
+        for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) m = fmax(m, __ldcg(P + c));
+        m = warp_max(m);
+        if (threadIdx.x == 0) res = m;
+    }
+    __syncthreads();
+    return res;
+}
+
+RF_DEV long long global_ns() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <bool PRE>
+__global__ void __launch_bounds__(KT, 1) simulate_kernel(SimArgs S) {
+    extern __shared__ __align__(16) double sval[];
+    __shared__ double red[32 * 8];
+    __shared__ double co[8];
+    __shared__ FillScratch ws[KT / 32];
+    __shared__ int zflag;
+    const KArgs& a = S.k;
+    const rafem_sim_params& p = S.p;
+    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+    const int warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int g0 = a.gpart[cta], g1 = a.gpart[cta + 1];
+    const int lo = 2 * g0, hi = 2 * g1;
+    const long long n2 = S.n2;
+    const int M = S.m.M;
+    const int e0 = (int)((long long)M * cta / G), e1 = (int)((long long)M * (cta + 1) / G);
+
+    // the pattern slice (columns, row starts) is constant: stage it once
+    const int s0 = __ldg(a.A.rp + g0), ns = __ldg(a.A.rp + g1) - s0;
+    int* scol = reinterpret_cast<int*>(sval + 2LL * ns);
+    int* srp = scol + ((ns + 3) & ~3);
+    for (int g = g0 + tid; g <= g1; g += blockDim.x) srp[g - g0] = __ldg(a.A.rp + g) - s0;
+    for (int s = tid; s < ns; s += blockDim.x) scol[s] = __ldg(a.A.col + s0 + s);
+    if (tid == 0) zflag = 0;
+    __syncthreads();
+    const Rows<2, true, false> rows{srp, scol, sval, g0};
+    double2* sv2 = reinterpret_cast<double2*>(sval);
+
+    Sync<GridMode> sy{a};
+    int par = 0;
+    const long long pstride = 8LL * G;
+    auto P = [&]() { return a.partial + par * pstride; };
+    int iacc = 0, iprev = 1, iit = 2, inew = 3;
+    auto X = [&](int i) { return S.xs + (long long)i * n2; };
+
+    for (int e = lo + tid; e < hi; e += blockDim.x) {  // initial_state (fem.py:170-180)
+        const double v0 = (e & 1) ? p.initial_temp : 0.0;
+        X(iacc)[e] = v0;
+        X(iprev)[e] = v0;
+    }
+
+    double t = 0.0, dt_state = p.dt_init, dt_prev = p.dt_init;
+    long long step = 0, passes = 0, corr = 0, inner = 0, halv = 0, bad = -1;
+    long long asm_ns = 0, sol_ns = 0;
+    int status = RAFEM_OK, failed_step = -1;
+    double failed_dt = 0.0;
+
+    while (t < p.total_time) {
+        if (p.max_steps > 0 && step >= p.max_steps) break;
+        const double remaining = p.total_time - t;
+        const bool final_step = dt_state >= remaining;
+        const double dt = final_step ? remaining : dt_state;
+        const double ratio = dt / dt_prev;
+        for (int e = lo + tid; e < hi; e += blockDim.x) {  // predictor (fem.py:437-449)
+            const double xa = X(iacc)[e];
+            X(iit)[e] = ((e & 1) && step >= 1) ? add(xa, mul(ratio, sub(xa, X(iprev)[e]))) : xa;
+        }
+        bool conv = false, abort_run = false;
+        int iters = 0;
+        for (int it = 1; it <= p.max_corrector_iters; ++it) {
+            iters = it;
+            ++passes;
+            const long long ta = global_ns();
+            sy.barrier();  // the iterate is complete everywhere
+            // ---- element phase (own elements)
+            double badv = 0.0;
+            const AsmFields f{X(iit) + 1, 2, X(iit), 2, X(iacc) + 1, 2, dt};
+            for (int e = e0 + tid; e < e1; e += blockDim.x)
+                if (element_tet(e, S.m, f, S.contrib, S.load)) badv = fmax(badv, (double)(M - e));
+            const double badmax = reduce_max1(sy, badv, P(), red);
+            par ^= 1;
+            if (badmax > 0.0) {  // PhysicsRangeError aborts the run (fem.py:274)
+                bad = M - (long long)badmax;
+                status = RAFEM_ERR_PHYSICS;
+                abort_run = true;
+                break;
+            }
+            // ---- fill own rows into the shared-memory slice
+            for (int i = g0 + warp; i < g1; i += nwarps)
+                fill_node_warp(i, S.m, S.contrib, S.load, sv2 + srp[i - g0], S.rhs, S.diag_raw, ws[warp]);
+            __syncthreads();
+            double dv[2] = {0.0, 0.0};
+            for (int i = g0 + tid; i < g1; i += blockDim.x) {
+                dv[0] = add(dv[0], S.diag_raw[2LL * i]);
+                dv[1] = add(dv[1], S.diag_raw[2LL * i + 1]);
+            }
+            sy.template reduce<2>(dv, 2, P(), co, red);
+            par ^= 1;
+            double scale = 1.0;  // fem.py:390-396
+            if (co[0] > 0.0 && co[1] > 0.0) scale = ldexp(1.0, (int)rint(log2(co[1] / co[0])));
+            // ---- scale + Dirichlet + Jacobi on own rows; x0 = iterate
+            for (int i = g0 + warp; i < g1; i += nwarps)
+                constrain_node_warp(i, S.m, scale, 1, p.applied_voltage, p.boundary_temp, sv2 + srp[i - g0], S.rhs,
+                                    PRE ? const_cast<double*>(a.minv) : nullptr, &zflag);
+            for (int e = lo + tid; e < hi; e += blockDim.x) X(inew)[e] = X(iit)[e];
+            __syncthreads();
+            double bv[2] = {0.0, 0.0};
+            for (int e = lo + tid; e < hi; e += blockDim.x) bv[0] = add(bv[0], mul(S.rhs[e], S.rhs[e]));
+            if (tid == 0) bv[1] = (double)zflag;
+            sy.template reduce<2>(bv, 2, P(), co, red);
+            par ^= 1;
+            if (co[1] > 0.0) {  // ValueError: zero diagonal under Jacobi (solver.py:416-417)
+                status = RAFEM_ERR_INVALID;
+                abort_run = true;
+                break;
+            }
+            const long long tb = global_ns();
+            // ---- solve (single-reduction PCG on the smem slice)
+            const double bnorm = sqrt(co[0]);
+            PcgOut o{0, 0.0, 1, RAFEM_OK};
+            if (bnorm == 0.0) {
+                for (int e = lo + tid; e < hi; e += blockDim.x) X(inew)[e] = 0.0;
+            } else {
+                KArgs kk = a;
+                kk.b = S.rhs;
+                kk.x = X(inew);
+                kk.res = nullptr;
+                o = pcg_core<2, PRE, GridMode>(kk, rows, sy, bnorm, co, red, par);
+            }
+            const long long tc = global_ns();
+            asm_ns += tb - ta;
+            sol_ns += tc - tb;
+            if (o.status == RAFEM_ERR_BREAKDOWN) break;  // SolverError -> step failure (fem.py:511-515)
+            inner += o.total;
+            if (!o.converged) break;  // fem.py:517-524
+            // ---- corrector delta (fem.py:527-528)
+            double dmax = 0.0;
+            for (int e = lo + tid; e < hi; e += blockDim.x) {
+                const double xo = X(iit)[e];
+                const double d = fabs(sub(X(inew)[e], xo)) / fmax(1.0, fabs(xo));
+                dmax = (d > dmax || d != d) ? d : dmax;
+            }
+            const double delta = reduce_max1(sy, dmax, P(), red);
+            par ^= 1;
+            const int tmp = iit;
+            iit = inew;
+            inew = tmp;
+            if (delta < p.corrector_tol) {
+                conv = true;
+                break;
+            }
+        }
+        if (abort_run) break;
+        corr += iters;
+        if (conv) {  // accept (fem.py:603-628)
+            const int old_prev = iprev;
+            iprev = iacc;
+            iacc = iit;
+            iit = old_prev;
+            dt_prev = dt;
+            t = final_step ? p.total_time : t + dt;
+            if (step < S.rec_cap) {
+                if (S.rec_x)
+                    for (int e = lo + tid; e < hi; e += blockDim.x) S.rec_x[step * n2 + e] = X(iacc)[e];
+                if (cta == 0 && tid == 0) {
+                    S.rec_time[step] = t;
+                    S.rec_dt[step] = dt;
+                    S.rec_iters[step] = iters;
+                }
+            }
+            ++step;
+            if (iters <= 5)
+                dt_state = fmin(dt * 1.5, p.dt_max);
+            else if (iters >= 20)
+                dt_state = fmax(dt * 0.75, p.dt_min);
+            else
+                dt_state = dt;
+        } else {
+            if (dt <= p.dt_min) {  // StepFailureError (fem.py:629-631)
+                status = RAFEM_ERR_STEP_FAILURE;
+                failed_step = (int)step;
+                failed_dt = dt;
+                break;
+            }
+            dt_state = fmax(dt * 0.5, p.dt_min);
+            ++halv;
+        }
+    }
+    for (int e = lo + tid; e < hi; e += blockDim.x) S.final_x[e] = X(iacc)[e];
+    if (cta == 0 && tid == 0) {
+        SimDevOut* o = S.out;
+        o->accepted = step;
+        o->corr = corr;
+        o->inner = inner;
+        o->halvings = halv;
+        o->passes = passes;
+        o->t = t;
+        o->status = status;
+        o->failed_step = failed_step;
+        o->failed_dt = failed_dt;
+        o->bad = bad;
+        o->asm_ns = asm_ns;
+        o->solve_ns = sol_ns;
+    }
+}
+
+}  // namespace rafem

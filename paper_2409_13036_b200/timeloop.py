@@ -247,6 +247,10 @@ class DeviceRun:
         rc = nat.lib().rafem_simulate(self.sys.handle, C.byref(p), C.byref(out), est, nat.ptr(rec_step),
                                       nat.ptr(rec_time), nat.ptr(rec_dt), nat.ptr(rec_it),
                                       nat.ptr(rec_x))
+        mode, ctas = C.c_int32(), C.c_int32()
+        nat.lib().rafem_last_solve_mode(nat.context(), C.byref(mode), C.byref(ctas))
+        self.last_mode = {2: "fused-simulation", 1: "cluster", 0: "grid"}.get(mode.value, "none")
+        self.last_ctas = ctas.value
         if rc == nat.ERR_STEP_FAILURE:
             raise StepFailureError(int(out.failed_step), float(out.failed_dt))
         if rc == nat.ERR_PHYSICS:

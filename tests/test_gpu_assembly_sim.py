@@ -259,3 +259,26 @@ def test_time_loop_failure_semantics():
                               SimConfig(total_time=6.0, solver=SolverConfig(backend="gmres",
                                                                             precondition="jacobi")))
     assert [r.dt for r in recs] == list(d["dt"]) and [r.time for r in recs] == list(d["time"])
+
+
+def test_fused_simulation_matches_multi_kernel_loop():
+    """The one-launch simulation kernel and the per-pass kernel loop agree."""
+    import os
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh
+    from paper_2409_13036_b200.timeloop import DeviceRun
+    mesh = generate_box_mesh(15, 15, 16)
+    cfg = SimConfig(total_time=40.0, solver=SolverConfig(backend="pcg", precondition="jacobi"))
+    run = DeviceRun(mesh)
+    fused, sf = run.run(cfg)
+    assert run.last_mode == "fused-simulation"
+    os.environ["RAFEM_NO_FUSED"] = "1"
+    try:
+        loop, sl = DeviceRun(mesh).run(cfg)
+    finally:
+        del os.environ["RAFEM_NO_FUSED"]
+    assert [(r.time, r.dt, r.corrector_iters) for r in fused] == [(r.time, r.dt, r.corrector_iters) for r in loop]
+    assert sf.total_solver_iterations == sl.total_solver_iterations and sf.passes == sl.passes
+    for a, b in zip(fused, loop):
+        assert np.max(np.abs(a.T - b.T)) <= 1e-9 * np.max(np.abs(b.T))
+        assert np.max(np.abs(a.V - b.V)) <= 1e-9 * np.max(np.abs(b.V))
+    _compare_run(fused, golden("run_A40_1e-10"), 1e-6, every_step=False)
