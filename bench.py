@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-c3", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c4", action="store_true")
     return ap.parse_args()
 
 
@@ -345,6 +346,13 @@ def run_ours(args):
             line["spmv_c3"] = c3_leg(hbm_peak, peak_src)
         except Exception as exc:  # noqa: BLE001
             line["spmv_c3"] = {"error": str(exc)[:300]}
+    if not args.no_c4:
+        try:
+            c4 = c4_leg(hbm_peak, peak_src, world, rank, local)
+        except Exception as exc:  # noqa: BLE001
+            c4 = {"error": str(exc)[:300]}
+        if rank == 0:
+            line["sharded_c4"] = c4
     if rank == 0 and not args.no_cpu:
         try:
             smp = cpu_sample(24, {"OPENBLAS_NUM_THREADS": "1", "OMP_NUM_THREADS": "1"})
@@ -380,6 +388,64 @@ def e2e_leg(mesh, mat, args, run_simulation, SimConfig, SolverConfig, world):
     return {"value": summ.accepted_steps * reps / wall, "unit": "steps/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "reps": reps,
             "path": "run_simulation -> assemble_global -> solve (host numpy in/out every pass)"}
+
+
+def c4_leg(hbm_peak, peak_src, world, rank, local):
+    """configs[3]: 16M-dof box, row-block sharded over the job's GPUs (one
+    shard per rank, NCCL halo exchange + scalar all-gathers between the
+    kernel-per-phase PCG phases); a cold solve to 1e-10."""
+    import torch
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh
+    from paper_2409_13036_b200 import _native as nat
+    from paper_2409_13036_b200.shard import ShardComm, ShardedSystem
+    t0 = time.perf_counter()
+    mesh = generate_box_mesh(200, 200, 200)
+    n = mesh.node_count
+    comm = None
+    if world > 1:
+        stream = torch.cuda.ExternalStream(nat.lib().rafem_stream(nat.context()))
+        comm = ShardComm(device_collectives=True, stream=stream)
+    sh = ShardedSystem(mesh, MaterialParams.default(), comm, batch=16)
+    p = sh.plan
+    tt = np.full(n, 37.0)
+    t_ext, v_ext = p.extend(tt), np.zeros(p.n_ext)
+    sh.assemble(t_ext, v_ext, t_ext, 0.5, SimConfig())  # warm
+    setup_s = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    a0 = time.perf_counter()
+    sh.assemble(t_ext, v_ext, t_ext, 0.5, SimConfig())
+    asm_s = time.perf_counter() - a0
+    x0 = np.empty(2 * p.n_own)
+    x0[0::2], x0[1::2] = 0.0, 37.0
+    cfg = SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-10)
+    sh.solve(x0=x0, config=SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-10,
+                                        max_total_iters=20))  # warm (communicators, caches)
+    x, st = sh.solve(x0=x0, config=cfg)
+    dev_ms, wall_ms = float(st.device_ms), st.wall_ns / 1e6
+    slots = sh.dm.slots
+    own_slots = int(sh.dm.dof_row_ptr[2 * p.n_own] // 2)
+    if world > 1:
+        import torch.distributed as dist
+        tt_ = torch.tensor([dev_ms, wall_ms, asm_s], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+        dev_ms, wall_ms, asm_s = (float(v) for v in tt_.tolist())
+        s_ = torch.tensor([own_slots], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(s_)
+        own_slots = int(s_.item())
+    it = st.iterations
+    N = n
+    S = own_slots
+    bytes_it = 20 * S + 4 * (N + 1) + 14 * 16 * N  # KP iteration: SpMV + 7 reads / 5 writes + u gather, w write
+    ach = it * bytes_it / (dev_ms / 1e3) / 1e9 if dev_ms > 0 else 0.0
+    return {"workload": "generate_box_mesh(200,200,200) cold system, 16,000,000 dofs",
+            "shards": world, "partition": "contiguous node-row blocks (x-slabs)",
+            "collectives": "NCCL halo send/recv + per-shard scalar all-gather" if world > 1 else "none (one shard)",
+            "iterations": it, "converged": bool(st.converged), "final_relative_residual": st.final_relative_residual,
+            "solve_device_ms_max_over_ranks": dev_ms, "solve_wall_ms": wall_ms,
+            "us_per_iteration": 1e3 * dev_ms / max(it, 1),
+            "aggregate_GBs": ach, "frac_of_1gpu_peak": ach / hbm_peak / world, "peak_source": peak_src,
+            "bytes_per_iteration": bytes_it, "assembly_s": asm_s, "setup_s": setup_s,
+            "kernel": "kp_spmv_kernel + kp_update_kernel (csrc/shard.cu)"}
 
 
 def c3_leg(hbm_peak, peak_src):

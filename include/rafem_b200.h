@@ -125,7 +125,8 @@ int rafem_device_info(rafem_ctx* ctx, int32_t* sm_count, int32_t* cc_major, int3
 int64_t rafem_kernel_launches(const rafem_ctx* ctx);
 /* the cudaStream_t every library call runs on (for external CUDA events) */
 void* rafem_stream(const rafem_ctx* ctx);
-/* diagnostics: last solve's execution mode (1 cluster-resident, 0 grid-wide)
+/* diagnostics: last solve's execution mode (1 cluster-resident, 0 grid-wide,
+ * 2 fused simulation, 3 grid-wide streaming PCG, 4 kernel-per-phase PCG)
  * and CTA count; per-iteration phase timestamps (SM clock64) of CTA 0 when
  * tracing is on: 8 slots per iteration, returns entries copied */
 int rafem_last_solve_mode(const rafem_ctx* ctx, int32_t* mode, int32_t* ctas);
@@ -199,6 +200,61 @@ int rafem_system_spmv_bench(rafem_system* sys, int32_t reps, double* ms_per_laun
 int rafem_simulate(rafem_system* sys, const rafem_sim_params* p, rafem_sim_summary* out,
                    int64_t rec_cap, int64_t* rec_step, double* rec_time, double* rec_dt,
                    int32_t* rec_iters, double* rec_x);
+
+/* ---- row-block shards and the kernel-per-phase PCG ------
+ *
+ * A shard is a rafem_system assembled on the sub-mesh of the tets touching
+ * its owned nodes, with local node ids [owned (n_owned) | ghosts]; its
+ * first n_owned node rows are complete rows of the global system.  The
+ * reference has no distributed path: these entry points split
+ * assemble_global (fem.py:325-430) at its one global reduction (the
+ * equilibration sums, fem.py:390-400) and solve (solver.py:580-636) at its
+ * dot products, so the caller can put collectives in between. */
+typedef struct rafem_kp rafem_kp;
+
+/* element kernel + slot fill (fem.py:247-388) for the whole sub-mesh;
+ * diag_sums[0..1] = (sum of V, sum of T) diagonal entries of the first
+ * n_owned node rows, the shard's share of fem.py:392-393. */
+int rafem_assemble_partial(rafem_system* sys, const double* t_iter, const double* v_iter,
+                           const double* t_prev, const rafem_assemble_params* p, int64_t n_owned,
+                           double* diag_sums, int64_t* bad_element);
+/* V-row scaling by the all-shard scale (fem.py:394-400) and Dirichlet
+ * elimination (fem.py:402-428). */
+int rafem_assemble_finish(rafem_system* sys, const rafem_assemble_params* p, double scale);
+
+/* PCG over the first n_owned node rows of sys; columns address an
+ * extended vector of n_ext nodes whose ghost tail [n_owned, n_ext) the
+ * caller refreshes (halo exchange) before each SpMV phase. */
+int rafem_kp_create(rafem_system* sys, int64_t n_owned, int64_t n_ext, int32_t nranks, int32_t rank,
+                    rafem_kp** out);
+void rafem_kp_destroy(rafem_kp* kp);
+/* owned node ids whose (V,T) values the neighbours need, in send order */
+int rafem_kp_set_halo(rafem_kp* kp, const int32_t* send_idx, int64_t n_send);
+/* device buffers for the caller's collectives: x and u extended vectors
+ * (double2 per node), packed send buffer, per-shard scalar slots
+ * (nranks x 4 doubles; slot `rank` is written by the library) */
+int rafem_kp_buffers(rafem_kp* kp, void** x_ext, void** u_ext, void** send_buf, void** rank_part);
+/* b (host, 2*n_owned; NULL = the assembled rhs), x0 (host or NULL = 0);
+ * Jacobi setup and the shard's ||b||^2 into its scalar slot */
+int rafem_kp_begin(rafem_kp* kp, const double* b, const double* x0, const rafem_solver_params* p);
+/* asynchronous phase launch (RAFEM_KP_*) */
+#define RAFEM_KP_BNORM_FINISH 0
+#define RAFEM_KP_HEAD 1
+#define RAFEM_KP_SPMV_AFTER_HEAD 2
+#define RAFEM_KP_SPMV 3
+#define RAFEM_KP_UPDATE_FIRST 4
+#define RAFEM_KP_UPDATE 5
+#define RAFEM_KP_PACK_X 6
+#define RAFEM_KP_PACK_U_AFTER_HEAD 7
+#define RAFEM_KP_PACK_U 8
+int rafem_kp_launch(rafem_kp* kp, int32_t phase);
+/* nranks == 1: `iters` SPMV + UPDATE pairs back to back (one iteration each) */
+int rafem_kp_iterate(rafem_kp* kp, int32_t iters);
+/* state (synchronises): flags bit0 done, bit1 need true residual, bit2 converged */
+int rafem_kp_state(rafem_kp* kp, int32_t* flags, int64_t* iterations, double* rel);
+/* owned x (host, 2*n_owned), SolveStats, history; returns the solve status */
+int rafem_kp_finish(rafem_kp* kp, double* x_out, rafem_solve_stats* st, double* hist, int64_t hist_cap,
+                    int64_t* cycle_lens, int64_t cycle_cap);
 
 #ifdef __cplusplus
 }

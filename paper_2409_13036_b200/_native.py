@@ -96,6 +96,17 @@ _SIGS = {
     "rafem_system_spmv": (i32, [vp, vp, vp]),
     "rafem_system_spmv_bench": (i32, [vp, i32, P(f64)]),
     "rafem_simulate": (i32, [vp, P(SimParams), P(SimSummaryC), i64, vp, vp, vp, vp, vp]),
+    "rafem_assemble_partial": (i32, [vp, vp, vp, vp, P(AssembleParams), i64, vp, P(i64)]),
+    "rafem_assemble_finish": (i32, [vp, P(AssembleParams), f64]),
+    "rafem_kp_create": (i32, [vp, i64, i64, i32, i32, P(vp)]),
+    "rafem_kp_destroy": (None, [vp]),
+    "rafem_kp_set_halo": (i32, [vp, vp, i64]),
+    "rafem_kp_buffers": (i32, [vp, P(vp), P(vp), P(vp), P(vp)]),
+    "rafem_kp_begin": (i32, [vp, vp, vp, P(SolverParams)]),
+    "rafem_kp_launch": (i32, [vp, i32]),
+    "rafem_kp_iterate": (i32, [vp, i32]),
+    "rafem_kp_state": (i32, [vp, P(i32), P(i64), P(f64)]),
+    "rafem_kp_finish": (i32, [vp, vp, P(SolveStatsC), vp, i64, vp, i64]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -155,6 +166,14 @@ def last_error() -> str:
 
 def kernel_launches() -> int:
     return int(lib().rafem_kernel_launches(context()))
+
+
+def last_solve_mode() -> tuple[int, int]:
+    """(mode, CTAs) of the last solve: 0 grid, 1 cluster, 2 fused simulation,
+    3 grid-wide streaming PCG, 4 kernel-per-phase PCG (rafem_b200.h)."""
+    mode, ctas = i32(), i32()
+    check(lib().rafem_last_solve_mode(context(), C.byref(mode), C.byref(ctas)), "last_solve_mode")
+    return mode.value, ctas.value
 
 
 def device_info() -> dict:

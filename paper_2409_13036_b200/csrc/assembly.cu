@@ -440,15 +440,16 @@ AsmMesh asm_mesh(const rafem_mesh* m) {
     return a;
 }
 
-int assemble_launch(rafem_system* s, const double* t_it, int ts, const double* v_it, int vs,
-                    const double* t_prev, int ps, const rafem_assemble_params& p,
-                    double* scale_dev, long long* bad_dev) {
+// element + fill kernels: raw (unscaled, unconstrained) values, rhs and the
+// per-row diagonal entries in s->diagpart
+int assemble_fill_launch(rafem_system* s, const double* t_it, int ts, const double* v_it, int vs,
+                         const double* t_prev, int ps, double dt, long long* bad_dev) {
     rafem_mesh* m = s->mesh;
     rafem_ctx* ctx = m->ctx;
     cudaStream_t st = ctx->stream;
     const int N = m->N, M = m->M;
     const AsmMesh am = asm_mesh(m);
-    const AsmFields f{t_it, ts, v_it, vs, t_prev, ps, p.dt};
+    const AsmFields f{t_it, ts, v_it, vs, t_prev, ps, dt};
     double2* contrib = reinterpret_cast<double2*>(s->contrib);
     double2* val2 = reinterpret_cast<double2*>(s->val2);
     RF_CUDA_TRY(ctx, cudaMemsetAsync(bad_dev, 0xff, sizeof(long long), st));
@@ -460,10 +461,43 @@ int assemble_launch(rafem_system* s, const double* t_it, int ts, const double* v
     if (N > 0) {
         const int blocks = (int)(((long long)N * 32 + 255) / 256);
         fill_kernel<<<blocks, 256, 0, st>>>(am, contrib, s->load, val2, s->rhs, s->diagpart);
+        ctx->launches++;
+    }
+    RF_CUDA_TRY(ctx, cudaGetLastError());
+    return RAFEM_OK;
+}
+
+// equilibration by a given (already reduced) scale + Dirichlet elimination
+int assemble_constrain_launch(rafem_system* s, const rafem_assemble_params& p, double scale) {
+    rafem_mesh* m = s->mesh;
+    rafem_ctx* ctx = m->ctx;
+    double* scale_dev = reinterpret_cast<double*>(s->status) + 104;
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(scale_dev, &scale, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    if (m->N > 0) {
+        const int blocks = (int)(((long long)m->N * 32 + 255) / 256);
+        constrain_kernel<<<blocks, 256, 0, ctx->stream>>>(asm_mesh(m), scale_dev, p.apply_constraints,
+                                                          p.applied_voltage, p.boundary_temp,
+                                                          reinterpret_cast<double2*>(s->val2), s->rhs);
+        ctx->launches++;
+    }
+    RF_CUDA_TRY(ctx, cudaGetLastError());
+    return RAFEM_OK;
+}
+
+int assemble_launch(rafem_system* s, const double* t_it, int ts, const double* v_it, int vs,
+                    const double* t_prev, int ps, const rafem_assemble_params& p,
+                    double* scale_dev, long long* bad_dev) {
+    rafem_mesh* m = s->mesh;
+    rafem_ctx* ctx = m->ctx;
+    cudaStream_t st = ctx->stream;
+    const int N = m->N;
+    if (int rc = assemble_fill_launch(s, t_it, ts, v_it, vs, t_prev, ps, p.dt, bad_dev)) return rc;
+    if (N > 0) {
+        const int blocks = (int)(((long long)N * 32 + 255) / 256);
         equil_kernel<<<1, 1024, 0, st>>>(s->diagpart, N, p.equilibrate, scale_dev);
-        constrain_kernel<<<blocks, 256, 0, st>>>(am, scale_dev, p.apply_constraints, p.applied_voltage,
-                                                 p.boundary_temp, val2, s->rhs);
-        ctx->launches += 3;
+        constrain_kernel<<<blocks, 256, 0, st>>>(asm_mesh(m), scale_dev, p.apply_constraints, p.applied_voltage,
+                                                 p.boundary_temp, reinterpret_cast<double2*>(s->val2), s->rhs);
+        ctx->launches += 2;
     } else {
         RF_CUDA_TRY(ctx, cudaMemcpyAsync(scale_dev, &s->scale, sizeof(double), cudaMemcpyHostToDevice, st));
     }

@@ -465,6 +465,7 @@ int rafem_system_create(rafem_mesh* m, rafem_system** out) {
 
 void rafem_system_destroy(rafem_system* s) {
     if (!s) return;
+    if (s->kp) rafem_kp_destroy(s->kp);
     for (void* p : {(void*)s->val2, (void*)s->rhs, (void*)s->contrib, (void*)s->load, (void*)s->diagpart,
                     (void*)s->minv, (void*)s->xin, (void*)s->status, (void*)s->xs})
         if (p) cudaFree(p);
@@ -521,6 +522,9 @@ int rafem_system_solve(rafem_system* s, const double* b, const double* x0, const
                        int64_t cycle_cap) {
     if (!s) return RAFEM_ERR_INVALID;
     rafem_ctx* ctx = s->mesh->ctx;
+    if (int rc = kp_system_solve(s, b, x0, p, x_out, st, hist, hist_cap, cycle_lens, cycle_cap);
+        rc != RAFEM_ERR_UNSUPPORTED)
+        return rc;
     const size_t n2 = 2 * (size_t)s->mesh->N;
     double* bdev = b ? s->xs + 4 * n2 : s->rhs;
     double* xdev = s->xs + 5 * n2;

@@ -85,6 +85,20 @@ RF_DEV void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned lon
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// Same, with an L2 cache-policy hint (e.g. evict_first for data read once).
+RF_DEV void tma_load_1d_hint(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                             unsigned long long policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+RF_DEV unsigned long long l2_policy_evict_first() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 RF_DEV void mbar_wait(unsigned long long* bar, unsigned parity) {
     asm volatile(
         "{\n\t.reg .pred P;\n"

@@ -148,6 +148,7 @@ struct rafem_system {
     double scale = 1.0;
     // native-loop state
     double* xs = nullptr;     // 5 x 2N dof vectors
+    rafem_kp* kp = nullptr;   // kernel-per-phase PCG for very large systems (shard.cu)
 };
 
 // error helpers (capi.cu)
@@ -178,6 +179,14 @@ int mesh_geometry(rafem_mesh* m);
 int assemble_launch(rafem_system* s, const double* t_it, int ts, const double* v_it, int vs,
                     const double* t_prev, int ps, const rafem_assemble_params& p,
                     double* scale_dev, long long* bad_dev);
+// shard.cu: single-shard kernel-per-phase PCG on an assembled system;
+// RAFEM_ERR_UNSUPPORTED when the system is not eligible
+int kp_system_solve(rafem_system* s, const double* b, const double* x0, const rafem_solver_params* p,
+                    double* x_out, rafem_solve_stats* st, double* hist, int64_t hist_cap, int64_t* cycle_lens,
+                    int64_t cycle_cap);
+int assemble_fill_launch(rafem_system* s, const double* t_it, int ts, const double* v_it, int vs,
+                         const double* t_prev, int ps, double dt, long long* bad_dev);
+int assemble_constrain_launch(rafem_system* s, const rafem_assemble_params& p, double scale);
 int expand_dof_vals(rafem_system* s, double* out_dev);
 int predictor_launch(rafem_ctx* ctx, double* x_it, const double* x_acc, const double* x_prev,
                      int N, int step, double ratio);

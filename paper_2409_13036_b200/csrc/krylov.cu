@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -956,6 +957,321 @@ RF_DEV void pcg_body(const KArgs& a, const R& rows) {
 
 
 // ---------------------------------------------------------------------------
+// Streaming PCG for systems far larger than L2 (paired W = 2 layout).
+//
+// At paper scale the solve is barrier-latency bound and the single-barrier
+// form above wins; at >= 1M dofs every iteration is an HBM sweep and the
+// on-the-fly operand of pcg_core (four gathered vectors per slot) makes the
+// SpMV gather-bound.  This variant materialises u = M^-1 r, so each slot
+// gathers ONE double2, and streams the CTA's matrix rows through shared
+// memory with TMA bulk copies (TmaSweep below), one thread per node row,
+// every gather of a row in flight before its left-to-right accumulation.
+// Same Chronopoulos-Gear recurrence, same history / restart / breakdown
+// semantics as pcg_core; two grid barriers per iteration instead of one,
+// which is ~2 % of an iteration at these sizes.
+
+constexpr int KS = 256;  // threads of the streaming kernels (one node row each per tile)
+constexpr int kSweepStages = 2;
+
+// Pipelined sweep over this CTA's node rows [g0, g1) in tiles of KS rows.
+// Tile loads are counted over the kernel's lifetime so the mbarrier
+// phases stay consistent across sweeps; prefetch() issues the next sweep's
+// first tiles early (e.g. before a grid barrier: the matrix is constant).
+struct TmaSweep {
+    const MatView* A;
+    unsigned long long* bar;
+    unsigned char* sm;
+    int bufbytes, valcap;
+    int g0, g1, ntiles;
+    unsigned base;  // tiles consumed before the current sweep
+    bool pending;   // first tiles of the next sweep already issued
+    unsigned long long pol;
+
+    RF_DEV void issue(int j) const {  // tile j of the sweep starting at `base` (thread 0)
+        const unsigned k = base + (unsigned)j;
+        const int b = (int)(k % kSweepStages);
+        const int r0 = g0 + j * KS, r1 = min(g1, r0 + KS);
+        const int s0 = __ldg(A->rp + r0), s1 = __ldg(A->rp + r1);
+        const int sa = s0 & ~3, se = (s1 + 3) & ~3;
+        unsigned char* dst = sm + (size_t)b * bufbytes;
+        const unsigned vb = 16u * (unsigned)(s1 - s0), cb = 4u * (unsigned)(se - sa);
+        mbar_expect_tx(&bar[b], vb + cb);
+        if (vb) tma_load_1d_hint(dst, A->val + 2LL * s0, vb, &bar[b], pol);
+        if (cb) tma_load_1d_hint(dst + (size_t)valcap * 16, A->col + sa, cb, &bar[b], pol);
+    }
+    RF_DEV void prefetch() {
+        if (!pending && threadIdx.x == 0) {
+            fence_proxy_async();
+            for (int j = 0; j < kSweepStages && j < ntiles; ++j) issue(j);
+        }
+        pending = true;
+    }
+    // wait out tiles issued by prefetch() when no sweep follows
+    RF_DEV void drain() {
+        if (pending)
+            for (int j = 0; j < kSweepStages && j < ntiles; ++j) {
+                const unsigned k = base + (unsigned)j;
+                mbar_wait(&bar[k % kSweepStages], (k / kSweepStages) & 1u);
+            }
+        pending = false;
+    }
+    // y = A src over this CTA's rows; epi(g, yV, yT) for every owned row.
+    template <int CH = 16, class Src, class Epi>
+    RF_DEV void run(const Src& src, Epi&& epi) {
+        prefetch();
+        for (int j = 0; j < ntiles; ++j) {
+            const unsigned k = base + (unsigned)j;
+            const int b = (int)(k % kSweepStages);
+            const int r0 = g0 + j * KS, r1 = min(g1, r0 + KS);
+            const int r = r0 + threadIdx.x;
+            int a0 = 0, a1 = 0;
+            if (r < r1) {
+                a0 = __ldg(A->rp + r);
+                a1 = __ldg(A->rp + r + 1);
+            }
+            const int s0 = __ldg(A->rp + r0);
+            const int sa = s0 & ~3;
+            mbar_wait(&bar[b], (k / kSweepStages) & 1u);
+            const double2* sv = reinterpret_cast<const double2*>(sm + (size_t)b * bufbytes);
+            const int* sc = reinterpret_cast<const int*>(sm + (size_t)b * bufbytes + (size_t)valcap * 16);
+            if (r < r1) {
+                double av = 0.0, at = 0.0;
+                for (int s = a0; s < a1; s += CH) {
+                    int c[CH];
+                    double2 xv[CH];
+#pragma unroll
+                    for (int q = 0; q < CH; ++q)
+                        if (s + q < a1) c[q] = sc[s + q - sa];
+#pragma unroll
+                    for (int q = 0; q < CH; ++q)
+                        if (s + q < a1) xv[q] = src.at2(c[q]);
+#pragma unroll
+                    for (int q = 0; q < CH; ++q)
+                        if (s + q < a1) {
+                            const double2 vv = sv[s + q - s0];
+                            av = add(av, mul(vv.x, xv[q].x));
+                            at = add(at, mul(vv.y, xv[q].y));
+                        }
+                }
+                epi(r, av, at);
+            }
+            __syncthreads();  // stage b fully read
+            if (threadIdx.x == 0 && j + kSweepStages < ntiles) {
+                fence_proxy_async();
+                issue(j + kSweepStages);
+            }
+        }
+        base += (unsigned)ntiles;
+        pending = false;
+    }
+};
+
+RF_DEV TmaSweep make_sweep(const MatView& A, unsigned char* sm, unsigned long long* bar, int g0, int g1,
+                           int bufbytes, int valcap) {
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < kSweepStages; ++b) mbar_init(&bar[b], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    TmaSweep t;
+    t.A = &A;
+    t.bar = bar;
+    t.sm = sm;
+    t.bufbytes = bufbytes;
+    t.valcap = valcap;
+    t.g0 = g0;
+    t.g1 = g1;
+    t.ntiles = g1 > g0 ? (g1 - g0 + KS - 1) / KS : 0;
+    t.base = 0;
+    t.pending = false;
+    t.pol = l2_policy_evict_first();
+    return t;
+}
+
+// Gathered operand inside a persistent kernel: coherent L1-cached loads
+// (never ld.global.nc: the vector is rewritten between sweeps).
+struct SrcVec2 {
+    const double* v;
+    RF_DEV double2 at2(int c) const { return __ldca(reinterpret_cast<const double2*>(v) + c); }
+};
+
+// Phase A of pcg_stream_kernel (owner rows, no gathers): p = u + beta p,
+// s = w + beta s, x += alpha p, r -= alpha s, u = M r; partials r.u, r.r
+// into v[0], v[2].  Kept out of line so its U-deep load batches get their
+// own register budget instead of competing with the inlined sweeps.
+template <bool PRE, int U>
+__device__ __noinline__ double2 phase_a(int g0, int g1, bool first, double alpha, double beta,
+                                        double2* __restrict__ x, double2* __restrict__ r, double2* __restrict__ u,
+                                        double2* __restrict__ w, double2* __restrict__ s, double2* __restrict__ p,
+                                        const double2* __restrict__ mv) {
+    const int tid = threadIdx.x;
+    double v[3] = {0.0, 0.0, 0.0};
+    auto M = [&](int g) { return PRE ? __ldg(mv + g) : make_double2(1.0, 1.0); };
+    // U nodes per thread per trip: 7U independent 16-B loads in
+    // flight per thread (one CTA of 256 threads per SM is too few
+    // warps to cover HBM latency one node at a time)
+    for (int gb = g0 + tid; gb < g1; gb += U * KS) {
+        double2 uo[U], wo[U], m[U], po[U], so[U], xo[U], ro[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int g = gb + k * KS;
+            if (g < g1) {
+                uo[k] = u[g];
+                wo[k] = w[g];
+                m[k] = M(g);
+                xo[k] = x[g];
+                ro[k] = r[g];
+                if (!first) {
+                    po[k] = p[g];
+                    so[k] = s[g];
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int g = gb + k * KS;
+            if (g < g1) {
+                double2 pn = uo[k], sn = wo[k];
+                if (!first) {
+                    pn = make_double2(add(uo[k].x, mul(beta, po[k].x)), add(uo[k].y, mul(beta, po[k].y)));
+                    sn = make_double2(add(wo[k].x, mul(beta, so[k].x)), add(wo[k].y, mul(beta, so[k].y)));
+                }
+                x[g] = make_double2(add(xo[k].x, mul(alpha, pn.x)), add(xo[k].y, mul(alpha, pn.y)));
+                const double2 rn =
+                    make_double2(sub(ro[k].x, mul(alpha, sn.x)), sub(ro[k].y, mul(alpha, sn.y)));
+                const double2 un = PRE ? make_double2(mul(m[k].x, rn.x), mul(m[k].y, rn.y)) : rn;
+                p[g] = pn;
+                s[g] = sn;
+                r[g] = rn;
+                u[g] = un;
+                v[0] = add(add(v[0], mul(rn.x, un.x)), mul(rn.y, un.y));
+                v[2] = add(add(v[2], mul(rn.x, rn.x)), mul(rn.y, rn.y));
+            }
+        }
+    }
+    return make_double2(v[0], v[2]);
+}
+
+template <bool PRE, int CH, int U>
+__global__ void __launch_bounds__(KS, 1) pcg_stream_kernel(KArgs a, int bufbytes, int valcap) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    __shared__ __align__(8) unsigned long long bar[kSweepStages];
+    __shared__ double red[32 * 8];
+    __shared__ double co[8];
+    const int cta = blockIdx.x, tid = threadIdx.x;
+    const int g0 = a.gpart[cta], g1 = a.gpart[cta + 1];
+    const long long pstride = 8LL * gridDim.x;
+    int par = 0;
+    Sync<GridMode> sy{a};
+    TmaSweep sw = make_sweep(a.A, dsm, bar, g0, g1, bufbytes, valcap);
+    sw.prefetch();  // overlaps the ||b|| reduction
+    const double bnorm = prologue<GridMode>(a, sy, 2 * g0, 2 * g1, co, red, par, pstride);
+    if (bnorm < 0.0) {
+        sw.drain();  // no bulk copy may outlive the CTA
+        return;
+    }
+    double2* x = reinterpret_cast<double2*>(a.x);
+    const double2* b = reinterpret_cast<const double2*>(a.b);
+    const double2* mv = reinterpret_cast<const double2*>(a.minv);
+    double2* r = reinterpret_cast<double2*>(a.r);
+    double2* u = reinterpret_cast<double2*>(a.z);
+    double2* w = reinterpret_cast<double2*>(a.w0);
+    double2* s = reinterpret_cast<double2*>(a.p1);
+    double2* p = reinterpret_cast<double2*>(a.p0);
+    auto M = [&](int g) { return PRE ? __ldg(mv + g) : make_double2(1.0, 1.0); };
+    auto round = [&](double (&v)[3], int nv) {
+        sy.template reduce<3>(v, nv, a.partial + par * pstride, co, red);
+        par ^= 1;
+    };
+
+    long long total = 0, cycles = 0, hlen = 0;
+    bool converged = false;
+    double rel = INFINITY;
+    int status = RAFEM_OK;
+    while (true) {
+        double gamma, alpha, beta = 0.0;
+        {  // r = b - A x, u = M r ; (r.u, -, r.r)
+            double v[3] = {0.0, 0.0, 0.0};
+            sw.template run<CH>(SrcVec2{a.x}, [&](int g, double yv, double yt) {
+                const double2 bb = b[g], m = M(g);
+                const double2 rr = make_double2(sub(bb.x, yv), sub(bb.y, yt));
+                const double2 uu = PRE ? make_double2(mul(m.x, rr.x), mul(m.y, rr.y)) : rr;
+                r[g] = rr;
+                u[g] = uu;
+                v[0] = add(add(v[0], mul(rr.x, uu.x)), mul(rr.y, uu.y));
+                v[2] = add(add(v[2], mul(rr.x, rr.x)), mul(rr.y, rr.y));
+            });
+            sw.prefetch();
+            round(v, 3);
+        }
+        rel = sqrt(co[2]) / bnorm;
+        if (rel <= a.tol) {
+            converged = true;
+            break;
+        }
+        if (total >= a.cap) break;
+        gamma = co[0];
+        {  // w = A u ; (w.u)
+            double v[3] = {0.0, 0.0, 0.0};
+            sw.template run<CH>(SrcVec2{a.z}, [&](int g, double yv, double yt) {
+                const double2 uu = __ldca(u + g);
+                w[g] = make_double2(yv, yt);
+                v[0] = add(add(v[0], mul(yv, uu.x)), mul(yt, uu.y));
+            });
+            round(v, 1);
+            if (!(gamma > 0.0) || !(co[0] > 0.0) || !isfinite(gamma) || !isfinite(co[0])) {
+                status = RAFEM_ERR_BREAKDOWN;
+                break;
+            }
+            alpha = gamma / co[0];
+        }
+        const long long hstart = hlen;
+        bool first = true;
+        while (true) {
+            double v[3] = {0.0, 0.0, 0.0};
+            // phase A (owner rows): p = u + beta p, s = w + beta s, x += alpha p,
+            // r -= alpha s, u = M r ; partials (r.u, -, r.r)
+            {
+                const double2 pa = phase_a<PRE, U>(g0, g1, first, alpha, beta, x, r, u, w, s, p, mv);
+                v[0] = pa.x;
+                v[2] = pa.y;
+            }
+            sw.prefetch();
+            sy.barrier();
+            // phase B: w = A u ; partial (w.u)
+            sw.template run<CH>(SrcVec2{a.z}, [&](int g, double yv, double yt) {
+                const double2 uu = __ldca(u + g);
+                w[g] = make_double2(yv, yt);
+                v[1] = add(add(v[1], mul(yv, uu.x)), mul(yt, uu.y));
+            });
+            sw.prefetch();
+            round(v, 3);
+            ++total;
+            const double est = sqrt(co[2]) / bnorm;
+            if (cta == 0 && tid == 0 && hlen < a.hist_cap) a.hist[hlen] = est;
+            ++hlen;
+            if (est <= a.tol || total >= a.cap) break;
+            const double gnew = co[0];
+            const double bnew = gnew / gamma;
+            const double den = co[1] - bnew * gnew / alpha;
+            if (!(gnew > 0.0) || !(den > 0.0) || !isfinite(den)) {
+                status = RAFEM_ERR_BREAKDOWN;
+                break;
+            }
+            alpha = gnew / den;
+            beta = bnew;
+            gamma = gnew;
+            first = false;
+        }
+        if (cta == 0 && tid == 0 && cycles < a.cyc_cap) a.cyc[cycles] = hlen - hstart;
+        ++cycles;
+        if (status != RAFEM_OK) break;
+    }
+    sw.drain();
+    if (a.res && cta == 0 && tid == 0) write_result(a.res, total, cycles, hlen, rel, converged, false, status);
+}
+
+// ---------------------------------------------------------------------------
 // kernels
 
 // A CTA's matrix slice staged in shared memory (constant for the solve):
@@ -1144,6 +1460,94 @@ __global__ void __launch_bounds__(256, 1) spmv_tma_kernel(MatView A, const doubl
     }
 }
 
+// Deeper pipeline of the same idea: ST stages of NT-row tiles (one thread
+// per node row), so ST-1 tile loads stay in flight while a tile is summed,
+// and each row issues up to CH operand gathers before its first
+// accumulation (a Kuhn-mesh row has <= 15 slots: one L2 round trip per
+// row instead of one per 4 slots).  The accumulation order is still the
+// row's stored order, left to right, so y stays bit-identical to
+// sparse.py:217-218.  HINT marks the streamed matrix evict-first in L2 so
+// the gathered x keeps its lines.
+template <int NT, int ST, int CH, bool HINT>
+__global__ void __launch_bounds__(NT, 1) spmv_tma_pipe_kernel(MatView A, const double* __restrict__ x,
+                                                              double* __restrict__ y, int valcap, int bufbytes) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ __align__(8) unsigned long long bar[ST];
+    const int N = A.ngroups;
+    const int tiles = (N + NT - 1) / NT;
+    const int mine = tiles > (int)blockIdx.x ? (tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int b = 0; b < ST; ++b) mbar_init(&bar[b], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    unsigned long long pol = 0;
+    if (HINT) pol = l2_policy_evict_first();
+    auto issue = [&](int i) {  // i-th tile of this CTA into stage i % ST
+        const int t = blockIdx.x + i * gridDim.x;
+        const int b = i % ST;
+        const int r0 = t * NT, r1 = min(N, r0 + NT);
+        const int s0 = __ldg(A.rp + r0), s1 = __ldg(A.rp + r1);
+        const int sa = s0 & ~3, se = (s1 + 3) & ~3;
+        unsigned char* base = sm + (size_t)b * bufbytes;
+        const unsigned vb = 16u * (unsigned)(s1 - s0), cb = 4u * (unsigned)(se - sa);
+        mbar_expect_tx(&bar[b], vb + cb);
+        if (HINT) {
+            if (vb) tma_load_1d_hint(base, A.val + 2LL * s0, vb, &bar[b], pol);
+            if (cb) tma_load_1d_hint(base + (size_t)valcap * 16, A.col + sa, cb, &bar[b], pol);
+        } else {
+            if (vb) tma_load_1d(base, A.val + 2LL * s0, vb, &bar[b]);
+            if (cb) tma_load_1d(base + (size_t)valcap * 16, A.col + sa, cb, &bar[b]);
+        }
+    };
+    if (threadIdx.x == 0)
+        for (int i = 0; i < ST && i < mine; ++i) issue(i);
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    for (int i = 0; i < mine; ++i) {
+        const int b = i % ST;
+        const int t = blockIdx.x + i * gridDim.x;
+        const int r0 = t * NT, r1 = min(N, r0 + NT);
+        const int r = r0 + threadIdx.x;
+        int a0 = 0, a1 = 0;
+        if (r < r1) {
+            a0 = __ldg(A.rp + r);
+            a1 = __ldg(A.rp + r + 1);
+        }
+        const int s0 = __ldg(A.rp + r0);
+        const int sa = s0 & ~3;
+        mbar_wait(&bar[b], (unsigned)(i / ST) & 1u);
+        const double2* sv = reinterpret_cast<const double2*>(sm + (size_t)b * bufbytes);
+        const int* sc = reinterpret_cast<const int*>(sm + (size_t)b * bufbytes + (size_t)valcap * 16);
+        if (r < r1) {
+            double av = 0.0, at = 0.0;
+            for (int s = a0; s < a1; s += CH) {
+                int c[CH];
+                double2 xv[CH];
+#pragma unroll
+                for (int j = 0; j < CH; ++j)
+                    if (s + j < a1) c[j] = sc[s + j - sa];
+#pragma unroll
+                for (int j = 0; j < CH; ++j)
+                    if (s + j < a1) xv[j] = __ldg(x2 + c[j]);
+#pragma unroll
+                for (int j = 0; j < CH; ++j)
+                    if (s + j < a1) {
+                        const double2 vv = sv[s + j - s0];
+                        av = add(av, mul(vv.x, xv[j].x));
+                        at = add(at, mul(vv.y, xv[j].y));
+                    }
+            }
+            reinterpret_cast<double2*>(y)[r] = make_double2(av, at);
+        }
+        __syncthreads();  // every thread is done with stage b
+        if (threadIdx.x == 0 && i + ST < mine) {
+            fence_proxy_async();  // generic reads of stage b before the async overwrite
+            issue(i + ST);
+        }
+    }
+}
+
 // delta = max |xn - xo| / max(1, |xo|)  (fem.py:527-528); nonnegative
 // doubles order like their bit patterns, so an integer atomicMax is an
 // exact, order-independent max.
@@ -1176,6 +1580,48 @@ int jacobi_minv(rafem_ctx* ctx, const MatView& A, double* minv_dev, int* flag_de
     return RAFEM_OK;
 }
 
+// Pipelined TMA SpMV launch; RAFEM_ERR_UNSUPPORTED when no configuration
+// fits the row degree (the caller then uses the two-stage kernel).
+// RAFEM_SPMV_CFG="NT,ST,HINT" selects a configuration (tuning only).
+struct PipeCfg {
+    int nt, st, hint;
+    const void* fn;
+};
+template <int NT, int ST, int HINT>
+static PipeCfg pipe_cfg() {
+    return {NT, ST, HINT, (const void*)spmv_tma_pipe_kernel<NT, ST, 16, HINT != 0>};
+}
+static int spmv_pipe_launch(rafem_ctx* ctx, const MatView& A, const double* x_dev, double* y_dev) {
+    static const PipeCfg cfgs[] = {pipe_cfg<256, 2, 1>(), pipe_cfg<128, 5, 1>(), pipe_cfg<128, 4, 1>(),
+                                   pipe_cfg<256, 2, 0>(), pipe_cfg<192, 3, 1>(), pipe_cfg<96, 6, 1>(),
+                                   pipe_cfg<128, 4, 0>(), pipe_cfg<64, 8, 1>()};
+    int want = 0;
+    if (const char* env = getenv("RAFEM_SPMV_CFG")) {
+        int nt = 0, st = 0, hint = 1;
+        if (sscanf(env, "%d,%d,%d", &nt, &st, &hint) >= 2) {
+            want = -1;
+            for (int i = 0; i < (int)(sizeof(cfgs) / sizeof(cfgs[0])); ++i)
+                if (cfgs[i].nt == nt && cfgs[i].st == st && cfgs[i].hint == hint) want = i;
+            if (want < 0) return RAFEM_ERR_UNSUPPORTED;
+        }
+    }
+    const PipeCfg& c = cfgs[want];
+    auto buf_bytes = [&](int t) { return t * A.maxdeg * 16 + ((t * A.maxdeg + 8) * 4 + 15) / 16 * 16; };
+    const size_t smem = (size_t)c.st * buf_bytes(c.nt);
+    if (smem > kSmemBudget) return RAFEM_ERR_UNSUPPORTED;
+    RF_CUDA_TRY(ctx, cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int tiles = (A.ngroups + c.nt - 1) / c.nt;
+    const int grid = std::min(tiles, ctx->sm_count);
+    int valcap = c.nt * A.maxdeg, bufbytes = buf_bytes(c.nt);
+    MatView Av = A;
+    const double* xp = x_dev;
+    double* yp = y_dev;
+    void* args[] = {&Av, &xp, &yp, &valcap, &bufbytes};
+    RF_CUDA_TRY(ctx, cudaLaunchKernel(c.fn, dim3(grid), dim3(c.nt), args, smem, ctx->stream));
+    ctx->launches++;
+    return RAFEM_OK;
+}
+
 static bool streams_matrix(const MatView& A) { return A.slots * (4 + 8LL * A.W) > (48LL << 20); }
 
 int spmv_launch(rafem_ctx* ctx, const MatView& A, const double* x_dev, double* y_dev) {
@@ -1184,6 +1630,7 @@ int spmv_launch(rafem_ctx* ctx, const MatView& A, const double* x_dev, double* y
     const bool stream = streams_matrix(A);
     const char* no_tma = getenv("RAFEM_NO_TMA_SPMV");
     if (A.W == 2 && stream && A.maxdeg > 0 && !(no_tma && no_tma[0] == '1')) {
+        if (int rc = spmv_pipe_launch(ctx, A, x_dev, y_dev); rc != RAFEM_ERR_UNSUPPORTED) return rc;
         int tr = 256;
         // per buffer: tr*maxdeg double2 values + (tr*maxdeg + 8) int32 columns, two buffers
         auto buf_bytes = [&](int t) { return t * A.maxdeg * 16 + ((t * A.maxdeg + 8) * 4 + 15) / 16 * 16; };
@@ -1319,6 +1766,7 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     const void* fn = nullptr;
     size_t smem = 0;
     bool cluster = false, hess_global = false;
+    int stream_buf = 0, stream_valcap = 0;
     PartInfo part;
     int G = 0;
     // Grid mode over every SM is the default: measured on B200 (mesh-B
@@ -1358,7 +1806,37 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
         }
     }
     int ms = stream ? 1 : 0;
-    if (!cluster) {
+    int threads = KT;
+    const char* no_sp = getenv("RAFEM_NO_STREAM_PCG");
+    if (!cluster && !gm && A.W == 2 && stream && A.maxdeg > 0 && p.grid_ctas <= 0 && !(no_sp && no_sp[0] == '1')) {
+        const int bufbytes = KS * A.maxdeg * 16 + ((KS * A.maxdeg + 8) * 4 + 15) / 16 * 16;
+        const size_t need = (size_t)kSweepStages * bufbytes;
+        if (need <= kSmemBudget) {
+            const char* us = getenv("RAFEM_STREAM_U");
+            const int uu = us ? atoi(us) : 4;
+            if (uu == 1)
+                fn = pre ? (const void*)pcg_stream_kernel<true, 12, 1> : (const void*)pcg_stream_kernel<false, 12, 1>;
+            else if (uu == 4)
+                fn = pre ? (const void*)pcg_stream_kernel<true, 12, 4> : (const void*)pcg_stream_kernel<false, 12, 4>;
+            else
+                fn = pre ? (const void*)pcg_stream_kernel<true, 12, 2> : (const void*)pcg_stream_kernel<false, 12, 2>;
+            RF_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+            int occ = 0;
+            RF_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, KS, need));
+            if (occ >= 1) {
+                G = std::max(1, std::min(ctx->sm_count, A.ngroups));
+                if (int rc = partition(ctx, A, G, false, part)) return rc;
+                smem = need;
+                threads = KS;
+                ms = 3;
+                stream_buf = bufbytes;
+                stream_valcap = KS * A.maxdeg;
+            } else {
+                fn = nullptr;
+            }
+        }
+    }
+    if (!cluster && ms != 3) {
         // one CTA per SM (the kernels are register-bound to 1 CTA/SM)
         int want = p.grid_ctas > 0 ? p.grid_ctas : ctx->sm_count;
         want = std::max(1, std::min(want, A.ngroups));
@@ -1455,6 +1933,7 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     }
     if (cluster) smem = (size_t)a.hess_smem * 8 + part.max_slice;
     void* args[] = {&a};
+    void* sargs[] = {&a, &stream_buf, &stream_valcap};
     if (ev_start) RF_CUDA_TRY(ctx, cudaEventRecord(ev_start, ctx->stream));
     if (cluster) {
         cudaLaunchConfig_t cfg{};
@@ -1472,8 +1951,9 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
         RF_CUDA_TRY(ctx, cudaLaunchKernelExC(&cfg, fn, args));
         ctx->last_mode = 1;
     } else {
-        RF_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fn, dim3(G), dim3(KT), args, smem, ctx->stream));
-        ctx->last_mode = 0;
+        RF_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fn, dim3(G), dim3(threads), ms == 3 ? sargs : args, smem,
+                                                     ctx->stream));
+        ctx->last_mode = ms == 3 ? 3 : 0;
     }
     if (ev_stop) RF_CUDA_TRY(ctx, cudaEventRecord(ev_stop, ctx->stream));
     ctx->last_ctas = G;

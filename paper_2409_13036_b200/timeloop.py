@@ -249,7 +249,7 @@ class DeviceRun:
                                       nat.ptr(rec_x))
         mode, ctas = C.c_int32(), C.c_int32()
         nat.lib().rafem_last_solve_mode(nat.context(), C.byref(mode), C.byref(ctas))
-        self.last_mode = {2: "fused-simulation", 1: "cluster", 0: "grid"}.get(mode.value, "none")
+        self.last_mode = {4: "kernel-per-phase-pcg", 3: "grid-streaming-pcg", 2: "fused-simulation", 1: "cluster", 0: "grid"}.get(mode.value, "none")
         self.last_ctas = ctas.value
         if rc == nat.ERR_STEP_FAILURE:
             raise StepFailureError(int(out.failed_step), float(out.failed_dt))

@@ -1,18 +1,19 @@
 #!/bin/bash
-# One gpurun call: smoke, GPU tests, bench, launch list, one ncu --set full capture.
-# Every step has its own timeout.
+# One gpurun call: smoke, GPU tests, bench, launch list, ncu --set full captures.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/nvidia-smi.txt 2>&1
 nproc > gpurun_out/host.txt; lscpu | grep -E 'Model name|^CPU\(s\)' >> gpurun_out/host.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 if [ -z "$SKIP_TESTS" ]; then
-timeout 900 python -m pytest tests -q -m gpu --timeout 300 ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 1200 python -m pytest tests -q -m gpu --timeout 600 ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 fi
 timeout 900 python bench.py --steps 5 --warmup 3 ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 if [ -z "$SKIP_NCU" ]; then
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu > gpurun_out/ncu_ll.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-c4 > gpurun_out/ncu_ll.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:simulate -c 1 -o gpurun_out/prof_simulate -f python scripts/launch_list.py pcg >> gpurun_out/ncu_ll.log 2>&1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:spmv -s 5 -c 1 -o gpurun_out/prof_spmv_c3 -f python scripts/c3_spmv.py >> gpurun_out/ncu_ll.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:spmv_tma -s 5 -c 1 -o gpurun_out/prof_spmv_c3 -f python scripts/c3_spmv.py >> gpurun_out/ncu_ll.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:"kp_spmv|kp_update" -s 10 -c 2 -o gpurun_out/prof_kp_c4 -f python scripts/kp_probe.py >> gpurun_out/ncu_ll.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_kp_c4.csv python scripts/kp_probe.py 200 200 200 20 >> gpurun_out/ncu_ll.log 2>&1
 fi
 echo done > gpurun_out/round_done.txt

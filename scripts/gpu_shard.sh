@@ -1,0 +1,6 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_shard.py -x -q --timeout 600 > gpurun_out/pytest_shard.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_shard.log
+timeout 300 python scripts/solve_tune.py > gpurun_out/solve_tune.txt 2>&1
+timeout 600 python scripts/solve_tune.py 200 200 200 >> gpurun_out/solve_tune.txt 2>&1

@@ -1,0 +1,167 @@
+"""GPU parity of the row-block sharded path.
+
+One GPU is available, so the multi-shard tests run 2-3 processes on
+cuda:0 with host-staged gloo collectives; the device code (sub-mesh
+assembly, kernel-per-phase PCG, halo pack) is the same that runs one
+process per GPU over NCCL.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import rafem_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _hot(n, seed=2409):
+    rng = np.random.default_rng(seed)
+    return 37.0 + rng.uniform(0, 30, n), rng.uniform(0, 25, n)
+
+
+def _sorted_rows(rp, col, val):
+    """Canonical row order (entries sorted by column inside each row)."""
+    c2, v2 = col.copy(), val.copy()
+    for i in range(rp.size - 1):
+        a, b = rp[i], rp[i + 1]
+        k = np.argsort(col[a:b], kind="stable")
+        c2[a:b], v2[a:b] = col[a:b][k], val[a:b][k]
+    return c2, v2
+
+
+def test_single_shard_matches_assemble_global_and_persistent_pcg():
+    from paper_2409_13036_b200 import (MaterialParams, SimConfig, SolverConfig, assemble_global,
+                                       generate_box_mesh, solve)
+    from paper_2409_13036_b200.shard import ShardedSystem
+    mesh = generate_box_mesh(12, 11, 13)
+    n = mesh.node_count
+    t, v = _hot(n)
+    cfg = SimConfig()
+    ref = assemble_global(mesh, MaterialParams.default(), cfg, t, v, t, 0.5)
+    sh = ShardedSystem(mesh, MaterialParams.default())
+    scale = sh.assemble(t, v, t, 0.5, cfg)
+    assert scale == ref.voltage_row_scale
+    rp, gcol, vals = sh.owned_rows()
+    assert np.array_equal(rp, ref.matrix.row_ptr) and np.array_equal(gcol, ref.matrix.col_idx)
+    assert np.array_equal(vals, ref.matrix.vals)
+    assert np.array_equal(sh.rhs(), ref.rhs)
+    x0 = np.empty(2 * n)
+    x0[0::2], x0[1::2] = v, t
+    scfg = SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-10)
+    x, st = sh.solve(x0=x0, config=scfg)
+    a = ref.matrix
+    res = np.linalg.norm(ref.rhs - O.matvec(a.row_ptr, a.col_idx, a.vals, x)) / np.linalg.norm(ref.rhs)
+    assert st.converged and res <= 1e-10
+    assert abs(st.final_relative_residual - res) < 1e-12
+    assert len(st.residual_history) == st.restarts + 1
+    xp, sp = solve(a, ref.rhs, x0=x0, config=scfg)
+    assert abs(st.iterations - sp.iterations) <= max(3, 0.03 * sp.iterations)
+    assert np.max(np.abs(x - xp)) <= 1e-7 * np.max(np.abs(xp))
+    x2, st2 = sh.solve(x0=x0, config=scfg)
+    assert np.array_equal(x, x2) and st.iterations == st2.iterations  # bit-reproducible
+    # exact guess: zero iterations, x0 returned bitwise (solver.py:448-450)
+    x3, st3 = sh.solve(x0=x, config=scfg)
+    assert st3.iterations == 0 and np.array_equal(x3, x)
+    # zero rhs: zero solution
+    x4, st4 = sh.solve(b=np.zeros(2 * n), x0=x0, config=scfg)
+    assert st4.converged and not np.any(x4)
+
+
+def _shard_worker(rank, world, port, dims, out_dir):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh
+        from paper_2409_13036_b200.shard import ShardComm, ShardedSystem
+        mesh = generate_box_mesh(*dims)
+        n = mesh.node_count
+        t, v = _hot(n)
+        comm = ShardComm(device_collectives=False)
+        sh = ShardedSystem(mesh, MaterialParams.default(), comm, batch=8)
+        p = sh.plan
+        scale = sh.assemble(p.extend(t), p.extend(v), p.extend(t), 0.5, SimConfig())
+        rp, gcol, vals = sh.owned_rows()
+        x0 = np.empty(2 * n)
+        x0[0::2], x0[1::2] = v, t
+        cfg = SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-10)
+        x, st = sh.solve(x0=x0[2 * p.lo:2 * p.hi], config=cfg)
+        np.savez(os.path.join(out_dir, f"s{rank}.npz"), x=x, lo=p.lo, hi=p.hi, it=st.iterations,
+                 rel=st.final_relative_residual, conv=st.converged, scale=scale, rp=rp, gcol=gcol, vals=vals,
+                 rhs=sh.rhs())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_assembly_and_pcg_across_processes(tmp_path, world):
+    import torch.multiprocessing as mp
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, assemble_global, generate_box_mesh
+    dims = (14, 9, 10)
+    port = 29100 + (os.getpid() % 500) + 11 * world
+    mp.start_processes(_shard_worker, args=(world, port, dims, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    mesh = generate_box_mesh(*dims)
+    n = mesh.node_count
+    t, v = _hot(n)
+    ref = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, v, t, 0.5)
+    a = ref.matrix
+    x = np.empty(2 * n)
+    its = set()
+    for r in range(world):
+        d = np.load(tmp_path / f"s{r}.npz")
+        lo, hi = int(d["lo"]), int(d["hi"])
+        assert float(d["scale"]) == ref.voltage_row_scale
+        r0, r1 = 2 * lo, 2 * hi
+        g_rp = a.row_ptr[r0:r1 + 1] - a.row_ptr[r0]
+        assert np.array_equal(d["rp"], g_rp)
+        gc, gv = _sorted_rows(g_rp, a.col_idx[a.row_ptr[r0]:a.row_ptr[r1]], a.vals[a.row_ptr[r0]:a.row_ptr[r1]])
+        lc, lv = _sorted_rows(d["rp"], d["gcol"], d["vals"])
+        assert np.array_equal(gc, lc) and np.array_equal(gv, lv)  # owned rows bit-identical
+        assert np.array_equal(d["rhs"], ref.rhs[r0:r1])
+        x[r0:r1] = d["x"]
+        assert bool(d["conv"])
+        its.add(int(d["it"]))
+    assert len(its) == 1
+    res = np.linalg.norm(ref.rhs - O.matvec(a.row_ptr, a.col_idx, a.vals, x)) / np.linalg.norm(ref.rhs)
+    assert res <= 1e-10
+    x0 = np.empty(2 * n)
+    x0[0::2], x0[1::2] = v, t
+    xo, so = O.pcg(a.row_ptr, a.col_idx, a.vals, ref.rhs, x0=x0, tol=1e-10)
+    assert abs(its.pop() - so.iterations) <= max(3, 0.05 * so.iterations)
+    assert np.max(np.abs(x - xo)) <= 1e-7 * np.max(np.abs(xo))
+
+
+def test_system_solve_routes_large_pcg_to_kernel_per_phase():
+    """rafem_system_solve hands PCG on very large systems to the
+    kernel-per-phase engine (forced here with RAFEM_KP=1 on a small box);
+    same contract and solution as the persistent kernel."""
+    from paper_2409_13036_b200 import (MaterialParams, SimConfig, SolverConfig, assemble_global,
+                                       generate_box_mesh, solve)
+    from paper_2409_13036_b200 import _native as nat
+    mesh = generate_box_mesh(30, 30, 30)
+    n = mesh.node_count
+    t, v = _hot(n, seed=4)
+    s = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, v, t, 0.5)
+    x0 = np.empty(2 * n)
+    x0[0::2], x0[1::2] = v, t
+    cfg = SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-10)
+    os.environ["RAFEM_KP"] = "1"
+    try:
+        x, st = solve(s.matrix, s.rhs, x0=x0, config=cfg)
+        assert nat.last_solve_mode()[0] == 4
+    finally:
+        del os.environ["RAFEM_KP"]
+    a = s.matrix
+    res = np.linalg.norm(s.rhs - O.matvec(a.row_ptr, a.col_idx, a.vals, x)) / np.linalg.norm(s.rhs)
+    assert st.converged and res <= 1e-10 and abs(st.final_relative_residual - res) < 1e-12
+    assert sum(len(h) for h in st.residual_history) == st.iterations
+    xp, sp = solve(a, s.rhs, x0=x0, config=cfg)
+    assert nat.last_solve_mode()[0] != 4
+    assert abs(st.iterations - sp.iterations) <= max(3, 0.03 * sp.iterations)
+    assert np.max(np.abs(x - xp)) <= 1e-7 * np.max(np.abs(xp))

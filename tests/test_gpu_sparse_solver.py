@@ -238,3 +238,60 @@ def test_tma_spmv_bitwise_at_1M_dofs():
     a = s.matrix
     assert np.array_equal(y_dev, y_plain)
     assert np.array_equal(y_dev, O.matvec(a.row_ptr, a.col_idx, a.vals, x))
+
+
+def _c3_system(hot: bool):
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, assemble_global, generate_box_mesh
+    mesh = generate_box_mesh(80, 80, 79)
+    n = mesh.node_count
+    if hot:
+        rng = np.random.default_rng(2409)
+        t, v = 37.0 + rng.uniform(0, 30, n), rng.uniform(0, 25, n)
+    else:
+        t, v = np.full(n, 37.0), np.zeros(n)
+    s = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, v, t, 0.5)
+    x0 = np.empty(2 * n)
+    x0[0::2], x0[1::2] = v, t
+    return s, x0
+
+
+def test_tma_spmv_pipeline_configs_bitwise_at_1M_dofs():
+    """Every pipelined streaming-SpMV configuration sums rows left to right."""
+    import os
+    from paper_2409_13036_b200 import spmv
+    s, _ = _c3_system(hot=True)
+    x = np.random.default_rng(6).standard_normal(s.rhs.size)
+    ref = O.matvec(s.matrix.row_ptr, s.matrix.col_idx, s.matrix.vals, x)
+    for cfg in ("256,2,1", "128,4,1", "192,3,1", "1,1,1"):  # 1,1,1: two-stage kernel
+        os.environ["RAFEM_SPMV_CFG"] = cfg
+        try:
+            assert np.array_equal(spmv(s.matrix, x), ref), cfg
+        finally:
+            del os.environ["RAFEM_SPMV_CFG"]
+
+
+@pytest.mark.parametrize("hot", [False, True])
+def test_streaming_pcg_at_1M_dofs(hot):
+    """configs[2]: the TMA-streaming PCG (matrix >> L2) meets the residual
+    contract, agrees with the single-barrier grid PCG, and is bit-reproducible."""
+    import os
+    from paper_2409_13036_b200 import SolverConfig, solve
+    from paper_2409_13036_b200 import _native as nat
+    s, x0 = _c3_system(hot)
+    a, b = s.matrix, s.rhs
+    cfg = SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-10)
+    x, st = solve(a, b, x0=x0, config=cfg)
+    assert nat.last_solve_mode()[0] == 3  # grid-wide streaming PCG
+    res = np.linalg.norm(b - O.matvec(a.row_ptr, a.col_idx, a.vals, x)) / np.linalg.norm(b)
+    assert st.converged and res <= 1e-10
+    assert abs(st.final_relative_residual - res) < 1e-12
+    x2, st2 = solve(a, b, x0=x0, config=cfg)
+    assert np.array_equal(x, x2) and st.iterations == st2.iterations
+    os.environ["RAFEM_NO_STREAM_PCG"] = "1"
+    try:
+        xg, sg = solve(a, b, x0=x0, config=cfg)
+    finally:
+        del os.environ["RAFEM_NO_STREAM_PCG"]
+    assert nat.last_solve_mode()[0] == 0
+    assert abs(st.iterations - sg.iterations) <= max(3, 0.03 * sg.iterations)
+    assert rel_err(x, xg) < 1e-7
