@@ -340,7 +340,8 @@ def run_ours(args):
     }
 
     if rank == 0 and not args.no_e2e:
-        line["e2e"] = e2e_leg(mesh, mat, args, run_simulation, SimConfig, SolverConfig, world)
+        line["e2e"] = e2e_leg(mesh, mat, args, SimConfig, SolverConfig, world)
+        line["e2e_plugin_seam"] = e2e_plugin_leg(mesh, mat, args, run_simulation, SimConfig, SolverConfig, world)
     if rank == 0 and not args.no_c3:
         try:
             line["spmv_c3"] = c3_leg(hbm_peak, peak_src)
@@ -371,8 +372,32 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def e2e_leg(mesh, mat, args, run_simulation, SimConfig, SolverConfig, world):
-    """Same metric through the public plug-in API with host buffers each pass."""
+def e2e_leg(mesh, mat, args, SimConfig, SolverConfig, world):
+    """Same metric end to end through the public whole-simulation API
+    (simulate_device -> rafem_mesh_create + rafem_simulate): every step
+    uploads the host mesh (nodes, tets, regions, Dirichlet kinds) from host
+    memory, runs the symbolic phase, and reads every accepted step's V/T
+    fields back to host arrays."""
+    from paper_2409_13036_b200 import simulate_device
+    cfg = SimConfig(total_time=TOTAL_TIME, solver=SolverConfig(backend=args.backend, precondition="jacobi"))
+    simulate_device(mesh, mat, cfg, cached=False)  # warm
+    reps = max(1, args.steps)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        recs, summ = simulate_device(mesh, mat, cfg, record_fields=True, cached=False)
+    wall = time.perf_counter() - t0
+    N, M = mesh.node_count, mesh.tet_count
+    h2d = 8 * 3 * N + 8 * 4 * M + 4 * M + 2 * N + 5 * 8  # nodes f64, tets i64, region idx i32, dof kinds u8, tables
+    d2h = len(recs) * (16 * N + 8 + 8 + 8 + 4) + 128  # per accepted step: V/T fields, step/time/dt/iters; summary
+    return {"value": int(summ.accepted_steps) * reps / wall, "unit": "steps/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "reps": reps,
+            "path": "simulate_device(cached=False): host mesh -> rafem_mesh_create -> rafem_simulate -> host "
+                    "fields of every accepted step (wall clock)"}
+
+
+def e2e_plugin_leg(mesh, mat, args, run_simulation, SimConfig, SolverConfig, world):
+    """Same metric through the reference's plug-in seam (run_simulation ->
+    assemble_global -> solve) with host numpy buffers every corrector pass."""
     cfg = SimConfig(total_time=TOTAL_TIME, solver=SolverConfig(backend=args.backend, precondition="jacobi"))
     run_simulation(mesh, mat, cfg)  # warm (mesh upload + symbolic phase cached)
     reps = max(1, min(args.steps, 3))

@@ -38,7 +38,7 @@ from . import _native as nat
 from .krylov import KrylovBreakdownError, SolveStats
 
 __all__ = ["ShardPlan", "partition_rows", "build_plan", "ShardComm", "ShardedPCG", "ShardedSystem",
-           "KPDeviceEngine"]
+           "KPDeviceEngine", "ShardedSimulation"]
 
 # phases of rafem_kp_launch (include/rafem_b200.h)
 BNORM_FINISH, HEAD, SPMV_AFTER_HEAD, SPMV, UPDATE_FIRST, UPDATE, PACK_X, PACK_U_AFTER_HEAD, PACK_U = range(9)
@@ -272,6 +272,45 @@ class ShardComm:
             rs, rn = plan.recv[q]
             ext[2 * (n0 + rs):2 * (n0 + rs + rn)].copy_(b.to(ext.device))
         self._sync(ext)
+
+    def exchange_fields(self, plan: ShardPlan, own: np.ndarray) -> np.ndarray:
+        """Owned node values (n_own, k) -> extended (n_ext, k): ghost rows
+        filled from their owners (host arrays; device-staged under NCCL)."""
+        import torch
+        own = np.ascontiguousarray(own, dtype=np.float64)
+        k = own.shape[1] if own.ndim == 2 else 1
+        flat = own.reshape(plan.n_own, k)
+        ext = np.empty((plan.n_ext, k))
+        ext[:plan.n_own] = flat
+        if self.size == 1 or not plan.neighbours:
+            return ext.reshape((plan.n_ext,) + own.shape[1:])
+        dev = torch.device("cuda", torch.cuda.current_device()) if self.device else torch.device("cpu")
+        sends, recvs, ops = [], {}, []
+        for q in plan.neighbours:
+            if q in plan.send and plan.send[q].size:
+                t = torch.from_numpy(np.ascontiguousarray(flat[plan.send[q]])).to(dev)
+                sends.append(t)
+                ops.append(self.dist.P2POp(self.dist.isend, t, q, group=self.group))
+            if q in plan.recv:
+                rs, rn = plan.recv[q]
+                recvs[q] = torch.empty((rn, k), dtype=torch.float64, device=dev)
+                ops.append(self.dist.P2POp(self.dist.irecv, recvs[q], q, group=self.group))
+        if self.device:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+        else:
+            reqs = [(self.dist.isend if op.op is self.dist.isend else self.dist.irecv)(op.tensor, op.peer,
+                                                                                       group=self.group)
+                    for op in ops]
+            for req in reqs:
+                req.wait()
+        for q, t in recvs.items():
+            rs, rn = plan.recv[q]
+            ext[plan.n_own + rs:plan.n_own + rs + rn] = t.cpu().numpy()
+        return ext.reshape((plan.n_ext,) + own.shape[1:])
+
+    def allreduce_max(self, v: float) -> float:
+        return float(np.max(self.allgather_host(np.array([v]))[:, 0])) if self.size > 1 else float(v)
 
     @staticmethod
     def _torch():
@@ -521,3 +560,125 @@ class ShardedSystem:
         p = _params(config, nat.METHOD_PCG)
         cap = int(config.max_total_iters) if config.max_total_iters is not None else 10 * n
         return self.pcg.solve(b, x0, p, min(cap, 1 << 20) + 1)
+
+
+# ---------------------------------------------------------------------------
+# the time loop over shards (configs 4-5: re-assembly every corrector pass)
+
+@dataclass
+class ShardStep:
+    step: int
+    time: float
+    dt: float
+    corrector_iters: int
+    T: np.ndarray | None  # owned node values
+    V: np.ndarray | None
+
+
+@dataclass
+class ShardSummary:
+    accepted_steps: int
+    total_corrector_iters: int
+    total_solver_iterations: int
+    dt_halvings: int
+    final_time: float
+    assemble_s: float
+    solve_s: float
+    wall_s: float
+
+
+class ShardedSimulation:
+    """run_simulation (fem.py:554-644) + corrector_step (fem.py:463-540) with
+    the fields distributed: every rank holds its owned node values, ghosts
+    arrive by halo exchange before each assembly, the corrector delta is an
+    all-reduce max, and every scalar decision (acceptance, dt growth /
+    shrink / halving) is taken on identical global values on all ranks.
+
+    ``system`` is a ShardedSystem (or any object with its ``plan``,
+    ``assemble`` and ``solve``); ``comm`` None means one shard.
+    """
+
+    def __init__(self, system, comm: ShardComm | None = None):
+        self.sys = system
+        self.comm = comm
+        self.plan = system.plan
+
+    def _ext(self, *fields):
+        own = np.stack(fields, axis=1)
+        if self.comm is None:
+            return [own[:, i].copy() for i in range(len(fields))]
+        ext = self.comm.exchange_fields(self.plan, own)
+        return [np.ascontiguousarray(ext[:, i]) for i in range(len(fields))]
+
+    def _max(self, v):
+        return self.comm.allreduce_max(v) if self.comm is not None else float(v)
+
+    def run(self, config, record_fields=False, max_steps=None, sink=None):
+        from .krylov import SolverError
+        from .timeloop import StepFailureError
+        n = self.plan.n_own
+        T = np.full(n, config.initial_temp)
+        V = np.zeros(n)
+        T_prev = T.copy()
+        t, dt_cur, dt_prev, step = 0.0, config.dt_init, config.dt_init, 0
+        corr = inner = halv = 0
+        asm_s = sol_s = 0.0
+        w0 = time.perf_counter()
+        recs = []
+        while t < config.total_time:
+            if max_steps is not None and step >= max_steps:
+                break
+            remaining = config.total_time - t
+            last = dt_cur >= remaining
+            dt = remaining if last else dt_cur
+            t_it = T + (dt / dt_prev) * (T - T_prev) if step >= 1 else T.copy()  # fem.py:445-449
+            v_it = V.copy()
+            x_old = np.empty(2 * n)
+            x_old[0::2], x_old[1::2] = v_it, t_it
+            ok, used = False, 0
+            for it in range(1, config.max_corrector_iters + 1):
+                used = it
+                a0 = time.perf_counter()
+                te, ve, tpe = self._ext(t_it, v_it, T)
+                self.sys.assemble(te, ve, tpe, dt, config)
+                a1 = time.perf_counter()
+                try:
+                    x_new, st = self.sys.solve(x0=x_old, config=config.solver)
+                except SolverError:
+                    break  # step failure (fem.py:511-515)
+                finally:
+                    sol_s += time.perf_counter() - a1
+                    asm_s += a1 - a0
+                inner += st.iterations
+                if not st.converged:
+                    break
+                d = float(np.max(np.abs(x_new - x_old) / np.maximum(1.0, np.abs(x_old)))) if n else 0.0
+                delta = self._max(d)
+                v_it, t_it = x_new[0::2].copy(), x_new[1::2].copy()
+                x_old = x_new
+                if delta < config.corrector_tol:
+                    ok = True
+                    break
+            corr += used
+            if ok:
+                T_prev, T, V = T, t_it, v_it
+                dt_prev = dt
+                t = config.total_time if last else t + dt
+                rec = ShardStep(step, t, dt, used, T.copy() if record_fields else None,
+                                V.copy() if record_fields else None)
+                recs.append(rec)
+                if sink is not None:
+                    sink(rec)
+                step += 1
+                if used <= 5:
+                    dt_cur = min(dt * 1.5, config.dt_max)
+                elif used >= 20:
+                    dt_cur = max(dt * 0.75, config.dt_min)
+                else:
+                    dt_cur = dt
+            else:
+                if dt <= config.dt_min:
+                    raise StepFailureError(step, dt)
+                dt_cur = max(dt * 0.5, config.dt_min)
+                halv += 1
+        return recs, ShardSummary(step, corr, inner, halv, t, asm_s, sol_s, time.perf_counter() - w0)

@@ -221,10 +221,13 @@ def _sim_params(config, record_fields: bool, max_steps: int | None) -> nat.SimPa
 class DeviceRun:
     """Reusable native simulation on one mesh (keeps the device system)."""
 
-    def __init__(self, mesh, material=None):
+    def __init__(self, mesh, material=None, cached: bool = True):
+        from .assembly import DeviceMesh
         self.mesh = mesh
         self.material = material or MaterialParams.default()
-        self.dm = device_mesh(mesh, self.material)
+        # cached=False uploads the mesh and redoes the symbolic phase (a
+        # cold start: what a fresh process or a new mesh costs)
+        self.dm = device_mesh(mesh, self.material) if cached else DeviceMesh(mesh, self.material)
         self.sys = SystemHandle(self.dm)
 
     def run(self, config, sink=None, record_fields=True, max_steps=None, rec_cap=None):
@@ -272,7 +275,7 @@ class DeviceRun:
         return records, out
 
 
-def simulate_device(mesh, material, config, sink=None, record_fields=True, max_steps=None):
+def simulate_device(mesh, material, config, sink=None, record_fields=True, max_steps=None, cached=True):
     """Native run_simulation; returns (records, SimSummaryC)."""
-    return DeviceRun(mesh, material).run(config, sink=sink, record_fields=record_fields,
-                                         max_steps=max_steps)
+    return DeviceRun(mesh, material, cached=cached).run(config, sink=sink, record_fields=record_fields,
+                                                        max_steps=max_steps)

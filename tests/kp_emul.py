@@ -211,3 +211,62 @@ def local_csr(row_ptr, col_idx, vals, plan):
     lc = 2 * g2l[cols // 2] + cols % 2
     assert np.all(lc >= 0), "a column of an owned row is neither owned nor ghost"
     return row_ptr[r0:r1 + 1] - s0, lc, vals[s0:s1].copy()
+
+
+class EmulShardSystem:
+    """Stand-in for ShardedSystem on CPU: oracle assembly of the shard's
+    sub-mesh, global equilibration scale from all-gathered owned-row
+    diagonal sums, NumpyKPEngine + ShardedPCG for the solve."""
+
+    def __init__(self, om, materials, plan, comm, O):
+        self.O, self.om, self.mats, self.plan, self.comm = O, om, materials, plan, comm
+        l2g = plan.local_to_global
+        pos = np.full(om.node_count, -1, dtype=np.int64)
+        pos[l2g] = np.arange(l2g.size)
+        sets = {}
+        for k, v in om.node_sets.items():
+            loc = pos[np.asarray(v)]
+            sets[k] = np.sort(loc[loc >= 0])
+        self.sub = O.OMesh(nodes=om.nodes[l2g], tets=plan.local_tets, regions=om.regions[plan.tet_ids],
+                           node_sets=sets)
+
+    def assemble(self, te, ve, tpe, dt, config):
+        O, p = self.O, self.plan
+        n2 = 2 * p.n_own
+        raw = O.assemble(self.sub, self.mats, config.applied_voltage, config.boundary_temp, te, ve, tpe, dt,
+                         equilibrate=False, apply_constraints=False)
+        d = O.diag_of(raw.row_ptr, raw.col_idx, raw.vals)[:n2]
+        rows = self.comm.allgather_host(np.array([d[0::2].sum(), d[1::2].sum()])) if self.comm else \
+            np.array([[d[0::2].sum(), d[1::2].sum()]])
+        sv, st = 0.0, 0.0
+        for r in range(rows.shape[0]):
+            sv += rows[r, 0]
+            st += rows[r, 1]
+        scale = 2.0 ** round(np.log2(st / sv)) if sv > 0 and st > 0 else 1.0
+        loc = O.assemble(self.sub, self.mats, config.applied_voltage, config.boundary_temp, te, ve, tpe, dt,
+                         equilibrate=False)
+        # scaling by a power of two commutes exactly with the elimination
+        mask, _ = O.dirichlet(self.sub, config.applied_voltage, config.boundary_temp)
+        er = O.row_of_entry(loc.row_ptr)
+        vrow = (er % 2 == 0) & ~mask[er]
+        vals = loc.vals.copy()
+        vals[vrow] *= scale
+        rhs = loc.rhs.copy()
+        rsel = np.zeros(rhs.size, dtype=bool)
+        rsel[0::2] = True
+        rhs[rsel & ~mask] *= scale
+        end = loc.row_ptr[n2]
+        self.rp, self.ci, self.va = loc.row_ptr[:n2 + 1].copy(), loc.col_idx[:end].copy(), vals[:end]
+        self.b = rhs[:n2].copy()
+        return scale
+
+    def solve(self, b=None, x0=None, config=None):
+        from paper_2409_13036_b200 import _native as nat
+        from paper_2409_13036_b200.shard import ShardedPCG
+        p = self.plan
+        eng = NumpyKPEngine(self.rp, self.ci, self.va, p.n_own, p.n_ext, p.nranks, p.rank, p.send_index())
+        prm = nat.SolverParams()
+        prm.method, prm.restart_m, prm.tolerance = 1, 30, config.tolerance
+        prm.max_total_iters = int(config.max_total_iters or 0)
+        prm.precondition = 1 if config.precondition == "jacobi" else 0
+        return ShardedPCG(eng, self.comm, p, batch=8).solve(self.b if b is None else b, x0, prm, 1 << 14)

@@ -153,3 +153,47 @@ def test_sharded_pcg_orchestration_gloo(tmp_path, world):
     xo, so = O.pcg(glob.row_ptr, glob.col_idx, glob.vals, glob.rhs, x0=x0, tol=tol)
     assert abs(its.pop() - so.iterations) <= max(3, 0.05 * so.iterations)
     assert np.max(np.abs(x - xo)) <= 1e-7 * np.max(np.abs(xo))
+
+
+def _sim_worker(rank, world, port, dims, total, out_dir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from kp_emul import EmulShardSystem
+        from paper_2409_13036_b200 import SimConfig, SolverConfig
+        from paper_2409_13036_b200.shard import ShardComm, ShardedSimulation
+        om = O.box_mesh(*dims)
+        n = om.node_count
+        comm = ShardComm(device_collectives=False)
+        plan = build_plan(om.tets, n, partition_rows(om.tets, n, world), rank)
+        sysm = EmulShardSystem(om, {0: O.OMaterial()}, plan, comm, O)
+        cfg = SimConfig(total_time=total, solver=SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-12))
+        recs, summ = ShardedSimulation(sysm, comm).run(cfg, record_fields=True)
+        np.savez(os.path.join(out_dir, f"m{rank}.npz"), lo=plan.lo,
+                 traj=np.array([(r.step, r.time, r.dt, r.corrector_iters) for r in recs]),
+                 T=np.array([r.T for r in recs]), V=np.array([r.V for r in recs]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_time_loop_gloo_matches_oracle_run(tmp_path):
+    """ShardedSimulation over 2 gloo ranks: same trajectory as the oracle's
+    single-process run (fem.py:554-644) and fields within 1e-8 of peak."""
+    import torch.multiprocessing as mp
+    dims, total, world = (7, 6, 8), 12.0, 2
+    port = 28600 + (os.getpid() % 500)
+    mp.start_processes(_sim_worker, args=(world, port, dims, total, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    om = O.box_mesh(*dims)
+    ref = O.run(om, {0: O.OMaterial()}, O.OSim(total_time=total, method="pcg", tolerance=1e-12))
+    parts = [np.load(tmp_path / f"m{r}.npz") for r in range(world)]
+    traj = [tuple(x) for x in parts[0]["traj"]]
+    assert all([tuple(x) for x in p["traj"]] == traj for p in parts)
+    assert traj == [(r.step, r.time, r.dt, r.corrector_iters) for r in ref.records]
+    T = np.concatenate([p["T"] for p in parts], axis=1)
+    V = np.concatenate([p["V"] for p in parts], axis=1)
+    for k, r in enumerate(ref.records):
+        assert np.max(np.abs(T[k] - r.T)) <= 1e-8 * np.max(np.abs(r.T))
+        assert np.max(np.abs(V[k] - r.V)) <= 1e-8 * max(np.max(np.abs(r.V)), 1.0)
