@@ -256,6 +256,41 @@ int rafem_kp_state(rafem_kp* kp, int32_t* flags, int64_t* iterations, double* re
 int rafem_kp_finish(rafem_kp* kp, double* x_out, rafem_solve_stats* st, double* hist, int64_t hist_cap,
                     int64_t* cycle_lens, int64_t cycle_cap);
 
+/* ---- device box mesh (mesh.py:306-375) and field comparison -------------
+ * generate_box_mesh on the device, bit-identical to the host generator:
+ * nodes (numpy.linspace coordinates), Kuhn tets, region 0, Dirichlet kinds
+ * (outer surface T dofs; the electrode columns' V dofs, whose node ids the
+ * caller computes with the same nearest-column rule); then the symbolic
+ * phase.  extent = {x0, x1, y0, y1, z0, z1}.  One material region. */
+int rafem_mesh_create_box(rafem_ctx* ctx, int32_t nx, int32_t ny, int32_t nz, const double* extent,
+                          const int64_t* electrode_pos, int64_t n_pos, const int64_t* electrode_neg,
+                          int64_t n_neg, double k, double rho_c, double sigma0, double alpha, double t_ref,
+                          rafem_mesh** out);
+/* node count (return) and tet count of a device mesh */
+int64_t rafem_mesh_counts(const rafem_mesh* mesh, int64_t* n_tets);
+/* host copies of the device mesh: nodes (3N), tets (4M, int32), dof kinds (2N); any may be NULL */
+int rafem_mesh_download(rafem_mesh* mesh, double* nodes, int32_t* tets, uint8_t* dof_kind);
+/* psnr_series kernels (metrics.py:47-64, 98-166): for each of `steps`
+ * field pairs of n values (ref/test, step-major, host or device memory),
+ * the sum of squared differences and max |ref|, fixed-order reductions */
+int rafem_field_compare(rafem_ctx* ctx, int64_t n, int64_t steps, const double* ref, const double* test,
+                        int32_t on_device, double* sq_err, double* max_abs_ref);
+
+/* ---- streamed records (results.py:59-94 ResultWriter.append per step) ----
+ * rafem_simulate with every accepted step's fields streamed to `fn` WHILE
+ * the simulation runs: the device kernel writes each accepted (V, T) dof
+ * vector into a ring of `ring_slots` device slots and publishes progress
+ * in mapped host memory; a host loop copies published slots out on a side
+ * stream and calls fn(user, step, time, dt, corrector_iters, x) with x the
+ * interleaved 2N dof vector in pinned host memory (valid during the call).
+ * The kernel waits for a free slot, so memory stays bounded at any record
+ * size.  A nonzero return from fn stops the delivery (the run completes)
+ * and the call returns RAFEM_ERR_INVALID. */
+typedef int32_t (*rafem_record_fn)(void* user, int64_t step, double time, double dt, int32_t corrector_iters,
+                                   const double* x);
+int rafem_simulate_stream(rafem_system* sys, const rafem_sim_params* p, rafem_sim_summary* out,
+                          int32_t ring_slots, rafem_record_fn fn, void* user);
+
 #ifdef __cplusplus
 }
 #endif

@@ -69,6 +69,8 @@ class SimSummaryC(C.Structure):
 
 
 P = C.POINTER
+# rafem_record_fn: (user, step, time, dt, corrector_iters, x[2N]) -> status
+RECORD_FN = C.CFUNCTYPE(i32, vp, i64, f64, f64, i32, P(f64))
 _SIGS = {
     "rafem_ctx_create": (i32, [C.c_int, P(vp)]),
     "rafem_ctx_destroy": (None, [vp]),
@@ -96,6 +98,11 @@ _SIGS = {
     "rafem_system_spmv": (i32, [vp, vp, vp]),
     "rafem_system_spmv_bench": (i32, [vp, i32, P(f64)]),
     "rafem_simulate": (i32, [vp, P(SimParams), P(SimSummaryC), i64, vp, vp, vp, vp, vp]),
+    "rafem_mesh_create_box": (i32, [vp, i32, i32, i32, vp, vp, i64, vp, i64, f64, f64, f64, f64, f64, P(vp)]),
+    "rafem_mesh_counts": (i64, [vp, P(i64)]),
+    "rafem_mesh_download": (i32, [vp, vp, vp, vp]),
+    "rafem_field_compare": (i32, [vp, i64, i64, vp, vp, i32, vp, vp]),
+    "rafem_simulate_stream": (i32, [vp, P(SimParams), P(SimSummaryC), i32, vp, vp]),
     "rafem_assemble_partial": (i32, [vp, vp, vp, vp, P(AssembleParams), i64, vp, P(i64)]),
     "rafem_assemble_finish": (i32, [vp, P(AssembleParams), f64]),
     "rafem_kp_create": (i32, [vp, i64, i64, i32, i32, P(vp)]),

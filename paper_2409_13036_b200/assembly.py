@@ -22,7 +22,7 @@ from .csr import DeviceCsrMatrix
 from .krylov import SolverConfig
 
 __all__ = [
-    "AssembledSystem", "MaterialParams", "PhysicsRangeError", "RegionMaterial", "SimConfig",
+    "AssembledSystem", "DeviceMesh", "MaterialParams", "PhysicsRangeError", "RegionMaterial", "SimConfig",
     "assemble_global", "device_mesh",
 ]
 
@@ -126,11 +126,48 @@ class DeviceMesh:
                                  nat.ptr(tab["alpha"]), nat.ptr(tab["t_ref"]), nat.ptr(kind),
                                  C.byref(h))
         nat.check(rc, "mesh setup")
+        self._adopt(h)
+
+    def _adopt(self, h):
+        L = nat.lib()
         self.handle = h
         self._finalizer = weakref.finalize(self, L.rafem_mesh_destroy, h)
         self.slots = int(L.rafem_mesh_slots(h))
         self._pattern = None
         self._pool: list = []
+
+    @classmethod
+    def from_box(cls, nx: int, ny: int, nz: int, material=None, extent=None) -> "DeviceMesh":
+        """generate_box_mesh (mesh.py:306-375) built directly in HBM
+        (rafem_mesh_create_box): no host mesh, no host validation pass."""
+        from .boxmesh import DEFAULT_EXTENT, electrode_nodes
+        material = material or MaterialParams.default()
+        extent = extent or DEFAULT_EXTENT
+        rm = material.for_region(0)
+        pos, neg = electrode_nodes(nx, ny, nz, extent)
+        ext = np.ascontiguousarray([v for ab in extent for v in ab], dtype=np.float64)
+        pos = np.ascontiguousarray(pos, dtype=np.int64)
+        neg = np.ascontiguousarray(neg, dtype=np.int64)
+        h = C.c_void_p()
+        rc = nat.lib().rafem_mesh_create_box(nat.context(), int(nx), int(ny), int(nz), nat.ptr(ext), nat.ptr(pos),
+                                             pos.size, nat.ptr(neg), neg.size, rm.k, rm.rho_c, rm.sigma0, rm.alpha,
+                                             rm.t_ref, C.byref(h))
+        nat.check(rc, "box mesh setup")
+        self = cls.__new__(cls)
+        nt = C.c_int64()
+        self.node_count = int(nat.lib().rafem_mesh_counts(h, C.byref(nt)))
+        self.tet_count = int(nt.value)
+        self.regions_tags = np.zeros(1, dtype=np.int64)
+        self._adopt(h)
+        return self
+
+    def download(self):
+        """(nodes (N, 3) f64, tets (M, 4) int64, dof kinds (2N,) u8) from HBM."""
+        nodes = np.empty((self.node_count, 3))
+        tets = np.empty((self.tet_count, 4), dtype=np.int32)
+        kind = np.empty(2 * self.node_count, dtype=np.uint8)
+        nat.check(nat.lib().rafem_mesh_download(self.handle, nat.ptr(nodes), nat.ptr(tets), nat.ptr(kind)), "download")
+        return nodes, tets.astype(np.int64), kind
 
     def node_pattern(self):
         if self._pattern is None:

@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-__all__ = ["MeshValidationError", "TetMesh", "generate_box_mesh", "REQUIRED_SETS"]
+__all__ = ["MeshValidationError", "TetMesh", "electrode_nodes", "generate_box_mesh", "REQUIRED_SETS"]
 
 GEOM_EPS = 1e-12
 REQUIRED_SETS = ("outer_boundary", "electrode_pos", "electrode_neg")
@@ -103,6 +103,32 @@ def _nearest(coords, target, high):
     return int(hits[-1] if high else hits[0])
 
 
+def electrode_nodes(nx: int, ny: int, nz: int, extent=DEFAULT_EXTENT):
+    """Node ids of the two electrode columns (mesh.py:350-375): nearest grid
+    column to each electrode's (x, y), z within the electrode span."""
+    (x0, x1), (y0, y1), (z0, z1) = extent
+    xs, ys, zs = np.linspace(x0, x1, nx), np.linspace(y0, y1, ny), np.linspace(z0, z1, nz)
+
+    def column(xt):
+        ci = _nearest(xs, xt, xt >= 0.0)
+        cj = _nearest(ys, ELECTRODE_Y, False)
+        ks = np.flatnonzero((zs >= ELECTRODE_Z[0]) & (zs <= ELECTRODE_Z[1]))
+        if ks.size == 0:
+            ks = np.array([_nearest(zs, 0.5 * (ELECTRODE_Z[0] + ELECTRODE_Z[1]), False)])
+        return ci, cj, ks
+
+    ip, jp, kp = column(ELECTRODE_X[0])
+    im, jm, km = column(ELECTRODE_X[1])
+    if ip == im and jp == jm:
+        if ip + 1 < nx:
+            ip += 1
+        else:
+            im -= 1
+    pos = ((ip * ny + jp) * nz + np.asarray(kp)).astype(np.int64)
+    neg = ((im * ny + jm) * nz + np.asarray(km)).astype(np.int64)
+    return pos, neg
+
+
 def generate_box_mesh(nx: int, ny: int, nz: int, extent=DEFAULT_EXTENT) -> TetMesh:
     """Structured box, 6 Kuhn tets per cell (mesh.py:306-375), bit-identical output."""
     if nx < 2 or ny < 2 or nz < 2:
@@ -135,23 +161,7 @@ def generate_box_mesh(nx: int, ny: int, nz: int, extent=DEFAULT_EXTENT) -> TetMe
     surf = (i == 0) | (i == nx - 1) | (j == 0) | (j == ny - 1) | (k == 0) | (k == nz - 1)
     outer = np.flatnonzero(surf.reshape(-1)).astype(np.int64)
 
-    def column(xt):
-        ci = _nearest(xs, xt, xt >= 0.0)
-        cj = _nearest(ys, ELECTRODE_Y, False)
-        ks = np.flatnonzero((zs >= ELECTRODE_Z[0]) & (zs <= ELECTRODE_Z[1]))
-        if ks.size == 0:
-            ks = np.array([_nearest(zs, 0.5 * (ELECTRODE_Z[0] + ELECTRODE_Z[1]), False)])
-        return ci, cj, ks
-
-    ip, jp, kp = column(ELECTRODE_X[0])
-    im, jm, km = column(ELECTRODE_X[1])
-    if ip == im and jp == jm:
-        if ip + 1 < nx:
-            ip += 1
-        else:
-            im -= 1
-    pos = ((ip * ny + jp) * nz + np.asarray(kp)).astype(np.int64)
-    neg = ((im * ny + jm) * nz + np.asarray(km)).astype(np.int64)
+    pos, neg = electrode_nodes(nx, ny, nz, extent)
     return TetMesh(nodes=nodes, tets=tets, regions=np.zeros(tets.shape[0], dtype=np.int64),
                    node_sets={"outer_boundary": outer, "electrode_pos": pos, "electrode_neg": neg},
                    trusted=True)

@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 using namespace rafem;
@@ -570,6 +571,169 @@ int rafem_system_spmv_bench(rafem_system* s, int32_t reps, double* ms_per_launch
 // vectors resident in HBM; the host only reads a 96-byte PassStatus per
 // corrector pass to take the same control decisions the reference takes.
 
+namespace {
+
+// SimulationSummary from the fused kernel's device summary; maps the run's
+// status onto the error taxonomy
+int fused_summary(rafem_ctx* ctx, const SimDevOut& so, std::chrono::steady_clock::time_point t_wall,
+                  rafem_sim_summary* out) {
+    out->accepted_steps = so.accepted;
+    out->total_corrector_iters = so.corr;
+    out->total_solver_iterations = so.inner;
+    out->dt_halvings = so.halvings;
+    out->passes = so.passes;
+    out->final_time = so.t;
+    out->status = so.status;
+    out->failed_step = so.failed_step;
+    out->failed_dt = so.failed_dt;
+    out->bad_element = so.bad;
+    out->assemble_ms = so.asm_ns * 1e-6;
+    out->solve_ms = so.solve_ns * 1e-6;
+    out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_wall).count();
+    if (so.status == RAFEM_ERR_PHYSICS) {
+        char buf[128];
+        std::snprintf(buf, sizeof(buf), "sigma(T) <= 0 in element %lld", (long long)so.bad);
+        return rafem_fail(ctx, so.status, buf);
+    }
+    if (so.status == RAFEM_ERR_STEP_FAILURE) {
+        char buf[160];
+        std::snprintf(buf, sizeof(buf), "step %d failed to converge with dt already at the floor (%g s)",
+                      so.failed_step, so.failed_dt);
+        return rafem_fail(ctx, so.status, buf);
+    }
+    if (so.status == RAFEM_ERR_INVALID)
+        return rafem_fail(ctx, so.status, "Jacobi preconditioning requires a zero-free diagonal");
+    return so.status;
+}
+
+int check_sim(rafem_ctx* ctx, const rafem_sim_params* p) {
+    if (int rc = check_params(ctx, &p->solver)) return rc;
+    if (!(p->total_time > 0.0) || !(p->dt_min > 0.0 && p->dt_min <= p->dt_init && p->dt_init <= p->dt_max) ||
+        !(p->corrector_tol > 0.0) || p->max_corrector_iters < 1)
+        return rafem_fail(ctx, RAFEM_ERR_INVALID, "invalid SimConfig");
+    return RAFEM_OK;
+}
+
+// host side of the record stream: copy each published record out of the
+// device ring on a side stream while the simulation kernel keeps running
+struct StreamPump {
+    rafem_ctx* ctx;
+    cudaStream_t copy;
+    const double* ring;  // device
+    int slots;
+    size_t rec_doubles;  // 2N + 4
+    volatile long long* prog;  // host view
+    volatile long long* cons;
+    double* hbuf;        // pinned, one record
+    rafem_record_fn fn;
+    void* user;
+    int cb_status;
+    long long consumed;
+};
+
+int pump_records(void* u) {
+    StreamPump& P = *static_cast<StreamPump*>(u);
+    const long long n2 = (long long)P.rec_doubles - 4;
+    while (true) {
+        const bool kernel_done = cudaStreamQuery(P.ctx->stream) != cudaErrorNotReady;
+        const long long produced = *P.prog;
+        if (P.consumed >= produced) {
+            if (kernel_done) break;
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
+            continue;
+        }
+        while (P.consumed < produced) {
+            const double* slot = P.ring + (P.consumed % P.slots) * P.rec_doubles;
+            RF_CUDA_TRY(P.ctx, cudaMemcpyAsync(P.hbuf, slot, sizeof(double) * P.rec_doubles, cudaMemcpyDeviceToHost,
+                                               P.copy));
+            RF_CUDA_TRY(P.ctx, cudaStreamSynchronize(P.copy));
+            if (P.cb_status == 0 && P.fn)
+                P.cb_status = P.fn(P.user, P.consumed, P.hbuf[0], P.hbuf[1], (int32_t)P.hbuf[2], P.hbuf + 4);
+            ++P.consumed;
+            *P.cons = P.cb_status ? (1LL << 60) : P.consumed;  // a failed sink releases the kernel
+        }
+        (void)n2;
+    }
+    return RAFEM_OK;
+}
+
+}  // namespace
+
+int rafem_simulate_stream(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary* out, int32_t ring_slots,
+                          rafem_record_fn fn, void* user) {
+    if (!s || !p || !out || ring_slots < 1) return RAFEM_ERR_INVALID;
+    rafem_mesh* m = s->mesh;
+    rafem_ctx* ctx = m->ctx;
+    std::memset(out, 0, sizeof(*out));
+    out->failed_step = -1;
+    out->bad_element = -1;
+    if (int rc = check_sim(ctx, p)) return rc;
+    const auto t_wall = std::chrono::steady_clock::now();
+    const size_t n2 = 2 * (size_t)m->N;
+    const char* nofused = getenv("RAFEM_NO_FUSED");
+    if (p->solver.method == RAFEM_METHOD_PCG && !(nofused && nofused[0] == '1')) {
+        StreamPump P{};
+        P.ctx = ctx;
+        P.slots = ring_slots;
+        P.rec_doubles = n2 + 4;
+        P.fn = fn;
+        P.user = user;
+        double* ring = nullptr;
+        long long* counters = nullptr;  // mapped: [prog, cons]
+        long long* dcounters = nullptr;
+        auto cleanup = [&]() {
+            if (P.copy) cudaStreamDestroy(P.copy);
+            if (ring) cudaFree(ring);
+            if (counters) cudaFreeHost(counters);
+            if (P.hbuf) cudaFreeHost(P.hbuf);
+        };
+        cudaError_t e = cudaMalloc(&ring, sizeof(double) * P.rec_doubles * ring_slots);
+        if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&counters), 2 * sizeof(long long), cudaHostAllocMapped);
+        if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&dcounters), counters, 0);
+        if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&P.hbuf), sizeof(double) * P.rec_doubles, 0);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&P.copy, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            cleanup();
+            return rafem_fail_cuda(ctx, e, "record stream setup", __FILE__, __LINE__);
+        }
+        counters[0] = 0;
+        counters[1] = 0;
+        P.ring = ring;
+        P.prog = counters;
+        P.cons = counters + 1;
+        SimStream ss{ring, ring_slots, dcounters, dcounters + 1, pump_records, &P};
+        SimDevOut so{};
+        float kms = 0.f;
+        const int frc = simulate_fused(s, p, &so, nullptr, nullptr, nullptr, nullptr, 0, s->xs + 5 * n2, &kms, &ss);
+        if (frc == RAFEM_OK && P.consumed < so.accepted) pump_records(&P);  // drain (kernel is done)
+        const int cb = P.cb_status;
+        cleanup();
+        if (frc == RAFEM_OK) {
+            const int rc = fused_summary(ctx, so, t_wall, out);
+            if (cb) return rafem_fail(ctx, RAFEM_ERR_INVALID, "record sink failed");
+            return rc;
+        }
+        if (frc != RAFEM_ERR_UNSUPPORTED) return frc;
+    }
+    // not eligible for the fused kernel: run, then hand the records over
+    const long long cap = std::min<long long>((long long)(2.0 * p->total_time / p->dt_init) + 64,
+                                              std::max<long long>(1, (long long)(8e9 / (8.0 * std::max<size_t>(n2, 1)))));
+    std::vector<int64_t> rs(cap);
+    std::vector<double> rt(cap), rd(cap), rx((size_t)cap * n2);
+    std::vector<int32_t> ri(cap);
+    rafem_sim_params q = *p;
+    q.record_fields = 1;
+    const int rc = rafem_simulate(s, &q, out, cap, rs.data(), rt.data(), rd.data(), ri.data(), rx.data());
+    const long long nrec = std::min<long long>(out->accepted_steps, cap);
+    std::vector<double> rec(n2);
+    for (long long k = 0; k < nrec && fn; ++k)
+        if (fn(user, k, rt[k], rd[k], ri[k], rx.data() + (size_t)k * n2)) {
+            if (rc == RAFEM_OK) return rafem_fail(ctx, RAFEM_ERR_INVALID, "record sink failed");
+            break;
+        }
+    return rc;
+}
+
 int rafem_simulate(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary* out, int64_t rec_cap,
                    int64_t* rec_step, double* rec_time, double* rec_dt, int32_t* rec_iters, double* rec_x) {
     if (!s || !p || !out) return RAFEM_ERR_INVALID;
@@ -578,10 +742,7 @@ int rafem_simulate(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary
     std::memset(out, 0, sizeof(*out));
     out->failed_step = -1;
     out->bad_element = -1;
-    if (int rc = check_params(ctx, &p->solver)) return rc;
-    if (!(p->total_time > 0.0) || !(p->dt_min > 0.0 && p->dt_min <= p->dt_init && p->dt_init <= p->dt_max) ||
-        !(p->corrector_tol > 0.0) || p->max_corrector_iters < 1)
-        return rafem_fail(ctx, RAFEM_ERR_INVALID, "invalid SimConfig");
+    if (int rc = check_sim(ctx, p)) return rc;
     const auto t_wall = std::chrono::steady_clock::now();
     const int N = m->N;
     const size_t n2 = 2 * (size_t)N;
@@ -627,33 +788,7 @@ int rafem_simulate(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary
                 if (d_rx) RF_CUDA_TRY(ctx, cudaMemcpy(rec_x, d_rx, sizeof(double) * n2 * nrec, cudaMemcpyDeviceToHost));
             }
             release();
-            out->accepted_steps = so.accepted;
-            out->total_corrector_iters = so.corr;
-            out->total_solver_iterations = so.inner;
-            out->dt_halvings = so.halvings;
-            out->passes = so.passes;
-            out->final_time = so.t;
-            out->status = so.status;
-            out->failed_step = so.failed_step;
-            out->failed_dt = so.failed_dt;
-            out->bad_element = so.bad;
-            out->assemble_ms = so.asm_ns * 1e-6;
-            out->solve_ms = so.solve_ns * 1e-6;
-            out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_wall).count();
-            if (so.status == RAFEM_ERR_PHYSICS) {
-                char buf[128];
-                std::snprintf(buf, sizeof(buf), "sigma(T) <= 0 in element %lld", (long long)so.bad);
-                return rafem_fail(ctx, so.status, buf);
-            }
-            if (so.status == RAFEM_ERR_STEP_FAILURE) {
-                char buf[160];
-                std::snprintf(buf, sizeof(buf), "step %d failed to converge with dt already at the floor (%g s)",
-                              so.failed_step, so.failed_dt);
-                return rafem_fail(ctx, so.status, buf);
-            }
-            if (so.status == RAFEM_ERR_INVALID)
-                return rafem_fail(ctx, so.status, "Jacobi preconditioning requires a zero-free diagonal");
-            return so.status;
+            return fused_summary(ctx, so, t_wall, out);
         }
         release();
         if (frc != RAFEM_ERR_UNSUPPORTED) return frc;

@@ -163,11 +163,22 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
                  KResult* res_dev, int* flag_dev, cudaEvent_t ev_start = nullptr,
                  cudaEvent_t ev_stop = nullptr);
 int jacobi_minv(rafem_ctx* ctx, const MatView& A, double* minv_dev, int* flag_dev);
+// Record streaming of the fused simulation: the kernel fills a device ring
+// and publishes progress in mapped host memory; `pump` (host) runs right
+// after the launch, consuming records until the kernel is done.
+struct SimStream {
+    double* ring;
+    int slots;
+    volatile long long* prog;  // device view of the mapped counters
+    volatile long long* cons;
+    int (*pump)(void* user);
+    void* user;
+};
 // fused device-resident simulation (krylov.cu + simulate_dev.cuh); returns
 // RAFEM_ERR_UNSUPPORTED when the system is not eligible (caller falls back)
 int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, double* rec_x_dev,
                    double* rec_time_dev, double* rec_dt_dev, int* rec_iters_dev, long long rec_cap,
-                   double* final_x_dev, float* ms);
+                   double* final_x_dev, float* ms, const SimStream* stream = nullptr);
 int krylov_read_history(rafem_ctx* ctx, const KResult& r, double* hist, long long hist_cap,
                         long long* cyc, long long cyc_cap);
 int spmv_launch(rafem_ctx* ctx, const MatView& A, const double* x_dev, double* y_dev);

@@ -1988,7 +1988,7 @@ namespace rafem {
 
 int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, double* rec_x_dev,
                    double* rec_time_dev, double* rec_dt_dev, int* rec_iters_dev, long long rec_cap,
-                   double* final_x_dev, float* ms) {
+                   double* final_x_dev, float* ms, const SimStream* stream) {
     rafem_mesh* mesh = s->mesh;
     rafem_ctx* ctx = mesh->ctx;
     const int N = mesh->N;
@@ -2074,6 +2074,12 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     S.rec_iters = rec_iters_dev;
     S.rec_cap = rec_cap;
     S.out = static_cast<SimDevOut*>(ctx->ws_simout.p);
+    if (stream) {
+        S.ring = stream->ring;
+        S.ring_slots = stream->slots;
+        S.prog = stream->prog;
+        S.cons = stream->cons;
+    }
     void* args[] = {&S};
     RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
     RF_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fn, dim3(G), dim3(KT), args, smem, ctx->stream));
@@ -2081,6 +2087,9 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     ctx->launches++;
     ctx->last_mode = 2;
     ctx->last_ctas = G;
+    if (stream && stream->pump) {  // consume records while the kernel runs
+        if (int rc = stream->pump(stream->user)) return rc;
+    }
     RF_CUDA_TRY(ctx, cudaMemcpyAsync(out, ctx->ws_simout.p, sizeof(SimDevOut), cudaMemcpyDeviceToHost, ctx->stream));
     RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     if (ms) cudaEventElapsedTime(ms, ctx->ev0, ctx->ev1);

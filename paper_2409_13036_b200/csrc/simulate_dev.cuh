@@ -37,6 +37,12 @@ struct SimArgs {
     int* rec_iters;
     long long rec_cap;
     SimDevOut* out;
+    // streamed records (rafem_simulate_stream): ring of ring_slots slots of
+    // (time, dt, iters, pad, 2N dofs); prog / cons live in mapped host memory
+    double* ring;
+    int ring_slots;
+    volatile long long* prog;  // accepted records complete in the ring (kernel writes)
+    volatile long long* cons;  // records the host has consumed (host writes)
 };
 
 // Max over CTAs of one nonnegative value (exact, order independent).
@@ -126,6 +132,10 @@ __global__ void __launch_bounds__(KT, 1) simulate_kernel(SimArgs S) {
             ++passes;
             const long long ta = global_ns();
             sy.barrier();  // the iterate is complete everywhere
+            if (S.ring && cta == 0 && tid == 0 && it == 1) {  // every accepted record is in the ring
+                __threadfence_system();
+                *S.prog = step;
+            }
             // ---- element phase (own elements)
             double badv = 0.0;
             const AsmFields f{X(iit) + 1, 2, X(iit), 2, X(iacc) + 1, 2, dt};
@@ -213,6 +223,24 @@ __global__ void __launch_bounds__(KT, 1) simulate_kernel(SimArgs S) {
             iit = old_prev;
             dt_prev = dt;
             t = final_step ? p.total_time : t + dt;
+            if (S.ring) {  // stream: wait for a free slot, then write this CTA's part
+                if (tid == 0) {
+                    long long spins = 0;
+                    while (step - *S.cons >= S.ring_slots) {
+                        __nanosleep(2000);
+                        if (++spins > (1LL << 31)) asm volatile("trap;");
+                    }
+                }
+                __syncthreads();
+                double* slot = S.ring + (step % S.ring_slots) * (n2 + 4);
+                for (int e = lo + tid; e < hi; e += blockDim.x) slot[4 + e] = X(iacc)[e];
+                if (cta == 0 && tid == 0) {
+                    slot[0] = t;
+                    slot[1] = dt;
+                    slot[2] = (double)iters;
+                    slot[3] = 0.0;
+                }
+            }
             if (step < S.rec_cap) {
                 if (S.rec_x)
                     for (int e = lo + tid; e < hi; e += blockDim.x) S.rec_x[step * n2 + e] = X(iacc)[e];
@@ -241,6 +269,13 @@ __global__ void __launch_bounds__(KT, 1) simulate_kernel(SimArgs S) {
         }
     }
     for (int e = lo + tid; e < hi; e += blockDim.x) S.final_x[e] = X(iacc)[e];
+    if (S.ring) {
+        sy.barrier();  // the last record is complete everywhere
+        if (cta == 0 && tid == 0) {
+            __threadfence_system();
+            *S.prog = step;
+        }
+    }
     if (cta == 0 && tid == 0) {
         SimDevOut* o = S.out;
         o->accepted = step;

@@ -230,6 +230,46 @@ class DeviceRun:
         self.dm = device_mesh(mesh, self.material) if cached else DeviceMesh(mesh, self.material)
         self.sys = SystemHandle(self.dm)
 
+    @classmethod
+    def from_device_mesh(cls, dm, material=None) -> "DeviceRun":
+        """A run on a mesh that only exists in HBM (DeviceMesh.from_box)."""
+        self = cls.__new__(cls)
+        self.mesh = None
+        self.material = material or MaterialParams.default()
+        self.dm = dm
+        self.sys = SystemHandle(dm)
+        return self
+
+    def run_streamed(self, config, sink, max_steps=None, ring_slots=8):
+        """Like run(record_fields=True) but each accepted step's fields reach
+        ``sink`` while the simulation is still running (rafem_simulate_stream:
+        device ring + mapped progress counters, bounded memory)."""
+        N = self.dm.node_count
+        p = _sim_params(config, True, max_steps)
+        out = nat.SimSummaryC()
+        err = []
+
+        def cb(_user, step, t, dt, iters, x):
+            try:
+                xa = np.ctypeslib.as_array(x, shape=(2 * N,))
+                sink(StepRecord(int(step), float(t), float(dt), int(iters), True, xa[1::2].copy(), xa[0::2].copy()))
+                return 0
+            except Exception as exc:  # noqa: BLE001 - surfaced after the run
+                err.append(exc)
+                return 1
+
+        fn = nat.RECORD_FN(cb)
+        rc = nat.lib().rafem_simulate_stream(self.sys.handle, C.byref(p), C.byref(out), int(ring_slots),
+                                             C.cast(fn, C.c_void_p), None)
+        if err:
+            raise err[0]
+        if rc == nat.ERR_STEP_FAILURE:
+            raise StepFailureError(int(out.failed_step), float(out.failed_dt))
+        if rc == nat.ERR_PHYSICS:
+            raise PhysicsRangeError(nat.last_error())
+        nat.check(rc, "simulate_stream")
+        return out
+
     def run(self, config, sink=None, record_fields=True, max_steps=None, rec_cap=None):
         N = self.dm.node_count
         # dt only shrinks on hard steps, so 2 x total/dt_init bounds typical runs;

@@ -202,8 +202,46 @@ def gen_runs(full: bool):
     np.savez_compressed(os.path.join(HERE, "run_b333_6s.npz"), **run_case((3, 3, 3), 6.0, 1e-10))
 
 
+def gen_results():
+    """results.py / metrics.py fixtures: a .rsf written by the reference
+    ResultWriter from seeded records, and psnr_series of two reference
+    runs of the same mesh at different solver tolerances."""
+    from rafem.metrics import psnr_series
+    from rafem.results import ResultWriter, StepRecord, read_result_file
+    rng = np.random.default_rng(1729)
+    n = 17
+    recs = [StepRecord(step=k, time=0.5 * (k + 1) + rng.uniform(), dt=rng.uniform(0.1, 2.0),
+                       corrector_iters=int(rng.integers(1, 9)), converged=True,
+                       T=37.0 + rng.uniform(0, 30, n), V=rng.uniform(0, 25, n)) for k in range(5)]
+    path = os.path.join(HERE, "seeded.rsf")
+    with ResultWriter(path, n) as w:
+        for r in recs:
+            w.append(r)
+    runs = {}
+    for tol in (1e-10, 1e-6):
+        out = os.path.join("/tmp", f"golden_psnr_{tol}.rsf")
+        mesh = generate_box_mesh(5, 4, 6)
+        cfg = SimConfig(total_time=20.0, solver=SolverConfig(backend="gmres", precondition="jacobi", tolerance=tol))
+        with ResultWriter(out, mesh.node_count) as w:
+            run_simulation(mesh, MaterialParams.default(), cfg, sink=w.append)
+        runs[tol] = read_result_file(out)
+    ser = psnr_series(runs[1e-10], runs[1e-6], (1e-5, 1e-12))
+    d = {"psnr_t": ser.psnr_t, "psnr_v": ser.psnr_v, "peak_t": ser.peak_t, "peak_v": ser.peak_v,
+         "control_t": ser.control_t, "control_v": ser.control_v, "steps": ser.steps, "times": ser.times}
+    for tag, run in (("ref", runs[1e-10]), ("test", runs[1e-6])):
+        d[f"{tag}_T"] = np.stack([r.T for r in run.steps])
+        d[f"{tag}_V"] = np.stack([r.V for r in run.steps])
+        d[f"{tag}_time"] = np.array([r.time for r in run.steps])
+        d[f"{tag}_step"] = np.array([r.step for r in run.steps])
+    np.savez_compressed(os.path.join(HERE, "psnr.npz"), **d)
+
+
 if __name__ == "__main__":
+    if "--only-results" in sys.argv:
+        gen_results()
+        sys.exit(0)
     full = "--full" in sys.argv
+    gen_results()
     gen_meshes()
     gen_sparse()
     gen_assembly()
