@@ -378,21 +378,28 @@ def e2e_leg(mesh, mat, args, SimConfig, SolverConfig, world):
     uploads the host mesh (nodes, tets, regions, Dirichlet kinds) from host
     memory, runs the symbolic phase, and reads every accepted step's V/T
     fields back to host arrays."""
-    from paper_2409_13036_b200 import simulate_device
+    from paper_2409_13036_b200.timeloop import DeviceRun
     cfg = SimConfig(total_time=TOTAL_TIME, solver=SolverConfig(backend=args.backend, precondition="jacobi"))
-    simulate_device(mesh, mat, cfg, cached=False)  # warm
+
+    def one():
+        recs = []
+        summ = DeviceRun(mesh, mat, cached=False).run_streamed(cfg, recs.append)
+        return recs, summ
+
+    one()  # warm
     reps = max(1, args.steps)
     t0 = time.perf_counter()
     for _ in range(reps):
-        recs, summ = simulate_device(mesh, mat, cfg, record_fields=True, cached=False)
+        recs, summ = one()
     wall = time.perf_counter() - t0
     N, M = mesh.node_count, mesh.tet_count
     h2d = 8 * 3 * N + 8 * 4 * M + 4 * M + 2 * N + 5 * 8  # nodes f64, tets i64, region idx i32, dof kinds u8, tables
     d2h = len(recs) * (16 * N + 8 + 8 + 8 + 4) + 128  # per accepted step: V/T fields, step/time/dt/iters; summary
     return {"value": int(summ.accepted_steps) * reps / wall, "unit": "steps/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "reps": reps,
-            "path": "simulate_device(cached=False): host mesh -> rafem_mesh_create -> rafem_simulate -> host "
-                    "fields of every accepted step (wall clock)"}
+            "path": "DeviceRun(cached=False).run_streamed: host mesh -> rafem_mesh_create -> "
+                    "rafem_simulate_stream -> host fields of every accepted step, streamed while the kernel runs "
+                    "(wall clock)"}
 
 
 def e2e_plugin_leg(mesh, mat, args, run_simulation, SimConfig, SolverConfig, world):

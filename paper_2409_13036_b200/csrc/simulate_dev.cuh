@@ -132,9 +132,18 @@ __global__ void __launch_bounds__(KT, 1) simulate_kernel(SimArgs S) {
             ++passes;
             const long long ta = global_ns();
             sy.barrier();  // the iterate is complete everywhere
-            if (S.ring && cta == 0 && tid == 0 && it == 1) {  // every accepted record is in the ring
+            if (S.ring && cta == 0 && tid == 0 && it == 1) {
                 __threadfence_system();
-                *S.prog = step;
+                *S.prog = step;  // every accepted record is in the ring
+                // this step's record goes to slot step % slots: one thread waits
+                // until the host has consumed that slot; the element-phase
+                // reduction below holds every other CTA back until it returns,
+                // so no other CTA ever polls host memory
+                long long spins = 0;
+                while (step - *S.cons >= S.ring_slots) {
+                    __nanosleep(2000);
+                    if (++spins > (1LL << 31)) asm volatile("trap;");
+                }
             }
             // ---- element phase (own elements)
             double badv = 0.0;
@@ -223,15 +232,7 @@ __global__ void __launch_bounds__(KT, 1) simulate_kernel(SimArgs S) {
             iit = old_prev;
             dt_prev = dt;
             t = final_step ? p.total_time : t + dt;
-            if (S.ring) {  // stream: wait for a free slot, then write this CTA's part
-                if (tid == 0) {
-                    long long spins = 0;
-                    while (step - *S.cons >= S.ring_slots) {
-                        __nanosleep(2000);
-                        if (++spins > (1LL << 31)) asm volatile("trap;");
-                    }
-                }
-                __syncthreads();
+            if (S.ring) {  // stream: the slot was freed before this step's first barrier
                 double* slot = S.ring + (step % S.ring_slots) * (n2 + 4);
                 for (int e = lo + tid; e < hi; e += blockDim.x) slot[4 + e] = X(iacc)[e];
                 if (cta == 0 && tid == 0) {
