@@ -24,6 +24,8 @@
 #include "common.cuh"
 #include "internal.hpp"
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <vector>
 
@@ -208,6 +210,38 @@ __global__ void adj_fill_kernel(const int* inc_ptr, const unsigned* inc_ea, cons
     }
 }
 
+// Per-slot contributor lists: thread per node row walks its incidences in
+// ascending element order; slot l of the row receives 16 e + 4 a + b for
+// every (element e, local row node a, local column node b) landing on it.
+__global__ void slot_count_kernel(const int* inc_ptr, const unsigned* inc_slot, const int* rp, int N, int* cnt) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    int c[kMaxDeg];
+    const int deg = rp[i + 1] - rp[i];
+    for (int l = 0; l < deg; ++l) c[l] = 0;
+    for (int p = inc_ptr[i]; p < inc_ptr[i + 1]; ++p) {
+        const unsigned pk = inc_slot[p];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) c[(pk >> (8 * b)) & 255u] += 1;
+    }
+    for (int l = 0; l < deg; ++l) cnt[rp[i] + l] = c[l];
+}
+
+__global__ void slot_fill_kernel(const int* inc_ptr, const unsigned* inc_ea, const unsigned* inc_slot,
+                                 const int* rp, int N, const int* slot_ptr, int* slot_src) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    int cur[kMaxDeg];
+    const int s0 = rp[i], deg = rp[i + 1] - s0;
+    for (int l = 0; l < deg; ++l) cur[l] = slot_ptr[s0 + l];
+    for (int p = inc_ptr[i]; p < inc_ptr[i + 1]; ++p) {
+        const unsigned ea = inc_ea[p], pk = inc_slot[p];
+        const int e = (int)(ea & 0x3fffffffu), a = (int)(ea >> 30);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) slot_src[cur[(pk >> (8 * b)) & 255u]++] = 16 * e + 4 * a + b;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // geometry (fem.py:229-244): edges e_k = p_k - p_0, det, inverse by
 // cofactors (column j of E^-1 is the cross product of the other two edges
@@ -274,7 +308,19 @@ __global__ void element_kernel(AsmMesh m, AsmFields f, double2* contrib, double*
     if (element_tet(e, m, f, contrib, load)) atomicMin(bad, (unsigned long long)e);
 }
 
-// 2. slot fill, one warp per node row
+// 2. slot fill: one thread per slot over its contributor list, then one
+//    thread per node row for the T rhs and the raw diagonal
+__global__ void __launch_bounds__(256) fill_slots_kernel(AsmMesh m, const double2* contrib, double2* val2, int S) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < S) val2[s] = fill_slot(s, m, contrib);
+}
+__global__ void __launch_bounds__(256) fill_rows_kernel(AsmMesh m, const double* load, const double2* val2,
+                                                        double* rhs, double* diag_raw) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m.N) fill_node_rhs(i, m, load, val2 + __ldg(m.rp + i), rhs, diag_raw);
+}
+
+// 2'. slot fill, one warp per node row (no contributor lists)
 __global__ void __launch_bounds__(256) fill_kernel(AsmMesh m, const double2* contrib, const double* load,
                                                    double2* val2, double* rhs, double* diag_raw) {
     __shared__ FillScratch ws[8];
@@ -398,6 +444,22 @@ int mesh_symbolic(rafem_mesh* m) {
         ctx->launches++;
     }
     RF_CUDA_TRY(ctx, cudaGetLastError());
+    // slot contributor lists (thread-per-slot fill) when 16 M fits an int
+    if (N > 0 && slots > 0 && 16LL * M < (1LL << 31) && m->maxdeg <= kMaxDeg) {
+        int* scnt = nullptr;
+        RF_CUDA_TRY(ctx, cudaMalloc(&scnt, sizeof(int) * (size_t)slots));
+        RF_CUDA_TRY(ctx, cudaMalloc(&m->slot_ptr, sizeof(int) * ((size_t)slots + 1)));
+        RF_CUDA_TRY(ctx, cudaMalloc(&m->slot_src, sizeof(int) * 16 * (size_t)M));
+        slot_count_kernel<<<(N + 127) / 128, 128, 0, st>>>(m->inc_ptr, m->inc_slot, m->rp, N, scnt);
+        ctx->launches++;
+        if (int rc = scan_ints(ctx, scnt, m->slot_ptr, slots)) return rc;
+        slot_fill_kernel<<<(N + 127) / 128, 128, 0, st>>>(m->inc_ptr, m->inc_ea, m->inc_slot, m->rp, N, m->slot_ptr,
+                                                          m->slot_src);
+        ctx->launches++;
+        RF_CUDA_TRY(ctx, cudaGetLastError());
+        RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+        cudaFree(scnt);
+    }
     RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
     cudaFree(cnt);
     cudaFree(cursor);
@@ -435,6 +497,8 @@ AsmMesh asm_mesh(const rafem_mesh* m) {
     a.inc_ea = m->inc_ea;
     a.inc_slot = m->inc_slot;
     a.kind = m->kind;
+    a.slot_ptr = m->slot_ptr;
+    a.slot_src = m->slot_src;
     a.N = m->N;
     a.M = m->M;
     return a;
@@ -459,9 +523,17 @@ int assemble_fill_launch(rafem_system* s, const double* t_it, int ts, const doub
         ctx->launches++;
     }
     if (N > 0) {
-        const int blocks = (int)(((long long)N * 32 + 255) / 256);
-        fill_kernel<<<blocks, 256, 0, st>>>(am, contrib, s->load, val2, s->rhs, s->diagpart);
-        ctx->launches++;
+        const char* wf = getenv("RAFEM_WARP_FILL");
+        if (am.slot_src && !(wf && wf[0] == '1')) {
+            const int S = (int)m->slots;
+            fill_slots_kernel<<<(S + 255) / 256, 256, 0, st>>>(am, contrib, val2, S);
+            fill_rows_kernel<<<(N + 255) / 256, 256, 0, st>>>(am, s->load, val2, s->rhs, s->diagpart);
+            ctx->launches += 2;
+        } else {
+            const int blocks = (int)(((long long)N * 32 + 255) / 256);
+            fill_kernel<<<blocks, 256, 0, st>>>(am, contrib, s->load, val2, s->rhs, s->diagpart);
+            ctx->launches++;
+        }
     }
     RF_CUDA_TRY(ctx, cudaGetLastError());
     return RAFEM_OK;

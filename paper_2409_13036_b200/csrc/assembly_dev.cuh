@@ -32,6 +32,8 @@ struct AsmMesh {
     const unsigned* inc_ea;   // tet | local << 30, ascending tet per node
     const unsigned* inc_slot; // 4 x uint8 row offsets
     const uint8_t* kind;  // 2N dof kinds
+    const int* slot_ptr;  // S + 1: per-slot contributor lists (null: warp fill)
+    const int* slot_src;  // 16 M: contrib index 16 e + 4 a + b, ascending e per slot
     int N, M;
 };
 
@@ -177,6 +179,54 @@ RF_DEV void fill_node_warp(int i, const AsmMesh& m, const double2* contrib, cons
     }
 }
 
+// Slot s: sum of its contributions in ascending element order (the
+// reference's duplicate-summation order, fem.py:381-387 + sparse.py:180-190),
+// every load of the list issued before the first add.  Same bits as
+// fill_node_warp, one thread per slot.
+RF_DEV double2 fill_slot(int s, const AsmMesh& m, const double2* __restrict__ contrib) {
+    const int k0 = __ldg(m.slot_ptr + s), k1 = __ldg(m.slot_ptr + s + 1);
+    double av = 0.0, at = 0.0;
+    for (int k = k0; k < k1; k += 8) {
+        double2 c[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (k + j < k1) c[j] = __ldcg(contrib + __ldg(m.slot_src + k + j));
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (k + j < k1) {
+                av = add(av, c[j].x);
+                at = add(at, c[j].y);
+            }
+    }
+    return make_double2(av, at);
+}
+
+// Node i after its slots are filled: T rhs = sum of the incident element
+// loads in ascending element order (fem.py:388), V rhs 0, raw diagonal.
+RF_DEV void fill_node_rhs(int i, const AsmMesh& m, const double* __restrict__ load, const double2* row,
+                          double* rhs, double* diag_raw) {
+    const int p0 = __ldg(m.inc_ptr + i), p1 = __ldg(m.inc_ptr + i + 1);
+    double racc = 0.0;
+    for (int p = p0; p < p1; p += 8) {
+        double l[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (p + j < p1) {
+                const unsigned ea = __ldg(m.inc_ea + p + j);
+                l[j] = __ldcg(load + 4LL * (ea & 0x3fffffffu) + (ea >> 30));
+            }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (p + j < p1) racc = add(racc, l[j]);
+    }
+    rhs[2LL * i] = 0.0;
+    rhs[2LL * i + 1] = racc;
+    const int d = __ldg(m.diag + i);
+    const double2 dv = d >= 0 ? row[d] : make_double2(0.0, 0.0);
+    diag_raw[2LL * i] = dv.x;
+    diag_raw[2LL * i + 1] = dv.y;
+}
+
 RF_DEV double dof_value(int kind, double applied, double btemp) {
     return kind == RAFEM_DOF_APPLIED_VOLTAGE ? applied : (kind == RAFEM_DOF_BOUNDARY_TEMP ? btemp : 0.0);
 }
@@ -185,9 +235,11 @@ RF_DEV double dof_value(int kind, double applied, double btemp) {
 // elimination keeping the explicit zeros (fem.py:398-428), in place on the
 // row's slots; optional Jacobi inverse diagonal of the final row.
 RF_DEV void constrain_node_warp(int i, const AsmMesh& m, double scale, int apply, double applied, double btemp,
-                                double2* vals, double* rhs, double* minv, int* zero_diag) {
+                                double2* vals, double* rhs, double* minv, int* zero_diag,
+                                const int* cols = nullptr) {
     const int lane = threadIdx.x & 31;
     const int s0 = __ldg(m.rp + i), deg = __ldg(m.rp + i + 1) - s0;
+    if (!cols) cols = m.col + s0;
     const int kV = apply ? m.kind[2LL * i] : 0, kT = apply ? m.kind[2LL * i + 1] : 0;
     const int dslot = __ldg(m.diag + i);
     double mV = 0.0, mT = 0.0;  // moved-column sums in storage order (fem.py:419-424)
@@ -197,7 +249,7 @@ RF_DEV void constrain_node_warp(int i, const AsmMesh& m, double scale, int apply
         double termV = 0.0, termT = 0.0;
         int movV = 0, movT = 0;
         if (l < deg) {
-            const int j = __ldg(m.col + s0 + l);
+            const int j = cols[l];
             const int cV = apply ? m.kind[2LL * j] : 0, cT = apply ? m.kind[2LL * j + 1] : 0;
             const double2 v = vals[l];
             const double vs = mul(v.x, scale);
@@ -218,13 +270,17 @@ RF_DEV void constrain_node_warp(int i, const AsmMesh& m, double scale, int apply
                 dT = outT;
             }
         }
-        for (int t = 0; t < 32; ++t) {
-            const double tv = __shfl_sync(0xffffffffu, termV, t);
-            const double tt = __shfl_sync(0xffffffffu, termT, t);
-            const int fv = __shfl_sync(0xffffffffu, movV, t);
-            const int ft = __shfl_sync(0xffffffffu, movT, t);
-            if (fv) mV = add(mV, tv);
-            if (ft) mT = add(mT, tt);
+        // moved-column terms in storage order; most rows have none
+        unsigned bv = __ballot_sync(0xffffffffu, movV), bt = __ballot_sync(0xffffffffu, movT);
+        while (bv) {
+            const int t = __ffs(bv) - 1;
+            bv &= bv - 1;
+            mV = add(mV, __shfl_sync(0xffffffffu, termV, t));
+        }
+        while (bt) {
+            const int t = __ffs(bt) - 1;
+            bt &= bt - 1;
+            mT = add(mT, __shfl_sync(0xffffffffu, termT, t));
         }
     }
     if (minv && dslot >= 0) {

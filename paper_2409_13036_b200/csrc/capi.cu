@@ -423,7 +423,8 @@ void rafem_mesh_destroy(rafem_mesh* m) {
     if (!m) return;
     for (void* p : {(void*)m->nodes, (void*)m->tets, (void*)m->region, (void*)m->regtab, (void*)m->kind,
                     (void*)m->rp, (void*)m->col, (void*)m->diag, (void*)m->inc_ptr, (void*)m->inc_ea,
-                    (void*)m->inc_slot, (void*)m->base, (void*)m->grad, (void*)m->vol})
+                    (void*)m->inc_slot, (void*)m->base, (void*)m->grad, (void*)m->vol, (void*)m->slot_ptr,
+                    (void*)m->slot_src})
         if (p) cudaFree(p);
     delete m;
 }

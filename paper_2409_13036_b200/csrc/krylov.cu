@@ -54,6 +54,9 @@ struct KArgs {
     double* p0;
     double* p1;
     double* q;
+    double* e0;       // pipelined PCG: s, and the second m buffer
+    double* e1;
+    double* e2;
     double* partial;  // 2 x (m + 2) x G
     double* hess;     // per-CTA Hessenberg scratch when it does not fit in smem
     long long hess_stride;
@@ -72,6 +75,7 @@ struct KArgs {
     int team;         // lanes per row group in the solver SpMV (power of two)
     unsigned long long* flags;  // 2 x G x 8 words of barrier/all-reduce slots
     unsigned epoch;             // per-launch flag epoch (never 0)
+    int pipe;                   // PCG: pipelined recurrence (pcg_pipe_core), W == 2 only
 };
 
 // Phase timestamps for diagnosis: slot k of iteration i at trace[i*8 + k].
@@ -943,6 +947,184 @@ RF_DEV PcgOut pcg_core(const KArgs& a, const R& rows, Sync<Mode>& sy, double bno
     return PcgOut{total, rel, converged ? 1 : 0, status};
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined PCG (Ghysels & Vanroose) for paper-scale systems: ONE grid
+// barrier per iteration, and the all-reduce of that iteration's dot
+// products is gathered WHILE the SpMV runs, because the SpMV operand
+// m = M^-1 w does not depend on it:
+//
+//   (after barrier i)  gather (r_i.u_i, w_i.u_i, r_i.r_i)  ||  n_i = A m_i
+//   alpha_i, beta_i from the gathered scalars (same recurrence as pcg_core)
+//   z = n + beta z, q = m + beta q, s = w + beta s, p = u + beta p
+//   x += alpha p, r -= alpha s, u -= alpha q, w -= alpha z, m' = M^-1 w
+//   publish (r.u, w.u, r.r) of the new vectors -> barrier i+1
+//
+// m is double-buffered (neighbours gather m_i while its owner writes
+// m_{i+1}); every other vector is owner-only.  Same contract as pcg_core:
+// one history entry per update, converged only on the TRUE residual (the
+// head recomputes r, u, w, m from x), breakdown -> RAFEM_ERR_BREAKDOWN.
+
+constexpr int kPipeRows = 256;  // max node rows per CTA (y staged in smem)
+
+template <bool PRE, class Mode, class R>
+RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, double bnorm, double* co, double* red,
+                            int& par) {
+    __shared__ double2 ybuf[kPipeRows];
+    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+    const int g0 = a.gpart[cta], g1 = a.gpart[cta + 1];
+    const int lo = 2 * g0, hi = 2 * g1;
+    const long long pstride = 8LL * G;
+    const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    double* x = a.x;
+    double* r = a.r;
+    double* u = a.z;
+    double* w = a.w0;
+    double* z = a.p1;
+    double* q = a.q;
+    double* sv = a.e0;
+    double* p = a.p0;
+    auto mb = [&](int i) { return i ? a.e1 : a.w1; };
+    auto M = [&](int e) { return PRE ? __ldg(a.minv + e) : 1.0; };
+
+    long long total = 0, cycles = 0, hlen = 0;
+    bool converged = false;
+    double rel = INFINITY;
+    int status = RAFEM_OK;
+    int cur = 0;  // m buffer gathered by the next SpMV
+
+    auto publish3 = [&](double (&v)[3]) {
+        block_sum<3>(v, red);
+        if (tid == 0) {
+            double* P = a.partial + par * pstride;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) P[(long long)j * G + cta] = v[j];
+        }
+    };
+    // the last warps fold the published partials while the others start the SpMV
+    auto gather3 = [&]() {
+        const int gw = warp - (nwarps - 3);
+        if (gw >= 0) {
+            const double s = reduce_partials_warp(a.partial + par * pstride + (long long)gw * G, G);
+            if (lane == 0) co[gw] = s;
+        }
+    };
+
+    while (true) {
+        {  // head: r = b - A x, u = M r ; then w = A u, m = M w ; partials of (r.u, w.u, r.r)
+            double v[3] = {0.0, 0.0, 0.0};
+            spmv_team<2>(rows, g0, g1, a.team, SrcPlain{x}, [&](int g, const double* y) {
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const int e = 2 * g + k;
+                    const double re = sub(a.b[e], y[k]);
+                    r[e] = re;
+                    u[e] = PRE ? mul(M(e), re) : re;
+                    v[2] = add(v[2], mul(re, re));
+                }
+            });
+            sy.template reduce<3>(v, 3, a.partial + par * pstride, co, red);
+            par ^= 1;
+        }
+        rel = sqrt(co[2]) / bnorm;
+        if (rel <= a.tol) {
+            converged = true;
+            break;
+        }
+        if (total >= a.cap) break;
+        {
+            double v[3] = {0.0, 0.0, 0.0};
+            double* m = mb(cur);
+            spmv_team<2>(rows, g0, g1, a.team, SrcPlain{u}, [&](int g, const double* y) {
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const int e = 2 * g + k;
+                    const double ue = u[e], re = r[e];
+                    w[e] = y[k];
+                    m[e] = PRE ? mul(M(e), y[k]) : y[k];
+                    v[0] = add(v[0], mul(re, ue));
+                    v[1] = add(v[1], mul(y[k], ue));
+                    v[2] = add(v[2], mul(re, re));
+                }
+            });
+            publish3(v);
+            sy.barrier();
+        }
+        double gamma = 0.0, alpha = 0.0;
+        bool first = true;
+        const long long hstart = hlen;
+        while (true) {
+            // n = A m (gathered) || fold the partials of the current vectors
+            gather3();
+            const double* m = mb(cur);
+            spmv_team<2>(rows, g0, g1, a.team, SrcPlain{m}, [&](int g, const double* y) {
+                ybuf[g - g0] = make_double2(y[0], y[1]);
+            });
+            __syncthreads();
+            par ^= 1;
+            const double gn = co[0], dn = co[1];
+            double beta = 0.0;
+            if (first) {
+                if (!(gn > 0.0) || !(dn > 0.0) || !isfinite(gn) || !isfinite(dn)) {
+                    status = RAFEM_ERR_BREAKDOWN;
+                    break;
+                }
+                alpha = gn / dn;
+            } else {
+                ++total;
+                const double est = sqrt(co[2]) / bnorm;
+                if (cta == 0 && tid == 0 && hlen < a.hist_cap) a.hist[hlen] = est;
+                ++hlen;
+                if (est <= a.tol || total >= a.cap) break;
+                beta = gn / gamma;
+                const double den = dn - beta * gn / alpha;
+                if (!(gn > 0.0) || !(den > 0.0) || !isfinite(den)) {
+                    status = RAFEM_ERR_BREAKDOWN;
+                    break;
+                }
+                alpha = gn / den;
+            }
+            gamma = gn;
+            double* mn = mb(cur ^ 1);
+            double v[3] = {0.0, 0.0, 0.0};
+            for (int e = lo + tid; e < hi; e += blockDim.x) {
+                const double ne = (e & 1) ? ybuf[(e >> 1) - g0].y : ybuf[(e >> 1) - g0].x;
+                const double me = m[e], we = w[e], ue = u[e];
+                double ze = ne, qe = me, se = we, pe = ue;
+                if (!first) {
+                    ze = add(ne, mul(beta, z[e]));
+                    qe = add(me, mul(beta, q[e]));
+                    se = add(we, mul(beta, sv[e]));
+                    pe = add(ue, mul(beta, p[e]));
+                }
+                z[e] = ze;
+                q[e] = qe;
+                sv[e] = se;
+                p[e] = pe;
+                x[e] = add(x[e], mul(alpha, pe));
+                const double rn = sub(r[e], mul(alpha, se));
+                const double un = sub(ue, mul(alpha, qe));
+                const double wn = sub(we, mul(alpha, ze));
+                r[e] = rn;
+                u[e] = un;
+                w[e] = wn;
+                mn[e] = PRE ? mul(M(e), wn) : wn;
+                v[0] = add(v[0], mul(rn, un));
+                v[1] = add(v[1], mul(wn, un));
+                v[2] = add(v[2], mul(rn, rn));
+            }
+            cur ^= 1;
+            first = false;
+            publish3(v);
+            sy.barrier();
+        }
+        if (cta == 0 && tid == 0 && cycles < a.cyc_cap) a.cyc[cycles] = hlen - hstart;
+        ++cycles;
+        if (status != RAFEM_OK) break;
+    }
+    if (a.res && cta == 0 && tid == 0) write_result(a.res, total, cycles, hlen, rel, converged, false, status);
+    return PcgOut{total, rel, converged ? 1 : 0, status};
+}
+
 template <int W, bool PRE, class Mode, class R>
 RF_DEV void pcg_body(const KArgs& a, const R& rows) {
     __shared__ double red[32 * 8];
@@ -952,6 +1134,12 @@ RF_DEV void pcg_body(const KArgs& a, const R& rows) {
     Sync<Mode> sy{a};
     const double bnorm = prologue<Mode>(a, sy, W * g0, W * g1, co, red, par, 8LL * gridDim.x);
     if (bnorm < 0.0) return;
+    if constexpr (W == 2) {
+        if (a.pipe) {
+            pcg_pipe_core<PRE, Mode>(a, rows, sy, bnorm, co, red, par);
+            return;
+        }
+    }
     pcg_core<W, PRE, Mode>(a, rows, sy, bnorm, co, red, par);
 }
 
@@ -1867,7 +2055,7 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     if (gm) {
         if (int rc = ensure(ctx, ctx->ws_basis, sizeof(double) * (size_t)(m + 1) * ldv)) return rc;
     }
-    if (int rc = ensure(ctx, ctx->ws_vec, sizeof(double) * (size_t)7 * ldv)) return rc;
+    if (int rc = ensure(ctx, ctx->ws_vec, sizeof(double) * (size_t)10 * ldv)) return rc;
     if (int rc = ensure(ctx, ctx->ws_partial, sizeof(double) * (size_t)2 * (std::max(m, 6) + 2) * G)) return rc;
     if (hess_global) {
         if (int rc = ensure(ctx, ctx->ws_hess, sizeof(double) * (size_t)hess_doubles * G)) return rc;
@@ -1893,6 +2081,9 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     a.p0 = vec + 4 * ldv;
     a.p1 = vec + 5 * ldv;
     a.q = vec + 6 * ldv;
+    a.e0 = vec + 7 * ldv;
+    a.e1 = vec + 8 * ldv;
+    a.e2 = vec + 9 * ldv;
     a.partial = static_cast<double*>(ctx->ws_partial.p);
     a.hess = hess_global ? static_cast<double*>(ctx->ws_hess.p) : nullptr;
     a.hess_stride = hess_doubles;
@@ -1926,10 +2117,20 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
         const int rows_per_cta = (A.ngroups + G - 1) / G;
         const int threads = (cluster && !gm) ? KTC : KT;
         int team = 1;
-        while (team < 16 && rows_per_cta * team * 2 <= threads) team *= 2;
+        // measured on B200 (probe_trace.py): the largest team with rows * team <= threads / 4
+        // (mesh B: 4 lanes, 1.8 us SpMV phase vs 2.6 with 8; mesh A: 8 lanes)
+        while (team < 16 && rows_per_cta * team * 4 <= threads) team *= 2;
         if (const char* env = getenv("RAFEM_TEAM")) team = std::max(1, std::min(32, atoi(env)));
         a.team = team;
         ctx->last_team = team;
+    }
+    {
+        // pipelined PCG for paper-scale systems (<= kPipeRows rows per CTA):
+        // RAFEM_PIPE=0 selects the single-reduction Chronopoulos-Gear kernel
+        const char* pe = getenv("RAFEM_PIPE");
+        const int rows_per_cta = (A.ngroups + G - 1) / G;
+        a.pipe = (!gm && A.W == 2 && !cluster && ms != 3 && rows_per_cta <= kPipeRows / 2 && !(pe && pe[0] == '0'))
+                     ? 1 : 0;
     }
     if (cluster) smem = (size_t)a.hess_smem * 8 + part.max_slice;
     void* args[] = {&a};
@@ -2004,7 +2205,15 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     A.maxdeg = mesh->maxdeg;
     if (mesh->maxdeg > 32) return RAFEM_ERR_UNSUPPORTED;
     const bool pre = p->solver.precondition == RAFEM_PRECOND_JACOBI;
-    const void* fn = pre ? (const void*)simulate_kernel<true> : (const void*)simulate_kernel<false>;
+    // RAFEM_SIM_THREADS=256 selects a 256-thread CTA (rows * team <= 256
+    // still holds at paper scale); measured on mesh B it runs the PCG
+    // iteration at the same 5.96 us and the assembly phases slower.
+    const int rows_per_cta0 = (N + std::max(1, std::min(ctx->sm_count, N)) - 1) / std::max(1, std::min(ctx->sm_count, N));
+    int nt = 512;  // measured: 256 threads gives the same PCG iteration and a slower assembly
+    (void)rows_per_cta0;
+    if (const char* env = getenv("RAFEM_SIM_THREADS")) nt = atoi(env) == 256 ? 256 : 512;
+    const void* fn = nt == 256 ? (pre ? (const void*)simulate_kernel<true, 256> : (const void*)simulate_kernel<false, 256>)
+                               : (pre ? (const void*)simulate_kernel<true, 512> : (const void*)simulate_kernel<false, 512>);
     const int G = std::max(1, std::min(ctx->sm_count, N));
     PartInfo part;
     if (A.slots * 20LL > (long long)G * (150 << 10)) return RAFEM_ERR_UNSUPPORTED;
@@ -2015,12 +2224,12 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     if (smem + fa.sharedSizeBytes > 227 * 1024) return RAFEM_ERR_UNSUPPORTED;
     RF_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
-    RF_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, KT, smem));
+    RF_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nt, smem));
     if (occ < 1 || G > occ * ctx->sm_count) return RAFEM_ERR_UNSUPPORTED;
 
     const long long n2 = 2LL * N;
     const long long ldv = (n2 + 31) / 32 * 32;
-    if (int rc = ensure(ctx, ctx->ws_vec, sizeof(double) * (size_t)7 * ldv)) return rc;
+    if (int rc = ensure(ctx, ctx->ws_vec, sizeof(double) * (size_t)10 * ldv)) return rc;
     if (int rc = ensure(ctx, ctx->ws_partial, sizeof(double) * (size_t)2 * 8 * G)) return rc;
     if (int rc = ensure(ctx, ctx->ws_simout, sizeof(SimDevOut))) return rc;
     {
@@ -2045,6 +2254,9 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     a.p0 = vec + 4 * ldv;
     a.p1 = vec + 5 * ldv;
     a.q = vec + 6 * ldv;
+    a.e0 = vec + 7 * ldv;
+    a.e1 = vec + 8 * ldv;
+    a.e2 = vec + 9 * ldv;
     a.partial = static_cast<double*>(ctx->ws_partial.p);
     a.m = 1;
     a.tol = p->solver.tolerance;
@@ -2054,10 +2266,15 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     {
         const int rows_per_cta = (N + G - 1) / G;
         int team = 1;
-        while (team < 16 && rows_per_cta * team * 2 <= KT) team *= 2;
+        // see krylov_solve: the largest team with rows * team <= 256 lanes
+        while (team < 16 && rows_per_cta * team * 2 <= 256) team *= 2;
         if (const char* env = getenv("RAFEM_TEAM")) team = std::max(1, std::min(32, atoi(env)));
         a.team = team;
         ctx->last_team = team;
+    }
+    {
+        const char* pe = getenv("RAFEM_PIPE");
+        a.pipe = ((N + G - 1) / G <= kPipeRows / 2 && !(pe && pe[0] == '0')) ? 1 : 0;
     }
     S.m = asm_mesh(mesh);
     S.contrib = reinterpret_cast<double2*>(s->contrib);
@@ -2074,6 +2291,12 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     S.rec_iters = rec_iters_dev;
     S.rec_cap = rec_cap;
     S.out = static_cast<SimDevOut*>(ctx->ws_simout.p);
+    if (ctx->trace_on) {  // per-pass phase stamps (rafem_get_trace)
+        if (int rc = ensure(ctx, ctx->ws_trace, sizeof(long long) * 8 * 4096)) return rc;
+        RF_CUDA_TRY(ctx, cudaMemsetAsync(ctx->ws_trace.p, 0, sizeof(long long) * 8 * 4096, ctx->stream));
+        S.ptrace = static_cast<long long*>(ctx->ws_trace.p);
+        S.ptrace_cap = 8 * 4096;
+    }
     if (stream) {
         S.ring = stream->ring;
         S.ring_slots = stream->slots;
@@ -2082,7 +2305,7 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     }
     void* args[] = {&S};
     RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
-    RF_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fn, dim3(G), dim3(KT), args, smem, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fn, dim3(G), dim3(nt), args, smem, ctx->stream));
     RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
     ctx->launches++;
     ctx->last_mode = 2;

@@ -43,6 +43,8 @@ struct SimArgs {
     int ring_slots;
     volatile long long* prog;  // accepted records complete in the ring (kernel writes)
     volatile long long* cons;  // records the host has consumed (host writes)
+    long long* ptrace;         // optional per-pass phase stamps (globaltimer ns), 8 per pass
+    long long ptrace_cap;
 };
 
 // Max over CTAs of one nonnegative value (exact, order independent).
@@ -68,12 +70,12 @@ RF_DEV long long global_ns() {
     return t;
 }
 
-template <bool PRE>
-__global__ void __launch_bounds__(KT, 1) simulate_kernel(SimArgs S) {
+template <bool PRE, int NT>
+__global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
     extern __shared__ __align__(16) double sval[];
     __shared__ double red[32 * 8];
     __shared__ double co[8];
-    __shared__ FillScratch ws[KT / 32];
+    __shared__ FillScratch ws[NT / 32];
     __shared__ int zflag;
     const KArgs& a = S.k;
     const rafem_sim_params& p = S.p;
@@ -131,7 +133,16 @@ __global__ void __launch_bounds__(KT, 1) simulate_kernel(SimArgs S) {
             iters = it;
             ++passes;
             const long long ta = global_ns();
+            // phase stamps: recomputed from `passes` at each use, so no extra
+            // register stays live across the PCG loop
+#define SIM_STAMP(k, v)                                                                     \
+    do {                                                                                    \
+        if (S.ptrace && cta == 0 && tid == 0 && passes * 8 <= S.ptrace_cap)                 \
+            S.ptrace[(passes - 1) * 8 + (k)] = (v);                                         \
+    } while (0)
+            SIM_STAMP(0, ta);
             sy.barrier();  // the iterate is complete everywhere
+            SIM_STAMP(1, global_ns());
             if (S.ring && cta == 0 && tid == 0 && it == 1) {
                 __threadfence_system();
                 *S.prog = step;  // every accepted record is in the ring
@@ -146,12 +157,13 @@ __global__ void __launch_bounds__(KT, 1) simulate_kernel(SimArgs S) {
                 }
             }
             // ---- element phase (own elements)
-            double badv = 0.0;
             const AsmFields f{X(iit) + 1, 2, X(iit), 2, X(iacc) + 1, 2, dt};
+            double badv = 0.0;
             for (int e = e0 + tid; e < e1; e += blockDim.x)
                 if (element_tet(e, S.m, f, S.contrib, S.load)) badv = fmax(badv, (double)(M - e));
             const double badmax = reduce_max1(sy, badv, P(), red);
             par ^= 1;
+            SIM_STAMP(2, global_ns());
             if (badmax > 0.0) {  // PhysicsRangeError aborts the run (fem.py:274)
                 bad = M - (long long)badmax;
                 status = RAFEM_ERR_PHYSICS;
@@ -159,6 +171,9 @@ __global__ void __launch_bounds__(KT, 1) simulate_kernel(SimArgs S) {
                 break;
             }
             // ---- fill own rows into the shared-memory slice
+            // (warp per row: the thread-per-slot fill of the standalone path
+            // needs wide load batches whose registers the PCG loop below
+            // cannot spare at 128 per thread)
             for (int i = g0 + warp; i < g1; i += nwarps)
                 fill_node_warp(i, S.m, S.contrib, S.load, sv2 + srp[i - g0], S.rhs, S.diag_raw, ws[warp]);
             __syncthreads();
@@ -169,12 +184,13 @@ __global__ void __launch_bounds__(KT, 1) simulate_kernel(SimArgs S) {
             }
             sy.template reduce<2>(dv, 2, P(), co, red);
             par ^= 1;
+            SIM_STAMP(3, global_ns());
             double scale = 1.0;  // fem.py:390-396
             if (co[0] > 0.0 && co[1] > 0.0) scale = ldexp(1.0, (int)rint(log2(co[1] / co[0])));
             // ---- scale + Dirichlet + Jacobi on own rows; x0 = iterate
             for (int i = g0 + warp; i < g1; i += nwarps)
                 constrain_node_warp(i, S.m, scale, 1, p.applied_voltage, p.boundary_temp, sv2 + srp[i - g0], S.rhs,
-                                    PRE ? const_cast<double*>(a.minv) : nullptr, &zflag);
+                                    PRE ? const_cast<double*>(a.minv) : nullptr, &zflag, scol + srp[i - g0]);
             for (int e = lo + tid; e < hi; e += blockDim.x) X(inew)[e] = X(iit)[e];
             __syncthreads();
             double bv[2] = {0.0, 0.0};
@@ -188,6 +204,7 @@ __global__ void __launch_bounds__(KT, 1) simulate_kernel(SimArgs S) {
                 break;
             }
             const long long tb = global_ns();
+            SIM_STAMP(4, tb);
             // ---- solve (single-reduction PCG on the smem slice)
             const double bnorm = sqrt(co[0]);
             PcgOut o{0, 0.0, 1, RAFEM_OK};
@@ -198,9 +215,12 @@ __global__ void __launch_bounds__(KT, 1) simulate_kernel(SimArgs S) {
                 kk.b = S.rhs;
                 kk.x = X(inew);
                 kk.res = nullptr;
-                o = pcg_core<2, PRE, GridMode>(kk, rows, sy, bnorm, co, red, par);
+                o = a.pipe ? pcg_pipe_core<PRE, GridMode>(kk, rows, sy, bnorm, co, red, par)
+                           : pcg_core<2, PRE, GridMode>(kk, rows, sy, bnorm, co, red, par);
             }
             const long long tc = global_ns();
+            SIM_STAMP(5, tc);
+            SIM_STAMP(7, o.total);
             asm_ns += tb - ta;
             sol_ns += tc - tb;
             if (o.status == RAFEM_ERR_BREAKDOWN) break;  // SolverError -> step failure (fem.py:511-515)
@@ -215,6 +235,7 @@ __global__ void __launch_bounds__(KT, 1) simulate_kernel(SimArgs S) {
             }
             const double delta = reduce_max1(sy, dmax, P(), red);
             par ^= 1;
+            SIM_STAMP(6, global_ns());
             const int tmp = iit;
             iit = inew;
             inew = tmp;
@@ -269,6 +290,7 @@ __global__ void __launch_bounds__(KT, 1) simulate_kernel(SimArgs S) {
             ++halv;
         }
     }
+#undef SIM_STAMP
     for (int e = lo + tid; e < hi; e += blockDim.x) S.final_x[e] = X(iacc)[e];
     if (S.ring) {
         sy.barrier();  // the last record is complete everywhere

@@ -282,3 +282,23 @@ def test_fused_simulation_matches_multi_kernel_loop():
         assert np.max(np.abs(a.T - b.T)) <= 1e-9 * np.max(np.abs(b.T))
         assert np.max(np.abs(a.V - b.V)) <= 1e-9 * np.max(np.abs(b.V))
     _compare_run(fused, golden("run_A40_1e-10"), 1e-6, every_step=False)
+
+
+def test_slot_list_fill_is_bitwise_warp_fill():
+    """The thread-per-slot fill over precomputed contributor lists sums in
+    the same (ascending element) order as the warp-per-row fill: same bits
+    for values, rhs and scale, on a hot iterate."""
+    import os
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, assemble_global, generate_box_mesh
+    mesh = generate_box_mesh(17, 13, 15)
+    n = mesh.node_count
+    rng = np.random.default_rng(77)
+    t, v, tp = 37.0 + rng.uniform(0, 30, n), rng.uniform(0, 25, n), 37.0 + rng.uniform(0, 5, n)
+    a = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, v, tp, 0.7)
+    os.environ["RAFEM_WARP_FILL"] = "1"
+    try:
+        b = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, v, tp, 0.7)
+    finally:
+        del os.environ["RAFEM_WARP_FILL"]
+    assert np.array_equal(a.matrix.vals, b.matrix.vals)
+    assert np.array_equal(a.rhs, b.rhs) and a.voltage_row_scale == b.voltage_row_scale
