@@ -444,26 +444,36 @@ int mesh_symbolic(rafem_mesh* m) {
         ctx->launches++;
     }
     RF_CUDA_TRY(ctx, cudaGetLastError());
-    // slot contributor lists (thread-per-slot fill) when 16 M fits an int
-    if (N > 0 && slots > 0 && 16LL * M < (1LL << 31) && m->maxdeg <= kMaxDeg) {
-        int* scnt = nullptr;
-        RF_CUDA_TRY(ctx, cudaMalloc(&scnt, sizeof(int) * (size_t)slots));
-        RF_CUDA_TRY(ctx, cudaMalloc(&m->slot_ptr, sizeof(int) * ((size_t)slots + 1)));
-        RF_CUDA_TRY(ctx, cudaMalloc(&m->slot_src, sizeof(int) * 16 * (size_t)M));
-        slot_count_kernel<<<(N + 127) / 128, 128, 0, st>>>(m->inc_ptr, m->inc_slot, m->rp, N, scnt);
-        ctx->launches++;
-        if (int rc = scan_ints(ctx, scnt, m->slot_ptr, slots)) return rc;
-        slot_fill_kernel<<<(N + 127) / 128, 128, 0, st>>>(m->inc_ptr, m->inc_ea, m->inc_slot, m->rp, N, m->slot_ptr,
-                                                          m->slot_src);
-        ctx->launches++;
-        RF_CUDA_TRY(ctx, cudaGetLastError());
-        RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
-        cudaFree(scnt);
-    }
     RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
     cudaFree(cnt);
     cudaFree(cursor);
     cudaFree(flags);
+    return RAFEM_OK;
+}
+
+// Per-slot contributor lists for the thread-per-slot fill; built on first
+// use (the fused simulation kernel fills warp-per-row and never needs them).
+// Returns without lists when 16 M does not fit an int.
+int mesh_slot_lists(rafem_mesh* m) {
+    rafem_ctx* ctx = m->ctx;
+    cudaStream_t st = ctx->stream;
+    m->slot_lists_tried = true;
+    const int N = m->N, M = m->M;
+    const long long slots = m->slots;
+    if (N <= 0 || slots <= 0 || 16LL * M >= (1LL << 31) || m->maxdeg > kMaxDeg) return RAFEM_OK;
+    int* scnt = nullptr;
+    RF_CUDA_TRY(ctx, cudaMalloc(&scnt, sizeof(int) * (size_t)slots));
+    RF_CUDA_TRY(ctx, cudaMalloc(&m->slot_ptr, sizeof(int) * ((size_t)slots + 1)));
+    RF_CUDA_TRY(ctx, cudaMalloc(&m->slot_src, sizeof(int) * 16 * (size_t)M));
+    slot_count_kernel<<<(N + 127) / 128, 128, 0, st>>>(m->inc_ptr, m->inc_slot, m->rp, N, scnt);
+    ctx->launches++;
+    if (int rc = scan_ints(ctx, scnt, m->slot_ptr, (int)slots)) return rc;
+    slot_fill_kernel<<<(N + 127) / 128, 128, 0, st>>>(m->inc_ptr, m->inc_ea, m->inc_slot, m->rp, N, m->slot_ptr,
+                                                      m->slot_src);
+    ctx->launches++;
+    RF_CUDA_TRY(ctx, cudaGetLastError());
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    cudaFree(scnt);
     return RAFEM_OK;
 }
 
@@ -512,6 +522,10 @@ int assemble_fill_launch(rafem_system* s, const double* t_it, int ts, const doub
     rafem_ctx* ctx = m->ctx;
     cudaStream_t st = ctx->stream;
     const int N = m->N, M = m->M;
+    const char* wf = getenv("RAFEM_WARP_FILL");
+    const bool warp_fill = wf && wf[0] == '1';
+    if (!warp_fill && !m->slot_lists_tried)
+        if (int rc = mesh_slot_lists(m)) return rc;
     const AsmMesh am = asm_mesh(m);
     const AsmFields f{t_it, ts, v_it, vs, t_prev, ps, dt};
     double2* contrib = reinterpret_cast<double2*>(s->contrib);
@@ -523,8 +537,7 @@ int assemble_fill_launch(rafem_system* s, const double* t_it, int ts, const doub
         ctx->launches++;
     }
     if (N > 0) {
-        const char* wf = getenv("RAFEM_WARP_FILL");
-        if (am.slot_src && !(wf && wf[0] == '1')) {
+        if (am.slot_src && !warp_fill) {
             const int S = (int)m->slots;
             fill_slots_kernel<<<(S + 255) / 256, 256, 0, st>>>(am, contrib, val2, S);
             fill_rows_kernel<<<(N + 255) / 256, 256, 0, st>>>(am, s->load, val2, s->rhs, s->diagpart);

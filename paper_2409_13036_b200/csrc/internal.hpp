@@ -131,6 +131,7 @@ struct rafem_mesh {
     unsigned* inc_slot = nullptr; // 4M: 4 x uint8 row offsets of the tet's nodes
     int* slot_ptr = nullptr;  // slots + 1: per-slot contributor lists
     int* slot_src = nullptr;  // 16M: contribution index 16 e + 4 a + b (ascending e per slot)
+    bool slot_lists_tried = false;
     // geometry (constant per mesh)
     double* base = nullptr;   // M x 10: vol * grad_a . grad_b, symmetric packed
     double* grad = nullptr;   // M x 12
