@@ -265,8 +265,25 @@ class SystemHandle:
 _MESH_CACHE: dict = {}
 
 
-def _material_key(mesh, material):
+_TAGS_CACHE: dict = {}
+
+
+def _region_tags(mesh):
+    """np.unique(mesh.regions), memoised per regions array (the plug-in seam
+    asks for it on every corrector pass; a 43K-tet unique costs ~0.1 ms)."""
+    key = id(mesh.regions)
+    hit = _TAGS_CACHE.get(key)
+    if hit is not None and hit[0] is mesh.regions:
+        return hit[1]
     tags = np.unique(mesh.regions)
+    if len(_TAGS_CACHE) > 64:
+        _TAGS_CACHE.clear()
+    _TAGS_CACHE[key] = (mesh.regions, tags)
+    return tags
+
+
+def _material_key(mesh, material):
+    tags = _region_tags(mesh)
     rows = []
     for t in tags:
         m = material.for_region(int(t))
