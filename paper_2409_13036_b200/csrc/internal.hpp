@@ -190,6 +190,7 @@ int vec_delta_launch(rafem_ctx* ctx, const double* xn, const double* xo, int n, 
 // assembly.cu
 int mesh_symbolic(rafem_mesh* m);
 int mesh_geometry(rafem_mesh* m);
+int mesh_slot_lists(rafem_mesh* m);  // per-slot contributor lists (built on first use)
 int assemble_launch(rafem_system* s, const double* t_it, int ts, const double* v_it, int vs,
                     const double* t_prev, int ps, const rafem_assemble_params& p,
                     double* scale_dev, long long* bad_dev);

@@ -966,9 +966,15 @@ RF_DEV PcgOut pcg_core(const KArgs& a, const R& rows, Sync<Mode>& sy, double bno
 
 constexpr int kPipeRows = 256;  // max node rows per CTA (y staged in smem)
 
+// bnorm < 0: ||b|| (and, with zflag, the zero-diagonal flag of the Jacobi
+// setup) are folded into the first head reduction instead of a separate
+// round; a raised flag returns RAFEM_ERR_INVALID, b == 0 gives x = 0.
+// x0_gather: where the FIRST head gathers the initial guess from (a copy of
+// x that is already complete on every CTA), so the caller's owner-only copy
+// into x needs no barrier of its own; later heads gather x itself.
 template <bool PRE, class Mode, class R>
 RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, double bnorm, double* co, double* red,
-                            int& par) {
+                            int& par, const int* zflag = nullptr, const double* x0_gather = nullptr) {
     __shared__ double2 ybuf[kPipeRows];
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
     const int g0 = a.gpart[cta], g1 = a.gpart[cta + 1];
@@ -1011,19 +1017,33 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
 
     while (true) {
         {  // head: r = b - A x, u = M r ; then w = A u, m = M w ; partials of (r.u, w.u, r.r)
+            const bool with_b = bnorm < 0.0;
             double v[3] = {0.0, 0.0, 0.0};
-            spmv_team<2>(rows, g0, g1, a.team, SrcPlain{x}, [&](int g, const double* y) {
+            const double* xg = x0_gather ? x0_gather : x;
+            x0_gather = nullptr;
+            spmv_team<2>(rows, g0, g1, a.team, SrcPlain{xg}, [&](int g, const double* y) {
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
                     const int e = 2 * g + k;
-                    const double re = sub(a.b[e], y[k]);
+                    const double be = a.b[e];
+                    const double re = sub(be, y[k]);
                     r[e] = re;
                     u[e] = PRE ? mul(M(e), re) : re;
                     v[2] = add(v[2], mul(re, re));
+                    if (with_b) v[0] = add(v[0], mul(be, be));
                 }
             });
+            if (with_b && zflag && tid == 0) v[1] = (double)*zflag;
             sy.template reduce<3>(v, 3, a.partial + par * pstride, co, red);
             par ^= 1;
+            if (with_b) {
+                if (co[1] > 0.0) return PcgOut{0, INFINITY, 0, RAFEM_ERR_INVALID};
+                bnorm = sqrt(co[0]);
+                if (bnorm == 0.0) {  // zero data: zero solution (solver.py:422-425)
+                    for (int e = lo + tid; e < hi; e += blockDim.x) x[e] = 0.0;
+                    return PcgOut{0, 0.0, 1, RAFEM_OK};
+                }
+            }
         }
         rel = sqrt(co[2]) / bnorm;
         if (rel <= a.tol) {
@@ -2205,13 +2225,14 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     A.maxdeg = mesh->maxdeg;
     if (mesh->maxdeg > 32) return RAFEM_ERR_UNSUPPORTED;
     const bool pre = p->solver.precondition == RAFEM_PRECOND_JACOBI;
-    // RAFEM_SIM_THREADS=256 selects a 256-thread CTA (rows * team <= 256
-    // still holds at paper scale); measured on mesh B it runs the PCG
-    // iteration at the same 5.96 us and the assembly phases slower.
-    const int rows_per_cta0 = (N + std::max(1, std::min(ctx->sm_count, N)) - 1) / std::max(1, std::min(ctx->sm_count, N));
-    int nt = 512;  // measured: 256 threads gives the same PCG iteration and a slower assembly
-    (void)rows_per_cta0;
-    if (const char* env = getenv("RAFEM_SIM_THREADS")) nt = atoi(env) == 256 ? 256 : 512;
+    // 256 threads per CTA: rows * team <= 256 holds at paper scale, the PCG
+    // iteration is as fast as with 512 (measured), and the 255-register cap
+    // leaves room for the thread-per-slot fill.  RAFEM_SIM_THREADS=512
+    // selects the wide CTA (warp-per-row fill).
+    int nt = 256;
+    if (const char* env = getenv("RAFEM_SIM_THREADS")) nt = atoi(env) == 512 ? 512 : 256;
+    if (nt == 256 && !mesh->slot_lists_tried)
+        if (int rc = mesh_slot_lists(mesh)) return rc;
     const void* fn = nt == 256 ? (pre ? (const void*)simulate_kernel<true, 256> : (const void*)simulate_kernel<false, 256>)
                                : (pre ? (const void*)simulate_kernel<true, 512> : (const void*)simulate_kernel<false, 512>);
     const int G = std::max(1, std::min(ctx->sm_count, N));

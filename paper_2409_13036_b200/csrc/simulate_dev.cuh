@@ -161,29 +161,38 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
             double badv = 0.0;
             for (int e = e0 + tid; e < e1; e += blockDim.x)
                 if (element_tet(e, S.m, f, S.contrib, S.load)) badv = fmax(badv, (double)(M - e));
-            const double badmax = reduce_max1(sy, badv, P(), red);
-            par ^= 1;
+            sy.barrier();  // a row's fill gathers contributions of other CTAs' elements
             SIM_STAMP(2, global_ns());
-            if (badmax > 0.0) {  // PhysicsRangeError aborts the run (fem.py:274)
+            // ---- fill own rows into the shared-memory slice
+            if (NT == 256 && S.m.slot_src) {
+                // thread per slot over its contributor list, then thread per row
+                // (at 256 threads the kernel has the registers for the wide batches)
+                for (int sl = tid; sl < ns; sl += blockDim.x) sv2[sl] = fill_slot(s0 + sl, S.m, S.contrib);
+                __syncthreads();
+                for (int i = g0 + tid; i < g1; i += blockDim.x)
+                    fill_node_rhs(i, S.m, S.load, sv2 + srp[i - g0], S.rhs, S.diag_raw);
+            } else {
+                for (int i = g0 + warp; i < g1; i += nwarps)
+                    fill_node_warp(i, S.m, S.contrib, S.load, sv2 + srp[i - g0], S.rhs, S.diag_raw, ws[warp]);
+            }
+            __syncthreads();
+            // diagonal sums and the PhysicsRange count in ONE reduction; the
+            // offending element is located only on the (aborting) bad path
+            double dv[3] = {0.0, 0.0, badv > 0.0 ? 1.0 : 0.0};
+            for (int i = g0 + tid; i < g1; i += blockDim.x) {
+                dv[0] = add(dv[0], S.diag_raw[2LL * i]);
+                dv[1] = add(dv[1], S.diag_raw[2LL * i + 1]);
+            }
+            sy.template reduce<3>(dv, 3, P(), co, red);
+            par ^= 1;
+            if (co[2] > 0.0) {  // PhysicsRangeError aborts the run (fem.py:274)
+                const double badmax = reduce_max1(sy, badv, P(), red);
+                par ^= 1;
                 bad = M - (long long)badmax;
                 status = RAFEM_ERR_PHYSICS;
                 abort_run = true;
                 break;
             }
-            // ---- fill own rows into the shared-memory slice
-            // (warp per row: the thread-per-slot fill of the standalone path
-            // needs wide load batches whose registers the PCG loop below
-            // cannot spare at 128 per thread)
-            for (int i = g0 + warp; i < g1; i += nwarps)
-                fill_node_warp(i, S.m, S.contrib, S.load, sv2 + srp[i - g0], S.rhs, S.diag_raw, ws[warp]);
-            __syncthreads();
-            double dv[2] = {0.0, 0.0};
-            for (int i = g0 + tid; i < g1; i += blockDim.x) {
-                dv[0] = add(dv[0], S.diag_raw[2LL * i]);
-                dv[1] = add(dv[1], S.diag_raw[2LL * i + 1]);
-            }
-            sy.template reduce<2>(dv, 2, P(), co, red);
-            par ^= 1;
             SIM_STAMP(3, global_ns());
             double scale = 1.0;  // fem.py:390-396
             if (co[0] > 0.0 && co[1] > 0.0) scale = ldexp(1.0, (int)rint(log2(co[1] / co[0])));
@@ -193,30 +202,45 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
                                     PRE ? const_cast<double*>(a.minv) : nullptr, &zflag, scol + srp[i - g0]);
             for (int e = lo + tid; e < hi; e += blockDim.x) X(inew)[e] = X(iit)[e];
             __syncthreads();
-            double bv[2] = {0.0, 0.0};
-            for (int e = lo + tid; e < hi; e += blockDim.x) bv[0] = add(bv[0], mul(S.rhs[e], S.rhs[e]));
-            if (tid == 0) bv[1] = (double)zflag;
-            sy.template reduce<2>(bv, 2, P(), co, red);
-            par ^= 1;
-            if (co[1] > 0.0) {  // ValueError: zero diagonal under Jacobi (solver.py:416-417)
-                status = RAFEM_ERR_INVALID;
-                abort_run = true;
-                break;
-            }
-            const long long tb = global_ns();
-            SIM_STAMP(4, tb);
-            // ---- solve (single-reduction PCG on the smem slice)
-            const double bnorm = sqrt(co[0]);
             PcgOut o{0, 0.0, 1, RAFEM_OK};
-            if (bnorm == 0.0) {
-                for (int e = lo + tid; e < hi; e += blockDim.x) X(inew)[e] = 0.0;
-            } else {
+            long long tb;
+            if (a.pipe) {
+                // ||b|| and the zero-diagonal flag ride on the PCG head's reduction
+                tb = global_ns();
+                SIM_STAMP(4, tb);
                 KArgs kk = a;
                 kk.b = S.rhs;
                 kk.x = X(inew);
                 kk.res = nullptr;
-                o = a.pipe ? pcg_pipe_core<PRE, GridMode>(kk, rows, sy, bnorm, co, red, par)
-                           : pcg_core<2, PRE, GridMode>(kk, rows, sy, bnorm, co, red, par);
+                o = pcg_pipe_core<PRE, GridMode>(kk, rows, sy, -1.0, co, red, par, &zflag, X(iit));
+                if (o.status == RAFEM_ERR_INVALID) {  // ValueError: zero diagonal under Jacobi (solver.py:416-417)
+                    status = RAFEM_ERR_INVALID;
+                    abort_run = true;
+                    break;
+                }
+            } else {
+                double bv[2] = {0.0, 0.0};
+                for (int e = lo + tid; e < hi; e += blockDim.x) bv[0] = add(bv[0], mul(S.rhs[e], S.rhs[e]));
+                if (tid == 0) bv[1] = (double)zflag;
+                sy.template reduce<2>(bv, 2, P(), co, red);
+                par ^= 1;
+                if (co[1] > 0.0) {  // ValueError: zero diagonal under Jacobi (solver.py:416-417)
+                    status = RAFEM_ERR_INVALID;
+                    abort_run = true;
+                    break;
+                }
+                tb = global_ns();
+                SIM_STAMP(4, tb);
+                const double bnorm = sqrt(co[0]);
+                if (bnorm == 0.0) {
+                    for (int e = lo + tid; e < hi; e += blockDim.x) X(inew)[e] = 0.0;
+                } else {
+                    KArgs kk = a;
+                    kk.b = S.rhs;
+                    kk.x = X(inew);
+                    kk.res = nullptr;
+                    o = pcg_core<2, PRE, GridMode>(kk, rows, sy, bnorm, co, red, par);
+                }
             }
             const long long tc = global_ns();
             SIM_STAMP(5, tc);
