@@ -314,8 +314,17 @@ def run_ours(args):
     else:
         bytes_total = iters * gmres_iter_bytes(N, S, 15) + passes * (20 * S + 4 * (N + 1) + 48 * N)
     achieved = bytes_total / (solve_ms / 1e3) / 1e9 if solve_ms > 0 else 0.0
+    # DRAM traffic of one launch from the committed ncu --set full capture of
+    # the same command (scripts/ncu_summary.py -> profiles/traffic.json)
+    traffic = None
+    tj = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tj):
+        try:
+            traffic = json.load(open(tj)).get("simulate_kernel")
+        except Exception:  # noqa: BLE001
+            traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None,
+                "frac": achieved / hbm_peak, "traffic": traffic,
                 "kernel": ("simulate_kernel<true> (whole run, one cooperative launch); bytes = PCG iterations"
                            if runner.last_mode == "fused-simulation" else f"{args.backend}_grid_kernel (persistent solve)"),
                 "launches": passes, "avg_launch_us": 1e3 * solve_ms / max(passes, 1),

@@ -1,4 +1,4 @@
-"""Short native run for an ncu launch list (a few accepted steps of mesh B)."""
+"""Native run of the mesh-B analog for ncu captures (full 900 s unless a step cap is given)."""
 import sys
 sys.path.insert(0, ".")
 from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh
@@ -6,4 +6,4 @@ from paper_2409_13036_b200.timeloop import DeviceRun
 backend = sys.argv[1] if len(sys.argv) > 1 else "pcg"
 r = DeviceRun(generate_box_mesh(20, 20, 21), MaterialParams.default())
 cfg = SimConfig(total_time=900.0, solver=SolverConfig(backend=backend, precondition="jacobi"))
-r.run(cfg, record_fields=False, max_steps=4)
+r.run(cfg, record_fields=False, max_steps=int(sys.argv[2]) if len(sys.argv) > 2 else None)

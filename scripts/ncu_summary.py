@@ -8,6 +8,7 @@ full raw page as CSV (profiles/TAG_<name>_raw.csv).
 """
 import collections
 import csv
+import json
 import io
 import os
 import subprocess
@@ -68,6 +69,24 @@ def report(path, out_txt, out_csv):
                 fh.write(f"{'traffic (dram read + write)':60s} {mb('dram__bytes_read.sum') + mb('dram__bytes_write.sum'):16.3f} MB\n")
 
 
+def traffic_json(path):
+    """profiles/traffic.json: {kernel short name: dram read + write bytes per launch}."""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, units = rows[0], rows[1]
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    out = {}
+    if os.path.exists("profiles/traffic.json"):
+        out = json.load(open("profiles/traffic.json"))
+    for r in rows[2:]:
+        name = r[h.index("Kernel Name")].split("(")[0].split("<")[0].replace("void ", "").replace("rafem::", "")
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(r[h.index(k)].replace(",", "")) * scale[units[h.index(k)]]
+        out[name] = tot
+    json.dump(out, open("profiles/traffic.json", "w"), indent=1)
+
+
 def main():
     tag = sys.argv[1]
     os.makedirs("profiles", exist_ok=True)
@@ -77,6 +96,7 @@ def main():
             launches(p, f"profiles/{tag}_{name}.txt")
         else:
             report(p, f"profiles/{tag}_{name}.txt", f"profiles/{tag}_{name}_raw.csv")
+            traffic_json(p)
 
 
 if __name__ == "__main__":
