@@ -352,176 +352,6 @@ def run_ours(args):
                         "not HBM; the HBM-bound kernels are reported in spmv_c3 and sharded_c4"}
 
     line = {
-        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (generated Kuhn box mesh; reference physics defaults)",
-        "impl": "reference",
-        "config": {"workload": "rafem-B900", "mesh": "generate_box_mesh(20,20,21)", "dofs": 16800,
-                   "total_time_s": TOTAL_TIME, "solver": "gmres(30)+jacobi tol 1e-10 (reference)",
-                   "step": f"{REF_WINDOW} accepted time steps of one continuing simulation"},
-        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} windows x {REF_WINDOW} accepted steps after "
-                                   f"{args.warmup} warm-up windows (bit-exact numpy port of rafem 0.1.0)"},
-        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "gpu_launches": 0,
-    }
-    print(json.dumps(line), flush=True)
-
-
-def _oracle_steps(O, mesh):
-    """Generator over accepted steps of the oracle's time loop (fem.py:554-644)."""
-    cfg = O.OSim(total_time=TOTAL_TIME)
-    N = mesh.node_count
-    geom = O.geometry(mesh)
-    T = np.full(N, cfg.initial_temp)
-    V = np.zeros(N)
-    T_prev = T.copy()
-    t, dt_cur, dt_prev, step = 0.0, cfg.dt_init, cfg.dt_init, 0
-    mats = {0: O.OMaterial()}
-    while t < cfg.total_time:
-        remaining = cfg.total_time - t
-        last = dt_cur >= remaining
-        dt = remaining if last else dt_cur
-        t_it = T + (dt / dt_prev) * (T - T_prev) if step >= 1 else T.copy()
-        v_it = V.copy()
-        x_old = np.empty(2 * N)
-        x_old[0::2], x_old[1::2] = v_it, t_it
-        ok, used = False, 0
-        for it_ in range(1, cfg.max_corrector_iters + 1):
-            used = it_
-            s = O.assemble(mesh, mats, cfg.applied_voltage, cfg.boundary_temp, t_it, v_it, T, dt, geom=geom)
-            x_new, st = O.gmres(s.row_ptr, s.col_idx, s.vals, s.rhs.copy(), x0=x_old.copy(),
-                                restart_m=30, tol=cfg.tolerance, precondition="jacobi")
-            if not st.converged:
-                break
-            delta = float(np.max(np.abs(x_new - x_old) / np.maximum(1.0, np.abs(x_old))))
-            v_it, t_it = x_new[0::2].copy(), x_new[1::2].copy()
-            x_old = x_new
-            if delta < cfg.corrector_tol:
-                ok = True
-                break
-        if not ok:
-            dt_cur = max(dt * 0.5, cfg.dt_min)
-            continue
-        T_prev, T, V = T, t_it, v_it
-        dt_prev = dt
-        t = cfg.total_time if last else t + dt
-        step += 1
-        dt_cur = min(dt * 1.5, cfg.dt_max) if used <= 5 else (max(dt * 0.75, cfg.dt_min) if used >= 20 else dt)
-        yield step
-
-
-# ---------------------------------------------------------------------------
-# our arm
-
-def pcg_iter_bytes(N, S):
-    """Algorithmic HBM bytes of one fused PCG iteration on the paired layout.
-
-    SpMV: 20 B per slot (int32 column + (V,T) double2) + 4(N+1) row_ptr.
-    Vectors, 16 B per node each: SpMV phase reads z, p_old; writes p, q;
-    update phase reads x, p, r, q, minv; writes x, r, z  -> 12 x 16N.
-    """
-    return 20 * S + 4 * (N + 1) + 12 * 16 * N
-
-
-def gmres_iter_bytes(N, S, k_avg):
-    """GMRES(m) CGS2 step k: SpMV + 2 passes over k+1 basis vectors + updates."""
-    n = 2 * N
-    return 20 * S + 4 * (N + 1) + 16 * N + (32 * (k_avg + 1) + 56) * n
-
-
-def run_ours(args):
-    import torch
-    rank, local, world = dist_env()
-    os.environ["RAFEM_DEVICE"] = str(local)
-    torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        import datetime
-        # a collective that never completes aborts the job instead of hanging it
-        dist.init_process_group("nccl", init_method="env://", timeout=datetime.timedelta(seconds=600))
-    from paper_2409_13036_b200 import _native as nat
-    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh, run_simulation
-    from paper_2409_13036_b200.timeloop import DeviceRun
-
-    peaks = {}
-    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(pk):
-        peaks = json.load(open(pk))
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-
-    mesh = generate_box_mesh(*MESH_B)
-    mat = MaterialParams.default()
-    cfg = SimConfig(total_time=TOTAL_TIME, solver=SolverConfig(backend=args.backend, precondition="jacobi"))
-    runner = DeviceRun(mesh, mat)
-    stream = torch.cuda.ExternalStream(nat.lib().rafem_stream(nat.context()))
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MB > L2
-
-    def one(record):
-        recs, summ = runner.run(cfg, record_fields=record)
-        return summ
-
-    for _ in range(args.warmup):
-        one(False)
-    launches0 = nat.kernel_launches()
-    times, summs = [], []
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            flush.fill_(1.0)
-            torch.cuda.synchronize()
-            if world > 1:
-                import torch.distributed as dist
-                dist.barrier()
-            ev0 = torch.cuda.Event(enable_timing=True)
-            ev1 = torch.cuda.Event(enable_timing=True)
-            ev0.record(stream)
-            summs.append(one(False))
-            ev1.record(stream)
-            ev1.synchronize()
-            times.append(ev0.elapsed_time(ev1))
-            torch.cuda.synchronize()
-    launches = nat.kernel_launches() - launches0
-    total_ms = float(sum(times))
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([total_ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    steps_per_run = summs[0].accepted_steps
-    value = world * args.steps * steps_per_run / (total_ms / 1e3)
-
-    # roofline of the dominant kernel (the persistent Krylov solve)
-    S, N = runner.dm.slots, runner.dm.node_count
-    iters = sum(s.total_solver_iterations for s in summs)
-    passes = sum(s.passes for s in summs)
-    solve_ms = sum(s.solve_ms for s in summs)
-    asm_ms = sum(s.assemble_ms for s in summs)
-    if args.backend == "pcg":
-        bytes_total = iters * pcg_iter_bytes(N, S) + passes * (20 * S + 4 * (N + 1) + 6 * 16 * N)
-    else:
-        bytes_total = iters * gmres_iter_bytes(N, S, 15) + passes * (20 * S + 4 * (N + 1) + 48 * N)
-    achieved = bytes_total / (solve_ms / 1e3) / 1e9 if solve_ms > 0 else 0.0
-    # DRAM traffic of one launch from the committed ncu --set full capture of
-    # the same command (scripts/ncu_summary.py -> profiles/traffic.json)
-    traffic = None
-    tj = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tj):
-        try:
-            traffic = json.load(open(tj)).get("simulate_kernel")
-        except Exception:  # noqa: BLE001
-            traffic = None
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": traffic,
-                "kernel": ("simulate_kernel<true> (whole run, one cooperative launch); bytes = PCG iterations"
-                           if runner.last_mode == "fused-simulation" else f"{args.backend}_grid_kernel (persistent solve)"),
-                "launches": passes, "avg_launch_us": 1e3 * solve_ms / max(passes, 1),
-                "share_of_step": solve_ms / total_ms if world == 1 else None,
-                "peak_source": peak_src,
-                "note": "paper-scale mesh: working set ~5 MB lives in L2; kernel is barrier-latency bound"}
-
-    line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
