@@ -302,10 +302,33 @@ __global__ void geometry_kernel(const double* nodes, const int* tets, int M, dou
 // numeric fill (device functions in assembly_dev.cuh)
 
 // 1. per element: sigma, the 16 (V, T) block contributions, T-rhs loads
-__global__ void element_kernel(AsmMesh m, AsmFields f, double2* contrib, double* load, unsigned long long* bad) {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= m.M) return;
-    if (element_tet(e, m, f, contrib, load)) atomicMin(bad, (unsigned long long)e);
+// 1. element kernel: a block of kElemBlock tets stages its geometry (base,
+//    gradients, volume: contiguous per block) through shared memory with
+//    coalesced loads, computes one tet per thread, and writes the block's
+//    contributions and loads back coalesced (each thread's 256 B of
+//    contributions would otherwise be 16 scattered 16-B stores).
+constexpr int kElemBlock = 64;
+__global__ void __launch_bounds__(kElemBlock) element_kernel(AsmMesh m, AsmFields f, double2* contrib, double* load,
+                                                             unsigned long long* bad) {
+    __shared__ double sgeo[kElemBlock * 23];
+    __shared__ double2 sout[kElemBlock * 16];
+    __shared__ double sload[kElemBlock * 4];
+    const long long e0 = (long long)blockIdx.x * kElemBlock;
+    const int nb = (int)min((long long)kElemBlock, (long long)m.M - e0);
+    for (int k = threadIdx.x; k < nb * 10; k += kElemBlock) sgeo[k] = __ldg(m.base + 10 * e0 + k);
+    for (int k = threadIdx.x; k < nb * 12; k += kElemBlock) sgeo[kElemBlock * 10 + k] = __ldg(m.grad + 12 * e0 + k);
+    for (int k = threadIdx.x; k < nb; k += kElemBlock) sgeo[kElemBlock * 22 + k] = __ldg(m.vol + e0 + k);
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < nb) {
+        const int e = (int)(e0 + t);
+        if (element_core(e, m, f, sgeo + 10 * t, sgeo + kElemBlock * 10 + 12 * t, sgeo[kElemBlock * 22 + t],
+                         sout + 16 * t, sload + 4 * t))
+            atomicMin(bad, (unsigned long long)e);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < nb * 16; k += kElemBlock) __stcg(contrib + 16 * e0 + k, sout[k]);
+    for (int k = threadIdx.x; k < nb * 4; k += kElemBlock) __stcg(load + 4 * e0 + k, sload[k]);
 }
 
 // 2. slot fill: one thread per slot over its contributor list, then one
@@ -329,22 +352,58 @@ __global__ void __launch_bounds__(256) fill_kernel(AsmMesh m, const double2* con
     fill_node_warp(i, m, contrib, load, val2 + __ldg(m.rp + i), rhs, diag_raw, ws[threadIdx.x >> 5]);
 }
 
-// 3. scale = 2^round(log2(sum diag_T / sum diag_V)) from a fixed-order
-//    reduction (one CTA, so the bits never depend on the grid).
-__global__ void __launch_bounds__(1024) equil_kernel(const double* diag_raw, int N, int equilibrate,
-                                                     double* scale_out) {
-    __shared__ double red[32 * 2];
+// 3. scale = 2^round(log2(sum diag_T / sum diag_V)) (fem.py:390-396) from
+//    the raw diagonal sums:
+// 3'. the same sums over n rows in two deterministic stages (G CTAs over
+//     contiguous chunks, then one CTA over the G partials in order), for
+//     large meshes where one CTA walking every row costs milliseconds
+__global__ void __launch_bounds__(256) diag_partial_kernel(const double* diag_raw, int n, int chunk, double* part) {
+    __shared__ double red[64];
+    const int r0 = blockIdx.x * chunk, r1 = min(n, r0 + chunk);
     double v[2] = {0.0, 0.0};
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
         v[0] = add(v[0], diag_raw[2LL * i]);
         v[1] = add(v[1], diag_raw[2LL * i + 1]);
     }
     block_sum<2>(v, red);
     if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = v[0];
+        part[2 * blockIdx.x + 1] = v[1];
+    }
+}
+__global__ void diag_finish_kernel(const double* part, int G, int equilibrate, double* sums, double* scale_out) {
+    if (threadIdx.x != 0) return;
+    double a = 0.0, b = 0.0;
+    for (int c = 0; c < G; ++c) {
+        a = add(a, part[2 * c]);
+        b = add(b, part[2 * c + 1]);
+    }
+    if (sums) {
+        sums[0] = a;
+        sums[1] = b;
+    }
+    if (scale_out) {
         double scale = 1.0;
-        if (equilibrate && v[0] > 0.0 && v[1] > 0.0) scale = ldexp(1.0, (int)rint(log2(v[1] / v[0])));
+        if (equilibrate && a > 0.0 && b > 0.0) scale = ldexp(1.0, (int)rint(log2(b / a)));
         *scale_out = scale;
     }
+}
+
+int diag_sums_launch(rafem_ctx* ctx, const double* diag_raw, int n, int equilibrate, double* sums_dev,
+                     double* scale_dev) {
+    const int chunk = 8192;
+    const int G = std::max(1, (n + chunk - 1) / chunk);
+    if (int rc = ensure(ctx, ctx->ws_diag, sizeof(double) * 2 * (size_t)G)) return rc;
+    double* part = static_cast<double*>(ctx->ws_diag.p);
+    if (n > 0) {
+        diag_partial_kernel<<<G, 256, 0, ctx->stream>>>(diag_raw, n, chunk, part);
+    } else {
+        RF_CUDA_TRY(ctx, cudaMemsetAsync(part, 0, sizeof(double) * 2, ctx->stream));
+    }
+    diag_finish_kernel<<<1, 32, 0, ctx->stream>>>(part, G, equilibrate, sums_dev, scale_dev);
+    ctx->launches += 2;
+    RF_CUDA_TRY(ctx, cudaGetLastError());
+    return RAFEM_OK;
 }
 
 // 4. voltage-row scaling and symmetric Dirichlet elimination, one warp per node row
@@ -532,7 +591,7 @@ int assemble_fill_launch(rafem_system* s, const double* t_it, int ts, const doub
     double2* val2 = reinterpret_cast<double2*>(s->val2);
     RF_CUDA_TRY(ctx, cudaMemsetAsync(bad_dev, 0xff, sizeof(long long), st));
     if (M > 0) {
-        element_kernel<<<(M + 127) / 128, 128, 0, st>>>(am, f, contrib, s->load,
+        element_kernel<<<(M + kElemBlock - 1) / kElemBlock, kElemBlock, 0, st>>>(am, f, contrib, s->load,
                                                         reinterpret_cast<unsigned long long*>(bad_dev));
         ctx->launches++;
     }
@@ -579,10 +638,10 @@ int assemble_launch(rafem_system* s, const double* t_it, int ts, const double* v
     if (int rc = assemble_fill_launch(s, t_it, ts, v_it, vs, t_prev, ps, p.dt, bad_dev)) return rc;
     if (N > 0) {
         const int blocks = (int)(((long long)N * 32 + 255) / 256);
-        equil_kernel<<<1, 1024, 0, st>>>(s->diagpart, N, p.equilibrate, scale_dev);
+        if (int rc = diag_sums_launch(ctx, s->diagpart, N, p.equilibrate, nullptr, scale_dev)) return rc;
         constrain_kernel<<<blocks, 256, 0, st>>>(asm_mesh(m), scale_dev, p.apply_constraints, p.applied_voltage,
                                                  p.boundary_temp, reinterpret_cast<double2*>(s->val2), s->rhs);
-        ctx->launches += 2;
+        ctx->launches += 1;
     } else {
         RF_CUDA_TRY(ctx, cudaMemcpyAsync(scale_dev, &s->scale, sizeof(double), cudaMemcpyHostToDevice, st));
     }

@@ -60,8 +60,11 @@ RF_DEV int sym_index(int a, int b) {
 }
 
 // Element e: 16 (V, T) block contributions in (a, b) row-major order and the
-// four T-rhs loads.  Returns true when sigma(Tbar) <= 0 (PhysicsRangeError).
-RF_DEV bool element_tet(int e, const AsmMesh& m, const AsmFields& f, double2* contrib, double* load) {
+// four T-rhs loads, from the element's packed base (10), gradients (12) and
+// volume wherever they are staged.  Returns true when sigma(Tbar) <= 0
+// (PhysicsRangeError).
+RF_DEV bool element_core(int e, const AsmMesh& m, const AsmFields& f, const double* b10, const double* g12,
+                         double vol, double2* out16, double* out4) {
     int nd[4];
 #pragma unroll
     for (int a = 0; a < 4; ++a) nd[a] = __ldg(m.tets + 4 * e + a);
@@ -82,10 +85,6 @@ RF_DEV bool element_tet(int e, const AsmMesh& m, const AsmFields& f, double2* co
     for (int a = 0; a < 4; ++a) tsum = add(tsum, tv[a]);
     const double tbar = tsum / 4.0;
     const double sigma = mul(sigma0, add(1.0, mul(alpha, sub(tbar, tref))));
-    const double vol = __ldg(m.vol + e);
-    double b10[10];
-#pragma unroll
-    for (int k = 0; k < 10; ++k) b10[k] = __ldg(m.base + 10LL * e + k);
     const double mdia = mul(vol, 0.1), moff = mul(vol, 0.05);  // vol (1 + d_ab) / 20
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -93,13 +92,13 @@ RF_DEV bool element_tet(int e, const AsmMesh& m, const AsmFields& f, double2* co
         for (int b = 0; b < 4; ++b) {
             const double bab = b10[sym_index(a, b)];
             const double mass = a == b ? mdia : moff;
-            contrib[16LL * e + 4 * a + b] = make_double2(mul(sigma, bab), add(mul(rcdt, mass), mul(kk, bab)));
+            out16[4 * a + b] = make_double2(mul(sigma, bab), add(mul(rcdt, mass), mul(kk, bab)));
         }
     double gv[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int d = 0; d < 3; ++d) gv[d] = add(gv[d], mul(vv[a], __ldg(m.grad + 12LL * e + 3 * a + d)));
+        for (int d = 0; d < 3; ++d) gv[d] = add(gv[d], mul(vv[a], g12[3 * a + d]));
     const double gg = add(add(mul(gv[0], gv[0]), mul(gv[2], gv[2])), mul(gv[1], gv[1]));
     const double fj = mul(mul(sigma, gg), vol) / 4.0;
     const double mo = mul(rcdt, moff), md = mul(rcdt, mdia);
@@ -108,9 +107,19 @@ RF_DEV bool element_tet(int e, const AsmMesh& m, const AsmFields& f, double2* co
         double t[4];
 #pragma unroll
         for (int b = 0; b < 4; ++b) t[b] = mul(a == b ? md : mo, tp[b]);
-        load[4LL * e + a] = add(add(add(t[0], t[2]), add(t[1], t[3])), fj);
+        out4[a] = add(add(add(t[0], t[2]), add(t[1], t[3])), fj);
     }
     return sigma <= 0.0;  // fem.py:274
+}
+
+// The same, reading the geometry and writing the outputs in global memory.
+RF_DEV bool element_tet(int e, const AsmMesh& m, const AsmFields& f, double2* contrib, double* load) {
+    double b10[10], g12[12];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) b10[k] = __ldg(m.base + 10LL * e + k);
+#pragma unroll
+    for (int k = 0; k < 12; ++k) g12[k] = __ldg(m.grad + 12LL * e + k);
+    return element_core(e, m, f, b10, g12, __ldg(m.vol + e), contrib + 16LL * e, load + 4LL * e);
 }
 
 // Per-warp staging for one node row's incident elements.

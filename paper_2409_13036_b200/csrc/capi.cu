@@ -197,7 +197,8 @@ void rafem_ctx_destroy(rafem_ctx* ctx) {
     if (!ctx) return;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (DevBuf* b : {&ctx->ws_basis, &ctx->ws_vec, &ctx->ws_partial, &ctx->ws_hess, &ctx->ws_hist,
-                      &ctx->ws_cyc, &ctx->ws_part, &ctx->ws_res, &ctx->ws_trace, &ctx->ws_flags, &ctx->ws_simout})
+                      &ctx->ws_cyc, &ctx->ws_part, &ctx->ws_res, &ctx->ws_trace, &ctx->ws_flags, &ctx->ws_simout,
+                      &ctx->ws_diag})
         if (b->p) cudaFree(b->p);
     if (ctx->pin) cudaFreeHost(ctx->pin);
     for (auto& e : ctx->part_cache) cudaFree(e.gpart);

@@ -92,6 +92,7 @@ struct rafem_ctx {
     rafem::DevBuf ws_trace;
     rafem::DevBuf ws_flags;     // grid barrier / all-reduce slots
     rafem::DevBuf ws_simout;    // fused simulation summary
+    rafem::DevBuf ws_diag;      // diagonal-sum partials of the assembly
     unsigned epoch = 0;         // per-launch flag epoch
     int last_mode = -1;  // 1: cluster-resident solve, 0: grid-wide cooperative solve
     int last_ctas = 0;
@@ -202,6 +203,10 @@ int kp_system_solve(rafem_system* s, const double* b, const double* x0, const ra
 int assemble_fill_launch(rafem_system* s, const double* t_it, int ts, const double* v_it, int vs,
                          const double* t_prev, int ps, double dt, long long* bad_dev);
 int assemble_constrain_launch(rafem_system* s, const rafem_assemble_params& p, double scale);
+// (sum of V, sum of T) raw diagonal entries of the first n node rows, two
+// deterministic stages; sums_dev (2 doubles) and/or the equilibration scale
+int diag_sums_launch(rafem_ctx* ctx, const double* diag_raw, int n, int equilibrate, double* sums_dev,
+                     double* scale_dev);
 int expand_dof_vals(rafem_system* s, double* out_dev);
 int predictor_launch(rafem_ctx* ctx, double* x_it, const double* x_acc, const double* x_prev,
                      int N, int step, double ratio);

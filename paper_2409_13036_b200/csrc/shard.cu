@@ -410,21 +410,6 @@ __global__ void kp_pack_kernel(KPArgs a, int idx, int which, int force) {
         a.send_buf[k] = v[__ldg(a.send_idx + k)];
 }
 
-// owned-row diagonal sums (V, T) in a fixed order (one CTA)
-__global__ void __launch_bounds__(1024) diag_sums_kernel(const double* diag_raw, int n_own, double* out) {
-    __shared__ double red[64];
-    double v[2] = {0.0, 0.0};
-    for (int i = threadIdx.x; i < n_own; i += blockDim.x) {
-        v[0] = add(v[0], diag_raw[2LL * i]);
-        v[1] = add(v[1], diag_raw[2LL * i + 1]);
-    }
-    block_sum<2>(v, red);
-    if (threadIdx.x == 0) {
-        out[0] = v[0];
-        out[1] = v[1];
-    }
-}
-
 }  // namespace rafem
 
 using namespace rafem;
@@ -813,12 +798,7 @@ int rafem_assemble_partial(rafem_system* s, const double* t_iter, const double* 
     double* dsum = reinterpret_cast<double*>(s->status) + 96;  // scratch past the pass status
     long long* dbad = reinterpret_cast<long long*>(s->status) + 100;
     if (int rc = assemble_fill_launch(s, s->xin, 1, s->xin + N, 1, s->xin + 2 * (size_t)N, 1, p->dt, dbad)) return rc;
-    if (n_owned > 0) {
-        diag_sums_kernel<<<1, 1024, 0, ctx->stream>>>(s->diagpart, (int)n_owned, dsum);
-        ctx->launches++;
-    } else {
-        RF_CUDA_TRY(ctx, cudaMemsetAsync(dsum, 0, 2 * sizeof(double), ctx->stream));
-    }
+    if (int rc = diag_sums_launch(ctx, s->diagpart, (int)n_owned, 0, dsum, nullptr)) return rc;
     double* hp = pin + 3 * (size_t)std::max(N, 1);
     RF_CUDA_TRY(ctx, cudaMemcpyAsync(hp, dsum, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     long long hb = -1;
