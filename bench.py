@@ -374,7 +374,7 @@ def run_ours(args):
         line["e2e_plugin_seam"] = e2e_plugin_leg(mesh, mat, args, run_simulation, SimConfig, SolverConfig, world)
     if rank == 0 and not args.no_c3:
         try:
-            line["spmv_c3"] = c3_leg(hbm_peak, peak_src)
+            line["spmv_c3"] = c3_leg(hbm_peak, peak_src, cpu_on=not args.no_cpu)
         except Exception as exc:  # noqa: BLE001
             line["spmv_c3"] = {"error": str(exc)[:300]}
     if not args.no_c4:
@@ -513,7 +513,7 @@ def c4_leg(hbm_peak, peak_src, world, rank, local):
             "kernel": "kp_spmv_kernel + kp_update_kernel (csrc/shard.cu)"}
 
 
-def c3_leg(hbm_peak, peak_src):
+def c3_leg(hbm_peak, peak_src, cpu_on=True):
     """1M-dof roofline study (configs[2]): SpMV and cold PCG solve on the device."""
     from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, assemble_global, generate_box_mesh, solve
     mesh = generate_box_mesh(80, 80, 79)
@@ -538,11 +538,32 @@ def c3_leg(hbm_peak, peak_src):
     x, st = solve(s.matrix, s.rhs, x0=x0, config=SolverConfig(backend="pcg", precondition="jacobi"))
     it_bytes = pcg_iter_bytes(N, S)
     solve_ach = st.iterations * it_bytes / (st.device_ms / 1e3) / 1e9 if st.device_ms else 0.0
-    return {"workload": "generate_box_mesh(80,80,79) cold system, 1,011,200 dofs",
+    cpu = {}
+    if cpu_on:
+        # the same matrix through the oracle port (reference arithmetic) on 1 core
+        try:
+            from oracle import rafem_oracle as O
+            a = s.matrix
+            rp, ci, va = a.row_ptr, a.col_idx, a.vals
+            xr = np.random.default_rng(3).standard_normal(2 * n)
+            t0 = time.perf_counter()
+            for _ in range(3):
+                O.matvec(rp, ci, va, xr)
+            cpu_spmv = (time.perf_counter() - t0) / 3
+            t0 = time.perf_counter()
+            _, so = O.gmres(rp, ci, va, s.rhs, x0=x0, restart_m=30, tol=1e-10, max_total_iters=5,
+                            precondition="jacobi")
+            cpu_git = (time.perf_counter() - t0) / max(so.iterations, 1)
+            cpu = {"kind": "port", "cores": 1, "spmv_ms": 1e3 * cpu_spmv, "gmres_ms_per_iteration": 1e3 * cpu_git,
+                   "spmv_speedup": cpu_spmv / (ms.value / 1e3),
+                   "sample": "3 oracle SpMVs and a 5-iteration GMRES(30)+Jacobi on the same matrix"}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"error": str(exc)[:200]}
+    return {"workload": "generate_box_mesh(80,80,79) cold system, 1,011,200 dofs", "cpu_baseline": cpu,
             "spmv": {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
                      "frac_of_8TBs": ach / 8000.0, "us_per_launch": 1e3 * ms.value,
                      "bytes_per_launch": b_paired, "layout": "node-paired CSR (int32 col + double2 per slot)",
-                     "kernel": "spmv_tma_kernel (TMA bulk-staged slot tiles, left-to-right rows)",
+                     "kernel": "spmv_tma_pipe_kernel (TMA bulk-staged slot tiles, left-to-right rows)",
                      "thread_per_row_kernel_GBs": b_paired / (ms_plain.value / 1e3) / 1e9,
                      "csr_equivalent_bytes": b_csr, "csr_equivalent_GBs": b_csr / (ms.value / 1e3) / 1e9,
                      "peak_source": peak_src},
