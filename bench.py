@@ -487,20 +487,22 @@ def c4_leg(hbm_peak, peak_src, world, rank, local):
                                         max_total_iters=20))  # warm (communicators, caches)
     x, st = sh.solve(x0=x0, config=cfg)
     dev_ms, wall_ms = float(st.device_ms), st.wall_ns / 1e6
-    slots = sh.dm.slots
     own_slots = int(sh.dm.dof_row_ptr[2 * p.n_own] // 2)
+    cls_on = (int(nat.lib().rafem_mesh_stencil_classes(sh.dm.handle)) > 0
+              and os.environ.get("RAFEM_NO_CLASSES", "0") != "1")
+    # KP iteration bytes of this shard: SpMV (20 B/slot, or 16 B/slot + 1 B/row
+    # with stencil-class columns) + 7 vector reads / 5 writes + u gather + w write
+    mine = ((16 * own_slots + p.n_own) if cls_on else 20 * own_slots) + 4 * (p.n_own + 1) + 14 * 16 * p.n_own
     if world > 1:
         import torch.distributed as dist
         tt_ = torch.tensor([dev_ms, wall_ms, asm_s], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
         dev_ms, wall_ms, asm_s = (float(v) for v in tt_.tolist())
-        s_ = torch.tensor([own_slots], device=f"cuda:{local}", dtype=torch.float64)
+        s_ = torch.tensor([float(mine)], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(s_)
-        own_slots = int(s_.item())
+        mine = int(s_.item())
     it = st.iterations
-    N = n
-    S = own_slots
-    bytes_it = 20 * S + 4 * (N + 1) + 14 * 16 * N  # KP iteration: SpMV + 7 reads / 5 writes + u gather, w write
+    bytes_it = mine
     ach = it * bytes_it / (dev_ms / 1e3) / 1e9 if dev_ms > 0 else 0.0
     return {"workload": "generate_box_mesh(200,200,200) cold system, 16,000,000 dofs",
             "shards": world, "partition": "contiguous node-row blocks (x-slabs)",
@@ -509,7 +511,8 @@ def c4_leg(hbm_peak, peak_src, world, rank, local):
             "solve_device_ms_max_over_ranks": dev_ms, "solve_wall_ms": wall_ms,
             "us_per_iteration": 1e3 * dev_ms / max(it, 1),
             "aggregate_GBs": ach, "frac_of_1gpu_peak": ach / hbm_peak / world, "peak_source": peak_src,
-            "bytes_per_iteration": bytes_it, "assembly_s": asm_s, "setup_s": setup_s,
+            "bytes_per_iteration": bytes_it, "columns": "stencil classes" if cls_on else "explicit int32",
+            "assembly_s": asm_s, "setup_s": setup_s,
             "kernel": "kp_spmv_kernel + kp_update_kernel (csrc/shard.cu)"}
 
 
@@ -524,18 +527,29 @@ def c3_leg(hbm_peak, peak_src, cpu_on=True):
     import ctypes as C
     from paper_2409_13036_b200 import _native as nat
     ms = C.c_double()
-    nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 50, C.byref(ms)), "spmv bench")
+    nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 50, 1, C.byref(ms)), "spmv bench")
     os.environ["RAFEM_NO_TMA_SPMV"] = "1"
     ms_plain = C.c_double()
-    nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 50, C.byref(ms_plain)), "spmv bench")
+    nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 50, 1, C.byref(ms_plain)), "spmv bench")
     del os.environ["RAFEM_NO_TMA_SPMV"]
     S, N = h.mesh.slots, n
-    b_paired = 20 * S + 4 * (N + 1) + 16 * N + 16 * N
+    ncls = int(nat.lib().rafem_mesh_stencil_classes(h.mesh.handle))
+    cls_on = ncls > 0 and os.environ.get("RAFEM_NO_CLASSES", "0") != "1"
+    b_explicit = 20 * S + 4 * (N + 1) + 16 * N + 16 * N
+    # bytes of the layout the kernel streams: with stencil classes only the
+    # (V, T) values per slot plus a class byte per row
+    b_paired = (16 * S + N + 4 * (N + 1) + 32 * N) if cls_on else b_explicit
     b_csr = 12 * (2 * S) + 4 * (2 * N + 1) + 8 * 2 * N + 8 * 2 * N
     ach = b_paired / (ms.value / 1e3) / 1e9
     x0 = np.empty(2 * n)
     x0[0::2], x0[1::2] = 0.0, 37.0
+    import torch
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    solve(s.matrix, s.rhs, x0=x0, config=SolverConfig(backend="pcg", precondition="jacobi"))  # warm
+    flush.fill_(2.0)
+    torch.cuda.synchronize()
     x, st = solve(s.matrix, s.rhs, x0=x0, config=SolverConfig(backend="pcg", precondition="jacobi"))
+    del flush
     it_bytes = pcg_iter_bytes(N, S)
     solve_ach = st.iterations * it_bytes / (st.device_ms / 1e3) / 1e9 if st.device_ms else 0.0
     cpu = {}
@@ -564,10 +578,14 @@ def c3_leg(hbm_peak, peak_src, cpu_on=True):
                      "frac_of_8TBs": ach / 8000.0, "us_per_launch": 1e3 * ms.value,
                      "bytes_per_launch": b_paired, "layout": "node-paired CSR (int32 col + double2 per slot)",
                      "kernel": "spmv_tma_pipe_kernel (TMA bulk-staged slot tiles, left-to-right rows)",
-                     "thread_per_row_kernel_GBs": b_paired / (ms_plain.value / 1e3) / 1e9,
+                     "thread_per_row_kernel_GBs": b_explicit / (ms_plain.value / 1e3) / 1e9,
                      "csr_equivalent_bytes": b_csr, "csr_equivalent_GBs": b_csr / (ms.value / 1e3) / 1e9,
-                     "peak_source": peak_src},
-            "pcg_cold_solve": {"iterations": st.iterations, "device_ms": st.device_ms,
+                     "columns": (f"stencil classes ({ncls}; computed, values-only TMA stream)" if cls_on
+                                 else "explicit int32 columns"),
+                     "explicit_columns_equivalent_GBs": b_explicit / (ms.value / 1e3) / 1e9,
+                     "l2": "flushed (256 MB write) before every timed launch", "peak_source": peak_src},
+            "pcg_cold_solve": {"l2": "flushed before the solve; iterations back to back",
+                               "iterations": st.iterations, "device_ms": st.device_ms,
                                "us_per_iteration": 1e3 * st.device_ms / max(st.iterations, 1),
                                "achieved_GBs": solve_ach, "frac": solve_ach / hbm_peak,
                                "final_relative_residual": st.final_relative_residual}}

@@ -169,6 +169,13 @@ int rafem_mesh_create(rafem_ctx* ctx, int64_t n_nodes, const double* nodes, int6
 void rafem_mesh_destroy(rafem_mesh* mesh);
 /* node-pattern size (slots); the dof CSR has 2*slots entries */
 int64_t rafem_mesh_slots(const rafem_mesh* mesh);
+/* stencil classes of the node pattern (built on first call): rows whose
+ * column offsets (col - row) coincide share a class, and the streaming
+ * SpMV kernels compute their columns instead of reading them (16 instead
+ * of 20 bytes per slot).  Returns the class count, 0 when the pattern has
+ * more than 255 distinct rows (unstructured meshes keep explicit columns),
+ * -1 on error. */
+int32_t rafem_mesh_stencil_classes(rafem_mesh* mesh);
 /* node-level pattern: row_ptr (N+1), col (slots) */
 int rafem_mesh_pattern(rafem_mesh* mesh, int64_t* node_row_ptr, int32_t* node_col);
 
@@ -187,9 +194,10 @@ int rafem_system_solve(rafem_system* sys, const double* b, const double* x0,
                        double* hist, int64_t hist_cap, int64_t* cycle_lens, int64_t cycle_cap);
 /* y = A x on the device-resident system (dof vectors, host) */
 int rafem_system_spmv(rafem_system* sys, const double* x, double* y);
-/* device-only SpMV timing: `reps` back-to-back launches of the standalone
- * SpMV kernel on a device-resident x, mean CUDA-event ms per launch */
-int rafem_system_spmv_bench(rafem_system* sys, int32_t reps, double* ms_per_launch);
+/* device-only SpMV timing on a device-resident x, mean CUDA-event ms per
+ * launch: `reps` back-to-back launches, or (flush_l2) each launch timed
+ * alone after a 256 MB write that evicts L2 */
+int rafem_system_spmv_bench(rafem_system* sys, int32_t reps, int32_t flush_l2, double* ms_per_launch);
 
 /* ---- native time loop (fem.py:554-644 around the device path) ------------ */
 /* Runs run_simulation's adaptive predictor-corrector loop with mesh, system,

@@ -89,6 +89,7 @@ _SIGS = {
     "rafem_mesh_create": (i32, [vp, i64, vp, i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, P(vp)]),
     "rafem_mesh_destroy": (None, [vp]),
     "rafem_mesh_slots": (i64, [vp]),
+    "rafem_mesh_stencil_classes": (i32, [vp]),
     "rafem_mesh_pattern": (i32, [vp, vp, vp]),
     "rafem_system_create": (i32, [vp, P(vp)]),
     "rafem_system_destroy": (None, [vp]),
@@ -96,7 +97,7 @@ _SIGS = {
     "rafem_system_download": (i32, [vp, vp, vp]),
     "rafem_system_solve": (i32, [vp, vp, vp, P(SolverParams), vp, P(SolveStatsC), vp, i64, vp, i64]),
     "rafem_system_spmv": (i32, [vp, vp, vp]),
-    "rafem_system_spmv_bench": (i32, [vp, i32, P(f64)]),
+    "rafem_system_spmv_bench": (i32, [vp, i32, i32, P(f64)]),
     "rafem_simulate": (i32, [vp, P(SimParams), P(SimSummaryC), i64, vp, vp, vp, vp, vp]),
     "rafem_mesh_create_box": (i32, [vp, i32, i32, i32, vp, vp, i64, vp, i64, f64, f64, f64, f64, f64, P(vp)]),
     "rafem_mesh_counts": (i64, [vp, P(i64)]),

@@ -536,6 +536,103 @@ int mesh_slot_lists(rafem_mesh* m) {
     return RAFEM_OK;
 }
 
+// Stencil classes.  A row's signature is its length and its column offsets
+// (col - row), sorted like the columns; rows with the same signature share
+// a class, and the SpMV kernels then compute columns instead of streaming
+// them (4 of the 20 bytes per slot).  64-bit FNV-1a hashes on the device,
+// classes assigned on the host, every row verified against its class on
+// the device (a hash collision disables the classes).
+__global__ void row_sig_kernel(const int* rp, const int* col, int N, unsigned long long* sig) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    unsigned long long h = 1469598103934665603ULL;
+    const int s0 = rp[i], s1 = rp[i + 1];
+    h = (h ^ (unsigned long long)(s1 - s0)) * 1099511628211ULL;
+    for (int s = s0; s < s1; ++s) h = (h ^ (unsigned long long)(unsigned)(col[s] - i)) * 1099511628211ULL;
+    sig[i] = h;
+}
+__global__ void cls_verify_kernel(const int* rp, const int* col, int N, const uint8_t* cls, const int* off,
+                                  const int* deg, int* bad) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int c = cls[i], s0 = rp[i], d = rp[i + 1] - s0;
+    bool ok = d == deg[c];
+    for (int k = 0; ok && k < d; ++k) ok = col[s0 + k] - i == off[c * kClsWidth + k];
+    if (!ok) atomicOr(bad, 1);
+}
+
+int mesh_stencil_classes(rafem_mesh* m) {
+    rafem_ctx* ctx = m->ctx;
+    cudaStream_t st = ctx->stream;
+    m->cls_tried = true;
+    const int N = m->N;
+    if (N <= 0 || m->maxdeg > kClsWidth) return RAFEM_OK;
+    unsigned long long* dsig = nullptr;
+    RF_CUDA_TRY(ctx, cudaMalloc(&dsig, sizeof(unsigned long long) * N));
+    row_sig_kernel<<<(N + 255) / 256, 256, 0, st>>>(m->rp, m->col, N, dsig);
+    ctx->launches++;
+    std::vector<unsigned long long> sig(N);
+    std::vector<int> rp(N + 1);
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(sig.data(), dsig, sizeof(unsigned long long) * N, cudaMemcpyDeviceToHost, st));
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(rp.data(), m->rp, sizeof(int) * (N + 1), cudaMemcpyDeviceToHost, st));
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    cudaFree(dsig);
+    std::vector<uint8_t> cls(N);
+    std::vector<unsigned long long> keys;
+    std::vector<int> rep;
+    for (int i = 0; i < N; ++i) {
+        int c = -1;
+        for (size_t k = 0; k < keys.size(); ++k)
+            if (keys[k] == sig[i]) {
+                c = (int)k;
+                break;
+            }
+        if (c < 0) {
+            if ((int)keys.size() >= kMaxClasses) return RAFEM_OK;  // unstructured: explicit columns
+            c = (int)keys.size();
+            keys.push_back(sig[i]);
+            rep.push_back(i);
+        }
+        cls[i] = (uint8_t)c;
+    }
+    const int ncls = (int)keys.size();
+    std::vector<int> off((size_t)ncls * kClsWidth, 0), deg(ncls);
+    for (int c = 0; c < ncls; ++c) {
+        const int i = rep[c], d = rp[i + 1] - rp[i];
+        deg[c] = d;
+        std::vector<int> cc(d);
+        RF_CUDA_TRY(ctx, cudaMemcpy(cc.data(), m->col + rp[i], sizeof(int) * d, cudaMemcpyDeviceToHost));
+        for (int k = 0; k < d; ++k) off[(size_t)c * kClsWidth + k] = cc[k] - i;
+    }
+    uint8_t* dcls = nullptr;
+    int* doff = nullptr;
+    int* ddeg = nullptr;
+    int* dbad = nullptr;
+    RF_CUDA_TRY(ctx, cudaMalloc(&dcls, N));
+    RF_CUDA_TRY(ctx, cudaMalloc(&doff, sizeof(int) * off.size()));
+    RF_CUDA_TRY(ctx, cudaMalloc(&ddeg, sizeof(int) * ncls + sizeof(int)));
+    dbad = ddeg + ncls;
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(dcls, cls.data(), N, cudaMemcpyHostToDevice, st));
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(doff, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice, st));
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(ddeg, deg.data(), sizeof(int) * ncls, cudaMemcpyHostToDevice, st));
+    RF_CUDA_TRY(ctx, cudaMemsetAsync(dbad, 0, sizeof(int), st));
+    cls_verify_kernel<<<(N + 255) / 256, 256, 0, st>>>(m->rp, m->col, N, dcls, doff, ddeg, dbad);
+    ctx->launches++;
+    int hbad = 0;
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    cudaFree(ddeg);
+    if (hbad) {  // hash collision: keep explicit columns
+        cudaFree(dcls);
+        cudaFree(doff);
+        return RAFEM_OK;
+    }
+    m->cls = dcls;
+    m->cls_off = doff;
+    m->ncls = ncls;
+    return RAFEM_OK;
+}
+
 int mesh_geometry(rafem_mesh* m) {
     rafem_ctx* ctx = m->ctx;
     const int M = m->M;

@@ -92,6 +92,8 @@ int check_params(rafem_ctx* ctx, const rafem_solver_params* p) {
 }
 
 MatView system_view(rafem_system* s) {
+    // stencil classes pay off only when the matrix streams from HBM
+    if (!s->mesh->cls_tried && (long long)s->mesh->slots * 20 > (48LL << 20)) mesh_stencil_classes(s->mesh);
     MatView A;
     A.rp = s->mesh->rp;
     A.col = s->mesh->col;
@@ -101,6 +103,9 @@ MatView system_view(rafem_system* s) {
     A.slots = s->mesh->slots;
     A.pattern_id = s->mesh->id;
     A.maxdeg = s->mesh->maxdeg;
+    A.cls = s->mesh->cls;
+    A.cls_off = s->mesh->cls_off;
+    A.ncls = s->mesh->ncls;
     return A;
 }
 
@@ -425,12 +430,18 @@ void rafem_mesh_destroy(rafem_mesh* m) {
     for (void* p : {(void*)m->nodes, (void*)m->tets, (void*)m->region, (void*)m->regtab, (void*)m->kind,
                     (void*)m->rp, (void*)m->col, (void*)m->diag, (void*)m->inc_ptr, (void*)m->inc_ea,
                     (void*)m->inc_slot, (void*)m->base, (void*)m->grad, (void*)m->vol, (void*)m->slot_ptr,
-                    (void*)m->slot_src})
+                    (void*)m->slot_src, (void*)m->cls, (void*)m->cls_off})
         if (p) cudaFree(p);
     delete m;
 }
 
 int64_t rafem_mesh_slots(const rafem_mesh* m) { return m ? m->slots : -1; }
+
+int32_t rafem_mesh_stencil_classes(rafem_mesh* m) {
+    if (!m) return -1;
+    if (!m->cls_tried && mesh_stencil_classes(m) != RAFEM_OK) return -1;
+    return m->ncls;
+}
 
 int rafem_mesh_pattern(rafem_mesh* m, int64_t* node_row_ptr, int32_t* node_col) {
     if (!m) return RAFEM_ERR_INVALID;
@@ -548,7 +559,7 @@ int rafem_system_spmv(rafem_system* s, const double* x, double* y) {
     return RAFEM_OK;
 }
 
-int rafem_system_spmv_bench(rafem_system* s, int32_t reps, double* ms_per_launch) {
+int rafem_system_spmv_bench(rafem_system* s, int32_t reps, int32_t flush_l2, double* ms_per_launch) {
     if (!s || reps < 1) return RAFEM_ERR_INVALID;
     rafem_ctx* ctx = s->mesh->ctx;
     const size_t n2 = 2 * (size_t)s->mesh->N;
@@ -557,14 +568,37 @@ int rafem_system_spmv_bench(rafem_system* s, int32_t reps, double* ms_per_launch
     if (int rc = fill_initial(ctx, dx, s->mesh->N, 1.25)) return rc;
     const MatView A = system_view(s);
     if (int rc = spmv_launch(ctx, A, dx, dy)) return rc;  // warm-up
-    RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
-    for (int r = 0; r < reps; ++r)
-        if (int rc = spmv_launch(ctx, A, dx, dy)) return rc;
-    RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
-    RF_CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
-    float ms = 0.f;
-    RF_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-    *ms_per_launch = ms / reps;
+    if (!flush_l2) {
+        RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+        for (int r = 0; r < reps; ++r)
+            if (int rc = spmv_launch(ctx, A, dx, dy)) return rc;
+        RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+        RF_CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
+        float ms = 0.f;
+        RF_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        *ms_per_launch = ms / reps;
+        return RAFEM_OK;
+    }
+    // cold L2: a 256 MB write between launches, each launch timed alone
+    void* flush = nullptr;
+    const size_t fb = 256u << 20;
+    RF_CUDA_TRY(ctx, cudaMalloc(&flush, fb));
+    double total = 0.0;
+    for (int r = 0; r < reps; ++r) {
+        RF_CUDA_TRY(ctx, cudaMemsetAsync(flush, r & 0xff, fb, ctx->stream));
+        RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+        if (int rc = spmv_launch(ctx, A, dx, dy)) {
+            cudaFree(flush);
+            return rc;
+        }
+        RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+        RF_CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
+        float ms = 0.f;
+        RF_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        total += ms;
+    }
+    cudaFree(flush);
+    *ms_per_launch = total / reps;
     return RAFEM_OK;
 }
 

@@ -55,7 +55,14 @@ struct MatView {
     long long slots;
     unsigned long long pattern_id = 0;  // nonzero: partitions may be cached
     int maxdeg = 0;                     // max slots per row group (0: unknown)
+    // stencil classes (structured meshes): column k of row g is
+    // g + cls_off[cls[g] * kClsWidth + k]; null = explicit columns only
+    const uint8_t* cls = nullptr;
+    const int* cls_off = nullptr;
+    int ncls = 0;
 };
+constexpr int kClsWidth = 16;   // max row length of a stencil class
+constexpr int kMaxClasses = 255;
 
 struct PartCacheEntry {
     unsigned long long pattern_id;
@@ -133,6 +140,10 @@ struct rafem_mesh {
     int* slot_ptr = nullptr;  // slots + 1: per-slot contributor lists
     int* slot_src = nullptr;  // 16M: contribution index 16 e + 4 a + b (ascending e per slot)
     bool slot_lists_tried = false;
+    uint8_t* cls = nullptr;   // N stencil class per node row (null: none)
+    int* cls_off = nullptr;   // ncls x kClsWidth column offsets
+    int ncls = 0;
+    bool cls_tried = false;
     // geometry (constant per mesh)
     double* base = nullptr;   // M x 10: vol * grad_a . grad_b, symmetric packed
     double* grad = nullptr;   // M x 12
@@ -192,6 +203,9 @@ int vec_delta_launch(rafem_ctx* ctx, const double* xn, const double* xo, int n, 
 int mesh_symbolic(rafem_mesh* m);
 int mesh_geometry(rafem_mesh* m);
 int mesh_slot_lists(rafem_mesh* m);  // per-slot contributor lists (built on first use)
+// stencil classes of the node pattern (built on first use; none when the
+// rows have more than kMaxClasses distinct offset signatures)
+int mesh_stencil_classes(rafem_mesh* m);
 int assemble_launch(rafem_system* s, const double* t_it, int ts, const double* v_it, int vs,
                     const double* t_prev, int ps, const rafem_assemble_params& p,
                     double* scale_dev, long long* bad_dev);

@@ -1676,14 +1676,21 @@ __global__ void __launch_bounds__(256, 1) spmv_tma_kernel(MatView A, const doubl
 // row's stored order, left to right, so y stays bit-identical to
 // sparse.py:217-218.  HINT marks the streamed matrix evict-first in L2 so
 // the gathered x keeps its lines.
-template <int NT, int ST, int CH, bool HINT>
+//
+// CLS: the matrix has stencil classes (MatView::cls): a row's columns are
+// row + cls_off[class][k], so only the values are streamed (16 of the 20
+// bytes per slot) and the columns come from a shared-memory table.
+template <int NT, int ST, int CH, bool HINT, bool CLS>
 __global__ void __launch_bounds__(NT, 1) spmv_tma_pipe_kernel(MatView A, const double* __restrict__ x,
                                                               double* __restrict__ y, int valcap, int bufbytes) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) unsigned long long bar[ST];
+    __shared__ int soff[CLS ? kMaxClasses * kClsWidth : 1];
     const int N = A.ngroups;
     const int tiles = (N + NT - 1) / NT;
     const int mine = tiles > (int)blockIdx.x ? (tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    if (CLS)
+        for (int k = threadIdx.x; k < A.ncls * kClsWidth; k += NT) soff[k] = __ldg(A.cls_off + k);
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int b = 0; b < ST; ++b) mbar_init(&bar[b], 1);
@@ -1699,7 +1706,7 @@ __global__ void __launch_bounds__(NT, 1) spmv_tma_pipe_kernel(MatView A, const d
         const int s0 = __ldg(A.rp + r0), s1 = __ldg(A.rp + r1);
         const int sa = s0 & ~3, se = (s1 + 3) & ~3;
         unsigned char* base = sm + (size_t)b * bufbytes;
-        const unsigned vb = 16u * (unsigned)(s1 - s0), cb = 4u * (unsigned)(se - sa);
+        const unsigned vb = 16u * (unsigned)(s1 - s0), cb = CLS ? 0u : 4u * (unsigned)(se - sa);
         mbar_expect_tx(&bar[b], vb + cb);
         if (HINT) {
             if (vb) tma_load_1d_hint(base, A.val + 2LL * s0, vb, &bar[b], pol);
@@ -1717,16 +1724,18 @@ __global__ void __launch_bounds__(NT, 1) spmv_tma_pipe_kernel(MatView A, const d
         const int t = blockIdx.x + i * gridDim.x;
         const int r0 = t * NT, r1 = min(N, r0 + NT);
         const int r = r0 + threadIdx.x;
-        int a0 = 0, a1 = 0;
+        int a0 = 0, a1 = 0, cid = 0;
         if (r < r1) {
             a0 = __ldg(A.rp + r);
             a1 = __ldg(A.rp + r + 1);
+            if (CLS) cid = __ldg(A.cls + r);
         }
         const int s0 = __ldg(A.rp + r0);
         const int sa = s0 & ~3;
         mbar_wait(&bar[b], (unsigned)(i / ST) & 1u);
         const double2* sv = reinterpret_cast<const double2*>(sm + (size_t)b * bufbytes);
         const int* sc = reinterpret_cast<const int*>(sm + (size_t)b * bufbytes + (size_t)valcap * 16);
+        const int* so = soff + cid * kClsWidth - a0;  // CLS: column of slot s is r + so[s]
         if (r < r1) {
             double av = 0.0, at = 0.0;
             for (int s = a0; s < a1; s += CH) {
@@ -1734,7 +1743,7 @@ __global__ void __launch_bounds__(NT, 1) spmv_tma_pipe_kernel(MatView A, const d
                 double2 xv[CH];
 #pragma unroll
                 for (int j = 0; j < CH; ++j)
-                    if (s + j < a1) c[j] = sc[s + j - sa];
+                    if (s + j < a1) c[j] = CLS ? r + so[s + j] : sc[s + j - sa];
 #pragma unroll
                 for (int j = 0; j < CH; ++j)
                     if (s + j < a1) xv[j] = __ldg(x2 + c[j]);
@@ -1746,7 +1755,7 @@ __global__ void __launch_bounds__(NT, 1) spmv_tma_pipe_kernel(MatView A, const d
                         at = add(at, mul(vv.y, xv[j].y));
                     }
             }
-            reinterpret_cast<double2*>(y)[r] = make_double2(av, at);
+            __stcs(reinterpret_cast<double2*>(y) + r, make_double2(av, at));  // evict-first: keep x in L2
         }
         __syncthreads();  // every thread is done with stage b
         if (threadIdx.x == 0 && i + ST < mine) {
@@ -1794,10 +1803,12 @@ int jacobi_minv(rafem_ctx* ctx, const MatView& A, double* minv_dev, int* flag_de
 struct PipeCfg {
     int nt, st, hint;
     const void* fn;
+    const void* fn_cls;
 };
 template <int NT, int ST, int HINT>
 static PipeCfg pipe_cfg() {
-    return {NT, ST, HINT, (const void*)spmv_tma_pipe_kernel<NT, ST, 16, HINT != 0>};
+    return {NT, ST, HINT, (const void*)spmv_tma_pipe_kernel<NT, ST, 16, HINT != 0, false>,
+            (const void*)spmv_tma_pipe_kernel<NT, ST, 16, HINT != 0, true>};
 }
 static int spmv_pipe_launch(rafem_ctx* ctx, const MatView& A, const double* x_dev, double* y_dev) {
     static const PipeCfg cfgs[] = {pipe_cfg<256, 2, 1>(), pipe_cfg<128, 5, 1>(), pipe_cfg<128, 4, 1>(),
@@ -1814,10 +1825,15 @@ static int spmv_pipe_launch(rafem_ctx* ctx, const MatView& A, const double* x_de
         }
     }
     const PipeCfg& c = cfgs[want];
-    auto buf_bytes = [&](int t) { return t * A.maxdeg * 16 + ((t * A.maxdeg + 8) * 4 + 15) / 16 * 16; };
+    const char* nc = getenv("RAFEM_NO_CLASSES");
+    const bool cls = A.cls && A.ncls > 0 && A.maxdeg <= kClsWidth && !(nc && nc[0] == '1');
+    const void* fn = cls ? c.fn_cls : c.fn;
+    auto buf_bytes = [&](int t) {
+        return t * A.maxdeg * 16 + (cls ? 0 : ((t * A.maxdeg + 8) * 4 + 15) / 16 * 16);
+    };
     const size_t smem = (size_t)c.st * buf_bytes(c.nt);
-    if (smem > kSmemBudget) return RAFEM_ERR_UNSUPPORTED;
-    RF_CUDA_TRY(ctx, cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > kSmemBudget - (cls ? sizeof(int) * kMaxClasses * kClsWidth : 0)) return RAFEM_ERR_UNSUPPORTED;
+    RF_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int tiles = (A.ngroups + c.nt - 1) / c.nt;
     const int grid = std::min(tiles, ctx->sm_count);
     int valcap = c.nt * A.maxdeg, bufbytes = buf_bytes(c.nt);
@@ -1825,7 +1841,7 @@ static int spmv_pipe_launch(rafem_ctx* ctx, const MatView& A, const double* x_de
     const double* xp = x_dev;
     double* yp = y_dev;
     void* args[] = {&Av, &xp, &yp, &valcap, &bufbytes};
-    RF_CUDA_TRY(ctx, cudaLaunchKernel(c.fn, dim3(grid), dim3(c.nt), args, smem, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(grid), dim3(c.nt), args, smem, ctx->stream));
     ctx->launches++;
     return RAFEM_OK;
 }

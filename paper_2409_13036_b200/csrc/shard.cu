@@ -87,12 +87,17 @@ RF_DEV bool kp_stopped(const KPState& s) { return s.done || s.need_head; }
 // copy into a double-buffered smem stage (evict-first in L2), and every
 // thread sums its row left to right with all of the row's gathers issued
 // before the first accumulation.
-template <class Epi>
+// CLS: stencil classes (MatView::cls) — only values are streamed, columns
+// come from the class table in shared memory.
+template <bool CLS, class Epi>
 RF_DEV void kp_sweep(const KPArgs& a, const double2* __restrict__ src, unsigned char* sm,
                      unsigned long long* bar, Epi&& epi) {
+    __shared__ int soff[CLS ? kMaxClasses * kClsWidth : 1];
     const int N = a.n_own;
     const int tiles = (N + KPT - 1) / KPT;
     const int mine = tiles > (int)blockIdx.x ? (tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    if (CLS)
+        for (int k = threadIdx.x; k < a.A.ncls * kClsWidth; k += blockDim.x) soff[k] = __ldg(a.A.cls_off + k);
     if (threadIdx.x == 0) {
         for (int b = 0; b < kKpStages; ++b) mbar_init(&bar[b], 1);
         mbar_fence_init();
@@ -106,7 +111,7 @@ RF_DEV void kp_sweep(const KPArgs& a, const double2* __restrict__ src, unsigned 
         const int s0 = __ldg(a.A.rp + r0), s1 = __ldg(a.A.rp + r1);
         const int sa = s0 & ~3, se = (s1 + 3) & ~3;
         unsigned char* dst = sm + (size_t)b * a.bufbytes;
-        const unsigned vb = 16u * (unsigned)(s1 - s0), cb = 4u * (unsigned)(se - sa);
+        const unsigned vb = 16u * (unsigned)(s1 - s0), cb = CLS ? 0u : 4u * (unsigned)(se - sa);
         mbar_expect_tx(&bar[b], vb + cb);
         if (vb) tma_load_1d_hint(dst, a.A.val + 2LL * s0, vb, &bar[b], pol);
         if (cb) tma_load_1d_hint(dst + (size_t)a.valcap * 16, a.A.col + sa, cb, &bar[b], pol);
@@ -118,16 +123,18 @@ RF_DEV void kp_sweep(const KPArgs& a, const double2* __restrict__ src, unsigned 
         const int t = blockIdx.x + i * gridDim.x;
         const int r0 = t * KPT, r1 = min(N, r0 + KPT);
         const int r = r0 + threadIdx.x;
-        int a0 = 0, a1 = 0;
+        int a0 = 0, a1 = 0, cid = 0;
         if (r < r1) {
             a0 = __ldg(a.A.rp + r);
             a1 = __ldg(a.A.rp + r + 1);
+            if (CLS) cid = __ldg(a.A.cls + r);
         }
         const int s0 = __ldg(a.A.rp + r0);
         const int sa = s0 & ~3;
         mbar_wait(&bar[b], (unsigned)(i / kKpStages) & 1u);
         const double2* sv = reinterpret_cast<const double2*>(sm + (size_t)b * a.bufbytes);
         const int* sc = reinterpret_cast<const int*>(sm + (size_t)b * a.bufbytes + (size_t)a.valcap * 16);
+        const int* so = soff + cid * kClsWidth - a0;
         if (r < r1) {
             double av = 0.0, at = 0.0;
             for (int s = a0; s < a1; s += 16) {
@@ -135,7 +142,7 @@ RF_DEV void kp_sweep(const KPArgs& a, const double2* __restrict__ src, unsigned 
                 double2 xv[16];
 #pragma unroll
                 for (int q = 0; q < 16; ++q)
-                    if (s + q < a1) c[q] = sc[s + q - sa];
+                    if (s + q < a1) c[q] = CLS ? r + so[s + q] : sc[s + q - sa];
 #pragma unroll
                 for (int q = 0; q < 16; ++q)
                     if (s + q < a1) xv[q] = __ldg(src + c[q]);
@@ -230,14 +237,14 @@ __global__ void kp_bnorm_finish_kernel(KPArgs a) {
 }
 
 // head: r = b - A x, u = M r ; partials (r.u, r.r) -> partA
-template <bool PRE>
+template <bool PRE, bool CLS>
 __global__ void __launch_bounds__(KPT, 1) kp_head_kernel(KPArgs a, int idx) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) unsigned long long bar[kKpStages];
     __shared__ double red[64];
     if (a.st[idx].done) return;
     double v[2] = {0.0, 0.0};
-    kp_sweep(a, a.x, sm, bar, [&](int g, double yv, double yt) {
+    kp_sweep<CLS>(a, a.x, sm, bar, [&](int g, double yv, double yt) {
         const double2 bb = a.b[g];
         const double2 rr = make_double2(sub(bb.x, yv), sub(bb.y, yt));
         double2 uu = rr;
@@ -255,6 +262,7 @@ __global__ void __launch_bounds__(KPT, 1) kp_head_kernel(KPArgs a, int idx) {
 
 // w = A u ; partial (w.u); last CTA folds (r.u, r.r) of the preceding
 // writer (ga CTAs) and (w.u) into rank_part[rank]
+template <bool CLS>
 __global__ void __launch_bounds__(KPT, 1) kp_spmv_kernel(KPArgs a, int idx, int after_head, int ga) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) unsigned long long bar[kKpStages];
@@ -262,9 +270,9 @@ __global__ void __launch_bounds__(KPT, 1) kp_spmv_kernel(KPArgs a, int idx, int 
     const KPState& st = a.st[idx];
     if (st.done || (!after_head && st.need_head)) return;
     double v[1] = {0.0};
-    kp_sweep(a, a.u, sm, bar, [&](int g, double yv, double yt) {
+    kp_sweep<CLS>(a, a.u, sm, bar, [&](int g, double yv, double yt) {
         const double2 uu = a.u[g];
-        a.w[g] = make_double2(yv, yt);
+        __stcs(a.w + g, make_double2(yv, yt));  // evict-first: keep the gathered u in L2
         v[0] = add(add(v[0], mul(yv, uu.x)), mul(yt, uu.y));
     });
     kp_publish<1>(v, a.partB, red);
@@ -457,9 +465,12 @@ int rafem_kp_create(rafem_system* sys, int64_t n_owned, int64_t n_ext, int32_t n
     if (n_owned < 1 || n_owned > m->N || n_ext < n_owned || n_ext > m->N || nranks < 1 || rank < 0 || rank >= nranks)
         return rafem_fail(ctx, RAFEM_ERR_INVALID, "kp_create: bad shard shape");
     if (m->maxdeg < 1) return rafem_fail(ctx, RAFEM_ERR_INVALID, "kp_create: empty pattern");
-    const int bufbytes = KPT * m->maxdeg * 16 + ((KPT * m->maxdeg + 8) * 4 + 15) / 16 * 16;
+    if (!m->cls_tried) mesh_stencil_classes(m);  // none on unstructured / renumbered shards
+    const char* nc = getenv("RAFEM_NO_CLASSES");
+    const bool cls = m->cls && m->ncls > 0 && m->maxdeg <= kClsWidth && !(nc && nc[0] == '1');
+    const int bufbytes = KPT * m->maxdeg * 16 + (cls ? 0 : ((KPT * m->maxdeg + 8) * 4 + 15) / 16 * 16);
     const size_t smem = (size_t)kKpStages * bufbytes;
-    if (smem > 220 * 1024)
+    if (smem > 200 * 1024)
         return rafem_fail(ctx, RAFEM_ERR_UNSUPPORTED, "kp_create: rows too long for the TMA tile buffers");
     rafem_kp* k = new rafem_kp();
     k->sys = sys;
@@ -496,6 +507,11 @@ int rafem_kp_create(rafem_system* sys, int64_t n_owned, int64_t n_ext, int32_t n
     a.A.W = 2;
     a.A.slots = m->slots;
     a.A.maxdeg = m->maxdeg;
+    if (cls) {
+        a.A.cls = m->cls;
+        a.A.cls_off = m->cls_off;
+        a.A.ncls = m->ncls;
+    }
     a.n_own = (int)n_owned;
     a.x = reinterpret_cast<double2*>(base + ox);
     a.u = reinterpret_cast<double2*>(base + ou);
@@ -517,8 +533,9 @@ int rafem_kp_create(rafem_system* sys, int64_t n_owned, int64_t n_ext, int32_t n
     a.valcap = KPT * m->maxdeg;
     cudaEventCreate(&k->e0);
     cudaEventCreate(&k->e1);
-    for (const void* fn : {(const void*)kp_head_kernel<true>, (const void*)kp_head_kernel<false>,
-                           (const void*)kp_spmv_kernel}) {
+    for (const void* fn : {(const void*)kp_head_kernel<true, false>, (const void*)kp_head_kernel<false, false>,
+                           (const void*)kp_spmv_kernel<false>, (const void*)kp_head_kernel<true, true>,
+                           (const void*)kp_head_kernel<false, true>, (const void*)kp_spmv_kernel<true>}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) {
             rafem_kp_destroy(k);
@@ -629,15 +646,25 @@ int rafem_kp_launch(rafem_kp* k, int32_t what) {
             k->idx = 0;
             break;
         case 1:
-            if (k->pre)
-                kp_head_kernel<true><<<k->g_spmv, KPT, k->smem, st>>>(a, k->idx);
-            else
-                kp_head_kernel<false><<<k->g_spmv, KPT, k->smem, st>>>(a, k->idx);
+            if (a.A.cls) {
+                if (k->pre)
+                    kp_head_kernel<true, true><<<k->g_spmv, KPT, k->smem, st>>>(a, k->idx);
+                else
+                    kp_head_kernel<false, true><<<k->g_spmv, KPT, k->smem, st>>>(a, k->idx);
+            } else {
+                if (k->pre)
+                    kp_head_kernel<true, false><<<k->g_spmv, KPT, k->smem, st>>>(a, k->idx);
+                else
+                    kp_head_kernel<false, false><<<k->g_spmv, KPT, k->smem, st>>>(a, k->idx);
+            }
             k->ga = k->g_spmv;
             break;
         case 2:
         case 3:
-            kp_spmv_kernel<<<k->g_spmv, KPT, k->smem, st>>>(a, k->idx, what == 2, k->ga);
+            if (a.A.cls)
+                kp_spmv_kernel<true><<<k->g_spmv, KPT, k->smem, st>>>(a, k->idx, what == 2, k->ga);
+            else
+                kp_spmv_kernel<false><<<k->g_spmv, KPT, k->smem, st>>>(a, k->idx, what == 2, k->ga);
             break;
         case 4:
         case 5:

@@ -9,5 +9,5 @@ mesh = generate_box_mesh(80, 80, 79)
 t = np.full(mesh.node_count, 37.0)
 s = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, np.zeros(mesh.node_count), t, 0.5)
 ms = C.c_double()
-nat.check(nat.lib().rafem_system_spmv_bench(s.device.handle, 10, C.byref(ms)), "spmv bench")
+nat.check(nat.lib().rafem_system_spmv_bench(s.device.handle, 10, 0, C.byref(ms)), "spmv bench")
 print("spmv ms", ms.value)

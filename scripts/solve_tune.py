@@ -17,7 +17,7 @@ x0 = np.empty(2 * n); x0[0::2], x0[1::2] = 0.0, 37.0
 cfg = SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-10)
 B = 20 * S + 4 * (n + 1) + 12 * 16 * n
 print(f"{dims}: {2*n} dofs, {S} slots, pcg bytes/iter {B/1e6:.1f} MB", flush=True)
-for env in [{}, {"RAFEM_NO_STREAM_PCG": "1"}]:
+for env in [{}, {"RAFEM_NO_CLASSES": "1"}, {"RAFEM_NO_STREAM_PCG": "1"}]:
     os.environ.update(env)
     for rep in range(2):
         x, st = solve(s.matrix, s.rhs, x0=x0, config=cfg)
@@ -31,13 +31,16 @@ for env in [{}, {"RAFEM_NO_STREAM_PCG": "1"}]:
 from paper_2409_13036_b200.shard import ShardedSystem
 import time as _t
 t0 = _t.time()
-sh = ShardedSystem(mesh, MaterialParams.default(), batch=int(os.environ.get("KP_BATCH", "32")))
-sh.assemble(t, np.zeros(n), t, 0.5, SimConfig())
-print(f"kp setup {_t.time()-t0:.1f}s", flush=True)
-for rep in range(2):
-    w0 = _t.perf_counter()
-    x, st = sh.solve(x0=x0, config=cfg)
-    w = _t.perf_counter() - w0
-us = 1e3 * st.device_ms / max(1, st.iterations)
-print(f"{'kp (kernel-per-phase)':32s} it {st.iterations} res {st.final_relative_residual:.3e} "
-      f"{st.device_ms:.2f} ms (wall {1e3*w:.1f} ms)  {us:.2f} us/it  {B/us/1e3:.0f} GB/s(alg 12x16N)", flush=True)
+for nc in ("0", "1"):
+    os.environ["RAFEM_NO_CLASSES"] = nc
+    sh = ShardedSystem(mesh, MaterialParams.default(), batch=int(os.environ.get("KP_BATCH", "32")))
+    sh.assemble(t, np.zeros(n), t, 0.5, SimConfig())
+    print(f"kp setup {_t.time()-t0:.1f}s", flush=True)
+    for rep in range(2):
+        w0 = _t.perf_counter()
+        x, st = sh.solve(x0=x0, config=cfg)
+        w = _t.perf_counter() - w0
+    us = 1e3 * st.device_ms / max(1, st.iterations)
+    print(f"{'kp classes=' + ('off' if nc == '1' else 'on'):32s} it {st.iterations} res {st.final_relative_residual:.3e} "
+          f"{st.device_ms:.2f} ms (wall {1e3*w:.1f} ms)  {us:.2f} us/it  {B/us/1e3:.0f} GB/s(alg 12x16N)", flush=True)
+    del sh

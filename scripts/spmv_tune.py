@@ -27,10 +27,12 @@ os.environ["RAFEM_NO_TMA_SPMV"] = "1"
 y_ref = np.empty(2 * N)
 nat.check(nat.lib().rafem_system_spmv(h.handle, x.ctypes.data, y_ref.ctypes.data), "spmv")
 ms = C.c_double()
-nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 30, C.byref(ms)), "bench")
+nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 30, int(os.environ.get("FLUSH", "1")), C.byref(ms)), "bench")
 print(f"thread-per-row      {1e3*ms.value:8.2f} us  {B/ms.value/1e6:8.1f} GB/s")
 del os.environ["RAFEM_NO_TMA_SPMV"]
-for cfg in ["legacy", "128,4,1", "128,5,1", "256,2,1", "256,2,0", "192,3,1", "96,6,1", "128,4,0", "64,8,1"]:
+for cfg in ["legacy", "256,2,1", "256,2,1/nocls", "192,3,1", "128,4,1"]:
+    os.environ["RAFEM_NO_CLASSES"] = "1" if cfg.endswith("/nocls") else "0"
+    cfg = cfg.split("/")[0]
     if cfg == "legacy":
         os.environ["RAFEM_SPMV_CFG"] = "1,1,1"  # no such config -> two-stage kernel
     else:
@@ -39,6 +41,6 @@ for cfg in ["legacy", "128,4,1", "128,5,1", "256,2,1", "256,2,0", "192,3,1", "96
     nat.check(nat.lib().rafem_system_spmv(h.handle, x.ctypes.data, y.ctypes.data), "spmv")
     best = 1e9
     for _ in range(3):
-        nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 30, C.byref(ms)), "bench")
+        nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 30, int(os.environ.get("FLUSH", "1")), C.byref(ms)), "bench")
         best = min(best, ms.value)
     print(f"{cfg:18s}  {1e3*best:8.2f} us  {B/best/1e6:8.1f} GB/s  bitexact={np.array_equal(y, y_ref)}", flush=True)

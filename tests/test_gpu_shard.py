@@ -212,3 +212,27 @@ def test_sharded_time_loop_matches_native_loop(tmp_path):
     for k, r in enumerate(ref):
         assert np.max(np.abs(T[k] - r.T)) <= 1e-8 * np.max(np.abs(r.T))
         assert np.max(np.abs(V[k] - r.V)) <= 1e-8 * np.max(np.abs(r.V))
+
+
+def test_stencil_class_columns_change_nothing_but_bytes():
+    """Kernel-per-phase PCG with computed (stencil-class) columns runs the
+    same arithmetic as with streamed columns: bit-identical solution."""
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh
+    from paper_2409_13036_b200.shard import ShardedSystem
+    mesh = generate_box_mesh(24, 22, 26)
+    n = mesh.node_count
+    t, v = _hot(n, seed=9)
+    x0 = np.empty(2 * n)
+    x0[0::2], x0[1::2] = v, t
+    cfg = SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-10)
+    out = []
+    for classes in ("0", "1"):
+        os.environ["RAFEM_NO_CLASSES"] = classes
+        try:
+            sh = ShardedSystem(mesh, MaterialParams.default())
+            sh.assemble(t, v, t, 0.5, SimConfig())
+            out.append(sh.solve(x0=x0, config=cfg))
+        finally:
+            del os.environ["RAFEM_NO_CLASSES"]
+    (xa, sa), (xb, sb) = out
+    assert sa.converged and np.array_equal(xa, xb) and sa.iterations == sb.iterations

@@ -263,11 +263,13 @@ def test_tma_spmv_pipeline_configs_bitwise_at_1M_dofs():
     x = np.random.default_rng(6).standard_normal(s.rhs.size)
     ref = O.matvec(s.matrix.row_ptr, s.matrix.col_idx, s.matrix.vals, x)
     for cfg in ("256,2,1", "128,4,1", "192,3,1", "1,1,1"):  # 1,1,1: two-stage kernel
-        os.environ["RAFEM_SPMV_CFG"] = cfg
-        try:
-            assert np.array_equal(spmv(s.matrix, x), ref), cfg
-        finally:
-            del os.environ["RAFEM_SPMV_CFG"]
+        for classes in ("0", "1"):  # stencil-class columns on / off
+            os.environ["RAFEM_SPMV_CFG"] = cfg
+            os.environ["RAFEM_NO_CLASSES"] = classes
+            try:
+                assert np.array_equal(spmv(s.matrix, x), ref), (cfg, classes)
+            finally:
+                del os.environ["RAFEM_SPMV_CFG"], os.environ["RAFEM_NO_CLASSES"]
 
 
 @pytest.mark.parametrize("hot", [False, True])
