@@ -1811,10 +1811,24 @@ static PipeCfg pipe_cfg() {
             (const void*)spmv_tma_pipe_kernel<NT, ST, 16, HINT != 0, true>};
 }
 static int spmv_pipe_launch(rafem_ctx* ctx, const MatView& A, const double* x_dev, double* y_dev) {
-    static const PipeCfg cfgs[] = {pipe_cfg<256, 2, 1>(), pipe_cfg<128, 5, 1>(), pipe_cfg<128, 4, 1>(),
-                                   pipe_cfg<256, 2, 0>(), pipe_cfg<192, 3, 1>(), pipe_cfg<96, 6, 1>(),
-                                   pipe_cfg<128, 4, 0>(), pipe_cfg<64, 8, 1>()};
-    int want = 0;
+    static const PipeCfg cfgs[] = {pipe_cfg<256, 2, 1>(), pipe_cfg<128, 4, 1>(), pipe_cfg<192, 3, 1>(),
+                                   pipe_cfg<256, 3, 1>(), pipe_cfg<384, 2, 1>(), pipe_cfg<512, 2, 1>()};
+    const char* nc = getenv("RAFEM_NO_CLASSES");
+    const bool cls = A.cls && A.ncls > 0 && A.maxdeg <= kClsWidth && !(nc && nc[0] == '1');
+    auto buf_bytes = [&](int t) {
+        return t * A.maxdeg * 16 + (cls ? 0 : ((t * A.maxdeg + 8) * 4 + 15) / 16 * 16);
+    };
+    const size_t budget = kSmemBudget - (cls ? sizeof(int) * kMaxClasses * kClsWidth : 0);
+    // default: the widest configuration whose stages fit (measured on B200,
+    // cold L2: 384 x 2 with stencil classes 411 us at 16M dofs, 256 x 2 521 us)
+    int want = -1;
+    for (int i : {4, 0, 1}) {
+        if ((size_t)cfgs[i].st * buf_bytes(cfgs[i].nt) <= budget) {
+            want = i;
+            break;
+        }
+    }
+    if (want < 0) return RAFEM_ERR_UNSUPPORTED;
     if (const char* env = getenv("RAFEM_SPMV_CFG")) {
         int nt = 0, st = 0, hint = 1;
         if (sscanf(env, "%d,%d,%d", &nt, &st, &hint) >= 2) {
@@ -1825,14 +1839,9 @@ static int spmv_pipe_launch(rafem_ctx* ctx, const MatView& A, const double* x_de
         }
     }
     const PipeCfg& c = cfgs[want];
-    const char* nc = getenv("RAFEM_NO_CLASSES");
-    const bool cls = A.cls && A.ncls > 0 && A.maxdeg <= kClsWidth && !(nc && nc[0] == '1');
     const void* fn = cls ? c.fn_cls : c.fn;
-    auto buf_bytes = [&](int t) {
-        return t * A.maxdeg * 16 + (cls ? 0 : ((t * A.maxdeg + 8) * 4 + 15) / 16 * 16);
-    };
     const size_t smem = (size_t)c.st * buf_bytes(c.nt);
-    if (smem > kSmemBudget - (cls ? sizeof(int) * kMaxClasses * kClsWidth : 0)) return RAFEM_ERR_UNSUPPORTED;
+    if (smem > budget) return RAFEM_ERR_UNSUPPORTED;
     RF_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int tiles = (A.ngroups + c.nt - 1) / c.nt;
     const int grid = std::min(tiles, ctx->sm_count);

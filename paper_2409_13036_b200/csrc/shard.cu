@@ -40,7 +40,10 @@
 
 namespace rafem {
 
-constexpr int KPT = 256;      // threads per CTA of the SpMV kernels (one node row each per tile)
+// threads per CTA of the SpMV kernels = node rows per tile: 384 with
+// stencil-class columns (values-only stages fit twice), else 256
+template <bool CLS>
+__host__ __device__ constexpr int kpt() { return CLS ? 384 : 256; }
 constexpr int KPU = 256;      // threads per CTA of the update kernel
 constexpr int kKpStages = 2;  // TMA pipeline depth
 
@@ -94,6 +97,7 @@ RF_DEV void kp_sweep(const KPArgs& a, const double2* __restrict__ src, unsigned 
                      unsigned long long* bar, Epi&& epi) {
     __shared__ int soff[CLS ? kMaxClasses * kClsWidth : 1];
     const int N = a.n_own;
+    constexpr int KPT = kpt<CLS>();
     const int tiles = (N + KPT - 1) / KPT;
     const int mine = tiles > (int)blockIdx.x ? (tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     if (CLS)
@@ -238,7 +242,7 @@ __global__ void kp_bnorm_finish_kernel(KPArgs a) {
 
 // head: r = b - A x, u = M r ; partials (r.u, r.r) -> partA
 template <bool PRE, bool CLS>
-__global__ void __launch_bounds__(KPT, 1) kp_head_kernel(KPArgs a, int idx) {
+__global__ void __launch_bounds__(kpt<CLS>(), 1) kp_head_kernel(KPArgs a, int idx) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) unsigned long long bar[kKpStages];
     __shared__ double red[64];
@@ -263,7 +267,7 @@ __global__ void __launch_bounds__(KPT, 1) kp_head_kernel(KPArgs a, int idx) {
 // w = A u ; partial (w.u); last CTA folds (r.u, r.r) of the preceding
 // writer (ga CTAs) and (w.u) into rank_part[rank]
 template <bool CLS>
-__global__ void __launch_bounds__(KPT, 1) kp_spmv_kernel(KPArgs a, int idx, int after_head, int ga) {
+__global__ void __launch_bounds__(kpt<CLS>(), 1) kp_spmv_kernel(KPArgs a, int idx, int after_head, int ga) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) unsigned long long bar[kKpStages];
     __shared__ double red[32];
@@ -468,9 +472,10 @@ int rafem_kp_create(rafem_system* sys, int64_t n_owned, int64_t n_ext, int32_t n
     if (!m->cls_tried) mesh_stencil_classes(m);  // none on unstructured / renumbered shards
     const char* nc = getenv("RAFEM_NO_CLASSES");
     const bool cls = m->cls && m->ncls > 0 && m->maxdeg <= kClsWidth && !(nc && nc[0] == '1');
+    const int KPT = cls ? kpt<true>() : kpt<false>();
     const int bufbytes = KPT * m->maxdeg * 16 + (cls ? 0 : ((KPT * m->maxdeg + 8) * 4 + 15) / 16 * 16);
     const size_t smem = (size_t)kKpStages * bufbytes;
-    if (smem > 200 * 1024)
+    if (smem > 200 * 1024 + (cls ? 0 : 16 * 1024))
         return rafem_fail(ctx, RAFEM_ERR_UNSUPPORTED, "kp_create: rows too long for the TMA tile buffers");
     rafem_kp* k = new rafem_kp();
     k->sys = sys;
@@ -648,23 +653,23 @@ int rafem_kp_launch(rafem_kp* k, int32_t what) {
         case 1:
             if (a.A.cls) {
                 if (k->pre)
-                    kp_head_kernel<true, true><<<k->g_spmv, KPT, k->smem, st>>>(a, k->idx);
+                    kp_head_kernel<true, true><<<k->g_spmv, kpt<true>(), k->smem, st>>>(a, k->idx);
                 else
-                    kp_head_kernel<false, true><<<k->g_spmv, KPT, k->smem, st>>>(a, k->idx);
+                    kp_head_kernel<false, true><<<k->g_spmv, kpt<true>(), k->smem, st>>>(a, k->idx);
             } else {
                 if (k->pre)
-                    kp_head_kernel<true, false><<<k->g_spmv, KPT, k->smem, st>>>(a, k->idx);
+                    kp_head_kernel<true, false><<<k->g_spmv, kpt<false>(), k->smem, st>>>(a, k->idx);
                 else
-                    kp_head_kernel<false, false><<<k->g_spmv, KPT, k->smem, st>>>(a, k->idx);
+                    kp_head_kernel<false, false><<<k->g_spmv, kpt<false>(), k->smem, st>>>(a, k->idx);
             }
             k->ga = k->g_spmv;
             break;
         case 2:
         case 3:
             if (a.A.cls)
-                kp_spmv_kernel<true><<<k->g_spmv, KPT, k->smem, st>>>(a, k->idx, what == 2, k->ga);
+                kp_spmv_kernel<true><<<k->g_spmv, kpt<true>(), k->smem, st>>>(a, k->idx, what == 2, k->ga);
             else
-                kp_spmv_kernel<false><<<k->g_spmv, KPT, k->smem, st>>>(a, k->idx, what == 2, k->ga);
+                kp_spmv_kernel<false><<<k->g_spmv, kpt<false>(), k->smem, st>>>(a, k->idx, what == 2, k->ga);
             break;
         case 4:
         case 5:

@@ -30,7 +30,7 @@ ms = C.c_double()
 nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 30, int(os.environ.get("FLUSH", "1")), C.byref(ms)), "bench")
 print(f"thread-per-row      {1e3*ms.value:8.2f} us  {B/ms.value/1e6:8.1f} GB/s")
 del os.environ["RAFEM_NO_TMA_SPMV"]
-for cfg in ["legacy", "256,2,1", "256,2,1/nocls", "192,3,1", "128,4,1"]:
+for cfg in ["legacy", "256,2,1", "256,2,1/nocls", "256,3,1", "384,2,1", "512,2,1", "192,3,1"]:
     os.environ["RAFEM_NO_CLASSES"] = "1" if cfg.endswith("/nocls") else "0"
     cfg = cfg.split("/")[0]
     if cfg == "legacy":
