@@ -503,6 +503,20 @@ def c4_leg(hbm_peak, peak_src, world, rank, local):
         mine = int(s_.item())
     it = st.iterations
     bytes_it = mine
+    spmv = None
+    if world == 1:  # the standalone SpMV on the same matrix, cold L2 every launch
+        import ctypes as C
+        msb = C.c_double()
+        nat.check(nat.lib().rafem_system_spmv_bench(sh.h.handle, 10, 1, C.byref(msb)), "spmv bench")
+        S1 = sh.dm.slots
+        b_sp = ((16 * S1 + n) if cls_on else 20 * S1) + 4 * (n + 1) + 32 * n
+        b_ex = 20 * S1 + 4 * (n + 1) + 32 * n
+        ach_sp = b_sp / (msb.value / 1e3) / 1e9
+        spmv = {"bound": "hbm", "achieved": ach_sp, "peak": hbm_peak, "unit": "GB/s", "frac": ach_sp / hbm_peak,
+                "frac_of_8TBs": ach_sp / 8000.0, "us_per_launch": 1e3 * msb.value, "bytes_per_launch": b_sp,
+                "explicit_columns_equivalent_GBs": b_ex / (msb.value / 1e3) / 1e9,
+                "kernel": "spmv_tma_pipe_kernel<384,2,stencil classes>" if cls_on else "spmv_tma_pipe_kernel<256,2>",
+                "l2": "flushed (256 MB write) before every timed launch"}
     ach = it * bytes_it / (dev_ms / 1e3) / 1e9 if dev_ms > 0 else 0.0
     return {"workload": "generate_box_mesh(200,200,200) cold system, 16,000,000 dofs",
             "shards": world, "partition": "contiguous node-row blocks (x-slabs)",
@@ -512,7 +526,7 @@ def c4_leg(hbm_peak, peak_src, world, rank, local):
             "us_per_iteration": 1e3 * dev_ms / max(it, 1),
             "aggregate_GBs": ach, "frac_of_1gpu_peak": ach / hbm_peak / world, "peak_source": peak_src,
             "bytes_per_iteration": bytes_it, "columns": "stencil classes" if cls_on else "explicit int32",
-            "assembly_s": asm_s, "setup_s": setup_s,
+            "assembly_s": asm_s, "setup_s": setup_s, "spmv": spmv,
             "kernel": "kp_spmv_kernel + kp_update_kernel (csrc/shard.cu)"}
 
 
