@@ -293,7 +293,8 @@ int rafem_field_compare(rafem_ctx* ctx, int64_t n, int64_t steps, const double* 
  * interleaved 2N dof vector in pinned host memory (valid during the call).
  * The kernel waits for a free slot, so memory stays bounded at any record
  * size.  A nonzero return from fn stops the delivery (the run completes)
- * and the call returns RAFEM_ERR_INVALID. */
+ * and the call returns RAFEM_ERR_INVALID.  fn must not call back into the
+ * library (the record buffer is the context's pinned staging area). */
 typedef int32_t (*rafem_record_fn)(void* user, int64_t step, double time, double dt, int32_t corrector_iters,
                                    const double* x);
 int rafem_simulate_stream(rafem_system* sys, const rafem_sim_params* p, rafem_sim_summary* out,

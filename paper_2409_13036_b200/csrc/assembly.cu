@@ -454,14 +454,14 @@ int mesh_symbolic(rafem_mesh* m) {
     int* cnt = nullptr;
     int* cursor = nullptr;
     int* flags = nullptr;  // [0] maxinc, [1] maxdeg, [2] overflow
-    RF_CUDA_TRY(ctx, cudaMalloc(&cnt, sizeof(int) * (N + 1)));
-    RF_CUDA_TRY(ctx, cudaMalloc(&cursor, sizeof(int) * (N + 1)));
-    RF_CUDA_TRY(ctx, cudaMalloc(&flags, sizeof(int) * 4));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&cnt, sizeof(int) * (N + 1)));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&cursor, sizeof(int) * (N + 1)));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&flags, sizeof(int) * 4));
     RF_CUDA_TRY(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * (N + 1), st));
     RF_CUDA_TRY(ctx, cudaMemsetAsync(flags, 0, sizeof(int) * 4, st));
-    RF_CUDA_TRY(ctx, cudaMalloc(&m->inc_ptr, sizeof(int) * (N + 1)));
-    RF_CUDA_TRY(ctx, cudaMalloc(&m->inc_ea, sizeof(unsigned) * 4 * (size_t)std::max(M, 1)));
-    RF_CUDA_TRY(ctx, cudaMalloc(&m->inc_slot, sizeof(unsigned) * 4 * (size_t)std::max(M, 1)));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&m->inc_ptr, sizeof(int) * (N + 1)));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&m->inc_ea, sizeof(unsigned) * 4 * (size_t)std::max(M, 1)));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&m->inc_slot, sizeof(unsigned) * 4 * (size_t)std::max(M, 1)));
     const int tb = 256;
     if (M > 0) {
         inc_count_kernel<<<(M + tb - 1) / tb, tb, 0, st>>>(m->tets, M, cnt);
@@ -483,30 +483,30 @@ int mesh_symbolic(rafem_mesh* m) {
     RF_CUDA_TRY(ctx, cudaMemcpyAsync(hflags, flags, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
     RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
     if (hflags[2]) {
-        cudaFree(cnt);
-        cudaFree(cursor);
-        cudaFree(flags);
+        dfree(ctx, cnt);
+        dfree(ctx, cursor);
+        dfree(ctx, flags);
         return rafem_fail(ctx, RAFEM_ERR_UNSUPPORTED, "a node has more than 255 neighbours; pattern too dense for the packed slot map");
     }
     m->maxinc = hflags[0];
     m->maxdeg = hflags[1];
-    RF_CUDA_TRY(ctx, cudaMalloc(&m->rp, sizeof(int) * (N + 1)));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&m->rp, sizeof(int) * (N + 1)));
     if (int rc = scan_ints(ctx, cnt, m->rp, N)) return rc;
     int slots = 0;
     RF_CUDA_TRY(ctx, cudaMemcpyAsync(&slots, m->rp + N, sizeof(int), cudaMemcpyDeviceToHost, st));
     RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
     m->slots = slots;
-    RF_CUDA_TRY(ctx, cudaMalloc(&m->col, sizeof(int) * ((size_t)std::max(slots, 1) + 8)));  // +8: 16-B TMA tail
-    RF_CUDA_TRY(ctx, cudaMalloc(&m->diag, sizeof(int) * (size_t)std::max(N, 1)));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&m->col, sizeof(int) * ((size_t)std::max(slots, 1) + 8)));  // +8: 16-B TMA tail
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&m->diag, sizeof(int) * (size_t)std::max(N, 1)));
     if (N > 0) {
         adj_fill_kernel<<<(N + 127) / 128, 128, 0, st>>>(m->inc_ptr, m->inc_ea, m->tets, N, m->rp, m->col, m->diag, m->inc_slot);
         ctx->launches++;
     }
     RF_CUDA_TRY(ctx, cudaGetLastError());
     RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
-    cudaFree(cnt);
-    cudaFree(cursor);
-    cudaFree(flags);
+    dfree(ctx, cnt);
+    dfree(ctx, cursor);
+    dfree(ctx, flags);
     return RAFEM_OK;
 }
 
@@ -521,9 +521,9 @@ int mesh_slot_lists(rafem_mesh* m) {
     const long long slots = m->slots;
     if (N <= 0 || slots <= 0 || 16LL * M >= (1LL << 31) || m->maxdeg > kMaxDeg) return RAFEM_OK;
     int* scnt = nullptr;
-    RF_CUDA_TRY(ctx, cudaMalloc(&scnt, sizeof(int) * (size_t)slots));
-    RF_CUDA_TRY(ctx, cudaMalloc(&m->slot_ptr, sizeof(int) * ((size_t)slots + 1)));
-    RF_CUDA_TRY(ctx, cudaMalloc(&m->slot_src, sizeof(int) * 16 * (size_t)M));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&scnt, sizeof(int) * (size_t)slots));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&m->slot_ptr, sizeof(int) * ((size_t)slots + 1)));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&m->slot_src, sizeof(int) * 16 * (size_t)M));
     slot_count_kernel<<<(N + 127) / 128, 128, 0, st>>>(m->inc_ptr, m->inc_slot, m->rp, N, scnt);
     ctx->launches++;
     if (int rc = scan_ints(ctx, scnt, m->slot_ptr, (int)slots)) return rc;
@@ -532,7 +532,7 @@ int mesh_slot_lists(rafem_mesh* m) {
     ctx->launches++;
     RF_CUDA_TRY(ctx, cudaGetLastError());
     RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
-    cudaFree(scnt);
+    dfree(ctx, scnt);
     return RAFEM_OK;
 }
 
@@ -568,7 +568,7 @@ int mesh_stencil_classes(rafem_mesh* m) {
     const int N = m->N;
     if (N <= 0 || m->maxdeg > kClsWidth) return RAFEM_OK;
     unsigned long long* dsig = nullptr;
-    RF_CUDA_TRY(ctx, cudaMalloc(&dsig, sizeof(unsigned long long) * N));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&dsig, sizeof(unsigned long long) * N));
     row_sig_kernel<<<(N + 255) / 256, 256, 0, st>>>(m->rp, m->col, N, dsig);
     ctx->launches++;
     std::vector<unsigned long long> sig(N);
@@ -576,7 +576,7 @@ int mesh_stencil_classes(rafem_mesh* m) {
     RF_CUDA_TRY(ctx, cudaMemcpyAsync(sig.data(), dsig, sizeof(unsigned long long) * N, cudaMemcpyDeviceToHost, st));
     RF_CUDA_TRY(ctx, cudaMemcpyAsync(rp.data(), m->rp, sizeof(int) * (N + 1), cudaMemcpyDeviceToHost, st));
     RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
-    cudaFree(dsig);
+    dfree(ctx, dsig);
     std::vector<uint8_t> cls(N);
     std::vector<unsigned long long> keys;
     std::vector<int> rep;
@@ -608,9 +608,9 @@ int mesh_stencil_classes(rafem_mesh* m) {
     int* doff = nullptr;
     int* ddeg = nullptr;
     int* dbad = nullptr;
-    RF_CUDA_TRY(ctx, cudaMalloc(&dcls, N));
-    RF_CUDA_TRY(ctx, cudaMalloc(&doff, sizeof(int) * off.size()));
-    RF_CUDA_TRY(ctx, cudaMalloc(&ddeg, sizeof(int) * ncls + sizeof(int)));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&dcls, N));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&doff, sizeof(int) * off.size()));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&ddeg, sizeof(int) * ncls + sizeof(int)));
     dbad = ddeg + ncls;
     RF_CUDA_TRY(ctx, cudaMemcpyAsync(dcls, cls.data(), N, cudaMemcpyHostToDevice, st));
     RF_CUDA_TRY(ctx, cudaMemcpyAsync(doff, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice, st));
@@ -621,10 +621,10 @@ int mesh_stencil_classes(rafem_mesh* m) {
     int hbad = 0;
     RF_CUDA_TRY(ctx, cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, st));
     RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
-    cudaFree(ddeg);
+    dfree(ctx, ddeg);
     if (hbad) {  // hash collision: keep explicit columns
-        cudaFree(dcls);
-        cudaFree(doff);
+        dfree(ctx, dcls);
+        dfree(ctx, doff);
         return RAFEM_OK;
     }
     m->cls = dcls;
@@ -636,9 +636,9 @@ int mesh_stencil_classes(rafem_mesh* m) {
 int mesh_geometry(rafem_mesh* m) {
     rafem_ctx* ctx = m->ctx;
     const int M = m->M;
-    RF_CUDA_TRY(ctx, cudaMalloc(&m->base, sizeof(double) * 10 * (size_t)std::max(M, 1)));
-    RF_CUDA_TRY(ctx, cudaMalloc(&m->grad, sizeof(double) * 12 * (size_t)std::max(M, 1)));
-    RF_CUDA_TRY(ctx, cudaMalloc(&m->vol, sizeof(double) * (size_t)std::max(M, 1)));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&m->base, sizeof(double) * 10 * (size_t)std::max(M, 1)));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&m->grad, sizeof(double) * 12 * (size_t)std::max(M, 1)));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&m->vol, sizeof(double) * (size_t)std::max(M, 1)));
     if (M > 0) {
         geometry_kernel<<<(M + 127) / 128, 128, 0, ctx->stream>>>(m->nodes, m->tets, M, m->base, m->grad, m->vol);
         ctx->launches++;

@@ -161,11 +161,11 @@ int rafem_mesh_create_box(rafem_ctx* ctx, int32_t nx, int32_t ny, int32_t nz, co
     cudaError_t e;
     long long* dids = nullptr;
 #define RF_MS(x) do { e = (x); if (e != cudaSuccess) { cudaFree(dids); rafem_mesh_destroy(m); return rafem_fail_cuda(ctx, e, #x, __FILE__, __LINE__); } } while (0)
-    RF_MS(cudaMalloc(&m->nodes, sizeof(double) * 3 * N));
-    RF_MS(cudaMalloc(&m->tets, sizeof(int) * 4 * M));
-    RF_MS(cudaMalloc(&m->region, sizeof(int) * M));
-    RF_MS(cudaMalloc(&m->regtab, sizeof(double) * 5));
-    RF_MS(cudaMalloc(&m->kind, 2 * N));
+    RF_MS(dmalloc(ctx, (void**)&m->nodes, sizeof(double) * 3 * N));
+    RF_MS(dmalloc(ctx, (void**)&m->tets, sizeof(int) * 4 * M));
+    RF_MS(dmalloc(ctx, (void**)&m->region, sizeof(int) * M));
+    RF_MS(dmalloc(ctx, (void**)&m->regtab, sizeof(double) * 5));
+    RF_MS(dmalloc(ctx, (void**)&m->kind, 2 * N));
     const double tab[5] = {k, rho_c, sigma0, alpha, t_ref};
     RF_MS(cudaMemcpyAsync(m->regtab, tab, sizeof(tab), cudaMemcpyHostToDevice, st));
     box_nodes_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(nx, ny, nz, extent[0], extent[1], extent[2],

@@ -41,6 +41,54 @@ int ensure(rafem_ctx* ctx, DevBuf& b, size_t bytes) {
     return RAFEM_OK;
 }
 
+cudaError_t dmalloc(rafem_ctx* ctx, void** p, size_t bytes) {
+    bytes = std::max<size_t>((bytes + 255) / 256 * 256, 256);
+    auto it = ctx->free_blocks.lower_bound(bytes);
+    if (it != ctx->free_blocks.end() && it->first <= 2 * bytes) {  // reuse a block of close size
+        *p = it->second;
+        ctx->cached_bytes -= it->first;
+        ctx->free_blocks.erase(it);
+        return cudaSuccess;
+    }
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {  // give the cache back to the driver and retry once
+        cudaGetLastError();
+        dcache_release(ctx);
+        e = cudaMalloc(p, bytes);
+    }
+    if (e == cudaSuccess) ctx->block_size[*p] = bytes;
+    return e;
+}
+
+void dfree(rafem_ctx* ctx, void* p) {
+    if (!p) return;
+    auto it = ctx->block_size.find(p);
+    if (it == ctx->block_size.end()) {
+        cudaFree(p);
+        return;
+    }
+    ctx->free_blocks.emplace(it->second, p);
+    ctx->cached_bytes += it->second;
+    // keep at most 8 GiB cached
+    while (ctx->cached_bytes > (8ull << 30) && !ctx->free_blocks.empty()) {
+        auto big = std::prev(ctx->free_blocks.end());
+        cudaFree(big->second);
+        ctx->block_size.erase(big->second);
+        ctx->cached_bytes -= big->first;
+        ctx->free_blocks.erase(big);
+    }
+}
+
+void dcache_release(rafem_ctx* ctx) {
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (auto& kv : ctx->free_blocks) {
+        cudaFree(kv.second);
+        ctx->block_size.erase(kv.second);
+    }
+    ctx->free_blocks.clear();
+    ctx->cached_bytes = 0;
+}
+
 void* pinned(rafem_ctx* ctx, size_t bytes) {
     if (ctx->pin_bytes >= bytes && ctx->pin) return ctx->pin;
     if (ctx->pin) {
@@ -205,6 +253,9 @@ void rafem_ctx_destroy(rafem_ctx* ctx) {
                       &ctx->ws_cyc, &ctx->ws_part, &ctx->ws_res, &ctx->ws_trace, &ctx->ws_flags, &ctx->ws_simout,
                       &ctx->ws_diag})
         if (b->p) cudaFree(b->p);
+    dcache_release(ctx);
+    if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
+    if (ctx->mapped) cudaFreeHost(ctx->mapped);
     if (ctx->pin) cudaFreeHost(ctx->pin);
     for (auto& e : ctx->part_cache) cudaFree(e.gpart);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -397,11 +448,11 @@ int rafem_mesh_create(rafem_ctx* ctx, int64_t n_nodes, const double* nodes, int6
     cudaError_t e;
 #define RF_MS(x) do { e = (x); if (e != cudaSuccess) { rafem_mesh_destroy(m); return rafem_fail_cuda(ctx, e, #x, __FILE__, __LINE__); } } while (0)
     const size_t N = std::max<int64_t>(n_nodes, 1), M = std::max<int64_t>(n_tets, 1);
-    RF_MS(cudaMalloc(&m->nodes, sizeof(double) * 3 * N));
-    RF_MS(cudaMalloc(&m->tets, sizeof(int) * 4 * M));
-    RF_MS(cudaMalloc(&m->region, sizeof(int) * M));
-    RF_MS(cudaMalloc(&m->regtab, sizeof(double) * 5 * n_regions));
-    RF_MS(cudaMalloc(&m->kind, 2 * N));
+    RF_MS(dmalloc(ctx, (void**)&m->nodes, sizeof(double) * 3 * N));
+    RF_MS(dmalloc(ctx, (void**)&m->tets, sizeof(int) * 4 * M));
+    RF_MS(dmalloc(ctx, (void**)&m->region, sizeof(int) * M));
+    RF_MS(dmalloc(ctx, (void**)&m->regtab, sizeof(double) * 5 * n_regions));
+    RF_MS(dmalloc(ctx, (void**)&m->kind, 2 * N));
     RF_MS(cudaMemcpy(m->nodes, nodes, sizeof(double) * 3 * n_nodes, cudaMemcpyHostToDevice));
     RF_MS(cudaMemcpy(m->tets, t32.data(), sizeof(int) * 4 * n_tets, cudaMemcpyHostToDevice));
     RF_MS(cudaMemcpy(m->region, reg.data(), sizeof(int) * n_tets, cudaMemcpyHostToDevice));
@@ -431,7 +482,7 @@ void rafem_mesh_destroy(rafem_mesh* m) {
                     (void*)m->rp, (void*)m->col, (void*)m->diag, (void*)m->inc_ptr, (void*)m->inc_ea,
                     (void*)m->inc_slot, (void*)m->base, (void*)m->grad, (void*)m->vol, (void*)m->slot_ptr,
                     (void*)m->slot_src, (void*)m->cls, (void*)m->cls_off})
-        if (p) cudaFree(p);
+        if (p) dfree(m->ctx, p);
     delete m;
 }
 
@@ -462,15 +513,15 @@ int rafem_system_create(rafem_mesh* m, rafem_system** out) {
     const size_t N = std::max(m->N, 1), M = std::max(m->M, 1), S = std::max<long long>(m->slots, 1);
     cudaError_t e;
 #define RF_SS(x) do { e = (x); if (e != cudaSuccess) { rafem_system_destroy(s); return rafem_fail_cuda(ctx, e, #x, __FILE__, __LINE__); } } while (0)
-    RF_SS(cudaMalloc(&s->val2, sizeof(double) * 2 * S));
-    RF_SS(cudaMalloc(&s->rhs, sizeof(double) * 2 * N));
-    RF_SS(cudaMalloc(&s->contrib, sizeof(double) * 32 * M));
-    RF_SS(cudaMalloc(&s->load, sizeof(double) * 4 * M));
-    RF_SS(cudaMalloc(&s->diagpart, sizeof(double) * 2 * N));
-    RF_SS(cudaMalloc(&s->minv, sizeof(double) * 2 * N));
-    RF_SS(cudaMalloc(&s->xin, sizeof(double) * (3 * N + 2 * S)));  // host inputs / dof expansion
-    RF_SS(cudaMalloc(&s->status, 1024));
-    RF_SS(cudaMalloc(&s->xs, sizeof(double) * 6 * 2 * N));
+    RF_SS(dmalloc(ctx, (void**)&s->val2, sizeof(double) * 2 * S));
+    RF_SS(dmalloc(ctx, (void**)&s->rhs, sizeof(double) * 2 * N));
+    RF_SS(dmalloc(ctx, (void**)&s->contrib, sizeof(double) * 32 * M));
+    RF_SS(dmalloc(ctx, (void**)&s->load, sizeof(double) * 4 * M));
+    RF_SS(dmalloc(ctx, (void**)&s->diagpart, sizeof(double) * 2 * N));
+    RF_SS(dmalloc(ctx, (void**)&s->minv, sizeof(double) * 2 * N));
+    RF_SS(dmalloc(ctx, (void**)&s->xin, sizeof(double) * (3 * N + 2 * S)));  // host inputs / dof expansion
+    RF_SS(dmalloc(ctx, (void**)&s->status, 1024));
+    RF_SS(dmalloc(ctx, (void**)&s->xs, sizeof(double) * 6 * 2 * N));
     RF_SS(cudaMemset(s->status, 0, 1024));
 #undef RF_SS
     *out = s;
@@ -482,7 +533,7 @@ void rafem_system_destroy(rafem_system* s) {
     if (s->kp) rafem_kp_destroy(s->kp);
     for (void* p : {(void*)s->val2, (void*)s->rhs, (void*)s->contrib, (void*)s->load, (void*)s->diagpart,
                     (void*)s->minv, (void*)s->xin, (void*)s->status, (void*)s->xs})
-        if (p) cudaFree(p);
+        if (p) dfree(s->mesh->ctx, p);
     delete s;
 }
 
@@ -715,23 +766,25 @@ int rafem_simulate_stream(rafem_system* s, const rafem_sim_params* p, rafem_sim_
         P.fn = fn;
         P.user = user;
         double* ring = nullptr;
-        long long* counters = nullptr;  // mapped: [prog, cons]
         long long* dcounters = nullptr;
         auto cleanup = [&]() {
-            if (P.copy) cudaStreamDestroy(P.copy);
-            if (ring) cudaFree(ring);
-            if (counters) cudaFreeHost(counters);
-            if (P.hbuf) cudaFreeHost(P.hbuf);
+            if (ring) dfree(ctx, ring);
         };
-        cudaError_t e = cudaMalloc(&ring, sizeof(double) * P.rec_doubles * ring_slots);
-        if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&counters), 2 * sizeof(long long), cudaHostAllocMapped);
-        if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&dcounters), counters, 0);
-        if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&P.hbuf), sizeof(double) * P.rec_doubles, 0);
-        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&P.copy, cudaStreamNonBlocking);
+        // ring from the context cache; side stream, mapped counters and the
+        // pinned record buffer are created once per context
+        cudaError_t e = dmalloc(ctx, reinterpret_cast<void**>(&ring), sizeof(double) * P.rec_doubles * ring_slots);
+        if (e == cudaSuccess && !ctx->mapped)
+            e = cudaHostAlloc(reinterpret_cast<void**>(&ctx->mapped), 2 * sizeof(long long), cudaHostAllocMapped);
+        if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&dcounters), ctx->mapped, 0);
+        if (e == cudaSuccess && !ctx->side_stream) e = cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking);
+        P.hbuf = e == cudaSuccess ? static_cast<double*>(pinned(ctx, sizeof(double) * P.rec_doubles)) : nullptr;
+        if (e == cudaSuccess && !P.hbuf) e = cudaErrorMemoryAllocation;
         if (e != cudaSuccess) {
             cleanup();
             return rafem_fail_cuda(ctx, e, "record stream setup", __FILE__, __LINE__);
         }
+        long long* counters = ctx->mapped;
+        P.copy = ctx->side_stream;
         counters[0] = 0;
         counters[1] = 0;
         P.ring = ring;

@@ -4,7 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/rafem_b200.h"
@@ -101,6 +103,13 @@ struct rafem_ctx {
     rafem::DevBuf ws_simout;    // fused simulation summary
     rafem::DevBuf ws_diag;      // diagonal-sum partials of the assembly
     unsigned epoch = 0;         // per-launch flag epoch
+    // device blocks of destroyed meshes / systems kept for reuse (a new mesh
+    // of the same size then costs no cudaMalloc / cudaFree, which synchronise)
+    std::multimap<size_t, void*> free_blocks;
+    std::unordered_map<void*, size_t> block_size;
+    size_t cached_bytes = 0;
+    cudaStream_t side_stream = nullptr;  // record copies of rafem_simulate_stream
+    long long* mapped = nullptr;         // 2 mapped host counters (record stream)
     int last_mode = -1;  // 1: cluster-resident solve, 0: grid-wide cooperative solve
     int last_ctas = 0;
     int last_team = 0;
@@ -237,6 +246,11 @@ int coo_to_csr_device(rafem_ctx* ctx, long long nrows, long long ncols, long lon
 
 // grow a device buffer to at least `bytes`
 int ensure(rafem_ctx* ctx, DevBuf& b, size_t bytes);
+// context-cached device allocation for mesh / system arrays (stream-ordered
+// reuse on the context stream); dfree returns the block to the cache
+cudaError_t dmalloc(rafem_ctx* ctx, void** p, size_t bytes);
+void dfree(rafem_ctx* ctx, void* p);
+void dcache_release(rafem_ctx* ctx);
 void* pinned(rafem_ctx* ctx, size_t bytes);
 
 }  // namespace rafem
