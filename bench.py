@@ -372,6 +372,10 @@ def run_ours(args):
     if rank == 0 and not args.no_e2e:
         line["e2e"] = e2e_leg(mesh, mat, args, SimConfig, SolverConfig, world)
         line["e2e_plugin_seam"] = e2e_plugin_leg(mesh, mat, args, run_simulation, SimConfig, SolverConfig, world)
+        # the reference's own solver configuration through the seam: device GMRES(30) + Jacobi
+        ga = argparse.Namespace(**vars(args))
+        ga.backend, ga.steps = "gmres", 1
+        line["e2e_plugin_seam_gmres"] = e2e_plugin_leg(mesh, mat, ga, run_simulation, SimConfig, SolverConfig, world)
     if rank == 0 and not args.no_c3:
         try:
             line["spmv_c3"] = c3_leg(hbm_peak, peak_src, cpu_on=not args.no_cpu)

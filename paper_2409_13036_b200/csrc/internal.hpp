@@ -72,6 +72,7 @@ struct PartCacheEntry {
     int G;
     int* gpart;
     size_t max_slice;
+    int max_groups;
 };
 
 // Growable device scratch owned by a context.

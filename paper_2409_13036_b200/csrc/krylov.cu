@@ -76,6 +76,8 @@ struct KArgs {
     unsigned long long* flags;  // 2 x G x 8 words of barrier/all-reduce slots
     unsigned epoch;             // per-launch flag epoch (never 0)
     int pipe;                   // PCG: pipelined recurrence (pcg_pipe_core), W == 2 only
+    long long vs_off;           // GMRES: own rows of the basis in dynamic smem at this double offset (0: global)
+    int vs_ld;                  // its row stride (own dofs of the widest CTA)
 };
 
 // Phase timestamps for diagnosis: slot k of iteration i at trace[i*8 + k].
@@ -345,6 +347,20 @@ RF_DEV void multidot(const double* V, long long ldv, int nv, const double* w, in
     }
 }
 
+// Per-CTA dots v_i . w over this CTA's own dofs with the basis rows in
+// shared memory (Vs[i * ld + (e - lo)]): one warp per coefficient, lanes
+// striding the dofs, a fixed xor-butterfly — no block-level reduction.
+RF_DEV void multidot_smem(const double* Vs, int ld, int nv, const double* w, int lo, int hi, double* P, int G) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int i = wid; i < nv; i += nw) {
+        const double* vi = Vs + (long long)i * ld - lo;
+        double acc = 0.0;
+        for (int e = lo + lane; e < hi; e += 32) acc = add(acc, mul(vi[e], w[e]));
+        acc = warp_sum(acc);
+        if (lane == 0) P[(long long)i * G + blockIdx.x] = acc;
+    }
+}
+
 // Cluster mode: copy this CTA's slice of the matrix into shared memory
 // (16-byte vector loads; the slice is constant for the whole solve).
 template <int W>
@@ -555,6 +571,9 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
     const long long pstride = (long long)(m + 2) * G;
     int par = 0;
     Sync<Mode> sy{a};
+    // basis row i, own dof e: in shared memory when the host reserved room
+    double* const Vs = a.vs_off ? dyn + a.vs_off : nullptr;
+    auto vrow = [&](int i) -> double* { return Vs ? Vs + (long long)i * a.vs_ld - lo : a.V + (long long)i * ldv; };
 
     const double bnorm = prologue<Mode>(a, sy, lo, hi, co, red, par, pstride);
     if (bnorm < 0.0) return;
@@ -613,7 +632,7 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
 
         for (int k = 0; k < m; ++k) {
             double* wk = (k & 1) ? a.w1 : a.w0;
-            double* Vk = a.V + (long long)k * ldv;
+            double* Vk = vrow(k);
             // v_k (own rows) and w = A (M^-1 v_k)       (solver.py:469-470)
             for (int e = lo + tid; e < hi; e += bd) Vk[e] = mul(src[e], src_scale);
             spmv_team<W>(rows, g0, g1, a.team, SrcBasis<PRE>{src, src_scale, a.minv}, [&](int g, const double* y) {
@@ -623,7 +642,10 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
             __syncthreads();
             // CGS pass 1: h_i = v_i . w
             double* P = a.partial + par * pstride;
-            multidot(a.V, ldv, k + 1, wk, lo, hi, P, G, red);
+            if (Vs)
+                multidot_smem(Vs, a.vs_ld, k + 1, wk, lo, hi, P, G);
+            else
+                multidot(a.V, ldv, k + 1, wk, lo, hi, P, G, red);
             sy.sync_gather(P, k + 1, co);
             par ^= 1;
             if (tid == 0)
@@ -631,11 +653,16 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
             // w -= sum h_i v_i ; CGS pass 2: c_i = v_i . w
             for (int e = lo + tid; e < hi; e += bd) {
                 double acc = wk[e];
-                for (int i = 0; i <= k; ++i) acc = sub(acc, mul(co[i], __ldca(a.V + (long long)i * ldv + e)));
+                for (int i = 0; i <= k; ++i) acc = sub(acc, mul(co[i], Vs ? vrow(i)[e] : __ldca(vrow(i) + e)));
                 wk[e] = acc;
             }
             P = a.partial + par * pstride;
-            multidot(a.V, ldv, k + 1, wk, lo, hi, P, G, red);
+            if (Vs) {
+                __syncthreads();  // the warps read other threads' w entries
+                multidot_smem(Vs, a.vs_ld, k + 1, wk, lo, hi, P, G);
+            } else {
+                multidot(a.V, ldv, k + 1, wk, lo, hi, P, G, red);
+            }
             sy.sync_gather(P, k + 1, co);
             par ^= 1;
             if (tid == 0)
@@ -646,7 +673,7 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
                 for (int e = lo + tid; e < hi; e += bd) {
                     double acc = wk[e];
                     for (int i = 0; i <= k; ++i)
-                        acc = sub(acc, mul(co[i], __ldca(a.V + (long long)i * ldv + e)));
+                        acc = sub(acc, mul(co[i], Vs ? vrow(i)[e] : __ldca(vrow(i) + e)));
                     wk[e] = acc;
                     v[0] = add(v[0], mul(acc, acc));
                 }
@@ -712,7 +739,7 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
             __syncthreads();
             for (int e = lo + tid; e < hi; e += bd) {
                 double u = 0.0;
-                for (int i = 0; i < used; ++i) u = add(u, mul(__ldca(a.V + (long long)i * ldv + e), yy[i]));
+                for (int i = 0; i < used; ++i) u = add(u, mul(Vs ? vrow(i)[e] : __ldca(vrow(i) + e), yy[i]));
                 if (PRE) u = mul(a.minv[e], u);
                 a.x[e] = add(a.x[e], u);
             }
@@ -1932,14 +1959,17 @@ static const void* select_cluster(bool gmres, int W, bool pre) {
 struct PartInfo {
     int* gpart = nullptr;
     size_t max_slice = 0;
+    int max_groups = 0;
 };
 
 static int partition(rafem_ctx* ctx, const MatView& A, int G, bool need_slice, PartInfo& out) {
     // cache hit?
     for (auto& e : ctx->part_cache) {
-        if (A.pattern_id && e.pattern_id == A.pattern_id && e.G == G && e.rp == A.rp) {
+        if (A.pattern_id && e.pattern_id == A.pattern_id && e.G == G && e.rp == A.rp &&
+            (!need_slice || e.max_slice > 0)) {
             out.gpart = e.gpart;
             out.max_slice = e.max_slice;
+            out.max_groups = e.max_groups;
             return RAFEM_OK;
         }
     }
@@ -1954,6 +1984,7 @@ static int partition(rafem_ctx* ctx, const MatView& A, int G, bool need_slice, P
     ctx->launches++;
     RF_CUDA_TRY(ctx, cudaGetLastError());
     size_t max_slice = 0;
+    int max_groups = 0;
     if (need_slice) {
         std::vector<int> hp(G + 1), hr(G + 1);
         RF_CUDA_TRY(ctx, cudaMemcpyAsync(hp.data(), gpart, sizeof(int) * (G + 1), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1966,11 +1997,14 @@ static int partition(rafem_ctx* ctx, const MatView& A, int G, bool need_slice, P
             const size_t ng = (size_t)(hp[c + 1] - hp[c]);
             const size_t bytes = ns * 8 * A.W + ((ns + 3) & ~(size_t)3) * 4 + (ng + 1) * 4;
             max_slice = std::max(max_slice, bytes);
+            max_groups = std::max(max_groups, (int)ng);
         }
+        max_slice = (max_slice + 15) / 16 * 16;
     }
-    if (A.pattern_id) ctx->part_cache.push_back({A.pattern_id, A.rp, G, gpart, max_slice});
+    if (A.pattern_id) ctx->part_cache.push_back({A.pattern_id, A.rp, G, gpart, max_slice, max_groups});
     out.gpart = gpart;
     out.max_slice = max_slice;
+    out.max_groups = max_groups;
     return RAFEM_OK;
 }
 
@@ -2000,6 +2034,8 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     size_t smem = 0;
     bool cluster = false, hess_global = false;
     int stream_buf = 0, stream_valcap = 0;
+    long long vs_off = 0;
+    int vs_ld = 0;
     PartInfo part;
     int G = 0;
     // Grid mode over every SM is the default: measured on B200 (mesh-B
@@ -2081,6 +2117,14 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
         if (small && hs_al + part.max_slice <= kSmemBudget) {
             ms = 2;
             smem = hs_al + part.max_slice;
+            // GMRES: the CTA's own rows of the Krylov basis in shared memory too
+            const char* nv = getenv("RAFEM_NO_SMEM_BASIS");
+            const size_t vs_bytes = (size_t)(m + 1) * A.W * part.max_groups * sizeof(double);
+            if (gm && smem + vs_bytes <= kSmemBudget && !(nv && nv[0] == '1')) {
+                vs_off = (long long)(smem / sizeof(double));
+                vs_ld = A.W * part.max_groups;
+                smem += vs_bytes;
+            }
         } else if (hess_bytes <= 160 * 1024) {
             smem = hess_bytes;
         } else {
@@ -2133,6 +2177,8 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     a.hess = hess_global ? static_cast<double*>(ctx->ws_hess.p) : nullptr;
     a.hess_stride = hess_doubles;
     a.hess_smem = ((cluster || ms == 2) && gm) ? (hess_doubles + 1) / 2 * 2 : 0;  // keep the slice 16-B aligned
+    a.vs_off = vs_off;
+    a.vs_ld = vs_ld;
     a.m = m;
     a.tol = p.tolerance;
     a.cap = p.max_total_iters > 0 ? p.max_total_iters : 10LL * n;
