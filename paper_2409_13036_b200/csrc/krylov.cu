@@ -350,10 +350,11 @@ RF_DEV void multidot(const double* V, long long ldv, int nv, const double* w, in
 // Per-CTA dots v_i . w over this CTA's own dofs with the basis rows in
 // shared memory (Vs[i * ld + (e - lo)]): one warp per coefficient, lanes
 // striding the dofs, a fixed xor-butterfly — no block-level reduction.
-RF_DEV void multidot_smem(const double* Vs, int ld, int nv, const double* w, int lo, int hi, double* P, int G) {
+RF_DEV void multidot_smem(const double* Vs, int ld, int nv, const double* w, int lo, int hi, double* P, int G,
+                          bool self = false) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int i = wid; i < nv; i += nw) {
-        const double* vi = Vs + (long long)i * ld - lo;
+    for (int i = wid; i < nv + (self ? 1 : 0); i += nw) {
+        const double* vi = i < nv ? Vs + (long long)i * ld - lo : w;  // coefficient nv: w . w
         double acc = 0.0;
         for (int e = lo + lane; e < hi; e += 32) acc = add(acc, mul(vi[e], w[e]));
         acc = warp_sum(acc);
@@ -659,16 +660,31 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
             P = a.partial + par * pstride;
             if (Vs) {
                 __syncthreads();  // the warps read other threads' w entries
-                multidot_smem(Vs, a.vs_ld, k + 1, wk, lo, hi, P, G);
+                multidot_smem(Vs, a.vs_ld, k + 1, wk, lo, hi, P, G, true);
             } else {
                 multidot(a.V, ldv, k + 1, wk, lo, hi, P, G, red);
             }
-            sy.sync_gather(P, k + 1, co);
+            sy.sync_gather(P, Vs ? k + 2 : k + 1, co);
             par ^= 1;
             if (tid == 0)
                 for (int i = 0; i <= k; ++i) H[(long long)k * (m + 1) + i] = add(H[(long long)k * (m + 1) + i], co[i]);
+            double hk1;
+            if (Vs) {
+                // ||w - V c||^2 = ||w||^2 - ||c||^2 (V orthonormal, c = V^T w, tiny
+                // after the first pass): no third reduction, only the barrier
+                // that makes the new w visible to the next SpMV's gathers
+                double cc = 0.0;
+                for (int i = 0; i <= k; ++i) cc = add(cc, mul(co[i], co[i]));
+                hk1 = sqrt(fmax(sub(co[k + 1], cc), 0.0));
+                for (int e = lo + tid; e < hi; e += bd) {
+                    double acc = wk[e];
+                    for (int i = 0; i <= k; ++i) acc = sub(acc, mul(co[i], vrow(i)[e]));
+                    wk[e] = acc;
+                }
+                sy.barrier();
+            }
             // w -= sum c_i v_i ; ||w||
-            {
+            else {
                 double v[1] = {0.0};
                 for (int e = lo + tid; e < hi; e += bd) {
                     double acc = wk[e];
@@ -680,8 +696,8 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
                 P = a.partial + par * pstride;
                 sy.template reduce<1>(v, 1, P, co, red);
                 par ^= 1;
+                hk1 = sqrt(co[0]);
             }
-            const double hk1 = sqrt(co[0]);
             total += 1;
             // Givens update of column k (solver.py:478-496), one thread per CTA
             if (tid == 0) {
