@@ -1007,7 +1007,7 @@ RF_DEV PcgOut pcg_core(const KArgs& a, const R& rows, Sync<Mode>& sy, double bno
 // one history entry per update, converged only on the TRUE residual (the
 // head recomputes r, u, w, m from x), breakdown -> RAFEM_ERR_BREAKDOWN.
 
-constexpr int kPipeRows = 256;  // max node rows per CTA (y staged in smem)
+constexpr int kPipeRows = 128;  // max node rows per CTA (y and the owner vectors staged in smem)
 
 // bnorm < 0: ||b|| (and, with zflag, the zero-diagonal flag of the Jacobi
 // setup) are folded into the first head reduction instead of a separate
@@ -1019,19 +1019,25 @@ template <bool PRE, class Mode, class R>
 RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, double bnorm, double* co, double* red,
                             int& par, const int* zflag = nullptr, const double* x0_gather = nullptr) {
     __shared__ double2 ybuf[kPipeRows];
+    // owner-only recurrence vectors live in shared memory (indexed by the
+    // global dof, offset by the CTA's first dof); u is mirrored to global
+    // memory only when a head's SpMV gathers it
+    __shared__ double s_r[2 * kPipeRows], s_u[2 * kPipeRows], s_w[2 * kPipeRows], s_z[2 * kPipeRows],
+        s_q[2 * kPipeRows], s_s[2 * kPipeRows], s_p[2 * kPipeRows];
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
     const int g0 = a.gpart[cta], g1 = a.gpart[cta + 1];
     const int lo = 2 * g0, hi = 2 * g1;
     const long long pstride = 8LL * G;
     const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     double* x = a.x;
-    double* r = a.r;
-    double* u = a.z;
-    double* w = a.w0;
-    double* z = a.p1;
-    double* q = a.q;
-    double* sv = a.e0;
-    double* p = a.p0;
+    double* r = s_r - lo;
+    double* u = s_u - lo;
+    double* ug = a.z;  // global copy of u for the head's gather
+    double* w = s_w - lo;
+    double* z = s_z - lo;
+    double* q = s_q - lo;
+    double* sv = s_s - lo;
+    double* p = s_p - lo;
     auto mb = [&](int i) { return i ? a.e1 : a.w1; };
     auto M = [&](int e) { return PRE ? __ldg(a.minv + e) : 1.0; };
 
@@ -1070,8 +1076,10 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                     const int e = 2 * g + k;
                     const double be = a.b[e];
                     const double re = sub(be, y[k]);
+                    const double ue = PRE ? mul(M(e), re) : re;
                     r[e] = re;
-                    u[e] = PRE ? mul(M(e), re) : re;
+                    u[e] = ue;
+                    ug[e] = ue;
                     v[2] = add(v[2], mul(re, re));
                     if (with_b) v[0] = add(v[0], mul(be, be));
                 }
@@ -1097,7 +1105,7 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
         {
             double v[3] = {0.0, 0.0, 0.0};
             double* m = mb(cur);
-            spmv_team<2>(rows, g0, g1, a.team, SrcPlain{u}, [&](int g, const double* y) {
+            spmv_team<2>(rows, g0, g1, a.team, SrcPlain{ug}, [&](int g, const double* y) {
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
                     const int e = 2 * g + k;
@@ -2236,7 +2244,7 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
         // RAFEM_PIPE=0 selects the single-reduction Chronopoulos-Gear kernel
         const char* pe = getenv("RAFEM_PIPE");
         const int rows_per_cta = (A.ngroups + G - 1) / G;
-        a.pipe = (!gm && A.W == 2 && !cluster && ms != 3 && rows_per_cta <= kPipeRows / 2 && !(pe && pe[0] == '0'))
+        a.pipe = (!gm && A.W == 2 && !cluster && ms != 3 && rows_per_cta <= kPipeRows && !(pe && pe[0] == '0'))
                      ? 1 : 0;
     }
     if (cluster) smem = (size_t)a.hess_smem * 8 + part.max_slice;
@@ -2314,14 +2322,12 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     const bool pre = p->solver.precondition == RAFEM_PRECOND_JACOBI;
     // 256 threads per CTA: rows * team <= 256 holds at paper scale, the PCG
     // iteration is as fast as with 512 (measured), and the 255-register cap
-    // leaves room for the thread-per-slot fill.  RAFEM_SIM_THREADS=512
-    // selects the wide CTA (warp-per-row fill).
-    int nt = 256;
-    if (const char* env = getenv("RAFEM_SIM_THREADS")) nt = atoi(env) == 512 ? 512 : 256;
-    if (nt == 256 && !mesh->slot_lists_tried)
+    // leaves room for the thread-per-slot fill and the pipelined PCG's
+    // shared-memory vectors.
+    const int nt = 256;
+    if (!mesh->slot_lists_tried)
         if (int rc = mesh_slot_lists(mesh)) return rc;
-    const void* fn = nt == 256 ? (pre ? (const void*)simulate_kernel<true, 256> : (const void*)simulate_kernel<false, 256>)
-                               : (pre ? (const void*)simulate_kernel<true, 512> : (const void*)simulate_kernel<false, 512>);
+    const void* fn = pre ? (const void*)simulate_kernel<true, 256> : (const void*)simulate_kernel<false, 256>;
     const int G = std::max(1, std::min(ctx->sm_count, N));
     PartInfo part;
     if (A.slots * 20LL > (long long)G * (150 << 10)) return RAFEM_ERR_UNSUPPORTED;
@@ -2382,7 +2388,7 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     }
     {
         const char* pe = getenv("RAFEM_PIPE");
-        a.pipe = ((N + G - 1) / G <= kPipeRows / 2 && !(pe && pe[0] == '0')) ? 1 : 0;
+        a.pipe = ((N + G - 1) / G <= kPipeRows && !(pe && pe[0] == '0')) ? 1 : 0;
     }
     S.m = asm_mesh(mesh);
     S.contrib = reinterpret_cast<double2*>(s->contrib);
