@@ -1023,7 +1023,8 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
     // global dof, offset by the CTA's first dof); u is mirrored to global
     // memory only when a head's SpMV gathers it
     __shared__ double s_r[2 * kPipeRows], s_u[2 * kPipeRows], s_w[2 * kPipeRows], s_z[2 * kPipeRows],
-        s_q[2 * kPipeRows], s_s[2 * kPipeRows], s_p[2 * kPipeRows];
+        s_q[2 * kPipeRows], s_s[2 * kPipeRows], s_p[2 * kPipeRows], s_x[2 * kPipeRows], s_m[2 * kPipeRows],
+        s_mv[2 * kPipeRows];
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
     const int g0 = a.gpart[cta], g1 = a.gpart[cta + 1];
     const int lo = 2 * g0, hi = 2 * g1;
@@ -1039,7 +1040,12 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
     double* sv = s_s - lo;
     double* p = s_p - lo;
     auto mb = [&](int i) { return i ? a.e1 : a.w1; };
-    auto M = [&](int e) { return PRE ? __ldg(a.minv + e) : 1.0; };
+    double* xs = s_x - lo;   // owner copy of x (written through to HBM)
+    double* ms = s_m - lo;   // owner copy of the current m
+    double* mvs = s_mv - lo; // owner Jacobi inverse diagonal
+    for (int e = lo + tid; e < hi; e += blockDim.x) mvs[e] = PRE ? __ldg(a.minv + e) : 1.0;
+    __syncthreads();
+    auto M = [&](int e) { return mvs[e]; };
 
     long long total = 0, cycles = 0, hlen = 0;
     bool converged = false;
@@ -1085,6 +1091,7 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                 }
             });
             if (with_b && zflag && tid == 0) v[1] = (double)*zflag;
+            for (int e = lo + tid; e < hi; e += blockDim.x) xs[e] = x[e];  // owner copy (synced below)
             sy.template reduce<3>(v, 3, a.partial + par * pstride, co, red);
             par ^= 1;
             if (with_b) {
@@ -1092,6 +1099,7 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                 bnorm = sqrt(co[0]);
                 if (bnorm == 0.0) {  // zero data: zero solution (solver.py:422-425)
                     for (int e = lo + tid; e < hi; e += blockDim.x) x[e] = 0.0;
+                    __syncthreads();
                     return PcgOut{0, 0.0, 1, RAFEM_OK};
                 }
             }
@@ -1111,7 +1119,9 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                     const int e = 2 * g + k;
                     const double ue = u[e], re = r[e];
                     w[e] = y[k];
-                    m[e] = PRE ? mul(M(e), y[k]) : y[k];
+                    const double me = PRE ? mul(M(e), y[k]) : y[k];
+                    m[e] = me;
+                    ms[e] = me;
                     v[0] = add(v[0], mul(re, ue));
                     v[1] = add(v[1], mul(y[k], ue));
                     v[2] = add(v[2], mul(re, re));
@@ -1159,7 +1169,7 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
             double v[3] = {0.0, 0.0, 0.0};
             for (int e = lo + tid; e < hi; e += blockDim.x) {
                 const double ne = (e & 1) ? ybuf[(e >> 1) - g0].y : ybuf[(e >> 1) - g0].x;
-                const double me = m[e], we = w[e], ue = u[e];
+                const double me = ms[e], we = w[e], ue = u[e];
                 double ze = ne, qe = me, se = we, pe = ue;
                 if (!first) {
                     ze = add(ne, mul(beta, z[e]));
@@ -1171,14 +1181,18 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                 q[e] = qe;
                 sv[e] = se;
                 p[e] = pe;
-                x[e] = add(x[e], mul(alpha, pe));
+                const double xn = add(xs[e], mul(alpha, pe));
+                xs[e] = xn;
+                x[e] = xn;
                 const double rn = sub(r[e], mul(alpha, se));
                 const double un = sub(ue, mul(alpha, qe));
                 const double wn = sub(we, mul(alpha, ze));
                 r[e] = rn;
                 u[e] = un;
                 w[e] = wn;
-                mn[e] = PRE ? mul(M(e), wn) : wn;
+                const double mne = PRE ? mul(M(e), wn) : wn;
+                mn[e] = mne;
+                ms[e] = mne;
                 v[0] = add(v[0], mul(rn, un));
                 v[1] = add(v[1], mul(wn, un));
                 v[2] = add(v[2], mul(rn, rn));
