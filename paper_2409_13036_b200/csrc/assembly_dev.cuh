@@ -243,14 +243,28 @@ RF_DEV double dof_value(int kind, double applied, double btemp) {
 // Node row i, one warp: voltage-row scaling and symmetric Dirichlet
 // elimination keeping the explicit zeros (fem.py:398-428), in place on the
 // row's slots; optional Jacobi inverse diagonal of the final row.
+// Staged variant: the row's length, diagonal offset, its own dof kinds and
+// its columns' kinds (ckind[l] = kind(2 col) | kind(2 col + 1) << 2) come
+// from shared memory; null ckind reads them from the mesh.
 RF_DEV void constrain_node_warp(int i, const AsmMesh& m, double scale, int apply, double applied, double btemp,
                                 double2* vals, double* rhs, double* minv, int* zero_diag,
-                                const int* cols = nullptr) {
+                                const int* cols = nullptr, const uint8_t* ckind = nullptr, int sdeg = 0,
+                                int sdslot = -1, int skV = 0, int skT = 0) {
     const int lane = threadIdx.x & 31;
-    const int s0 = __ldg(m.rp + i), deg = __ldg(m.rp + i + 1) - s0;
-    if (!cols) cols = m.col + s0;
-    const int kV = apply ? m.kind[2LL * i] : 0, kT = apply ? m.kind[2LL * i + 1] : 0;
-    const int dslot = __ldg(m.diag + i);
+    int deg, kV, kT, dslot;
+    if (ckind) {
+        deg = sdeg;
+        dslot = sdslot;
+        kV = apply ? skV : 0;
+        kT = apply ? skT : 0;
+    } else {
+        const int s0 = __ldg(m.rp + i);
+        deg = __ldg(m.rp + i + 1) - s0;
+        if (!cols) cols = m.col + s0;
+        kV = apply ? m.kind[2LL * i] : 0;
+        kT = apply ? m.kind[2LL * i + 1] : 0;
+        dslot = __ldg(m.diag + i);
+    }
     double mV = 0.0, mT = 0.0;  // moved-column sums in storage order (fem.py:419-424)
     double dV = 0.0, dT = 0.0;
     for (int cb = 0; cb < deg; cb += 32) {
@@ -259,7 +273,16 @@ RF_DEV void constrain_node_warp(int i, const AsmMesh& m, double scale, int apply
         int movV = 0, movT = 0;
         if (l < deg) {
             const int j = cols[l];
-            const int cV = apply ? m.kind[2LL * j] : 0, cT = apply ? m.kind[2LL * j + 1] : 0;
+            int cV = 0, cT = 0;
+            if (apply) {
+                if (ckind) {
+                    cV = ckind[l] & 3;
+                    cT = ckind[l] >> 2;
+                } else {
+                    cV = m.kind[2LL * j];
+                    cT = m.kind[2LL * j + 1];
+                }
+            }
             const double2 v = vals[l];
             const double vs = mul(v.x, scale);
             if (!kV && cV) {

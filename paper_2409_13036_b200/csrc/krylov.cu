@@ -2348,8 +2348,33 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     if (int rc = partition(ctx, A, G, true, part)) return rc;
     cudaFuncAttributes fa;
     RF_CUDA_TRY(ctx, cudaFuncGetAttributes(&fa, fn));
-    const size_t smem = part.max_slice;
+    size_t smem = part.max_slice;
     if (smem + fa.sharedSizeBytes > 227 * 1024) return RAFEM_ERR_UNSUPPORTED;
+    // room to stage each CTA's assembly index data (simulate_dev.cuh)
+    int stage_fill = 0;
+    if (mesh->slot_src && !(getenv("RAFEM_NO_STAGE_FILL") && getenv("RAFEM_NO_STAGE_FILL")[0] == '1')) {
+        std::vector<int> hg(G + 1), hrp(N + 1), hip(N + 1);
+        RF_CUDA_TRY(ctx, cudaMemcpy(hg.data(), part.gpart, sizeof(int) * (G + 1), cudaMemcpyDeviceToHost));
+        RF_CUDA_TRY(ctx, cudaMemcpy(hrp.data(), mesh->rp, sizeof(int) * (N + 1), cudaMemcpyDeviceToHost));
+        RF_CUDA_TRY(ctx, cudaMemcpy(hip.data(), mesh->inc_ptr, sizeof(int) * (N + 1), cudaMemcpyDeviceToHost));
+        std::vector<int> hsp(mesh->slots + 1);
+        RF_CUDA_TRY(ctx, cudaMemcpy(hsp.data(), mesh->slot_ptr, sizeof(int) * (mesh->slots + 1), cudaMemcpyDeviceToHost));
+        size_t need = 0;
+        for (int c = 0; c < G; ++c) {
+            const size_t nr = (size_t)(hg[c + 1] - hg[c]);
+            const size_t ns = (size_t)(hrp[hg[c + 1]] - hrp[hg[c]]);
+            const size_t nsrc = (size_t)(hsp[hrp[hg[c + 1]]] - hsp[hrp[hg[c]]]);
+            const size_t ninc = (size_t)(hip[hg[c + 1]] - hip[hg[c]]);
+            const size_t slice = ns * 16 + ((ns + 3) & ~(size_t)3) * 4 + (nr + 1) * 4;
+            const size_t extra = (ns + 1) * 4 + nsrc * 4 + (nr + 1) * 4 + ninc * 4 + nr * 4 + ns + 2 * nr;
+            need = std::max(need, slice + extra);
+        }
+        need = (need + 15) / 16 * 16;
+        if (need + fa.sharedSizeBytes <= 227 * 1024) {
+            smem = std::max(smem, need);
+            stage_fill = 1;
+        }
+    }
     RF_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     RF_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nt, smem));
@@ -2405,6 +2430,7 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
         a.pipe = ((N + G - 1) / G <= kPipeRows && !(pe && pe[0] == '0')) ? 1 : 0;
     }
     S.m = asm_mesh(mesh);
+    S.stage_fill = stage_fill;
     S.contrib = reinterpret_cast<double2*>(s->contrib);
     S.load = s->load;
     S.rhs = s->rhs;

@@ -45,6 +45,7 @@ struct SimArgs {
     volatile long long* cons;  // records the host has consumed (host writes)
     long long* ptrace;         // optional per-pass phase stamps (globaltimer ns), 8 per pass
     long long ptrace_cap;
+    int stage_fill;            // contributor lists, incidences and dof kinds staged in smem
 };
 
 // Max over CTAs of one nonnegative value (exact, order independent).
@@ -93,6 +94,40 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
     int* srp = scol + ((ns + 3) & ~3);
     for (int g = g0 + tid; g <= g1; g += blockDim.x) srp[g - g0] = __ldg(a.A.rp + g) - s0;
     for (int s = tid; s < ns; s += blockDim.x) scol[s] = __ldg(a.A.col + s0 + s);
+    // the assembly's constant index data for this CTA's rows, staged once so
+    // a pass's fill and constraint steps do no dependent index loads:
+    // [slot list offsets | contributor list | incidence offsets | incidences |
+    //  diagonal offsets | column kinds per slot | dof kinds per row]
+    const int nr = g1 - g0;
+    int* sptr = srp + nr + 1;
+    int nsrc = 0, ninc = 0;
+    int *ssrc = nullptr, *iptr = nullptr, *sdg = nullptr;
+    unsigned* iea = nullptr;
+    uint8_t *ckd = nullptr, *rkd = nullptr;
+    if (S.stage_fill) {
+        const int sp0 = __ldg(S.m.slot_ptr + s0), ip0 = __ldg(S.m.inc_ptr + g0);
+        nsrc = __ldg(S.m.slot_ptr + s0 + ns) - sp0;
+        ninc = __ldg(S.m.inc_ptr + g1) - ip0;
+        ssrc = sptr + ns + 1;
+        iptr = ssrc + nsrc;
+        iea = reinterpret_cast<unsigned*>(iptr + nr + 1);
+        sdg = reinterpret_cast<int*>(iea + ninc);
+        ckd = reinterpret_cast<uint8_t*>(sdg + nr);
+        rkd = ckd + ns;
+        for (int k = tid; k <= ns; k += blockDim.x) sptr[k] = __ldg(S.m.slot_ptr + s0 + k) - sp0;
+        for (int k = tid; k < nsrc; k += blockDim.x) ssrc[k] = __ldg(S.m.slot_src + sp0 + k);
+        for (int r = tid; r <= nr; r += blockDim.x) iptr[r] = __ldg(S.m.inc_ptr + g0 + r) - ip0;
+        for (int k = tid; k < ninc; k += blockDim.x) iea[k] = __ldg(S.m.inc_ea + ip0 + k);
+        for (int r = tid; r < nr; r += blockDim.x) {
+            sdg[r] = __ldg(S.m.diag + g0 + r);
+            rkd[2 * r] = S.m.kind[2LL * (g0 + r)];
+            rkd[2 * r + 1] = S.m.kind[2LL * (g0 + r) + 1];
+        }
+        for (int k = tid; k < ns; k += blockDim.x) {
+            const int j = __ldg(a.A.col + s0 + k);
+            ckd[k] = (uint8_t)(S.m.kind[2LL * j] | (S.m.kind[2LL * j + 1] << 2));
+        }
+    }
     if (tid == 0) zflag = 0;
     __syncthreads();
     const Rows<2, true, false> rows{srp, scol, sval, g0};
@@ -164,7 +199,50 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
             sy.barrier();  // a row's fill gathers contributions of other CTAs' elements
             SIM_STAMP(2, global_ns());
             // ---- fill own rows into the shared-memory slice
-            if (NT == 256 && S.m.slot_src) {
+            if (S.stage_fill) {
+                // thread per slot over its staged contributor list (every gather of
+                // a chunk in flight), then thread per row for the T rhs and diagonal
+                for (int sl = tid; sl < ns; sl += blockDim.x) {
+                    const int k0 = sptr[sl], k1 = sptr[sl + 1];
+                    double av = 0.0, at = 0.0;
+                    for (int k = k0; k < k1; k += 8) {
+                        double2 c[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            if (k + q < k1) c[q] = __ldcg(S.contrib + ssrc[k + q]);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            if (k + q < k1) {
+                                av = add(av, c[q].x);
+                                at = add(at, c[q].y);
+                            }
+                    }
+                    sv2[sl] = make_double2(av, at);
+                }
+                __syncthreads();
+                for (int r = tid; r < nr; r += blockDim.x) {
+                    const int p0 = iptr[r], p1 = iptr[r + 1];
+                    double racc = 0.0;
+                    for (int pp = p0; pp < p1; pp += 8) {
+                        double l[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            if (pp + q < p1) {
+                                const unsigned ea = iea[pp + q];
+                                l[q] = __ldcg(S.load + 4LL * (ea & 0x3fffffffu) + (ea >> 30));
+                            }
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            if (pp + q < p1) racc = add(racc, l[q]);
+                    }
+                    const long long i = g0 + r;
+                    S.rhs[2 * i] = 0.0;
+                    S.rhs[2 * i + 1] = racc;
+                    const double2 dvv = sdg[r] >= 0 ? sv2[srp[r] + sdg[r]] : make_double2(0.0, 0.0);
+                    S.diag_raw[2 * i] = dvv.x;
+                    S.diag_raw[2 * i + 1] = dvv.y;
+                }
+            } else if (NT == 256 && S.m.slot_src) {
                 // thread per slot over its contributor list, then thread per row
                 // (at 256 threads the kernel has the registers for the wide batches)
                 for (int sl = tid; sl < ns; sl += blockDim.x) sv2[sl] = fill_slot(s0 + sl, S.m, S.contrib);
@@ -197,9 +275,16 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
             double scale = 1.0;  // fem.py:390-396
             if (co[0] > 0.0 && co[1] > 0.0) scale = ldexp(1.0, (int)rint(log2(co[1] / co[0])));
             // ---- scale + Dirichlet + Jacobi on own rows; x0 = iterate
-            for (int i = g0 + warp; i < g1; i += nwarps)
-                constrain_node_warp(i, S.m, scale, 1, p.applied_voltage, p.boundary_temp, sv2 + srp[i - g0], S.rhs,
-                                    PRE ? const_cast<double*>(a.minv) : nullptr, &zflag, scol + srp[i - g0]);
+            for (int i = g0 + warp; i < g1; i += nwarps) {
+                const int r = i - g0;
+                if (S.stage_fill)
+                    constrain_node_warp(i, S.m, scale, 1, p.applied_voltage, p.boundary_temp, sv2 + srp[r], S.rhs,
+                                        PRE ? const_cast<double*>(a.minv) : nullptr, &zflag, scol + srp[r],
+                                        ckd + srp[r], srp[r + 1] - srp[r], sdg[r], rkd[2 * r], rkd[2 * r + 1]);
+                else
+                    constrain_node_warp(i, S.m, scale, 1, p.applied_voltage, p.boundary_temp, sv2 + srp[r], S.rhs,
+                                        PRE ? const_cast<double*>(a.minv) : nullptr, &zflag, scol + srp[r]);
+            }
             for (int e = lo + tid; e < hi; e += blockDim.x) X(inew)[e] = X(iit)[e];
             __syncthreads();
             PcgOut o{0, 0.0, 1, RAFEM_OK};
