@@ -381,6 +381,11 @@ def run_ours(args):
             line["spmv_c3"] = c3_leg(hbm_peak, peak_src, cpu_on=not args.no_cpu)
         except Exception as exc:  # noqa: BLE001
             line["spmv_c3"] = {"error": str(exc)[:300]}
+    if rank == 0 and not args.no_c3:
+        try:
+            line["small_c1"] = c1_leg(args)
+        except Exception as exc:  # noqa: BLE001
+            line["small_c1"] = {"error": str(exc)[:300]}
     if not args.no_c4:
         try:
             c4 = c4_leg(hbm_peak, peak_src, world, rank, local)
@@ -457,6 +462,49 @@ def e2e_plugin_leg(mesh, mat, args, run_simulation, SimConfig, SolverConfig, wor
     return {"value": summ.accepted_steps * reps / wall, "unit": "steps/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "reps": reps,
             "path": "run_simulation -> assemble_global -> solve (host numpy in/out every pass)"}
+
+
+def c1_leg(args):
+    """configs[0]: the mesh-A analog (15x15x16, 7,200 dofs), 40 s simulated
+    (10 accepted steps), native loop vs the CPU port on one core."""
+    import torch
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh
+    from paper_2409_13036_b200.timeloop import DeviceRun
+    from paper_2409_13036_b200 import _native as nat
+    mesh = generate_box_mesh(15, 15, 16)
+    cfg = SimConfig(total_time=40.0, solver=SolverConfig(backend=args.backend, precondition="jacobi"))
+    run = DeviceRun(mesh, MaterialParams.default())
+    for _ in range(3):
+        run.run(cfg, record_fields=False)
+    stream = torch.cuda.ExternalStream(nat.lib().rafem_stream(nat.context()))
+    times = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, summ = run.run(cfg, record_fields=False)
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = float(np.median(times))
+    out = {"workload": "generate_box_mesh(15,15,16), 40 s simulated", "accepted_steps": int(summ.accepted_steps),
+           "corrector_passes": int(summ.passes), "ms_per_run": ms,
+           "steps_per_s": int(summ.accepted_steps) / (ms / 1e3)}
+    if not args.no_cpu:
+        smp = subprocess.run([sys.executable, "-c", (
+            "import sys,json,time; sys.path.insert(0, %r)\n"
+            "from oracle import rafem_oracle as O\n"
+            "m = O.box_mesh(15, 15, 16)\n"
+            "t0 = time.perf_counter(); r = O.run(m, {0: O.OMaterial()}, O.OSim(total_time=40.0), keep_fields=False)\n"
+            "print(json.dumps({'steps': r.accepted_steps, 'wall_s': time.perf_counter() - t0}))\n") % ROOT],
+            capture_output=True, text=True, env=dict(os.environ, OPENBLAS_NUM_THREADS="1", OMP_NUM_THREADS="1"),
+            timeout=300)
+        if smp.returncode == 0:
+            c = json.loads(smp.stdout.strip().splitlines()[-1])
+            out["cpu_baseline"] = {"kind": "port", "cores": 1, "wall_s": c["wall_s"],
+                                   "steps_per_s": c["steps"] / c["wall_s"],
+                                   "sample": "the whole 40 s run, GMRES(30)+Jacobi 1e-10"}
+            out["speedup_vs_cpu"] = c["wall_s"] / (ms / 1e3)
+    return out
 
 
 def c4_leg(hbm_peak, peak_src, world, rank, local):
