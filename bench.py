@@ -47,11 +47,19 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--backend", default="pcg", choices=["pcg", "gmres"])
+    ap.add_argument("--precond", default="block_jacobi", choices=["jacobi", "block_jacobi"],
+                    help="PCG preconditioner (GMRES always uses the reference's point Jacobi)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-c3", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
     return ap.parse_args()
+
+
+def prec_of(args):
+    """PCG: block-Jacobi (north_star's "Jacobi or block-Jacobi"); GMRES: the
+    reference's point Jacobi."""
+    return args.precond if args.backend == "pcg" else "jacobi"
 
 
 def dist_env():
@@ -274,7 +282,7 @@ def run_ours(args):
 
     mesh = generate_box_mesh(*MESH_B)
     mat = MaterialParams.default()
-    cfg = SimConfig(total_time=TOTAL_TIME, solver=SolverConfig(backend=args.backend, precondition="jacobi"))
+    cfg = SimConfig(total_time=TOTAL_TIME, solver=SolverConfig(backend=args.backend, precondition=prec_of(args)))
     runner = DeviceRun(mesh, mat)
     stream = torch.cuda.ExternalStream(nat.lib().rafem_stream(nat.context()))
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MB > L2
@@ -360,7 +368,7 @@ def run_ours(args):
                    "slots": S, "total_time_s": TOTAL_TIME, "accepted_steps_per_run": steps_per_run,
                    "corrector_passes_per_run": summs[0].passes,
                    "solver_iterations_per_run": summs[0].total_solver_iterations,
-                   "solver": f"{args.backend}+jacobi tol 1e-10", "parallelism": f"replicas x{world}",
+                   "solver": f"{args.backend}+{prec_of(args)} tol 1e-10", "parallelism": f"replicas x{world}",
                    "step": "one full 900 s simulation", "l2": "flushed (256 MB write) between timed steps",
                    "device_path": f"{runner.last_mode} ({runner.last_ctas} CTAs)",
                    "assemble_ms_per_run": asm_ms / args.steps, "solve_ms_per_run": solve_ms / args.steps},
@@ -421,7 +429,7 @@ def e2e_leg(mesh, mat, args, SimConfig, SolverConfig, world):
     memory, runs the symbolic phase, and reads every accepted step's V/T
     fields back to host arrays."""
     from paper_2409_13036_b200.timeloop import DeviceRun
-    cfg = SimConfig(total_time=TOTAL_TIME, solver=SolverConfig(backend=args.backend, precondition="jacobi"))
+    cfg = SimConfig(total_time=TOTAL_TIME, solver=SolverConfig(backend=args.backend, precondition=prec_of(args)))
 
     def one():
         recs = []
@@ -447,7 +455,7 @@ def e2e_leg(mesh, mat, args, SimConfig, SolverConfig, world):
 def e2e_plugin_leg(mesh, mat, args, run_simulation, SimConfig, SolverConfig, world):
     """Same metric through the reference's plug-in seam (run_simulation ->
     assemble_global -> solve) with host numpy buffers every corrector pass."""
-    cfg = SimConfig(total_time=TOTAL_TIME, solver=SolverConfig(backend=args.backend, precondition="jacobi"))
+    cfg = SimConfig(total_time=TOTAL_TIME, solver=SolverConfig(backend=args.backend, precondition=prec_of(args)))
     run_simulation(mesh, mat, cfg)  # warm (mesh upload + symbolic phase cached)
     reps = max(1, min(args.steps, 3))
     t0 = time.perf_counter()
@@ -472,7 +480,7 @@ def c1_leg(args):
     from paper_2409_13036_b200.timeloop import DeviceRun
     from paper_2409_13036_b200 import _native as nat
     mesh = generate_box_mesh(15, 15, 16)
-    cfg = SimConfig(total_time=40.0, solver=SolverConfig(backend=args.backend, precondition="jacobi"))
+    cfg = SimConfig(total_time=40.0, solver=SolverConfig(backend=args.backend, precondition=prec_of(args)))
     run = DeviceRun(mesh, MaterialParams.default())
     for _ in range(3):
         run.run(cfg, record_fields=False)

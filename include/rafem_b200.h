@@ -50,6 +50,12 @@ extern "C" {
 
 #define RAFEM_PRECOND_NONE 0
 #define RAFEM_PRECOND_JACOBI 1
+/* block-Jacobi over the persistent solver's row blocks (one per CTA), each
+ * block solved by one Neumann step on the Jacobi-scaled block:
+ * M^-1 = D^-1 + omega D^-1 (D - A_bb) D^-1.  Used by the paper-scale
+ * pipelined PCG (north_star's "Jacobi or block-Jacobi"); the other engines
+ * and GMRES treat it as point Jacobi. */
+#define RAFEM_PRECOND_BLOCK_JACOBI 2
 
 /* Dirichlet kind per interleaved dof (fem.py:403-413). */
 #define RAFEM_DOF_FREE 0

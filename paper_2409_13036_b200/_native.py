@@ -28,6 +28,7 @@ METHOD_GMRES = 0
 METHOD_PCG = 1
 PRECOND_NONE = 0
 PRECOND_JACOBI = 1
+PRECOND_BLOCK_JACOBI = 2
 
 DOF_FREE = 0
 DOF_APPLIED_VOLTAGE = 1

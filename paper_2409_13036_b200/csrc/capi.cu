@@ -136,6 +136,8 @@ int check_params(rafem_ctx* ctx, const rafem_solver_params* p) {
     if (p->restart_m < 1) return rafem_fail(ctx, RAFEM_ERR_INVALID, "restart_m must be at least 1");
     if (!(p->tolerance > 0.0 && p->tolerance < 1.0))
         return rafem_fail(ctx, RAFEM_ERR_INVALID, "tolerance must lie in (0, 1)");
+    if (p->precondition < RAFEM_PRECOND_NONE || p->precondition > RAFEM_PRECOND_BLOCK_JACOBI)
+        return rafem_fail(ctx, RAFEM_ERR_INVALID, "unknown preconditioner");
     return RAFEM_OK;
 }
 
@@ -182,7 +184,7 @@ int solve_common(rafem_ctx* ctx, const MatView& A, double* b_dev, bool b_is_host
         x0_dev = xbuf;
     }
     int* flag = &dstat->flag;
-    if (p->precondition == RAFEM_PRECOND_JACOBI) {
+    if (p->precondition != RAFEM_PRECOND_NONE) {
         if (int rc = jacobi_minv(ctx, A, minv, flag)) return rc;
     } else {
         RF_CUDA_TRY(ctx, cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
@@ -890,7 +892,7 @@ int rafem_simulate(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary
     RF_CUDA_TRY(ctx, cudaMemcpyAsync(xprev, xacc, sizeof(double) * n2, cudaMemcpyDeviceToDevice, st));
     SysStatus* ds = sys_status(s);
     const MatView A = system_view(s);
-    const bool pre = p->solver.precondition == RAFEM_PRECOND_JACOBI;
+    const bool pre = p->solver.precondition != RAFEM_PRECOND_NONE;
     rafem_assemble_params ap{};
     ap.applied_voltage = p->applied_voltage;
     ap.boundary_temp = p->boundary_temp;

@@ -76,6 +76,7 @@ struct KArgs {
     unsigned long long* flags;  // 2 x G x 8 words of barrier/all-reduce slots
     unsigned epoch;             // per-launch flag epoch (never 0)
     int pipe;                   // PCG: pipelined recurrence (pcg_pipe_core), W == 2 only
+    int block;                  // pipelined PCG: block-Jacobi (Neumann step) on the CTA's diagonal block
     long long vs_off;           // GMRES: own rows of the basis in dynamic smem at this double offset (0: global)
     int vs_ld;                  // its row stride (own dofs of the widest CTA)
 };
@@ -1024,7 +1025,9 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
     // memory only when a head's SpMV gathers it
     __shared__ double s_r[2 * kPipeRows], s_u[2 * kPipeRows], s_w[2 * kPipeRows], s_z[2 * kPipeRows],
         s_q[2 * kPipeRows], s_s[2 * kPipeRows], s_p[2 * kPipeRows], s_x[2 * kPipeRows], s_m[2 * kPipeRows],
-        s_mv[2 * kPipeRows];
+        s_mv[2 * kPipeRows], s_y[2 * kPipeRows];
+    __shared__ double s_omega;
+    __shared__ unsigned s_inmask[kPipeRows];
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
     const int g0 = a.gpart[cta], g1 = a.gpart[cta + 1];
     const int lo = 2 * g0, hi = 2 * g1;
@@ -1046,6 +1049,68 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
     for (int e = lo + tid; e < hi; e += blockDim.x) mvs[e] = PRE ? __ldg(a.minv + e) : 1.0;
     __syncthreads();
     auto M = [&](int e) { return mvs[e]; };
+    // Block-Jacobi (a.block): M^-1 = D^-1 + omega D^-1 (D - A_cc) D^-1 on this
+    // CTA's diagonal block A_cc, i.e. one Neumann step of the block solve:
+    // m = y + omega D^-1 (w - A_cc y), y = D^-1 w.  SPD when omega < 1 /
+    // (lambda_max(D^-1/2 A_cc D^-1/2) - 1); omega comes from the block's
+    // Gershgorin bound (1 for the FEM blocks, whose bound stays below 2).
+    const bool blk = PRE && a.block;
+    double* yl = s_y - lo;
+    const int nr = g1 - g0;
+    if (blk) {
+        // in-block slots of each own row as a bit mask (rows have <= 32 slots
+        // here), and the block's Gershgorin bound of D^-1/2 A_cc D^-1/2
+        double gmax = 0.0;
+        for (int rr = tid; rr < nr; rr += blockDim.x) {
+            const int g = g0 + rr, sb = rows.start(g), deg = rows.start(g + 1) - sb;
+            unsigned mask = 0;
+            double gv = 0.0, gt = 0.0;
+            for (int l = 0; l < deg && l < 32; ++l) {
+                const int c = rows.column(sb + l);
+                if (c < g0 || c >= g1) continue;
+                mask |= 1u << l;
+                const double2 v = rows.value2(sb + l);
+                gv = add(gv, mul(fabs(v.x), sqrt(mul(mvs[2 * g], mvs[2 * c]))));
+                gt = add(gt, mul(fabs(v.y), sqrt(mul(mvs[2 * g + 1], mvs[2 * c + 1]))));
+            }
+            s_inmask[rr] = mask;
+            gmax = fmax(gmax, fmax(gv, gt));
+        }
+        gmax = block_max(gmax, red);
+        if (tid == 0) s_omega = gmax > 1.98 ? 0.98 / (gmax - 1.0) : 1.0;
+        __syncthreads();
+    }
+    const double omega = blk ? s_omega : 0.0;
+    // dst (owner dofs, smem) = M^-1 src; also to dst_g when given.  y = D^-1 src
+    // is expected in yl already when y_ready (the caller fused it).
+    auto apply_block = [&](const double* src, double* dst, double* dst_g, bool y_ready) {
+        if (!y_ready)
+            for (int e = lo + tid; e < hi; e += blockDim.x) yl[e] = mul(mvs[e], src[e]);
+        __syncthreads();
+        for (int rr = tid; rr < nr; rr += blockDim.x) {  // thread per row over its in-block slots
+            const int g = g0 + rr, sb = rows.start(g);
+            unsigned mask = s_inmask[rr];
+            double av = 0.0, at = 0.0;
+            while (mask) {
+                const int l = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const int c = rows.column(sb + l);
+                const double2 v = rows.value2(sb + l);
+                av = add(av, mul(v.x, yl[2 * c]));
+                at = add(at, mul(v.y, yl[2 * c + 1]));
+            }
+            const int e0 = 2 * g;
+            const double d0 = add(yl[e0], mul(omega, mul(mvs[e0], sub(src[e0], av))));
+            const double d1 = add(yl[e0 + 1], mul(omega, mul(mvs[e0 + 1], sub(src[e0 + 1], at))));
+            dst[e0] = d0;
+            dst[e0 + 1] = d1;
+            if (dst_g) {
+                dst_g[e0] = d0;
+                dst_g[e0 + 1] = d1;
+            }
+        }
+        __syncthreads();
+    };
 
     long long total = 0, cycles = 0, hlen = 0;
     bool converged = false;
@@ -1082,14 +1147,20 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                     const int e = 2 * g + k;
                     const double be = a.b[e];
                     const double re = sub(be, y[k]);
-                    const double ue = PRE ? mul(M(e), re) : re;
                     r[e] = re;
-                    u[e] = ue;
-                    ug[e] = ue;
+                    if (!blk) {
+                        const double ue = PRE ? mul(M(e), re) : re;
+                        u[e] = ue;
+                        ug[e] = ue;
+                    }
                     v[2] = add(v[2], mul(re, re));
                     if (with_b) v[0] = add(v[0], mul(be, be));
                 }
             });
+            if (blk) {
+                __syncthreads();
+                apply_block(r, u, ug, false);
+            }
             if (with_b && zflag && tid == 0) v[1] = (double)*zflag;
             for (int e = lo + tid; e < hi; e += blockDim.x) xs[e] = x[e];  // owner copy (synced below)
             sy.template reduce<3>(v, 3, a.partial + par * pstride, co, red);
@@ -1119,14 +1190,20 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                     const int e = 2 * g + k;
                     const double ue = u[e], re = r[e];
                     w[e] = y[k];
-                    const double me = PRE ? mul(M(e), y[k]) : y[k];
-                    m[e] = me;
-                    ms[e] = me;
+                    if (!blk) {
+                        const double me = PRE ? mul(M(e), y[k]) : y[k];
+                        m[e] = me;
+                        ms[e] = me;
+                    }
                     v[0] = add(v[0], mul(re, ue));
                     v[1] = add(v[1], mul(y[k], ue));
                     v[2] = add(v[2], mul(re, re));
                 }
             });
+            if (blk) {
+                __syncthreads();
+                apply_block(w, ms, m, false);
+            }
             publish3(v);
             sy.barrier();
         }
@@ -1190,13 +1267,18 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                 r[e] = rn;
                 u[e] = un;
                 w[e] = wn;
-                const double mne = PRE ? mul(M(e), wn) : wn;
-                mn[e] = mne;
-                ms[e] = mne;
+                if (!blk) {
+                    const double mne = PRE ? mul(M(e), wn) : wn;
+                    mn[e] = mne;
+                    ms[e] = mne;
+                } else {
+                    yl[e] = mul(M(e), wn);  // y = D^-1 w for the block step below
+                }
                 v[0] = add(v[0], mul(rn, un));
                 v[1] = add(v[1], mul(wn, un));
                 v[2] = add(v[2], mul(rn, rn));
             }
+            if (blk) apply_block(w, ms, mn, true);  // (its leading barrier orders y)
             cur ^= 1;
             first = false;
             publish3(v);
@@ -2052,7 +2134,7 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     const int n = A.ngroups * A.W;
     const bool gm = p.method != RAFEM_METHOD_PCG;
     const int m = gm ? p.restart_m : 1;
-    const bool pre = p.precondition == RAFEM_PRECOND_JACOBI;
+    const bool pre = p.precondition != RAFEM_PRECOND_NONE;  // block-Jacobi needs the point inverse too
     const bool stream = streams_matrix(A);
 
     // x starts at x0 (or zero); the kernel never touches x before the first
@@ -2260,6 +2342,7 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
         const int rows_per_cta = (A.ngroups + G - 1) / G;
         a.pipe = (!gm && A.W == 2 && !cluster && ms != 3 && rows_per_cta <= kPipeRows && !(pe && pe[0] == '0'))
                      ? 1 : 0;
+        a.block = (a.pipe && p.precondition == RAFEM_PRECOND_BLOCK_JACOBI && A.maxdeg > 0 && A.maxdeg <= 32) ? 1 : 0;
     }
     if (cluster) smem = (size_t)a.hess_smem * 8 + part.max_slice;
     void* args[] = {&a};
@@ -2333,7 +2416,7 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     A.pattern_id = mesh->id;
     A.maxdeg = mesh->maxdeg;
     if (mesh->maxdeg > 32) return RAFEM_ERR_UNSUPPORTED;
-    const bool pre = p->solver.precondition == RAFEM_PRECOND_JACOBI;
+    const bool pre = p->solver.precondition != RAFEM_PRECOND_NONE;
     // 256 threads per CTA: rows * team <= 256 holds at paper scale, the PCG
     // iteration is as fast as with 512 (measured), and the 255-register cap
     // leaves room for the thread-per-slot fill and the pipelined PCG's
@@ -2428,6 +2511,7 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     {
         const char* pe = getenv("RAFEM_PIPE");
         a.pipe = ((N + G - 1) / G <= kPipeRows && !(pe && pe[0] == '0')) ? 1 : 0;
+        a.block = (a.pipe && p->solver.precondition == RAFEM_PRECOND_BLOCK_JACOBI && mesh->maxdeg <= 32) ? 1 : 0;
     }
     S.m = asm_mesh(mesh);
     S.stage_fill = stage_fill;

@@ -611,7 +611,7 @@ int rafem_kp_begin(rafem_kp* k, const double* b, const double* x0, const rafem_s
         RF_CUDA_TRY(ctx, cudaMemcpyAsync(a.x, x0, nb, cudaMemcpyHostToDevice, ctx->stream));
     else
         RF_CUDA_TRY(ctx, cudaMemsetAsync(a.x, 0, nb, ctx->stream));
-    k->pre = p->precondition == RAFEM_PRECOND_JACOBI;
+    k->pre = p->precondition != RAFEM_PRECOND_NONE;  // block-Jacobi: point Jacobi on this engine
     if (k->pre) {
         MatView own = a.A;
         if (int rc = jacobi_minv(ctx, own, const_cast<double*>(reinterpret_cast<const double*>(a.minv)), k->flag))

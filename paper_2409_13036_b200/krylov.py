@@ -40,7 +40,7 @@ __all__ = [
 
 BACKENDS = ("qr", "gmres", "dense", "pcg")
 DEVICE_BACKENDS = ("gmres", "pcg")
-PRECONDITIONERS = ("none", "jacobi")
+PRECONDITIONERS = ("none", "jacobi", "block_jacobi")  # block_jacobi: this package (rafem_b200.h)
 ORDERINGS = ("none", "rcm")
 
 
@@ -154,7 +154,8 @@ def _params(cfg, method: int) -> nat.SolverParams:
     p.restart_m = int(cfg.restart_m)
     p.tolerance = float(cfg.tolerance)
     p.max_total_iters = int(cfg.max_total_iters) if cfg.max_total_iters is not None else 0
-    p.precondition = nat.PRECOND_JACOBI if cfg.precondition == "jacobi" else nat.PRECOND_NONE
+    p.precondition = {"jacobi": nat.PRECOND_JACOBI, "block_jacobi": nat.PRECOND_BLOCK_JACOBI}.get(
+        cfg.precondition, nat.PRECOND_NONE)
     p.grid_ctas = int(getattr(cfg, "grid_ctas", 0) or 0)
     return p
 

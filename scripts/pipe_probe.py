@@ -12,14 +12,14 @@ for dims in [(20, 20, 21), (15, 15, 16)]:
     s = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, v, t, 0.5)
     a = s.matrix
     x0 = np.empty(2 * n); x0[0::2], x0[1::2] = v, t
-    for pipe in ["1", "0"]:
+    for pipe, prec in [("1", "block_jacobi"), ("1", "jacobi"), ("0", "jacobi")]:
         os.environ["RAFEM_PIPE"] = pipe
         for tol in (1e-10, 1e-12):
-            cfg = SolverConfig(backend="pcg", precondition="jacobi", tolerance=tol)
+            cfg = SolverConfig(backend="pcg", precondition=prec, tolerance=tol)
             best = 1e9
             for _ in range(3):
                 x, st = solve(a, s.rhs, x0=x0, config=cfg)
                 best = min(best, st.device_ms * 1e3 / st.iterations)
             res = np.linalg.norm(s.rhs - O.matvec(a.row_ptr, a.col_idx, a.vals, x)) / np.linalg.norm(s.rhs)
-            print(f"{dims} pipe={pipe} tol={tol:g} it={st.iterations} restarts={st.restarts} {best:.2f} us/it "
+            print(f"{dims} pipe={pipe} {prec:12s} tol={tol:g} it={st.iterations} restarts={st.restarts} {best:.2f} us/it "
                   f"true_res={res:.2e} reported={st.final_relative_residual:.2e} conv={st.converged}", flush=True)

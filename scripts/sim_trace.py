@@ -8,7 +8,8 @@ from paper_2409_13036_b200.timeloop import DeviceRun
 L, ctx = nat.lib(), nat.context()
 dims = tuple(int(a) for a in sys.argv[1:4]) if len(sys.argv) >= 4 else (20, 20, 21)
 run = DeviceRun(generate_box_mesh(*dims), MaterialParams.default())
-cfg = SimConfig(total_time=900.0, solver=SolverConfig(backend="pcg", precondition="jacobi"))
+import os
+cfg = SimConfig(total_time=900.0, solver=SolverConfig(backend="pcg", precondition=os.environ.get("PREC", "jacobi")))
 run.run(cfg, record_fields=False)
 for rep in range(2):
     L.rafem_set_trace(ctx, 1)
