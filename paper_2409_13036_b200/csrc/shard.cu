@@ -777,7 +777,7 @@ int kp_system_solve(rafem_system* s, const double* b, const double* x0, const ra
     if (!s->kp) {
         if (int rc = rafem_kp_create(s, m->N, m->N, 1, 0, &s->kp)) {
             s->kp = nullptr;
-            return rc == RAFEM_ERR_UNSUPPORTED ? rc : rc;
+            return rc;  // RAFEM_ERR_UNSUPPORTED: the caller keeps the persistent engine
         }
         if (int rc = rafem_kp_set_halo(s->kp, nullptr, 0)) return rc;
     }

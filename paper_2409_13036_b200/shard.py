@@ -208,7 +208,10 @@ class ShardComm:
             return
         if self.device:
             with self._ctx():
-                self.dist.all_gather_into_tensor(slots, slots[r * w:(r + 1) * w], group=self.group)
+                # a separate input buffer (not a view of the output) keeps NCCL's
+                # in-place rules out of the picture
+                mine = slots[r * w:(r + 1) * w].clone()
+                self.dist.all_gather_into_tensor(slots, mine, group=self.group)
             return
         self._sync(slots)
         mine = slots[r * w:(r + 1) * w].cpu().clone()
