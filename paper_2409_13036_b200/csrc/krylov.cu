@@ -6,18 +6,24 @@
 //
 // One launch runs a whole solve.  Every CTA owns a contiguous block of row
 // groups (balanced by slots + rows), keeps its share of every vector, and
-// meets the others only at barriers around the scalar reductions.  Two
-// execution modes share the same solver bodies:
+// meets the others only at barriers around the scalar reductions.  Engines
+// (chosen in krylov_solve):
 //
-//   * cluster mode (paper-scale systems): ONE thread-block cluster of up to
-//     16 CTAs.  Each CTA copies its matrix slice into shared memory once and
-//     the barriers are hardware cluster barriers (~0.2 us), so a Krylov
-//     iteration costs a few microseconds with no HBM matrix traffic.
-//   * grid mode (large systems): a cooperative launch of one CTA per SM
-//     with grid-wide barriers; matrix slots stream from HBM with
-//     evict-first loads while the gathered vectors stay in L2.
+//   * grid mode, smem slices (paper scale, the default there): a
+//     cooperative launch of one CTA per SM, each CTA's matrix slice staged
+//     in shared memory once; PCG runs the pipelined recurrence
+//     (pcg_pipe_core: one barrier per iteration, the dot-product gather
+//     overlapped with the SpMV, owner vectors in shared memory, optional
+//     block-Jacobi), GMRES keeps its own basis rows in shared memory.
+//   * grid mode, global rows: the same bodies reading the matrix from HBM.
+//   * streaming PCG (pcg_stream_kernel, matrices >= 48 MB): rows staged by
+//     TMA bulk copies, materialised preconditioned residual.
+//   * cluster mode (RAFEM_SOLVER_MODE=cluster): one thread-block cluster
+//     with DSMEM barriers; measured slower, kept for experiments.
+//   The kernel-per-phase PCG for the largest and sharded systems lives in
+//   shard.cu; the whole-simulation kernel in simulate_dev.cuh.
 //
-// Reductions are deterministic in both modes: per-thread partial sums in
+// Reductions are deterministic in every mode: per-thread partial sums in
 // a fixed order, a fixed xor-butterfly per warp, per-CTA partials in global
 // memory, and every CTA re-reduces the G partials in the same fixed order,
 // so all CTAs take identical control decisions and results are bitwise
