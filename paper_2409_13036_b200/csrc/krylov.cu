@@ -1213,9 +1213,16 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
             publish3(v);
             sy.barrier();
         }
-        double gamma = 0.0, alpha = 0.0;
+        // alpha_{i+1} = gn / (dn - beta gn / alpha_i), beta = gn / gamma, is
+        // evaluated as gn / (dn - (gn * ig) * gn) with ig = 1 / (gamma alpha_i)
+        // formed while the previous update streams: one division (not three
+        // plus a square root) between the gathered scalars and the update.
+        // The convergence test compares squared norms; the history keeps the
+        // squared estimates and is rescaled once after the solve.
+        double gamma = 0.0, alpha = 0.0, ig = 0.0, igam = 0.0;
         bool first = true;
         const long long hstart = hlen;
+        const double thr = mul(mul(a.tol, bnorm), mul(a.tol, bnorm));
         while (true) {
             // n = A m (gathered) || fold the partials of the current vectors
             gather3();
@@ -1235,12 +1242,12 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                 alpha = gn / dn;
             } else {
                 ++total;
-                const double est = sqrt(co[2]) / bnorm;
-                if (cta == 0 && tid == 0 && hlen < a.hist_cap) a.hist[hlen] = est;
+                const double rr = co[2];
+                if (cta == 0 && tid == 0 && hlen < a.hist_cap) a.hist[hlen] = rr;
                 ++hlen;
-                if (est <= a.tol || total >= a.cap) break;
-                beta = gn / gamma;
-                const double den = dn - beta * gn / alpha;
+                if (rr <= thr || total >= a.cap) break;
+                beta = gn * igam;
+                const double den = fma(-(gn * ig), gn, dn);
                 if (!(gn > 0.0) || !(den > 0.0) || !isfinite(den)) {
                     status = RAFEM_ERR_BREAKDOWN;
                     break;
@@ -1248,6 +1255,8 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                 alpha = gn / den;
             }
             gamma = gn;
+            igam = 1.0 / gn;
+            ig = 1.0 / (gn * alpha);
             double* mn = mb(cur ^ 1);
             double v[3] = {0.0, 0.0, 0.0};
             for (int e = lo + tid; e < hi; e += blockDim.x) {
@@ -1291,6 +1300,11 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
             sy.barrier();
         }
         if (cta == 0 && tid == 0 && cycles < a.cyc_cap) a.cyc[cycles] = hlen - hstart;
+        if (cta == 0) {  // squared estimates of this cycle -> relative residuals
+            __syncthreads();
+            for (long long h = hstart + tid; h < hlen && h < a.hist_cap; h += blockDim.x)
+                a.hist[h] = sqrt(a.hist[h]) / bnorm;
+        }
         ++cycles;
         if (status != RAFEM_OK) break;
     }
