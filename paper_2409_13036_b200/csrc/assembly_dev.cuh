@@ -240,6 +240,41 @@ RF_DEV double dof_value(int kind, double applied, double btemp) {
     return kind == RAFEM_DOF_APPLIED_VOLTAGE ? applied : (kind == RAFEM_DOF_BOUNDARY_TEMP ? btemp : 0.0);
 }
 
+// Node row i, one thread, everything staged in shared memory (the fused
+// simulation's slice): the same per-slot arithmetic as constrain_node_warp
+// and the moved-column sums in the same storage order, so the row is
+// bit-identical; the rows of a CTA run side by side instead of a warp
+// walking them one after another.
+RF_DEV void constrain_node_thread(int i, double scale, double applied, double btemp, double2* vals, double* rhs,
+                                  double* minv, int* zero_diag, const int* cols, const uint8_t* ckind, int deg,
+                                  int dslot, int kV, int kT, double rt) {
+    double mV = 0.0, mT = 0.0, dV = 0.0, dT = 0.0;
+    for (int l = 0; l < deg; ++l) {
+        const int j = cols[l];
+        const int cV = ckind[l] & 3, cT = ckind[l] >> 2;
+        const double2 v = vals[l];
+        const double vs = mul(v.x, scale);
+        if (!kV && cV) mV = add(mV, mul(vs, dof_value(cV, applied, btemp)));
+        if (!kT && cT) mT = add(mT, mul(v.y, dof_value(cT, applied, btemp)));
+        double outV = vs, outT = v.y;
+        if (kV || cV) outV = (kV && j == i) ? 1.0 : 0.0;
+        if (kT || cT) outT = (kT && j == i) ? 1.0 : 0.0;
+        vals[l] = make_double2(outV, outT);
+        if (l == dslot) {
+            dV = outV;
+            dT = outT;
+        }
+    }
+    rhs[2LL * i] = kV ? dof_value(kV, applied, btemp) : sub(0.0, mV);
+    rhs[2LL * i + 1] = kT ? dof_value(kT, applied, btemp) : sub(rt, mT);
+    if (minv) {
+        if (dslot < 0) dV = dT = 0.0;
+        if (dV == 0.0 || dT == 0.0) atomicOr(zero_diag, 1);
+        minv[2LL * i] = 1.0 / dV;
+        minv[2LL * i + 1] = 1.0 / dT;
+    }
+}
+
 // Node row i, one warp: voltage-row scaling and symmetric Dirichlet
 // elimination keeping the explicit zeros (fem.py:398-428), in place on the
 // row's slots; optional Jacobi inverse diagonal of the final row.
@@ -249,7 +284,7 @@ RF_DEV double dof_value(int kind, double applied, double btemp) {
 RF_DEV void constrain_node_warp(int i, const AsmMesh& m, double scale, int apply, double applied, double btemp,
                                 double2* vals, double* rhs, double* minv, int* zero_diag,
                                 const int* cols = nullptr, const uint8_t* ckind = nullptr, int sdeg = 0,
-                                int sdslot = -1, int skV = 0, int skT = 0) {
+                                int sdslot = -1, int skV = 0, int skT = 0, const double* srt = nullptr) {
     const int lane = threadIdx.x & 31;
     int deg, kV, kT, dslot;
     if (ckind) {
@@ -322,7 +357,7 @@ RF_DEV void constrain_node_warp(int i, const AsmMesh& m, double scale, int apply
     }
     if (lane == 0) {
         double rv = 0.0;  // V rhs is zero before constraints (fem.py:388, 400)
-        double rt = rhs[2LL * i + 1];
+        double rt = srt ? *srt : rhs[2LL * i + 1];  // srt: the fill's T rhs staged in smem
         if (apply) {
             rv = kV ? dof_value(kV, applied, btemp) : sub(rv, mV);
             rt = kT ? dof_value(kT, applied, btemp) : sub(rt, mT);

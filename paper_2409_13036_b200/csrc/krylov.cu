@@ -945,7 +945,7 @@ RF_DEV PcgOut pcg_core(const KArgs& a, const R& rows, Sync<Mode>& sy, double bno
                     o.r[k] = ro[e];
                     o.w[k] = wo[e];
                     o.s[k] = mode == 2 ? so[e] : 0.0;
-                    o.m[k] = PRE ? __ldg(a.minv + e) : 1.0;
+                    o.m[k] = PRE ? __ldcg(a.minv + e) : 1.0;
                     o.p[k] = mode == 2 ? p[e] : 0.0;
                     o.x[k] = a.x[e];
                 }
@@ -1052,7 +1052,7 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
     double* xs = s_x - lo;   // owner copy of x (written through to HBM)
     double* ms = s_m - lo;   // owner copy of the current m
     double* mvs = s_mv - lo; // owner Jacobi inverse diagonal
-    for (int e = lo + tid; e < hi; e += blockDim.x) mvs[e] = PRE ? __ldg(a.minv + e) : 1.0;
+    for (int e = lo + tid; e < hi; e += blockDim.x) mvs[e] = PRE ? __ldcg(a.minv + e) : 1.0;
     __syncthreads();
     auto M = [&](int e) { return mvs[e]; };
     // Block-Jacobi (a.block): M^-1 = D^-1 + omega D^-1 (D - A_cc) D^-1 on this
@@ -2469,7 +2469,7 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
             const size_t nsrc = (size_t)(hsp[hrp[hg[c + 1]]] - hsp[hrp[hg[c]]]);
             const size_t ninc = (size_t)(hip[hg[c + 1]] - hip[hg[c]]);
             const size_t slice = ns * 16 + ((ns + 3) & ~(size_t)3) * 4 + (nr + 1) * 4;
-            const size_t extra = (ns + 1) * 4 + nsrc * 4 + (nr + 1) * 4 + ninc * 4 + nr * 4 + ns + 2 * nr;
+            const size_t extra = (ns + 1) * 4 + nsrc * 4 + (nr + 1) * 4 + ninc * 4 + nr * 4 + ns + 2 * nr + 8 + 8 * nr;
             need = std::max(need, slice + extra);
         }
         need = (need + 15) / 16 * 16;

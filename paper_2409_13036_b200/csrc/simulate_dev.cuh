@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
     int *ssrc = nullptr, *iptr = nullptr, *sdg = nullptr;
     unsigned* iea = nullptr;
     uint8_t *ckd = nullptr, *rkd = nullptr;
+    double* srt = nullptr;  // T rhs of the own rows between the fill and the constraints
     if (S.stage_fill) {
         const int sp0 = __ldg(S.m.slot_ptr + s0), ip0 = __ldg(S.m.inc_ptr + g0);
         nsrc = __ldg(S.m.slot_ptr + s0 + ns) - sp0;
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
         sdg = reinterpret_cast<int*>(iea + ninc);
         ckd = reinterpret_cast<uint8_t*>(sdg + nr);
         rkd = ckd + ns;
+        srt = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(rkd + 2 * nr) + 7) & ~uintptr_t(7));
         for (int k = tid; k <= ns; k += blockDim.x) sptr[k] = __ldg(S.m.slot_ptr + s0 + k) - sp0;
         for (int k = tid; k < nsrc; k += blockDim.x) ssrc[k] = __ldg(S.m.slot_src + sp0 + k);
         for (int r = tid; r <= nr; r += blockDim.x) iptr[r] = __ldg(S.m.inc_ptr + g0 + r) - ip0;
@@ -199,6 +201,9 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
             sy.barrier();  // a row's fill gathers contributions of other CTAs' elements
             SIM_STAMP(2, global_ns());
             // ---- fill own rows into the shared-memory slice
+            // diagonal sums and the PhysicsRange count in ONE reduction; the
+            // offending element is located only on the (aborting) bad path
+            double dv[3] = {0.0, 0.0, badv > 0.0 ? 1.0 : 0.0};
             if (S.stage_fill) {
                 // thread per slot over its staged contributor list (every gather of
                 // a chunk in flight), then thread per row for the T rhs and diagonal
@@ -236,11 +241,12 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
                             if (pp + q < p1) racc = add(racc, l[q]);
                     }
                     const long long i = g0 + r;
-                    S.rhs[2 * i] = 0.0;
-                    S.rhs[2 * i + 1] = racc;
+                    srt[r] = racc;
                     const double2 dvv = sdg[r] >= 0 ? sv2[srp[r] + sdg[r]] : make_double2(0.0, 0.0);
                     S.diag_raw[2 * i] = dvv.x;
                     S.diag_raw[2 * i + 1] = dvv.y;
+                    dv[0] = add(dv[0], dvv.x);  // same rows, same order as the loop below
+                    dv[1] = add(dv[1], dvv.y);
                 }
             } else if (NT == 256 && S.m.slot_src) {
                 // thread per slot over its contributor list, then thread per row
@@ -254,13 +260,11 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
                     fill_node_warp(i, S.m, S.contrib, S.load, sv2 + srp[i - g0], S.rhs, S.diag_raw, ws[warp]);
             }
             __syncthreads();
-            // diagonal sums and the PhysicsRange count in ONE reduction; the
-            // offending element is located only on the (aborting) bad path
-            double dv[3] = {0.0, 0.0, badv > 0.0 ? 1.0 : 0.0};
-            for (int i = g0 + tid; i < g1; i += blockDim.x) {
-                dv[0] = add(dv[0], S.diag_raw[2LL * i]);
-                dv[1] = add(dv[1], S.diag_raw[2LL * i + 1]);
-            }
+            if (!S.stage_fill)
+                for (int i = g0 + tid; i < g1; i += blockDim.x) {
+                    dv[0] = add(dv[0], S.diag_raw[2LL * i]);
+                    dv[1] = add(dv[1], S.diag_raw[2LL * i + 1]);
+                }
             sy.template reduce<3>(dv, 3, P(), co, red);
             par ^= 1;
             if (co[2] > 0.0) {  // PhysicsRangeError aborts the run (fem.py:274)
@@ -274,18 +278,24 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
             SIM_STAMP(3, global_ns());
             double scale = 1.0;  // fem.py:390-396
             if (co[0] > 0.0 && co[1] > 0.0) scale = ldexp(1.0, (int)rint(log2(co[1] / co[0])));
-            // ---- scale + Dirichlet + Jacobi on own rows; x0 = iterate
-            for (int i = g0 + warp; i < g1; i += nwarps) {
-                const int r = i - g0;
-                if (S.stage_fill)
-                    constrain_node_warp(i, S.m, scale, 1, p.applied_voltage, p.boundary_temp, sv2 + srp[r], S.rhs,
-                                        PRE ? const_cast<double*>(a.minv) : nullptr, &zflag, scol + srp[r],
-                                        ckd + srp[r], srp[r + 1] - srp[r], sdg[r], rkd[2 * r], rkd[2 * r + 1]);
-                else
+            // ---- scale + Dirichlet + Jacobi on own rows; x0 = iterate (its
+            // loads issued ahead of the constraint loop)
+            const int ec = lo + tid;
+            const double xc = ec < hi ? X(iit)[ec] : 0.0;
+            if (S.stage_fill)
+                for (int r = tid; r < nr; r += blockDim.x)
+                    constrain_node_thread(g0 + r, scale, p.applied_voltage, p.boundary_temp, sv2 + srp[r], S.rhs,
+                                          PRE ? const_cast<double*>(a.minv) : nullptr, &zflag, scol + srp[r],
+                                          ckd + srp[r], srp[r + 1] - srp[r], sdg[r], rkd[2 * r], rkd[2 * r + 1],
+                                          srt[r]);
+            else
+                for (int i = g0 + warp; i < g1; i += nwarps) {
+                    const int r = i - g0;
                     constrain_node_warp(i, S.m, scale, 1, p.applied_voltage, p.boundary_temp, sv2 + srp[r], S.rhs,
                                         PRE ? const_cast<double*>(a.minv) : nullptr, &zflag, scol + srp[r]);
-            }
-            for (int e = lo + tid; e < hi; e += blockDim.x) X(inew)[e] = X(iit)[e];
+                }
+            if (ec < hi) X(inew)[ec] = xc;
+            for (int e = ec + blockDim.x; e < hi; e += blockDim.x) X(inew)[e] = X(iit)[e];
             __syncthreads();
             PcgOut o{0, 0.0, 1, RAFEM_OK};
             long long tb;
