@@ -1224,12 +1224,34 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
         const long long hstart = hlen;
         const double thr = mul(mul(a.tol, bnorm), mul(a.tol, bnorm));
         while (true) {
-            // n = A m (gathered) || fold the partials of the current vectors
-            gather3();
+            // n = A m (gathered) || fold the partials of the current vectors.
+            // The folding warps issue their partial loads first and add them
+            // up after their own share of the SpMV, so the fold's round trip
+            // hides under the SpMV's (same order as reduce_partials_warp).
+            constexpr int kFold = 5;  // partials per lane in flight: G <= 160
+            const int gw = warp - (nwarps - 3);
+            double pv[kFold];
+            if (gw >= 0) {
+                if (G <= 32 * kFold) {
+                    const double* src = a.partial + par * pstride + (long long)gw * G;
+#pragma unroll
+                    for (int j = 0; j < kFold; ++j) pv[j] = lane + 32 * j < G ? __ldcg(src + lane + 32 * j) : 0.0;
+                } else {
+                    gather3();
+                }
+            }
             const double* m = mb(cur);
             spmv_team<2>(rows, g0, g1, a.team, SrcPlain{m}, [&](int g, const double* y) {
                 ybuf[g - g0] = make_double2(y[0], y[1]);
             });
+            if (gw >= 0 && G <= 32 * kFold) {
+                double sacc = 0.0;
+#pragma unroll
+                for (int j = 0; j < kFold; ++j)
+                    if (lane + 32 * j < G) sacc = add(sacc, pv[j]);
+                sacc = warp_sum(sacc);
+                if (lane == 0) co[gw] = sacc;
+            }
             __syncthreads();
             par ^= 1;
             const double gn = co[0], dn = co[1];
