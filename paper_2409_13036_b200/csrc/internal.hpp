@@ -73,6 +73,7 @@ struct PartCacheEntry {
     int* gpart;
     size_t max_slice;
     int max_groups;
+    bool by_rows;
 };
 
 // Growable device scratch owned by a context.

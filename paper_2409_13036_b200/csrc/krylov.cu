@@ -1726,7 +1726,7 @@ __global__ void __launch_bounds__(KTC, 1) pcg_cluster_kernel(KArgs a) {
 
 // Balanced partition of row groups: CTA c starts at the first group whose
 // weight prefix (slots + groups) reaches c/G of the total.
-__global__ void partition_kernel(const int* rp, int ngroups, int G, int* gpart) {
+__global__ void partition_kernel(const int* rp, int ngroups, int G, int* gpart, int by_rows) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c > G) return;
     if (c == 0) {
@@ -1735,6 +1735,10 @@ __global__ void partition_kernel(const int* rp, int ngroups, int G, int* gpart) 
     }
     if (c == G) {
         gpart[G] = ngroups;
+        return;
+    }
+    if (by_rows) {
+        gpart[c] = (int)((long long)ngroups * c / G);
         return;
     }
     const long long total = (long long)rp[ngroups] + ngroups;
@@ -2124,10 +2128,21 @@ struct PartInfo {
     int max_groups = 0;
 };
 
-static int partition(rafem_ctx* ctx, const MatView& A, int G, bool need_slice, PartInfo& out) {
+// by_rows: equal row-group counts (ceil(ngroups / G) at most per CTA) for
+// the pipelined PCG, whose SpMV phase costs one team pass per 256 / team
+// rows: a slot-balanced split hands the CTAs with many short boundary rows
+// a second pass (measured: 79-row CTAs set the iteration time at mesh B).
+// The pipelined PCG runs (RAFEM_PIPE=0 selects the single-reduction kernel)
+static bool pipe_rows(bool gm, int W, int ngroups, int G) {
+    const char* pe = getenv("RAFEM_PIPE");
+    return !gm && W == 2 && (ngroups + G - 1) / G <= kPipeRows && !(pe && pe[0] == '0');
+}
+
+static int partition(rafem_ctx* ctx, const MatView& A, int G, bool need_slice, PartInfo& out,
+                     bool by_rows = false) {
     // cache hit?
     for (auto& e : ctx->part_cache) {
-        if (A.pattern_id && e.pattern_id == A.pattern_id && e.G == G && e.rp == A.rp &&
+        if (A.pattern_id && e.pattern_id == A.pattern_id && e.G == G && e.rp == A.rp && e.by_rows == by_rows &&
             (!need_slice || e.max_slice > 0)) {
             out.gpart = e.gpart;
             out.max_slice = e.max_slice;
@@ -2142,7 +2157,7 @@ static int partition(rafem_ctx* ctx, const MatView& A, int G, bool need_slice, P
         if (int rc = ensure(ctx, ctx->ws_part, sizeof(int) * (size_t)(G + 1))) return rc;
         gpart = static_cast<int*>(ctx->ws_part.p);
     }
-    partition_kernel<<<(G + 1 + 127) / 128, 128, 0, ctx->stream>>>(A.rp, A.ngroups, G, gpart);
+    partition_kernel<<<(G + 1 + 127) / 128, 128, 0, ctx->stream>>>(A.rp, A.ngroups, G, gpart, by_rows ? 1 : 0);
     ctx->launches++;
     RF_CUDA_TRY(ctx, cudaGetLastError());
     size_t max_slice = 0;
@@ -2163,7 +2178,7 @@ static int partition(rafem_ctx* ctx, const MatView& A, int G, bool need_slice, P
         }
         max_slice = (max_slice + 15) / 16 * 16;
     }
-    if (A.pattern_id) ctx->part_cache.push_back({A.pattern_id, A.rp, G, gpart, max_slice, max_groups});
+    if (A.pattern_id) ctx->part_cache.push_back({A.pattern_id, A.rp, G, gpart, max_slice, max_groups, by_rows});
     out.gpart = gpart;
     out.max_slice = max_slice;
     out.max_groups = max_groups;
@@ -2274,7 +2289,7 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
         G = want;
         // stage the matrix slice in smem when it fits next to the Hessenberg scratch
         const bool small = A.slots * (4 + 8LL * A.W) <= (long long)G * (160 << 10);
-        if (int rc = partition(ctx, A, G, small, part)) return rc;
+        if (int rc = partition(ctx, A, G, small, part, pipe_rows(gm, A.W, A.ngroups, G))) return rc;
         const size_t hs_al = (size_t)((hess_doubles + 1) / 2 * 2) * 8;
         if (small && hs_al + part.max_slice <= kSmemBudget) {
             ms = 2;
@@ -2470,7 +2485,7 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     const int G = std::max(1, std::min(ctx->sm_count, N));
     PartInfo part;
     if (A.slots * 20LL > (long long)G * (150 << 10)) return RAFEM_ERR_UNSUPPORTED;
-    if (int rc = partition(ctx, A, G, true, part)) return rc;
+    if (int rc = partition(ctx, A, G, true, part, pipe_rows(false, 2, N, G))) return rc;
     cudaFuncAttributes fa;
     RF_CUDA_TRY(ctx, cudaFuncGetAttributes(&fa, fn));
     size_t smem = part.max_slice;
