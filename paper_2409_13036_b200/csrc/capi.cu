@@ -255,11 +255,12 @@ void rafem_ctx_destroy(rafem_ctx* ctx) {
                       &ctx->ws_cyc, &ctx->ws_part, &ctx->ws_res, &ctx->ws_trace, &ctx->ws_flags, &ctx->ws_simout,
                       &ctx->ws_diag})
         if (b->p) cudaFree(b->p);
+    for (auto& e : ctx->part_cache) dfree(ctx, e.gpart);
+    ctx->part_cache.clear();
     dcache_release(ctx);
     if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
     if (ctx->mapped) cudaFreeHost(ctx->mapped);
     if (ctx->pin) cudaFreeHost(ctx->pin);
-    for (auto& e : ctx->part_cache) cudaFree(e.gpart);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->ev2) cudaEventDestroy(ctx->ev2);
@@ -480,6 +481,14 @@ int rafem_mesh_create(rafem_ctx* ctx, int64_t n_nodes, const double* nodes, int6
 
 void rafem_mesh_destroy(rafem_mesh* m) {
     if (!m) return;
+    auto& pc = m->ctx->part_cache;  // partitions cached for this mesh's pattern
+    for (size_t i = 0; i < pc.size();)
+        if (pc[i].pattern_id == m->id) {
+            dfree(m->ctx, pc[i].gpart);
+            pc.erase(pc.begin() + i);
+        } else {
+            ++i;
+        }
     for (void* p : {(void*)m->nodes, (void*)m->tets, (void*)m->region, (void*)m->regtab, (void*)m->kind,
                     (void*)m->rp, (void*)m->col, (void*)m->diag, (void*)m->inc_ptr, (void*)m->inc_ea,
                     (void*)m->inc_slot, (void*)m->base, (void*)m->grad, (void*)m->vol, (void*)m->slot_ptr,

@@ -2152,7 +2152,7 @@ static int partition(rafem_ctx* ctx, const MatView& A, int G, bool need_slice, P
     }
     int* gpart = nullptr;
     if (A.pattern_id) {
-        RF_CUDA_TRY(ctx, cudaMalloc(&gpart, sizeof(int) * (G + 1)));
+        RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&gpart, sizeof(int) * (G + 1)));
     } else {
         if (int rc = ensure(ctx, ctx->ws_part, sizeof(int) * (size_t)(G + 1))) return rc;
         gpart = static_cast<int*>(ctx->ws_part.p);
