@@ -356,7 +356,8 @@ def run_ours(args):
                 "share_of_step": (launch_ms * launches / total_ms) if world == 1 else None,
                 "peak_source": peak_src,
                 "note": "paper-scale mesh: the working set (~5 MB) lives in L2 and shared memory, so the "
-                        "kernel is bound by grid-barrier + L2 round-trip latency (~4.8 us per PCG iteration), "
+                        "kernel is bound by grid-barrier + L2 round-trip latency "
+                        f"({1e3 * solve_ms / max(iters, 1):.2f} us of solve per PCG iteration, heads included), "
                         "not HBM; the HBM-bound kernels are reported in spmv_c3 and sharded_c4"}
 
     line = {
