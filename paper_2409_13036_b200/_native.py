@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librafem_b200.so")
+LIB_PATH = os.environ.get("RAFEM_LIB") or os.path.join(HERE, "librafem_b200.so")  # RAFEM_LIB: A/B builds
 
 OK = 0
 ERR_BREAKDOWN = 1

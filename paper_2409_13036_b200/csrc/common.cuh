@@ -69,6 +69,19 @@ RF_DEV double block_max(double v, double* red) {
     return warp_max(s);
 }
 
+// ---- per-thread asynchronous global -> shared copies (cp.async) ----------
+RF_DEV void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+RF_DEV void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+RF_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // ---- TMA 1-D bulk copies (cp.async.bulk) completing on an mbarrier -------
 RF_DEV unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 RF_DEV void mbar_init(unsigned long long* bar, unsigned count) {

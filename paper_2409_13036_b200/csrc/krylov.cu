@@ -2481,13 +2481,16 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     const int nt = 256;
     if (!mesh->slot_lists_tried)
         if (int rc = mesh_slot_lists(mesh)) return rc;
-    const void* fn = pre ? (const void*)simulate_kernel<true, 256> : (const void*)simulate_kernel<false, 256>;
+    const void* fn = pre ? (const void*)simulate_kernel<true, 256, false> : (const void*)simulate_kernel<false, 256, false>;
+    const void* fn_lean = pre ? (const void*)simulate_kernel<true, 256, true> : (const void*)simulate_kernel<false, 256, true>;
+    const bool pipe = pipe_rows(false, 2, N, std::max(1, std::min(ctx->sm_count, N)));
     const int G = std::max(1, std::min(ctx->sm_count, N));
     PartInfo part;
     if (A.slots * 20LL > (long long)G * (150 << 10)) return RAFEM_ERR_UNSUPPORTED;
     if (int rc = partition(ctx, A, G, true, part, pipe_rows(false, 2, N, G))) return rc;
-    cudaFuncAttributes fa;
+    cudaFuncAttributes fa, fa_lean;
     RF_CUDA_TRY(ctx, cudaFuncGetAttributes(&fa, fn));
+    RF_CUDA_TRY(ctx, cudaFuncGetAttributes(&fa_lean, fn_lean));
     size_t smem = part.max_slice;
     if (smem + fa.sharedSizeBytes > 227 * 1024) return RAFEM_ERR_UNSUPPORTED;
     // room to stage each CTA's assembly index data (simulate_dev.cuh)
@@ -2499,7 +2502,7 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
         RF_CUDA_TRY(ctx, cudaMemcpy(hip.data(), mesh->inc_ptr, sizeof(int) * (N + 1), cudaMemcpyDeviceToHost));
         std::vector<int> hsp(mesh->slots + 1);
         RF_CUDA_TRY(ctx, cudaMemcpy(hsp.data(), mesh->slot_ptr, sizeof(int) * (mesh->slots + 1), cudaMemcpyDeviceToHost));
-        size_t need = 0;
+        size_t need = 0, need2 = 0;
         for (int c = 0; c < G; ++c) {
             const size_t nr = (size_t)(hg[c + 1] - hg[c]);
             const size_t ns = (size_t)(hrp[hg[c + 1]] - hrp[hg[c]]);
@@ -2508,9 +2511,22 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
             const size_t slice = ns * 16 + ((ns + 3) & ~(size_t)3) * 4 + (nr + 1) * 4;
             const size_t extra = (ns + 1) * 4 + nsrc * 4 + (nr + 1) * 4 + ninc * 4 + nr * 4 + ns + 2 * nr + 8 + 8 * nr;
             need = std::max(need, slice + extra);
+            // + the pass's contributions and loads, copied in by cp.async
+            need2 = std::max(need2, slice + extra + 16 + nsrc * 16 + ninc * 8);
         }
         need = (need + 15) / 16 * 16;
-        if (need + fa.sharedSizeBytes <= 227 * 1024) {
+        need2 = (need2 + 15) / 16 * 16;
+        const char* nsc = getenv("RAFEM_NO_STAGE_CONTRIB");
+        const char* nl = getenv("RAFEM_NO_LEAN_SIM");
+        if (pipe && need2 + fa_lean.sharedSizeBytes <= 227 * 1024 && !(nsc && nsc[0] == '1') &&
+            !(nl && nl[0] == '1')) {
+            smem = std::max(smem, need2);
+            stage_fill = 2;
+            fn = fn_lean;  // pipelined PCG + cp.async fill, nothing else compiled in
+        } else if (need2 + fa.sharedSizeBytes <= 227 * 1024 && !(nsc && nsc[0] == '1')) {
+            smem = std::max(smem, need2);
+            stage_fill = 2;
+        } else if (need + fa.sharedSizeBytes <= 227 * 1024) {
             smem = std::max(smem, need);
             stage_fill = 1;
         }
@@ -2566,8 +2582,7 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
         ctx->last_team = team;
     }
     {
-        const char* pe = getenv("RAFEM_PIPE");
-        a.pipe = ((N + G - 1) / G <= kPipeRows && !(pe && pe[0] == '0')) ? 1 : 0;
+        a.pipe = pipe ? 1 : 0;
         a.block = (a.pipe && p->solver.precondition == RAFEM_PRECOND_BLOCK_JACOBI && mesh->maxdeg <= 32) ? 1 : 0;
     }
     S.m = asm_mesh(mesh);

@@ -71,12 +71,63 @@ RF_DEV long long global_ns() {
     return t;
 }
 
-template <bool PRE, int NT>
+// Fill phase with stage_fill == 2: every contribution and load of the CTA's
+// rows copied into shared memory by cp.async (no registers held across the
+// round trip: one round trip for the whole fill), then the same left-to-
+// right sums per slot and per row from shared memory (bit-identical to the
+// register-chunked fill).  Out of line: a once-per-pass phase that should
+// not share a register allocation with the PCG loop.
+__device__ __noinline__ void fill_staged_cp(int nsrc, int ninc, int ns, int nr, int g0, double2* cst, double* lst,
+                                            const int* ssrc, const unsigned* iea, const int* sptr, const int* iptr,
+                                            double2* sv2, double* srt, const int* sdg, const int* srp,
+                                            const double2* contrib, const double* load, double* diag_raw,
+                                            double* dv) {
+    const int tid = threadIdx.x;
+    for (int k = tid; k < nsrc; k += blockDim.x) cp_async16(cst + k, contrib + ssrc[k]);
+    for (int k = tid; k < ninc; k += blockDim.x) {
+        const unsigned ea = iea[k];
+        cp_async8(lst + k, load + 4LL * (ea & 0x3fffffffu) + (ea >> 30));
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    for (int sl = tid; sl < ns; sl += blockDim.x) {
+        double av = 0.0, at = 0.0;
+        for (int k = sptr[sl], k1 = sptr[sl + 1]; k < k1; ++k) {
+            const double2 c = cst[k];
+            av = add(av, c.x);
+            at = add(at, c.y);
+        }
+        sv2[sl] = make_double2(av, at);
+    }
+    for (int r = tid; r < nr; r += blockDim.x) {
+        double racc = 0.0;
+        for (int k = iptr[r], k1 = iptr[r + 1]; k < k1; ++k) racc = add(racc, lst[k]);
+        srt[r] = racc;
+    }
+    __syncthreads();
+    double d0 = dv[0], d1 = dv[1];
+    for (int r = tid; r < nr; r += blockDim.x) {
+        const long long i = g0 + r;
+        const double2 dvv = sdg[r] >= 0 ? sv2[srp[r] + sdg[r]] : make_double2(0.0, 0.0);
+        diag_raw[2 * i] = dvv.x;
+        diag_raw[2 * i + 1] = dvv.y;
+        d0 = add(d0, dvv.x);
+        d1 = add(d1, dvv.y);
+    }
+    dv[0] = d0;
+    dv[1] = d1;
+}
+
+// LEAN: the paper-scale instantiation (pipelined PCG, cp.async-staged fill)
+// with every other path compiled out: a smaller kernel whose PCG loop does
+// not share instruction-cache space and register allocation with code it
+// never runs (the generic instantiation picks its paths at run time).
+template <bool PRE, int NT, bool LEAN>
 __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
     extern __shared__ __align__(16) double sval[];
     __shared__ double red[32 * 8];
     __shared__ double co[8];
-    __shared__ FillScratch ws[NT / 32];
+    __shared__ FillScratch ws[LEAN ? 1 : NT / 32];
     __shared__ int zflag;
     const KArgs& a = S.k;
     const rafem_sim_params& p = S.p;
@@ -105,7 +156,9 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
     unsigned* iea = nullptr;
     uint8_t *ckd = nullptr, *rkd = nullptr;
     double* srt = nullptr;  // T rhs of the own rows between the fill and the constraints
-    if (S.stage_fill) {
+    double2* cst = nullptr;  // stage_fill 2: the pass's slot contributions, list order
+    double* lst = nullptr;   //               and the rows' element loads, incidence order
+    if (LEAN || S.stage_fill) {
         const int sp0 = __ldg(S.m.slot_ptr + s0), ip0 = __ldg(S.m.inc_ptr + g0);
         nsrc = __ldg(S.m.slot_ptr + s0 + ns) - sp0;
         ninc = __ldg(S.m.inc_ptr + g1) - ip0;
@@ -116,6 +169,10 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
         ckd = reinterpret_cast<uint8_t*>(sdg + nr);
         rkd = ckd + ns;
         srt = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(rkd + 2 * nr) + 7) & ~uintptr_t(7));
+        if (LEAN || S.stage_fill == 2) {
+            cst = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(srt + nr) + 15) & ~uintptr_t(15));
+            lst = reinterpret_cast<double*>(cst + nsrc);
+        }
         for (int k = tid; k <= ns; k += blockDim.x) sptr[k] = __ldg(S.m.slot_ptr + s0 + k) - sp0;
         for (int k = tid; k < nsrc; k += blockDim.x) ssrc[k] = __ldg(S.m.slot_src + sp0 + k);
         for (int r = tid; r <= nr; r += blockDim.x) iptr[r] = __ldg(S.m.inc_ptr + g0 + r) - ip0;
@@ -204,7 +261,11 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
             // diagonal sums and the PhysicsRange count in ONE reduction; the
             // offending element is located only on the (aborting) bad path
             double dv[3] = {0.0, 0.0, badv > 0.0 ? 1.0 : 0.0};
-            if (S.stage_fill) {
+            if (LEAN || S.stage_fill == 2) {
+                fill_staged_cp(nsrc, ninc, ns, nr, g0, cst, lst, ssrc, iea, sptr, iptr, sv2, srt, sdg, srp, S.contrib,
+                               S.load, S.diag_raw, dv);
+            } else if (LEAN) {
+            } else if (S.stage_fill) {
                 // thread per slot over its staged contributor list (every gather of
                 // a chunk in flight), then thread per row for the T rhs and diagonal
                 for (int sl = tid; sl < ns; sl += blockDim.x) {
@@ -260,7 +321,7 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
                     fill_node_warp(i, S.m, S.contrib, S.load, sv2 + srp[i - g0], S.rhs, S.diag_raw, ws[warp]);
             }
             __syncthreads();
-            if (!S.stage_fill)
+            if (!LEAN && !S.stage_fill)
                 for (int i = g0 + tid; i < g1; i += blockDim.x) {
                     dv[0] = add(dv[0], S.diag_raw[2LL * i]);
                     dv[1] = add(dv[1], S.diag_raw[2LL * i + 1]);
@@ -282,7 +343,7 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
             // loads issued ahead of the constraint loop)
             const int ec = lo + tid;
             const double xc = ec < hi ? X(iit)[ec] : 0.0;
-            if (S.stage_fill)
+            if (LEAN || S.stage_fill)
                 for (int r = tid; r < nr; r += blockDim.x)
                     constrain_node_thread(g0 + r, scale, p.applied_voltage, p.boundary_temp, sv2 + srp[r], S.rhs,
                                           PRE ? const_cast<double*>(a.minv) : nullptr, &zflag, scol + srp[r],
@@ -299,7 +360,7 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
             __syncthreads();
             PcgOut o{0, 0.0, 1, RAFEM_OK};
             long long tb;
-            if (a.pipe) {
+            if (LEAN || a.pipe) {
                 // ||b|| and the zero-diagonal flag ride on the PCG head's reduction
                 tb = global_ns();
                 SIM_STAMP(4, tb);
