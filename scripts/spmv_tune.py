@@ -30,7 +30,9 @@ ms = C.c_double()
 nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 30, int(os.environ.get("FLUSH", "1")), C.byref(ms)), "bench")
 print(f"thread-per-row      {1e3*ms.value:8.2f} us  {B/ms.value/1e6:8.1f} GB/s")
 del os.environ["RAFEM_NO_TMA_SPMV"]
-for cfg in ["legacy", "256,2,1", "256,2,1/nocls", "256,3,1", "384,2,1", "512,2,1", "192,3,1"]:
+cfgs = os.environ.get("CFGS", "legacy 256,2,1 256,2,1/nocls 256,3,1 384,2,1 512,2,1 192,3,1 "
+                      "128,3,1,2 96,4,1,2 128,2,1,3 64,4,1,3 192,2,1,2 128,4,1 128,2,1,2").split()
+for cfg in cfgs:
     os.environ["RAFEM_NO_CLASSES"] = "1" if cfg.endswith("/nocls") else "0"
     cfg = cfg.split("/")[0]
     if cfg == "legacy":
