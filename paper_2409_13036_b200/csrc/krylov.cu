@@ -83,6 +83,7 @@ struct KArgs {
     unsigned epoch;             // per-launch flag epoch (never 0)
     int pipe;                   // PCG: pipelined recurrence (pcg_pipe_core), W == 2 only
     int block;                  // pipelined PCG: block-Jacobi (Neumann step) on the CTA's diagonal block
+    unsigned long long* gbar;   // grid-barrier arrival counter (zeroed before each launch); null: cg grid sync
     long long vs_off;           // GMRES: own rows of the basis in dynamic smem at this double offset (0: global)
     int vs_ld;                  // its row stride (own dofs of the widest CTA)
 };
@@ -426,10 +427,47 @@ RF_DEV unsigned long long ld_relaxed(const unsigned long long* p) {
 }
 constexpr long long kSpinCap = 1LL << 31;
 
+// Grid barrier on a monotonically increasing arrival counter: after the
+// CTA's bar.sync one thread adds 1 with release semantics and spins with
+// acquire loads until all G CTAs of this round have arrived (target =
+// rounds * G).  Release after bar.sync is cumulative over the CTA's
+// writes, and the acquire (which invalidates the SM's L1) before the
+// closing bar.sync orders every thread's later loads after them.  Measured
+// on B200 with 128 doubles written per CTA before each barrier
+// (scripts/microbench_bar.cu): 1.70 us per round vs 2.54 us for
+// cooperative_groups' grid sync (see grid_counter for the in-kernel result).
+RF_DEV void grid_barrier(unsigned long long* ctr, unsigned long long target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
+        long long spins = 0;
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+            if (++spins > kSpinCap) asm volatile("trap;");
+        } while (v < target);
+    }
+    __syncthreads();
+}
+
 template <class Mode>
 struct Sync {
     const KArgs& a;
     unsigned round = 0;
+    unsigned long long nbar = 0;  // grid barriers passed (counter-barrier target)
+
+    RF_DEV void grid_sync() {
+        if constexpr (Mode::kCluster) {
+            Mode::sync();
+        } else {
+            if (a.gbar) {
+                ++nbar;
+                grid_barrier(a.gbar, nbar * gridDim.x);
+            } else {
+                Mode::sync();
+            }
+        }
+    }
 
     RF_DEV unsigned flag() const { return (a.epoch << 16) | (round & 0xffffu); }
     RF_DEV unsigned long long* slot(int cta) const {
@@ -442,7 +480,7 @@ struct Sync {
         const int G = gridDim.x;
         if constexpr (Mode::kCluster || !Mode::kFlags) {
             publish<NV>(v, nv, P, 0, G, red);
-            Mode::sync();
+            grid_sync();
             gather(P, nv, G, co);
             return;
         } else {
@@ -502,7 +540,7 @@ struct Sync {
     // Barrier only (vector visibility).
     RF_DEV void barrier() {
         if constexpr (Mode::kCluster || !Mode::kFlags) {
-            Mode::sync();
+            grid_sync();
         } else {
             __syncthreads();
             const unsigned f = flag();
@@ -1089,32 +1127,52 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
     const double omega = blk ? s_omega : 0.0;
     // dst (owner dofs, smem) = M^-1 src; also to dst_g when given.  y = D^-1 src
     // is expected in yl already when y_ready (the caller fused it).
-    auto apply_block = [&](const double* src, double* dst, double* dst_g, bool y_ready) {
-        if (!y_ready)
-            for (int e = lo + tid; e < hi; e += blockDim.x) yl[e] = mul(mvs[e], src[e]);
-        __syncthreads();
-        for (int rr = tid; rr < nr; rr += blockDim.x) {  // thread per row over its in-block slots
-            const int g = g0 + rr, sb = rows.start(g);
-            unsigned mask = s_inmask[rr];
+    // The block step's rows run on the threads below `nthr` (whole warps), a
+    // team of bt lanes per row: lane l takes the in-block slots l, l + bt, ...
+    // of its row in stored order and the team combines them with a fixed
+    // xor-butterfly, so the result is deterministic (bt == 1 is the plain
+    // left-to-right row sum).
+    auto block_rows = [&](const double* src, double* dst, double* dst_g, int nthr) {
+        int bt = 1;
+        while (bt < 8 && ((nr * bt * 2 + 31) & ~31) <= nthr) bt *= 2;
+        if (tid < ((nr * bt + 31) & ~31)) {
+            const int rr = tid / bt, l = tid & (bt - 1);
             double av = 0.0, at = 0.0;
-            while (mask) {
-                const int l = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const int c = rows.column(sb + l);
-                const double2 v = rows.value2(sb + l);
-                av = add(av, mul(v.x, yl[2 * c]));
-                at = add(at, mul(v.y, yl[2 * c + 1]));
+            if (rr < nr) {
+                const int sb = rows.start(g0 + rr);
+                const unsigned pat = bt == 1 ? 0xffffffffu : bt == 2 ? 0x55555555u : bt == 4 ? 0x11111111u : 0x01010101u;
+                unsigned mask = s_inmask[rr] & (pat << l);
+                while (mask) {
+                    const int k = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    const int c = rows.column(sb + k);
+                    const double2 v = rows.value2(sb + k);
+                    av = add(av, mul(v.x, yl[2 * c]));
+                    at = add(at, mul(v.y, yl[2 * c + 1]));
+                }
             }
-            const int e0 = 2 * g;
-            const double d0 = add(yl[e0], mul(omega, mul(mvs[e0], sub(src[e0], av))));
-            const double d1 = add(yl[e0 + 1], mul(omega, mul(mvs[e0 + 1], sub(src[e0 + 1], at))));
-            dst[e0] = d0;
-            dst[e0 + 1] = d1;
-            if (dst_g) {
-                dst_g[e0] = d0;
-                dst_g[e0 + 1] = d1;
+            for (int o = bt >> 1; o > 0; o >>= 1) {
+                av = add(av, __shfl_xor_sync(0xffffffffu, av, o));
+                at = add(at, __shfl_xor_sync(0xffffffffu, at, o));
+            }
+            if (rr < nr && l == 0) {
+                const int e0 = 2 * (g0 + rr);
+                const double d0 = add(yl[e0], mul(omega, mul(mvs[e0], sub(src[e0], av))));
+                const double d1 = add(yl[e0 + 1], mul(omega, mul(mvs[e0 + 1], sub(src[e0 + 1], at))));
+                dst[e0] = d0;
+                dst[e0 + 1] = d1;
+                if (dst_g) {
+                    dst_g[e0] = d0;
+                    dst_g[e0 + 1] = d1;
+                }
             }
         }
+    };
+    // dst (owner dofs, smem) = M^-1 src; also to dst_g when given.
+    auto apply_block = [&](const double* src, double* dst, double* dst_g) {
+        for (int e = lo + tid; e < hi; e += blockDim.x) yl[e] = mul(mvs[e], src[e]);
+        __syncthreads();
+        block_rows(src, dst, dst_g, blockDim.x);
         __syncthreads();
     };
 
@@ -1165,7 +1223,7 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
             });
             if (blk) {
                 __syncthreads();
-                apply_block(r, u, ug, false);
+                apply_block(r, u, ug);
             }
             if (with_b && zflag && tid == 0) v[1] = (double)*zflag;
             for (int e = lo + tid; e < hi; e += blockDim.x) xs[e] = x[e];  // owner copy (synced below)
@@ -1208,7 +1266,7 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
             });
             if (blk) {
                 __syncthreads();
-                apply_block(w, ms, m, false);
+                apply_block(w, ms, m);
             }
             publish3(v);
             sy.barrier();
@@ -1219,7 +1277,7 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
         // plus a square root) between the gathered scalars and the update.
         // The convergence test compares squared norms; the history keeps the
         // squared estimates and is rescaled once after the solve.
-        double gamma = 0.0, alpha = 0.0, ig = 0.0, igam = 0.0;
+        double alpha = 0.0, ig = 0.0, igam = 0.0;
         bool first = true;
         const long long hstart = hlen;
         const double thr = mul(mul(a.tol, bnorm), mul(a.tol, bnorm));
@@ -1229,6 +1287,7 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
             // up after their own share of the SpMV, so the fold's round trip
             // hides under the SpMV's (same order as reduce_partials_warp).
             constexpr int kFold = 5;  // partials per lane in flight: G <= 160
+            stamp(a, total, 0);
             const int gw = warp - (nwarps - 3);
             double pv[kFold];
             if (gw >= 0) {
@@ -1253,6 +1312,7 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                 if (lane == 0) co[gw] = sacc;
             }
             __syncthreads();
+            stamp(a, total, 1);
             par ^= 1;
             const double gn = co[0], dn = co[1];
             double beta = 0.0;
@@ -1276,9 +1336,6 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                 }
                 alpha = gn / den;
             }
-            gamma = gn;
-            igam = 1.0 / gn;
-            ig = 1.0 / (gn * alpha);
             double* mn = mb(cur ^ 1);
             double v[3] = {0.0, 0.0, 0.0};
             for (int e = lo + tid; e < hi; e += blockDim.x) {
@@ -1315,11 +1372,50 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                 v[1] = add(v[1], mul(wn, un));
                 v[2] = add(v[2], mul(rn, rn));
             }
-            if (blk) apply_block(w, ms, mn, true);  // (its leading barrier orders y)
+            // 1 / gn and 1 / (gn alpha) are first needed by the next iteration
+            igam = 1.0 / gn;
+            ig = 1.0 / (gn * alpha);
+            // the CTA's dot partials: groups of 4 lanes pre-combine theirs
+            // (owner dofs sit on threads < 2 * kPipeRows), the 64 group sums
+            // per value go through shared memory (`red`, 256 doubles, is not
+            // used inside the iteration), and the last three warps each fold
+            // one value while the other warps run the block step
+            double* tv = red;  // 3 x 64 doubles
+            if (tid < 2 * kPipeRows) {
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    v[j] = add(v[j], __shfl_xor_sync(0xffffffffu, v[j], 1));
+                    v[j] = add(v[j], __shfl_xor_sync(0xffffffffu, v[j], 2));
+                }
+                if ((lane & 3) == 0)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) tv[j * (kPipeRows / 2) + (tid >> 2)] = v[j];
+            }
+            for (int i = blockDim.x + tid; i < 2 * kPipeRows; i += blockDim.x)  // (narrow CTAs)
+                if ((i & 3) == 0)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) tv[j * (kPipeRows / 2) + (i >> 2)] = 0.0;
+            __syncthreads();  // y (block step) and the partials are complete
+            stamp(a, total, 2);
+            {
+                const int gw = warp - (nwarps - 3);
+                if (gw >= 0) {
+                    const double* t = tv + gw * (kPipeRows / 2) + lane * (kPipeRows / 64);
+                    double sacc = 0.0;
+#pragma unroll
+                    for (int k = 0; k < kPipeRows / 64; ++k) sacc = add(sacc, t[k]);
+                    sacc = warp_sum(sacc);
+                    if (lane == 0) a.partial[par * pstride + (long long)gw * G + cta] = sacc;
+                } else if (blk) {
+                    block_rows(w, ms, mn, (nwarps - 3) * 32);
+                }
+            }
+            stamp(a, total, 3);
             cur ^= 1;
             first = false;
-            publish3(v);
+            stamp(a, total, 4);
             sy.barrier();
+            stamp(a, total, 5);
         }
         if (cta == 0 && tid == 0 && cycles < a.cyc_cap) a.cyc[cycles] = hlen - hstart;
         if (cta == 0) {  // squared estimates of this cycle -> relative residuals
@@ -1878,7 +1974,7 @@ __global__ void __launch_bounds__(NT, 1) spmv_tma_pipe_kernel(MatView A, const d
                                                               double* __restrict__ y, int valcap, int bufbytes) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) unsigned long long bar[ST];
-    __shared__ int soff[CLS ? kMaxClasses * kClsWidth : 1];
+    int* soff = reinterpret_cast<int*>(sm + (size_t)ST * bufbytes);  // CLS: the class table after the stages
     const int N = A.ngroups;
     const int tiles = (N + NT - 1) / NT;
     const int mine = tiles > (int)blockIdx.x ? (tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
@@ -1976,6 +2072,16 @@ __global__ void delta_kernel(const double* xn, const double* xo, int n, unsigned
 // ---------------------------------------------------------------------------
 // host launchers
 
+// The grid-barrier counter lives after the 2 x G x 8 barrier slots of
+// ws_flags.  Opt-in (RAFEM_CNT_SYNC=1): in the microbenchmark it beats
+// cooperative_groups' grid sync by 0.8 us per round when every CTA has
+// just written global data, but inside the fused simulation it measured
+// 4.71 vs 4.60 us per PCG iteration (r1j), so the default stays cg.
+static unsigned long long* grid_counter(rafem_ctx*, unsigned long long* flags, int G) {
+    const char* e = getenv("RAFEM_CNT_SYNC");
+    return !(e && e[0] == '1') ? nullptr : flags + 2 * 8 * (size_t)std::max(G, 1);
+}
+
 int jacobi_minv(rafem_ctx* ctx, const MatView& A, double* minv_dev, int* flag_dev) {
     RF_CUDA_TRY(ctx, cudaMemsetAsync(flag_dev, 0, sizeof(int), ctx->stream));
     const int blocks = (A.ngroups + 255) / 256;
@@ -1992,7 +2098,8 @@ int jacobi_minv(rafem_ctx* ctx, const MatView& A, double* minv_dev, int* flag_de
 
 // Pipelined TMA SpMV launch; RAFEM_ERR_UNSUPPORTED when no configuration
 // fits the row degree (the caller then uses the two-stage kernel).
-// RAFEM_SPMV_CFG="NT,ST,HINT" selects a configuration (tuning only).
+// RAFEM_SPMV_CFG="NT,ST,HINT[,CPS]" selects a configuration and CTAs per SM
+// (tuning only).
 struct PipeCfg {
     int nt, st, hint;
     const void* fn;
@@ -2005,26 +2112,38 @@ static PipeCfg pipe_cfg() {
 }
 static int spmv_pipe_launch(rafem_ctx* ctx, const MatView& A, const double* x_dev, double* y_dev) {
     static const PipeCfg cfgs[] = {pipe_cfg<256, 2, 1>(), pipe_cfg<128, 4, 1>(), pipe_cfg<192, 3, 1>(),
-                                   pipe_cfg<256, 3, 1>(), pipe_cfg<384, 2, 1>(), pipe_cfg<512, 2, 1>()};
+                                   pipe_cfg<256, 3, 1>(), pipe_cfg<384, 2, 1>(), pipe_cfg<512, 2, 1>(),
+                                   pipe_cfg<128, 3, 1>(), pipe_cfg<96, 4, 1>(),  pipe_cfg<128, 2, 1>(),
+                                   pipe_cfg<64, 4, 1>(),  pipe_cfg<192, 2, 1>()};
+    int cps = 1;  // CTAs per SM
     const char* nc = getenv("RAFEM_NO_CLASSES");
     const bool cls = A.cls && A.ncls > 0 && A.maxdeg <= kClsWidth && !(nc && nc[0] == '1');
     auto buf_bytes = [&](int t) {
         return t * A.maxdeg * 16 + (cls ? 0 : ((t * A.maxdeg + 8) * 4 + 15) / 16 * 16);
     };
-    const size_t budget = kSmemBudget - (cls ? sizeof(int) * kMaxClasses * kClsWidth : 0);
+    const size_t tab = cls ? sizeof(int) * (size_t)A.ncls * kClsWidth : 0;
+    const size_t budget = kSmemBudget - tab;
     // default: the widest configuration whose stages fit (measured on B200,
     // cold L2: 384 x 2 with stencil classes 411 us at 16M dofs, 256 x 2 521 us)
+    // (measured r1j, cold L2: two CTAs per SM of 192 x 2 405 us at 16M dofs,
+    // 36.9 us at 1M; one CTA of 384 x 2 416 / 37.6 us)
+    auto fits = [&](int i, int k) {
+        const size_t sm = (size_t)cfgs[i].st * buf_bytes(cfgs[i].nt);
+        return sm <= budget && (size_t)k * (sm + tab + 1024) <= 228 * 1024;
+    };
     int want = -1;
-    for (int i : {4, 0, 1}) {
-        if ((size_t)cfgs[i].st * buf_bytes(cfgs[i].nt) <= budget) {
+    for (auto [i, k] : {std::pair{10, 2}, std::pair{4, 1}, std::pair{0, 1}, std::pair{1, 1}}) {
+        if (fits(i, k)) {
             want = i;
+            cps = k;
             break;
         }
     }
     if (want < 0) return RAFEM_ERR_UNSUPPORTED;
     if (const char* env = getenv("RAFEM_SPMV_CFG")) {
-        int nt = 0, st = 0, hint = 1;
-        if (sscanf(env, "%d,%d,%d", &nt, &st, &hint) >= 2) {
+        int nt = 0, st = 0, hint = 1, ec = 1;
+        if (sscanf(env, "%d,%d,%d,%d", &nt, &st, &hint, &ec) >= 2) {
+            cps = std::max(1, ec);
             want = -1;
             for (int i = 0; i < (int)(sizeof(cfgs) / sizeof(cfgs[0])); ++i)
                 if (cfgs[i].nt == nt && cfgs[i].st == st && cfgs[i].hint == hint) want = i;
@@ -2033,11 +2152,12 @@ static int spmv_pipe_launch(rafem_ctx* ctx, const MatView& A, const double* x_de
     }
     const PipeCfg& c = cfgs[want];
     const void* fn = cls ? c.fn_cls : c.fn;
-    const size_t smem = (size_t)c.st * buf_bytes(c.nt);
-    if (smem > budget) return RAFEM_ERR_UNSUPPORTED;
+    const size_t smem = (size_t)c.st * buf_bytes(c.nt) + tab;
+    if (smem > kSmemBudget) return RAFEM_ERR_UNSUPPORTED;
     RF_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int tiles = (A.ngroups + c.nt - 1) / c.nt;
-    const int grid = std::min(tiles, ctx->sm_count);
+    if ((size_t)cps * (smem + 1024) > 228 * 1024) return RAFEM_ERR_UNSUPPORTED;
+    const int grid = std::min(tiles, ctx->sm_count * cps);
     int valcap = c.nt * A.maxdeg, bufbytes = buf_bytes(c.nt);
     MatView Av = A;
     const double* xp = x_dev;
@@ -2366,7 +2486,7 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     a.res = res_dev;
     a.flag = flag_dev;
     {  // barrier / all-reduce slots: zeroed once, distinguished per launch by the epoch
-        const size_t fb = sizeof(unsigned long long) * 2 * 8 * (size_t)std::max(G, 1);
+        const size_t fb = sizeof(unsigned long long) * (2 * 8 * (size_t)std::max(G, 1) + 8);
         if (ctx->ws_flags.bytes < fb) {
             if (int rc = ensure(ctx, ctx->ws_flags, fb)) return rc;
             RF_CUDA_TRY(ctx, cudaMemsetAsync(ctx->ws_flags.p, 0, ctx->ws_flags.bytes, ctx->stream));
@@ -2374,6 +2494,8 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
         ctx->epoch = ctx->epoch % 0xffffu + 1;
         a.flags = static_cast<unsigned long long*>(ctx->ws_flags.p);
         a.epoch = ctx->epoch;
+        a.gbar = grid_counter(ctx, a.flags, G);
+        if (a.gbar) RF_CUDA_TRY(ctx, cudaMemsetAsync(a.gbar, 0, sizeof(unsigned long long), ctx->stream));
     }
     if (ctx->trace_on) {
         if (int rc = ensure(ctx, ctx->ws_trace, sizeof(long long) * 8 * 4096)) return rc;
@@ -2542,7 +2664,7 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     if (int rc = ensure(ctx, ctx->ws_partial, sizeof(double) * (size_t)2 * 8 * G)) return rc;
     if (int rc = ensure(ctx, ctx->ws_simout, sizeof(SimDevOut))) return rc;
     {
-        const size_t fb = sizeof(unsigned long long) * 2 * 8 * (size_t)G;
+        const size_t fb = sizeof(unsigned long long) * (2 * 8 * (size_t)G + 8);
         if (ctx->ws_flags.bytes < fb) {
             if (int rc = ensure(ctx, ctx->ws_flags, fb)) return rc;
             RF_CUDA_TRY(ctx, cudaMemsetAsync(ctx->ws_flags.p, 0, ctx->ws_flags.bytes, ctx->stream));
@@ -2572,6 +2694,8 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     a.cap = p->solver.max_total_iters > 0 ? p->solver.max_total_iters : 10LL * n2;
     a.flags = static_cast<unsigned long long*>(ctx->ws_flags.p);
     a.epoch = ctx->epoch;
+    a.gbar = grid_counter(ctx, a.flags, G);
+    if (a.gbar) RF_CUDA_TRY(ctx, cudaMemsetAsync(a.gbar, 0, sizeof(unsigned long long), ctx->stream));
     {
         const int rows_per_cta = (N + G - 1) / G;
         int team = 1;
