@@ -539,6 +539,34 @@ int mesh_slot_lists(rafem_mesh* m) {
     return RAFEM_OK;
 }
 
+__global__ void slot_pos_kernel(const int* slot_src, long long n, int* cpos) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        cpos[slot_src[k]] = (int)k;
+}
+__global__ void load_pos_kernel(const unsigned* inc_ea, long long n, int* lpos) {
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+        const unsigned ea = inc_ea[p];
+        lpos[4LL * (ea & 0x3fffffffu) + (ea >> 30)] = (int)p;
+    }
+}
+
+// Inverse maps of the contributor and incidence lists: where the element
+// phase of the fused simulation stores each contribution and load so that
+// every row block reads its own as one contiguous range.
+int mesh_slot_positions(rafem_mesh* m) {
+    rafem_ctx* ctx = m->ctx;
+    if (m->contrib_pos || !m->slot_src) return RAFEM_OK;
+    const long long M = m->M;
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&m->contrib_pos, sizeof(int) * 16 * (size_t)M));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&m->load_pos, sizeof(int) * 4 * (size_t)M));
+    const int blocks = (int)std::min<long long>((16 * M + 255) / 256, 4LL * ctx->sm_count * 8);
+    slot_pos_kernel<<<std::max(blocks, 1), 256, 0, ctx->stream>>>(m->slot_src, 16 * M, m->contrib_pos);
+    load_pos_kernel<<<std::max(blocks, 1), 256, 0, ctx->stream>>>(m->inc_ea, 4 * M, m->load_pos);
+    ctx->launches += 2;
+    RF_CUDA_TRY(ctx, cudaGetLastError());
+    return RAFEM_OK;
+}
+
 // Stencil classes.  A row's signature is its length and its column offsets
 // (col - row), sorted like the columns; rows with the same signature share
 // a class, and the SpMV kernels then compute columns instead of streaming
@@ -668,6 +696,8 @@ AsmMesh asm_mesh(const rafem_mesh* m) {
     a.kind = m->kind;
     a.slot_ptr = m->slot_ptr;
     a.slot_src = m->slot_src;
+    a.cpos = m->contrib_pos;
+    a.lpos = m->load_pos;
     a.N = m->N;
     a.M = m->M;
     return a;

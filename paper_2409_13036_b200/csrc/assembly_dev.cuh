@@ -34,6 +34,8 @@ struct AsmMesh {
     const uint8_t* kind;  // 2N dof kinds
     const int* slot_ptr;  // S + 1: per-slot contributor lists (null: warp fill)
     const int* slot_src;  // 16 M: contrib index 16 e + 4 a + b, ascending e per slot
+    const int* cpos;      // 16 M: slot-list position of contribution 16 e + 4 a + b (null: tet-major)
+    const int* lpos;      // 4 M: incidence-list position of load 4 e + a
     int N, M;
 };
 
@@ -120,6 +122,38 @@ RF_DEV bool element_tet(int e, const AsmMesh& m, const AsmFields& f, double2* co
 #pragma unroll
     for (int k = 0; k < 12; ++k) g12[k] = __ldg(m.grad + 12LL * e + k);
     return element_core(e, m, f, b10, g12, __ldg(m.vol + e), contrib + 16LL * e, load + 4LL * e);
+}
+
+// The same with the outputs scattered to their positions in the per-slot
+// contributor lists and per-node incidence lists (m.cpos, m.lpos), so a
+// row block's contributions and loads are contiguous, already in summation
+// order, for the fill that follows.
+RF_DEV bool element_tet_slot_major(int e, const AsmMesh& m, const AsmFields& f, double2* contrib, double* load) {
+    double b10[10], g12[12];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) b10[k] = __ldg(m.base + 10LL * e + k);
+#pragma unroll
+    for (int k = 0; k < 12; ++k) g12[k] = __ldg(m.grad + 12LL * e + k);
+    const int4* cp = reinterpret_cast<const int4*>(m.cpos + 16LL * e);
+    int4 q[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = __ldg(cp + k);
+    const int4 lp = __ldg(reinterpret_cast<const int4*>(m.lpos + 4LL * e));
+    double2 o16[16];
+    double o4[4];
+    const bool bad = element_core(e, m, f, b10, g12, __ldg(m.vol + e), o16, o4);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        contrib[q[k].x] = o16[4 * k];
+        contrib[q[k].y] = o16[4 * k + 1];
+        contrib[q[k].z] = o16[4 * k + 2];
+        contrib[q[k].w] = o16[4 * k + 3];
+    }
+    load[lp.x] = o4[0];
+    load[lp.y] = o4[1];
+    load[lp.z] = o4[2];
+    load[lp.w] = o4[3];
+    return bad;
 }
 
 // Per-warp staging for one node row's incident elements.

@@ -492,7 +492,8 @@ void rafem_mesh_destroy(rafem_mesh* m) {
     for (void* p : {(void*)m->nodes, (void*)m->tets, (void*)m->region, (void*)m->regtab, (void*)m->kind,
                     (void*)m->rp, (void*)m->col, (void*)m->diag, (void*)m->inc_ptr, (void*)m->inc_ea,
                     (void*)m->inc_slot, (void*)m->base, (void*)m->grad, (void*)m->vol, (void*)m->slot_ptr,
-                    (void*)m->slot_src, (void*)m->cls, (void*)m->cls_off})
+                    (void*)m->slot_src, (void*)m->cls, (void*)m->cls_off, (void*)m->contrib_pos,
+                    (void*)m->load_pos})
         if (p) dfree(m->ctx, p);
     delete m;
 }

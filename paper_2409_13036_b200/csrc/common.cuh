@@ -89,6 +89,7 @@ RF_DEV void mbar_init(unsigned long long* bar, unsigned count) {
 }
 RF_DEV void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 RF_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+RF_DEV void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
 RF_DEV void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }

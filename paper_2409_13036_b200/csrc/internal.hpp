@@ -151,6 +151,8 @@ struct rafem_mesh {
     int* slot_ptr = nullptr;  // slots + 1: per-slot contributor lists
     int* slot_src = nullptr;  // 16M: contribution index 16 e + 4 a + b (ascending e per slot)
     bool slot_lists_tried = false;
+    int* contrib_pos = nullptr;  // 16M: list position (slot_src order) of contribution 16 e + 4 a + b
+    int* load_pos = nullptr;     // 4M: list position (inc_ea order) of load 4 e + a
     uint8_t* cls = nullptr;   // N stencil class per node row (null: none)
     int* cls_off = nullptr;   // ncls x kClsWidth column offsets
     int ncls = 0;
@@ -214,6 +216,7 @@ int vec_delta_launch(rafem_ctx* ctx, const double* xn, const double* xo, int n, 
 int mesh_symbolic(rafem_mesh* m);
 int mesh_geometry(rafem_mesh* m);
 int mesh_slot_lists(rafem_mesh* m);  // per-slot contributor lists (built on first use)
+int mesh_slot_positions(rafem_mesh* m);  // their inverse maps (fused simulation, built on first use)
 // stencil classes of the node pattern (built on first use; none when the
 // rows have more than kMaxClasses distinct offset signatures)
 int mesh_stencil_classes(rafem_mesh* m);

@@ -1338,6 +1338,7 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
             }
             double* mn = mb(cur ^ 1);
             double v[3] = {0.0, 0.0, 0.0};
+            stamp(a, total, 6);
             for (int e = lo + tid; e < hi; e += blockDim.x) {
                 const double ne = (e & 1) ? ybuf[(e >> 1) - g0].y : ybuf[(e >> 1) - g0].x;
                 const double me = ms[e], we = w[e], ue = u[e];
@@ -1372,6 +1373,7 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                 v[1] = add(v[1], mul(wn, un));
                 v[2] = add(v[2], mul(rn, rn));
             }
+            stamp(a, total, 7);
             // 1 / gn and 1 / (gn alpha) are first needed by the next iteration
             igam = 1.0 / gn;
             ig = 1.0 / (gn * alpha);
@@ -2634,7 +2636,7 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
             const size_t extra = (ns + 1) * 4 + nsrc * 4 + (nr + 1) * 4 + ninc * 4 + nr * 4 + ns + 2 * nr + 8 + 8 * nr;
             need = std::max(need, slice + extra);
             // + the pass's contributions and loads, copied in by cp.async
-            need2 = std::max(need2, slice + extra + 16 + nsrc * 16 + ninc * 8);
+            need2 = std::max(need2, slice + extra + 32 + nsrc * 16 + ninc * 8);
         }
         need = (need + 15) / 16 * 16;
         need2 = (need2 + 15) / 16 * 16;
@@ -2709,7 +2711,16 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
         a.pipe = pipe ? 1 : 0;
         a.block = (a.pipe && p->solver.precondition == RAFEM_PRECOND_BLOCK_JACOBI && mesh->maxdeg <= 32) ? 1 : 0;
     }
+    // slot-major element outputs for the cp.async fill (RAFEM_NO_SLOT_MAJOR=1: tet-major)
+    const char* nsm = getenv("RAFEM_NO_SLOT_MAJOR");
+    const bool slot_major = stage_fill == 2 && !(nsm && nsm[0] == '1');
+    if (slot_major)
+        if (int rc = mesh_slot_positions(mesh)) return rc;
     S.m = asm_mesh(mesh);
+    if (!slot_major) {
+        S.m.cpos = nullptr;
+        S.m.lpos = nullptr;
+    }
     S.stage_fill = stage_fill;
     S.contrib = reinterpret_cast<double2*>(s->contrib);
     S.load = s->load;

@@ -81,28 +81,64 @@ __device__ __noinline__ void fill_staged_cp(int nsrc, int ninc, int ns, int nr, 
                                             const int* ssrc, const unsigned* iea, const int* sptr, const int* iptr,
                                             double2* sv2, double* srt, const int* sdg, const int* srp,
                                             const double2* contrib, const double* load, double* diag_raw,
-                                            double* dv) {
+                                            double* dv, int sp0, int ip0, unsigned long long* fbar,
+                                            unsigned fpar) {
     const int tid = threadIdx.x;
-    for (int k = tid; k < nsrc; k += blockDim.x) cp_async16(cst + k, contrib + ssrc[k]);
-    for (int k = tid; k < ninc; k += blockDim.x) {
-        const unsigned ea = iea[k];
-        cp_async8(lst + k, load + 4LL * (ea & 0x3fffffffu) + (ea >> 30));
+    if (sp0 >= 0) {
+        // slot-major element outputs: the block's contributions and loads are
+        // two contiguous ranges, streamed in by two TMA bulk copies (the loads
+        // from the 16-byte aligned element at or before ip0; an odd last
+        // element is read by thread 0)
+        const int a0 = ip0 & ~1, tot = (ip0 - a0) + ninc, nb = tot & ~1;
+        double* lraw = lst - (ip0 - a0);
+        if (tid == 0) {
+            fence_proxy_async_all();  // generic accesses (earlier sums, other CTAs' stores) before the async copies
+            const unsigned cb = 16u * (unsigned)nsrc, lb = 8u * (unsigned)nb;
+            mbar_expect_tx(fbar, cb + lb);
+            if (cb) tma_load_1d(cst, contrib + sp0, cb, fbar);
+            if (lb) tma_load_1d(lraw, load + a0, lb, fbar);
+            if (tot & 1) lraw[nb] = __ldcg(load + a0 + nb);
+        }
+        mbar_wait(fbar, fpar);
+    } else {
+        for (int k = tid; k < nsrc; k += blockDim.x) cp_async16(cst + k, contrib + ssrc[k]);
+        for (int k = tid; k < ninc; k += blockDim.x) {
+            const unsigned ea = iea[k];
+            cp_async8(lst + k, load + 4LL * (ea & 0x3fffffffu) + (ea >> 30));
+        }
     }
     cp_async_wait_all();
     __syncthreads();
-    for (int sl = tid; sl < ns; sl += blockDim.x) {
-        double av = 0.0, at = 0.0;
-        for (int k = sptr[sl], k1 = sptr[sl + 1]; k < k1; ++k) {
-            const double2 c = cst[k];
-            av = add(av, c.x);
-            at = add(at, c.y);
+    // slots and rows (T rhs) as one work list over the CTA; each sum runs
+    // left to right in list order, four loads in flight ahead of the adds
+    for (int w = tid; w < ns + nr; w += blockDim.x) {
+        if (w < ns) {
+            double av = 0.0, at = 0.0;
+            int k = sptr[w];
+            const int k1 = sptr[w + 1];
+            for (; k + 4 <= k1; k += 4) {
+                const double2 c0 = cst[k], c1 = cst[k + 1], c2 = cst[k + 2], c3 = cst[k + 3];
+                av = add(add(add(add(av, c0.x), c1.x), c2.x), c3.x);
+                at = add(add(add(add(at, c0.y), c1.y), c2.y), c3.y);
+            }
+            for (; k < k1; ++k) {
+                const double2 c = cst[k];
+                av = add(av, c.x);
+                at = add(at, c.y);
+            }
+            sv2[w] = make_double2(av, at);
+        } else {
+            const int r = w - ns;
+            double racc = 0.0;
+            int k = iptr[r];
+            const int k1 = iptr[r + 1];
+            for (; k + 4 <= k1; k += 4) {
+                const double l0 = lst[k], l1 = lst[k + 1], l2 = lst[k + 2], l3 = lst[k + 3];
+                racc = add(add(add(add(racc, l0), l1), l2), l3);
+            }
+            for (; k < k1; ++k) racc = add(racc, lst[k]);
+            srt[r] = racc;
         }
-        sv2[sl] = make_double2(av, at);
-    }
-    for (int r = tid; r < nr; r += blockDim.x) {
-        double racc = 0.0;
-        for (int k = iptr[r], k1 = iptr[r + 1]; k < k1; ++k) racc = add(racc, lst[k]);
-        srt[r] = racc;
     }
     __syncthreads();
     double d0 = dv[0], d1 = dv[1];
@@ -158,8 +194,16 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
     double* srt = nullptr;  // T rhs of the own rows between the fill and the constraints
     double2* cst = nullptr;  // stage_fill 2: the pass's slot contributions, list order
     double* lst = nullptr;   //               and the rows' element loads, incidence order
+    int sp0 = -1, ip0 = -1;  // slot-major contributions: the block's list offsets
+    __shared__ __align__(8) unsigned long long fbar;  // TMA fill copies
+    unsigned fpar = 0;
+    if (tid == 0) {
+        mbar_init(&fbar, 1);
+        mbar_fence_init();
+    }
     if (LEAN || S.stage_fill) {
-        const int sp0 = __ldg(S.m.slot_ptr + s0), ip0 = __ldg(S.m.inc_ptr + g0);
+        sp0 = __ldg(S.m.slot_ptr + s0);
+        ip0 = __ldg(S.m.inc_ptr + g0);
         nsrc = __ldg(S.m.slot_ptr + s0 + ns) - sp0;
         ninc = __ldg(S.m.inc_ptr + g1) - ip0;
         ssrc = sptr + ns + 1;
@@ -171,7 +215,7 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
         srt = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(rkd + 2 * nr) + 7) & ~uintptr_t(7));
         if (LEAN || S.stage_fill == 2) {
             cst = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(srt + nr) + 15) & ~uintptr_t(15));
-            lst = reinterpret_cast<double*>(cst + nsrc);
+            lst = reinterpret_cast<double*>(cst + nsrc) + (ip0 & 1);  // TMA: 16-byte aligned at element ip0 & ~1
         }
         for (int k = tid; k <= ns; k += blockDim.x) sptr[k] = __ldg(S.m.slot_ptr + s0 + k) - sp0;
         for (int k = tid; k < nsrc; k += blockDim.x) ssrc[k] = __ldg(S.m.slot_src + sp0 + k);
@@ -197,6 +241,7 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
     const long long pstride = 8LL * G;
     auto P = [&]() { return a.partial + par * pstride; };
     int iacc = 0, iprev = 1, iit = 2, inew = 3;
+    const bool smaj = S.m.cpos != nullptr && (LEAN || S.stage_fill == 2);
     auto X = [&](int i) { return S.xs + (long long)i * n2; };
 
     for (int e = lo + tid; e < hi; e += blockDim.x) {  // initial_state (fem.py:170-180)
@@ -253,8 +298,13 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
             // ---- element phase (own elements)
             const AsmFields f{X(iit) + 1, 2, X(iit), 2, X(iacc) + 1, 2, dt};
             double badv = 0.0;
-            for (int e = e0 + tid; e < e1; e += blockDim.x)
-                if (element_tet(e, S.m, f, S.contrib, S.load)) badv = fmax(badv, (double)(M - e));
+            if (smaj) {
+                for (int e = e0 + tid; e < e1; e += blockDim.x)
+                    if (element_tet_slot_major(e, S.m, f, S.contrib, S.load)) badv = fmax(badv, (double)(M - e));
+            } else {
+                for (int e = e0 + tid; e < e1; e += blockDim.x)
+                    if (element_tet(e, S.m, f, S.contrib, S.load)) badv = fmax(badv, (double)(M - e));
+            }
             sy.barrier();  // a row's fill gathers contributions of other CTAs' elements
             SIM_STAMP(2, global_ns());
             // ---- fill own rows into the shared-memory slice
@@ -263,7 +313,8 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
             double dv[3] = {0.0, 0.0, badv > 0.0 ? 1.0 : 0.0};
             if (LEAN || S.stage_fill == 2) {
                 fill_staged_cp(nsrc, ninc, ns, nr, g0, cst, lst, ssrc, iea, sptr, iptr, sv2, srt, sdg, srp, S.contrib,
-                               S.load, S.diag_raw, dv);
+                               S.load, S.diag_raw, dv, smaj ? sp0 : -1, ip0, &fbar, fpar);
+                if (smaj) fpar ^= 1u;
             } else if (LEAN) {
             } else if (S.stage_fill) {
                 // thread per slot over its staged contributor list (every gather of

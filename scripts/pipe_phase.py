@@ -26,5 +26,10 @@ for rep in range(3):
     tr = tr[ok]
     d = np.diff(tr[:, :6], axis=1).mean(axis=0) / 1.965e3
     per = np.diff(tr[:, 0]).mean() / 1.965e3
+    # slots 2-7 are stamped after the iteration counter moved on: align them
+    t1 = tr[:-1, 1]
+    nx = tr[1:]
+    sc = (nx[:, 6] - t1).mean() / 1.965e3, (nx[:, 7] - nx[:, 6]).mean() / 1.965e3, (nx[:, 2] - nx[:, 7]).mean() / 1.965e3
+    print(f"   update split: scalars {sc[0]:.2f} loop {sc[1]:.2f} divisions+partials+bar {sc[2]:.2f} us")
     print(f"{prec}: it={st.iterations} dev={st.device_ms*1e3:.0f}us ({st.device_ms*1e3/max(st.iterations,1):.2f} us/it) | "
           f"spmv+fold {d[0]:.2f} update {d[1]:.2f} block {d[2]:.2f} publish {d[3]:.2f} barrier {d[4]:.2f} | iter {per:.2f} us")
