@@ -280,7 +280,9 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
             S.ptrace[(passes - 1) * 8 + (k)] = (v);                                         \
     } while (0)
             SIM_STAMP(0, ta);
-            sy.barrier();  // the iterate is complete everywhere
+            // the predicted iterate is complete everywhere; a later pass's
+            // iterate was completed before the previous pass's delta reduction
+            if (it == 1) sy.barrier();
             SIM_STAMP(1, global_ns());
             if (S.ring && cta == 0 && tid == 0 && it == 1) {
                 __threadfence_system();
