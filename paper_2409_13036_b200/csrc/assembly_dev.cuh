@@ -127,8 +127,10 @@ RF_DEV bool element_tet(int e, const AsmMesh& m, const AsmFields& f, double2* co
 // The same with the outputs scattered to their positions in the per-slot
 // contributor lists and per-node incidence lists (m.cpos, m.lpos), so a
 // row block's contributions and loads are contiguous, already in summation
-// order, for the fill that follows.
-RF_DEV bool element_tet_slot_major(int e, const AsmMesh& m, const AsmFields& f, double2* contrib, double* load) {
+// order, for the fill that follows.  ds[0], ds[1] accumulate the element's
+// diagonal V and T contributions (the equilibration sums, fem.py:390-396).
+RF_DEV bool element_tet_slot_major(int e, const AsmMesh& m, const AsmFields& f, double2* contrib, double* load,
+                                   double* ds) {
     double b10[10], g12[12];
 #pragma unroll
     for (int k = 0; k < 10; ++k) b10[k] = __ldg(m.base + 10LL * e + k);
@@ -153,6 +155,11 @@ RF_DEV bool element_tet_slot_major(int e, const AsmMesh& m, const AsmFields& f, 
     load[lp.y] = o4[1];
     load[lp.z] = o4[2];
     load[lp.w] = o4[3];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        ds[0] = add(ds[0], o16[5 * a].x);
+        ds[1] = add(ds[1], o16[5 * a].y);
+    }
     return bad;
 }
 

@@ -5,13 +5,15 @@
 // (fem.py:463-540), assemble_global (fem.py:325-430) and the Krylov solve.
 // Every CTA owns a contiguous block of node rows (the solver partition) and
 // a contiguous block of elements.  Per corrector pass:
-//   barrier -> element phase (own elements: sigma, 16 (V,T) contributions,
-//   T loads) -> max-reduce PhysicsRange flag -> fill own rows straight into
-//   the CTA's shared-memory matrix slice (warp per row, ascending element
-//   order) -> sum-reduce diagonal sums -> equilibration scale + Dirichlet
-//   elimination + Jacobi inverse diagonal on own rows -> reduce ||b||^2 and
-//   the zero-diagonal flag -> single-reduction PCG on the smem slice ->
-//   max-reduce the corrector delta.
+//   barrier (first pass of a step) -> element phase (own elements: sigma,
+//   16 (V,T) contributions, T loads, scattered to their slot-list
+//   positions; diagonal sums) -> ONE reduction of the equilibration sums
+//   and the PhysicsRange flag -> the row block's contributions and loads
+//   by two TMA bulk copies, fill sums into the CTA's shared-memory matrix
+//   slice -> equilibration scale + Dirichlet elimination + Jacobi inverse
+//   diagonal on own rows -> pipelined PCG on the smem slice (||b||^2 and
+//   the zero-diagonal flag ride on its head reduction) -> max-reduce the
+//   corrector delta.
 // The time-step control (predictor, acceptance, dt growth / shrink /
 // halving, StepFailure) is scalar logic every CTA evaluates on identical,
 // deterministically reduced values, so all CTAs take the same branches and
@@ -301,13 +303,20 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
             const AsmFields f{X(iit) + 1, 2, X(iit), 2, X(iacc) + 1, 2, dt};
             double badv = 0.0;
             if (smaj) {
+                // the equilibration sums come from the elements' diagonal
+                // contributions and ride, with the PhysicsRange count, on the
+                // reduction that also orders the contributions before the fill
+                double ev[3] = {0.0, 0.0, 0.0};
                 for (int e = e0 + tid; e < e1; e += blockDim.x)
-                    if (element_tet_slot_major(e, S.m, f, S.contrib, S.load)) badv = fmax(badv, (double)(M - e));
+                    if (element_tet_slot_major(e, S.m, f, S.contrib, S.load, ev)) badv = fmax(badv, (double)(M - e));
+                ev[2] = badv > 0.0 ? 1.0 : 0.0;
+                sy.template reduce<3>(ev, 3, P(), co, red);
+                par ^= 1;
             } else {
                 for (int e = e0 + tid; e < e1; e += blockDim.x)
                     if (element_tet(e, S.m, f, S.contrib, S.load)) badv = fmax(badv, (double)(M - e));
+                sy.barrier();  // a row's fill gathers contributions of other CTAs' elements
             }
-            sy.barrier();  // a row's fill gathers contributions of other CTAs' elements
             SIM_STAMP(2, global_ns());
             // ---- fill own rows into the shared-memory slice
             // diagonal sums and the PhysicsRange count in ONE reduction; the
@@ -379,8 +388,10 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
                     dv[0] = add(dv[0], S.diag_raw[2LL * i]);
                     dv[1] = add(dv[1], S.diag_raw[2LL * i + 1]);
                 }
-            sy.template reduce<3>(dv, 3, P(), co, red);
-            par ^= 1;
+            if (!smaj) {
+                sy.template reduce<3>(dv, 3, P(), co, red);
+                par ^= 1;
+            }
             if (co[2] > 0.0) {  // PhysicsRangeError aborts the run (fem.py:274)
                 const double badmax = reduce_max1(sy, badv, P(), red);
                 par ^= 1;

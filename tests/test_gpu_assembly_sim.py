@@ -327,15 +327,18 @@ def test_block_jacobi_pcg_full_run_vs_reference():
 def test_lean_and_generic_simulation_kernels_are_bitwise_equal():
     """The paper-scale instantiation of the fused simulation (pipelined PCG +
     cp.async-staged fill, everything else compiled out), the generic kernel
-    taking the same paths at run time, and the generic kernel with the
-    register-chunked fill give the same bits: same sums in the same order."""
+    taking the same paths at run time, the generic kernel with the
+    register-chunked fill, and the lean kernel with tet-major element
+    outputs gathered per element instead of the slot-major layout fetched
+    by TMA give the same bits: same sums in the same order."""
     import os
     from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh
     from paper_2409_13036_b200.timeloop import DeviceRun
     mesh = generate_box_mesh(15, 15, 16)
     cfg = SimConfig(total_time=40.0, solver=SolverConfig(backend="pcg", precondition="block_jacobi"))
     runs = []
-    for env in ({}, {"RAFEM_NO_LEAN_SIM": "1"}, {"RAFEM_NO_LEAN_SIM": "1", "RAFEM_NO_STAGE_CONTRIB": "1"}):
+    for env in ({}, {"RAFEM_NO_LEAN_SIM": "1"}, {"RAFEM_NO_LEAN_SIM": "1", "RAFEM_NO_STAGE_CONTRIB": "1"},
+                {"RAFEM_NO_SLOT_MAJOR": "1"}):
         os.environ.update(env)
         try:
             recs, summ = DeviceRun(mesh).run(cfg)

@@ -262,7 +262,8 @@ def test_tma_spmv_pipeline_configs_bitwise_at_1M_dofs():
     s, _ = _c3_system(hot=True)
     x = np.random.default_rng(6).standard_normal(s.rhs.size)
     ref = O.matvec(s.matrix.row_ptr, s.matrix.col_idx, s.matrix.vals, x)
-    for cfg in ("256,2,1", "128,4,1", "192,3,1", "1,1,1"):  # 1,1,1: two-stage kernel
+    # NT,ST,HINT[,CTAs per SM]; 1,1,1: the two-stage kernel
+    for cfg in ("256,2,1", "128,4,1", "192,3,1", "192,2,1,2", "128,2,1,3", "1,1,1"):
         for classes in ("0", "1"):  # stencil-class columns on / off
             os.environ["RAFEM_SPMV_CFG"] = cfg
             os.environ["RAFEM_NO_CLASSES"] = classes
