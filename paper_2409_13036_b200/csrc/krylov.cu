@@ -1062,7 +1062,8 @@ constexpr int kPipeRows = 128;  // max node rows per CTA (y and the owner vector
 // into x needs no barrier of its own; later heads gather x itself.
 template <bool PRE, class Mode, class R>
 RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, double bnorm, double* co, double* red,
-                            int& par, const int* zflag = nullptr, const double* x0_gather = nullptr) {
+                            int& par, const int* zflag = nullptr, const double* x0_gather = nullptr,
+                            const double* xold = nullptr, double* dmax = nullptr) {
     __shared__ double2 ybuf[kPipeRows];
     // owner-only recurrence vectors live in shared memory (indexed by the
     // global dof, offset by the CTA's first dof); u is mirrored to global
@@ -1226,8 +1227,36 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                 apply_block(r, u, ug);
             }
             if (with_b && zflag && tid == 0) v[1] = (double)*zflag;
-            for (int e = lo + tid; e < hi; e += blockDim.x) xs[e] = x[e];  // owner copy (synced below)
-            sy.template reduce<3>(v, 3, a.partial + par * pstride, co, red);
+            if (xold) {
+                // the corrector delta of this iterate against xold (fem.py:527-528)
+                // rides on the head's reduction: max over CTAs by a fourth warp
+                double dm = 0.0;
+                for (int e = lo + tid; e < hi; e += blockDim.x) {
+                    const double xe = x[e], xo = xold[e];
+                    xs[e] = xe;  // owner copy (synced below)
+                    const double d = fabs(sub(xe, xo)) / fmax(1.0, fabs(xo));
+                    dm = (d > dm || d != d) ? d : dm;
+                }
+                double* P = a.partial + par * pstride;
+                dm = block_max(dm, red);
+                if (tid == 0) P[3LL * G + cta] = dm;
+                publish<3>(v, 3, P, 0, G, red);
+                sy.barrier();
+                if (warp < 3) {
+                    const double s = reduce_partials_warp(P + (long long)warp * G, G);
+                    if (lane == 0) co[warp] = s;
+                } else if (warp == 3) {
+                    double mx = 0.0;
+                    for (int c = lane; c < G; c += 32) mx = fmax(mx, __ldcg(P + 3LL * G + c));
+                    mx = warp_max(mx);
+                    if (lane == 0) co[3] = mx;
+                }
+                __syncthreads();
+                *dmax = co[3];
+            } else {
+                for (int e = lo + tid; e < hi; e += blockDim.x) xs[e] = x[e];  // owner copy (synced below)
+                sy.template reduce<3>(v, 3, a.partial + par * pstride, co, red);
+            }
             par ^= 1;
             if (with_b) {
                 if (co[1] > 0.0) return PcgOut{0, INFINITY, 0, RAFEM_ERR_INVALID};
@@ -1235,6 +1264,7 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                 if (bnorm == 0.0) {  // zero data: zero solution (solver.py:422-425)
                     for (int e = lo + tid; e < hi; e += blockDim.x) x[e] = 0.0;
                     __syncthreads();
+                    if (dmax) *dmax = -1.0;  // x changed after the head: the caller computes the delta
                     return PcgOut{0, 0.0, 1, RAFEM_OK};
                 }
             }

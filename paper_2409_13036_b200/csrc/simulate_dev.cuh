@@ -423,6 +423,7 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
             for (int e = ec + blockDim.x; e < hi; e += blockDim.x) X(inew)[e] = X(iit)[e];
             __syncthreads();
             PcgOut o{0, 0.0, 1, RAFEM_OK};
+            double hdelta = -1.0;  // delta from the pipelined PCG's final head (< 0: not computed)
             long long tb;
             if (LEAN || a.pipe) {
                 // ||b|| and the zero-diagonal flag ride on the PCG head's reduction
@@ -432,7 +433,7 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
                 kk.b = S.rhs;
                 kk.x = X(inew);
                 kk.res = nullptr;
-                o = pcg_pipe_core<PRE, GridMode>(kk, rows, sy, -1.0, co, red, par, &zflag, X(iit));
+                o = pcg_pipe_core<PRE, GridMode>(kk, rows, sy, -1.0, co, red, par, &zflag, X(iit), X(iit), &hdelta);
                 if (o.status == RAFEM_ERR_INVALID) {  // ValueError: zero diagonal under Jacobi (solver.py:416-417)
                     status = RAFEM_ERR_INVALID;
                     abort_run = true;
@@ -470,15 +471,19 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
             if (o.status == RAFEM_ERR_BREAKDOWN) break;  // SolverError -> step failure (fem.py:511-515)
             inner += o.total;
             if (!o.converged) break;  // fem.py:517-524
-            // ---- corrector delta (fem.py:527-528)
-            double dmax = 0.0;
-            for (int e = lo + tid; e < hi; e += blockDim.x) {
-                const double xo = X(iit)[e];
-                const double d = fabs(sub(X(inew)[e], xo)) / fmax(1.0, fabs(xo));
-                dmax = (d > dmax || d != d) ? d : dmax;
+            // ---- corrector delta (fem.py:527-528): from the PCG's final head
+            // (the converged iterate) when it computed one
+            double delta = hdelta;
+            if (!(delta >= 0.0)) {
+                double dmax = 0.0;
+                for (int e = lo + tid; e < hi; e += blockDim.x) {
+                    const double xo = X(iit)[e];
+                    const double d = fabs(sub(X(inew)[e], xo)) / fmax(1.0, fabs(xo));
+                    dmax = (d > dmax || d != d) ? d : dmax;
+                }
+                delta = reduce_max1(sy, dmax, P(), red);
+                par ^= 1;
             }
-            const double delta = reduce_max1(sy, dmax, P(), red);
-            par ^= 1;
             SIM_STAMP(6, global_ns());
             const int tmp = iit;
             iit = inew;
