@@ -603,6 +603,14 @@ def c3_leg(hbm_peak, peak_src, cpu_on=True):
     from paper_2409_13036_b200 import _native as nat
     ms = C.c_double()
     nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 50, 1, C.byref(ms)), "spmv bench")
+    # SURVEY §8(d) C3 protocol: 1,000 back-to-back SpMVs (no flush; the
+    # 137 MB stream exceeds the 126 MB L2, and the matrix is marked
+    # evict-first), with and without programmatic dependent launch
+    ms_b2b, ms_b2b_plain = C.c_double(), C.c_double()
+    nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 1000, 0, C.byref(ms_b2b)), "spmv bench")
+    os.environ["RAFEM_NO_PDL"] = "1"
+    nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 1000, 0, C.byref(ms_b2b_plain)), "spmv bench")
+    del os.environ["RAFEM_NO_PDL"]
     os.environ["RAFEM_NO_TMA_SPMV"] = "1"
     ms_plain = C.c_double()
     nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 50, 1, C.byref(ms_plain)), "spmv bench")
@@ -658,7 +666,14 @@ def c3_leg(hbm_peak, peak_src, cpu_on=True):
                      "columns": (f"stencil classes ({ncls}; computed, values-only TMA stream)" if cls_on
                                  else "explicit int32 columns"),
                      "explicit_columns_equivalent_GBs": b_explicit / (ms.value / 1e3) / 1e9,
-                     "l2": "flushed (256 MB write) before every timed launch", "peak_source": peak_src},
+                     "l2": "flushed (256 MB write) before every timed launch", "peak_source": peak_src,
+                     "back_to_back": {"launches": 1000, "us_per_launch": 1e3 * ms_b2b.value,
+                                      "achieved": b_paired / (ms_b2b.value / 1e3) / 1e9,
+                                      "frac": b_paired / (ms_b2b.value / 1e3) / 1e9 / hbm_peak,
+                                      "us_per_launch_without_pdl": 1e3 * ms_b2b_plain.value,
+                                      "note": "no flush between launches (the matrix stream exceeds L2); "
+                                              "programmatic dependent launch streams a launch's first tiles "
+                                              "while the previous one drains"}},
             "pcg_cold_solve": {"l2": "flushed before the solve; iterations back to back",
                                "iterations": st.iterations, "device_ms": st.device_ms,
                                "us_per_iteration": 1e3 * st.device_ms / max(st.iterations, 1),

@@ -632,9 +632,19 @@ int rafem_system_spmv_bench(rafem_system* s, int32_t reps, int32_t flush_l2, dou
     const MatView A = system_view(s);
     if (int rc = spmv_launch(ctx, A, dx, dy)) return rc;  // warm-up
     if (!flush_l2) {
+        // back to back: each launch may stream its first matrix tiles while
+        // the previous one drains (programmatic dependent launch; the matrix
+        // is constant here, x and y are touched only after the dependency
+        // wait).  RAFEM_NO_PDL=1: plain stream order.
+        const char* np = getenv("RAFEM_NO_PDL");
+        ctx->spmv_pdl = !(np && np[0] == '1');
         RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
         for (int r = 0; r < reps; ++r)
-            if (int rc = spmv_launch(ctx, A, dx, dy)) return rc;
+            if (int rc = spmv_launch(ctx, A, dx, dy)) {
+                ctx->spmv_pdl = false;
+                return rc;
+            }
+        ctx->spmv_pdl = false;
         RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
         RF_CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
         float ms = 0.f;

@@ -115,6 +115,7 @@ struct rafem_ctx {
     int last_mode = -1;  // 1: cluster-resident solve, 0: grid-wide cooperative solve
     int last_ctas = 0;
     int last_team = 0;
+    bool spmv_pdl = false;  // streaming SpMV launched with programmatic dependent launch (back-to-back bench)
 };
 
 struct rafem_matrix {

@@ -2037,8 +2037,14 @@ __global__ void __launch_bounds__(NT, 1) spmv_tma_pipe_kernel(MatView A, const d
             if (cb) tma_load_1d(base + (size_t)valcap * 16, A.col + sa, cb, &bar[b]);
         }
     };
+    // programmatic dependent launch (no-ops otherwise): let the next kernel
+    // in the stream start its prologue as this grid's CTAs retire, and
+    // stream this grid's first matrix tiles (constant data) before waiting
+    // for the previous kernel, which may still be writing x or reading y
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (threadIdx.x == 0)
         for (int i = 0; i < ST && i < mine; ++i) issue(i);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const double2* x2 = reinterpret_cast<const double2*>(x);
     for (int i = 0; i < mine; ++i) {
         const int b = i % ST;
@@ -2195,7 +2201,21 @@ static int spmv_pipe_launch(rafem_ctx* ctx, const MatView& A, const double* x_de
     const double* xp = x_dev;
     double* yp = y_dev;
     void* args[] = {&Av, &xp, &yp, &valcap, &bufbytes};
-    RF_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(grid), dim3(c.nt), args, smem, ctx->stream));
+    if (ctx->spmv_pdl) {
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(grid);
+        lc.blockDim = dim3(c.nt);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = ctx->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        RF_CUDA_TRY(ctx, cudaLaunchKernelExC(&lc, fn, args));
+    } else {
+        RF_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(grid), dim3(c.nt), args, smem, ctx->stream));
+    }
     ctx->launches++;
     return RAFEM_OK;
 }
