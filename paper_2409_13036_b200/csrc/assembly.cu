@@ -431,13 +431,21 @@ __global__ void expand_kernel(const int* rp, int N, const double* val2, double* 
 
 // predictor (fem.py:437-449) on interleaved dof vectors: V carries over,
 // T + (dt/dt_prev)(T - T_prev) once history exists.
+// fem.py:437-449: T extrapolated in time, V carried over.  x_start (may be
+// null): the first pass's solver start, with V extrapolated like T.
 __global__ void predictor_kernel(double* x_it, const double* x_acc, const double* x_prev, int N,
-                                 int step, double ratio) {
+                                 int step, double ratio, double* x_start) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
     const double t = x_acc[2LL * i + 1];
+    const double tp = step >= 1 ? add(t, mul(ratio, sub(t, x_prev[2LL * i + 1]))) : t;
     x_it[2LL * i] = x_acc[2LL * i];
-    x_it[2LL * i + 1] = step >= 1 ? add(t, mul(ratio, sub(t, x_prev[2LL * i + 1]))) : t;
+    x_it[2LL * i + 1] = tp;
+    if (x_start) {
+        const double v = x_acc[2LL * i];
+        x_start[2LL * i] = step >= 1 ? add(v, mul(ratio, sub(v, x_prev[2LL * i]))) : v;
+        x_start[2LL * i + 1] = tp;
+    }
 }
 
 __global__ void fill_state_kernel(double* x, int N, double t0) {
@@ -791,8 +799,8 @@ int expand_dof_vals(rafem_system* s, double* out_dev) {
 }
 
 int predictor_launch(rafem_ctx* ctx, double* x_it, const double* x_acc, const double* x_prev, int N,
-                     int step, double ratio) {
-    predictor_kernel<<<(N + 255) / 256, 256, 0, ctx->stream>>>(x_it, x_acc, x_prev, N, step, ratio);
+                     int step, double ratio, double* x_start) {
+    predictor_kernel<<<(N + 255) / 256, 256, 0, ctx->stream>>>(x_it, x_acc, x_prev, N, step, ratio, x_start);
     ctx->launches++;
     RF_CUDA_TRY(ctx, cudaGetLastError());
     return RAFEM_OK;

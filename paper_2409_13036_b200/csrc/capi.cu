@@ -928,7 +928,12 @@ int rafem_simulate(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary
         const double remaining = p->total_time - t;
         const bool final_step = dt_state >= remaining;
         const double dt = final_step ? remaining : dt_state;
-        if (int rc = predictor_launch(ctx, xit, xacc, xprev, N, (int)step, dt / dt_prev)) return rc;
+        // PCG: the first pass's solver starts from V extrapolated in time as
+        // well (same system and delta reference; simulate_dev.cuh)
+        const char* nv = getenv("RAFEM_NO_VX0");
+        const bool vx0 = p->solver.method == RAFEM_METHOD_PCG && !(nv && nv[0] == '1');
+        if (int rc = predictor_launch(ctx, xit, xacc, xprev, N, (int)step, dt / dt_prev, vx0 ? xnew : nullptr))
+            return rc;
         bool converged = false;
         int iters = 0;
         for (int it = 1; it <= p->max_corrector_iters; ++it) {
@@ -943,8 +948,8 @@ int rafem_simulate(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary
             } else {
                 RF_CUDA_TRY(ctx, cudaMemsetAsync(&ds->flag, 0, sizeof(int), st));
             }
-            if (int rc = krylov_solve(ctx, A, s->rhs, xit, xnew, s->minv, p->solver, &ds->pass.solve, &ds->flag,
-                                      ctx->ev1, ctx->ev2))
+            if (int rc = krylov_solve(ctx, A, s->rhs, (vx0 && it == 1) ? xnew : xit, xnew, s->minv, p->solver,
+                                      &ds->pass.solve, &ds->flag, ctx->ev1, ctx->ev2))
                 return rc;
             if (int rc = vec_delta_launch(ctx, xnew, xit, (int)n2, &ds->pass.delta)) return rc;
             PassStatus hs;

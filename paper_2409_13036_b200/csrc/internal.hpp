@@ -238,7 +238,8 @@ int diag_sums_launch(rafem_ctx* ctx, const double* diag_raw, int n, int equilibr
                      double* scale_dev);
 int expand_dof_vals(rafem_system* s, double* out_dev);
 int predictor_launch(rafem_ctx* ctx, double* x_it, const double* x_acc, const double* x_prev,
-                     int N, int step, double ratio);
+                     int N, int step, double ratio,
+                     double* x_start = nullptr);
 int fill_initial(rafem_ctx* ctx, double* x, int N, double t0);
 struct AsmMesh;
 AsmMesh asm_mesh(const rafem_mesh* m);

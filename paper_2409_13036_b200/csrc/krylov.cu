@@ -2772,6 +2772,10 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
         S.m.lpos = nullptr;
     }
     S.stage_fill = stage_fill;
+    {
+        const char* nv = getenv("RAFEM_NO_VX0");
+        S.vx0 = !(nv && nv[0] == '1');
+    }
     S.contrib = reinterpret_cast<double2*>(s->contrib);
     S.load = s->load;
     S.rhs = s->rhs;

@@ -48,6 +48,7 @@ struct SimArgs {
     long long* ptrace;         // optional per-pass phase stamps (globaltimer ns), 8 per pass
     long long ptrace_cap;
     int stage_fill;            // contributor lists, incidences and dof kinds staged in smem
+    int vx0;                   // pipelined PCG: first pass of a step starts from V extrapolated in time
 };
 
 // Max over CTAs of one nonnegative value (exact, order independent).
@@ -264,9 +265,19 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
         const bool final_step = dt_state >= remaining;
         const double dt = final_step ? remaining : dt_state;
         const double ratio = dt / dt_prev;
-        for (int e = lo + tid; e < hi; e += blockDim.x) {  // predictor (fem.py:437-449)
+        // predictor (fem.py:437-449): T extrapolated in time, V carried over.
+        // With vx0 the first pass's SOLVER starts from both extrapolated
+        // (X(inew), complete everywhere after the pass's first barrier); the
+        // iterate the pass assembles from and measures its delta against is
+        // still the reference predictor in X(iit).  Same systems, same
+        // trajectory, ~30 % fewer PCG iterations on the first passes
+        // (scripts/x0_extrap_probe.py).
+        const bool vx0 = S.vx0 != 0;
+        for (int e = lo + tid; e < hi; e += blockDim.x) {
             const double xa = X(iacc)[e];
-            X(iit)[e] = ((e & 1) && step >= 1) ? add(xa, mul(ratio, sub(xa, X(iprev)[e]))) : xa;
+            const double xe = step >= 1 ? add(xa, mul(ratio, sub(xa, X(iprev)[e]))) : xa;
+            X(iit)[e] = (e & 1) ? xe : xa;
+            if (vx0) X(inew)[e] = xe;
         }
         bool conv = false, abort_run = false;
         int iters = 0;
@@ -419,8 +430,11 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
                     constrain_node_warp(i, S.m, scale, 1, p.applied_voltage, p.boundary_temp, sv2 + srp[r], S.rhs,
                                         PRE ? const_cast<double*>(a.minv) : nullptr, &zflag, scol + srp[r]);
                 }
-            if (ec < hi) X(inew)[ec] = xc;
-            for (int e = ec + blockDim.x; e < hi; e += blockDim.x) X(inew)[e] = X(iit)[e];
+            const bool x0_new = vx0 && it == 1;  // X(inew) already holds the first pass's start
+            if (!x0_new) {
+                if (ec < hi) X(inew)[ec] = xc;
+                for (int e = ec + blockDim.x; e < hi; e += blockDim.x) X(inew)[e] = X(iit)[e];
+            }
             __syncthreads();
             PcgOut o{0, 0.0, 1, RAFEM_OK};
             double hdelta = -1.0;  // delta from the pipelined PCG's final head (< 0: not computed)
@@ -433,7 +447,8 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
                 kk.b = S.rhs;
                 kk.x = X(inew);
                 kk.res = nullptr;
-                o = pcg_pipe_core<PRE, GridMode>(kk, rows, sy, -1.0, co, red, par, &zflag, X(iit), X(iit), &hdelta);
+                o = pcg_pipe_core<PRE, GridMode>(kk, rows, sy, -1.0, co, red, par, &zflag, x0_new ? X(inew) : X(iit),
+                                                 X(iit), &hdelta);
                 if (o.status == RAFEM_ERR_INVALID) {  // ValueError: zero diagonal under Jacobi (solver.py:416-417)
                     status = RAFEM_ERR_INVALID;
                     abort_run = true;
