@@ -16,11 +16,12 @@ sys.path.insert(0, '.')
 from oracle import rafem_oracle as O
 
 
-def run(mesh, cfg, c, precondition="jacobi", vfirst=False):
+def run(mesh, cfg, c, precondition="jacobi", vfirst=False, quad=False):
     N = mesh.node_count
     geom = O.geometry(mesh)
     mats = {0: O.OMaterial()}
     T = np.full(N, cfg.initial_temp); V = np.zeros(N); T_prev = T.copy(); V_prev = V.copy()
+    T_prev2, V_prev2, dt_prev2 = T.copy(), V.copy(), cfg.dt_init
     first_its = later_its = 0
     t, dt_cur, dt_prev, step = 0.0, cfg.dt_init, cfg.dt_init, 0
     passes = inner = 0
@@ -42,6 +43,13 @@ def run(mesh, cfg, c, precondition="jacobi", vfirst=False):
             if vfirst and x_prev is None and step >= 1:  # first pass: V extrapolated in time like T
                 x0 = x_old.copy()
                 x0[0::2] = V + (dt / dt_prev) * (V - V_prev)
+                if quad and step >= 2:  # quadratic (Lagrange through the last three accepted steps)
+                    t0_, t1_, t2_, te = -dt_prev - dt_prev2, -dt_prev, 0.0, dt
+                    l0 = (te - t1_) * (te - t2_) / ((t0_ - t1_) * (t0_ - t2_))
+                    l1 = (te - t0_) * (te - t2_) / ((t1_ - t0_) * (t1_ - t2_))
+                    l2 = (te - t0_) * (te - t1_) / ((t2_ - t0_) * (t2_ - t1_))
+                    x0[0::2] = l0 * V_prev2 + l1 * V_prev + l2 * V
+                    x0[1::2] = l0 * T_prev2 + l1 * T_prev + l2 * T
             x_new, st = O.pcg(s.row_ptr, s.col_idx, s.vals, s.rhs.copy(), x0=x0.copy(), tol=cfg.tolerance,
                               precondition=precondition)
             inner += st.iterations
@@ -56,6 +64,7 @@ def run(mesh, cfg, c, precondition="jacobi", vfirst=False):
                 ok = True
                 break
         assert ok
+        T_prev2, V_prev2, dt_prev2 = T_prev, V_prev, dt_prev
         T_prev, T, V_prev, V = T, t_it, V, v_it
         dt_prev = dt
         t = cfg.total_time if last else t + dt
@@ -68,13 +77,13 @@ def run(mesh, cfg, c, precondition="jacobi", vfirst=False):
 
 mesh = O.box_mesh(20, 20, 21)
 cfg = O.OSim(total_time=900.0, method="pcg")
-variants = [(0.0, False), (0.0, True)] if len(sys.argv) == 1 else \
-    [(float(a), "--vfirst" in sys.argv) for a in sys.argv[1:] if a != "--vfirst"]
+variants = [(0.0, False, False), (0.0, True, False)] if len(sys.argv) == 1 else \
+    [(float(a), "--vfirst" in sys.argv, "--quad" in sys.argv) for a in sys.argv[1:] if not a.startswith("--")]
 base = None
-for c, vfirst in variants:
+for c, vfirst, quad in variants:
     t0 = time.perf_counter()
-    steps, passes, inner, traj = run(mesh, cfg, c, vfirst=vfirst)
+    steps, passes, inner, traj = run(mesh, cfg, c, vfirst=vfirst, quad=quad)
     same = "" if base is None else ("same trajectory" if traj == base else "TRAJECTORY DIFFERS")
     base = base or traj
-    print(f"c={c:4.2f} vfirst={vfirst}: steps {steps} passes {passes} PCG iterations {inner} "
+    print(f"c={c:4.2f} vfirst={vfirst} quad={quad}: steps {steps} passes {passes} PCG iterations {inner} "
           f"({time.perf_counter() - t0:.0f} s) {same}", flush=True)
