@@ -2110,6 +2110,21 @@ __global__ void delta_kernel(const double* xn, const double* xo, int n, unsigned
 // ---------------------------------------------------------------------------
 // host launchers
 
+// Per row-block boundary c <= G: gpart[c], rp[gpart[c]] and, with the
+// optional arrays, inc_ptr[gpart[c]] and slot_ptr[rp[gpart[c]]]; `nout`
+// of these rows (each G + 1 ints) are written to out.
+__global__ void block_bounds_kernel(const int* gpart, int G, const int* rp, const int* inc_ptr, const int* slot_ptr,
+                                    int* out, int nout) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c > G) return;
+    const int g = gpart[c], s = rp[g];
+    const int n = G + 1;
+    out[c] = g;
+    out[n + c] = s;
+    if (nout > 2) out[2 * n + c] = inc_ptr ? inc_ptr[g] : 0;
+    if (nout > 3) out[3 * n + c] = slot_ptr ? slot_ptr[s] : 0;
+}
+
 // The grid-barrier counter lives after the 2 x G x 8 barrier slots of
 // ws_flags.  Opt-in (RAFEM_CNT_SYNC=1): in the microbenchmark it beats
 // cooperative_groups' grid sync by 0.8 us per round when every CTA has
@@ -2335,12 +2350,18 @@ static int partition(rafem_ctx* ctx, const MatView& A, int G, bool need_slice, P
     size_t max_slice = 0;
     int max_groups = 0;
     if (need_slice) {
-        std::vector<int> hp(G + 1), hr(G + 1);
-        RF_CUDA_TRY(ctx, cudaMemcpyAsync(hp.data(), gpart, sizeof(int) * (G + 1), cudaMemcpyDeviceToHost, ctx->stream));
+        // the block boundaries and their row starts in one copy (gathered on
+        // the device: G + 1 single-int copies cost ~1 ms of driver calls)
+        std::vector<int> hb(2 * (G + 1));
+        int* db = nullptr;
+        RF_CUDA_TRY(ctx, dmalloc(ctx, reinterpret_cast<void**>(&db), sizeof(int) * 2 * (G + 1)));
+        block_bounds_kernel<<<(G + 1 + 127) / 128, 128, 0, ctx->stream>>>(gpart, G, A.rp, nullptr, nullptr, db, 2);
+        ctx->launches++;
+        RF_CUDA_TRY(ctx, cudaMemcpyAsync(hb.data(), db, sizeof(int) * 2 * (G + 1), cudaMemcpyDeviceToHost, ctx->stream));
         RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-        for (int c = 0; c <= G; ++c)
-            RF_CUDA_TRY(ctx, cudaMemcpyAsync(&hr[c], A.rp + hp[c], sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-        RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        dfree(ctx, db);
+        const int* hp = hb.data();
+        const int* hr = hb.data() + (G + 1);
         for (int c = 0; c < G; ++c) {
             const size_t ns = (size_t)(hr[c + 1] - hr[c]);
             const size_t ng = (size_t)(hp[c + 1] - hp[c]);
@@ -2670,18 +2691,26 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     // room to stage each CTA's assembly index data (simulate_dev.cuh)
     int stage_fill = 0;
     if (mesh->slot_src && !(getenv("RAFEM_NO_STAGE_FILL") && getenv("RAFEM_NO_STAGE_FILL")[0] == '1')) {
-        std::vector<int> hg(G + 1), hrp(N + 1), hip(N + 1);
-        RF_CUDA_TRY(ctx, cudaMemcpy(hg.data(), part.gpart, sizeof(int) * (G + 1), cudaMemcpyDeviceToHost));
-        RF_CUDA_TRY(ctx, cudaMemcpy(hrp.data(), mesh->rp, sizeof(int) * (N + 1), cudaMemcpyDeviceToHost));
-        RF_CUDA_TRY(ctx, cudaMemcpy(hip.data(), mesh->inc_ptr, sizeof(int) * (N + 1), cudaMemcpyDeviceToHost));
-        std::vector<int> hsp(mesh->slots + 1);
-        RF_CUDA_TRY(ctx, cudaMemcpy(hsp.data(), mesh->slot_ptr, sizeof(int) * (mesh->slots + 1), cudaMemcpyDeviceToHost));
+        // per block: row, slot, incidence and contributor-list boundaries,
+        // gathered on the device and copied once
+        const int n1 = G + 1;
+        std::vector<int> hb(4 * (size_t)n1);
+        int* db = nullptr;
+        RF_CUDA_TRY(ctx, dmalloc(ctx, reinterpret_cast<void**>(&db), sizeof(int) * 4 * (size_t)n1));
+        block_bounds_kernel<<<(n1 + 127) / 128, 128, 0, ctx->stream>>>(part.gpart, G, mesh->rp, mesh->inc_ptr,
+                                                                       mesh->slot_ptr, db, 4);
+        ctx->launches++;
+        RF_CUDA_TRY(ctx, cudaMemcpyAsync(hb.data(), db, sizeof(int) * 4 * (size_t)n1, cudaMemcpyDeviceToHost,
+                                         ctx->stream));
+        RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        dfree(ctx, db);
+        const int *hg = hb.data(), *hrs = hb.data() + n1, *hip = hb.data() + 2 * n1, *hsp = hb.data() + 3 * n1;
         size_t need = 0, need2 = 0;
         for (int c = 0; c < G; ++c) {
             const size_t nr = (size_t)(hg[c + 1] - hg[c]);
-            const size_t ns = (size_t)(hrp[hg[c + 1]] - hrp[hg[c]]);
-            const size_t nsrc = (size_t)(hsp[hrp[hg[c + 1]]] - hsp[hrp[hg[c]]]);
-            const size_t ninc = (size_t)(hip[hg[c + 1]] - hip[hg[c]]);
+            const size_t ns = (size_t)(hrs[c + 1] - hrs[c]);
+            const size_t nsrc = (size_t)(hsp[c + 1] - hsp[c]);
+            const size_t ninc = (size_t)(hip[c + 1] - hip[c]);
             const size_t slice = ns * 16 + ((ns + 3) & ~(size_t)3) * 4 + (nr + 1) * 4;
             const size_t extra = (ns + 1) * 4 + nsrc * 4 + (nr + 1) * 4 + ninc * 4 + nr * 4 + ns + 2 * nr + 8 + 8 * nr;
             need = std::max(need, slice + extra);
