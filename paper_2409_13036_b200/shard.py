@@ -29,6 +29,7 @@ Per shard:
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -622,7 +623,10 @@ class ShardedSimulation:
         n = self.plan.n_own
         T = np.full(n, config.initial_temp)
         V = np.zeros(n)
-        T_prev = T.copy()
+        T_prev, V_prev = T.copy(), V.copy()
+        # like the fused kernel: a step's first solve starts from V extrapolated
+        # in time too (the pass still assembles from / compares with x_old)
+        vx0 = os.environ.get("RAFEM_NO_VX0", "0") != "1"
         t, dt_cur, dt_prev, step = 0.0, config.dt_init, config.dt_init, 0
         corr = inner = halv = 0
         asm_s = sol_s = 0.0
@@ -645,8 +649,12 @@ class ShardedSimulation:
                 te, ve, tpe = self._ext(t_it, v_it, T)
                 self.sys.assemble(te, ve, tpe, dt, config)
                 a1 = time.perf_counter()
+                x0 = x_old
+                if vx0 and it == 1 and step >= 1:
+                    x0 = x_old.copy()
+                    x0[0::2] = V + (dt / dt_prev) * (V - V_prev)
                 try:
-                    x_new, st = self.sys.solve(x0=x_old, config=config.solver)
+                    x_new, st = self.sys.solve(x0=x0, config=config.solver)
                 except SolverError:
                     break  # step failure (fem.py:511-515)
                 finally:
@@ -664,7 +672,7 @@ class ShardedSimulation:
                     break
             corr += used
             if ok:
-                T_prev, T, V = T, t_it, v_it
+                T_prev, T, V_prev, V = T, t_it, V, v_it
                 dt_prev = dt
                 t = config.total_time if last else t + dt
                 rec = ShardStep(step, t, dt, used, T.copy() if record_fields else None,
