@@ -679,6 +679,7 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
         for (int k = 0; k < m; ++k) {
             double* wk = (k & 1) ? a.w1 : a.w0;
             double* Vk = vrow(k);
+            stamp(a, total, 0);
             // v_k (own rows) and w = A (M^-1 v_k)       (solver.py:469-470)
             for (int e = lo + tid; e < hi; e += bd) Vk[e] = mul(src[e], src_scale);
             spmv_team<W>(rows, g0, g1, a.team, SrcBasis<PRE>{src, src_scale, a.minv}, [&](int g, const double* y) {
@@ -686,13 +687,16 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
                 for (int w = 0; w < W; ++w) wk[W * g + w] = y[w];
             });
             __syncthreads();
+            stamp(a, total, 1);
             // CGS pass 1: h_i = v_i . w
             double* P = a.partial + par * pstride;
             if (Vs)
                 multidot_smem(Vs, a.vs_ld, k + 1, wk, lo, hi, P, G);
             else
                 multidot(a.V, ldv, k + 1, wk, lo, hi, P, G, red);
+            stamp(a, total, 2);
             sy.sync_gather(P, k + 1, co);
+            stamp(a, total, 3);
             par ^= 1;
             if (tid == 0)
                 for (int i = 0; i <= k; ++i) H[(long long)k * (m + 1) + i] = co[i];
@@ -709,7 +713,9 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
             } else {
                 multidot(a.V, ldv, k + 1, wk, lo, hi, P, G, red);
             }
+            stamp(a, total, 4);
             sy.sync_gather(P, Vs ? k + 2 : k + 1, co);
+            stamp(a, total, 5);
             par ^= 1;
             if (tid == 0)
                 for (int i = 0; i <= k; ++i) H[(long long)k * (m + 1) + i] = add(H[(long long)k * (m + 1) + i], co[i]);
@@ -743,6 +749,7 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
                 par ^= 1;
                 hk1 = sqrt(co[0]);
             }
+            stamp(a, total, 6);
             total += 1;
             // Givens update of column k (solver.py:478-496), one thread per CTA
             if (tid == 0) {
@@ -1246,9 +1253,7 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                     const double s = reduce_partials_warp(P + (long long)warp * G, G);
                     if (lane == 0) co[warp] = s;
                 } else if (warp == 3) {
-                    double mx = 0.0;
-                    for (int c = lane; c < G; c += 32) mx = fmax(mx, __ldcg(P + 3LL * G + c));
-                    mx = warp_max(mx);
+                    const double mx = reduce_max_partials_warp(P + 3LL * G, G);
                     if (lane == 0) co[3] = mx;
                 }
                 __syncthreads();

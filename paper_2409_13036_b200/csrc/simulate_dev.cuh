@@ -59,9 +59,7 @@ RF_DEV double reduce_max1(Sync<Mode>& sy, double v, double* P, double* red) {
     if (threadIdx.x == 0) P[blockIdx.x] = v;
     sy.barrier();
     if (threadIdx.x < 32) {
-        double m = 0.0;
-        for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) m = fmax(m, __ldcg(P + c));
-        m = warp_max(m);
+        const double m = reduce_max_partials_warp(P, (int)gridDim.x);
         if (threadIdx.x == 0) res = m;
     }
     __syncthreads();

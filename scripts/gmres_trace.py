@@ -22,7 +22,7 @@ tr = tr.reshape(-1, 8)[5:min(st.iterations, 4000) - 1]
 ok = (tr[:, :7] > 0).all(axis=1)
 tr = tr[ok]
 d = np.diff(tr[:, :7], axis=1) / 1.965e3
-names = ["spmv", "multidot1", "sync_gather1", "update1+multidot2", "sync_gather2", "update2+norm reduce"]
+names = ["basis row + spmv", "multidot1", "sync_gather1", "update1+multidot2", "sync_gather2", "update2+barrier"]
 print(f"gmres: {st.iterations} its, {st.device_ms*1e3/st.iterations:.2f} us/it")
 for i, nme in enumerate(names):
     print(f"  {nme:22s} {d[:, i].mean():6.2f} us")
