@@ -2683,8 +2683,11 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
         if (int rc = mesh_slot_lists(mesh)) return rc;
     const void* fn = pre ? (const void*)simulate_kernel<true, 256, false> : (const void*)simulate_kernel<false, 256, false>;
     const void* fn_lean = pre ? (const void*)simulate_kernel<true, 256, true> : (const void*)simulate_kernel<false, 256, true>;
-    const bool pipe = pipe_rows(false, 2, N, std::max(1, std::min(ctx->sm_count, N)));
-    const int G = std::max(1, std::min(ctx->sm_count, N));
+    // one CTA per SM (RAFEM_SIM_CTAS overrides, for experiments)
+    int gsim = ctx->sm_count;
+    if (const char* e = getenv("RAFEM_SIM_CTAS")) gsim = std::max(1, std::min(ctx->sm_count, atoi(e)));
+    const bool pipe = pipe_rows(false, 2, N, std::max(1, std::min(gsim, N)));
+    const int G = std::max(1, std::min(gsim, N));
     PartInfo part;
     if (A.slots * 20LL > (long long)G * (150 << 10)) return RAFEM_ERR_UNSUPPORTED;
     if (int rc = partition(ctx, A, G, true, part, pipe_rows(false, 2, N, G))) return rc;
