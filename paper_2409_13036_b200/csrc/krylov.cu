@@ -1112,21 +1112,37 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
     if (blk) {
         // in-block slots of each own row as a bit mask (rows have <= 32 slots
         // here), and the block's Gershgorin bound of D^-1/2 A_cc D^-1/2
+        // a team of lanes per row (slots l, l + bt, ...), D^-1/2 staged once
         double gmax = 0.0;
-        for (int rr = tid; rr < nr; rr += blockDim.x) {
-            const int g = g0 + rr, sb = rows.start(g), deg = rows.start(g + 1) - sb;
+        for (int e = lo + tid; e < hi; e += blockDim.x) s_y[e - lo] = sqrt(mvs[e]);
+        __syncthreads();
+        const double* sq = s_y - lo;
+        int bt = 1;
+        while (bt < 8 && ((nr * bt * 2 + 31) & ~31) <= (int)blockDim.x) bt *= 2;
+        for (int base = 0; base < nr * bt; base += blockDim.x) {
+            const int q = base + tid, rr = q / bt, l0 = q & (bt - 1);
             unsigned mask = 0;
             double gv = 0.0, gt = 0.0;
-            for (int l = 0; l < deg && l < 32; ++l) {
-                const int c = rows.column(sb + l);
-                if (c < g0 || c >= g1) continue;
-                mask |= 1u << l;
-                const double2 v = rows.value2(sb + l);
-                gv = add(gv, mul(fabs(v.x), sqrt(mul(mvs[2 * g], mvs[2 * c]))));
-                gt = add(gt, mul(fabs(v.y), sqrt(mul(mvs[2 * g + 1], mvs[2 * c + 1]))));
+            if (rr < nr) {
+                const int g = g0 + rr, sb = rows.start(g), deg = rows.start(g + 1) - sb;
+                for (int l = l0; l < deg && l < 32; l += bt) {
+                    const int c = rows.column(sb + l);
+                    if (c < g0 || c >= g1) continue;
+                    mask |= 1u << l;
+                    const double2 v = rows.value2(sb + l);
+                    gv = add(gv, mul(fabs(v.x), mul(sq[2 * g], sq[2 * c])));
+                    gt = add(gt, mul(fabs(v.y), mul(sq[2 * g + 1], sq[2 * c + 1])));
+                }
             }
-            s_inmask[rr] = mask;
-            gmax = fmax(gmax, fmax(gv, gt));
+            for (int o = bt >> 1; o > 0; o >>= 1) {  // (whole warps: bt divides 32)
+                mask |= __shfl_xor_sync(0xffffffffu, mask, o);
+                gv = add(gv, __shfl_xor_sync(0xffffffffu, gv, o));
+                gt = add(gt, __shfl_xor_sync(0xffffffffu, gt, o));
+            }
+            if (rr < nr && l0 == 0) {
+                s_inmask[rr] = mask;
+                gmax = fmax(gmax, fmax(gv, gt));
+            }
         }
         gmax = block_max(gmax, red);
         if (tid == 0) s_omega = gmax > 1.98 ? 0.98 / (gmax - 1.0) : 1.0;
