@@ -91,7 +91,12 @@ class SimConfig:
 
 def _region_tables(mesh, material):
     """Region tag -> row index and per-region coefficient tables (fem.py:212-226)."""
-    tags, index = np.unique(mesh.regions, return_inverse=True)
+    reg = np.asarray(mesh.regions)
+    lo = int(reg.min()) if reg.size else 0
+    if reg.size and lo == int(reg.max()):  # one region (the common case): no sort
+        tags, index = np.array([lo]), np.zeros(reg.shape, dtype=np.int32)
+    else:
+        tags, index = np.unique(reg, return_inverse=True)
     mats = [material.for_region(int(t)) for t in tags]  # KeyError like the reference
     tab = {name: np.ascontiguousarray([getattr(m, name) for m in mats], dtype=np.float64)
            for name in ("k", "rho_c", "sigma0", "alpha", "t_ref")}
