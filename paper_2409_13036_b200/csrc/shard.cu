@@ -40,10 +40,14 @@
 
 namespace rafem {
 
-// threads per CTA of the SpMV kernels = node rows per tile: 384 with
-// stencil-class columns (values-only stages fit twice), else 256
+// threads per CTA of the SpMV kernels = node rows per tile: with
+// stencil-class columns 192, two CTAs per SM (values-only stages fit twice
+// per CTA; measured on the streaming SpMV, r1j: 405 vs 416 us at 16M dofs
+// for one 384-row CTA per SM), else 256 at one CTA per SM
 template <bool CLS>
-__host__ __device__ constexpr int kpt() { return CLS ? 384 : 256; }
+__host__ __device__ constexpr int kpt() { return CLS ? 192 : 256; }
+template <bool CLS>
+__host__ __device__ constexpr int kpc() { return CLS ? 2 : 1; }  // SpMV CTAs per SM
 constexpr int KPU = 256;      // threads per CTA of the update kernel
 constexpr int kKpStages = 2;  // TMA pipeline depth
 
@@ -242,7 +246,7 @@ __global__ void kp_bnorm_finish_kernel(KPArgs a) {
 
 // head: r = b - A x, u = M r ; partials (r.u, r.r) -> partA
 template <bool PRE, bool CLS>
-__global__ void __launch_bounds__(kpt<CLS>(), 1) kp_head_kernel(KPArgs a, int idx) {
+__global__ void __launch_bounds__(kpt<CLS>(), kpc<CLS>()) kp_head_kernel(KPArgs a, int idx) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) unsigned long long bar[kKpStages];
     __shared__ double red[64];
@@ -267,7 +271,7 @@ __global__ void __launch_bounds__(kpt<CLS>(), 1) kp_head_kernel(KPArgs a, int id
 // w = A u ; partial (w.u); last CTA folds (r.u, r.r) of the preceding
 // writer (ga CTAs) and (w.u) into rank_part[rank]
 template <bool CLS>
-__global__ void __launch_bounds__(kpt<CLS>(), 1) kp_spmv_kernel(KPArgs a, int idx, int after_head, int ga) {
+__global__ void __launch_bounds__(kpt<CLS>(), kpc<CLS>()) kp_spmv_kernel(KPArgs a, int idx, int after_head, int ga) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) unsigned long long bar[kKpStages];
     __shared__ double red[32];
@@ -483,7 +487,7 @@ int rafem_kp_create(rafem_system* sys, int64_t n_owned, int64_t n_ext, int32_t n
     k->n_ext = (int)n_ext;
     k->smem = smem;
     const int tiles = (int)((n_owned + KPT - 1) / KPT);
-    k->g_spmv = std::max(1, std::min(tiles, ctx->sm_count));
+    k->g_spmv = std::max(1, std::min(tiles, (cls ? kpc<true>() : kpc<false>()) * ctx->sm_count));
     k->g_upd = std::max(1, std::min((int)((n_owned + KPU - 1) / KPU), 4 * ctx->sm_count));
     const int gmax = std::max(k->g_spmv, k->g_upd);
     // layout: x_ext, u_ext (n_ext), r, w, s, p, b, minv (n_own) double2; partA 2*gmax, partB gmax,
