@@ -633,7 +633,11 @@ def c3_leg(hbm_peak, peak_src, cpu_on=True):
     torch.cuda.synchronize()
     x, st = solve(s.matrix, s.rhs, x0=x0, config=SolverConfig(backend="pcg", precondition="jacobi"))
     del flush
-    it_bytes = pcg_iter_bytes(N, S)
+    mode = nat.last_solve_mode()[0]
+    if mode == 4:  # kernel-per-phase engine: its SpMV bytes + 7 vector reads / 5 writes + u gather + w write
+        it_bytes = ((16 * S + N) if cls_on else 20 * S) + 4 * (N + 1) + 14 * 16 * N
+    else:
+        it_bytes = pcg_iter_bytes(N, S)
     solve_ach = st.iterations * it_bytes / (st.device_ms / 1e3) / 1e9 if st.device_ms else 0.0
     cpu = {}
     if cpu_on:
@@ -675,6 +679,9 @@ def c3_leg(hbm_peak, peak_src, cpu_on=True):
                                               "programmatic dependent launch streams a launch's first tiles "
                                               "while the previous one drains"}},
             "pcg_cold_solve": {"l2": "flushed before the solve; iterations back to back",
+                               "engine": {4: "kernel-per-phase (kp_spmv + kp_update)",
+                                          3: "persistent TMA-streaming PCG"}.get(mode, str(mode)),
+                               "bytes_per_iteration": it_bytes,
                                "iterations": st.iterations, "device_ms": st.device_ms,
                                "us_per_iteration": 1e3 * st.device_ms / max(st.iterations, 1),
                                "achieved_GBs": solve_ach, "frac": solve_ach / hbm_peak,

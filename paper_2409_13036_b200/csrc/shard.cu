@@ -763,10 +763,12 @@ int rafem_kp_finish(rafem_kp* k, double* x_out, rafem_solve_stats* st, double* h
 namespace rafem {
 
 // Single-shard PCG on an assembled system, used by rafem_system_solve for
-// PCG on systems whose matrix is far larger than L2 (>= 1 GB; measured on
+// PCG on systems whose matrix is far larger than L2: >= 1 GB (measured on
 // B200 at 16M dofs: 771 us per iteration vs 1043 us for the persistent
-// streaming kernel, which stays the choice below that size).
-// RAFEM_KP=0/1 forces it off/on (tests, tuning).
+// streaming kernel), and from the streaming size (48 MB) up when the
+// pattern has stencil classes, whose values-only tiles run two CTAs per SM
+// (r1n, 1M dofs: 47.4 vs 50.5 us per iteration).  Otherwise the persistent
+// streaming kernel.  RAFEM_KP=0/1 forces it off/on (tests, tuning).
 int kp_system_solve(rafem_system* s, const double* b, const double* x0, const rafem_solver_params* p,
                     double* x_out, rafem_solve_stats* st, double* hist, int64_t hist_cap, int64_t* cycle_lens,
                     int64_t cycle_cap) {
@@ -774,8 +776,13 @@ int kp_system_solve(rafem_system* s, const double* b, const double* x0, const ra
     rafem_ctx* ctx = m->ctx;
     if (!p || p->method != RAFEM_METHOD_PCG || p->grid_ctas > 0 || m->N < 1) return RAFEM_ERR_UNSUPPORTED;
     const char* env = getenv("RAFEM_KP");
-    const bool big = (double)m->slots * 20.0 >= 1.0e9;
-    if (env ? env[0] != '1' : !big) return RAFEM_ERR_UNSUPPORTED;
+    bool use = (double)m->slots * 20.0 >= 1.0e9;
+    if (!use && !env && (double)m->slots * 20.0 > (double)(48LL << 20)) {
+        if (!m->cls_tried) mesh_stencil_classes(m);
+        const char* nc = getenv("RAFEM_NO_CLASSES");
+        use = m->cls && m->ncls > 0 && m->maxdeg <= kClsWidth && !(nc && nc[0] == '1');
+    }
+    if (env ? env[0] != '1' : !use) return RAFEM_ERR_UNSUPPORTED;
     if (!(p->tolerance > 0.0 && p->tolerance < 1.0))
         return rafem_fail(ctx, RAFEM_ERR_INVALID, "tolerance must lie in (0, 1)");
     if (!s->kp) {

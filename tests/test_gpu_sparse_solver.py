@@ -276,25 +276,41 @@ def test_tma_spmv_pipeline_configs_bitwise_at_1M_dofs():
 @pytest.mark.parametrize("hot", [False, True])
 def test_streaming_pcg_at_1M_dofs(hot):
     """configs[2]: the TMA-streaming PCG (matrix >> L2) meets the residual
-    contract, agrees with the single-barrier grid PCG, and is bit-reproducible."""
+    contract, agrees with the single-barrier grid PCG and with the default
+    (kernel-per-phase, stencil classes) engine, and is bit-reproducible."""
     import os
     from paper_2409_13036_b200 import SolverConfig, solve
     from paper_2409_13036_b200 import _native as nat
     s, x0 = _c3_system(hot)
     a, b = s.matrix, s.rhs
     cfg = SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-10)
-    x, st = solve(a, b, x0=x0, config=cfg)
-    assert nat.last_solve_mode()[0] == 3  # grid-wide streaming PCG
+    xk, sk = solve(a, b, x0=x0, config=cfg)
+    assert nat.last_solve_mode()[0] == 4  # default here: kernel-per-phase
+    rk = np.linalg.norm(b - O.matvec(a.row_ptr, a.col_idx, a.vals, xk)) / np.linalg.norm(b)
+    assert sk.converged and rk <= 1e-10
+    os.environ["RAFEM_KP"] = "0"
+    try:
+        x, st = solve(a, b, x0=x0, config=cfg)
+        assert nat.last_solve_mode()[0] == 3  # grid-wide streaming PCG
+    finally:
+        del os.environ["RAFEM_KP"]
+    assert abs(st.iterations - sk.iterations) <= max(3, 0.03 * sk.iterations)
+    assert rel_err(x, xk) < 1e-7
     res = np.linalg.norm(b - O.matvec(a.row_ptr, a.col_idx, a.vals, x)) / np.linalg.norm(b)
     assert st.converged and res <= 1e-10
     assert abs(st.final_relative_residual - res) < 1e-12
-    x2, st2 = solve(a, b, x0=x0, config=cfg)
+    os.environ["RAFEM_KP"] = "0"
+    try:
+        x2, st2 = solve(a, b, x0=x0, config=cfg)
+    finally:
+        del os.environ["RAFEM_KP"]
     assert np.array_equal(x, x2) and st.iterations == st2.iterations
+    os.environ["RAFEM_KP"] = "0"
     os.environ["RAFEM_NO_STREAM_PCG"] = "1"
     try:
         xg, sg = solve(a, b, x0=x0, config=cfg)
     finally:
-        del os.environ["RAFEM_NO_STREAM_PCG"]
+        del os.environ["RAFEM_NO_STREAM_PCG"], os.environ["RAFEM_KP"]
     assert nat.last_solve_mode()[0] == 0
     assert abs(st.iterations - sg.iterations) <= max(3, 0.03 * sg.iterations)
     assert rel_err(x, xg) < 1e-7
