@@ -10,7 +10,7 @@ timeout 1200 python -m pytest tests -q -m gpu --timeout 600 ${PYTEST_ARGS} > gpu
 fi
 timeout 900 python bench.py --steps 5 --warmup 3 ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 if [ -z "$SKIP_NCU" ]; then
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-c4 > gpurun_out/ncu_ll.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-c4 --no-c3 > gpurun_out/ncu_ll.log 2>&1
 PREC=block_jacobi timeout 900 ncu --set full --import-source on --clock-control none -k regex:simulate -c 1 -o gpurun_out/prof_simulate -f python scripts/launch_list.py pcg >> gpurun_out/ncu_ll.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:spmv_tma -s 5 -c 1 -o gpurun_out/prof_spmv_c3 -f python scripts/c3_spmv.py >> gpurun_out/ncu_ll.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:"kp_spmv|kp_update|spmv_tma" -s 10 -c 3 -o gpurun_out/prof_kp_c4 -f python scripts/kp_probe.py >> gpurun_out/ncu_ll.log 2>&1
