@@ -1223,6 +1223,7 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
         }
     };
 
+    bool first_head = true;
     while (true) {
         {  // head: r = b - A x, u = M r ; then w = A u, m = M w ; partials of (r.u, w.u, r.r)
             const bool with_b = bnorm < 0.0;
@@ -1245,7 +1246,9 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                     if (with_b) v[0] = add(v[0], mul(be, be));
                 }
             });
-            if (blk) {
+            // later heads usually end the solve: their block step waits until
+            // the true residual says the iteration continues
+            if (blk && first_head) {
                 __syncthreads();
                 apply_block(r, u, ug);
             }
@@ -1296,6 +1299,12 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
             break;
         }
         if (total >= a.cap) break;
+        if (blk && !first_head) {  // restart on the true residual: u = M r, visible to the SpMV below
+            __syncthreads();
+            apply_block(r, u, ug);
+            sy.barrier();
+        }
+        first_head = false;
         {
             double v[3] = {0.0, 0.0, 0.0};
             double* m = mb(cur);
