@@ -16,8 +16,10 @@
 //     overlapped with the SpMV, owner vectors in shared memory, optional
 //     block-Jacobi), GMRES keeps its own basis rows in shared memory.
 //   * grid mode, global rows: the same bodies reading the matrix from HBM.
-//   * streaming PCG (pcg_stream_kernel, matrices >= 48 MB): rows staged by
-//     TMA bulk copies, materialised preconditioned residual.
+//   * streaming PCG (pcg_stream_kernel, matrices >= 48 MB without stencil
+//     classes): rows staged by TMA bulk copies, materialised preconditioned
+//     residual.  Patterns with stencil classes (and any matrix >= 1 GB) go
+//     to the kernel-per-phase engine in shard.cu instead (kp_system_solve).
 //   * cluster mode (RAFEM_SOLVER_MODE=cluster): one thread-block cluster
 //     with DSMEM barriers; measured slower, kept for experiments.
 //   The kernel-per-phase PCG for the largest and sharded systems lives in
