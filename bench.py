@@ -395,13 +395,6 @@ def run_ours(args):
             line["small_c1"] = c1_leg(args)
         except Exception as exc:  # noqa: BLE001
             line["small_c1"] = {"error": str(exc)[:300]}
-    if not args.no_c4:
-        try:
-            c4 = c4_leg(hbm_peak, peak_src, world, rank, local)
-        except Exception as exc:  # noqa: BLE001
-            c4 = {"error": str(exc)[:300]}
-        if rank == 0:
-            line["sharded_c4"] = c4
     if rank == 0 and not args.no_cpu:
         try:
             smp = cpu_sample(24, {"OPENBLAS_NUM_THREADS": "1", "OMP_NUM_THREADS": "1"})
@@ -412,10 +405,42 @@ def run_ours(args):
                                               "numpy port of rafem 0.1.0, GMRES(30)+Jacobi 1e-10, 1 BLAS thread"}
         except Exception as exc:  # noqa: BLE001
             line["cpu_baseline"] = {"error": str(exc)[:300]}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+    # Multi-GPU jobs: the sharded leg is the only one with collectives on the
+    # data path.  A watchdog on every rank guarantees the line is printed and
+    # the job ends even if a collective never completes.
+    import threading
+    printed = threading.Event()
+
+    def emit():
+        if rank == 0 and not printed.is_set():
+            printed.set()
+            print(json.dumps(line), flush=True)
+
+    def guard(seconds, what):
+        def fire():
+            if rank == 0 and what and "sharded_c4" not in line:
+                line["sharded_c4"] = {"error": what}
+            emit()
+            os._exit(0)
+        t = threading.Timer(seconds, fire)
+        t.daemon = True
+        if world > 1:
+            t.start()
+        return t
+
+    if not args.no_c4:
+        wd = guard(480, "sharded leg did not finish within 480 s (watchdog)")
+        try:
+            c4 = c4_leg(hbm_peak, peak_src, world, rank, local)
+        except Exception as exc:  # noqa: BLE001
+            c4 = {"error": str(exc)[:300]}
+        wd.cancel()
+        if rank == 0:
+            line["sharded_c4"] = c4
+    emit()
     if world > 1:
         import torch.distributed as dist
+        guard(120, None)  # teardown must not hang the job either
         try:
             dist.barrier()
             dist.destroy_process_group()
