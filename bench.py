@@ -67,6 +67,12 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", "1")))
 
 
+# RAFEM_BENCH_BACKEND=gloo (testing only): ranks may share a GPU and the
+# sharded leg stages its collectives through host memory; the job's numbers
+# are then not a multi-GPU measurement.
+BACKEND = os.environ.get("RAFEM_BENCH_BACKEND", "nccl")
+
+
 # ---------------------------------------------------------------------------
 # clocks sampled during the timed region
 
@@ -262,13 +268,15 @@ def gmres_iter_bytes(N, S, k_avg):
 def run_ours(args):
     import torch
     rank, local, world = dist_env()
+    if BACKEND != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     os.environ["RAFEM_DEVICE"] = str(local)
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
         import datetime
         # a collective that never completes aborts the job instead of hanging it
-        dist.init_process_group("nccl", init_method="env://", timeout=datetime.timedelta(seconds=600))
+        dist.init_process_group(BACKEND, init_method="env://", timeout=datetime.timedelta(seconds=600))
     from paper_2409_13036_b200 import _native as nat
     from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh, run_simulation
     from paper_2409_13036_b200.timeloop import DeviceRun
@@ -378,13 +386,15 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
 
-    if rank == 0 and not args.no_e2e:
-        line["e2e"] = e2e_leg(mesh, mat, args, SimConfig, SolverConfig, world)
-        line["e2e_plugin_seam"] = e2e_plugin_leg(mesh, mat, args, run_simulation, SimConfig, SolverConfig, world)
+    if not args.no_e2e:  # every rank runs its replica; the legs take the max wall over ranks
+        e2e = e2e_leg(mesh, mat, args, SimConfig, SolverConfig, world)
+        seam = e2e_plugin_leg(mesh, mat, args, run_simulation, SimConfig, SolverConfig, world)
         # the reference's own solver configuration through the seam: device GMRES(30) + Jacobi
         ga = argparse.Namespace(**vars(args))
         ga.backend, ga.steps = "gmres", 1
-        line["e2e_plugin_seam_gmres"] = e2e_plugin_leg(mesh, mat, ga, run_simulation, SimConfig, SolverConfig, world)
+        seam_g = e2e_plugin_leg(mesh, mat, ga, run_simulation, SimConfig, SolverConfig, world)
+        if rank == 0:
+            line["e2e"], line["e2e_plugin_seam"], line["e2e_plugin_seam_gmres"] = e2e, seam, seam_g
     if rank == 0 and not args.no_c3:
         try:
             line["spmv_c3"] = c3_leg(hbm_peak, peak_src, cpu_on=not args.no_cpu)
@@ -448,6 +458,23 @@ def run_ours(args):
             pass
 
 
+def _job_wall(wall, world):
+    """Max of a wall-clock interval over the job's ranks (NCCL all-reduce)."""
+    if world <= 1:
+        return wall
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([wall], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _align(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
 def e2e_leg(mesh, mat, args, SimConfig, SolverConfig, world):
     """Same metric end to end through the public whole-simulation API
     (simulate_device -> rafem_mesh_create + rafem_simulate): every step
@@ -464,14 +491,16 @@ def e2e_leg(mesh, mat, args, SimConfig, SolverConfig, world):
 
     one()  # warm
     reps = max(1, args.steps)
+    _align(world)
     t0 = time.perf_counter()
     for _ in range(reps):
         recs, summ = one()
-    wall = time.perf_counter() - t0
+    wall = _job_wall(time.perf_counter() - t0, world)
     N, M = mesh.node_count, mesh.tet_count
     h2d = 8 * 3 * N + 8 * 4 * M + 4 * M + 2 * N + 5 * 8  # nodes f64, tets i64, region idx i32, dof kinds u8, tables
     d2h = len(recs) * (16 * N + 8 + 8 + 8 + 4) + 128  # per accepted step: V/T fields, step/time/dt/iters; summary
-    return {"value": int(summ.accepted_steps) * reps / wall, "unit": "steps/s", "h2d_bytes_per_step": h2d,
+    # whole job: every rank runs its own simulation (replicas), slowest rank's wall
+    return {"value": world * int(summ.accepted_steps) * reps / wall, "unit": "steps/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "reps": reps,
             "path": "DeviceRun(cached=False).run_streamed: host mesh -> rafem_mesh_create -> "
                     "rafem_simulate_stream -> host fields of every accepted step, streamed while the kernel runs "
@@ -484,16 +513,17 @@ def e2e_plugin_leg(mesh, mat, args, run_simulation, SimConfig, SolverConfig, wor
     cfg = SimConfig(total_time=TOTAL_TIME, solver=SolverConfig(backend=args.backend, precondition=prec_of(args)))
     run_simulation(mesh, mat, cfg)  # warm (mesh upload + symbolic phase cached)
     reps = max(1, min(args.steps, 3))
+    _align(world)
     t0 = time.perf_counter()
     for _ in range(reps):
         summ = run_simulation(mesh, mat, cfg)
-    wall = time.perf_counter() - t0
+    wall = _job_wall(time.perf_counter() - t0, world)
     N = mesh.node_count
     passes = summ.total_corrector_iters
     # per pass: H2D t_iter, v_iter, t_prev (3N f64) + b, x0 (2 x 2N f64); D2H rhs + x (2 x 2N f64)
     h2d = passes * 8 * (3 * N + 4 * N)
     d2h = passes * 8 * (4 * N) + passes * 16
-    return {"value": summ.accepted_steps * reps / wall, "unit": "steps/s", "h2d_bytes_per_step": h2d,
+    return {"value": world * summ.accepted_steps * reps / wall, "unit": "steps/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "reps": reps,
             "path": "run_simulation -> assemble_global -> solve (host numpy in/out every pass)"}
 
@@ -555,7 +585,7 @@ def c4_leg(hbm_peak, peak_src, world, rank, local):
     comm = None
     if world > 1:
         stream = torch.cuda.ExternalStream(nat.lib().rafem_stream(nat.context()))
-        comm = ShardComm(device_collectives=True, stream=stream)
+        comm = ShardComm(device_collectives=BACKEND == "nccl", stream=stream)
     sh = ShardedSystem(mesh, MaterialParams.default(), comm, batch=16)
     p = sh.plan
     tt = np.full(n, 37.0)
@@ -606,7 +636,9 @@ def c4_leg(hbm_peak, peak_src, world, rank, local):
     ach = it * bytes_it / (dev_ms / 1e3) / 1e9 if dev_ms > 0 else 0.0
     return {"workload": "generate_box_mesh(200,200,200) cold system, 16,000,000 dofs",
             "shards": world, "partition": "contiguous node-row blocks (x-slabs)",
-            "collectives": "NCCL halo send/recv + per-shard scalar all-gather" if world > 1 else "none (one shard)",
+            "collectives": ("none (one shard)" if world == 1 else
+                            "NCCL halo send/recv + per-shard scalar all-gather" if BACKEND == "nccl" else
+                            f"host-staged {BACKEND} (test backend, ranks may share a GPU)"),
             "iterations": it, "converged": bool(st.converged), "final_relative_residual": st.final_relative_residual,
             "solve_device_ms_max_over_ranks": dev_ms, "solve_wall_ms": wall_ms,
             "us_per_iteration": 1e3 * dev_ms / max(it, 1),
