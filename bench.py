@@ -668,6 +668,13 @@ def c3_leg(hbm_peak, peak_src, cpu_on=True):
     os.environ["RAFEM_NO_PDL"] = "1"
     nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 1000, 0, C.byref(ms_b2b_plain)), "spmv bench")
     del os.environ["RAFEM_NO_PDL"]
+    b2b_dram = None  # DRAM bytes of one launch inside a back-to-back chain (committed ncu capture)
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1k_spmv_c3_back_to_back_ncu.txt")) as fh:
+            rows = [ln.split() for ln in fh if ln[:1].isdigit()]
+        b2b_dram = sum(int(r[1]) + int(r[2]) for r in rows) / len(rows) if rows else None
+    except (OSError, ValueError, IndexError):
+        pass
     os.environ["RAFEM_NO_TMA_SPMV"] = "1"
     ms_plain = C.c_double()
     nat.check(nat.lib().rafem_system_spmv_bench(h.handle, 50, 1, C.byref(ms_plain)), "spmv bench")
@@ -732,9 +739,16 @@ def c3_leg(hbm_peak, peak_src, cpu_on=True):
                                       "achieved": b_paired / (ms_b2b.value / 1e3) / 1e9,
                                       "frac": b_paired / (ms_b2b.value / 1e3) / 1e9 / hbm_peak,
                                       "us_per_launch_without_pdl": 1e3 * ms_b2b_plain.value,
-                                      "note": "no flush between launches (the matrix stream exceeds L2); "
-                                              "programmatic dependent launch streams a launch's first tiles "
-                                              "while the previous one drains"}},
+                                      "dram_bytes_per_launch": b2b_dram,
+                                      "dram_GBs": (b2b_dram / (ms_b2b.value / 1e3) / 1e9) if b2b_dram else None,
+                                      "dram_frac": (b2b_dram / (ms_b2b.value / 1e3) / 1e9 / hbm_peak)
+                                      if b2b_dram else None,
+                                      "protocol": "SURVEY 8(d) C3: 1,000 back-to-back SpMVs; the 137 MB matrix "
+                                                  "stream exceeds the 126 MB L2, x (8 MB) stays L2-resident",
+                                      "note": "no flush between launches; programmatic dependent launch streams "
+                                              "a launch's first tiles while the previous one drains; DRAM bytes per "
+                                              "launch from ncu inside such a chain "
+                                              "(profiles/r1k_spmv_c3_back_to_back_ncu.txt)"}},
             "pcg_cold_solve": {"l2": "flushed before the solve; iterations back to back",
                                "engine": {4: "kernel-per-phase (kp_spmv + kp_update)",
                                           3: "persistent TMA-streaming PCG"}.get(mode, str(mode)),
