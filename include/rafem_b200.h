@@ -136,6 +136,10 @@ void* rafem_stream(const rafem_ctx* ctx);
  * and CTA count; per-iteration phase timestamps (SM clock64) of CTA 0 when
  * tracing is on: 8 slots per iteration, returns entries copied */
 int rafem_last_solve_mode(const rafem_ctx* ctx, int32_t* mode, int32_t* ctas);
+/* preconditioner the last solve (or fused simulation) actually applied,
+ * RAFEM_PRECOND_*: block-Jacobi exists only in the paper-scale pipelined
+ * PCG; the other engines and GMRES apply point Jacobi when it is requested */
+int rafem_last_solve_precond(const rafem_ctx* ctx, int32_t* precond);
 int rafem_set_trace(rafem_ctx* ctx, int32_t on);
 int64_t rafem_get_trace(rafem_ctx* ctx, int64_t* out, int64_t cap);
 

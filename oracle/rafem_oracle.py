@@ -540,11 +540,13 @@ class ORun:
     wall_s: float
 
 
-def run(mesh: OMesh, materials: dict, cfg: OSim, keep_fields=True, max_steps=None) -> ORun:
+def run(mesh: OMesh, materials: dict, cfg: OSim, keep_fields=True, max_steps=None, on_step=None) -> ORun:
     """Adaptive predictor-corrector loop (fem.py:554-644, 463-540).
 
     ``max_steps`` stops after that many accepted steps (a bounded sample
     of the workload for CPU timing); ``None`` runs to ``total_time``.
+    ``on_step(record)`` is called per accepted step, like the reference's
+    ``sink`` (fem.py:609-610).
     """
     t0 = time.perf_counter()
     N = mesh.node_count
@@ -598,6 +600,8 @@ def run(mesh: OMesh, materials: dict, cfg: OSim, keep_fields=True, max_steps=Non
             t = cfg.total_time if last else t + dt
             recs.append(ORecord(step, t, dt, used, T if keep_fields else None,
                                 V if keep_fields else None))
+            if on_step is not None:
+                on_step(recs[-1])
             step += 1
             if used <= 5:
                 dt_cur = min(dt * 1.5, cfg.dt_max)

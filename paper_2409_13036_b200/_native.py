@@ -80,6 +80,7 @@ _SIGS = {
     "rafem_kernel_launches": (i64, [vp]),
     "rafem_stream": (vp, [vp]),
     "rafem_last_solve_mode": (i32, [vp, P(i32), P(i32)]),
+    "rafem_last_solve_precond": (i32, [vp, P(i32)]),
     "rafem_set_trace": (i32, [vp, i32]),
     "rafem_get_trace": (i64, [vp, vp, i64]),
     "rafem_spmv": (i32, [vp, i64, i64, i64, vp, vp, vp, vp, vp]),
@@ -183,6 +184,17 @@ def last_solve_mode() -> tuple[int, int]:
     mode, ctas = i32(), i32()
     check(lib().rafem_last_solve_mode(context(), C.byref(mode), C.byref(ctas)), "last_solve_mode")
     return mode.value, ctas.value
+
+
+PRECOND_NAMES = {PRECOND_NONE: "none", PRECOND_JACOBI: "jacobi", PRECOND_BLOCK_JACOBI: "block_jacobi"}
+
+
+def last_solve_precond() -> str:
+    """Preconditioner the last solve actually applied ("none", "jacobi",
+    "block_jacobi"; block-Jacobi only exists in the paper-scale pipelined PCG)."""
+    v = i32()
+    check(lib().rafem_last_solve_precond(context(), C.byref(v)), "last_solve_precond")
+    return PRECOND_NAMES.get(v.value, "none")
 
 
 def device_info() -> dict:

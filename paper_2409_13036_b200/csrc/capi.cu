@@ -291,6 +291,12 @@ int rafem_last_solve_mode(const rafem_ctx* ctx, int32_t* mode, int32_t* ctas) {
     return RAFEM_OK;
 }
 
+int rafem_last_solve_precond(const rafem_ctx* ctx, int32_t* precond) {
+    if (!ctx || !precond) return RAFEM_ERR_INVALID;
+    *precond = ctx->last_precond;
+    return RAFEM_OK;
+}
+
 int rafem_set_trace(rafem_ctx* ctx, int32_t on) {
     if (!ctx) return RAFEM_ERR_INVALID;
     ctx->trace_on = on ? 1 : 0;
@@ -766,147 +772,67 @@ int pump_records(void* u) {
     return RAFEM_OK;
 }
 
-}  // namespace
 
-int rafem_simulate_stream(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary* out, int32_t ring_slots,
-                          rafem_record_fn fn, void* user) {
-    if (!s || !p || !out || ring_slots < 1) return RAFEM_ERR_INVALID;
-    rafem_mesh* m = s->mesh;
-    rafem_ctx* ctx = m->ctx;
-    std::memset(out, 0, sizeof(*out));
-    out->failed_step = -1;
-    out->bad_element = -1;
-    if (int rc = check_sim(ctx, p)) return rc;
-    const auto t_wall = std::chrono::steady_clock::now();
-    const size_t n2 = 2 * (size_t)m->N;
-    const char* nofused = getenv("RAFEM_NO_FUSED");
-    if (p->solver.method == RAFEM_METHOD_PCG && !(nofused && nofused[0] == '1')) {
-        StreamPump P{};
-        P.ctx = ctx;
-        P.slots = ring_slots;
-        P.rec_doubles = n2 + 4;
-        P.fn = fn;
-        P.user = user;
-        double* ring = nullptr;
-        long long* dcounters = nullptr;
-        auto cleanup = [&]() {
-            if (ring) dfree(ctx, ring);
-        };
-        // ring from the context cache; side stream, mapped counters and the
-        // pinned record buffer are created once per context
-        cudaError_t e = dmalloc(ctx, reinterpret_cast<void**>(&ring), sizeof(double) * P.rec_doubles * ring_slots);
-        if (e == cudaSuccess && !ctx->mapped)
-            e = cudaHostAlloc(reinterpret_cast<void**>(&ctx->mapped), 2 * sizeof(long long), cudaHostAllocMapped);
-        if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&dcounters), ctx->mapped, 0);
-        if (e == cudaSuccess && !ctx->side_stream) e = cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking);
-        P.hbuf = e == cudaSuccess ? static_cast<double*>(pinned(ctx, sizeof(double) * P.rec_doubles)) : nullptr;
-        if (e == cudaSuccess && !P.hbuf) e = cudaErrorMemoryAllocation;
-        if (e != cudaSuccess) {
-            cleanup();
-            return rafem_fail_cuda(ctx, e, "record stream setup", __FILE__, __LINE__);
-        }
-        long long* counters = ctx->mapped;
-        P.copy = ctx->side_stream;
-        counters[0] = 0;
-        counters[1] = 0;
-        P.ring = ring;
-        P.prog = counters;
-        P.cons = counters + 1;
-        SimStream ss{ring, ring_slots, dcounters, dcounters + 1, pump_records, &P};
-        SimDevOut so{};
-        float kms = 0.f;
-        const int frc = simulate_fused(s, p, &so, nullptr, nullptr, nullptr, nullptr, 0, s->xs + 5 * n2, &kms, &ss);
-        if (frc == RAFEM_OK && P.consumed < so.accepted) pump_records(&P);  // drain (kernel is done)
-        const int cb = P.cb_status;
-        cleanup();
-        if (frc == RAFEM_OK) {
-            const int rc = fused_summary(ctx, so, t_wall, out);
-            if (cb) return rafem_fail(ctx, RAFEM_ERR_INVALID, "record sink failed");
-            return rc;
-        }
-        if (frc != RAFEM_ERR_UNSUPPORTED) return frc;
+// rafem_simulate's record sink: the first rec_cap steps into the caller's arrays
+struct RecordArrays {
+    long long cap;
+    int64_t* step;
+    double* time;
+    double* dt;
+    int32_t* iters;
+    double* x;
+    size_t n2;
+    cudaStream_t st;
+};
+
+int record_to_arrays(void* u, long long step, double t, double dt, int iters, const double* xacc) {
+    auto& R = *static_cast<RecordArrays*>(u);
+    if (step >= R.cap) return 0;
+    if (R.step) R.step[step] = step;
+    if (R.time) R.time[step] = t;
+    if (R.dt) R.dt[step] = dt;
+    if (R.iters) R.iters[step] = iters;
+    if (R.x) {
+        const cudaError_t e = cudaMemcpyAsync(R.x + (size_t)step * R.n2, xacc, sizeof(double) * R.n2,
+                                              cudaMemcpyDeviceToHost, R.st);
+        if (e != cudaSuccess) return RAFEM_ERR_CUDA;
     }
-    // not eligible for the fused kernel: run, then hand the records over
-    const long long cap = std::min<long long>((long long)(2.0 * p->total_time / p->dt_init) + 64,
-                                              std::max<long long>(1, (long long)(8e9 / (8.0 * std::max<size_t>(n2, 1)))));
-    std::vector<int64_t> rs(cap);
-    std::vector<double> rt(cap), rd(cap), rx((size_t)cap * n2);
-    std::vector<int32_t> ri(cap);
-    rafem_sim_params q = *p;
-    q.record_fields = 1;
-    const int rc = rafem_simulate(s, &q, out, cap, rs.data(), rt.data(), rd.data(), ri.data(), rx.data());
-    const long long nrec = std::min<long long>(out->accepted_steps, cap);
-    std::vector<double> rec(n2);
-    for (long long k = 0; k < nrec && fn; ++k)
-        if (fn(user, k, rt[k], rd[k], ri[k], rx.data() + (size_t)k * n2)) {
-            if (rc == RAFEM_OK) return rafem_fail(ctx, RAFEM_ERR_INVALID, "record sink failed");
-            break;
-        }
-    return rc;
+    return 0;
 }
 
-int rafem_simulate(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary* out, int64_t rec_cap,
-                   int64_t* rec_step, double* rec_time, double* rec_dt, int32_t* rec_iters, double* rec_x) {
-    if (!s || !p || !out) return RAFEM_ERR_INVALID;
+// rafem_simulate_stream's sink on the per-pass loop: each accepted state
+// through one pinned record buffer straight to the caller's fn
+struct RecordStream {
+    rafem_ctx* ctx;
+    double* hbuf;  // pinned, 2N
+    size_t n2;
+    rafem_record_fn fn;
+    void* user;
+};
+
+int record_to_stream(void* u, long long step, double t, double dt, int iters, const double* xacc) {
+    auto& R = *static_cast<RecordStream*>(u);
+    if (cudaMemcpyAsync(R.hbuf, xacc, sizeof(double) * R.n2, cudaMemcpyDeviceToHost, R.ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(R.ctx->stream) != cudaSuccess)
+        return RAFEM_ERR_CUDA;
+    return R.fn ? (R.fn(R.user, step, t, dt, (int32_t)iters, R.hbuf) ? 1 : 0) : 0;
+}
+
+// Per-pass native loop (the fallback when the fused kernel does not apply,
+// e.g. GMRES): every accepted step's device state xacc (2N dofs) is handed
+// to fn as it is accepted — a record costs 2N doubles of host memory only
+// for as long as fn holds it.  fn returns 0, a CUDA status (< 0, aborts)
+// or > 0 (the sink refused: delivery stops, the run completes, the call
+// returns RAFEM_ERR_INVALID).
+using AcceptFn = int (*)(void* u, long long step, double t, double dt, int iters, const double* xacc_dev);
+
+int simulate_host_loop(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary* out,
+                       std::chrono::steady_clock::time_point t_wall, AcceptFn fn, void* u) {
     rafem_mesh* m = s->mesh;
     rafem_ctx* ctx = m->ctx;
-    std::memset(out, 0, sizeof(*out));
-    out->failed_step = -1;
-    out->bad_element = -1;
-    if (int rc = check_sim(ctx, p)) return rc;
-    const auto t_wall = std::chrono::steady_clock::now();
     const int N = m->N;
     const size_t n2 = 2 * (size_t)N;
     cudaStream_t st = ctx->stream;
-
-    // Preferred path: the whole simulation in one persistent kernel (PCG).
-    const char* nofused = getenv("RAFEM_NO_FUSED");
-    if (p->solver.method == RAFEM_METHOD_PCG && !(nofused && nofused[0] == '1')) {
-        const long long cap = std::max<long long>(rec_cap, 0);
-        double* d_rx = nullptr;
-        double* d_rt = nullptr;
-        double* d_rd = nullptr;
-        int* d_ri = nullptr;
-        // record buffers from the context's allocation cache: the field buffer
-        // is sized for the caller's capacity (hundreds of MB for a 900 s run),
-        // and a cudaMalloc / cudaFree pair of that size per call cost more
-        // than the simulation itself (45 vs 26 ms per mesh-B run)
-        auto release = [&]() {
-            for (void* q : {(void*)d_rx, (void*)d_rt, (void*)d_rd, (void*)d_ri})
-                if (q) dfree(ctx, q);
-        };
-        if (cap > 0) {
-            RF_CUDA_TRY(ctx, dmalloc(ctx, reinterpret_cast<void**>(&d_rt), sizeof(double) * cap));
-            RF_CUDA_TRY(ctx, dmalloc(ctx, reinterpret_cast<void**>(&d_rd), sizeof(double) * cap));
-            RF_CUDA_TRY(ctx, dmalloc(ctx, reinterpret_cast<void**>(&d_ri), sizeof(int) * cap));
-            if (p->record_fields && rec_x)
-                RF_CUDA_TRY(ctx, dmalloc(ctx, reinterpret_cast<void**>(&d_rx), sizeof(double) * n2 * cap));
-        }
-        SimDevOut so{};
-        float kms = 0.f;
-        const int frc = simulate_fused(s, p, &so, d_rx, d_rt, d_rd, d_ri, cap, s->xs + 5 * n2, &kms);
-        if (frc == RAFEM_OK) {
-            const long long nrec = std::min<long long>(so.accepted, cap);
-            if (nrec > 0) {
-                std::vector<double> ht(nrec), hd(nrec);
-                std::vector<int> hi(nrec);
-                RF_CUDA_TRY(ctx, cudaMemcpy(ht.data(), d_rt, sizeof(double) * nrec, cudaMemcpyDeviceToHost));
-                RF_CUDA_TRY(ctx, cudaMemcpy(hd.data(), d_rd, sizeof(double) * nrec, cudaMemcpyDeviceToHost));
-                RF_CUDA_TRY(ctx, cudaMemcpy(hi.data(), d_ri, sizeof(int) * nrec, cudaMemcpyDeviceToHost));
-                for (long long k = 0; k < nrec; ++k) {
-                    if (rec_step) rec_step[k] = k;
-                    if (rec_time) rec_time[k] = ht[k];
-                    if (rec_dt) rec_dt[k] = hd[k];
-                    if (rec_iters) rec_iters[k] = hi[k];
-                }
-                if (d_rx) RF_CUDA_TRY(ctx, cudaMemcpy(rec_x, d_rx, sizeof(double) * n2 * nrec, cudaMemcpyDeviceToHost));
-            }
-            release();
-            return fused_summary(ctx, so, t_wall, out);
-        }
-        release();
-        if (frc != RAFEM_ERR_UNSUPPORTED) return frc;
-    }
     double* xacc = s->xs;            // accepted (V, T)
     double* xprev = s->xs + n2;      // accepted one step earlier
     double* xit = s->xs + 2 * n2;    // current iterate (x_old)
@@ -922,6 +848,7 @@ int rafem_simulate(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary
     ap.apply_constraints = 1;
     ap.equilibrate = 1;
 
+    bool rec_failed = false;
     double t = 0.0, dt_state = p->dt_init, dt_prev = p->dt_init;
     long long step = 0, passes = 0, total_corr = 0, total_inner = 0, halvings = 0;
     double asm_ms = 0.0, sol_ms = 0.0;
@@ -992,15 +919,11 @@ int rafem_simulate(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary
             xit = old_prev;
             dt_prev = dt;
             t = final_step ? p->total_time : t + dt;
-            if (step < rec_cap) {
-                if (rec_step) rec_step[step] = step;
-                if (rec_time) rec_time[step] = t;
-                if (rec_dt) rec_dt[step] = dt;
-                if (rec_iters) rec_iters[step] = iters;
-                if (p->record_fields && rec_x)
-                    RF_CUDA_TRY(ctx, cudaMemcpyAsync(rec_x + (size_t)step * n2, xacc, sizeof(double) * n2,
-                                                     cudaMemcpyDeviceToHost, st));
-            }
+            if (fn && !rec_failed)
+                if (int rc = fn(u, step, t, dt, iters, xacc)) {
+                    if (rc < 0) return rc;  // CUDA error while handing the record over
+                    rec_failed = true;      // the sink refused: stop delivering, finish the run
+                }
             ++step;
             if (iters <= 5)
                 dt_state = std::min(dt * 1.5, p->dt_max);
@@ -1043,7 +966,141 @@ int rafem_simulate(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary
                       out->failed_step, out->failed_dt);
         return rafem_fail(ctx, status, buf);
     }
+    if (status == RAFEM_OK && rec_failed) return rafem_fail(ctx, RAFEM_ERR_INVALID, "record sink failed");
     return status;
+}
+
+}  // namespace
+
+int rafem_simulate_stream(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary* out, int32_t ring_slots,
+                          rafem_record_fn fn, void* user) {
+    if (!s || !p || !out || ring_slots < 1) return RAFEM_ERR_INVALID;
+    rafem_mesh* m = s->mesh;
+    rafem_ctx* ctx = m->ctx;
+    std::memset(out, 0, sizeof(*out));
+    out->failed_step = -1;
+    out->bad_element = -1;
+    if (int rc = check_sim(ctx, p)) return rc;
+    const auto t_wall = std::chrono::steady_clock::now();
+    const size_t n2 = 2 * (size_t)m->N;
+    const char* nofused = getenv("RAFEM_NO_FUSED");
+    if (p->solver.method == RAFEM_METHOD_PCG && !(nofused && nofused[0] == '1')) {
+        StreamPump P{};
+        P.ctx = ctx;
+        P.slots = ring_slots;
+        P.rec_doubles = n2 + 4;
+        P.fn = fn;
+        P.user = user;
+        double* ring = nullptr;
+        long long* dcounters = nullptr;
+        auto cleanup = [&]() {
+            if (ring) dfree(ctx, ring);
+        };
+        // ring from the context cache; side stream, mapped counters and the
+        // pinned record buffer are created once per context
+        cudaError_t e = dmalloc(ctx, reinterpret_cast<void**>(&ring), sizeof(double) * P.rec_doubles * ring_slots);
+        if (e == cudaSuccess && !ctx->mapped)
+            e = cudaHostAlloc(reinterpret_cast<void**>(&ctx->mapped), 2 * sizeof(long long), cudaHostAllocMapped);
+        if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&dcounters), ctx->mapped, 0);
+        if (e == cudaSuccess && !ctx->side_stream) e = cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking);
+        P.hbuf = e == cudaSuccess ? static_cast<double*>(pinned(ctx, sizeof(double) * P.rec_doubles)) : nullptr;
+        if (e == cudaSuccess && !P.hbuf) e = cudaErrorMemoryAllocation;
+        if (e != cudaSuccess) {
+            cleanup();
+            return rafem_fail_cuda(ctx, e, "record stream setup", __FILE__, __LINE__);
+        }
+        long long* counters = ctx->mapped;
+        P.copy = ctx->side_stream;
+        counters[0] = 0;
+        counters[1] = 0;
+        P.ring = ring;
+        P.prog = counters;
+        P.cons = counters + 1;
+        SimStream ss{ring, ring_slots, dcounters, dcounters + 1, pump_records, &P};
+        SimDevOut so{};
+        float kms = 0.f;
+        const int frc = simulate_fused(s, p, &so, nullptr, nullptr, nullptr, nullptr, 0, s->xs + 5 * n2, &kms, &ss);
+        if (frc == RAFEM_OK && P.consumed < so.accepted) pump_records(&P);  // drain (kernel is done)
+        const int cb = P.cb_status;
+        cleanup();
+        if (frc == RAFEM_OK) {
+            const int rc = fused_summary(ctx, so, t_wall, out);
+            if (cb) return rafem_fail(ctx, RAFEM_ERR_INVALID, "record sink failed");
+            return rc;
+        }
+        if (frc != RAFEM_ERR_UNSUPPORTED) return frc;
+    }
+    // not eligible for the fused kernel: the per-pass loop hands each
+    // accepted step to fn as it is accepted (bounded memory at any size)
+    RecordStream rs{ctx, static_cast<double*>(pinned(ctx, sizeof(double) * n2)), n2, fn, user};
+    if (!rs.hbuf) return rafem_fail(ctx, RAFEM_ERR_CUDA, "pinned record buffer");
+    return simulate_host_loop(s, p, out, t_wall, record_to_stream, &rs);
+}
+
+int rafem_simulate(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary* out, int64_t rec_cap,
+                   int64_t* rec_step, double* rec_time, double* rec_dt, int32_t* rec_iters, double* rec_x) {
+    if (!s || !p || !out) return RAFEM_ERR_INVALID;
+    rafem_mesh* m = s->mesh;
+    rafem_ctx* ctx = m->ctx;
+    std::memset(out, 0, sizeof(*out));
+    out->failed_step = -1;
+    out->bad_element = -1;
+    if (int rc = check_sim(ctx, p)) return rc;
+    const auto t_wall = std::chrono::steady_clock::now();
+    const int N = m->N;
+    const size_t n2 = 2 * (size_t)N;
+    cudaStream_t st = ctx->stream;
+
+    // Preferred path: the whole simulation in one persistent kernel (PCG).
+    const char* nofused = getenv("RAFEM_NO_FUSED");
+    if (p->solver.method == RAFEM_METHOD_PCG && !(nofused && nofused[0] == '1')) {
+        const long long cap = std::max<long long>(rec_cap, 0);
+        double* d_rx = nullptr;
+        double* d_rt = nullptr;
+        double* d_rd = nullptr;
+        int* d_ri = nullptr;
+        // record buffers from the context's allocation cache: the field buffer
+        // is sized for the caller's capacity (hundreds of MB for a 900 s run),
+        // and a cudaMalloc / cudaFree pair of that size per call cost more
+        // than the simulation itself (45 vs 26 ms per mesh-B run)
+        auto release = [&]() {
+            for (void* q : {(void*)d_rx, (void*)d_rt, (void*)d_rd, (void*)d_ri})
+                if (q) dfree(ctx, q);
+        };
+        if (cap > 0) {
+            RF_CUDA_TRY(ctx, dmalloc(ctx, reinterpret_cast<void**>(&d_rt), sizeof(double) * cap));
+            RF_CUDA_TRY(ctx, dmalloc(ctx, reinterpret_cast<void**>(&d_rd), sizeof(double) * cap));
+            RF_CUDA_TRY(ctx, dmalloc(ctx, reinterpret_cast<void**>(&d_ri), sizeof(int) * cap));
+            if (p->record_fields && rec_x)
+                RF_CUDA_TRY(ctx, dmalloc(ctx, reinterpret_cast<void**>(&d_rx), sizeof(double) * n2 * cap));
+        }
+        SimDevOut so{};
+        float kms = 0.f;
+        const int frc = simulate_fused(s, p, &so, d_rx, d_rt, d_rd, d_ri, cap, s->xs + 5 * n2, &kms);
+        if (frc == RAFEM_OK) {
+            const long long nrec = std::min<long long>(so.accepted, cap);
+            if (nrec > 0) {
+                std::vector<double> ht(nrec), hd(nrec);
+                std::vector<int> hi(nrec);
+                RF_CUDA_TRY(ctx, cudaMemcpy(ht.data(), d_rt, sizeof(double) * nrec, cudaMemcpyDeviceToHost));
+                RF_CUDA_TRY(ctx, cudaMemcpy(hd.data(), d_rd, sizeof(double) * nrec, cudaMemcpyDeviceToHost));
+                RF_CUDA_TRY(ctx, cudaMemcpy(hi.data(), d_ri, sizeof(int) * nrec, cudaMemcpyDeviceToHost));
+                for (long long k = 0; k < nrec; ++k) {
+                    if (rec_step) rec_step[k] = k;
+                    if (rec_time) rec_time[k] = ht[k];
+                    if (rec_dt) rec_dt[k] = hd[k];
+                    if (rec_iters) rec_iters[k] = hi[k];
+                }
+                if (d_rx) RF_CUDA_TRY(ctx, cudaMemcpy(rec_x, d_rx, sizeof(double) * n2 * nrec, cudaMemcpyDeviceToHost));
+            }
+            release();
+            return fused_summary(ctx, so, t_wall, out);
+        }
+        release();
+        if (frc != RAFEM_ERR_UNSUPPORTED) return frc;
+    }
+    RecordArrays ra{rec_cap, rec_step, rec_time, rec_dt, rec_iters, p->record_fields ? rec_x : nullptr, n2, st};
+    return simulate_host_loop(s, p, out, t_wall, record_to_arrays, &ra);
 }
 
 }  // extern "C"

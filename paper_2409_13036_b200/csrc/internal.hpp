@@ -114,6 +114,7 @@ struct rafem_ctx {
     long long* mapped = nullptr;         // 2 mapped host counters (record stream)
     int last_mode = -1;  // 1: cluster-resident solve, 0: grid-wide cooperative solve
     int last_ctas = 0;
+    int last_precond = -1;  // preconditioner the last solve applied (RAFEM_PRECOND_*)
     int last_team = 0;
     bool spmv_pdl = false;  // streaming SpMV launched with programmatic dependent launch (back-to-back bench)
 };

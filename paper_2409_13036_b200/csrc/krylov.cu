@@ -2627,6 +2627,7 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
         a.pipe = (!gm && A.W == 2 && !cluster && ms != 3 && rows_per_cta <= kPipeRows && !(pe && pe[0] == '0'))
                      ? 1 : 0;
         a.block = (a.pipe && p.precondition == RAFEM_PRECOND_BLOCK_JACOBI && A.maxdeg > 0 && A.maxdeg <= 32) ? 1 : 0;
+        ctx->last_precond = a.block ? RAFEM_PRECOND_BLOCK_JACOBI : (pre ? RAFEM_PRECOND_JACOBI : RAFEM_PRECOND_NONE);
     }
     if (cluster) smem = (size_t)a.hess_smem * 8 + part.max_slice;
     void* args[] = {&a};
@@ -2824,6 +2825,7 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     {
         a.pipe = pipe ? 1 : 0;
         a.block = (a.pipe && p->solver.precondition == RAFEM_PRECOND_BLOCK_JACOBI && mesh->maxdeg <= 32) ? 1 : 0;
+        ctx->last_precond = a.block ? RAFEM_PRECOND_BLOCK_JACOBI : (pre ? RAFEM_PRECOND_JACOBI : RAFEM_PRECOND_NONE);
     }
     // slot-major element outputs for the cp.async fill (RAFEM_NO_SLOT_MAJOR=1: tet-major)
     const char* nsm = getenv("RAFEM_NO_SLOT_MAJOR");

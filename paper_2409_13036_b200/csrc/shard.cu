@@ -853,6 +853,7 @@ int kp_system_solve(rafem_system* s, const double* b, const double* x0, const ra
     }
     ctx->last_mode = 4;
     ctx->last_ctas = k->g_spmv;
+    ctx->last_precond = p->precondition != RAFEM_PRECOND_NONE ? RAFEM_PRECOND_JACOBI : RAFEM_PRECOND_NONE;
     const int status = rafem_kp_finish(k, x_out, st, hist, hist_cap, cycle_lens, cycle_cap);
     if (status == RAFEM_ERR_BREAKDOWN)
         return rafem_fail(ctx, RAFEM_ERR_BREAKDOWN, "PCG breakdown: system not SPD under the preconditioner");

@@ -116,6 +116,9 @@ class SolveStats:
     ordering_ns: int = 0
     residual_history: list = field(default_factory=list)
     device_ms: float = 0.0
+    # the preconditioner the device solve applied: "block_jacobi" requests
+    # are served by point Jacobi outside the paper-scale pipelined PCG
+    precondition_applied: str = "none"
 
 
 @dataclass
@@ -189,6 +192,7 @@ def _device_solve(a, b, x0, cfg, method):
     stats.converged = bool(st.converged)
     stats.stagnated = bool(st.stagnated)
     stats.device_ms = float(st.device_ms)
+    stats.precondition_applied = nat.last_solve_precond()
     ncyc = min(int(st.cycles), hist_cap)
     lens = cyc[:ncyc]
     hl = min(int(st.history_len), hist_cap)

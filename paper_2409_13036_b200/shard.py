@@ -188,7 +188,15 @@ class ShardComm:
         if device_collectives is None:
             device_collectives = dist.get_backend(group) == "nccl"
         self.device = device_collectives
-        self.stream = stream  # torch stream the device collectives are ordered on
+        # torch stream the device collectives are ordered on.  The library
+        # enqueues its phase kernels (pack, SpMV, update) on its own
+        # non-blocking stream, so device collectives must run on THAT stream
+        # to be ordered after the pack and before the SpMV: default to it.
+        if self.device and stream is None:
+            import torch
+            from . import _native as nat
+            stream = torch.cuda.ExternalStream(nat.lib().rafem_stream(nat.context()))
+        self.stream = stream
 
     def _ctx(self):
         import contextlib

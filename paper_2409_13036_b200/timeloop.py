@@ -270,7 +270,35 @@ class DeviceRun:
         nat.check(rc, "simulate_stream")
         return out
 
+    def _run_collect(self, config, sink, max_steps, keep=True):
+        """Records through run_streamed (bounded device memory, no step cap)."""
+        records = []
+
+        def take(rec):
+            if keep:
+                records.append(rec)
+            if sink is not None:
+                sink(rec)
+        out = self.run_streamed(config, take, max_steps)
+        self._note_mode()
+        return records, out
+
+    def _note_mode(self):
+        mode, ctas = C.c_int32(), C.c_int32()
+        nat.lib().rafem_last_solve_mode(nat.context(), C.byref(mode), C.byref(ctas))
+        self.last_mode = {4: "kernel-per-phase-pcg", 3: "grid-streaming-pcg", 2: "fused-simulation", 1: "cluster",
+                          0: "grid"}.get(mode.value, "none")
+        self.last_ctas = ctas.value
+        self.last_precond = nat.last_solve_precond()
+
     def run(self, config, sink=None, record_fields=True, max_steps=None, rec_cap=None):
+        """Run the simulation; returns (records, SimSummaryC).
+
+        Field records go to host buffers sized up front (2 x total/dt_init +
+        64 steps).  When those would exceed 8 GB, or the run accepts more
+        steps than they hold (dt shrinking on hard physics), the records
+        are delivered through the streaming path instead (the run is
+        deterministic, so a re-run reproduces it exactly)."""
         N = self.dm.node_count
         # dt only shrinks on hard steps, so 2 x total/dt_init bounds typical runs;
         # np.zeros is lazily paged, so the generous field buffer costs nothing unused
@@ -278,8 +306,8 @@ class DeviceRun:
         est = min(est, 200000)
         if max_steps:
             est = min(est, int(max_steps))
-        if record_fields:
-            est = max(1, min(est, int(8e9 // (16 * max(N, 1)))))
+        if record_fields and rec_cap is None and est * 16 * max(N, 1) > 8e9:
+            return self._run_collect(config, sink, max_steps)
         rec_step = np.zeros(est, dtype=np.int64)
         rec_time = np.zeros(est)
         rec_dt = np.zeros(est)
@@ -290,16 +318,21 @@ class DeviceRun:
         rc = nat.lib().rafem_simulate(self.sys.handle, C.byref(p), C.byref(out), est, nat.ptr(rec_step),
                                       nat.ptr(rec_time), nat.ptr(rec_dt), nat.ptr(rec_it),
                                       nat.ptr(rec_x))
-        mode, ctas = C.c_int32(), C.c_int32()
-        nat.lib().rafem_last_solve_mode(nat.context(), C.byref(mode), C.byref(ctas))
-        self.last_mode = {4: "kernel-per-phase-pcg", 3: "grid-streaming-pcg", 2: "fused-simulation", 1: "cluster", 0: "grid"}.get(mode.value, "none")
-        self.last_ctas = ctas.value
+        self._note_mode()
         if rc == nat.ERR_STEP_FAILURE:
             raise StepFailureError(int(out.failed_step), float(out.failed_dt))
         if rc == nat.ERR_PHYSICS:
             raise PhysicsRangeError(nat.last_error())
         nat.check(rc, "simulate")
         nsteps = int(out.accepted_steps)
+        if nsteps > est and rec_cap is None:
+            import warnings
+            warnings.warn(f"{nsteps} accepted steps exceed the {est}-record buffer; re-running through the "
+                          "record stream", RuntimeWarning, stacklevel=2)
+            if record_fields:
+                return self._run_collect(config, sink, max_steps)
+            _, out2 = self._run_collect(config, None, max_steps, keep=False)
+            return [], out2
         records = []
         for k in range(min(nsteps, est)):
             if record_fields:
