@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-c3", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--ref-worker", default=None, help=argparse.SUPPRESS)
     return ap.parse_args()
 
@@ -486,6 +487,11 @@ def run_ours(args):
         wd.cancel()
         if rank == 0:
             line["sharded_c4"] = c4
+    if not args.no_c5 and world == 1:
+        try:
+            line["c5_1gpu"] = c5_leg(hbm_peak, peak_src)
+        except Exception as exc:  # noqa: BLE001
+            line["c5_1gpu"] = {"error": str(exc)[:300]}
     emit()
     if world > 1:
         import torch.distributed as dist
@@ -698,7 +704,15 @@ def c4_leg(hbm_peak, peak_src, world, rank, local):
                 "kernel": "spmv_tma_pipe_kernel<384,2,stencil classes>" if cls_on else "spmv_tma_pipe_kernel<256,2>",
                 "l2": "flushed (256 MB write) before every timed launch"}
     ach = it * bytes_it / (dev_ms / 1e3) / 1e9 if dev_ms > 0 else 0.0
+    # configs[3]'s run itself: 10 accepted steps (total_time 40 s), every
+    # corrector pass re-assembled, fields resident in HBM on every shard
+    loop = None
+    try:
+        loop = time_loop_leg(sh, comm, world, local, hbm_peak, peak_src, bytes_it, cls_on)
+    except Exception as exc:  # noqa: BLE001
+        loop = {"error": str(exc)[:300]}
     return {"workload": "generate_box_mesh(200,200,200) cold system, 16,000,000 dofs",
+            "time_loop": loop,
             "shards": world, "partition": "contiguous node-row blocks (x-slabs)",
             "collectives": ("none (one shard)" if world == 1 else
                             "NCCL halo send/recv + per-shard scalar all-gather" if BACKEND == "nccl" else
@@ -710,6 +724,85 @@ def c4_leg(hbm_peak, peak_src, world, rank, local):
             "bytes_per_iteration": bytes_it, "columns": "stencil classes" if cls_on else "explicit int32",
             "assembly_s": asm_s, "setup_s": setup_s, "spmv": spmv,
             "kernel": "kp_spmv_kernel + kp_update_kernel (csrc/shard.cu)"}
+
+
+def time_loop_leg(sh, comm, world, local, hbm_peak, peak_src, bytes_it, cls_on, total=40.0):
+    """run_simulation over the shards with the device-resident loop
+    (shard.DeviceShardedSimulation): `total` simulated seconds (10 steps of
+    the default 4 s), re-assembly every corrector pass."""
+    import torch
+    from paper_2409_13036_b200 import SimConfig, SolverConfig
+    from paper_2409_13036_b200.shard import DeviceShardedSimulation
+    cfg = SimConfig(total_time=total, solver=SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-10))
+    loop = DeviceShardedSimulation(sh, comm)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    recs, sm = loop.run(cfg)
+    torch.cuda.synchronize()
+    wall, asm_s, sol_s, sol_dev = sm.wall_s, sm.assemble_s, sm.solve_s, sm.solve_device_ms
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([wall, asm_s, sol_s, sol_dev], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wall, asm_s, sol_s, sol_dev = (float(v) for v in t.tolist())
+    loop.close()
+    N, S, M = sh.dm.node_count, sh.dm.slots, sh.dm.tet_count
+    # assembly roofline: element phase + slot fill + constraints of the shard (asm_pass_bytes)
+    asm_bytes = asm_pass_bytes(N, S, M)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([float(asm_bytes)], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t)
+        asm_bytes = float(t.item())
+    asm_ach = sm.passes * asm_bytes / asm_s / 1e9 if asm_s > 0 else 0.0
+    sol_ach = sm.total_solver_iterations * bytes_it / (sol_dev / 1e3) / 1e9 if sol_dev > 0 else 0.0
+    return {"total_time_s": total, "accepted_steps": sm.accepted_steps, "corrector_passes": sm.passes,
+            "solver_iterations": sm.total_solver_iterations, "wall_s": wall,
+            "steps_per_s": sm.accepted_steps / wall if wall > 0 else 0.0,
+            "assemble_s": asm_s, "solve_s": sol_s, "solve_device_ms": sol_dev,
+            "assemble_ms_per_pass": 1e3 * asm_s / max(sm.passes, 1),
+            "us_per_pcg_iteration": 1e3 * sol_dev / max(sm.total_solver_iterations, 1),
+            "solve_roofline": {"bound": "hbm", "achieved": sol_ach, "peak": hbm_peak * world, "unit": "GB/s",
+                               "frac": sol_ach / hbm_peak / world, "bytes_per_iteration": bytes_it,
+                               "peak_source": peak_src},
+            "assembly_roofline": {"bound": "hbm", "achieved": asm_ach, "peak": hbm_peak * world, "unit": "GB/s",
+                                  "frac": asm_ach / hbm_peak / world, "bytes_per_pass": asm_bytes,
+                                  "formula": "bench.asm_pass_bytes (element + fill + constraints, wall clock "
+                                             "of the pass incl. the sums' reduction)",
+                                  "peak_source": peak_src},
+            "fields": "device-resident (rafem_sl_*): per pass a 4-double halo per boundary node, the "
+                      "equilibration sums and one corrector-delta scalar cross the host",
+            "solver": "kernel-per-phase PCG + Jacobi 1e-10"}
+
+
+def c5_leg(hbm_peak, peak_src):
+    """configs[4] on one GPU: the ~64M-dof box (318^3 nodes, 63.9M dofs)
+    built on the device, 10 steps with re-assembly every corrector pass."""
+    from paper_2409_13036_b200 import _native as nat
+    from paper_2409_13036_b200.assembly import DeviceMesh
+    from paper_2409_13036_b200.shard import ShardedSystem
+    t0 = time.perf_counter()
+    dm = DeviceMesh.from_box(318, 318, 318)
+    sh = ShardedSystem.from_device_mesh(dm, batch=16)
+    setup_s = time.perf_counter() - t0
+    N, S = dm.node_count, dm.slots
+    cls_on = (int(nat.lib().rafem_mesh_stencil_classes(dm.handle)) > 0
+              and os.environ.get("RAFEM_NO_CLASSES", "0") != "1")
+    bytes_it = ((16 * S + N) if cls_on else 20 * S) + 4 * (N + 1) + 14 * 16 * N
+    out = time_loop_leg(sh, None, 1, 0, hbm_peak, peak_src, bytes_it, cls_on)
+    out.update({"workload": f"generate_box_mesh(318,318,318) on the device, {2 * N:,} dofs, 10 steps "
+                            "(total_time 40 s), re-assembly every corrector pass",
+                "shards": 1, "setup_s": setup_s, "columns": "stencil classes" if cls_on else "explicit int32",
+                "hbm_gb_in_use": None})
+    try:
+        import torch
+        free, total = torch.cuda.mem_get_info()
+        out["hbm_gb_in_use"] = (total - free) / 1e9
+    except Exception:  # noqa: BLE001
+        pass
+    return out
 
 
 def c3_leg(hbm_peak, peak_src, cpu_on=True):

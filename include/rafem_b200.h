@@ -274,6 +274,40 @@ int rafem_kp_state(rafem_kp* kp, int32_t* flags, int64_t* iterations, double* re
 int rafem_kp_finish(rafem_kp* kp, double* x_out, rafem_solve_stats* st, double* hist, int64_t hist_cap,
                     int64_t* cycle_lens, int64_t cycle_cap);
 
+/* ---- device-resident shard time loop (run_simulation / corrector_step,
+ * fem.py:463-644, over one row block) ------------------------------------
+ * The shard's accepted, previous and iterate (V, T) states over its
+ * extended node set stay in HBM.  Per corrector pass the caller only moves
+ * the halo (rafem_sl_pack -> exchange send4 into ghost4 -> rafem_sl_unpack;
+ * 4 doubles per node: iterate V, T, accepted V, T), the equilibration sums
+ * (rafem_sl_assemble_partial -> reduce -> rafem_assemble_finish), the
+ * kp phases' collectives, and the corrector delta (a max over shards). */
+typedef struct rafem_shard_loop rafem_shard_loop;
+int rafem_sl_create(rafem_kp* kp, rafem_shard_loop** out);
+void rafem_sl_destroy(rafem_shard_loop* sl);
+/* device buffers: send4 (4 x n_send doubles, kp send order), ghost4 (4 x
+ * n_ghost doubles, ghost order) */
+int rafem_sl_buffers(rafem_shard_loop* sl, void** send4, void** ghost4);
+/* T = initial_temp, V = 0 (fem.py:573-576) */
+int rafem_sl_init(rafem_shard_loop* sl, double initial_temp);
+/* predictor (fem.py:437-449), ratio = dt / dt_prev; vx0: the solver start
+ * extrapolates V as well (the first pass of a step) */
+int rafem_sl_predict(rafem_shard_loop* sl, int32_t step, double ratio, int32_t vx0);
+int rafem_sl_pack(rafem_shard_loop* sl);
+int rafem_sl_unpack(rafem_shard_loop* sl);
+/* rafem_assemble_partial on the device iterate */
+int rafem_sl_assemble_partial(rafem_shard_loop* sl, double dt, double* diag_sums, int64_t* bad_element);
+/* kp solve of the assembled system from the predictor's start (from_start)
+ * or the iterate; then rafem_kp_launch phases as for rafem_kp_begin */
+int rafem_sl_solve_begin(rafem_shard_loop* sl, const rafem_solver_params* p, int32_t from_start);
+/* solve status (return) and stats; the shard's corrector delta
+ * (fem.py:526-528) to *delta; the iterate becomes the solution */
+int rafem_sl_solve_end(rafem_shard_loop* sl, rafem_solve_stats* st, double* delta);
+/* accept the step (fem.py:604-607) */
+int rafem_sl_accept(rafem_shard_loop* sl);
+/* owned accepted (V, T) dofs, interleaved, 2 x n_owned doubles (host) */
+int rafem_sl_download(rafem_shard_loop* sl, double* x_out);
+
 /* ---- device box mesh (mesh.py:306-375) and field comparison -------------
  * generate_box_mesh on the device, bit-identical to the host generator:
  * nodes (numpy.linspace coordinates), Kuhn tets, region 0, Dirichlet kinds

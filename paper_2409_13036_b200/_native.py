@@ -117,6 +117,18 @@ _SIGS = {
     "rafem_kp_iterate": (i32, [vp, i32]),
     "rafem_kp_state": (i32, [vp, P(i32), P(i64), P(f64)]),
     "rafem_kp_finish": (i32, [vp, vp, P(SolveStatsC), vp, i64, vp, i64]),
+    "rafem_sl_create": (i32, [vp, P(vp)]),
+    "rafem_sl_destroy": (None, [vp]),
+    "rafem_sl_buffers": (i32, [vp, P(vp), P(vp)]),
+    "rafem_sl_init": (i32, [vp, f64]),
+    "rafem_sl_predict": (i32, [vp, i32, f64, i32]),
+    "rafem_sl_pack": (i32, [vp]),
+    "rafem_sl_unpack": (i32, [vp]),
+    "rafem_sl_assemble_partial": (i32, [vp, f64, vp, P(i64)]),
+    "rafem_sl_solve_begin": (i32, [vp, P(SolverParams), i32]),
+    "rafem_sl_solve_end": (i32, [vp, P(SolveStatsC), P(f64)]),
+    "rafem_sl_accept": (i32, [vp]),
+    "rafem_sl_download": (i32, [vp, vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -639,7 +639,13 @@ int rafem_kp_buffers(rafem_kp* k, void** x_ext, void** u_ext, void** send_buf, v
     return RAFEM_OK;
 }
 
-int rafem_kp_begin(rafem_kp* k, const double* b, const double* x0, const rafem_solver_params* p) {
+}  // extern "C"
+
+// b: host array, or NULL for the assembled rhs of the shard's system;
+// x0: host array, NULL = zero, or (keep_x) the owned part of a.x as the
+// caller's device code left it (the device-resident shard time loop)
+static int kp_begin_impl(rafem_kp* k, const double* b, const double* x0, bool keep_x,
+                         const rafem_solver_params* p) {
     if (!k || !p) return RAFEM_ERR_INVALID;
     rafem_ctx* ctx = k->ctx;
     if (p->method != RAFEM_METHOD_PCG) return rafem_fail(ctx, RAFEM_ERR_INVALID, "kp solver is PCG only");
@@ -647,14 +653,13 @@ int rafem_kp_begin(rafem_kp* k, const double* b, const double* x0, const rafem_s
         return rafem_fail(ctx, RAFEM_ERR_INVALID, "tolerance must lie in (0, 1)");
     KPArgs& a = k->a;
     const size_t nb = sizeof(double2) * a.n_own;
-    // b: host array, or NULL for the assembled rhs of the shard's system
     if (b)
         RF_CUDA_TRY(ctx, cudaMemcpyAsync((void*)a.b, b, nb, cudaMemcpyHostToDevice, ctx->stream));
     else
         RF_CUDA_TRY(ctx, cudaMemcpyAsync((void*)a.b, k->sys->rhs, nb, cudaMemcpyDeviceToDevice, ctx->stream));
     if (x0)
         RF_CUDA_TRY(ctx, cudaMemcpyAsync(a.x, x0, nb, cudaMemcpyHostToDevice, ctx->stream));
-    else
+    else if (!keep_x)
         RF_CUDA_TRY(ctx, cudaMemsetAsync(a.x, 0, nb, ctx->stream));
     k->pre = p->precondition != RAFEM_PRECOND_NONE;  // block-Jacobi: point Jacobi on this engine
     if (k->pre) {
@@ -680,6 +685,12 @@ int rafem_kp_begin(rafem_kp* k, const double* b, const double* x0, const rafem_s
     RF_CUDA_TRY(ctx, cudaEventRecord(k->e0, ctx->stream));
     kp_bnorm_kernel<<<k->g_upd, KPU, 0, ctx->stream>>>(a);
     return kp_launch_check(ctx);
+}
+
+extern "C" {
+
+int rafem_kp_begin(rafem_kp* k, const double* b, const double* x0, const rafem_solver_params* p) {
+    return kp_begin_impl(k, b, x0, false, p);
 }
 
 // Phase launches (asynchronous).  what: 0 bnorm-finish, 1 head, 2 spmv after
@@ -907,6 +918,223 @@ int rafem_assemble_finish(rafem_system* s, const rafem_assemble_params* p, doubl
     if (int rc = assemble_constrain_launch(s, *p, scale)) return rc;
     RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     s->scale = scale;
+    return RAFEM_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Device-resident shard time loop (run_simulation / corrector_step,
+// fem.py:463-644, over one row block): the accepted, previous and iterate
+// (V, T) states of the shard's extended node set live in HBM; per corrector
+// pass the host only moves a halo of 4 doubles per boundary node, the
+// equilibration sums, the solver state and the corrector delta (one
+// scalar).  Same kernels and arithmetic as the single-GPU per-pass native
+// loop (capi.cu simulate_host_loop): predictor_kernel, the fill on strided
+// views of the iterate, vec_delta.
+
+namespace rafem {
+
+// send4[k] = (x_it V, x_it T, x_acc V, x_acc T) of owned node idx[k]
+__global__ void sl_pack_kernel(const double2* __restrict__ xit, const double2* __restrict__ xacc,
+                               const int* __restrict__ idx, int n, double2* __restrict__ send4) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int i = __ldg(idx + k);
+        send4[2 * k] = xit[i];
+        send4[2 * k + 1] = xacc[i];
+    }
+}
+
+// ghost node g (local id n_own + g) <- ghost4[g]
+__global__ void sl_unpack_kernel(double2* __restrict__ xit, double2* __restrict__ xacc,
+                                 const double2* __restrict__ ghost4, int n_own, int n_ghost) {
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n_ghost; g += gridDim.x * blockDim.x) {
+        xit[n_own + g] = ghost4[2 * g];
+        xacc[n_own + g] = ghost4[2 * g + 1];
+    }
+}
+
+}  // namespace rafem
+
+struct rafem_shard_loop {
+    rafem_kp* kp = nullptr;
+    rafem_ctx* ctx = nullptr;
+    int n_own = 0, n_ext = 0;
+    double* block = nullptr;
+    double* xacc = nullptr;   // accepted (V, T), extended
+    double* xprev = nullptr;  // accepted one step earlier, extended
+    double* xit = nullptr;    // corrector iterate x_old, extended
+    double* send4 = nullptr;  // 4 doubles per send node
+    double* ghost4 = nullptr; // 4 doubles per ghost node
+    double* scr = nullptr;    // delta, diag sums, bad element
+};
+
+extern "C" {
+
+int rafem_sl_create(rafem_kp* kp, rafem_shard_loop** out) {
+    if (!kp || !out) return RAFEM_ERR_INVALID;
+    *out = nullptr;
+    rafem_ctx* ctx = kp->ctx;
+    rafem_shard_loop* l = new rafem_shard_loop();
+    l->kp = kp;
+    l->ctx = ctx;
+    l->n_own = kp->a.n_own;
+    l->n_ext = kp->n_ext;
+    const size_t ext2 = 2 * (size_t)l->n_ext, s4 = 4 * (size_t)std::max(kp->a.n_send, 1);
+    const size_t g4 = 4 * (size_t)std::max(l->n_ext - l->n_own, 1);
+    const size_t total = 3 * ext2 + s4 + g4 + 8;
+    cudaError_t e = cudaMalloc(&l->block, sizeof(double) * total);
+    if (e != cudaSuccess) {
+        delete l;
+        return rafem_fail_cuda(ctx, e, "cudaMalloc(shard loop)", __FILE__, __LINE__);
+    }
+    l->xacc = l->block;
+    l->xprev = l->xacc + ext2;
+    l->xit = l->xprev + ext2;
+    l->send4 = l->xit + ext2;
+    l->ghost4 = l->send4 + s4;
+    l->scr = l->ghost4 + g4;
+    *out = l;
+    return RAFEM_OK;
+}
+
+void rafem_sl_destroy(rafem_shard_loop* l) {
+    if (!l) return;
+    if (l->ctx) cudaStreamSynchronize(l->ctx->stream);
+    if (l->block) cudaFree(l->block);
+    delete l;
+}
+
+int rafem_sl_buffers(rafem_shard_loop* l, void** send4, void** ghost4) {
+    if (!l) return RAFEM_ERR_INVALID;
+    if (send4) *send4 = l->send4;
+    if (ghost4) *ghost4 = l->ghost4;
+    return RAFEM_OK;
+}
+
+// T = initial_temp, V = 0 on every node of the extended set (fem.py:573-576)
+int rafem_sl_init(rafem_shard_loop* l, double initial_temp) {
+    if (!l) return RAFEM_ERR_INVALID;
+    rafem_ctx* ctx = l->ctx;
+    if (int rc = fill_initial(ctx, l->xacc, l->n_ext, initial_temp)) return rc;
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(l->xprev, l->xacc, sizeof(double) * 2 * l->n_ext, cudaMemcpyDeviceToDevice,
+                                     ctx->stream));
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(l->xit, l->xacc, sizeof(double) * 2 * l->n_ext, cudaMemcpyDeviceToDevice,
+                                     ctx->stream));
+    return RAFEM_OK;
+}
+
+// predictor (fem.py:437-449) on the owned nodes: x_it = (V, T + ratio (T -
+// T_prev)); with vx0 the solver start (the kp engine's x) also extrapolates
+// V ("Solver start"), else the solve starts from x_it
+int rafem_sl_predict(rafem_shard_loop* l, int32_t step, double ratio, int32_t vx0) {
+    if (!l) return RAFEM_ERR_INVALID;
+    double* xs = vx0 ? reinterpret_cast<double*>(l->kp->a.x) : nullptr;
+    return predictor_launch(l->ctx, l->xit, l->xacc, l->xprev, l->n_own, step, ratio, xs);
+}
+
+int rafem_sl_pack(rafem_shard_loop* l) {
+    if (!l) return RAFEM_ERR_INVALID;
+    rafem_ctx* ctx = l->ctx;
+    const int n = l->kp->a.n_send;
+    if (n == 0) return RAFEM_OK;
+    sl_pack_kernel<<<std::min((n + 255) / 256, 4 * ctx->sm_count), 256, 0, ctx->stream>>>(
+        reinterpret_cast<const double2*>(l->xit), reinterpret_cast<const double2*>(l->xacc), l->kp->a.send_idx, n,
+        reinterpret_cast<double2*>(l->send4));
+    ctx->launches++;
+    RF_CUDA_TRY(ctx, cudaGetLastError());
+    return RAFEM_OK;
+}
+
+int rafem_sl_unpack(rafem_shard_loop* l) {
+    if (!l) return RAFEM_ERR_INVALID;
+    rafem_ctx* ctx = l->ctx;
+    const int ng = l->n_ext - l->n_own;
+    if (ng == 0) return RAFEM_OK;
+    sl_unpack_kernel<<<std::min((ng + 255) / 256, 4 * ctx->sm_count), 256, 0, ctx->stream>>>(
+        reinterpret_cast<double2*>(l->xit), reinterpret_cast<double2*>(l->xacc),
+        reinterpret_cast<const double2*>(l->ghost4), l->n_own, ng);
+    ctx->launches++;
+    RF_CUDA_TRY(ctx, cudaGetLastError());
+    return RAFEM_OK;
+}
+
+// element + fill from the device iterate (t_it, v_it) and the accepted T
+// (fem.py:247-388); owned diagonal sums / bad element out, as
+// rafem_assemble_partial.  The caller reduces the sums over the shards and
+// calls rafem_assemble_finish.
+int rafem_sl_assemble_partial(rafem_shard_loop* l, double dt, double* diag_sums, int64_t* bad_element) {
+    if (!l || !diag_sums) return RAFEM_ERR_INVALID;
+    rafem_ctx* ctx = l->ctx;
+    if (!(dt > 0.0)) return rafem_fail(ctx, RAFEM_ERR_INVALID, "dt must be positive");
+    rafem_system* s = l->kp->sys;
+    long long* dbad = reinterpret_cast<long long*>(l->scr + 4);
+    if (int rc = assemble_fill_launch(s, l->xit + 1, 2, l->xit, 2, l->xacc + 1, 2, dt, dbad)) return rc;
+    if (int rc = diag_sums_launch(ctx, s->diagpart, l->n_own, 0, l->scr + 1, nullptr)) return rc;
+    double hb[5];
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(hb, l->scr, sizeof(hb), cudaMemcpyDeviceToHost, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    diag_sums[0] = hb[1];
+    diag_sums[1] = hb[2];
+    long long bad;
+    std::memcpy(&bad, hb + 4, sizeof(bad));
+    if (bad_element) *bad_element = bad;
+    if (bad >= 0) {
+        char buf[128];
+        std::snprintf(buf, sizeof(buf), "sigma(T) <= 0 in element %lld", bad);
+        return rafem_fail(ctx, RAFEM_ERR_PHYSICS, buf);
+    }
+    return RAFEM_OK;
+}
+
+// PCG on the shard's assembled system, b = its rhs, x0 = the predictor's
+// start (from_start) or x_it; then the usual kp phases (rafem_kp_launch)
+int rafem_sl_solve_begin(rafem_shard_loop* l, const rafem_solver_params* p, int32_t from_start) {
+    if (!l || !p) return RAFEM_ERR_INVALID;
+    rafem_ctx* ctx = l->ctx;
+    if (!from_start)
+        RF_CUDA_TRY(ctx, cudaMemcpyAsync(l->kp->a.x, l->xit, sizeof(double2) * l->n_own, cudaMemcpyDeviceToDevice,
+                                         ctx->stream));
+    return kp_begin_impl(l->kp, nullptr, nullptr, true, p);
+}
+
+// solve stats + the corrector delta max|x_new - x_old| / max(1, |x_old|)
+// over the owned dofs (fem.py:526-528), then x_old <- x_new (fem.py:529-530)
+int rafem_sl_solve_end(rafem_shard_loop* l, rafem_solve_stats* st, double* delta) {
+    if (!l || !delta) return RAFEM_ERR_INVALID;
+    rafem_ctx* ctx = l->ctx;
+    rafem_kp* k = l->kp;
+    KPState s;
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(&s, k->a.st + k->idx, sizeof(s), cudaMemcpyDeviceToHost, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (s.bnorm == 0.0 && s.done)  // zero rhs: x = 0 (solver.py:425-429)
+        RF_CUDA_TRY(ctx, cudaMemsetAsync(k->a.x, 0, sizeof(double2) * l->n_own, ctx->stream));
+    const int status = rafem_kp_finish(k, nullptr, st, nullptr, 0, nullptr, 0);
+    if (status != RAFEM_OK) return status;
+    const double* xn = reinterpret_cast<const double*>(k->a.x);
+    if (int rc = vec_delta_launch(ctx, xn, l->xit, 2 * l->n_own, l->scr)) return rc;
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(l->xit, xn, sizeof(double2) * l->n_own, cudaMemcpyDeviceToDevice, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(delta, l->scr, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return RAFEM_OK;
+}
+
+// accept the step (fem.py:604-607): prev <- acc <- iterate
+int rafem_sl_accept(rafem_shard_loop* l) {
+    if (!l) return RAFEM_ERR_INVALID;
+    double* old_prev = l->xprev;
+    l->xprev = l->xacc;
+    l->xacc = l->xit;
+    l->xit = old_prev;
+    return RAFEM_OK;
+}
+
+// the owned accepted (V, T) dof vector (2 * n_own doubles, interleaved)
+int rafem_sl_download(rafem_shard_loop* l, double* x_out) {
+    if (!l || !x_out) return RAFEM_ERR_INVALID;
+    rafem_ctx* ctx = l->ctx;
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(x_out, l->xacc, sizeof(double2) * l->n_own, cudaMemcpyDeviceToHost, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     return RAFEM_OK;
 }
 

@@ -39,7 +39,7 @@ from . import _native as nat
 from .krylov import KrylovBreakdownError, SolveStats
 
 __all__ = ["ShardPlan", "partition_rows", "build_plan", "ShardComm", "ShardedPCG", "ShardedSystem",
-           "KPDeviceEngine", "ShardedSimulation"]
+           "KPDeviceEngine", "ShardedSimulation", "DeviceShardedSimulation"]
 
 # phases of rafem_kp_launch (include/rafem_b200.h)
 BNORM_FINISH, HEAD, SPMV_AFTER_HEAD, SPMV, UPDATE_FIRST, UPDATE, PACK_X, PACK_U_AFTER_HEAD, PACK_U = range(9)
@@ -245,13 +245,16 @@ class ShardComm:
         self.dist.all_gather(out, t, group=self.group)
         return torch.stack(out).numpy()
 
-    def halo(self, plan: ShardPlan, send_buf, ext, n_send: int):
-        """ext[n_own + recv[q]] <- neighbour q's packed values for this shard.
-        send_buf / ext: tensors of doubles (2 per node)."""
+    def halo(self, plan: ShardPlan, send_buf, ext, n_send: int, width: int = 2, base: int | None = None):
+        """ext[width * (base + recv[q])] <- neighbour q's packed values for
+        this shard.  send_buf / ext: tensors of doubles, `width` per node;
+        base = n_own for an extended vector (the default), 0 for a
+        ghost-only buffer."""
         if self.size == 1 or not plan.neighbours:
             return
         offs = plan.send_offsets()
-        n0 = plan.n_own
+        n0 = plan.n_own if base is None else base
+        w = width
         P2P = self.dist.P2POp
         if self.device:
             with self._ctx():
@@ -259,30 +262,30 @@ class ShardComm:
                 for q in plan.neighbours:
                     so, sn = offs[q]
                     if sn:
-                        ops.append(P2P(self.dist.isend, send_buf[2 * so:2 * (so + sn)], q, group=self.group))
+                        ops.append(P2P(self.dist.isend, send_buf[w * so:w * (so + sn)], q, group=self.group))
                     if q in plan.recv:
                         rs, rn = plan.recv[q]
-                        ops.append(P2P(self.dist.irecv, ext[2 * (n0 + rs):2 * (n0 + rs + rn)], q, group=self.group))
+                        ops.append(P2P(self.dist.irecv, ext[w * (n0 + rs):w * (n0 + rs + rn)], q, group=self.group))
                 if ops:
                     for req in self.dist.batch_isend_irecv(ops):
                         req.wait()
             return
         self._sync(ext)
-        sb = send_buf[:2 * n_send].cpu().clone() if n_send else None
+        sb = send_buf[:w * n_send].cpu().clone() if n_send else None
         bufs, reqs = {}, []
         for q in plan.neighbours:
             so, sn = offs[q]
             if sn:
-                reqs.append(self.dist.isend(sb[2 * so:2 * (so + sn)].clone(), q, group=self.group))
+                reqs.append(self.dist.isend(sb[w * so:w * (so + sn)].clone(), q, group=self.group))
             if q in plan.recv:
                 rs, rn = plan.recv[q]
-                bufs[q] = ext.new_empty(2 * rn, device="cpu")
+                bufs[q] = ext.new_empty(w * rn, device="cpu")
                 reqs.append(self.dist.irecv(bufs[q], q, group=self.group))
         for req in reqs:
             req.wait()
         for q, b in bufs.items():
             rs, rn = plan.recv[q]
-            ext[2 * (n0 + rs):2 * (n0 + rs + rn)].copy_(b.to(ext.device))
+            ext[w * (n0 + rs):w * (n0 + rs + rn)].copy_(b.to(ext.device))
         self._sync(ext)
 
     def exchange_fields(self, plan: ShardPlan, own: np.ndarray) -> np.ndarray:
@@ -429,6 +432,30 @@ class ShardedPCG:
         e = self.e
         t0 = time.perf_counter_ns()
         e.begin(b, x0, params)
+        self.run_phases()
+        rc, x, st, hist, cyc = e.finish(hist_cap)
+        stats = SolveStats()
+        stats.iterations = int(st.iterations)
+        stats.restarts = int(st.restarts)
+        stats.final_relative_residual = float(st.final_relative_residual)
+        stats.converged = bool(st.converged)
+        stats.device_ms = float(st.device_ms)
+        lens = cyc[:min(int(st.cycles), hist_cap)]
+        hv = hist[:min(int(st.history_len), hist_cap)]
+        out, pos = [], 0
+        for ln in lens:
+            out.append([float(v) for v in hv[pos:pos + int(ln)]])
+            pos += int(ln)
+        stats.residual_history = out
+        stats.wall_ns = max(time.perf_counter_ns() - t0, 1)
+        if rc == nat.ERR_BREAKDOWN:
+            raise KrylovBreakdownError("PCG breakdown: system not SPD under the preconditioner")
+        nat.check(rc, "kp solve")
+        return x, stats
+
+    def run_phases(self):
+        """Every phase of one begun solve, up to the done flag."""
+        e = self.e
         self._slots()
         e.launch(BNORM_FINISH)
         flags, _, _ = e.state()
@@ -454,25 +481,6 @@ class ShardedPCG:
                 else:
                     e.iterate(self.batch)  # SPMV + UPDATE pairs, no host round trip
                 flags, _, _ = e.state()
-        rc, x, st, hist, cyc = e.finish(hist_cap)
-        stats = SolveStats()
-        stats.iterations = int(st.iterations)
-        stats.restarts = int(st.restarts)
-        stats.final_relative_residual = float(st.final_relative_residual)
-        stats.converged = bool(st.converged)
-        stats.device_ms = float(st.device_ms)
-        lens = cyc[:min(int(st.cycles), hist_cap)]
-        hv = hist[:min(int(st.history_len), hist_cap)]
-        out, pos = [], 0
-        for ln in lens:
-            out.append([float(v) for v in hv[pos:pos + int(ln)]])
-            pos += int(ln)
-        stats.residual_history = out
-        stats.wall_ns = max(time.perf_counter_ns() - t0, 1)
-        if rc == nat.ERR_BREAKDOWN:
-            raise KrylovBreakdownError("PCG breakdown: system not SPD under the preconditioner")
-        nat.check(rc, "kp solve")
-        return x, stats
 
 
 # ---------------------------------------------------------------------------
@@ -499,6 +507,25 @@ class ShardedSystem:
         self.pcg = ShardedPCG(self.engine, comm, self.plan, batch=batch)
         self.scale = 1.0
 
+    @classmethod
+    def from_device_mesh(cls, dm, batch: int = 16) -> "ShardedSystem":
+        """One shard owning every row of a device mesh (DeviceMesh.from_box:
+        no host mesh at all — the 64M-dof configs[4] on one GPU)."""
+        from .assembly import SystemHandle
+        self = cls.__new__(cls)
+        self.comm = None
+        n = dm.node_count
+        self.plan = ShardPlan(rank=0, nranks=1, bounds=np.array([0, n], dtype=np.int64), n_own=n,
+                              ghosts=np.zeros(0, dtype=np.int64), tet_ids=None, local_tets=None)
+        self.mesh = self.lmesh = None
+        self.material = None
+        self.dm = dm
+        self.h = SystemHandle(dm)
+        self.engine = KPDeviceEngine(self.h.handle, n, n, 1, 0, None)
+        self.pcg = ShardedPCG(self.engine, None, self.plan, batch=batch)
+        self.scale = 1.0
+        return self
+
     @property
     def n_own(self) -> int:
         return self.plan.n_own
@@ -507,7 +534,6 @@ class ShardedSystem:
         """Assemble this shard's rows; fields are owned + ghost node values
         (ShardPlan.extend).  Raises PhysicsRangeError on every rank if any
         shard sees sigma <= 0 (lowest global element id)."""
-        from .assembly import PhysicsRangeError
         if dt <= 0.0:
             raise ValueError("dt must be positive")
         n = self.plan.n_ext
@@ -515,19 +541,33 @@ class ShardedSystem:
         for a in arrs:
             if a.shape != (n,):
                 raise ValueError("shard field length must be owned + ghost node count")
-        p = nat.AssembleParams()
-        p.dt = float(dt)
-        p.applied_voltage = float(config.applied_voltage)
-        p.boundary_temp = float(config.boundary_temp)
-        p.apply_constraints = 1 if apply_constraints else 0
-        p.equilibrate = 1 if equilibrate else 0
+        p = self.assemble_params(dt, config, apply_constraints, equilibrate)
         sums = np.zeros(2)
         bad = C.c_int64(-1)
         rc = nat.lib().rafem_assemble_partial(self.h.handle, nat.ptr(arrs[0]), nat.ptr(arrs[1]), nat.ptr(arrs[2]),
                                               C.byref(p), self.plan.n_own, nat.ptr(sums), C.byref(bad))
         if rc not in (nat.OK, nat.ERR_PHYSICS):
             nat.check(rc, "assemble_partial")
-        gbad = float(self.plan.tet_ids[bad.value]) if bad.value >= 0 else -1.0
+        return self._finish(sums, bad.value, p, equilibrate)
+
+    @staticmethod
+    def assemble_params(dt, config, apply_constraints=True, equilibrate=True):
+        p = nat.AssembleParams()
+        p.dt = float(dt)
+        p.applied_voltage = float(config.applied_voltage)
+        p.boundary_temp = float(config.boundary_temp)
+        p.apply_constraints = 1 if apply_constraints else 0
+        p.equilibrate = 1 if equilibrate else 0
+        return p
+
+    def _finish(self, sums, bad: int, p, equilibrate: bool) -> float:
+        """The one global reduction of assemble_global (fem.py:390-400) over
+        the shards' owned diagonal sums, in rank order; PhysicsRangeError on
+        every rank for the lowest global bad element; then the scale and
+        the Dirichlet elimination (rafem_assemble_finish)."""
+        from .assembly import PhysicsRangeError
+        tid = self.plan.tet_ids
+        gbad = (float(tid[bad]) if tid is not None else float(bad)) if bad >= 0 else -1.0
         row = np.array([sums[0], sums[1], gbad])
         allr = self.comm.allgather_host(row) if self.comm is not None else row[None]
         bads = allr[:, 2][allr[:, 2] >= 0]
@@ -597,6 +637,8 @@ class ShardSummary:
     assemble_s: float
     solve_s: float
     wall_s: float
+    passes: int = 0
+    solve_device_ms: float = 0.0
 
 
 class ShardedSimulation:
@@ -701,3 +743,145 @@ class ShardedSimulation:
                 dt_cur = max(dt * 0.5, config.dt_min)
                 halv += 1
         return recs, ShardSummary(step, corr, inner, halv, t, asm_s, sol_s, time.perf_counter() - w0)
+
+
+class DeviceShardedSimulation:
+    """ShardedSimulation with the fields in HBM (csrc/shard.cu, rafem_sl_*).
+
+    The same control contract (run_simulation, fem.py:554-644, and
+    corrector_step, fem.py:463-540): the shard's accepted / previous /
+    iterate states never leave the device; per corrector pass the host
+    exchanges a 4-double halo per boundary node, the equilibration sums,
+    the kp solver's collectives, and ONE scalar (the corrector delta,
+    all-reduced max) on which every rank takes the same decision.  Records
+    (owned fields of each accepted step) are read back only on request.
+    """
+
+    def __init__(self, system: ShardedSystem, comm: ShardComm | None = None):
+        import torch
+        self.sys = system
+        self.comm = comm
+        self.plan = system.plan
+        self.L = nat.lib()
+        h = C.c_void_p()
+        nat.check(self.L.rafem_sl_create(system.engine.h, C.byref(h)), "sl_create")
+        self.h = h
+        ps, pg = C.c_void_p(), C.c_void_p()
+        nat.check(self.L.rafem_sl_buffers(h, C.byref(ps), C.byref(pg)), "sl_buffers")
+        dev = torch.device("cuda", torch.cuda.current_device())
+        n_send = system.engine.n_send
+        n_ghost = self.plan.n_ext - self.plan.n_own
+        self.send4 = torch.as_tensor(_CudaArray(ps.value, 4 * max(n_send, 1)), device=dev)
+        self.ghost4 = torch.as_tensor(_CudaArray(pg.value, 4 * max(n_ghost, 1)), device=dev)
+        self.n_send = n_send
+
+    def close(self):
+        if self.h:
+            self.L.rafem_sl_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _halo(self):
+        """Ghost nodes' iterate and accepted (V, T) from their owners."""
+        if self.comm is None or self.comm.size == 1 or not self.plan.neighbours:
+            return
+        nat.check(self.L.rafem_sl_pack(self.h), "sl_pack")
+        self.comm.halo(self.plan, self.send4, self.ghost4, self.n_send, width=4, base=0)
+        nat.check(self.L.rafem_sl_unpack(self.h), "sl_unpack")
+
+    def _max(self, v):
+        return self.comm.allreduce_max(v) if self.comm is not None else float(v)
+
+    def download(self):
+        """(T, V) owned node values of the accepted state (host)."""
+        x = np.empty(2 * self.plan.n_own)
+        nat.check(self.L.rafem_sl_download(self.h, nat.ptr(x)), "sl_download")
+        return x[1::2].copy(), x[0::2].copy()
+
+    def run(self, config, record_fields=False, max_steps=None, sink=None):
+        from .krylov import _params
+        from .timeloop import StepFailureError
+        sysm, L, h = self.sys, self.L, self.h
+        params = _params(config.solver, nat.METHOD_PCG)
+        if config.solver.backend != "pcg":
+            raise ValueError("the sharded time loop solves with the kernel-per-phase PCG (backend='pcg')")
+        vx0 = os.environ.get("RAFEM_NO_VX0", "0") != "1"
+        nat.check(L.rafem_sl_init(h, float(config.initial_temp)), "sl_init")
+        t, dt_cur, dt_prev, step = 0.0, config.dt_init, config.dt_init, 0
+        corr = inner = halv = passes = 0
+        asm_s = sol_s = 0.0
+        sol_dev_ms = 0.0
+        w0 = time.perf_counter()
+        recs = []
+        sums = np.zeros(2)
+        bad = C.c_int64(-1)
+        st = nat.SolveStatsC()
+        delta = C.c_double()
+        while t < config.total_time:
+            if max_steps is not None and step >= max_steps:
+                break
+            remaining = config.total_time - t
+            last = dt_cur >= remaining
+            dt = remaining if last else dt_cur
+            start = vx0 and step >= 1
+            nat.check(L.rafem_sl_predict(h, step, dt / dt_prev, 1 if start else 0), "sl_predict")
+            p = sysm.assemble_params(dt, config)
+            ok, used = False, 0
+            for it in range(1, config.max_corrector_iters + 1):
+                used = it
+                passes += 1
+                a0 = time.perf_counter()
+                self._halo()
+                rc = L.rafem_sl_assemble_partial(h, float(dt), nat.ptr(sums), C.byref(bad))
+                if rc not in (nat.OK, nat.ERR_PHYSICS):
+                    nat.check(rc, "sl_assemble_partial")
+                sysm._finish(sums, bad.value, p, True)
+                a1 = time.perf_counter()
+                nat.check(L.rafem_sl_solve_begin(h, C.byref(params), 1 if (start and it == 1) else 0),
+                          "sl_solve_begin")
+                sysm.pcg.run_phases()
+                rc = L.rafem_sl_solve_end(h, C.byref(st), C.byref(delta))
+                sol_s += time.perf_counter() - a1
+                asm_s += a1 - a0
+                sol_dev_ms += float(st.device_ms)
+                if rc == nat.ERR_BREAKDOWN:
+                    break  # SolverError -> step failure (fem.py:511-515)
+                nat.check(rc, "sl_solve_end")
+                inner += int(st.iterations)
+                if not st.converged:
+                    break
+                d = self._max(delta.value)
+                if d < config.corrector_tol:
+                    ok = True
+                    break
+            corr += used
+            if ok:
+                nat.check(L.rafem_sl_accept(h), "sl_accept")
+                dt_prev = dt
+                t = config.total_time if last else t + dt
+                T = V = None
+                if record_fields:
+                    T, V = self.download()
+                rec = ShardStep(step, t, dt, used, T, V)
+                recs.append(rec)
+                if sink is not None:
+                    sink(rec)
+                step += 1
+                if used <= 5:
+                    dt_cur = min(dt * 1.5, config.dt_max)
+                elif used >= 20:
+                    dt_cur = max(dt * 0.75, config.dt_min)
+                else:
+                    dt_cur = dt
+            else:
+                if dt <= config.dt_min:
+                    raise StepFailureError(step, dt)
+                dt_cur = max(dt * 0.5, config.dt_min)
+                halv += 1
+        return recs, ShardSummary(step, corr, inner, halv, t, asm_s, sol_s, time.perf_counter() - w0, passes,
+                                  sol_dev_ms)

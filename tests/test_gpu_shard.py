@@ -239,3 +239,97 @@ def test_stencil_class_columns_change_nothing_but_bytes():
     (xa, sa), (xb, sb) = out
     assert sa.converged and sb.converged and abs(sa.iterations - sb.iterations) <= 1
     assert np.max(np.abs(xa - xb)) <= 1e-9 * np.max(np.abs(xb))
+
+
+# ---------------------------------------------------------------------------
+# device-resident shard time loop (rafem_sl_*, DeviceShardedSimulation)
+
+def _dsim_worker(rank, world, port, dims, total, out_dir, which):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh
+        from paper_2409_13036_b200.shard import (DeviceShardedSimulation, ShardComm, ShardedSimulation,
+                                                 ShardedSystem)
+        mesh = generate_box_mesh(*dims)
+        comm = ShardComm(device_collectives=False) if world > 1 else None
+        sh = ShardedSystem(mesh, MaterialParams.default(), comm, batch=8)
+        cfg = SimConfig(total_time=total, solver=SolverConfig(backend="pcg", precondition="jacobi",
+                                                              tolerance=1e-12))
+        loop = (DeviceShardedSimulation if which == "device" else ShardedSimulation)(sh, comm)
+        recs, summ = loop.run(cfg, record_fields=True)
+        np.savez(os.path.join(out_dir, f"{which}_w{world}_r{rank}.npz"),
+                 traj=np.array([(r.step, r.time, r.dt, r.corrector_iters) for r in recs]),
+                 T=np.array([r.T for r in recs]), V=np.array([r.V for r in recs]),
+                 inner=summ.total_solver_iterations)
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def _run_dsim(tmp_path, dims, total, world, which):
+    import torch.multiprocessing as mp
+    port = 26100 + (os.getpid() % 400) + 7 * world + (3 if which == "device" else 0)
+    mp.start_processes(_dsim_worker, args=(world, port, dims, total, str(tmp_path), which), nprocs=world,
+                       join=True, start_method="spawn")
+    parts = [np.load(tmp_path / f"{which}_w{world}_r{r}.npz") for r in range(world)]
+    traj = [tuple(x) for x in parts[0]["traj"]]
+    for p in parts[1:]:
+        assert [tuple(x) for x in p["traj"]] == traj
+    return (traj, np.concatenate([p["T"] for p in parts], axis=1), np.concatenate([p["V"] for p in parts], axis=1),
+            int(parts[0]["inner"]))
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_device_sharded_time_loop_is_bitwise_host_sharded_loop(tmp_path, world):
+    """The device-resident loop keeps the shard's states in HBM; it runs the
+    same arithmetic as the host-field ShardedSimulation (predictor without
+    FMA contraction, the same fill, the same kp solve, the same delta), so
+    trajectory and every step's fields are bit-identical."""
+    dims, total = (15, 15, 16), 40.0
+    a = _run_dsim(tmp_path, dims, total, world, "device")
+    b = _run_dsim(tmp_path, dims, total, world, "host")
+    assert a[0] == b[0] and a[3] == b[3]
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+
+
+def test_device_sharded_time_loop_1_vs_2_shards_mid_size(tmp_path):
+    """configs[3]/[4] semantics at 60^3 nodes (432,000 dofs, 10 steps):
+    1 and 2 shards follow the native single-GPU loop's trajectory and agree
+    with each other to the fixed-order reductions' rounding."""
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh, simulate_device
+    dims, total = (60, 60, 60), 40.0
+    one = _run_dsim(tmp_path, dims, total, 1, "device")
+    two = _run_dsim(tmp_path, dims, total, 2, "device")
+    assert one[0] == two[0] and len(one[0]) == 10
+    for k in range(len(one[0])):
+        assert np.max(np.abs(one[1][k] - two[1][k])) <= 1e-9 * np.max(np.abs(one[1][k]))
+        assert np.max(np.abs(one[2][k] - two[2][k])) <= 1e-9 * np.max(np.abs(one[2][k]))
+    cfg = SimConfig(total_time=total, solver=SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-12))
+    ref, _ = simulate_device(generate_box_mesh(*dims), MaterialParams.default(), cfg)
+    assert one[0] == [(r.step, r.time, r.dt, r.corrector_iters) for r in ref]
+    for k, r in enumerate(ref):
+        assert np.max(np.abs(one[1][k] - r.T)) <= 1e-8 * np.max(np.abs(r.T))
+        assert np.max(np.abs(one[2][k] - r.V)) <= 1e-8 * np.max(np.abs(r.V))
+
+
+def test_device_sharded_loop_on_a_device_box_mesh():
+    """One shard straight from DeviceMesh.from_box (no host mesh: the
+    configs[4] path) equals the same loop on the host-generated mesh."""
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh
+    from paper_2409_13036_b200.assembly import DeviceMesh
+    from paper_2409_13036_b200.shard import DeviceShardedSimulation, ShardedSystem
+    dims = (24, 22, 26)
+    cfg = SimConfig(total_time=40.0, solver=SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-10))
+    a, sa = DeviceShardedSimulation(ShardedSystem(generate_box_mesh(*dims), MaterialParams.default())).run(
+        cfg, record_fields=True)
+    b, sb = DeviceShardedSimulation(ShardedSystem.from_device_mesh(DeviceMesh.from_box(*dims))).run(
+        cfg, record_fields=True)
+    assert sa.total_solver_iterations == sb.total_solver_iterations and sa.passes == sb.passes
+    for x, y in zip(a, b):
+        assert (x.step, x.time, x.dt, x.corrector_iters) == (y.step, y.time, y.dt, y.corrector_iters)
+        assert np.array_equal(x.T, y.T) and np.array_equal(x.V, y.V)
