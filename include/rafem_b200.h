@@ -188,6 +188,12 @@ int64_t rafem_mesh_slots(const rafem_mesh* mesh);
 int32_t rafem_mesh_stencil_classes(rafem_mesh* mesh);
 /* node-level pattern: row_ptr (N+1), col (slots) */
 int rafem_mesh_pattern(rafem_mesh* mesh, int64_t* node_row_ptr, int32_t* node_col);
+/* shard sub-mesh (local ids [owned | ghosts by (owner, id)]): the ghosts
+ * [n_owned, n_owned + n_below) have global ids below the owned block, so
+ * the Dirichlet elimination's moved-column sums (fem.py:419-424) walk each
+ * row in GLOBAL column order and the owned rows' rhs is bitwise the
+ * unsharded one.  Rows must have <= 32 slots when n_below > 0. */
+int rafem_mesh_set_shard_order(rafem_mesh* mesh, int64_t n_owned, int64_t n_below);
 
 int rafem_system_create(rafem_mesh* mesh, rafem_system** out);
 void rafem_system_destroy(rafem_system* sys);

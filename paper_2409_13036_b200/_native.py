@@ -93,6 +93,7 @@ _SIGS = {
     "rafem_mesh_slots": (i64, [vp]),
     "rafem_mesh_stencil_classes": (i32, [vp]),
     "rafem_mesh_pattern": (i32, [vp, vp, vp]),
+    "rafem_mesh_set_shard_order": (i32, [vp, i64, i64]),
     "rafem_system_create": (i32, [vp, P(vp)]),
     "rafem_system_destroy": (None, [vp]),
     "rafem_assemble": (i32, [vp, vp, vp, vp, P(AssembleParams), P(f64), P(i64)]),

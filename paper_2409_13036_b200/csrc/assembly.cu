@@ -355,6 +355,42 @@ __global__ void __launch_bounds__(256) fill_kernel(AsmMesh m, const double2* con
     fill_node_warp(i, m, contrib, load, val2 + __ldg(m.rp + i), rhs, diag_raw, ws[threadIdx.x >> 5]);
 }
 
+// 1+2 fused: one warp per node row computes its incident elements' rows and
+//    sums them in place (no per-element intermediate in HBM: 288 B per tet
+//    written and read back by the two-kernel path)
+__global__ void __launch_bounds__(256) element_scalars_kernel(AsmMesh m, AsmFields f, double* sig, double* load4,
+                                                             unsigned long long* bad) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m.M) return;
+    double s, l4[4];
+    if (element_scalars(e, m, f, &s, l4)) atomicMin(bad, (unsigned long long)e);
+    __stcg(sig + e, s);
+    __stcg(reinterpret_cast<double2*>(load4 + 4LL * e), make_double2(l4[0], l4[1]));
+    __stcg(reinterpret_cast<double2*>(load4 + 4LL * e) + 1, make_double2(l4[2], l4[3]));
+}
+constexpr int kFillRegions = 64;  // region table of the half-warp fill in shared memory
+__global__ void __launch_bounds__(256) fused_fill_half_kernel(AsmMesh m, double dt, const double* sig,
+                                                              const double* load4, double2* val2, double* rhs,
+                                                              double* diag_raw) {
+    __shared__ FillScratch ws[16];
+    __shared__ double rk[kFillRegions], rrc[kFillRegions];
+    for (int r = threadIdx.x; r < m.nreg; r += blockDim.x) {
+        rk[r] = m.regtab[r];
+        rrc[r] = m.regtab[m.nreg + r] / dt;  // element_core's rcdt
+    }
+    __syncthreads();
+    const int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 4);
+    if (i >= m.N) return;  // whole half-warps exit together
+    fill_node_fused_half(i, m, rk, rrc, sig, load4, val2, rhs, diag_raw, ws[threadIdx.x >> 4]);
+}
+__global__ void __launch_bounds__(256) fused_fill_kernel(AsmMesh m, double dt, const double* sig, const double* load4,
+                                                         double2* val2, double* rhs, double* diag_raw) {
+    __shared__ FillScratch ws[8];
+    const int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (i >= m.N) return;  // whole warps exit together
+    fill_node_fused(i, m, dt, sig, load4, val2 + __ldg(m.rp + i), rhs, diag_raw, ws[threadIdx.x >> 5]);
+}
+
 // 3. scale = 2^round(log2(sum diag_T / sum diag_V)) (fem.py:390-396) from
 //    the raw diagonal sums:
 // 3'. the same sums over n rows in two deterministic stages (G CTAs over
@@ -415,6 +451,14 @@ __global__ void __launch_bounds__(256) constrain_kernel(AsmMesh m, const double*
     const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (i >= m.N) return;
     constrain_node_warp(i, m, *scale_p, apply, applied, btemp, val2 + __ldg(m.rp + i), rhs, nullptr, nullptr);
+}
+
+__global__ void __launch_bounds__(256) constrain_half_kernel(AsmMesh m, const double* scale_p, int apply,
+                                                             double applied, double btemp, double2* val2,
+                                                             double* rhs) {
+    const int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 4);
+    if (i >= m.N) return;  // whole half-warps exit together
+    constrain_node_half(i, m, *scale_p, apply, applied, btemp, val2, rhs);
 }
 
 // dof-order values for CsrMatrix.vals: row 2i then row 2i+1 per node.
@@ -686,6 +730,24 @@ int mesh_geometry(rafem_mesh* m) {
     return RAFEM_OK;
 }
 
+int system_contrib(rafem_system* s) {
+    if (s->contrib) return RAFEM_OK;
+    rafem_ctx* ctx = s->mesh->ctx;
+    const size_t M = std::max(s->mesh->M, 1);
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&s->contrib, sizeof(double) * 32 * M));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&s->load, sizeof(double) * 4 * M));
+    return RAFEM_OK;
+}
+
+int system_escal(rafem_system* s) {
+    if (s->esig) return RAFEM_OK;
+    rafem_ctx* ctx = s->mesh->ctx;
+    const size_t M = std::max(s->mesh->M, 1);
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&s->esig, sizeof(double) * M));
+    RF_CUDA_TRY(ctx, dmalloc(ctx, (void**)&s->eload, sizeof(double) * 4 * M));
+    return RAFEM_OK;
+}
+
 AsmMesh asm_mesh(const rafem_mesh* m) {
     AsmMesh a;
     a.tets = m->tets;
@@ -708,6 +770,8 @@ AsmMesh asm_mesh(const rafem_mesh* m) {
     a.lpos = m->load_pos;
     a.N = m->N;
     a.M = m->M;
+    a.own_end = m->own_end >= 0 ? m->own_end : m->N;
+    a.below_end = m->below_end >= 0 ? m->below_end : m->N;
     return a;
 }
 
@@ -721,13 +785,42 @@ int assemble_fill_launch(rafem_system* s, const double* t_it, int ts, const doub
     const int N = m->N, M = m->M;
     const char* wf = getenv("RAFEM_WARP_FILL");
     const bool warp_fill = wf && wf[0] == '1';
-    if (!warp_fill && !m->slot_lists_tried)
+    // fused element + fill (default; RAFEM_FUSED_FILL=0: element kernel +
+    // contributor-list fill through the per-element intermediate)
+    const char* ff = getenv("RAFEM_FUSED_FILL");
+    const bool fused = !(ff && ff[0] == '0') && !warp_fill;
+    if (!fused && !warp_fill && !m->slot_lists_tried)
         if (int rc = mesh_slot_lists(m)) return rc;
     const AsmMesh am = asm_mesh(m);
     const AsmFields f{t_it, ts, v_it, vs, t_prev, ps, dt};
     double2* contrib = reinterpret_cast<double2*>(s->contrib);
     double2* val2 = reinterpret_cast<double2*>(s->val2);
     RF_CUDA_TRY(ctx, cudaMemsetAsync(bad_dev, 0xff, sizeof(long long), st));
+    if (fused) {
+        if (int rc = system_escal(s)) return rc;
+        if (M > 0) {
+            element_scalars_kernel<<<(M + 255) / 256, 256, 0, st>>>(am, f, s->esig, s->eload,
+                                                                    reinterpret_cast<unsigned long long*>(bad_dev));
+            ctx->launches++;
+        }
+        if (N > 0) {
+            const char* hf = getenv("RAFEM_HALF_FILL");
+            if (m->maxdeg <= 16 && m->maxinc <= 32 && m->nreg <= kFillRegions && !(hf && hf[0] == '0')) {
+                const long long blocks = ((long long)N * 16 + 255) / 256;
+                fused_fill_half_kernel<<<(unsigned)blocks, 256, 0, st>>>(am, dt, s->esig, s->eload, val2, s->rhs,
+                                                                         s->diagpart);
+            } else {
+                const long long blocks = ((long long)N * 32 + 255) / 256;
+                fused_fill_kernel<<<(unsigned)blocks, 256, 0, st>>>(am, dt, s->esig, s->eload, val2, s->rhs,
+                                                                    s->diagpart);
+            }
+            ctx->launches++;
+        }
+        RF_CUDA_TRY(ctx, cudaGetLastError());
+        return RAFEM_OK;
+    }
+    if (int rc = system_contrib(s)) return rc;
+    contrib = reinterpret_cast<double2*>(s->contrib);
     if (M > 0) {
         element_kernel<<<(M + kElemBlock - 1) / kElemBlock, kElemBlock, 0, st>>>(am, f, contrib, s->load,
                                                         reinterpret_cast<unsigned long long*>(bad_dev));
@@ -749,6 +842,28 @@ int assemble_fill_launch(rafem_system* s, const double* t_it, int ts, const doub
     return RAFEM_OK;
 }
 
+// V-row scaling + Dirichlet elimination (fem.py:394-428) of the filled rows:
+// 16 lanes per row when rows have at most 16 slots (RAFEM_HALF_FILL=0: a warp)
+static int constrain_launch(rafem_system* s, const rafem_assemble_params& p, const double* scale_dev) {
+    rafem_mesh* m = s->mesh;
+    rafem_ctx* ctx = m->ctx;
+    const char* hf = getenv("RAFEM_HALF_FILL");
+    if (m->maxdeg <= 16 && !(hf && hf[0] == '0')) {
+        const int blocks = (int)(((long long)m->N * 16 + 255) / 256);
+        constrain_half_kernel<<<blocks, 256, 0, ctx->stream>>>(asm_mesh(m), scale_dev, p.apply_constraints,
+                                                               p.applied_voltage, p.boundary_temp,
+                                                               reinterpret_cast<double2*>(s->val2), s->rhs);
+    } else {
+        const int blocks = (int)(((long long)m->N * 32 + 255) / 256);
+        constrain_kernel<<<blocks, 256, 0, ctx->stream>>>(asm_mesh(m), scale_dev, p.apply_constraints,
+                                                          p.applied_voltage, p.boundary_temp,
+                                                          reinterpret_cast<double2*>(s->val2), s->rhs);
+    }
+    ctx->launches++;
+    RF_CUDA_TRY(ctx, cudaGetLastError());
+    return RAFEM_OK;
+}
+
 // equilibration by a given (already reduced) scale + Dirichlet elimination
 int assemble_constrain_launch(rafem_system* s, const rafem_assemble_params& p, double scale) {
     rafem_mesh* m = s->mesh;
@@ -756,11 +871,7 @@ int assemble_constrain_launch(rafem_system* s, const rafem_assemble_params& p, d
     double* scale_dev = reinterpret_cast<double*>(s->status) + 104;
     RF_CUDA_TRY(ctx, cudaMemcpyAsync(scale_dev, &scale, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     if (m->N > 0) {
-        const int blocks = (int)(((long long)m->N * 32 + 255) / 256);
-        constrain_kernel<<<blocks, 256, 0, ctx->stream>>>(asm_mesh(m), scale_dev, p.apply_constraints,
-                                                          p.applied_voltage, p.boundary_temp,
-                                                          reinterpret_cast<double2*>(s->val2), s->rhs);
-        ctx->launches++;
+        if (int rc = constrain_launch(s, p, scale_dev)) return rc;
     }
     RF_CUDA_TRY(ctx, cudaGetLastError());
     return RAFEM_OK;
@@ -777,9 +888,9 @@ int assemble_launch(rafem_system* s, const double* t_it, int ts, const double* v
     if (N > 0) {
         const int blocks = (int)(((long long)N * 32 + 255) / 256);
         if (int rc = diag_sums_launch(ctx, s->diagpart, N, p.equilibrate, nullptr, scale_dev)) return rc;
-        constrain_kernel<<<blocks, 256, 0, st>>>(asm_mesh(m), scale_dev, p.apply_constraints, p.applied_voltage,
-                                                 p.boundary_temp, reinterpret_cast<double2*>(s->val2), s->rhs);
-        ctx->launches += 1;
+        (void)blocks;
+        (void)st;
+        if (int rc = constrain_launch(s, p, scale_dev)) return rc;
     } else {
         RF_CUDA_TRY(ctx, cudaMemcpyAsync(scale_dev, &s->scale, sizeof(double), cudaMemcpyHostToDevice, st));
     }

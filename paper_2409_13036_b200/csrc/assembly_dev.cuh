@@ -37,6 +37,7 @@ struct AsmMesh {
     const int* cpos;      // 16 M: slot-list position of contribution 16 e + 4 a + b (null: tet-major)
     const int* lpos;      // 4 M: incidence-list position of load 4 e + a
     int N, M;
+    int own_end, below_end;  // rafem_mesh::own_end / below_end (N, N: natural order)
 };
 
 // nodal fields with strides (host inputs are contiguous N-arrays; the device
@@ -229,6 +230,232 @@ RF_DEV void fill_node_warp(int i, const AsmMesh& m, const double2* contrib, cons
     }
 }
 
+// Per-element scalars of the fused fill (element_scalars_kernel): sigma(Tbar)
+// and the four T-rhs loads, with element_core's arithmetic operation for
+// operation (the same bits).  Returns true when sigma <= 0.
+RF_DEV bool element_scalars(int e, const AsmMesh& m, const AsmFields& f, double* sig, double* load4) {
+    int nd[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) nd[k] = __ldg(m.tets + 4 * e + k);
+    const int rg = __ldg(m.region + e);
+    const double rcdt = m.regtab[m.nreg + rg] / f.dt;
+    const double sigma0 = m.regtab[2 * m.nreg + rg], alpha = m.regtab[3 * m.nreg + rg];
+    const double tref = m.regtab[4 * m.nreg + rg];
+    double g[12];
+    const double2* gp = reinterpret_cast<const double2*>(m.grad + 12LL * e);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        const double2 q = __ldg(gp + k);
+        g[2 * k] = q.x;
+        g[2 * k + 1] = q.y;
+    }
+    const double vol = __ldg(m.vol + e);
+    double tv[4], vv[4], tp[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        tv[k] = __ldcg(f.t + (long long)f.ts * nd[k]);
+        vv[k] = __ldcg(f.v + (long long)f.vs * nd[k]);
+        tp[k] = __ldcg(f.tp + (long long)f.ps * nd[k]);
+    }
+    double tsum = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tsum = add(tsum, tv[k]);
+    const double tbar = tsum / 4.0;
+    const double sigma = mul(sigma0, add(1.0, mul(alpha, sub(tbar, tref))));
+    const double mdia = mul(vol, 0.1), moff = mul(vol, 0.05);
+    double gv[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) gv[d] = add(gv[d], mul(vv[k], g[3 * k + d]));
+    const double gg = add(add(mul(gv[0], gv[0]), mul(gv[2], gv[2])), mul(gv[1], gv[1]));
+    const double fj = mul(mul(sigma, gg), vol) / 4.0;
+    const double mo = mul(rcdt, moff), md = mul(rcdt, mdia);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        double t[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) t[b] = mul(a == b ? md : mo, tp[b]);
+        load4[a] = add(add(add(t[0], t[2]), add(t[1], t[3])), fj);
+    }
+    *sig = sigma;
+    return sigma <= 0.0;  // fem.py:274
+}
+
+// Row a of element e: the four (V, T) contributions (a, b = 0..3) from the
+// stored base row, the volume, the region's k and rho_c / dt and the
+// element's sigma (element_core's arithmetic, the same bits).
+RF_DEV void element_row(int e, int a, const AsmMesh& m, double dt, const double* sig, double2* out4) {
+    const int rg = __ldg(m.region + e);
+    const double kk = m.regtab[rg];
+    const double rcdt = m.regtab[m.nreg + rg] / dt;
+    const double vol = __ldg(m.vol + e);
+    const double sigma = __ldcg(sig + e);
+    const double mdia = mul(vol, 0.1), moff = mul(vol, 0.05);
+    const double* b10 = m.base + 10LL * e;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const int lo = a < b ? a : b, hi = a < b ? b : a;
+        const double bab = __ldg(b10 + lo * 4 - (lo * (lo - 1)) / 2 + (hi - lo));
+        const double mass = a == b ? mdia : moff;
+        out4[b] = make_double2(mul(sigma, bab), add(mul(rcdt, mass), mul(kk, bab)));
+    }
+}
+
+// Node row i, one warp, element phase fused into the fill: lane p computes
+// row a of its incident element p (ascending element order) in registers
+// from the element's stored geometry and its sigma (element_scalars), stages
+// the four contributions, their row offsets and the load in shared memory,
+// and every lane (slot l) then walks the incidences in order adding what
+// lands on its column — fill_node_warp's summation with the contributions
+// computed instead of read back from HBM (bit-identical).
+RF_DEV void fill_node_fused(int i, const AsmMesh& m, double dt, const double* sig, const double* load4,
+                            double2* out, double* rhs, double* diag_raw, FillScratch& ws) {
+    const int lane = threadIdx.x & 31;
+    const int deg = __ldg(m.rp + i + 1) - __ldg(m.rp + i);
+    const int p0 = __ldg(m.inc_ptr + i), ninc = __ldg(m.inc_ptr + i + 1) - p0;
+    const int dslot = __ldg(m.diag + i);
+    // one pass over the incidences when the row fits a warp (box meshes);
+    // longer rows recompute per 32-slot chunk
+    for (int cb = 0; cb < deg; cb += 32) {
+        const int l = cb + lane;
+        double accV = 0.0, accT = 0.0, racc = 0.0;
+        for (int pc = 0; pc < ninc; pc += 32) {
+            const int p = pc + lane;
+            if (p < ninc) {
+                const unsigned ea = __ldg(m.inc_ea + p0 + p);
+                const int e = (int)(ea & 0x3fffffffu), a = (int)(ea >> 30);
+                ws.off[lane] = __ldg(m.inc_slot + p0 + p);
+                element_row(e, a, m, dt, sig, ws.c[lane]);
+                ws.ld[lane] = __ldcg(load4 + 4LL * e + a);
+            }
+            __syncwarp();
+            // a tet holds column l at most once: one SIMD byte compare finds
+            // which of its four row offsets (if any) is this lane's slot
+            const int nq = min(32, ninc - pc);
+            const unsigned lrep = (unsigned)l * 0x01010101u;
+            for (int q = 0; q < nq; ++q) {
+                const unsigned hit = __vcmpeq4(ws.off[q], lrep);
+                if (hit) {
+                    const double2 c = ws.c[q][(__ffs(hit) - 1) >> 3];
+                    accV = add(accV, c.x);
+                    accT = add(accT, c.y);
+                }
+                if (lane == 0) racc = add(racc, ws.ld[q]);
+            }
+            __syncwarp();
+        }
+        if (l < deg) {
+            out[l] = make_double2(accV, accT);
+            if (l == dslot) {
+                diag_raw[2LL * i] = accV;
+                diag_raw[2LL * i + 1] = accT;
+            }
+        }
+        if (cb == 0 && lane == 0) {
+            rhs[2LL * i] = 0.0;
+            rhs[2LL * i + 1] = racc;
+        }
+    }
+    if (dslot < 0 && lane == 0) {
+        diag_raw[2LL * i] = 0.0;
+        diag_raw[2LL * i + 1] = 0.0;
+    }
+}
+
+// The same with 16 lanes per row, two rows per warp (rows of at most 16
+// slots and 32 incident elements, e.g. Kuhn boxes: 15 and 24): twice the
+// rows in flight per warp and half the accumulation instructions per row.
+// A lane's (up to) two incidences issue all their loads before either is
+// computed; the region's k and rho_c / dt come from a per-block table (rk,
+// rrc; the same IEEE quotient).  Same per-contribution arithmetic and order.
+struct RowLoads {
+    double bab[4], vol, sigma, ld;
+    int rg;
+};
+RF_DEV void row_loads(unsigned ea, const AsmMesh& m, const double* sig, const double* load4, RowLoads& r) {
+    const int e = (int)(ea & 0x3fffffffu), a = (int)(ea >> 30);
+    r.rg = __ldg(m.region + e);
+    r.vol = __ldg(m.vol + e);
+    r.sigma = __ldcg(sig + e);
+    r.ld = __ldcg(load4 + 4LL * e + a);
+    const double* b10 = m.base + 10LL * e;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const int lo = a < b ? a : b, hi = a < b ? b : a;
+        r.bab[b] = __ldg(b10 + lo * 4 - (lo * (lo - 1)) / 2 + (hi - lo));
+    }
+}
+RF_DEV void row_contrib(unsigned ea, const RowLoads& r, const double* rk, const double* rrc, double2* out4) {
+    const int a = (int)(ea >> 30);
+    const double kk = rk[r.rg], rcdt = rrc[r.rg];
+    const double mdia = mul(r.vol, 0.1), moff = mul(r.vol, 0.05);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const double mass = a == b ? mdia : moff;
+        out4[b] = make_double2(mul(r.sigma, r.bab[b]), add(mul(rcdt, mass), mul(kk, r.bab[b])));
+    }
+}
+RF_DEV void fill_node_fused_half(int i, const AsmMesh& m, const double* rk, const double* rrc, const double* sig,
+                                 const double* load4, double2* val2, double* rhs, double* diag_raw, FillScratch& ws) {
+    const int lane = threadIdx.x & 31, hl = lane & 15;
+    const unsigned hmask = 0xffffu << (lane & 16);
+    const int r0 = __ldg(m.rp + i), deg = __ldg(m.rp + i + 1) - r0;
+    const int p0 = __ldg(m.inc_ptr + i), ninc = __ldg(m.inc_ptr + i + 1) - p0;
+    const int dslot = __ldg(m.diag + i);
+    const bool ha = hl < ninc, hb = hl + 16 < ninc;
+    unsigned ea = 0, eb = 0;
+    if (ha) {
+        ea = __ldg(m.inc_ea + p0 + hl);
+        ws.off[hl] = __ldg(m.inc_slot + p0 + hl);
+    }
+    if (hb) {
+        eb = __ldg(m.inc_ea + p0 + hl + 16);
+        ws.off[hl + 16] = __ldg(m.inc_slot + p0 + hl + 16);
+    }
+    RowLoads la, lb;
+    if (ha) row_loads(ea, m, sig, load4, la);
+    if (hb) row_loads(eb, m, sig, load4, lb);
+    if (ha) {
+        row_contrib(ea, la, rk, rrc, ws.c[hl]);
+        ws.ld[hl] = la.ld;
+    }
+    if (hb) {
+        row_contrib(eb, lb, rk, rrc, ws.c[hl + 16]);
+        ws.ld[hl + 16] = lb.ld;
+    }
+    __syncwarp(hmask);
+    // branch-free walk: every lane reads the (q, b) entry its column would
+    // take and adds it only on a hit (an add of the untaken value would
+    // change nothing but the bits of -0.0; the select keeps them exact)
+    double accV = 0.0, accT = 0.0, racc = 0.0;
+    const unsigned lrep = (unsigned)hl * 0x01010101u;
+#pragma unroll 4
+    for (int q = 0; q < ninc; ++q) {
+        const unsigned hit = __vcmpeq4(ws.off[q], lrep);
+        const double2 c = ws.c[q][(__ffs(hit | 0x80000000u) - 1) >> 3];
+        const double av = add(accV, c.x), at = add(accT, c.y);
+        accV = hit ? av : accV;
+        accT = hit ? at : accT;
+        racc = add(racc, ws.ld[q]);  // (used by lane 0 only)
+    }
+    if (hl < deg) {
+        val2[r0 + hl] = make_double2(accV, accT);
+        if (hl == dslot) {
+            diag_raw[2LL * i] = accV;
+            diag_raw[2LL * i + 1] = accT;
+        }
+    }
+    if (hl == 0) {
+        rhs[2LL * i] = 0.0;
+        rhs[2LL * i + 1] = racc;
+        if (dslot < 0) {
+            diag_raw[2LL * i] = 0.0;
+            diag_raw[2LL * i + 1] = 0.0;
+        }
+    }
+}
+
 // Slot s: sum of its contributions in ascending element order (the
 // reference's duplicate-summation order, fem.py:381-387 + sparse.py:180-190),
 // every load of the list issued before the first add.  Same bits as
@@ -378,17 +605,30 @@ RF_DEV void constrain_node_warp(int i, const AsmMesh& m, double scale, int apply
                 dT = outT;
             }
         }
-        // moved-column terms in storage order; most rows have none
-        unsigned bv = __ballot_sync(0xffffffffu, movV), bt = __ballot_sync(0xffffffffu, movT);
-        while (bv) {
-            const int t = __ffs(bv) - 1;
-            bv &= bv - 1;
-            mV = add(mV, __shfl_sync(0xffffffffu, termV, t));
-        }
-        while (bt) {
-            const int t = __ffs(bt) - 1;
-            bt &= bt - 1;
-            mT = add(mT, __shfl_sync(0xffffffffu, termT, t));
+        // moved-column terms in global column order (= storage order except
+        // on shard meshes, whose below-owner ghosts are stored after the
+        // owned columns: those lanes go first); most rows have none
+        const unsigned bv = __ballot_sync(0xffffffffu, movV), bt = __ballot_sync(0xffffffffu, movT);
+        if (bv | bt) {
+            const int jc = l < deg ? cols[l] : 0x7fffffff;
+            const unsigned gb = __ballot_sync(0xffffffffu, jc >= m.own_end && jc < m.below_end);
+            const unsigned groups[3] = {gb, ~gb & __ballot_sync(0xffffffffu, jc < m.own_end), 0xffffffffu};
+            unsigned done = 0;
+#pragma unroll
+            for (int gi = 0; gi < 3; ++gi) {
+                unsigned gv = bv & groups[gi] & ~done, gt = bt & groups[gi] & ~done;
+                done |= groups[gi];
+                while (gv) {
+                    const int t = __ffs(gv) - 1;
+                    gv &= gv - 1;
+                    mV = add(mV, __shfl_sync(0xffffffffu, termV, t));
+                }
+                while (gt) {
+                    const int t = __ffs(gt) - 1;
+                    gt &= gt - 1;
+                    mT = add(mT, __shfl_sync(0xffffffffu, termT, t));
+                }
+            }
         }
     }
     if (minv && dslot >= 0) {
@@ -411,6 +651,73 @@ RF_DEV void constrain_node_warp(int i, const AsmMesh& m, double scale, int apply
             minv[2LL * i] = 1.0 / dV;
             minv[2LL * i + 1] = 1.0 / dT;
         }
+    }
+}
+
+
+// Node row i, 16 lanes (rows of at most 16 slots, two rows per warp): the
+// same per-slot arithmetic and moved-column order as constrain_node_warp
+// (global column order on shard meshes), bit-identical rows with half the
+// instructions per row.
+RF_DEV void constrain_node_half(int i, const AsmMesh& m, double scale, int apply, double applied, double btemp,
+                                double2* vals, double* rhs) {
+    const int lane = threadIdx.x & 31, hl = lane & 15, hb = lane & 16;
+    const unsigned hmask = 0xffffu << hb;
+    const int s0 = __ldg(m.rp + i), deg = __ldg(m.rp + i + 1) - s0;
+    const int kV = apply ? m.kind[2LL * i] : 0, kT = apply ? m.kind[2LL * i + 1] : 0;
+    double termV = 0.0, termT = 0.0;
+    int movV = 0, movT = 0, jc = 0x7fffffff;
+    if (hl < deg) {
+        const int j = __ldg(m.col + s0 + hl);
+        jc = j;
+        const int cV = apply ? m.kind[2LL * j] : 0, cT = apply ? m.kind[2LL * j + 1] : 0;
+        const double2 v = vals[s0 + hl];
+        const double vs = mul(v.x, scale);
+        if (!kV && cV) {
+            movV = 1;
+            termV = mul(vs, dof_value(cV, applied, btemp));
+        }
+        if (!kT && cT) {
+            movT = 1;
+            termT = mul(v.y, dof_value(cT, applied, btemp));
+        }
+        double outV = vs, outT = v.y;
+        if (kV || cV) outV = (kV && j == i) ? 1.0 : 0.0;
+        if (kT || cT) outT = (kT && j == i) ? 1.0 : 0.0;
+        vals[s0 + hl] = make_double2(outV, outT);
+    }
+    double mV = 0.0, mT = 0.0;
+    const unsigned bv = (__ballot_sync(hmask, movV) >> hb) & 0xffffu;
+    const unsigned bt = (__ballot_sync(hmask, movT) >> hb) & 0xffffu;
+    if (bv | bt) {
+        const unsigned gb = (__ballot_sync(hmask, jc >= m.own_end && jc < m.below_end) >> hb) & 0xffffu;
+        const unsigned ob = (__ballot_sync(hmask, jc < m.own_end) >> hb) & 0xffffu;
+        const unsigned groups[3] = {gb, ~gb & ob, 0xffffu};
+        unsigned done = 0;
+#pragma unroll
+        for (int gi = 0; gi < 3; ++gi) {
+            unsigned gv = bv & groups[gi] & ~done, gt = bt & groups[gi] & ~done;
+            done |= groups[gi];
+            while (gv) {
+                const int t = __ffs(gv) - 1;
+                gv &= gv - 1;
+                mV = add(mV, __shfl_sync(hmask, termV, t + hb));
+            }
+            while (gt) {
+                const int t = __ffs(gt) - 1;
+                gt &= gt - 1;
+                mT = add(mT, __shfl_sync(hmask, termT, t + hb));
+            }
+        }
+    }
+    if (hl == 0) {
+        double rv = 0.0, rt = rhs[2LL * i + 1];
+        if (apply) {
+            rv = kV ? dof_value(kV, applied, btemp) : sub(rv, mV);
+            rt = kT ? dof_value(kT, applied, btemp) : sub(rt, mT);
+        }
+        rhs[2LL * i] = rv;
+        rhs[2LL * i + 1] = rt;
     }
 }
 

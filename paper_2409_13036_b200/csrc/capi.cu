@@ -512,6 +512,17 @@ int32_t rafem_mesh_stencil_classes(rafem_mesh* m) {
     return m->ncls;
 }
 
+int rafem_mesh_set_shard_order(rafem_mesh* m, int64_t n_owned, int64_t n_below) {
+    if (!m) return RAFEM_ERR_INVALID;
+    if (n_owned < 0 || n_below < 0 || n_owned + n_below > m->N)
+        return rafem_fail(m->ctx, RAFEM_ERR_INVALID, "shard order: owned + below-owner ghosts exceed the nodes");
+    if (m->maxdeg > 32 && n_below > 0)
+        return rafem_fail(m->ctx, RAFEM_ERR_UNSUPPORTED, "shard order: rows longer than 32 slots");
+    m->own_end = (int)n_owned;
+    m->below_end = (int)(n_owned + n_below);
+    return RAFEM_OK;
+}
+
 int rafem_mesh_pattern(rafem_mesh* m, int64_t* node_row_ptr, int32_t* node_col) {
     if (!m) return RAFEM_ERR_INVALID;
     rafem_ctx* ctx = m->ctx;
@@ -533,8 +544,8 @@ int rafem_system_create(rafem_mesh* m, rafem_system** out) {
 #define RF_SS(x) do { e = (x); if (e != cudaSuccess) { rafem_system_destroy(s); return rafem_fail_cuda(ctx, e, #x, __FILE__, __LINE__); } } while (0)
     RF_SS(dmalloc(ctx, (void**)&s->val2, sizeof(double) * 2 * S));
     RF_SS(dmalloc(ctx, (void**)&s->rhs, sizeof(double) * 2 * N));
-    RF_SS(dmalloc(ctx, (void**)&s->contrib, sizeof(double) * 32 * M));
-    RF_SS(dmalloc(ctx, (void**)&s->load, sizeof(double) * 4 * M));
+    // s->contrib / s->load (288 B per tet) only for the paths that stage
+    // per-element outputs: system_contrib() allocates them on first use
     RF_SS(dmalloc(ctx, (void**)&s->diagpart, sizeof(double) * 2 * N));
     RF_SS(dmalloc(ctx, (void**)&s->minv, sizeof(double) * 2 * N));
     RF_SS(dmalloc(ctx, (void**)&s->xin, sizeof(double) * (3 * N + 2 * S)));  // host inputs / dof expansion
@@ -549,7 +560,8 @@ int rafem_system_create(rafem_mesh* m, rafem_system** out) {
 void rafem_system_destroy(rafem_system* s) {
     if (!s) return;
     if (s->kp) rafem_kp_destroy(s->kp);
-    for (void* p : {(void*)s->val2, (void*)s->rhs, (void*)s->contrib, (void*)s->load, (void*)s->diagpart,
+    for (void* p : {(void*)s->val2, (void*)s->rhs, (void*)s->contrib, (void*)s->load, (void*)s->esig,
+                    (void*)s->eload, (void*)s->diagpart,
                     (void*)s->minv, (void*)s->xin, (void*)s->status, (void*)s->xs})
         if (p) dfree(s->mesh->ctx, p);
     delete s;

@@ -147,6 +147,10 @@ struct rafem_mesh {
     int* rp = nullptr;        // N + 1
     int* col = nullptr;       // slots
     int* diag = nullptr;      // N: slot offset of the diagonal within its row
+    // shard meshes: local ids [own_end, below_end) are ghosts whose global
+    // ids precede the owned block; the constraint sums walk each row in
+    // global column order (below ghosts, owned, the rest).  -1: natural order
+    int own_end = -1, below_end = -1;
     int* inc_ptr = nullptr;   // N + 1
     unsigned* inc_ea = nullptr;   // 4M: tet | (local index << 30)
     unsigned* inc_slot = nullptr; // 4M: 4 x uint8 row offsets of the tet's nodes
@@ -171,6 +175,8 @@ struct rafem_system {
     double* rhs = nullptr;    // 2N
     double* contrib = nullptr; // M x 16 x (V, T) element block contributions
     double* load = nullptr;   // M x 4 T-rhs element contributions
+    double* esig = nullptr;   // M: sigma(Tbar) per element (fused fill)
+    double* eload = nullptr;  // M x 4: T-rhs loads per element (fused fill)
     double* diagpart = nullptr; // 2 x G partial diag sums
     double* minv = nullptr;   // 2N
     double* xin = nullptr;    // 3N staging for host inputs / 2N iterate buffers
@@ -238,6 +244,10 @@ int assemble_constrain_launch(rafem_system* s, const rafem_assemble_params& p, d
 int diag_sums_launch(rafem_ctx* ctx, const double* diag_raw, int n, int equilibrate, double* sums_dev,
                      double* scale_dev);
 int expand_dof_vals(rafem_system* s, double* out_dev);
+// per-element contribution / load buffers of a system, allocated on first use
+int system_contrib(rafem_system* s);
+// per-element scalars of the fused fill (sigma, 4 loads), allocated on first use
+int system_escal(rafem_system* s);
 int predictor_launch(rafem_ctx* ctx, double* x_it, const double* x_acc, const double* x_prev,
                      int N, int step, double ratio,
                      double* x_start = nullptr);

@@ -726,15 +726,28 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
                 // ||w - V c||^2 = ||w||^2 - ||c||^2 (V orthonormal, c = V^T w, tiny
                 // after the first pass): no third reduction, only the barrier
                 // that makes the new w visible to the next SpMV's gathers
+                // Near an invariant subspace ||c||^2 approaches ||w||^2 and the
+                // difference cancels: then (same decision on every CTA, the
+                // scalars are identical) the norm is reduced explicitly.
                 double cc = 0.0;
                 for (int i = 0; i <= k; ++i) cc = add(cc, mul(co[i], co[i]));
-                hk1 = sqrt(fmax(sub(co[k + 1], cc), 0.0));
+                const bool explicit_norm = cc > 1e-8 * co[k + 1];
+                double v[1] = {0.0};
                 for (int e = lo + tid; e < hi; e += bd) {
                     double acc = wk[e];
                     for (int i = 0; i <= k; ++i) acc = sub(acc, mul(co[i], vrow(i)[e]));
                     wk[e] = acc;
+                    v[0] = add(v[0], mul(acc, acc));
                 }
-                sy.barrier();
+                if (explicit_norm) {
+                    P = a.partial + par * pstride;
+                    sy.template reduce<1>(v, 1, P, co, red);
+                    par ^= 1;
+                    hk1 = sqrt(co[0]);
+                } else {
+                    hk1 = sqrt(sub(co[k + 1], cc));
+                    sy.barrier();
+                }
             }
             // w -= sum c_i v_i ; ||w||
             else {
@@ -2842,6 +2855,7 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
         const char* nv = getenv("RAFEM_NO_VX0");
         S.vx0 = !(nv && nv[0] == '1');
     }
+    if (int rc = system_contrib(s)) return rc;
     S.contrib = reinterpret_cast<double2*>(s->contrib);
     S.load = s->load;
     S.rhs = s->rhs;

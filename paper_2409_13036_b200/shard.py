@@ -501,6 +501,11 @@ class ShardedSystem:
         self.material = material
         self.lmesh = local_mesh(mesh, self.plan)
         self.dm = DeviceMesh(self.lmesh, material)
+        # below-owner ghosts precede the owned block in global order: the
+        # constraint sums follow global column order (owned rhs bitwise the
+        # unsharded one)
+        n_below = int(np.count_nonzero(self.plan.ghosts < self.plan.lo))
+        nat.check(nat.lib().rafem_mesh_set_shard_order(self.dm.handle, self.plan.n_own, n_below), "shard order")
         self.h = SystemHandle(self.dm)
         self.engine = KPDeviceEngine(self.h.handle, self.plan.n_own, self.plan.n_ext, nranks, rank,
                                      self.plan.send_index())

@@ -388,3 +388,29 @@ def test_first_pass_solver_start_extrapolates_v_without_changing_the_run():
         assert np.max(np.abs(a.T - b.T)) <= 1e-6 * np.max(np.abs(b.T))
         assert np.max(np.abs(a.V - b.V)) <= 1e-6 * np.max(np.abs(b.V))
     _compare_run(new, golden("run_B900_1e-10"), 1e-6, every_step=False)
+
+
+@pytest.mark.parametrize("dims", [(30, 28, 31), (4, 3, 5)])
+def test_fused_element_fill_is_bitwise_the_two_kernel_fill(dims, monkeypatch):
+    """The fused element + fill (one warp per node row computes its incident
+    elements' rows in registers; default) sums the same contributions in
+    the same order as the element kernel + contributor-list fill
+    (RAFEM_FUSED_FILL=0): values, rhs and scale are bit-identical, also with
+    two material regions."""
+    from paper_2409_13036_b200 import (MaterialParams, RegionMaterial, SimConfig, assemble_global,
+                                       generate_box_mesh)
+    mesh = generate_box_mesh(*dims)
+    n = mesh.node_count
+    rng = np.random.default_rng(11)
+    mesh.regions = (rng.random(mesh.tet_count) < 0.3).astype(np.int64)
+    mat = MaterialParams({0: RegionMaterial(), 1: RegionMaterial(k=0.9e-3, rho_c=2.5e-3, sigma0=0.35e-3,
+                                                                  alpha=0.01)})
+    t, v = 37.0 + 30 * rng.random(n), 25 * rng.random(n)
+    out = []
+    for mode in ("1", "0"):
+        monkeypatch.setenv("RAFEM_FUSED_FILL", mode)
+        for kw in ({}, dict(apply_constraints=False, equilibrate=False)):
+            s = assemble_global(mesh, mat, SimConfig(), t, v, t, 0.5, **kw)
+            out.append((s.matrix.vals.copy(), s.rhs.copy(), s.voltage_row_scale))
+    for a, b in zip(out[:2], out[2:]):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
