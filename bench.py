@@ -394,6 +394,8 @@ def run_ours(args):
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": traffic,
+                "traffic_source": ("DRAM bytes of one launch from the committed ncu --set full capture "
+                                   "(profiles/traffic.json), not measured in this run") if traffic else None,
                 "kernel": ("simulate_kernel (whole 900 s run in one cooperative launch)" if fused
                            else f"{args.backend}_grid_kernel (persistent solve)"),
                 "launches": launches, "avg_launch_us": 1e3 * launch_ms,
@@ -700,9 +702,14 @@ def c4_leg(hbm_peak, peak_src, world, rank, local):
         ach_sp = b_sp / (msb.value / 1e3) / 1e9
         spmv = {"bound": "hbm", "achieved": ach_sp, "peak": hbm_peak, "unit": "GB/s", "frac": ach_sp / hbm_peak,
                 "frac_of_8TBs": ach_sp / 8000.0, "us_per_launch": 1e3 * msb.value, "bytes_per_launch": b_sp,
-                "explicit_columns_equivalent_GBs": b_ex / (msb.value / 1e3) / 1e9,
-                "kernel": "spmv_tma_pipe_kernel<384,2,stencil classes>" if cls_on else "spmv_tma_pipe_kernel<256,2>",
+                "kernel": "spmv_tma_pipe_kernel<192,2,stencil classes>" if cls_on else "spmv_tma_pipe_kernel<256,2>",
                 "l2": "flushed (256 MB write) before every timed launch"}
+        # the general-mesh layout (explicit int32 columns, 20 B per slot),
+        # measured on the same matrix: what an unstructured mesh streams
+        try:
+            spmv["explicit_columns"] = explicit_leg(sh, n, S1, b_ex, hbm_peak, x0, it)
+        except Exception as exc:  # noqa: BLE001
+            spmv["explicit_columns"] = {"error": str(exc)[:200]}
     ach = it * bytes_it / (dev_ms / 1e3) / 1e9 if dev_ms > 0 else 0.0
     # configs[3]'s run itself: 10 accepted steps (total_time 40 s), every
     # corrector pass re-assembled, fields resident in HBM on every shard
@@ -724,6 +731,41 @@ def c4_leg(hbm_peak, peak_src, world, rank, local):
             "bytes_per_iteration": bytes_it, "columns": "stencil classes" if cls_on else "explicit int32",
             "assembly_s": asm_s, "setup_s": setup_s, "spmv": spmv,
             "kernel": "kp_spmv_kernel + kp_update_kernel (csrc/shard.cu)"}
+
+
+def explicit_leg(sh, n, S, b_ex, hbm_peak, x0, it_classes, handle=None):
+    """SpMV and cold PCG with explicit int32 columns (RAFEM_NO_CLASSES=1:
+    no stencil classes, the layout of a general tetrahedral mesh) on a
+    single-shard system, timed like the class layout."""
+    import ctypes as C
+    from paper_2409_13036_b200 import SolverConfig
+    from paper_2409_13036_b200 import _native as nat
+    from paper_2409_13036_b200.shard import KPDeviceEngine, ShardedPCG
+    os.environ["RAFEM_NO_CLASSES"] = "1"
+    try:
+        ms = C.c_double()
+        h = handle if handle is not None else sh.h.handle
+        nat.check(nat.lib().rafem_system_spmv_bench(h, 10, 1, C.byref(ms)), "spmv bench")
+        eng = KPDeviceEngine(h, n, n, 1, 0, None)
+        pcg = ShardedPCG(eng, None, None, batch=16)
+        from paper_2409_13036_b200.krylov import _params
+        cfg = SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-10)
+        pcg.solve(None, x0, _params(cfg, nat.METHOD_PCG), 1 << 14)
+        _, st = pcg.solve(None, x0, _params(cfg, nat.METHOD_PCG), 1 << 14)
+        eng.close()
+    finally:
+        del os.environ["RAFEM_NO_CLASSES"]
+    it_bytes = 20 * S + 4 * (n + 1) + 14 * 16 * n
+    ach = b_ex / (ms.value / 1e3) / 1e9
+    pach = st.iterations * it_bytes / (st.device_ms / 1e3) / 1e9 if st.device_ms > 0 else 0.0
+    return {"spmv": {"us_per_launch": 1e3 * ms.value, "bytes_per_launch": b_ex, "achieved": ach,
+                     "frac": ach / hbm_peak, "unit": "GB/s", "l2": "flushed before every timed launch",
+                     "kernel": "spmv_tma_pipe_kernel<256,2> (explicit columns)"},
+            "pcg": {"iterations": st.iterations, "iterations_with_classes": it_classes,
+                    "us_per_iteration": 1e3 * st.device_ms / max(st.iterations, 1), "bytes_per_iteration": it_bytes,
+                    "achieved": pach, "frac": pach / hbm_peak, "unit": "GB/s",
+                    "kernel": "kp_spmv_kernel<explicit> + kp_update_kernel"},
+            "measured": "in this run (not rescaled)"}
 
 
 def time_loop_leg(sh, comm, world, local, hbm_peak, peak_src, bytes_it, cls_on, total=40.0):
@@ -855,6 +897,10 @@ def c3_leg(hbm_peak, peak_src, cpu_on=True):
     x, st = solve(s.matrix, s.rhs, x0=x0, config=SolverConfig(backend="pcg", precondition="jacobi"))
     del flush
     mode = nat.last_solve_mode()[0]
+    try:
+        expl = explicit_leg(None, N, S, b_explicit, hbm_peak, x0, st.iterations, handle=h.handle)
+    except Exception as exc:  # noqa: BLE001
+        expl = {"error": str(exc)[:200]}
     if mode == 4:  # kernel-per-phase engine: its SpMV bytes + 7 vector reads / 5 writes + u gather + w write
         it_bytes = ((16 * S + N) if cls_on else 20 * S) + 4 * (N + 1) + 14 * 16 * N
     else:
@@ -897,6 +943,8 @@ def c3_leg(hbm_peak, peak_src, cpu_on=True):
                                       "frac": b_paired / (ms_b2b.value / 1e3) / 1e9 / hbm_peak,
                                       "us_per_launch_without_pdl": 1e3 * ms_b2b_plain.value,
                                       "dram_bytes_per_launch": b2b_dram,
+                                      "dram_source": "committed ncu capture of launches inside such a chain "
+                                                     "(profiles/r1k_spmv_c3_back_to_back_ncu.txt), not this run",
                                       "dram_GBs": (b2b_dram / (ms_b2b.value / 1e3) / 1e9) if b2b_dram else None,
                                       "dram_frac": (b2b_dram / (ms_b2b.value / 1e3) / 1e9 / hbm_peak)
                                       if b2b_dram else None,
@@ -906,6 +954,7 @@ def c3_leg(hbm_peak, peak_src, cpu_on=True):
                                               "a launch's first tiles while the previous one drains; DRAM bytes per "
                                               "launch from ncu inside such a chain "
                                               "(profiles/r1k_spmv_c3_back_to_back_ncu.txt)"}},
+            "explicit_columns": expl,
             "pcg_cold_solve": {"l2": "flushed before the solve; iterations back to back",
                                "engine": {4: "kernel-per-phase (kp_spmv + kp_update)",
                                           3: "persistent TMA-streaming PCG"}.get(mode, str(mode)),

@@ -272,10 +272,29 @@ int rafem_kp_begin(rafem_kp* kp, const double* b, const double* x0, const rafem_
 #define RAFEM_KP_PACK_U_AFTER_HEAD 7
 #define RAFEM_KP_PACK_U 8
 int rafem_kp_launch(rafem_kp* kp, int32_t phase);
-/* nranks == 1: `iters` SPMV + UPDATE pairs back to back (one iteration each) */
+/* nranks == 1 (or connected with rafem_kp_ipc_connect): `iters` iterations
+ * back to back ([PACK_U +] SPMV + UPDATE each), no host round trip */
 int rafem_kp_iterate(rafem_kp* kp, int32_t iters);
 /* state (synchronises): flags bit0 done, bit1 need true residual, bit2 converged */
 int rafem_kp_state(rafem_kp* kp, int32_t* flags, int64_t* iterations, double* rel);
+/* Device-initiated data plane (one process per GPU of a node; also two
+ * processes sharing one GPU): instead of the caller's collectives between
+ * the phases, the phase kernels write the halo straight into the
+ * neighbours' ghost ranges and the 4 scalars into every peer's slot array
+ * through CUDA IPC mappings of the peers' kp blocks (NVLink peer memory),
+ * each exchange announced by a system-scope release of a sequence word that
+ * the consuming kernel acquires.  After connect, RAFEM_KP_PACK_* push,
+ * every phase waits for its inputs itself and rafem_kp_iterate runs any
+ * number of iterations without the host.
+ * export: this shard's 64-byte cudaIpcMemHandle_t and 4 byte offsets
+ * (x_ext, u_ext, slot array, flag block).  connect: every shard's handle and
+ * offsets (rank order; own entry ignored), the send segments (neighbour,
+ * [start, end) in send order, the neighbour's ghost node index of the
+ * segment's first entry) and the ranks this shard receives from. */
+int rafem_kp_ipc_export(rafem_kp* kp, void* handle, int64_t* offsets);
+int rafem_kp_ipc_connect(rafem_kp* kp, const void* handles, const int64_t* offsets, int32_t nseg,
+                         const int32_t* seg_peer, const int64_t* seg_start, const int64_t* seg_dst_node,
+                         int32_t n_recv_peers, const int32_t* recv_peers);
 /* owned x (host, 2*n_owned), SolveStats, history; returns the solve status */
 int rafem_kp_finish(rafem_kp* kp, double* x_out, rafem_solve_stats* st, double* hist, int64_t hist_cap,
                     int64_t* cycle_lens, int64_t cycle_cap);

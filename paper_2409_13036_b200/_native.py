@@ -118,6 +118,8 @@ _SIGS = {
     "rafem_kp_iterate": (i32, [vp, i32]),
     "rafem_kp_state": (i32, [vp, P(i32), P(i64), P(f64)]),
     "rafem_kp_finish": (i32, [vp, vp, P(SolveStatsC), vp, i64, vp, i64]),
+    "rafem_kp_ipc_export": (i32, [vp, vp, vp]),
+    "rafem_kp_ipc_connect": (i32, [vp, vp, vp, i32, vp, vp, vp, i32, vp]),
     "rafem_sl_create": (i32, [vp, P(vp)]),
     "rafem_sl_destroy": (None, [vp]),
     "rafem_sl_buffers": (i32, [vp, P(vp), P(vp)]),

@@ -68,6 +68,26 @@ struct KPState {
     double bnorm, alpha, beta, gamma, rel;
 };
 
+// Device-initiated data plane (rafem_kp_ipc_connect): every shard maps its
+// peers' kp blocks (CUDA IPC; NVLink peer memory across GPUs) and the phase
+// kernels move the halo and the scalar slots themselves — remote stores,
+// then a system-scope release of a per-(kind, sender) sequence word in the
+// receiver's flag block; consumers acquire it at kernel start.  No host
+// collective and no host round trip per iteration.
+constexpr int kIpcRanks = 8;  // shards per job on this path (one node)
+constexpr int kIpcKinds = 4;  // 0 halo of x, 1 halo of u, 2 scalar slots
+enum { kIpcX = 0, kIpcU = 1, kIpcS = 2 };
+struct KPIpc {
+    int rank, nranks, nseg;
+    unsigned send_mask, recv_mask, slot_mask;       // halo peers I send to / receive from; slot peers
+    int seg_start[kIpcRanks + 1];                   // send-index ranges per neighbour
+    int seg_peer[kIpcRanks];
+    double2* seg_dst[2][kIpcRanks];                 // [x | u] ghost range of me in the peer's vector
+    double* slot_dst[kIpcRanks];                    // peer's rank_part + 4 * rank
+    unsigned long long* peer_flags[kIpcRanks];      // peer's flag block
+    unsigned long long* my_flags;                   // kinds x ranks sequence words
+};
+
 struct KPArgs {
     MatView A;  // owned node rows; columns into the extended vector
     int n_own;
@@ -95,6 +115,8 @@ struct KPArgs {
     double2* send_buf;
     int n_send;
     int bufbytes, valcap;  // TMA tile buffers
+    const KPIpc* ipc;      // device-initiated halo / slots (null: the host's collectives)
+    unsigned long long seq_wait, seq_push;  // sequence numbers of this launch's exchange
 };
 
 RF_DEV bool kp_stopped(const KPState& s) { return s.done || s.need_head; }
@@ -216,6 +238,73 @@ RF_DEV double kp_fold(const double* part, int n, int stride, int j) {
     return warp_sum(s);
 }
 
+// ---- device-initiated exchange (KPIpc) ------------------------------------
+RF_DEV unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+RF_DEV void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+RF_DEV unsigned long long global_timer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// thread 0 of the CTA waits until every rank in `mask` has published
+// sequence >= seq for `kind`; the CTA's barrier then orders its reads after
+// the acquire.  A peer silent for 60 s traps instead of hanging the GPU.
+RF_DEV void ipc_wait(const KPIpc* ipc, int kind, unsigned mask, unsigned long long seq) {
+    if (threadIdx.x == 0) {
+        const unsigned long long t0 = global_timer();
+        for (int r = 0; r < ipc->nranks; ++r) {
+            if (!((mask >> r) & 1u)) continue;
+            const unsigned long long* f = ipc->my_flags + kind * kIpcRanks + r;
+            while (ld_acquire_sys(f) < seq) {
+                if (global_timer() - t0 > 60000000000ULL) asm volatile("trap;");
+                __nanosleep(64);
+            }
+        }
+    }
+    __syncthreads();
+}
+// one thread, after the data it announces is written (and fenced at
+// system scope by every writer): publish `seq` to every rank in `mask`
+RF_DEV void ipc_signal(const KPIpc* ipc, int kind, unsigned mask, unsigned long long seq) {
+    __threadfence_system();
+    for (int r = 0; r < ipc->nranks; ++r)
+        if ((mask >> r) & 1u) st_release_sys(ipc->peer_flags[r] + kind * kIpcRanks + ipc->rank, seq);
+}
+// the shard's 4 slot values to every peer's rank_part, then the signal
+// Slot regions alternate with the sequence parity: a peer two exchanges
+// ahead cannot exist (its next slot needs this shard's next halo, sent only
+// after this shard's update consumed the current slots), so two regions of
+// nranks x 4 doubles keep a fast peer from overwriting unread values.
+RF_DEV double* slot_region(const KPArgs& a, unsigned long long seq) {
+    return a.rank_part + (a.ipc ? 4LL * a.nranks * (long long)(seq & 1ULL) : 0LL);
+}
+RF_DEV void ipc_push_slots(const KPIpc* ipc, const double* o, unsigned long long seq) {
+    const long long par = 4LL * ipc->nranks * (long long)(seq & 1ULL);
+    for (int r = 0; r < ipc->nranks; ++r)
+        if ((ipc->slot_mask >> r) & 1u)
+            for (int j = 0; j < 4; ++j) ipc->slot_dst[r][par + j] = o[j];
+    ipc_signal(ipc, kIpcS, ipc->slot_mask, seq);
+}
+// last-CTA ticket whose writers fenced at system scope (remote stores)
+RF_DEV bool kp_last_cta_sys(unsigned* counter) {
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const unsigned t = atomicAdd(counter, 1u);
+        last = t == gridDim.x - 1;
+        if (last) *counter = 0u;
+    }
+    __syncthreads();
+    return last;
+}
+
 // ---- kernels --------------------------------------------------------------
 
 // ||b||^2 partial of this shard -> rank_part[rank].x
@@ -231,9 +320,10 @@ __global__ void __launch_bounds__(KPU) kp_bnorm_kernel(KPArgs a) {
     if (kp_last_cta(a.counter) && threadIdx.x < 32) {
         const double s = kp_fold(a.partA, gridDim.x, 1, 0);
         if (threadIdx.x == 0) {
-            double* o = a.rank_part + 4LL * a.rank;
+            double* o = slot_region(a, a.seq_push) + 4LL * a.rank;
             o[0] = s;
             o[1] = o[2] = o[3] = 0.0;
+            if (a.ipc) ipc_push_slots(a.ipc, o, a.seq_push);
         }
     }
 }
@@ -241,9 +331,11 @@ __global__ void __launch_bounds__(KPU) kp_bnorm_kernel(KPArgs a) {
 // bnorm from the gathered shard slots; initial state in st[0]
 __global__ void kp_bnorm_finish_kernel(KPArgs a) {
     pdl_begin();
+    if (a.ipc) ipc_wait(a.ipc, kIpcS, a.ipc->slot_mask, a.seq_wait);
     if (threadIdx.x != 0) return;
     double s = 0.0;
-    for (int q = 0; q < a.nranks; ++q) s = add(s, a.rank_part[4LL * q]);
+    const double* rp = slot_region(a, a.seq_wait);
+    for (int q = 0; q < a.nranks; ++q) s = add(s, rp[4LL * q]);
     KPState st{};
     st.bnorm = sqrt(s);
     st.rel = INFINITY;
@@ -265,6 +357,7 @@ __global__ void __launch_bounds__(kpt<CLS>(), kpc<CLS>()) kp_head_kernel(KPArgs 
     __shared__ __align__(8) unsigned long long bar[kKpStages];
     __shared__ double red[64];
     if (a.st[idx].done) return;
+    if (a.ipc) ipc_wait(a.ipc, kIpcX, a.ipc->recv_mask, a.seq_wait);
     double v[2] = {0.0, 0.0};
     kp_sweep<CLS>(a, a.x, sm, bar, [&](int g, double yv, double yt) {
         const double2 bb = a.b[g];
@@ -292,6 +385,7 @@ __global__ void __launch_bounds__(kpt<CLS>(), kpc<CLS>()) kp_spmv_kernel(KPArgs 
     __shared__ double red[32];
     const KPState& st = a.st[idx];
     if (st.done || (!after_head && st.need_head)) return;
+    if (a.ipc) ipc_wait(a.ipc, kIpcU, a.ipc->recv_mask, a.seq_wait);
     double v[1] = {0.0};
     kp_sweep<CLS>(a, a.u, sm, bar, [&](int g, double yv, double yt) {
         const double2 uu = a.u[g];
@@ -304,11 +398,12 @@ __global__ void __launch_bounds__(kpt<CLS>(), kpc<CLS>()) kp_spmv_kernel(KPArgs 
         const double rr = kp_fold(a.partA, ga, 2, 1);
         const double wu = kp_fold(a.partB, gridDim.x, 1, 0);
         if (threadIdx.x == 0) {
-            double* o = a.rank_part + 4LL * a.rank;
+            double* o = slot_region(a, a.seq_push) + 4LL * a.rank;
             o[0] = ru;
             o[1] = wu;
             o[2] = rr;
             o[3] = 0.0;
+            if (a.ipc) ipc_push_slots(a.ipc, o, a.seq_push);
         }
     }
 }
@@ -322,11 +417,14 @@ __global__ void __launch_bounds__(KPU) kp_update_kernel(KPArgs a, int idx, int f
     __shared__ double co[3];
     KPState S = a.st[idx];
     const bool was_stopped = S.done || (!first && S.need_head);
+    if (a.ipc && !was_stopped) ipc_wait(a.ipc, kIpcS, a.ipc->slot_mask, a.seq_wait);
     if (threadIdx.x < 32) {  // gathered shard slots, rank order
         double t[3] = {0.0, 0.0, 0.0};
-        if (threadIdx.x == 0)
+        if (threadIdx.x == 0) {
+            const double* rp = slot_region(a, a.seq_wait);
             for (int q = 0; q < a.nranks; ++q)
-                for (int j = 0; j < 3; ++j) t[j] = add(t[j], a.rank_part[4LL * q + j]);
+                for (int j = 0; j < 3; ++j) t[j] = add(t[j], rp[4LL * q + j]);
+        }
         if (threadIdx.x == 0) {
             co[0] = t[0];
             co[1] = t[1];
@@ -443,6 +541,21 @@ __global__ void kp_pack_kernel(KPArgs a, int idx, int which, int force) {
         a.send_buf[k] = v[__ldg(a.send_idx + k)];
 }
 
+// halo push: every send entry straight into the neighbour's ghost range
+// (remote store through the peer mapping), then one release per neighbour
+__global__ void kp_ipc_push_kernel(KPArgs a, int idx, int which, int force) {
+    const KPState& st = a.st[idx];
+    if (st.done || (!force && st.need_head)) return;
+    const KPIpc* ipc = a.ipc;
+    const double2* v = which ? a.u : a.x;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < a.n_send; k += gridDim.x * blockDim.x) {
+        int sg = 0;
+        while (sg + 1 < ipc->nseg && k >= ipc->seg_start[sg + 1]) ++sg;
+        ipc->seg_dst[which][sg][k - ipc->seg_start[sg]] = v[__ldg(a.send_idx + k)];
+    }
+    if (kp_last_cta_sys(a.counter) && threadIdx.x == 0) ipc_signal(ipc, which ? kIpcU : kIpcX, ipc->send_mask, a.seq_push);
+}
+
 }  // namespace rafem
 
 using namespace rafem;
@@ -468,6 +581,11 @@ struct rafem_kp {
     int* flag = nullptr;
     int launches_at_begin = 0;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
+    // device-initiated data plane (rafem_kp_ipc_connect)
+    size_t off_x = 0, off_u = 0, off_rp = 0, off_fl = 0;  // byte offsets in `block` (exported)
+    KPIpc* ipc_dev = nullptr;
+    void* peer_base[kIpcRanks] = {};
+    unsigned long long seq[kIpcKinds] = {};
 };
 
 namespace {
@@ -540,8 +658,9 @@ int rafem_kp_create(rafem_system* sys, int64_t n_owned, int64_t n_ext, int32_t n
     const size_t orr = take(v2 * n_owned), ow = take(v2 * n_owned), os = take(v2 * n_owned), op = take(v2 * n_owned);
     const size_t ob = take(v2 * n_owned), om = take(v2 * n_owned);
     const size_t opa = take(sizeof(double) * 2 * gmax), opb = take(sizeof(double) * gmax);
-    const size_t orp = take(sizeof(double) * 4 * nranks), ost = take(sizeof(KPState) * 2);
+    const size_t orp = take(sizeof(double) * 8 * nranks), ost = take(sizeof(KPState) * 2);
     const size_t oc = take(sizeof(unsigned)), of = take(sizeof(int));
+    const size_t ofl = take(sizeof(unsigned long long) * kIpcKinds * kIpcRanks);  // zeroed with the block
     cudaError_t e = cudaMalloc(&k->block, off);
     if (e != cudaSuccess) {
         delete k;
@@ -577,6 +696,10 @@ int rafem_kp_create(rafem_system* sys, int64_t n_owned, int64_t n_ext, int32_t n
     a.st = reinterpret_cast<KPState*>(base + ost);
     a.counter = reinterpret_cast<unsigned*>(base + oc);
     k->flag = reinterpret_cast<int*>(base + of);
+    k->off_x = ox;
+    k->off_u = ou;
+    k->off_rp = orp;
+    k->off_fl = ofl;
     a.nranks = nranks;
     a.rank = rank;
     a.bufbytes = bufbytes;
@@ -599,6 +722,9 @@ int rafem_kp_create(rafem_system* sys, int64_t n_owned, int64_t n_ext, int32_t n
 void rafem_kp_destroy(rafem_kp* k) {
     if (!k) return;
     if (k->ctx) cudaStreamSynchronize(k->ctx->stream);
+    for (void* pb : k->peer_base)
+        if (pb) cudaIpcCloseMemHandle(pb);
+    if (k->ipc_dev) cudaFree(k->ipc_dev);
     if (k->block) cudaFree(k->block);
     if (k->sendb) cudaFree(k->sendb);
     if (k->sidx) cudaFree(k->sidx);
@@ -683,6 +809,7 @@ static int kp_begin_impl(rafem_kp* k, const double* b, const double* x0, bool ke
     a.cyc_cap = hc;
     k->idx = 0;
     RF_CUDA_TRY(ctx, cudaEventRecord(k->e0, ctx->stream));
+    if (a.ipc) a.seq_push = ++k->seq[kIpcS];
     kp_bnorm_kernel<<<k->g_upd, KPU, 0, ctx->stream>>>(a);
     return kp_launch_check(ctx);
 }
@@ -701,6 +828,16 @@ int rafem_kp_launch(rafem_kp* k, int32_t what) {
     rafem_ctx* ctx = k->ctx;
     KPArgs& a = k->a;
     cudaStream_t st = ctx->stream;
+    if (a.ipc) {  // this launch's exchange: wait for / publish the kind's next sequence number
+        if (what == 0 || what == 4 || what == 5) a.seq_wait = k->seq[kIpcS];
+        if (what == 1) a.seq_wait = k->seq[kIpcX];
+        if (what == 2 || what == 3) {
+            a.seq_wait = k->seq[kIpcU];
+            a.seq_push = ++k->seq[kIpcS];
+        }
+        if (what == 6) a.seq_push = ++k->seq[kIpcX];
+        if (what == 7 || what == 8) a.seq_push = ++k->seq[kIpcU];
+    }
     switch (what) {
         case 0:
             kp_go(k->pdl, kp_bnorm_finish_kernel, 1, 32, 0, st, a);
@@ -739,11 +876,13 @@ int rafem_kp_launch(rafem_kp* k, int32_t what) {
         case 6:
         case 7:
         case 8:
-            if (a.n_send > 0)
-                kp_pack_kernel<<<std::max(1, std::min((a.n_send + 255) / 256, 4 * ctx->sm_count)), 256, 0, st>>>(
+            if (a.n_send <= 0) return RAFEM_OK;
+            if (a.ipc)  // straight into the neighbours' ghost ranges
+                kp_ipc_push_kernel<<<std::max(1, std::min((a.n_send + 255) / 256, 4 * ctx->sm_count)), 256, 0, st>>>(
                     a, k->idx, what != 6, what != 8);
             else
-                return RAFEM_OK;
+                kp_pack_kernel<<<std::max(1, std::min((a.n_send + 255) / 256, 4 * ctx->sm_count)), 256, 0, st>>>(
+                    a, k->idx, what != 6, what != 8);
             break;
         default:
             return rafem_fail(ctx, RAFEM_ERR_INVALID, "kp_launch: unknown phase");
@@ -754,11 +893,81 @@ int rafem_kp_launch(rafem_kp* k, int32_t what) {
 // Single-shard driver: `iters` SPMV + UPDATE pairs back to back (no host
 // round trip), for nranks == 1.
 int rafem_kp_iterate(rafem_kp* k, int32_t iters) {
-    if (!k || k->a.nranks != 1) return RAFEM_ERR_INVALID;
+    if (!k || (k->a.nranks != 1 && !k->a.ipc)) return RAFEM_ERR_INVALID;
     for (int i = 0; i < iters; ++i) {
+        if (k->a.ipc)  // the halo of u goes out by itself (device-initiated)
+            if (int rc = rafem_kp_launch(k, RAFEM_KP_PACK_U)) return rc;
         if (int rc = rafem_kp_launch(k, 3)) return rc;  // w = A u (u from the last update)
         if (int rc = rafem_kp_launch(k, 5)) return rc;
     }
+    return RAFEM_OK;
+}
+
+// ---- device-initiated data plane ------------------------------------------
+int rafem_kp_ipc_export(rafem_kp* k, void* handle, int64_t* offsets) {
+    if (!k || !handle || !offsets) return RAFEM_ERR_INVALID;
+    rafem_ctx* ctx = k->ctx;
+    cudaIpcMemHandle_t h;
+    RF_CUDA_TRY(ctx, cudaIpcGetMemHandle(&h, k->block));
+    std::memcpy(handle, &h, sizeof(h));
+    offsets[0] = (int64_t)k->off_x;
+    offsets[1] = (int64_t)k->off_u;
+    offsets[2] = (int64_t)k->off_rp;
+    offsets[3] = (int64_t)k->off_fl;
+    return RAFEM_OK;
+}
+
+int rafem_kp_ipc_connect(rafem_kp* k, const void* handles, const int64_t* offsets, int32_t nseg,
+                         const int32_t* seg_peer, const int64_t* seg_start, const int64_t* seg_dst_node,
+                         int32_t n_recv_peers, const int32_t* recv_peers) {
+    if (!k || !handles || !offsets || nseg < 0 || n_recv_peers < 0) return RAFEM_ERR_INVALID;
+    rafem_ctx* ctx = k->ctx;
+    KPArgs& a = k->a;
+    const int R = a.nranks, me = a.rank;
+    if (R < 2 || R > kIpcRanks || nseg > kIpcRanks)
+        return rafem_fail(ctx, RAFEM_ERR_UNSUPPORTED, "ipc: 2..8 shards with at most 8 neighbours");
+    if (nseg && seg_start[nseg] != a.n_send) return rafem_fail(ctx, RAFEM_ERR_INVALID, "ipc: send segments != halo");
+    KPIpc h{};
+    h.rank = me;
+    h.nranks = R;
+    h.nseg = nseg;
+    char* base[kIpcRanks] = {};
+    const cudaIpcMemHandle_t* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
+    for (int r = 0; r < R; ++r) {
+        if (r == me) {
+            base[r] = static_cast<char*>(k->block);
+            continue;
+        }
+        if (!k->peer_base[r]) {
+            void* pb = nullptr;
+            RF_CUDA_TRY(ctx, cudaIpcOpenMemHandle(&pb, hs[r], cudaIpcMemLazyEnablePeerAccess));
+            k->peer_base[r] = pb;
+        }
+        base[r] = static_cast<char*>(k->peer_base[r]);
+        h.slot_mask |= 1u << r;
+        h.slot_dst[r] = reinterpret_cast<double*>(base[r] + offsets[4 * r + 2]) + 4LL * me;
+        h.peer_flags[r] = reinterpret_cast<unsigned long long*>(base[r] + offsets[4 * r + 3]);
+    }
+    for (int sgi = 0; sgi < nseg; ++sgi) {
+        const int q = seg_peer[sgi];
+        if (q < 0 || q >= R || q == me) return rafem_fail(ctx, RAFEM_ERR_INVALID, "ipc: bad neighbour");
+        h.seg_peer[sgi] = q;
+        h.seg_start[sgi] = (int)seg_start[sgi];
+        h.seg_dst[0][sgi] = reinterpret_cast<double2*>(base[q] + offsets[4 * q + 0]) + seg_dst_node[sgi];
+        h.seg_dst[1][sgi] = reinterpret_cast<double2*>(base[q] + offsets[4 * q + 1]) + seg_dst_node[sgi];
+        h.send_mask |= 1u << q;
+    }
+    h.seg_start[nseg] = (int)(nseg ? seg_start[nseg] : 0);
+    for (int i = 0; i < n_recv_peers; ++i) {
+        if (recv_peers[i] < 0 || recv_peers[i] >= R || recv_peers[i] == me)
+            return rafem_fail(ctx, RAFEM_ERR_INVALID, "ipc: bad receive peer");
+        h.recv_mask |= 1u << recv_peers[i];
+    }
+    h.my_flags = reinterpret_cast<unsigned long long*>(base[me] + k->off_fl);
+    if (!k->ipc_dev) RF_CUDA_TRY(ctx, cudaMalloc(&k->ipc_dev, sizeof(KPIpc)));
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(k->ipc_dev, &h, sizeof(KPIpc), cudaMemcpyHostToDevice, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    a.ipc = k->ipc_dev;
     return RAFEM_OK;
 }
 

@@ -39,7 +39,7 @@ from . import _native as nat
 from .krylov import KrylovBreakdownError, SolveStats
 
 __all__ = ["ShardPlan", "partition_rows", "build_plan", "ShardComm", "ShardedPCG", "ShardedSystem",
-           "KPDeviceEngine", "ShardedSimulation", "DeviceShardedSimulation"]
+           "KPDeviceEngine", "ShardedSimulation", "DeviceShardedSimulation", "connect_ipc"]
 
 # phases of rafem_kp_launch (include/rafem_b200.h)
 BNORM_FINISH, HEAD, SPMV_AFTER_HEAD, SPMV, UPDATE_FIRST, UPDATE, PACK_X, PACK_U_AFTER_HEAD, PACK_U = range(9)
@@ -418,13 +418,14 @@ class ShardedPCG:
     def __init__(self, engine, comm: ShardComm | None, plan: ShardPlan | None, batch: int = 16):
         self.e, self.comm, self.plan, self.batch = engine, comm, plan, batch
         self.multi = comm is not None and comm.size > 1
+        self.ipc = False  # device-initiated halo / slots (connect_ipc)
 
     def _slots(self):
-        if self.multi:
+        if self.multi and not self.ipc:
             self.comm.allgather_slots(self.e.slots)
 
     def _halo(self, which):
-        if self.multi:
+        if self.multi and not self.ipc:
             self.comm.halo(self.plan, self.e.send_buf, self.e.u_ext if which == "u" else self.e.x_ext,
                            self.e.n_send)
 
@@ -471,7 +472,7 @@ class ShardedPCG:
             e.launch(UPDATE_FIRST)
             flags, _, _ = e.state()
             while not flags & (FLAG_DONE | FLAG_NEED_HEAD):
-                if self.multi:
+                if self.multi and not self.ipc:
                     for _ in range(self.batch):
                         e.launch(PACK_U)
                         self._halo("u")
@@ -479,8 +480,42 @@ class ShardedPCG:
                         self._slots()
                         e.launch(UPDATE)
                 else:
-                    e.iterate(self.batch)  # SPMV + UPDATE pairs, no host round trip
+                    # single shard, or the device-initiated data plane: a batch of
+                    # iterations with no host collective and no host round trip
+                    e.iterate(self.batch)
                 flags, _, _ = e.state()
+
+
+def connect_ipc(engine: "KPDeviceEngine", plan: ShardPlan, comm: ShardComm, pcg: "ShardedPCG | None" = None):
+    """Switch one shard's PCG to the device-initiated data plane
+    (rafem_kp_ipc_connect): every rank exports its kp block, the handles,
+    layouts and ghost offsets are all-gathered once (the only host
+    collective), and from then on the phase kernels push the halo into the
+    neighbours' ghost ranges and the scalar slots into every peer through
+    the IPC mappings themselves.  Collective over the group."""
+    L = nat.lib()
+    hb = (C.c_char * 64)()
+    offs = np.zeros(4, dtype=np.int64)
+    nat.check(L.rafem_kp_ipc_export(engine.h, hb, nat.ptr(offs)), "kp_ipc_export")
+    mine = {"rank": plan.rank, "n_own": plan.n_own, "recv": dict(plan.recv), "handle": bytes(hb),
+            "offs": offs.tolist()}
+    allv = [None] * comm.size
+    comm.dist.all_gather_object(allv, mine, group=comm.group)
+    allv.sort(key=lambda d: d["rank"])
+    handles = b"".join(d["handle"] for d in allv)
+    aoffs = np.ascontiguousarray(np.array([d["offs"] for d in allv], dtype=np.int64).reshape(-1))
+    so = plan.send_offsets()
+    segs = [(q, o, n) for q, (o, n) in so.items() if n > 0]
+    peer = np.array([q for q, _, _ in segs], dtype=np.int32)
+    start = np.array([o for _, o, _ in segs] + [sum(n for _, _, n in segs)], dtype=np.int64)
+    dst = np.array([allv[q]["n_own"] + allv[q]["recv"][plan.rank][0] for q, _, _ in segs], dtype=np.int64)
+    recv = np.array(sorted(plan.recv), dtype=np.int32)
+    hbuf = (C.c_char * len(handles)).from_buffer_copy(handles)
+    nat.check(L.rafem_kp_ipc_connect(engine.h, hbuf, nat.ptr(aoffs), len(segs), nat.ptr(peer), nat.ptr(start),
+                                     nat.ptr(dst), recv.size, nat.ptr(recv)), "kp_ipc_connect")
+    comm.dist.barrier(group=comm.group)  # every peer mapped before anyone pushes
+    if pcg is not None:
+        pcg.ipc = True
 
 
 # ---------------------------------------------------------------------------
@@ -489,7 +524,8 @@ class ShardedPCG:
 class ShardedSystem:
     """assemble_global + solve for one row block of the global system."""
 
-    def __init__(self, mesh, material, comm: ShardComm | None = None, bounds=None, batch: int = 16):
+    def __init__(self, mesh, material, comm: ShardComm | None = None, bounds=None, batch: int = 16,
+                 ipc: bool = False):
         from .assembly import DeviceMesh, SystemHandle
         self.comm = comm
         nranks = comm.size if comm is not None else 1
@@ -511,6 +547,8 @@ class ShardedSystem:
                                      self.plan.send_index())
         self.pcg = ShardedPCG(self.engine, comm, self.plan, batch=batch)
         self.scale = 1.0
+        if ipc and comm is not None and comm.size > 1:
+            connect_ipc(self.engine, self.plan, comm, self.pcg)
 
     @classmethod
     def from_device_mesh(cls, dm, batch: int = 16) -> "ShardedSystem":

@@ -333,3 +333,79 @@ def test_device_sharded_loop_on_a_device_box_mesh():
     for x, y in zip(a, b):
         assert (x.step, x.time, x.dt, x.corrector_iters) == (y.step, y.time, y.dt, y.corrector_iters)
         assert np.array_equal(x.T, y.T) and np.array_equal(x.V, y.V)
+
+
+# ---------------------------------------------------------------------------
+# device-initiated data plane (rafem_kp_ipc_*): halo and scalar slots moved
+# by the phase kernels through CUDA IPC mappings (two or three processes on
+# this one GPU; NVLink peer memory across GPUs of a node)
+
+def _ipc_worker(rank, world, port, dims, out_dir, ipc, loop):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh
+        from paper_2409_13036_b200 import _native as nat
+        from paper_2409_13036_b200.shard import DeviceShardedSimulation, ShardComm, ShardedSystem
+        mesh = generate_box_mesh(*dims)
+        n = mesh.node_count
+        t, v = _hot(n)
+        comm = ShardComm(device_collectives=False)
+        sh = ShardedSystem(mesh, MaterialParams.default(), comm, batch=8, ipc=ipc)
+        p = sh.plan
+        tag = f"{'ipc' if ipc else 'host'}_{'loop' if loop else 'solve'}_w{world}_r{rank}"
+        if loop:
+            cfg = SimConfig(total_time=40.0, solver=SolverConfig(backend="pcg", precondition="jacobi",
+                                                                 tolerance=1e-10))
+            recs, summ = DeviceShardedSimulation(sh, comm).run(cfg, record_fields=True)
+            np.savez(os.path.join(out_dir, tag + ".npz"),
+                     traj=np.array([(r.step, r.time, r.dt, r.corrector_iters) for r in recs]),
+                     T=np.array([r.T for r in recs]), V=np.array([r.V for r in recs]),
+                     inner=summ.total_solver_iterations)
+            return
+        sh.assemble(p.extend(t), p.extend(v), p.extend(t), 0.5, SimConfig())
+        x0 = np.empty(2 * n)
+        x0[0::2], x0[1::2] = v, t
+        cfg = SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-10)
+        l0 = nat.kernel_launches()
+        x, st = sh.solve(x0=x0[2 * p.lo:2 * p.hi], config=cfg)
+        np.savez(os.path.join(out_dir, tag + ".npz"), x=x, it=st.iterations, conv=st.converged,
+                 rel=st.final_relative_residual, launches=nat.kernel_launches() - l0)
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_ipc(tmp_path, world, dims, ipc, loop=False):
+    import torch.multiprocessing as mp
+    port = 25100 + (os.getpid() % 400) + 5 * world + (2 if ipc else 0) + (1 if loop else 0)
+    mp.start_processes(_ipc_worker, args=(world, port, dims, str(tmp_path), ipc, loop), nprocs=world, join=True,
+                       start_method="spawn")
+    tag = f"{'ipc' if ipc else 'host'}_{'loop' if loop else 'solve'}_w{world}"
+    return [np.load(tmp_path / f"{tag}_r{r}.npz") for r in range(world)]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ipc_data_plane_solve_is_bitwise_the_host_collectives(tmp_path, world):
+    """Same kernels and arithmetic, only the transport changes: the
+    device-initiated halo / slot exchange gives bit-identical solutions and
+    iteration counts to the host-staged collectives."""
+    dims = (14, 9, 10)
+    a = _run_ipc(tmp_path, world, dims, ipc=True)
+    b = _run_ipc(tmp_path, world, dims, ipc=False)
+    for pa, pb in zip(a, b):
+        assert bool(pa["conv"]) and int(pa["it"]) == int(pb["it"])
+        assert np.array_equal(pa["x"], pb["x"])
+        assert float(pa["rel"]) == float(pb["rel"]) <= 1e-10
+
+
+def test_ipc_data_plane_time_loop_is_bitwise_the_host_collectives(tmp_path):
+    dims = (15, 15, 16)
+    a = _run_ipc(tmp_path, 2, dims, ipc=True, loop=True)
+    b = _run_ipc(tmp_path, 2, dims, ipc=False, loop=True)
+    for pa, pb in zip(a, b):
+        assert np.array_equal(pa["traj"], pb["traj"]) and int(pa["inner"]) == int(pb["inner"])
+        assert np.array_equal(pa["T"], pb["T"]) and np.array_equal(pa["V"], pb["V"])
