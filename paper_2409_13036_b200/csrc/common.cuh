@@ -108,6 +108,10 @@ RF_DEV void tma_load_1d_hint(void* dst, const void* src, unsigned bytes, unsigne
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+// bulk L2 prefetch of [src, src + bytes) (16-byte aligned and sized)
+RF_DEV void prefetch_l2_bulk(const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 RF_DEV unsigned long long l2_policy_evict_first() {
     unsigned long long p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

@@ -2048,7 +2048,8 @@ __global__ void __launch_bounds__(256, 1) spmv_tma_kernel(MatView A, const doubl
 // bytes per slot) and the columns come from a shared-memory table.
 template <int NT, int ST, int CH, bool HINT, bool CLS>
 __global__ void __launch_bounds__(NT, 1) spmv_tma_pipe_kernel(MatView A, const double* __restrict__ x,
-                                                              double* __restrict__ y, int valcap, int bufbytes) {
+                                                              double* __restrict__ y, int valcap, int bufbytes,
+                                                              int xpf) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) unsigned long long bar[ST];
     int* soff = reinterpret_cast<int*>(sm + (size_t)ST * bufbytes);  // CLS: the class table after the stages
@@ -2081,6 +2082,11 @@ __global__ void __launch_bounds__(NT, 1) spmv_tma_pipe_kernel(MatView A, const d
             if (vb) tma_load_1d(base, A.val + 2LL * s0, vb, &bar[b]);
             if (cb) tma_load_1d(base + (size_t)valcap * 16, A.col + sa, cb, &bar[b]);
         }
+        // the tile's own x rows into L2 a tile-time before its gathers need
+        // them: a wave of tiles gathers mostly within the wave's own rows
+        // (box stencils reach one plane), so a cold x is not a DRAM round
+        // trip per tile
+        if (xpf && r1 > r0) prefetch_l2_bulk(x + 2LL * r0, 16u * (unsigned)(r1 - r0));
     };
     // programmatic dependent launch (no-ops otherwise): let the next kernel
     // in the stream start its prologue as this grid's CTAs retire, and
@@ -2260,7 +2266,12 @@ static int spmv_pipe_launch(rafem_ctx* ctx, const MatView& A, const double* x_de
     MatView Av = A;
     const double* xp = x_dev;
     double* yp = y_dev;
-    void* args[] = {&Av, &xp, &yp, &valcap, &bufbytes};
+    // per-tile bulk L2 prefetch of the tile's own x rows (RAFEM_XPF=1; off by
+    // default — measured r2, cold L2: C3 36.9 -> 35.7 us, C4 401 -> 416 us
+    // with the default 192 x 2 tiles; it helps only the narrower tiles)
+    const char* xe = getenv("RAFEM_XPF");
+    int xpf = (xe && xe[0] == '1') ? 1 : 0;
+    void* args[] = {&Av, &xp, &yp, &valcap, &bufbytes, &xpf};
     if (ctx->spmv_pdl) {
         cudaLaunchConfig_t lc{};
         lc.gridDim = dim3(grid);
