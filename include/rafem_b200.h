@@ -132,7 +132,8 @@ int64_t rafem_kernel_launches(const rafem_ctx* ctx);
 /* the cudaStream_t every library call runs on (for external CUDA events) */
 void* rafem_stream(const rafem_ctx* ctx);
 /* diagnostics: last solve's execution mode (1 cluster-resident, 0 grid-wide,
- * 2 fused simulation, 3 grid-wide streaming PCG, 4 kernel-per-phase PCG)
+ * 2 fused simulation, 3 grid-wide streaming PCG, 4 kernel-per-phase PCG,
+ * 5 cluster-resident pipelined PCG (DSMEM halos), 6 cluster-resident simulation)
  * and CTA count; per-iteration phase timestamps (SM clock64) of CTA 0 when
  * tracing is on: 8 slots per iteration, returns entries copied */
 int rafem_last_solve_mode(const rafem_ctx* ctx, int32_t* mode, int32_t* ctas);

@@ -136,10 +136,12 @@ class DeviceMesh:
     def _adopt(self, h):
         L = nat.lib()
         self.handle = h
-        self._finalizer = weakref.finalize(self, L.rafem_mesh_destroy, h)
+        # pooled systems reference the mesh: one finalizer frees them first
+        # (also at interpreter exit, where finalizers run before __del__)
+        self._pool: list = []
+        self._finalizer = weakref.finalize(self, _destroy_mesh, L, h, self._pool)
         self.slots = int(L.rafem_mesh_slots(h))
         self._pattern = None
-        self._pool: list = []
 
     @classmethod
     def from_box(cls, nx: int, ny: int, nz: int, material=None, extent=None) -> "DeviceMesh":
@@ -215,18 +217,20 @@ class DeviceMesh:
         return h
 
     def release_system(self, h):
+        if not self._finalizer.alive:  # mesh already freed (interpreter exit): nothing to return to
+            return
         if len(self._pool) < 4:
             self._pool.append(h)
         else:
             nat.lib().rafem_system_destroy(h)
 
-    def __del__(self):
-        try:
-            for h in self._pool:
-                nat.lib().rafem_system_destroy(h)
-            self._pool = []
-        except Exception:
-            pass
+
+
+def _destroy_mesh(L, h, pool):
+    for s in pool:
+        L.rafem_system_destroy(s)
+    pool.clear()
+    L.rafem_mesh_destroy(h)
 
 
 class SystemHandle:

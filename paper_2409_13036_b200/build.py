@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                 "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["krylov.cu", "assembly.cu", "sparse.cu", "capi.cu", "shard.cu", "boxmesh.cu"]
+SOURCES = ["krylov.cu", "assembly.cu", "sparse.cu", "capi.cu", "shard.cu", "boxmesh.cu", "cluster.cu"]
 HEADERS = ["common.cuh", "internal.hpp", "assembly_dev.cuh", "simulate_dev.cuh"]
 
 

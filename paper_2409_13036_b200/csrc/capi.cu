@@ -257,6 +257,7 @@ void rafem_ctx_destroy(rafem_ctx* ctx) {
         if (b->p) cudaFree(b->p);
     for (auto& e : ctx->part_cache) dfree(ctx, e.gpart);
     ctx->part_cache.clear();
+    cluster_plans_release(ctx);
     dcache_release(ctx);
     if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
     if (ctx->mapped) cudaFreeHost(ctx->mapped);

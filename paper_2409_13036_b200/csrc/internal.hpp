@@ -116,7 +116,8 @@ struct rafem_ctx {
     int last_ctas = 0;
     int last_precond = -1;  // preconditioner the last solve applied (RAFEM_PRECOND_*)
     int last_team = 0;
-    bool spmv_pdl = false;  // streaming SpMV launched with programmatic dependent launch (back-to-back bench)
+    bool spmv_pdl = false;
+    std::vector<void*> cluster_plans;  // cluster.cu plans (ClusterPlan*), released with the context  // streaming SpMV launched with programmatic dependent launch (back-to-back bench)
 };
 
 struct rafem_matrix {
@@ -215,6 +216,12 @@ struct SimStream {
 int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, double* rec_x_dev,
                    double* rec_time_dev, double* rec_dt_dev, int* rec_iters_dev, long long rec_cap,
                    double* final_x_dev, float* ms, const SimStream* stream = nullptr);
+// cluster.cu: cluster-resident PCG for paper-scale node-paired systems;
+// RAFEM_ERR_UNSUPPORTED when the system is not eligible
+int cluster_pcg_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, double* x_dev, const double* minv_dev,
+                      const rafem_solver_params& p, KResult* res_dev, int* flag_dev, cudaEvent_t ev_start,
+                      cudaEvent_t ev_stop);
+void cluster_plans_release(rafem_ctx* ctx);
 int krylov_read_history(rafem_ctx* ctx, const KResult& r, double* hist, long long hist_cap,
                         long long* cyc, long long cyc_cap);
 int spmv_launch(rafem_ctx* ctx, const MatView& A, const double* x_dev, double* y_dev);

@@ -2456,6 +2456,12 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     const size_t hess_bytes = (size_t)hess_doubles * 8;
 
     // ---- choose the execution mode
+    // paper-scale PCG: the cluster-resident engine (cluster.cu) when the
+    // system fits one cluster's shared memory
+    if (!gm) {
+        const int crc = cluster_pcg_solve(ctx, A, b_dev, x_dev, minv_dev, p, res_dev, flag_dev, ev_start, ev_stop);
+        if (crc != RAFEM_ERR_UNSUPPORTED) return crc;
+    }
     const void* fn = nullptr;
     size_t smem = 0;
     bool cluster = false, hess_global = false;

@@ -339,3 +339,47 @@ def test_block_jacobi_pcg_on_fem_systems(dims):
         assert st.iterations < 0.85 * sj.iterations
     x2, st2 = solve(a, b, x0=x0, config=SolverConfig(backend="pcg", precondition="block_jacobi", tolerance=1e-10))
     assert np.array_equal(x, x2) and st.iterations == st2.iterations
+
+
+@pytest.mark.parametrize("dims", [(6, 5, 7), (15, 15, 16), (20, 20, 21)])
+def test_cluster_resident_pcg_vs_grid_pcg(dims):
+    """Cluster-resident PCG (cluster.cu: one 16-CTA cluster, DSMEM halos and
+    partials over st.async + mbarriers) against the 148-CTA grid PCG on the
+    same device-assembled system: same iteration count within 3 %, true
+    residual <= tol, solutions within 1e-7, bit-reproducible, stats contract;
+    exact x0 comes back bitwise and b = 0 gives x = 0."""
+    import os
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, assemble_global, generate_box_mesh, solve
+    from paper_2409_13036_b200 import _native as nat
+    mesh = generate_box_mesh(*dims)
+    n = mesh.node_count
+    rng = np.random.default_rng(77)
+    t, v = 37.0 + rng.uniform(0, 30, n), rng.uniform(0, 25, n)
+    s = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, v, t, 0.5)
+    a, b = s.matrix, s.rhs
+    x0 = np.empty(2 * n)
+    x0[0::2], x0[1::2] = v, t
+    for prec in ("jacobi", "none"):
+        cfg = SolverConfig(backend="pcg", precondition=prec, tolerance=1e-10)
+        x, st = solve(a, b, x0=x0, config=cfg)
+        assert nat.last_solve_mode()[0] == 5, nat.last_solve_mode()
+        res = np.linalg.norm(b - O.matvec(a.row_ptr, a.col_idx, a.vals, x)) / np.linalg.norm(b)
+        assert st.converged and res <= 1e-10 and abs(st.final_relative_residual - res) < 1e-12
+        hist = [h for cyc in st.residual_history for h in cyc]
+        assert len(hist) == st.iterations and st.restarts == len(st.residual_history) - 1
+        assert hist[-1] <= 1e-10 * (1 + 1e-9)  # the recursive estimate that ended the last cycle
+        x2, st2 = solve(a, b, x0=x0, config=cfg)
+        assert np.array_equal(x, x2) and st.iterations == st2.iterations
+        os.environ["RAFEM_CLUSTER"] = "0"
+        try:
+            xg, sg = solve(a, b, x0=x0, config=cfg)
+        finally:
+            del os.environ["RAFEM_CLUSTER"]
+        assert nat.last_solve_mode()[0] == 0
+        assert abs(st.iterations - sg.iterations) <= max(3, 0.03 * sg.iterations)
+        assert rel_err(x, xg) < 1e-7
+    # exact guess: returned bitwise with zero iterations; zero data: zero solution
+    xe, se = solve(a, b, x0=x, config=SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-6))
+    assert se.iterations == 0 and np.array_equal(xe, x)
+    xz, sz = solve(a, np.zeros_like(b), x0=x0, config=SolverConfig(backend="pcg", precondition="jacobi"))
+    assert sz.converged and not np.any(xz)
