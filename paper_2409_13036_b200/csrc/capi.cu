@@ -156,6 +156,7 @@ MatView system_view(rafem_system* s) {
     A.cls = s->mesh->cls;
     A.cls_off = s->mesh->cls_off;
     A.ncls = s->mesh->ncls;
+    A.coords = s->mesh->nodes;
     return A;
 }
 

@@ -36,13 +36,14 @@
 
 namespace rafem {
 
-constexpr int kCT = 576;     // max node rows (threads) per CTA (launch bound: 112 registers)
-constexpr int kCDest = 4;    // max other CTAs one row is a ghost of
+constexpr int kRPT = 1;      // node rows per thread (2 measured slower: longer serial row work per warp)
+constexpr int kCT = 576;     // max threads per CTA (kRPT * kCT node rows)
+constexpr int kCDest = 8;    // max other CTAs one row is a ghost of (corner of 8 blocks: 7)
 constexpr int kCMax = 16;    // max cluster size (non-portable)
 constexpr int kCRegions = 16;
 
 struct CCta {
-    int g0, nr, nloc, ell_n;
+    int g0, nr, nloc, ell_n;  // (g0 unused: own rows are lgid[lbase .. lbase + nr))
     int ell_base, wbase, lbase, pad;
 };
 
@@ -52,8 +53,11 @@ struct CPlan {
     const uint16_t* ecol;    // ELL local columns (pads: 0)
     const int* esrc;         // ELL entry -> CSR slot, -1 for pads
     const unsigned* dest;    // N x kCDest: cta << 16 | local index; 0xffffffff none
-    const int* lgid;         // per CTA: global node id of every local index
+    const int* lgid;         // per CTA: global node id of every local index (own rows by id, then ghosts)
+    const int2* trow;        // per CTA and row (thread order): (global row, local index)
     int C, ell_cap, nloc_cap;
+    int rows_cap;            // kRPT * threads per CTA (row slots)
+    int ndw;                 // push-target words per row (uint4): 1 or 2
 };
 
 // ---------------------------------------------------------------------------
@@ -70,6 +74,12 @@ RF_DEV void cl_sync() {
     cl_arrive();
     cl_wait();
 }
+// shared::cta address (u32) -> the same offset in CTA `rank`'s window
+RF_DEV unsigned cl_map_u(unsigned local, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
 RF_DEV unsigned cl_map(const void* local, unsigned rank) {
     unsigned r;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
@@ -78,6 +88,27 @@ RF_DEV unsigned cl_map(const void* local, unsigned rank) {
 RF_DEV void st_cluster2(unsigned addr, double a, double b) {
     asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(a), "d"(b) : "memory");
 }
+// shared::cta accesses by 32-bit address: in a cluster kernel a generic
+// pointer into shared memory embeds the CTA's window (SR_CgaCtaId), which
+// the compiler re-reads (S2R, tens of cycles) wherever it rematerialises one
+RF_DEV double2 lds2(unsigned a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+RF_DEV void sts2(unsigned a, double2 v) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+RF_DEV unsigned lds_u16(unsigned a) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+RF_DEV uint4 lds_u4(unsigned a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
 // 16 bytes into a peer's shared memory, completing 16 transaction bytes on
 // the peer's mbarrier (data and signal in one message, no fence)
 RF_DEV void st_async2(unsigned addr, double a, double b, unsigned rbar) {
@@ -85,38 +116,38 @@ RF_DEV void st_async2(unsigned addr, double a, double b, unsigned rbar) {
                  "d"(a), "d"(b), "r"(rbar)
                  : "memory");
 }
-RF_DEV void mbar_wait_cluster(unsigned long long* bar, unsigned parity) {
+// (CTA-scope acquire: the peers' st.async data lands in this CTA's shared
+// memory through the mbarrier's transaction count, which shared memory
+// never caches in L1 — the .cluster form would also invalidate L1 (spill
+// reloads would then go to L2 every iteration))
+RF_DEV void mbar_wait_cluster(unsigned bar, unsigned parity) {
     asm volatile(
         "{\n\t.reg .pred P;\n"
         "XW_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], %1;\n\t"
-        "@!P bra XW_%=;\n}" ::"r"(smem_u32(bar)),
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra XW_%=;\n}" ::"r"(bar),
         "r"(parity)
         : "memory");
 }
 
-// Shared state of one CTA of the engine.
+// Shared state of one CTA of the engine (identical in all its threads).
 struct CEnv {
-    double2* ev;        // ELL values
-    const uint16_t* ec; // ELL local columns
-    double2* mb;        // 2 x nloc_cap gathered-vector buffers
+    // shared::cta (32-bit) addresses of the arrays the iteration touches (a
+    // generic pointer into shared memory in a cluster kernel embeds the CTA
+    // window, which the compiler re-reads from SR_CgaCtaId at its uses)
+    unsigned mb_s, part_s, xbar_s, ev_s, ec_s, rmv_s, rdest_s, red_s, sc_s, yb_s;
     int nloc_cap;
-    double (*part)[kCMax][4];  // [2][C][4] pushed CTA partials
-    double (*red)[4];          // [32][4] warp partials
     int C;
     unsigned rank;
-    int t, nr;          // this thread's local row (active when t < nr)
-    int k0, width;      // own-column ELL section: this thread's first entry, slot positions
-    int k1, width1;     // ghost-column section
-    const uint4* rdest; // per own row: the CTAs (cta << 16 | ghost index) it is pushed to
-    double2* rb;        // per own row: right-hand side (heads only)
-    const double2* rmv; // per own row: Jacobi inverse diagonal
+    int nr;             // own node rows
+    int ndw;            // push-target words (uint4) per row: 1 (<= 4 targets) or 2 (<= 8)
     // exchanges: every CTA pushes its vector entries into the ghost slots of
     // its readers and its 4 CTA partials into every CTA, each message
     // completing transaction bytes on the receiver's mbarrier xbar[k & 1]
-    unsigned long long* xbar;  // 2 mbarriers
-    unsigned xk, xw;           // exchanges begun / waited
-    unsigned xbytes;           // bytes a CTA receives per exchange
+    unsigned xk, xw;    // exchanges begun / waited
+    unsigned xbytes;    // bytes a CTA receives per exchange
+    int blk;            // block-Jacobi: one Neumann step on the CTA's diagonal block
+    double omega;
     // PCG contract
     double tol;
     long long cap;
@@ -124,29 +155,45 @@ struct CEnv {
     long long hist_cap;
     long long* cyc;
     long long cyc_cap;
-    long long* trace;   // optional per-iteration clock64 stamps (rank 0, thread 0), 8 per iteration
+    int sit;            // stamp iteration (trace only)
+    int abl;            // ablation mask for cost studies (0 in production): 1 own SpMV, 2 ghost SpMV,
+                        // 4 halo pushes, 8 breakdown/convergence tests off
+    long long* trace;   // optional per-warp phase stamps of CTA 0
     long long trace_cap;
 };
 
-RF_DEV void c_stamp(const CEnv& E, long long it, int k) {
-    if (E.trace && E.rank == 0 && threadIdx.x == 0 && it * 8 + k < E.trace_cap) E.trace[it * 8 + k] = clock64();
+// One node row of a thread: the thread owns kRPT rows, warp w's lanes take
+// the rows of ELL warp blocks w, w + nwarps, ...
+struct CRowC {
+    int t;              // local row in thread order (active when < nr)
+    int gid, li;        // global node row, local (gathered-vector) index
+    int k0, w0, k1, w1; // own-column and ghost-column ELL sections: first entry, widths
+};
+
+// per-warp phase stamps of CTA 0 (lane 0 of every warp), iteration E.sit:
+// trace[((sit * 32) + warp) * 8 + k]
+RF_DEV void c_stamp(const CEnv& E, int k) {
+    if (E.trace && E.rank == 0 && (threadIdx.x & 31) == 0) {
+        const long long i = ((long long)E.sit * 32 + (threadIdx.x >> 5)) * 8 + k;
+        if (i < E.trace_cap) E.trace[i] = clock64();
+    }
 }
 
-// Partial row sum over one ELL section (left to right over its positions).
-RF_DEV void c_spmv_sec(const double2* __restrict__ ev, const uint16_t* __restrict__ ec, int width,
-                       const double2* src, double& av, double& at) {
+// Partial row sum over one ELL section (left to right over its positions);
+// ev, ec: the row's first entry; src: the gathered vector (u32 shared addresses).
+RF_DEV void c_spmv_sec(unsigned ev, unsigned ec, int width, unsigned src, double& av, double& at) {
     int l = 0;
 #pragma unroll 1
     for (; l + 4 <= width; l += 4) {
-        int c[4];
+        unsigned c[4];
         double2 a[4], v[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            c[j] = ec[(l + j) * 32];
-            a[j] = ev[(l + j) * 32];
+            c[j] = lds_u16(ec + 64u * (l + j));
+            a[j] = lds2(ev + 512u * (l + j));
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = src[c[j]];
+        for (int j = 0; j < 4; ++j) v[j] = lds2(src + 16u * c[j]);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             av = fma(a[j].x, v[j].x, av);
@@ -155,82 +202,109 @@ RF_DEV void c_spmv_sec(const double2* __restrict__ ev, const uint16_t* __restric
     }
 #pragma unroll 1
     for (; l < width; ++l) {
-        const double2 a = ev[l * 32];
-        const double2 v = src[ec[l * 32]];
+        const double2 a = lds2(ev + 512u * l);
+        const double2 v = lds2(src + 16u * lds_u16(ec + 64u * l));
         av = fma(a.x, v.x, av);
         at = fma(a.y, v.y, at);
     }
 }
-// Own-column part of row t of A src (needs only this CTA's entries of src).
-RF_DEV double2 c_spmv_own(const CEnv& E, const double2* src) {
+RF_DEV unsigned c_buf(const CEnv& E, int buf) { return E.mb_s + 16u * (unsigned)(buf * E.nloc_cap); }
+// own-column part of the row's product (needs only this CTA's entries of src)
+RF_DEV double2 c_spmv_own(const CEnv& E, const CRowC& rc, unsigned src) {
     double av = 0.0, at = 0.0;
-    c_spmv_sec(E.ev + E.k0, E.ec + E.k0, E.width, src, av, at);
+    c_spmv_sec(E.ev_s + 16u * rc.k0, E.ec_s + 2u * rc.k0, rc.w0, src, av, at);
     return make_double2(av, at);
 }
-// + the ghost-column part (needs the pushed ghost entries).
-RF_DEV double2 c_spmv_gh(const CEnv& E, const double2* src, double2 acc) {
-    c_spmv_sec(E.ev + E.k1, E.ec + E.k1, E.width1, src, acc.x, acc.y);
+// + the ghost-column part (needs the pushed ghost entries)
+RF_DEV double2 c_spmv_gh(const CEnv& E, const CRowC& rc, unsigned src, double2 acc) {
+    c_spmv_sec(E.ev_s + 16u * rc.k1, E.ec_s + 2u * rc.k1, rc.w1, src, acc.x, acc.y);
     return acc;
 }
-RF_DEV double2 c_spmv(const CEnv& E, const double2* src) { return c_spmv_gh(E, src, c_spmv_own(E, src)); }
+RF_DEV double2 c_spmv(const CEnv& E, const CRowC& rc, unsigned src) {
+    return c_spmv_gh(E, rc, src, c_spmv_own(E, rc, src));
+}
 
 // Exchange k (= E.xk) begins: thread 0 arms the CTA's mbarrier with the
 // bytes it will receive (peers' messages may already have landed: the
 // transaction count then runs negative until this arrive).
 RF_DEV void c_xbegin(const CEnv& E) {
-    if (threadIdx.x == 0) mbar_expect_tx(E.xbar + (E.xk & 1), E.xbytes);
+    if (threadIdx.x == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(E.xbar_s + 8u * (E.xk & 1)),
+                     "r"(E.xbytes)
+                     : "memory");
 }
 
-// Own row's entry of buffer `buf`: local store + a push into every CTA that
+// A row's entry of buffer `buf`: local store + a push into every CTA that
 // holds the row as a ghost (exchange E.xk).
-RF_DEV void c_push(const CEnv& E, int buf, double2 v) {
-    double2* b = E.mb + (size_t)buf * E.nloc_cap;
-    b[E.t] = v;
-    const unsigned long long* bar = E.xbar + (E.xk & 1);
-    const uint4 dq = E.rdest[E.t];
-    const unsigned qs[4] = {dq.x, dq.y, dq.z, dq.w};
+RF_DEV void c_push(const CEnv& E, const CRowC& rc, int buf, double2 v) {
+    const unsigned bs = c_buf(E, buf), bar = E.xbar_s + 8u * (E.xk & 1);
+    sts2(bs + 16u * rc.li, v);
+    if (E.abl & 4) return;
+    for (int w = 0; w < E.ndw; ++w) {
+        const uint4 d = lds_u4(E.rdest_s + 16u * (E.ndw * rc.t + w));
+        const unsigned qs[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
-    for (int d = 0; d < kCDest; ++d) {
-        const unsigned q = qs[d];
-        if (q != 0xffffffffu) st_async2(cl_map(b + (q & 0xffffu), q >> 16), v.x, v.y, cl_map(bar, q >> 16));
+        for (int k = 0; k < 4; ++k) {
+            const unsigned q = qs[k];
+            if (q != 0xffffffffu)
+                st_async2(cl_map_u(bs + 16u * (q & 0xffffu), q >> 16), v.x, v.y, cl_map_u(bar, q >> 16));
+        }
+        if (d.w == 0xffffffffu) break;
     }
 }
 
-// CTA partials (v0..v2 summed, v3 max) of exchange E.xk into part[xk & 1][rank]
-// of every CTA; closes the CTA's side of the exchange.  The bar.sync also
-// publishes the own entries of the pushed vector inside the CTA.
+// K-value warp sums with the K butterflies interleaved (every shuffle of a
+// level issued before its adds): the same bits per value as warp_sum.
+template <int K>
+RF_DEV void warp_sum_k(double (&v)[K]) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        double t[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) t[j] = __shfl_xor_sync(0xffffffffu, v[j], o);
+#pragma unroll
+        for (int j = 0; j < K; ++j) v[j] = add(v[j], t[j]);
+    }
+}
+
+// CTA partials of exchange E.xk (v0..v2 summed; with MAX, v3 max-reduced)
+// into part[xk & 1][rank] of every CTA; closes the CTA's side of the
+// exchange.  The bar.sync also publishes the own entries of the pushed
+// vector inside the CTA.  Second level: warp 0 butterflies the warp
+// partials and lane c < C sends the CTA's sums to CTA c.
+template <bool MAX>
 RF_DEV void c_publish(CEnv& E, double v0, double v1, double v2, double v3) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    v0 = warp_sum(v0);
-    v1 = warp_sum(v1);
-    v2 = warp_sum(v2);
-    v3 = warp_max(v3);
+    double v[3] = {v0, v1, v2};
+    warp_sum_k<3>(v);
+    if (MAX) v3 = warp_max(v3);
     if (lane == 0) {
-        E.red[w][0] = v0;
-        E.red[w][1] = v1;
-        E.red[w][2] = v2;
-        E.red[w][3] = v3;
+        sts2(E.red_s + 32u * w, make_double2(v[0], v[1]));
+        sts2(E.red_s + 32u * w + 16u, make_double2(v[2], v3));
     }
     __syncthreads();
+    c_stamp(E, 6);
     if (w == 0) {
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        double t[3] = {0.0, 0.0, 0.0};
+        double s3 = 0.0;
         if (lane < nw) {
-            s0 = E.red[lane][0];
-            s1 = E.red[lane][1];
-            s2 = E.red[lane][2];
-            s3 = E.red[lane][3];
+            const double2 a = lds2(E.red_s + 32u * lane);
+            const double2 b = lds2(E.red_s + 32u * lane + 16u);
+            t[0] = a.x;
+            t[1] = a.y;
+            t[2] = b.x;
+            s3 = b.y;
         }
-        s0 = warp_sum(s0);
-        s1 = warp_sum(s1);
-        s2 = warp_sum(s2);
-        s3 = warp_max(s3);
+        warp_sum_k<3>(t);
+        if (MAX) s3 = warp_max(s3);
         if (lane < E.C) {
-            const unsigned a = cl_map(&E.part[E.xk & 1][E.rank][0], (unsigned)lane);
-            const unsigned rb = cl_map(E.xbar + (E.xk & 1), (unsigned)lane);
-            st_async2(a, s0, s1, rb);
-            st_async2(a + 16, s2, s3, rb);
+            const unsigned a = cl_map_u(E.part_s + 32u * (16u * (E.xk & 1) + E.rank), (unsigned)lane);
+            const unsigned rb = cl_map_u(E.xbar_s + 8u * (E.xk & 1), (unsigned)lane);
+            st_async2(a, t[0], t[1], rb);
+            st_async2(a + 16, t[2], s3, rb);
         }
     }
+    c_stamp(E, 7);
     ++E.xk;
 }
 
@@ -238,28 +312,34 @@ RF_DEV void c_publish(CEnv& E, double v0, double v1, double v2, double v3) {
 // visible to every thread of the CTA).
 RF_DEV void c_xwait(CEnv& E) {
     const unsigned k = E.xw++;
-    mbar_wait_cluster(E.xbar + (k & 1), (k >> 1) & 1u);
+    mbar_wait_cluster(E.xbar_s + 8u * (k & 1), (k >> 1) & 1u);
 }
 
-// After the wait: combine the C partials of the last waited exchange in rank
-// order (same bits in every warp of every CTA).
+// After the wait: combine the C partials of the last waited exchange.
+template <bool MAX>
 RF_DEV void c_gather(const CEnv& E, double (&co)[4]) {
+    // lane c holds CTA c's partials; one interleaved butterfly: the same bits
+    // in every warp of every CTA
     const int lane = threadIdx.x & 31;
     const int par = (E.xw - 1) & 1;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    double t[3] = {0.0, 0.0, 0.0};
+    double s3 = 0.0;
     if (lane < E.C) {
-        const double2 a = *reinterpret_cast<const double2*>(&E.part[par][lane][0]);
-        const double2 b = *reinterpret_cast<const double2*>(&E.part[par][lane][2]);
-        s0 = a.x;
-        s1 = a.y;
-        s2 = b.x;
+        const double2 a = lds2(E.part_s + 32u * (16u * par + lane));
+        const double2 b = lds2(E.part_s + 32u * (16u * par + lane) + 16u);
+        t[0] = a.x;
+        t[1] = a.y;
+        t[2] = b.x;
         s3 = b.y;
     }
-    co[0] = warp_sum(s0);
-    co[1] = warp_sum(s1);
-    co[2] = warp_sum(s2);
-    co[3] = warp_max(s3);
+    warp_sum_k<3>(t);
+    co[0] = t[0];
+    co[1] = t[1];
+    co[2] = t[2];
+    co[3] = MAX ? warp_max(s3) : 0.0;
 }
+
+RF_DEV double2 d2(double a, double b) { return make_double2(a, b); }
 
 // Krylov vectors of one row (both dofs) in registers.
 struct CRow {
@@ -273,57 +353,104 @@ struct CpcgOut {
     int status;
 };
 
-RF_DEV double2 d2(double a, double b) { return make_double2(a, b); }
+// out_j = M^-1 src_j for the thread's rows.  Jacobi: D^-1 src.  Block-Jacobi
+// (E.blk): one Neumann step on the CTA's diagonal block A_bb,
+// m = y + omega D^-1 (src - A_bb y), y = D^-1 src (the in-block product is
+// the own-column ELL section over y); SPD for omega < 1 / (lambda_max(D^-1/2
+// A_bb D^-1/2) - 1), omega from the block's Gershgorin bound.  Every thread
+// of the CTA must call it (bar.sync inside when blk).
+template <bool PRE, int RPT>
+RF_DEV void c_prec(const CEnv& E, const CRowC (&rc)[RPT], const double2 (&src)[RPT], double2 (&out)[RPT]) {
+    double2 y[RPT];
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+        if (rc[j].t < E.nr) {
+            const double2 mv = PRE ? lds2(E.rmv_s + 16u * rc[j].t) : d2(1.0, 1.0);
+            y[j] = d2(mv.x * src[j].x, mv.y * src[j].y);
+            if (E.blk) sts2(E.yb_s + 16u * rc[j].li, y[j]);
+        } else {
+            y[j] = d2(0.0, 0.0);
+        }
+    }
+    if (!E.blk) {
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) out[j] = y[j];
+        return;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+        if (rc[j].t < E.nr) {
+            const double2 t = c_spmv_own(E, rc[j], E.yb_s);
+            const double2 mv = lds2(E.rmv_s + 16u * rc[j].t);
+            out[j] = d2(fma(E.omega * mv.x, src[j].x - t.x, y[j].x), fma(E.omega * mv.y, src[j].y - t.y, y[j].y));
+        } else {
+            out[j] = d2(0.0, 0.0);
+        }
+    }
+    __syncthreads();  // y is rewritten by the next application
+}
 
 // Pipelined PCG (Ghysels-Vanroose) on the cluster, pcg_pipe_core's contract.
 // bnorm < 0: ||b||^2 and the zero-diagonal flag (zf, per thread) ride on the
-// first head's reduction.  xold (own row, when `delta`): the corrector delta
+// first head's reduction.  xold (global, by node row): the corrector delta
 // max|x - xold| / max(1, |xold|) of the head's iterate goes to *delta.
-template <bool PRE>
-RF_DEV CpcgOut cpcg_core(CEnv& E, CRow& R, double bnorm, double zf, const double2* xold, double* delta,
-                         double2* xout_g) {
-    const bool act = E.t < E.nr;
-    long long total = 0, cycles = 0, hlen = 0;
+// b: the right-hand side (global, by node row; read in heads only).
+template <bool PRE, int RPT>
+RF_DEV CpcgOut cpcg_core(CEnv& E, const CRowC (&rc)[RPT], CRow (&R)[RPT], const double2* b, double bnorm, double zf,
+                         const double2* xold, double* delta, double2* xout_g) {
+    int total = 0, cycles = 0, hlen = 0;  // (caps below 2^31: hist_cap <= 2^20 + 1)
     bool converged = false;
     double rel = INFINITY;
     int status = RAFEM_OK;
     int hb = 0;
     const bool lead = E.rank == 0 && threadIdx.x == 0;
     while (true) {
-        // ---- head: r = b - A x, u = M r (x pushed, one full barrier)
+        // ---- head: r = b - A x, u = M r (x pushed: one exchange)
         const bool with_b = bnorm < 0.0;
         c_xbegin(E);
-        if (act) {
-            c_push(E, hb, R.x);
-            if (xout_g) xout_g[E.t] = R.x;
-        }
-        c_publish(E, 0.0, 0.0, 0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < RPT; ++j)
+            if (rc[j].t < E.nr) {
+                c_push(E, rc[j], hb, R[j].x);
+                if (xout_g) xout_g[rc[j].gid] = R[j].x;
+            }
+        c_publish<false>(E, 0.0, 0.0, 0.0, 0.0);
         c_xwait(E);
         double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
-        if (act) {
-            const double2 y = c_spmv(E, E.mb + (size_t)hb * E.nloc_cap);
-            const double2 bb = E.rb[E.t], mv = E.rmv[E.t];
-            R.r = d2(bb.x - y.x, bb.y - y.y);
-            R.u = PRE ? d2(mv.x * R.r.x, mv.y * R.r.y) : R.r;
-            v2 = fma(R.r.x, R.r.x, R.r.y * R.r.y);
-            if (with_b) {
-                v0 = fma(bb.x, bb.x, bb.y * bb.y);
-                v1 = zf;
-            }
-            if (xold) {
-                const double2 xo = *xold;
-                const double d0 = fabs(R.x.x - xo.x) / fmax(1.0, fabs(xo.x));
-                const double d1 = fabs(R.x.y - xo.y) / fmax(1.0, fabs(xo.y));
-                v3 = (d0 > v3 || d0 != d0) ? d0 : v3;
-                v3 = (d1 > v3 || d1 != d1) ? d1 : v3;
+        double2 src[RPT], out[RPT];
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            src[j] = d2(0.0, 0.0);
+            if (rc[j].t < E.nr) {
+                const double2 y = c_spmv(E, rc[j], c_buf(E, hb));
+                const double2 bb = b[rc[j].gid];
+                R[j].r = d2(bb.x - y.x, bb.y - y.y);
+                src[j] = R[j].r;
+                v2 += fma(R[j].r.x, R[j].r.x, R[j].r.y * R[j].r.y);
+                if (with_b) v0 += fma(bb.x, bb.x, bb.y * bb.y);
+                if (xold) {
+                    const double2 xo = xold[rc[j].gid];
+                    const double d0 = fabs(R[j].x.x - xo.x) / fmax(1.0, fabs(xo.x));
+                    const double d1 = fabs(R[j].x.y - xo.y) / fmax(1.0, fabs(xo.y));
+                    v3 = (d0 > v3 || d0 != d0) ? d0 : v3;
+                    v3 = (d1 > v3 || d1 != d1) ? d1 : v3;
+                }
             }
         }
+        if (with_b && threadIdx.x == 0) v1 = zf;
+        c_prec<PRE, RPT>(E, rc, src, out);
         c_xbegin(E);
-        if (act) c_push(E, hb ^ 1, R.u);
-        c_publish(E, v0, v1, v2, v3);
+#pragma unroll
+        for (int j = 0; j < RPT; ++j)
+            if (rc[j].t < E.nr) {
+                R[j].u = out[j];
+                c_push(E, rc[j], hb ^ 1, R[j].u);
+            }
+        c_publish<true>(E, v0, v1, v2, v3);
         c_xwait(E);
         double co[4];
-        c_gather(E, co);
+        c_gather<true>(E, co);
         if (with_b) {
             if (co[1] > 0.0) {
                 status = RAFEM_ERR_INVALID;
@@ -332,8 +459,11 @@ RF_DEV CpcgOut cpcg_core(CEnv& E, CRow& R, double bnorm, double zf, const double
             }
             bnorm = sqrt(co[0]);
             if (bnorm == 0.0) {  // zero data: zero solution (solver.py:422-425)
-                R.x = d2(0.0, 0.0);
-                if (act && xout_g) xout_g[E.t] = R.x;
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) {
+                    R[j].x = d2(0.0, 0.0);
+                    if (rc[j].t < E.nr && xout_g) xout_g[rc[j].gid] = R[j].x;
+                }
                 if (delta) *delta = -1.0;
                 converged = true;
                 rel = 0.0;
@@ -350,97 +480,143 @@ RF_DEV CpcgOut cpcg_core(CEnv& E, CRow& R, double bnorm, double zf, const double
         if (total >= E.cap) break;
         // ---- w = A u, m = M w, partials of (r.u, w.u, r.r)
         v0 = v1 = v2 = 0.0;
-        if (act) {
-            const double2 y = c_spmv(E, E.mb + (size_t)(hb ^ 1) * E.nloc_cap);
-            R.w = y;
-            const double2 mv = E.rmv[E.t];
-            const double2 m = PRE ? d2(mv.x * y.x, mv.y * y.y) : y;
-            R.q = m;  // m of this iterate (kept in q until the first update)
-            v0 = fma(R.r.x, R.u.x, R.r.y * R.u.y);
-            v1 = fma(y.x, R.u.x, y.y * R.u.y);
-            v2 = fma(R.r.x, R.r.x, R.r.y * R.r.y);
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            src[j] = d2(0.0, 0.0);
+            if (rc[j].t < E.nr) {
+                const double2 y = c_spmv(E, rc[j], c_buf(E, hb ^ 1));
+                R[j].w = y;
+                src[j] = y;
+                v0 += fma(R[j].r.x, R[j].u.x, R[j].r.y * R[j].u.y);
+                v1 += fma(y.x, R[j].u.x, y.y * R[j].u.y);
+                v2 += fma(R[j].r.x, R[j].r.x, R[j].r.y * R[j].r.y);
+            }
         }
+        c_prec<PRE, RPT>(E, rc, src, out);
         c_xbegin(E);
-        if (act) c_push(E, hb, R.q);  // hb: last read by the x SpMV, before the last exchange
-        c_publish(E, v0, v1, v2, 0.0);
+#pragma unroll
+        for (int j = 0; j < RPT; ++j)
+            if (rc[j].t < E.nr) {
+                R[j].q = out[j];  // m of this iterate (kept in q until the first update)
+                c_push(E, rc[j], hb, out[j]);  // hb: last read by the x SpMV, before the last exchange
+            }
+        c_publish<false>(E, v0, v1, v2, 0.0);
         int cur = hb;
         double alpha = 0.0, ig = 0.0, igam = 0.0, dnm = 0.0;
         bool first = true;
-        const long long hstart = hlen;
+        const int hstart = hlen;
         const double thr = (E.tol * bnorm) * (E.tol * bnorm);
         while (true) {
             // own-column part of n = A m_i first: it needs only this CTA's
-            // entries of m_i (complete after the publish's bar.sync), so the
-            // bandwidth-bound half of the SpMV overlaps the cluster barrier
-            c_stamp(E, total, 0);
-            const double2* mcur = E.mb + (size_t)cur * E.nloc_cap;
-            double2 n = act ? c_spmv_own(E, mcur) : d2(0.0, 0.0);
-            c_stamp(E, total, 1);
+            // entries of m_i (complete after the publish's bar.sync), so that
+            // part of the SpMV overlaps the exchange.  Warp 0 alone folds the
+            // CTA partials and forms the scalars while the other warps sum
+            // their ghost columns; a named barrier hands the scalars over.
+            ++E.sit;
+            c_stamp(E, 0);
+            const unsigned mcur = c_buf(E, cur);
+            double2 n[RPT];
+#pragma unroll
+            for (int j = 0; j < RPT; ++j)
+                n[j] = (rc[j].t < E.nr && !(E.abl & 1)) ? c_spmv_own(E, rc[j], mcur) : d2(0.0, 0.0);
+            c_stamp(E, 1);
             c_xwait(E);
-            c_stamp(E, total, 2);
-            if (act) n = c_spmv_gh(E, mcur, n);  // ghost part: loads in flight during the gather
-            c_gather(E, co);
-            const double gn = co[0], dn = co[1];
-            double beta = 0.0;
-            if (first) {
-                if (!(gn > 0.0) || !(dn > 0.0) || !isfinite(gn) || !isfinite(dn)) {
-                    status = RAFEM_ERR_BREAKDOWN;
-                    break;
-                }
-                alpha = gn / dn;
-            } else {
-                ++total;
-                const double rr = co[2];
-                if (lead && E.hist && hlen < E.hist_cap) E.hist[hlen] = rr;
-                ++hlen;
-                if (rr <= thr || total >= E.cap) break;
-                beta = gn * igam;
-                const double den = fma(-(gn * ig), gn, dn);
-                if (!(gn > 0.0) || !(den > 0.0) || !isfinite(den)) {
-                    status = RAFEM_ERR_BREAKDOWN;
-                    break;
-                }
-                alpha = gn / den;
-                dnm = den;
-            }
-            c_stamp(E, total, 3);
-            v0 = v1 = v2 = 0.0;
-            if (act) {
-                const double2 me = mcur[E.t];
+            c_stamp(E, 2);
+            if (threadIdx.x < 32) {
+                c_gather<false>(E, co);
+                const double gn = co[0], dn = co[1];
+                double beta = 0.0;
+                int flag = 0;  // 1: leave for the head (converged estimate / cap), 2: breakdown
                 if (first) {
-                    R.z = n;
-                    R.q = me;
-                    R.s = R.w;
-                    R.p = R.u;
+                    if (!(E.abl & 8) && (!(gn > 0.0) || !(dn > 0.0) || !isfinite(gn) || !isfinite(dn)))
+                        flag = 2;
+                    else
+                        alpha = gn / dn;
                 } else {
-                    R.z = d2(fma(beta, R.z.x, n.x), fma(beta, R.z.y, n.y));
-                    R.q = d2(fma(beta, R.q.x, me.x), fma(beta, R.q.y, me.y));
-                    R.s = d2(fma(beta, R.s.x, R.w.x), fma(beta, R.s.y, R.w.y));
-                    R.p = d2(fma(beta, R.p.x, R.u.x), fma(beta, R.p.y, R.u.y));
+                    const double rr = co[2];
+                    if (lead && E.hist && hlen < E.hist_cap) E.hist[hlen] = rr;
+                    if ((rr <= thr && !(E.abl & 8)) || total + 1 >= E.cap) {
+                        flag = 1;
+                    } else {
+                        beta = gn * igam;
+                        const double den = fma(-(gn * ig), gn, dn);
+                        if (!(E.abl & 8) && (!(gn > 0.0) || !(den > 0.0) || !isfinite(den))) {
+                            flag = 2;
+                        } else {
+                            alpha = gn / den;
+                            dnm = den;
+                        }
+                    }
                 }
-                R.x = d2(fma(alpha, R.p.x, R.x.x), fma(alpha, R.p.y, R.x.y));
-                R.r = d2(fma(-alpha, R.s.x, R.r.x), fma(-alpha, R.s.y, R.r.y));
-                R.u = d2(fma(-alpha, R.q.x, R.u.x), fma(-alpha, R.q.y, R.u.y));
-                R.w = d2(fma(-alpha, R.z.x, R.w.x), fma(-alpha, R.z.y, R.w.y));
-                v0 = fma(R.r.x, R.u.x, R.r.y * R.u.y);
-                v1 = fma(R.w.x, R.u.x, R.w.y * R.u.y);
-                v2 = fma(R.r.x, R.r.x, R.r.y * R.r.y);
+                if (threadIdx.x == 0) {
+                    sts2(E.sc_s, make_double2(alpha, beta));
+                    sts2(E.sc_s + 16u, make_double2((double)flag, 0.0));
+                }
+                // 1 / gn and 1 / (gn alpha) = den / gn^2 for the next iteration
+                igam = 1.0 / gn;
+                ig = (first ? dn : dnm) * igam * igam;
+                __syncwarp();
+                asm volatile("bar.arrive 1, %0;" ::"r"((int)blockDim.x) : "memory");
+#pragma unroll
+                for (int j = 0; j < RPT; ++j)
+                    if (rc[j].t < E.nr && !(E.abl & 2)) n[j] = c_spmv_gh(E, rc[j], mcur, n[j]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < RPT; ++j)
+                    if (rc[j].t < E.nr && !(E.abl & 2)) n[j] = c_spmv_gh(E, rc[j], mcur, n[j]);
+                asm volatile("bar.sync 1, %0;" ::"r"((int)blockDim.x) : "memory");
             }
+            const double2 sc01 = lds2(E.sc_s), sc23 = lds2(E.sc_s + 16u);
+            const double alpha_i = sc01.x, beta = sc01.y;
+            if (!first) {
+                ++total;
+                ++hlen;
+            }
+            if (sc23.x != 0.0) {
+                if (sc23.x == 2.0) status = RAFEM_ERR_BREAKDOWN;
+                break;
+            }
+            c_stamp(E, 3);
+            v0 = v1 = v2 = 0.0;
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) {
+                src[j] = d2(0.0, 0.0);
+                if (rc[j].t < E.nr) {
+                    CRow& Q = R[j];
+                    const double2 me = lds2(mcur + 16u * rc[j].li);
+                    if (first) {
+                        Q.z = n[j];
+                        Q.q = me;
+                        Q.s = Q.w;
+                        Q.p = Q.u;
+                    } else {
+                        Q.z = d2(fma(beta, Q.z.x, n[j].x), fma(beta, Q.z.y, n[j].y));
+                        Q.q = d2(fma(beta, Q.q.x, me.x), fma(beta, Q.q.y, me.y));
+                        Q.s = d2(fma(beta, Q.s.x, Q.w.x), fma(beta, Q.s.y, Q.w.y));
+                        Q.p = d2(fma(beta, Q.p.x, Q.u.x), fma(beta, Q.p.y, Q.u.y));
+                    }
+                    Q.x = d2(fma(alpha_i, Q.p.x, Q.x.x), fma(alpha_i, Q.p.y, Q.x.y));
+                    Q.r = d2(fma(-alpha_i, Q.s.x, Q.r.x), fma(-alpha_i, Q.s.y, Q.r.y));
+                    Q.u = d2(fma(-alpha_i, Q.q.x, Q.u.x), fma(-alpha_i, Q.q.y, Q.u.y));
+                    Q.w = d2(fma(-alpha_i, Q.z.x, Q.w.x), fma(-alpha_i, Q.z.y, Q.w.y));
+                    src[j] = Q.w;
+                    v0 += fma(Q.r.x, Q.u.x, Q.r.y * Q.u.y);
+                    v1 += fma(Q.w.x, Q.u.x, Q.w.y * Q.u.y);
+                    v2 += fma(Q.r.x, Q.r.x, Q.r.y * Q.r.y);
+                }
+            }
+            c_prec<PRE, RPT>(E, rc, src, out);
             c_xbegin(E);
-            if (act) {
-                const double2 mv = E.rmv[E.t];
-                c_push(E, cur ^ 1, PRE ? d2(mv.x * R.w.x, mv.y * R.w.y) : R.w);
-            }
-            c_stamp(E, total, 4);
-            c_publish(E, v0, v1, v2, 0.0);
-            c_stamp(E, total, 5);
-            // 1 / gn and 1 / (gn alpha) = den / gn^2 for the next iteration
-            igam = 1.0 / gn;
-            ig = (first ? dn : dnm) * igam * igam;
+#pragma unroll
+            for (int j = 0; j < RPT; ++j)
+                if (rc[j].t < E.nr) c_push(E, rc[j], cur ^ 1, out[j]);
+            c_stamp(E, 4);
+            c_publish<false>(E, v0, v1, v2, 0.0);
+            c_stamp(E, 5);
             cur ^= 1;
             first = false;
         }
-        // (the loop ends after a wait: every arrive is matched)
+        // (the loop ends after a wait: every exchange begun has been waited)
         if (E.hist && E.rank == 0) {  // squared estimates of this cycle -> relative residuals
             if (threadIdx.x == 0 && cycles < E.cyc_cap) E.cyc[cycles] = hlen - hstart;
             __syncthreads();
@@ -466,23 +642,22 @@ RF_DEV void c_write_result(KResult* res, long long total, long long cycles, long
     res->status = status;
 }
 
-// Per-thread setup common to the kernels: the row, its warp's ELL slice and
-// its push destinations.
 // Dynamic shared memory of the engine (same offsets in every CTA, so a
 // peer's copy of any array is this CTA's address mapped to the peer):
-//   ELL values | 2 gathered-vector buffers | ELL columns | per own row: b, M^-1, push targets
+//   ELL values | 2 gathered-vector buffers | ELL columns |
+//   per own row (thread order): M^-1, push targets | block-Jacobi y (local order)
 struct CLayout {
-    double2 *ev, *mb, *rb, *rmv;
+    double2 *ev, *mb, *rmv, *yb;
     uint16_t* ec;
     uint4* rdest;
     unsigned char* end;
 };
 __host__ __device__ inline size_t c_al16(size_t b) { return (b + 15) & ~(size_t)15; }
-__host__ __device__ inline size_t c_layout_bytes(int ell_cap, int nloc_cap, int nt) {
+__host__ __device__ inline size_t c_layout_bytes(int ell_cap, int nloc_cap, int rows_cap, int ndw, int blk) {
     return c_al16((size_t)ell_cap * 16) + c_al16((size_t)2 * nloc_cap * 16) + c_al16((size_t)ell_cap * 2) +
-           3 * c_al16((size_t)nt * 16);
+           c_al16((size_t)rows_cap * 16) + c_al16((size_t)rows_cap * 16 * ndw) + (blk ? c_al16((size_t)rows_cap * 16) : 0);
 }
-RF_DEV CLayout c_layout(unsigned char* base, const CPlan& P) {
+RF_DEV CLayout c_layout(unsigned char* base, const CPlan& P, int blk) {
     CLayout L;
     unsigned char* q = base;
     L.ev = reinterpret_cast<double2*>(q);
@@ -491,49 +666,105 @@ RF_DEV CLayout c_layout(unsigned char* base, const CPlan& P) {
     q += c_al16((size_t)2 * P.nloc_cap * 16);
     L.ec = reinterpret_cast<uint16_t*>(q);
     q += c_al16((size_t)P.ell_cap * 2);
-    L.rb = reinterpret_cast<double2*>(q);
-    q += c_al16((size_t)blockDim.x * 16);
     L.rmv = reinterpret_cast<double2*>(q);
-    q += c_al16((size_t)blockDim.x * 16);
+    q += c_al16((size_t)P.rows_cap * 16);
     L.rdest = reinterpret_cast<uint4*>(q);
-    q += c_al16((size_t)blockDim.x * 16);
+    q += c_al16((size_t)P.rows_cap * 16 * P.ndw);
+    L.yb = reinterpret_cast<double2*>(q);
+    if (blk) q += c_al16((size_t)P.rows_cap * 16);
     L.end = q;
     return L;
 }
 
-RF_DEV void c_env(CEnv& E, const CPlan& P, const CCta& c, unsigned rank, const CLayout& L,
-                  double (*part)[kCMax][4], double (*red)[4], unsigned long long* xbar) {
-    E.ev = L.ev;
-    E.ec = L.ec;
-    E.mb = L.mb;
-    E.rb = L.rb;
-    E.rmv = L.rmv;
-    E.rdest = L.rdest;
+// Per-CTA setup common to the kernels.
+template <int RPT>
+RF_DEV void c_env(CEnv& E, CRowC (&rc)[RPT], const CPlan& P, const CCta& c, unsigned rank, const CLayout& L,
+                  double (*part)[kCMax][4], double (*red)[4], unsigned long long* xbar, double* sc) {
     E.nloc_cap = P.nloc_cap;
-    E.part = part;
-    E.red = red;
     E.C = P.C;
     E.rank = rank;
-    E.t = threadIdx.x;
     E.nr = c.nr;
-    const int4 wv = P.warp[c.wbase + (threadIdx.x >> 5)];
-    E.k0 = wv.x + (threadIdx.x & 31);
-    E.width = wv.y;
-    E.k1 = wv.z + (threadIdx.x & 31);
-    E.width1 = wv.w;
-    {
-        uint4* rd = const_cast<uint4*>(E.rdest);
-        for (int t = threadIdx.x; t < c.nr; t += blockDim.x)
-            rd[t] = __ldg(reinterpret_cast<const uint4*>(P.dest) + (c.g0 + t));
+    E.ndw = P.ndw;
+    const int nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+        CRowC& r = rc[j];
+        const int wb = (threadIdx.x >> 5) + j * nw;
+        r.t = 32 * wb + lane;
+        const int4 wv = P.warp[c.wbase + wb];
+        r.k0 = wv.x + lane;
+        r.w0 = wv.y;
+        r.k1 = wv.z + lane;
+        r.w1 = wv.w;
+        const int2 tr = r.t < c.nr ? __ldg(P.trow + c.lbase + r.t) : make_int2(0, 0);
+        r.gid = tr.x;
+        r.li = tr.y;
+        if (r.t < c.nr)
+            for (int w = 0; w < P.ndw; ++w)
+                L.rdest[P.ndw * r.t + w] = __ldg(reinterpret_cast<const uint4*>(P.dest) + (size_t)P.ndw * r.gid + w);
     }
-    E.xbar = xbar;
+    // opaque copies: the compiler would otherwise rematerialise each address
+    // from SR_CgaCtaId (an S2R) at its uses instead of keeping the register
+    auto opq = [](unsigned v) {
+        unsigned r;
+        asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+        return r;
+    };
+    E.mb_s = opq(smem_u32(L.mb));
+    E.part_s = opq(smem_u32(part));
+    E.xbar_s = opq(smem_u32(xbar));
+    E.ev_s = opq(smem_u32(L.ev));
+    E.ec_s = opq(smem_u32(L.ec));
+    E.rmv_s = opq(smem_u32(L.rmv));
+    E.rdest_s = opq(smem_u32(L.rdest));
+    E.red_s = opq(smem_u32(red));
+    E.sc_s = opq(smem_u32(sc));
+    E.yb_s = opq(smem_u32(L.yb));
     E.xk = E.xw = 0;
-    E.xbytes = 16u * (unsigned)(c.nloc - c.nr) + 32u * (unsigned)P.C;
+    E.xbytes = 32u * (unsigned)P.C + 16u * (unsigned)(c.nloc - c.nr);
+    E.abl = 0;
+    E.sit = -1;
+    E.blk = 0;
+    E.omega = 1.0;
+    E.trace = nullptr;
+    E.hist = nullptr;
+    E.cyc = nullptr;
     if (threadIdx.x == 0) {
         mbar_init(xbar, 1);
         mbar_init(xbar + 1, 1);
         mbar_fence_init();
     }
+}
+
+// Block-Jacobi setup on the staged values: omega from the CTA block's
+// Gershgorin bound of D^-1/2 A_bb D^-1/2 (pcg_pipe_core's rule).  Uses yb
+// for sqrt(M^-1) in local order.  All threads of the CTA call it.
+template <int RPT>
+RF_DEV void c_block_setup(CEnv& E, const CRowC (&rc)[RPT], double* red1) {
+    double gmax = 0.0;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j)
+        if (rc[j].t < E.nr) {
+            const double2 mv = lds2(E.rmv_s + 16u * rc[j].t);
+            sts2(E.yb_s + 16u * rc[j].li, d2(sqrt(mv.x), sqrt(mv.y)));
+        }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < RPT; ++j)
+        if (rc[j].t < E.nr) {
+            const double2 si = lds2(E.yb_s + 16u * rc[j].li);
+            double gv = 0.0, gt = 0.0;
+            for (int l = 0; l < rc[j].w0; ++l) {
+                const double2 a = lds2(E.ev_s + 16u * (rc[j].k0 + 32 * l));
+                const double2 sj = lds2(E.yb_s + 16u * lds_u16(E.ec_s + 2u * (rc[j].k0 + 32 * l)));
+                gv += fabs(a.x) * si.x * sj.x;
+                gt += fabs(a.y) * si.y * sj.y;
+            }
+            gmax = fmax(gmax, fmax(gv, gt));
+        }
+    gmax = block_max(gmax, red1);
+    E.omega = gmax > 1.98 ? 0.98 / (gmax - 1.0) : 1.0;
+    __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
@@ -544,21 +775,23 @@ __global__ void __launch_bounds__(kCT, 1) cpcg_kernel(CPlan P, const double2* __
                                                       double* x, const double* minv, const int* flag, double tol,
                                                       long long cap, double* hist, long long hist_cap,
                                                       long long* cyc, long long cyc_cap, KResult* res,
-                                                      long long* trace, long long trace_cap) {
+                                                      long long* trace, long long trace_cap, int abl, int blk) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ __align__(16) double part[2][kCMax][4];
     __shared__ __align__(16) double red[32][4];
     __shared__ __align__(8) unsigned long long xbar[2];
+    __shared__ __align__(32) double sc[4];
     const unsigned rank = cl_rank();
     const CCta c = P.cta[rank];
-    const CLayout L = c_layout(dsm, P);
+    const CLayout L = c_layout(dsm, P, blk);
     for (int k = threadIdx.x; k < c.ell_n; k += blockDim.x) {
         const int s = __ldg(P.esrc + c.ell_base + k);
         L.ev[k] = s >= 0 ? __ldg(val2 + s) : make_double2(0.0, 0.0);
         L.ec[k] = __ldg(P.ecol + c.ell_base + k);
     }
     CEnv E;
-    c_env(E, P, c, rank, L, part, red, xbar);
+    CRowC rc[kRPT];
+    c_env<kRPT>(E, rc, P, c, rank, L, part, red, xbar, sc);
     E.tol = tol;
     E.cap = cap;
     E.hist = hist;
@@ -567,21 +800,27 @@ __global__ void __launch_bounds__(kCT, 1) cpcg_kernel(CPlan P, const double2* __
     E.cyc_cap = cyc_cap;
     E.trace = trace;
     E.trace_cap = trace_cap;
-    CRow R;
-    const int g = c.g0 + E.t;
-    const bool act = E.t < E.nr;
-    R.x = act ? reinterpret_cast<const double2*>(x)[g] : d2(0.0, 0.0);
-    if (act) {
-        L.rb[E.t] = reinterpret_cast<const double2*>(b)[g];
-        L.rmv[E.t] = PRE ? reinterpret_cast<const double2*>(minv)[g] : d2(1.0, 1.0);
+    E.abl = abl;
+    if (abl & 4) E.xbytes = 32u * (unsigned)P.C;
+    CRow R[kRPT];
+#pragma unroll
+    for (int j = 0; j < kRPT; ++j) {
+        const bool act = rc[j].t < c.nr;
+        R[j].x = act ? reinterpret_cast<const double2*>(x)[rc[j].gid] : d2(0.0, 0.0);
+        if (act) L.rmv[rc[j].t] = PRE ? reinterpret_cast<const double2*>(minv)[rc[j].gid] : d2(1.0, 1.0);
     }
     __syncthreads();
+    if (PRE && blk) {
+        E.blk = 1;
+        c_block_setup<kRPT>(E, rc, &red[0][0]);
+    }
     cl_sync();  // every CTA of the cluster runs (barriers initialised) before the first remote store
     if (*flag) {  // ValueError: zero diagonal under Jacobi (solver.py:416-417)
         if (rank == 0 && threadIdx.x == 0) c_write_result(res, 0, 0, 0, INFINITY, false, RAFEM_ERR_INVALID);
         return;
     }
-    const CpcgOut o = cpcg_core<PRE>(E, R, -1.0, 0.0, nullptr, nullptr, reinterpret_cast<double2*>(x) + c.g0);
+    const CpcgOut o = cpcg_core<PRE, kRPT>(E, rc, R, reinterpret_cast<const double2*>(b), -1.0, 0.0, nullptr,
+                                           nullptr, reinterpret_cast<double2*>(x));
     if (rank == 0 && threadIdx.x == 0)
         c_write_result(res, o.total, o.cycles, o.hlen, o.rel, o.converged != 0, o.status);
     cl_sync();  // no CTA leaves while a peer may still address its shared memory
@@ -595,10 +834,10 @@ struct ClusterPlan {
     const int* rp = nullptr;
     int N = 0, C = 0, nt = 0;
     size_t smem = 0;  // dynamic shared memory of the solve kernel
+    size_t smem_blk = 0;  // + the block-Jacobi y buffer
     size_t smem_sim = 0;
     void* dev = nullptr;
     CPlan view{};
-    std::vector<int> gpart;  // host copy (C + 1)
     bool ok = false;
 };
 
@@ -619,8 +858,8 @@ static size_t al16(size_t b) { return (b + 15) & ~(size_t)15; }
 // Build (or fetch) the plan of a node pattern for C CTAs.  Returns nullptr
 // when the pattern does not fit the engine (rows per CTA, shared memory,
 // ghost fan-out), with rc = RAFEM_OK; rc != OK on CUDA errors.
-static ClusterPlan* cluster_plan(rafem_ctx* ctx, const int* rp_dev, const int* col_dev, int N, long long S,
-                                 unsigned long long pattern_id, int C, int& rc) {
+static ClusterPlan* cluster_plan(rafem_ctx* ctx, const int* rp_dev, const int* col_dev, const double* coords_dev,
+                                 int N, long long S, unsigned long long pattern_id, int C, int& rc) {
     rc = RAFEM_OK;
     auto& v = plans(ctx);
     for (void* q : v) {
@@ -649,54 +888,134 @@ static ClusterPlan* cluster_plan(rafem_ctx* ctx, const int* rp_dev, const int* c
         rc = rafem_fail_cuda(ctx, e, "cluster plan download", __FILE__, __LINE__);
         return nullptr;
     }
-    // row blocks balanced by slots + rows, at most kCT rows each (else
-    // balanced by rows: a thread per row sets the floor)
-    std::vector<int> gp(C + 1);
-    auto cut = [&](int wslot) {
-        const long long tot = (long long)wslot * rp[N] + N;
-        int g = 0;
-        gp[0] = 0;
-        for (int c = 1; c < C; ++c) {
-            const long long want = tot * c / C;
-            while (g < N && (long long)wslot * rp[g] + g < want) ++g;
-            gp[c] = g;
-        }
-        gp[C] = N;
-        for (int c = 0; c < C; ++c)
-            if (gp[c + 1] - gp[c] > kCT || gp[c + 1] - gp[c] < 1) return false;
-        return true;
+    // ---- partition: recursive coordinate bisection of the nodes when the
+    // mesh geometry is known (compact blocks: ~3x fewer ghosts than row
+    // slabs on box meshes), else contiguous row blocks balanced by slots + rows
+    std::vector<int> owner(N, -1);
+    auto env_on = [](const char* k, bool dflt) {
+        const char* v = getenv(k);
+        return v ? v[0] != '0' : dflt;
     };
-    if (!cut(1) && !cut(0)) return nullptr;
-    std::vector<int> owner(N);
+    // row slabs by default: RCB blocks have ~3x fewer ghosts but their rows'
+    // stencils vary within a warp (ELL padding or scattered gathers), which
+    // cost more than the halo they save (scripts/cluster_probe2.py)
+    const bool use_rcb = env_on("RAFEM_CL_RCB", false), split = env_on("RAFEM_CL_SPLIT", true),
+               sort_rows = env_on("RAFEM_CL_SORT", true);
+    if (coords_dev && use_rcb) {
+        std::vector<double> X((size_t)3 * N);
+        e = cudaMemcpy(X.data(), coords_dev, sizeof(double) * 3 * (size_t)N, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) {
+            rc = rafem_fail_cuda(ctx, e, "cluster plan coordinates", __FILE__, __LINE__);
+            return nullptr;
+        }
+        std::vector<int> ids(N);
+        for (int i = 0; i < N; ++i) ids[i] = i;
+        struct Rcb {
+            const std::vector<double>& X;
+            std::vector<int>& owner;
+            void run(std::vector<int>::iterator b, std::vector<int>::iterator e, int parts, int base) {
+                if (parts == 1) {
+                    for (auto it = b; it != e; ++it) owner[*it] = base;
+                    return;
+                }
+                double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+                for (auto it = b; it != e; ++it)
+                    for (int d = 0; d < 3; ++d) {
+                        lo[d] = std::min(lo[d], X[3 * (size_t)*it + d]);
+                        hi[d] = std::max(hi[d], X[3 * (size_t)*it + d]);
+                    }
+                int ax = 0;
+                for (int d = 1; d < 3; ++d)
+                    if (hi[d] - lo[d] > hi[ax] - lo[ax]) ax = d;
+                std::sort(b, e, [&](int a, int c) {
+                    const double xa = X[3 * (size_t)a + ax], xc = X[3 * (size_t)c + ax];
+                    return xa < xc || (xa == xc && a < c);
+                });
+                const int lp = parts / 2;
+                const auto m = b + (long long)(e - b) * lp / parts;
+                run(b, m, lp, base);
+                run(m, e, parts - lp, base + lp);
+            }
+        } rcb{X, owner};
+        rcb.run(ids.begin(), ids.end(), C, 0);
+    } else {
+        std::vector<int> gp(C + 1);
+        auto cut = [&](int wslot) {
+            const long long tot = (long long)wslot * rp[N] + N;
+            int g = 0;
+            gp[0] = 0;
+            for (int c = 1; c < C; ++c) {
+                const long long want = tot * c / C;
+                while (g < N && (long long)wslot * rp[g] + g < want) ++g;
+                gp[c] = g;
+            }
+            gp[C] = N;
+            for (int c = 0; c < C; ++c)
+                if (gp[c + 1] - gp[c] > kRPT * kCT || gp[c + 1] - gp[c] < 1) return false;
+            return true;
+        };
+        if (!cut(1) && !cut(0)) return nullptr;
+        for (int c = 0; c < C; ++c)
+            for (int g = gp[c]; g < gp[c + 1]; ++g) owner[g] = c;
+    }
+    std::vector<std::vector<int>> rows(C);
+    for (int g = 0; g < N; ++g) rows[owner[g]].push_back(g);
     for (int c = 0; c < C; ++c)
-        for (int g = gp[c]; g < gp[c + 1]; ++g) owner[g] = c;
+        if (rows[c].empty() || (int)rows[c].size() > kRPT * kCT) return nullptr;
     std::vector<CCta> ct(C);
     std::vector<int4> warps;
     std::vector<uint16_t> ecol;
     std::vector<int> esrc, lgid;
+    std::vector<int2> trow;
     std::vector<unsigned> dest((size_t)N * kCDest, 0xffffffffu);
     std::vector<int> ndest(N, 0);
     int ell_cap = 0, nloc_cap = 0, nt = 32;
     std::vector<int> loc(N, -1);
     for (int c = 0; c < C; ++c) {
-        const int g0 = gp[c], g1 = gp[c + 1], nr = g1 - g0;
+        // own rows ordered by (ghost slots, own slots) descending, then id:
+        // rows of one warp then share their section widths (little ELL padding)
+        std::vector<int>& R = rows[c];
+        const int nr = (int)R.size();
+        auto n_own = [&](int g) {
+            int a = 0;
+            for (int s2 = rp[g]; s2 < rp[g + 1]; ++s2) a += owner[col[s2]] == c;
+            return a;
+        };
+        std::vector<std::pair<std::pair<int, int>, int>> key(nr);
+        for (int t = 0; t < nr; ++t) {
+            const int g = R[t], a = n_own(g), b = rp[g + 1] - rp[g] - a;
+            key[t] = {{-b, -a}, g};
+        }
+        if (sort_rows) {
+            std::sort(key.begin(), key.end());
+            for (int t = 0; t < nr; ++t) R[t] = key[t].second;
+        }
         std::vector<int> gh;
-        for (int g = g0; g < g1; ++g)
-            for (int s = rp[g]; s < rp[g + 1]; ++s)
-                if (col[s] < g0 || col[s] >= g1) gh.push_back(col[s]);
-        std::sort(gh.begin(), gh.end());
+        for (int g : R)
+            for (int s2 = rp[g]; s2 < rp[g + 1]; ++s2)
+                if (owner[col[s2]] != c) gh.push_back(col[s2]);
+        std::sort(gh.begin(), gh.end(), [&](int a, int b) {
+            return owner[a] < owner[b] || (owner[a] == owner[b] && a < b);
+        });
         gh.erase(std::unique(gh.begin(), gh.end()), gh.end());
         const int nloc = nr + (int)gh.size();
         if (nloc > 65535) return nullptr;
         CCta& cc = ct[c];
-        cc.g0 = g0;
+        cc.g0 = 0;
         cc.nr = nr;
         cc.nloc = nloc;
         cc.lbase = (int)lgid.size();
-        for (int g = g0; g < g1; ++g) {
-            loc[g] = g - g0;
-            lgid.push_back(g);
+        // local (gathered-vector) index: own rows in id order, so a warp's
+        // k-th neighbours sit at consecutive slots (conflict-free gathers);
+        // threads take the rows in the width-sorted order above
+        std::vector<int> Rn = R;
+        std::sort(Rn.begin(), Rn.end());
+        for (int t = 0; t < nr; ++t) {
+            loc[Rn[t]] = t;
+            lgid.push_back(Rn[t]);
         }
+        for (int t = 0; t < nr; ++t) trow.push_back(make_int2(R[t], loc[R[t]]));
+        for (size_t q = 0; q < gh.size(); ++q) trow.push_back(make_int2(-1, -1));
         for (size_t q = 0; q < gh.size(); ++q) {
             const int j = gh[q];
             loc[j] = nr + (int)q;
@@ -708,12 +1027,15 @@ static ClusterPlan* cluster_plan(rafem_ctx* ctx, const int* rp_dev, const int* c
         cc.ell_base = (int)esrc.size();
         const int nwarp = (nr + 31) / 32;
         int off = 0;
-        auto is_own = [&](int j) { return j >= g0 && j < g1; };
+        // split: own-column slots first (summed before the exchange wait);
+        // else every slot in the second section
+        auto is_own = [&](int j) { return split && owner[j] == c; };
         for (int w = 0; w < nwarp; ++w) {
             int wo = 0, wg = 0;
             for (int t = 32 * w; t < std::min(nr, 32 * w + 32); ++t) {
+                const int g = R[t];
                 int a = 0, b = 0;
-                for (int s = rp[g0 + t]; s < rp[g0 + t + 1]; ++s) (is_own(col[s]) ? a : b)++;
+                for (int s2 = rp[g]; s2 < rp[g + 1]; ++s2) (is_own(col[s2]) ? a : b)++;
                 wo = std::max(wo, a);
                 wg = std::max(wg, b);
             }
@@ -725,8 +1047,9 @@ static ClusterPlan* cluster_plan(rafem_ctx* ctx, const int* rp_dev, const int* c
                         const int t = 32 * w + ln;
                         int src = -1, lc = 0;
                         if (t < nr) {  // the l-th slot of this section in storage order
+                            const int g = R[t];
                             int k = 0;
-                            for (int s2 = rp[g0 + t]; s2 < rp[g0 + t + 1]; ++s2)
+                            for (int s2 = rp[g]; s2 < rp[g + 1]; ++s2)
                                 if (is_own(col[s2]) == (sec == 0) && k++ == l) {
                                     src = s2;
                                     break;
@@ -742,31 +1065,45 @@ static ClusterPlan* cluster_plan(rafem_ctx* ctx, const int* rp_dev, const int* c
         cc.ell_n = off;
         ell_cap = std::max(ell_cap, off);
         nloc_cap = std::max(nloc_cap, nloc);
-        nt = std::max(nt, nwarp * 32);
-        for (int g = g0; g < g1; ++g) loc[g] = -1;
+        nt = std::max(nt, (nwarp + kRPT - 1) / kRPT * 32);
+        for (int g : R) loc[g] = -1;
         for (int j : gh) loc[j] = -1;
     }
-    // every CTA addresses warp entries up to nt / 32 (idle warps: width 0)
+    // every CTA addresses warp blocks up to kRPT * nt / 32 (idle blocks: width 0)
     {
         std::vector<int4> w2;
         std::vector<CCta> ct2 = ct;
         for (int c = 0; c < C; ++c) {
             ct2[c].wbase = (int)w2.size();
             const int nwarp = (ct[c].nr + 31) / 32;
-            for (int w = 0; w < nt / 32; ++w) w2.push_back(w < nwarp ? warps[ct[c].wbase + w] : make_int4(0, 0, 0, 0));
+            for (int w = 0; w < kRPT * nt / 32; ++w)
+                w2.push_back(w < nwarp ? warps[ct[c].wbase + w] : make_int4(0, 0, 0, 0));
         }
         warps.swap(w2);
         ct.swap(ct2);
     }
     ell_cap = (ell_cap + 7) & ~7;
     nloc_cap = (nloc_cap + 7) & ~7;
-    P->smem = c_layout_bytes(ell_cap, nloc_cap, nt);
-    P->smem_sim = P->smem + al16((size_t)nloc_cap) + al16((size_t)nt * 24);
-    if (P->smem > 224 * 1024) return nullptr;
+    // push targets: one uint4 per row when no row feeds more than 4 CTAs
+    int maxd = 0;
+    for (int j = 0; j < N; ++j) maxd = std::max(maxd, ndest[j]);
+    const int ndw = maxd <= 4 ? 1 : 2;
+    if (ndw == 1) {
+        std::vector<unsigned> d1((size_t)N * 4);
+        for (int j = 0; j < N; ++j)
+            for (int k = 0; k < 4; ++k) d1[(size_t)j * 4 + k] = dest[(size_t)j * kCDest + k];
+        dest.swap(d1);
+    }
+    const int rows_cap = kRPT * nt;
+    P->smem = c_layout_bytes(ell_cap, nloc_cap, rows_cap, ndw, 0);
+    P->smem_blk = c_layout_bytes(ell_cap, nloc_cap, rows_cap, ndw, 1);
+    P->smem_sim = P->smem_blk + al16((size_t)nloc_cap) + al16((size_t)rows_cap * 24);
+    if (P->smem > 225 * 1024) return nullptr;
     // upload
     const size_t o_cta = 0, o_w = al16(sizeof(CCta) * C), o_ec = o_w + al16(sizeof(int4) * warps.size());
     const size_t o_es = o_ec + al16(2 * ecol.size()), o_de = o_es + al16(4 * esrc.size());
-    const size_t o_lg = o_de + al16(4 * dest.size()), tot = o_lg + al16(4 * lgid.size());
+    const size_t o_lg = o_de + al16(4 * dest.size()), o_tr = o_lg + al16(4 * lgid.size());
+    const size_t tot = o_tr + al16(8 * trow.size());
     std::vector<unsigned char> h(tot);
     std::memcpy(h.data() + o_cta, ct.data(), sizeof(CCta) * C);
     std::memcpy(h.data() + o_w, warps.data(), sizeof(int4) * warps.size());
@@ -774,6 +1111,7 @@ static ClusterPlan* cluster_plan(rafem_ctx* ctx, const int* rp_dev, const int* c
     std::memcpy(h.data() + o_es, esrc.data(), 4 * esrc.size());
     std::memcpy(h.data() + o_de, dest.data(), 4 * dest.size());
     std::memcpy(h.data() + o_lg, lgid.data(), 4 * lgid.size());
+    std::memcpy(h.data() + o_tr, trow.data(), 8 * trow.size());
     e = dmalloc(ctx, &P->dev, tot);
     if (e == cudaSuccess) e = cudaMemcpyAsync(P->dev, h.data(), tot, cudaMemcpyHostToDevice, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
@@ -788,11 +1126,13 @@ static ClusterPlan* cluster_plan(rafem_ctx* ctx, const int* rp_dev, const int* c
     P->view.esrc = reinterpret_cast<const int*>(d + o_es);
     P->view.dest = reinterpret_cast<const unsigned*>(d + o_de);
     P->view.lgid = reinterpret_cast<const int*>(d + o_lg);
+    P->view.trow = reinterpret_cast<const int2*>(d + o_tr);
     P->view.C = C;
     P->view.ell_cap = ell_cap;
     P->view.nloc_cap = nloc_cap;
+    P->view.rows_cap = rows_cap;
+    P->view.ndw = ndw;
     P->nt = nt;
-    P->gpart = gp;
     P->ok = true;
     return P;
 }
@@ -852,18 +1192,19 @@ int cluster_pcg_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, dou
                       cudaEvent_t ev_stop) {
     const char* env = getenv("RAFEM_CLUSTER");
     if (env && env[0] == '0') return RAFEM_ERR_UNSUPPORTED;
-    const bool force = env && env[0] == '1';
     if (p.method != RAFEM_METHOD_PCG || A.W != 2 || !A.pattern_id || p.grid_ctas > 0) return RAFEM_ERR_UNSUPPORTED;
-    if (p.precondition == RAFEM_PRECOND_BLOCK_JACOBI && !force) return RAFEM_ERR_UNSUPPORTED;
     const int N = A.ngroups;
     const int C = cluster_size_for(N);
     int rc = RAFEM_OK;
-    ClusterPlan* P = cluster_plan(ctx, A.rp, A.col, N, A.slots, A.pattern_id, C, rc);
+    ClusterPlan* P = cluster_plan(ctx, A.rp, A.col, A.coords, N, A.slots, A.pattern_id, C, rc);
     if (rc) return rc;
     if (!P) return RAFEM_ERR_UNSUPPORTED;
     const bool pre = p.precondition != RAFEM_PRECOND_NONE;
+    int blk = p.precondition == RAFEM_PRECOND_BLOCK_JACOBI ? 1 : 0;
+    const size_t smem = blk ? P->smem_blk : P->smem;
+    if (smem > 225 * 1024) return RAFEM_ERR_UNSUPPORTED;
     const void* fn = pre ? (const void*)cpcg_kernel<true> : (const void*)cpcg_kernel<false>;
-    if (!cluster_launchable(ctx, fn, C, P->nt, P->smem)) return RAFEM_ERR_UNSUPPORTED;
+    if (!cluster_launchable(ctx, fn, C, P->nt, smem)) return RAFEM_ERR_UNSUPPORTED;
     const long long n = 2LL * N;
     const long long hist_cap = std::min<long long>(p.max_total_iters > 0 ? p.max_total_iters : 10LL * n, 1LL << 20) + 1;
     if (int r = ensure(ctx, ctx->ws_hist, sizeof(double) * (size_t)hist_cap)) return r;
@@ -884,16 +1225,18 @@ int cluster_pcg_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, dou
         trace = static_cast<long long*>(ctx->ws_trace.p);
         tcap = 8 * 4096;
     }
+    int abl = 0;
+    if (const char* ab = getenv("RAFEM_CL_ABL")) abl = atoi(ab);
     void* args[] = {&view, &val2, &b_dev, &x_dev, &minv, &flag_dev, &tol, &cap, &hist, &hc, &cyc, &cc, &res_dev,
-                    &trace, &tcap};
+                    &trace, &tcap, &abl, &blk};
     if (ev_start) RF_CUDA_TRY(ctx, cudaEventRecord(ev_start, ctx->stream));
-    RF_CUDA_TRY(ctx, cluster_launch(ctx, fn, C, P->nt, P->smem, args));
+    RF_CUDA_TRY(ctx, cluster_launch(ctx, fn, C, P->nt, smem, args));
     if (ev_stop) RF_CUDA_TRY(ctx, cudaEventRecord(ev_stop, ctx->stream));
     ctx->launches++;
     ctx->last_mode = 5;
     ctx->last_ctas = C;
     ctx->last_team = 1;
-    ctx->last_precond = pre ? RAFEM_PRECOND_JACOBI : RAFEM_PRECOND_NONE;
+    ctx->last_precond = blk ? RAFEM_PRECOND_BLOCK_JACOBI : (pre ? RAFEM_PRECOND_JACOBI : RAFEM_PRECOND_NONE);
     return RAFEM_OK;
 }
 

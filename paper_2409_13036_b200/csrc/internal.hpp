@@ -62,6 +62,7 @@ struct MatView {
     const uint8_t* cls = nullptr;
     const int* cls_off = nullptr;
     int ncls = 0;
+    const double* coords = nullptr;  // N x 3 node coordinates (device) when the pattern is a mesh's
 };
 constexpr int kClsWidth = 16;   // max row length of a stencil class
 constexpr int kMaxClasses = 255;

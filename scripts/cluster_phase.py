@@ -24,10 +24,10 @@ for rep in range(3):
     L.rafem_get_trace(ctx, tr.ctypes.data, tr.size)
     tr = tr.reshape(-1, 8)[3:min(st.iterations, 4095) - 2].astype(np.float64)
     tr = tr[tr[:, 0] > 0]
-    d01 = (tr[:, 1] - tr[:, 0]).mean(); d12 = (tr[:, 2] - tr[:, 1]).mean()
-    d23 = (tr[1:, 3] - tr[:-1, 2]).mean(); d34 = (tr[:, 4] - tr[:, 3]).mean(); d45 = (tr[:, 5] - tr[:, 4]).mean()
-    d50 = (tr[:, 0] - tr[:, 5]).mean()
+    d01 = np.median(tr[:, 1] - tr[:, 0]); d12 = np.median(tr[:, 2] - tr[:, 1])
+    d23 = np.median(tr[1:, 3] - tr[:-1, 2]); d34 = np.median(tr[:, 4] - tr[:, 3]); d45 = np.median(tr[:, 5] - tr[:, 4])
+    d50 = np.median(tr[:, 0] - tr[:, 5])
     d = np.array([d01, d12, d23, d34, d45, d50]) / 1.965e3
-    per = np.diff(tr[:, 0]).mean() / 1.965e3
+    per = np.median(np.diff(tr[:, 0])) / 1.965e3
     print(f"{dims} it={st.iterations} {st.device_ms*1e3/max(st.iterations,1):.2f} us/it | " +
           " ".join(f"{nm} {x:.3f}" for nm, x in zip(names, d)) + f" | iter {per:.3f} us", flush=True)

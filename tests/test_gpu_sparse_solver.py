@@ -334,7 +334,7 @@ def test_block_jacobi_pcg_on_fem_systems(dims):
     res = np.linalg.norm(b - O.matvec(a.row_ptr, a.col_idx, a.vals, x)) / np.linalg.norm(b)
     assert st.converged and res <= 1e-10 and abs(st.final_relative_residual - res) < 1e-12
     xj, sj = solve(a, b, x0=x0, config=SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-10))
-    assert rel_err(x, xj) < 1e-8
+    assert rel_err(x, xj) < 1e-7  # two solutions at residual 1e-10 (kappa ~ 1e3)
     if n > 3000:
         assert st.iterations < 0.85 * sj.iterations
     x2, st2 = solve(a, b, x0=x0, config=SolverConfig(backend="pcg", precondition="block_jacobi", tolerance=1e-10))
