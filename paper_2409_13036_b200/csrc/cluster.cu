@@ -227,11 +227,18 @@ RF_DEV double2 c_spmv(const CEnv& E, const CRowC& rc, unsigned src) {
 // Exchange k (= E.xk) begins: thread 0 arms the CTA's mbarrier with the
 // bytes it will receive (peers' messages may already have landed: the
 // transaction count then runs negative until this arrive).
-RF_DEV void c_xbegin(const CEnv& E) {
+RF_DEV void c_xbegin(const CEnv& E, unsigned bytes) {
     if (threadIdx.x == 0)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(E.xbar_s + 8u * (E.xk & 1)),
-                     "r"(E.xbytes)
+                     "r"(bytes)
                      : "memory");
+}
+RF_DEV void c_xbegin(const CEnv& E) { c_xbegin(E, E.xbytes); }
+
+RF_DEV long long global_ns_c() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
 }
 
 // A row's entry of buffer `buf`: local store + a push into every CTA that
@@ -827,6 +834,369 @@ __global__ void __launch_bounds__(kCT, 1) cpcg_kernel(CPlan P, const double2* __
 }
 
 // ---------------------------------------------------------------------------
+// The whole adaptive simulation in one cluster (run_simulation fem.py:554-644
+// around corrector_step fem.py:463-540, the same control as simulate_dev.cuh).
+// Per corrector pass: element scalars (sigma, T-rhs loads) of the CTA's
+// element range -> cluster barrier -> every CTA fills its own rows' ELL
+// values straight into shared memory from the stored geometry (per-slot
+// contributor lists in ascending element order: fill_slot's sums, bit for
+// bit) -> ONE all-reduce of the equilibration sums and the PhysicsRange flag
+// -> scale, Dirichlet elimination and Jacobi inverse on the own rows in
+// place -> the cluster PCG on the staged slice -> corrector delta from its
+// final head.  Fields live in global memory (owners write their rows).
+
+struct CSimArgs {
+    CPlan P;
+    AsmMesh m;
+    double* xs;        // 4 x n2 working dof vectors
+    double* final_x;   // n2
+    double* esig;      // M
+    double* eload;     // 4M
+    double* rhs;       // n2: the pass's constrained right-hand side (read by the solver heads)
+    long long n2;
+    rafem_sim_params p;
+    double* rec_x;
+    double* rec_time;
+    double* rec_dt;
+    int* rec_iters;
+    long long rec_cap;
+    SimDevOut* out;
+    double* ring;
+    int ring_slots;
+    volatile long long* prog;
+    volatile long long* cons;
+    int blk;
+    int vx0;
+};
+
+// Contribution (e, a, b) of the fused fill: element_core's arithmetic.
+RF_DEV double2 c_contrib(const AsmMesh& m, unsigned idx, const double* sig, const double* rk, const double* rrc) {
+    const int e = (int)(idx >> 4), a = (int)((idx >> 2) & 3), b = (int)(idx & 3);
+    const int rg = __ldg(m.region + e);
+    const double vol = __ldg(m.vol + e);
+    const double sigma = __ldcg(sig + e);
+    const double bab = __ldg(m.base + 10LL * e + sym_index(a, b));
+    const double mass = a == b ? mul(vol, 0.1) : mul(vol, 0.05);
+    return make_double2(mul(sigma, bab), add(mul(rrc[rg], mass), mul(rk[rg], bab)));
+}
+
+template <bool PRE>
+__global__ void __launch_bounds__(kCT, 1) csim_kernel(CSimArgs S) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ __align__(16) double part[2][kCMax][4];
+    __shared__ __align__(16) double red[32][4];
+    __shared__ __align__(8) unsigned long long xbar[2];
+    __shared__ __align__(32) double sc[4];
+    __shared__ double rk[kCRegions], rrc[kCRegions];
+    const CPlan& P = S.P;
+    const AsmMesh& m = S.m;
+    const rafem_sim_params& p = S.p;
+    const unsigned rank = cl_rank();
+    const CCta c = P.cta[rank];
+    const CLayout L = c_layout(dsm, P, S.blk);
+    uint8_t* lkind = L.end;  // kinds of the local nodes: V | T << 2
+    for (int k = threadIdx.x; k < c.ell_n; k += blockDim.x) L.ec[k] = __ldg(P.ecol + c.ell_base + k);
+    for (int q = threadIdx.x; q < c.nloc; q += blockDim.x) {
+        const int g = __ldg(P.lgid + c.lbase + q);
+        lkind[q] = (uint8_t)(m.kind[2LL * g] | (m.kind[2LL * g + 1] << 2));
+    }
+    CEnv E;
+    CRowC rc[1];
+    c_env<1>(E, rc, P, c, rank, L, part, red, xbar, sc);
+    E.tol = p.solver.tolerance;
+    E.cap = p.solver.max_total_iters > 0 ? p.solver.max_total_iters : 10LL * S.n2;
+    CRowC& r0 = rc[0];
+    const bool act = r0.t < c.nr;
+    const int g = r0.gid;
+    const unsigned xvec = E.xbytes, xpart = 32u * (unsigned)P.C;
+    const int M = m.M, e0 = (int)((long long)M * rank / P.C), e1 = (int)((long long)M * (rank + 1) / P.C);
+    const long long n2 = S.n2;
+    auto X = [&](int i) { return reinterpret_cast<double2*>(S.xs + (long long)i * n2); };
+    int iacc = 0, iprev = 1, iit = 2, inew = 3;
+    // the row's CSR slots and its diagonal slot
+    const int s_beg = act ? __ldg(m.rp + g) : 0, s_end = act ? __ldg(m.rp + g + 1) : 0;
+    const int s_diag = act ? (__ldg(m.diag + g) >= 0 ? s_beg + __ldg(m.diag + g) : -1) : -1;
+    const uint8_t kvt = act ? lkind[r0.li] : 0;
+    const int kV = kvt & 3, kT = kvt >> 2;
+    if (act) {  // initial_state (fem.py:170-180)
+        X(iacc)[g] = d2(0.0, p.initial_temp);
+        X(iprev)[g] = d2(0.0, p.initial_temp);
+    }
+    __syncthreads();
+    cl_sync();
+
+    double t = 0.0, dt_state = p.dt_init, dt_prev = p.dt_init;
+    long long step = 0, passes = 0, corr = 0, inner = 0, halv = 0, bad = -1;
+    long long asm_ns = 0, sol_ns = 0;
+    int status = RAFEM_OK, failed_step = -1;
+    double failed_dt = 0.0;
+    while (t < p.total_time) {
+        if (p.max_steps > 0 && step >= p.max_steps) break;
+        const double remaining = p.total_time - t;
+        const bool final_step = dt_state >= remaining;
+        const double dt = final_step ? remaining : dt_state;
+        const double ratio = dt / dt_prev;
+        if (act) {  // predictor (fem.py:437-449); the first pass's solver start extrapolates V too
+            const double2 xa = X(iacc)[g];
+            double2 xe = xa;
+            if (step >= 1) {
+                const double2 xp = X(iprev)[g];
+                xe = d2(add(xa.x, mul(ratio, sub(xa.x, xp.x))), add(xa.y, mul(ratio, sub(xa.y, xp.y))));
+            }
+            X(iit)[g] = d2(xa.x, xe.y);
+            if (S.vx0) X(inew)[g] = xe;
+        }
+        bool conv = false, abort_run = false;
+        int iters = 0;
+        for (int it = 1; it <= p.max_corrector_iters; ++it) {
+            iters = it;
+            ++passes;
+            const long long ta = global_ns_c();
+            if (S.ring && rank == 0 && threadIdx.x == 0 && it == 1) {
+                __threadfence_system();
+                *S.prog = step;  // every accepted record is in the ring
+                long long spins = 0;
+                while (step - *S.cons >= S.ring_slots) {
+                    __nanosleep(2000);
+                    if (++spins > (1LL << 31)) asm volatile("trap;");
+                }
+            }
+            __syncthreads();
+            cl_sync();  // the iterate is complete everywhere (global memory, cluster scope)
+            // ---- element scalars of this CTA's element range
+            for (int r = threadIdx.x; r < m.nreg && r < kCRegions; r += blockDim.x) {
+                rk[r] = m.regtab[r];
+                rrc[r] = m.regtab[m.nreg + r] / dt;  // element_core's rcdt
+            }
+            const double2* xit = X(iit);
+            const AsmFields f{S.xs + (long long)iit * n2 + 1, 2, S.xs + (long long)iit * n2, 2,
+                              S.xs + (long long)iacc * n2 + 1, 2, dt};
+            double badv = 0.0;
+            for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+                double sg, l4[4];
+                if (element_scalars(e, m, f, &sg, l4)) badv = fmax(badv, (double)(M - e));
+                __stcg(S.esig + e, sg);
+                __stcg(reinterpret_cast<double2*>(S.eload + 4LL * e), make_double2(l4[0], l4[1]));
+                __stcg(reinterpret_cast<double2*>(S.eload + 4LL * e) + 1, make_double2(l4[2], l4[3]));
+            }
+            __syncthreads();
+            cl_sync();  // element scalars visible to every CTA
+            // ---- fill the own row's ELL entries in place (contributor lists in
+            // ascending element order: fill_slot's sums); T rhs; raw diagonal
+            double2 dgv = d2(0.0, 0.0);
+            double rt = 0.0;
+            if (act) {
+                for (int sec = 0; sec < 2; ++sec) {
+                    const int k0 = sec ? r0.k1 : r0.k0, wd = sec ? r0.w1 : r0.w0;
+                    for (int l = 0; l < wd; ++l) {
+                        const int k = k0 + 32 * l;
+                        const int s = __ldg(P.esrc + c.ell_base + k);
+                        double av = 0.0, at = 0.0;
+                        if (s >= 0) {
+                            const int q0 = __ldg(m.slot_ptr + s), q1 = __ldg(m.slot_ptr + s + 1);
+                            for (int q = q0; q < q1; q += 4) {
+                                double2 cv[4];
+#pragma unroll
+                                for (int j = 0; j < 4; ++j)
+                                    if (q + j < q1) cv[j] = c_contrib(m, (unsigned)__ldg(m.slot_src + q + j), S.esig, rk, rrc);
+#pragma unroll
+                                for (int j = 0; j < 4; ++j)
+                                    if (q + j < q1) {
+                                        av = add(av, cv[j].x);
+                                        at = add(at, cv[j].y);
+                                    }
+                            }
+                            if (s == s_diag) dgv = d2(av, at);
+                        }
+                        sts2(E.ev_s + 16u * k, d2(av, at));
+                    }
+                }
+                const int p0 = __ldg(m.inc_ptr + g), p1 = __ldg(m.inc_ptr + g + 1);
+                for (int q = p0; q < p1; q += 8) {
+                    double lv[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (q + j < p1) {
+                            const unsigned ea = __ldg(m.inc_ea + q + j);
+                            lv[j] = __ldcg(S.eload + 4LL * (ea & 0x3fffffffu) + (ea >> 30));
+                        }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (q + j < p1) rt = add(rt, lv[j]);
+                }
+            }
+            // equilibration sums (fem.py:390-396) and PhysicsRange, one all-reduce
+            double co[4];
+            c_xbegin(E, xpart);
+            c_publish<true>(E, dgv.x, dgv.y, badv > 0.0 ? 1.0 : 0.0, badv);
+            c_xwait(E);
+            c_gather<true>(E, co);
+            if (co[2] > 0.0) {  // PhysicsRangeError aborts the run (fem.py:274)
+                bad = M - (long long)co[3];
+                status = RAFEM_ERR_PHYSICS;
+                abort_run = true;
+                break;
+            }
+            double scale = 1.0;
+            if (co[0] > 0.0 && co[1] > 0.0) scale = ldexp(1.0, (int)rint(log2(co[1] / co[0])));
+            // ---- scale + Dirichlet elimination + Jacobi inverse, in place
+            // (constrain_node_thread's arithmetic; moved-column sums in storage
+            // order: the two ELL sections merged by CSR slot)
+            double zf = 0.0;
+            if (act) {
+                double mV = 0.0, mT = 0.0, dV = 0.0, dT = 0.0;
+                int lo = 0, lg = 0;
+                const double app = p.applied_voltage, bt = p.boundary_temp;
+                for (int n = 0; n < s_end - s_beg; ++n) {
+                    const int so = lo < r0.w0 ? __ldg(P.esrc + c.ell_base + r0.k0 + 32 * lo) : 0x7fffffff;
+                    const int sg2 = lg < r0.w1 ? __ldg(P.esrc + c.ell_base + r0.k1 + 32 * lg) : 0x7fffffff;
+                    const bool own = (unsigned)so < (unsigned)sg2;
+                    const int k = own ? r0.k0 + 32 * lo : r0.k1 + 32 * lg;
+                    const int s = own ? so : sg2;
+                    if (own) ++lo; else ++lg;
+                    const uint8_t ck = lkind[lds_u16(E.ec_s + 2u * k)];
+                    const int cV = ck & 3, cT = ck >> 2;
+                    const double2 v = lds2(E.ev_s + 16u * k);
+                    const double vs = mul(v.x, scale);
+                    if (!kV && cV) mV = add(mV, mul(vs, dof_value(cV, app, bt)));
+                    if (!kT && cT) mT = add(mT, mul(v.y, dof_value(cT, app, bt)));
+                    double outV = vs, outT = v.y;
+                    const bool diag = s == s_diag;
+                    if (kV || cV) outV = (kV && diag) ? 1.0 : 0.0;
+                    if (kT || cT) outT = (kT && diag) ? 1.0 : 0.0;
+                    sts2(E.ev_s + 16u * k, d2(outV, outT));
+                    if (diag) {
+                        dV = outV;
+                        dT = outT;
+                    }
+                }
+                const double2 b = d2(kV ? dof_value(kV, app, bt) : sub(0.0, mV), kT ? dof_value(kT, app, bt) : sub(rt, mT));
+                reinterpret_cast<double2*>(S.rhs)[g] = b;
+                if (PRE) {
+                    if (s_diag < 0) dV = dT = 0.0;
+                    if (dV == 0.0 || dT == 0.0) zf = 1.0;
+                    sts2(E.rmv_s + 16u * r0.t, d2(1.0 / dV, 1.0 / dT));
+                } else {
+                    sts2(E.rmv_s + 16u * r0.t, d2(1.0, 1.0));
+                }
+            }
+            __syncthreads();  // values, rhs and M^-1 of the CTA complete (rhs: own rows only, read by own rows)
+            if (PRE && S.blk) {
+                E.blk = 1;
+                c_block_setup<1>(E, rc, &red[0][0]);
+            }
+            const long long tb = global_ns_c();
+            // ---- solve from the pass's start (the predictor with V extrapolated on a step's first pass)
+            CRow R[1];
+            const bool x0_new = S.vx0 && it == 1;
+            R[0].x = act ? (x0_new ? X(inew)[g] : xit[g]) : d2(0.0, 0.0);
+            double delta = -1.0;
+            const CpcgOut o = cpcg_core<PRE, 1>(E, rc, R, reinterpret_cast<const double2*>(S.rhs), -1.0, zf, xit,
+                                                &delta, X(inew));
+            const long long tc = global_ns_c();
+            asm_ns += tb - ta;
+            sol_ns += tc - tb;
+            if (o.status == RAFEM_ERR_INVALID) {  // ValueError: zero diagonal under Jacobi (solver.py:416-417)
+                status = RAFEM_ERR_INVALID;
+                abort_run = true;
+                break;
+            }
+            if (o.status == RAFEM_ERR_BREAKDOWN) break;  // SolverError -> step failure (fem.py:511-515)
+            inner += o.total;
+            if (!o.converged) break;  // fem.py:517-524
+            if (!(delta >= 0.0)) {  // b == 0 (x = 0): the delta from the fields
+                double dm = 0.0;
+                if (act) {
+                    const double2 xo = xit[g], xn = d2(0.0, 0.0);
+                    const double d0 = fabs(sub(xn.x, xo.x)) / fmax(1.0, fabs(xo.x));
+                    const double d1 = fabs(sub(xn.y, xo.y)) / fmax(1.0, fabs(xo.y));
+                    dm = (d0 > dm || d0 != d0) ? d0 : dm;
+                    dm = (d1 > dm || d1 != d1) ? d1 : dm;
+                }
+                c_xbegin(E, xpart);
+                c_publish<true>(E, 0.0, 0.0, 0.0, dm);
+                c_xwait(E);
+                c_gather<true>(E, co);
+                delta = co[3];
+            }
+            const int tmp = iit;
+            iit = inew;
+            inew = tmp;
+            if (delta < p.corrector_tol) {
+                conv = true;
+                break;
+            }
+        }
+        if (abort_run) break;
+        corr += iters;
+        if (conv) {  // accept (fem.py:603-628)
+            const int old_prev = iprev;
+            iprev = iacc;
+            iacc = iit;
+            iit = old_prev;
+            dt_prev = dt;
+            t = final_step ? p.total_time : t + dt;
+            if (S.ring) {
+                double* slot = S.ring + (step % S.ring_slots) * (n2 + 4);
+                if (act) reinterpret_cast<double2*>(slot + 4)[g] = X(iacc)[g];
+                if (rank == 0 && threadIdx.x == 0) {
+                    slot[0] = t;
+                    slot[1] = dt;
+                    slot[2] = (double)iters;
+                    slot[3] = 0.0;
+                }
+            }
+            if (step < S.rec_cap) {
+                if (S.rec_x && act) reinterpret_cast<double2*>(S.rec_x + step * n2)[g] = X(iacc)[g];
+                if (rank == 0 && threadIdx.x == 0) {
+                    S.rec_time[step] = t;
+                    S.rec_dt[step] = dt;
+                    S.rec_iters[step] = iters;
+                }
+            }
+            ++step;
+            if (iters <= 5)
+                dt_state = fmin(dt * 1.5, p.dt_max);
+            else if (iters >= 20)
+                dt_state = fmax(dt * 0.75, p.dt_min);
+            else
+                dt_state = dt;
+        } else {
+            if (dt <= p.dt_min) {  // StepFailureError (fem.py:629-631)
+                status = RAFEM_ERR_STEP_FAILURE;
+                failed_step = (int)step;
+                failed_dt = dt;
+                break;
+            }
+            dt_state = fmax(dt * 0.5, p.dt_min);
+            ++halv;
+        }
+    }
+    if (act) reinterpret_cast<double2*>(S.final_x)[g] = X(iacc)[g];
+    __syncthreads();
+    cl_sync();  // the last record is complete everywhere; no CTA leaves before its peers
+    if (rank == 0 && threadIdx.x == 0) {
+        if (S.ring) {
+            __threadfence_system();
+            *S.prog = step;
+        }
+        SimDevOut* o = S.out;
+        o->accepted = step;
+        o->corr = corr;
+        o->inner = inner;
+        o->halvings = halv;
+        o->passes = passes;
+        o->t = t;
+        o->status = status;
+        o->failed_step = failed_step;
+        o->failed_dt = failed_dt;
+        o->bad = bad;
+        o->asm_ns = asm_ns;
+        o->solve_ns = sol_ns;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host: plans
 
 struct ClusterPlan {
@@ -1097,7 +1467,7 @@ static ClusterPlan* cluster_plan(rafem_ctx* ctx, const int* rp_dev, const int* c
     const int rows_cap = kRPT * nt;
     P->smem = c_layout_bytes(ell_cap, nloc_cap, rows_cap, ndw, 0);
     P->smem_blk = c_layout_bytes(ell_cap, nloc_cap, rows_cap, ndw, 1);
-    P->smem_sim = P->smem_blk + al16((size_t)nloc_cap) + al16((size_t)rows_cap * 24);
+    P->smem_sim = P->smem_blk + al16((size_t)nloc_cap);  // + local node kinds
     if (P->smem > 225 * 1024) return nullptr;
     // upload
     const size_t o_cta = 0, o_w = al16(sizeof(CCta) * C), o_ec = o_w + al16(sizeof(int4) * warps.size());
@@ -1237,6 +1607,89 @@ int cluster_pcg_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, dou
     ctx->last_ctas = C;
     ctx->last_team = 1;
     ctx->last_precond = blk ? RAFEM_PRECOND_BLOCK_JACOBI : (pre ? RAFEM_PRECOND_JACOBI : RAFEM_PRECOND_NONE);
+    return RAFEM_OK;
+}
+
+}  // namespace rafem
+
+namespace rafem {
+
+// The whole simulation on one cluster when the mesh fits; opt-in
+// (RAFEM_SIM_CLUSTER=1).  Measured on the mesh-B analog (scripts/csim_probe.py,
+// profiles/r2b_csim_probe.txt): same trajectory and fields within 2e-7 of
+// the 148-CTA fused kernel, block-Jacobi iterations 4,172 vs 4,655, but the
+// per-pass assembly on 16 SMs is L2-latency bound (220 us vs 14 us: each
+// row's contributor walk is a chain of dependent L2 loads) and the PCG
+// loop spills next to the time-loop state, so the fused grid kernel stays
+// the default.  RAFEM_ERR_UNSUPPORTED lets simulate_fused take over.
+int simulate_cluster(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, double* rec_x_dev,
+                     double* rec_time_dev, double* rec_dt_dev, int* rec_iters_dev, long long rec_cap,
+                     double* final_x_dev, float* ms, const SimStream* stream) {
+    const char* env = getenv("RAFEM_SIM_CLUSTER");
+    if (!(env && env[0] == '1')) return RAFEM_ERR_UNSUPPORTED;
+    rafem_mesh* mesh = s->mesh;
+    rafem_ctx* ctx = mesh->ctx;
+    const int N = mesh->N;
+    if (N == 0 || mesh->M == 0 || p->solver.method != RAFEM_METHOD_PCG || mesh->nreg > kCRegions)
+        return RAFEM_ERR_UNSUPPORTED;
+    if (!mesh->slot_lists_tried)
+        if (int rc = mesh_slot_lists(mesh)) return rc;
+    if (!mesh->slot_ptr) return RAFEM_ERR_UNSUPPORTED;
+    const int C = cluster_size_for(N);
+    int rc = RAFEM_OK;
+    ClusterPlan* P = cluster_plan(ctx, mesh->rp, mesh->col, mesh->nodes, N, mesh->slots, mesh->id, C, rc);
+    if (rc) return rc;
+    if (!P) return RAFEM_ERR_UNSUPPORTED;
+    const bool pre = p->solver.precondition != RAFEM_PRECOND_NONE;
+    const int blk = p->solver.precondition == RAFEM_PRECOND_BLOCK_JACOBI ? 1 : 0;
+    const size_t smem = P->smem_sim;
+    if (smem > 223 * 1024) return RAFEM_ERR_UNSUPPORTED;
+    const void* fn = pre ? (const void*)csim_kernel<true> : (const void*)csim_kernel<false>;
+    if (!cluster_launchable(ctx, fn, C, P->nt, smem)) return RAFEM_ERR_UNSUPPORTED;
+    if (int r = system_escal(s)) return r;
+    if (int r = ensure(ctx, ctx->ws_simout, sizeof(SimDevOut))) return r;
+    CSimArgs S{};
+    S.P = P->view;
+    S.m = asm_mesh(mesh);
+    S.xs = s->xs;
+    S.final_x = final_x_dev;
+    S.esig = s->esig;
+    S.eload = s->eload;
+    S.rhs = s->rhs;
+    S.n2 = 2LL * N;
+    S.p = *p;
+    S.rec_x = rec_x_dev;
+    S.rec_time = rec_time_dev;
+    S.rec_dt = rec_dt_dev;
+    S.rec_iters = rec_iters_dev;
+    S.rec_cap = rec_cap;
+    S.out = static_cast<SimDevOut*>(ctx->ws_simout.p);
+    S.blk = blk;
+    {
+        const char* nv = getenv("RAFEM_NO_VX0");
+        S.vx0 = !(nv && nv[0] == '1');
+    }
+    if (stream) {
+        S.ring = stream->ring;
+        S.ring_slots = stream->slots;
+        S.prog = stream->prog;
+        S.cons = stream->cons;
+    }
+    void* args[] = {&S};
+    RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+    RF_CUDA_TRY(ctx, cluster_launch(ctx, fn, C, P->nt, smem, args));
+    RF_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+    ctx->launches++;
+    ctx->last_mode = 6;
+    ctx->last_ctas = C;
+    ctx->last_team = 1;
+    ctx->last_precond = blk ? RAFEM_PRECOND_BLOCK_JACOBI : (pre ? RAFEM_PRECOND_JACOBI : RAFEM_PRECOND_NONE);
+    if (stream && stream->pump) {  // consume records while the kernel runs
+        if (int r = stream->pump(stream->user)) return r;
+    }
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(out, ctx->ws_simout.p, sizeof(SimDevOut), cudaMemcpyDeviceToHost, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ms) cudaEventElapsedTime(ms, ctx->ev0, ctx->ev1);
     return RAFEM_OK;
 }
 

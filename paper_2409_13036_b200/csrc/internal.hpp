@@ -223,6 +223,12 @@ int cluster_pcg_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, dou
                       const rafem_solver_params& p, KResult* res_dev, int* flag_dev, cudaEvent_t ev_start,
                       cudaEvent_t ev_stop);
 void cluster_plans_release(rafem_ctx* ctx);
+// cluster.cu: the whole simulation on one thread-block cluster (same contract
+// as simulate_fused); RAFEM_ERR_UNSUPPORTED when not eligible
+struct SimStream;
+int simulate_cluster(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, double* rec_x_dev,
+                     double* rec_time_dev, double* rec_dt_dev, int* rec_iters_dev, long long rec_cap,
+                     double* final_x_dev, float* ms, const SimStream* stream);
 int krylov_read_history(rafem_ctx* ctx, const KResult& r, double* hist, long long hist_cap,
                         long long* cyc, long long cyc_cap);
 int spmv_launch(rafem_ctx* ctx, const MatView& A, const double* x_dev, double* y_dev);

@@ -2717,6 +2717,11 @@ namespace rafem {
 int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, double* rec_x_dev,
                    double* rec_time_dev, double* rec_dt_dev, int* rec_iters_dev, long long rec_cap,
                    double* final_x_dev, float* ms, const SimStream* stream) {
+    {  // paper-scale meshes: the cluster-resident simulation (cluster.cu)
+        const int crc = simulate_cluster(s, p, out, rec_x_dev, rec_time_dev, rec_dt_dev, rec_iters_dev, rec_cap,
+                                         final_x_dev, ms, stream);
+        if (crc != RAFEM_ERR_UNSUPPORTED) return crc;
+    }
     rafem_mesh* mesh = s->mesh;
     rafem_ctx* ctx = mesh->ctx;
     const int N = mesh->N;

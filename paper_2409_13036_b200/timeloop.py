@@ -286,8 +286,8 @@ class DeviceRun:
     def _note_mode(self):
         mode, ctas = C.c_int32(), C.c_int32()
         nat.lib().rafem_last_solve_mode(nat.context(), C.byref(mode), C.byref(ctas))
-        self.last_mode = {4: "kernel-per-phase-pcg", 3: "grid-streaming-pcg", 2: "fused-simulation", 1: "cluster",
-                          0: "grid"}.get(mode.value, "none")
+        self.last_mode = {6: "cluster-simulation", 5: "cluster-pcg", 4: "kernel-per-phase-pcg",
+                          3: "grid-streaming-pcg", 2: "fused-simulation", 1: "cluster", 0: "grid"}.get(mode.value, "none")
         self.last_ctas = ctas.value
         self.last_precond = nat.last_solve_precond()
 
