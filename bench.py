@@ -441,6 +441,11 @@ def run_ours(args):
             line["spmv_c3"] = {"error": str(exc)[:300]}
     if rank == 0 and not args.no_c3:
         try:
+            line["paper_solve"] = paper_solve_leg()
+        except Exception as exc:  # noqa: BLE001
+            line["paper_solve"] = {"error": str(exc)[:300]}
+    if rank == 0 and not args.no_c3:
+        try:
             line["small_c1"] = c1_leg(args)
         except Exception as exc:  # noqa: BLE001
             line["small_c1"] = {"error": str(exc)[:300]}
@@ -604,6 +609,43 @@ def e2e_plugin_leg(mesh, mat, args, run_simulation, SimConfig, SolverConfig, wor
     d2h = passes * 8 * (4 * N) + passes * 16
     return {"value": world * summ.accepted_steps * reps / wall, "unit": "steps/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "reps": reps, "reference_driven": ref_ok, "path": path}
+
+
+def paper_solve_leg():
+    """Standalone paper-scale solve (the plug-in seam's solve() path): the
+    mesh-B analog's system at a hot iterate (seeded fields), PCG to 1e-10
+    from the iterate, on the cluster-resident engine (one 16-CTA cluster,
+    DSMEM halos, cluster.cu; the default for paper-scale PCG) and on the
+    148-CTA grid engine (RAFEM_CLUSTER=0), best of 5 device-timed solves."""
+    import numpy as np
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, assemble_global, generate_box_mesh, solve
+    from paper_2409_13036_b200 import _native as nat
+    mesh = generate_box_mesh(*MESH_B)
+    n = mesh.node_count
+    rng = np.random.default_rng(2409)
+    t = 37 + rng.uniform(0, 30, n)
+    v = rng.uniform(0, 25, n)
+    s = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, v, t, 0.5)
+    x0 = np.empty(2 * n)
+    x0[0::2], x0[1::2] = v, t
+    out = {"workload": "generate_box_mesh(20,20,21) system at a seeded hot iterate, x0 = iterate, tol 1e-10"}
+    for prec in ("jacobi", "block_jacobi"):
+        for eng in ("cluster", "grid"):
+            if eng == "grid":
+                os.environ["RAFEM_CLUSTER"] = "0"
+            try:
+                best, st = 1e9, None
+                for _ in range(5):
+                    x, st = solve(s.matrix, s.rhs, x0=x0, config=SolverConfig(backend="pcg", precondition=prec))
+                    best = min(best, st.device_ms * 1e3)
+                mode = nat.last_solve_mode()
+            finally:
+                os.environ.pop("RAFEM_CLUSTER", None)
+            out[f"{eng}_{prec}"] = {"iterations": st.iterations, "solve_us": best,
+                                    "us_per_iteration": best / max(st.iterations, 1),
+                                    "engine": {5: "cluster-resident PCG (16 CTAs)", 0: "grid PCG (148 CTAs)"}.get(
+                                        mode[0], str(mode)), "ctas": mode[1]}
+    return out
 
 
 def c1_leg(args):

@@ -1,7 +1,9 @@
 #!/bin/bash
-# Round-2: new shard-loop + at-scale parity tests, bench with the C4 / C5 legs.
+# Round-2 checkpoint: smoke, every GPU test, bench (our arm), launch list.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
-free -g > gpurun_out/host_mem.txt
-timeout 1500 python -m pytest tests/test_gpu_shard.py tests/test_gpu_scale.py -q -x --timeout 1400 -rs -s > gpurun_out/pytest_r2b.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_r2b.log
-timeout 900 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench_r2b.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_r2b.log
+nvidia-smi > gpurun_out/nvidia-smi.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 2400 python -m pytest tests -q -m gpu --timeout 1800 -rs ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 1200 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+echo done > gpurun_out/round_done.txt
