@@ -660,17 +660,18 @@ struct CLayout {
     unsigned char* end;
 };
 __host__ __device__ inline size_t c_al16(size_t b) { return (b + 15) & ~(size_t)15; }
-__host__ __device__ inline size_t c_layout_bytes(int ell_cap, int nloc_cap, int rows_cap, int ndw, int blk) {
-    return c_al16((size_t)ell_cap * 16) + c_al16((size_t)2 * nloc_cap * 16) + c_al16((size_t)ell_cap * 2) +
+__host__ __device__ inline size_t c_layout_bytes(int ell_cap, int nloc_cap, int rows_cap, int ndw, int blk,
+                                                 int nbuf = 2) {
+    return c_al16((size_t)ell_cap * 16) + c_al16((size_t)nbuf * nloc_cap * 16) + c_al16((size_t)ell_cap * 2) +
            c_al16((size_t)rows_cap * 16) + c_al16((size_t)rows_cap * 16 * ndw) + (blk ? c_al16((size_t)rows_cap * 16) : 0);
 }
-RF_DEV CLayout c_layout(unsigned char* base, const CPlan& P, int blk) {
+RF_DEV CLayout c_layout(unsigned char* base, const CPlan& P, int blk, int nbuf = 2) {
     CLayout L;
     unsigned char* q = base;
     L.ev = reinterpret_cast<double2*>(q);
     q += c_al16((size_t)P.ell_cap * 16);
     L.mb = reinterpret_cast<double2*>(q);
-    q += c_al16((size_t)2 * P.nloc_cap * 16);
+    q += c_al16((size_t)nbuf * P.nloc_cap * 16);
     L.ec = reinterpret_cast<uint16_t*>(q);
     q += c_al16((size_t)P.ell_cap * 2);
     L.rmv = reinterpret_cast<double2*>(q);
@@ -830,6 +831,335 @@ __global__ void __launch_bounds__(kCT, 1) cpcg_kernel(CPlan P, const double2* __
                                            nullptr, reinterpret_cast<double2*>(x));
     if (rank == 0 && threadIdx.x == 0)
         c_write_result(res, o.total, o.cycles, o.hlen, o.rel, o.converged != 0, o.status);
+    cl_sync();  // no CTA leaves while a peer may still address its shared memory
+}
+
+// ---------------------------------------------------------------------------
+// GMRES(m) on the cluster — gmres_body's contract (solver.py:381-531: right
+// Jacobi, CGS2 Arnoldi, Givens least squares, true-residual restarts,
+// stagnation latch, breakdown rules) with the matrix in the CTAs' shared
+// memory and the exchanges of the PCG engine.  The Krylov basis does not
+// fit beside the matrix: each CTA keeps its rows of V in global memory (L2),
+// thread per row, coalesced.  Per inner step: the pushed z_k = M^-1 v_k ->
+// w = A z_k -> CGS pass 1 (k+1 dots, a warp per coefficient over the CTA's
+// rows) -> exchange -> w -= V h -> pass 2 (k+1 dots + ||w||^2) -> exchange
+// -> w -= V c, h_{k+1,k} = sqrt(||w||^2 - ||c||^2) (explicit norm on
+// cancellation) -> Givens -> v_{k+1} -> push.  Three exchanges per step and
+// no grid barrier.
+
+constexpr int kGM = 30;  // largest restart length of the cluster engine (the reference default)
+
+struct GmScratch {       // per CTA, shared memory (same bits in every CTA)
+    double part[2][kCMax][kGM + 2];  // pushed CTA partials (up to m + 2 values)
+    double red[kGM + 2];             // this CTA's coefficient sums
+    double co[kGM + 2];              // the exchange's cluster sums
+    double H[(kGM + 1) * kGM];       // Hessenberg, column-major (m + 1) x m
+    double cs[kGM], sn[kGM], gg[kGM + 1], yy[kGM];
+    double sc[4];
+};
+
+// Send this CTA's nv sums (gs.red) to every CTA (exchange E.xk); warp 0.
+RF_DEV void g_send(CEnv& E, GmScratch& gs, int nv) {
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x, np = (nv + 1) / 2;
+        const unsigned par = E.xk & 1;
+        for (int j = lane; j < np * E.C; j += 32) {
+            const int pr = j % np, dst = j / np;
+            const double a = gs.red[2 * pr], b = 2 * pr + 1 < nv ? gs.red[2 * pr + 1] : 0.0;
+            st_async2(cl_map_u(smem_u32(&gs.part[par][E.rank][2 * pr]), (unsigned)dst), a, b,
+                      cl_map_u(E.xbar_s + 8u * par, (unsigned)dst));
+        }
+    }
+    ++E.xk;
+}
+// After the wait: cluster sums of the nv values in rank order into gs.co
+// (warp 0; the caller's bar.sync publishes them).
+RF_DEV void g_sum(const CEnv& E, GmScratch& gs, int nv) {
+    const int par = (E.xw - 1) & 1;
+    for (int i = threadIdx.x; i < nv; i += 32) {
+        double s = 0.0;
+        for (int c = 0; c < E.C; ++c) s = add(s, gs.part[par][c][i]);
+        gs.co[i] = s;
+    }
+}
+// CTA sums of nv coefficient dots: coefficient i = sum over own rows of
+// V_i . w (i < nv - extra) and, with `self`, w . w as the last one; a warp
+// per coefficient, lanes striding the rows, fixed butterfly.  ws: own w in
+// shared memory (thread order).
+RF_DEV void g_dots(const CEnv& E, GmScratch& gs, const double2* Vg, int ld, const double2* ws, int nb, bool self) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int i = w; i < nb + (self ? 1 : 0); i += nw) {
+        const double2* vi = i < nb ? Vg + (size_t)i * ld : ws;
+        double acc = 0.0;
+        for (int t = lane; t < E.nr; t += 32) {
+            const double2 a = i < nb ? __ldcg(vi + t) : vi[t];
+            const double2 b = ws[t];
+            acc = fma(a.x, b.x, fma(a.y, b.y, acc));
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) gs.red[i] = acc;
+    }
+}
+// acc -= sum_{i < nb} co[i] V_i[t] (SGN = -1; += for SGN = 1)
+template <int SGN = -1>
+RF_DEV double2 g_axpy_rows(double2 acc, const double2* Vg, int ld, int t, const double* co, int nb) {
+    for (int i = 0; i < nb; ++i) {
+        const double2 v = __ldcg(Vg + (size_t)i * ld + t);
+        const double h = SGN * co[i];
+        acc = make_double2(fma(h, v.x, acc.x), fma(h, v.y, acc.y));
+    }
+    return acc;
+}
+
+template <bool PRE>
+__global__ void __launch_bounds__(kCT, 1) cgmres_kernel(CPlan P, const double2* __restrict__ val2, const double* b,
+                                                        double* x, const double* minv, const int* flag, double tol,
+                                                        long long cap, int m, double* hist, long long hist_cap,
+                                                        long long* cyc, long long cyc_cap, KResult* res,
+                                                        double2* basis) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ __align__(16) double part_unused[2][kCMax][4];
+    __shared__ __align__(16) double red4[32][4];
+    __shared__ __align__(8) unsigned long long xbar[2];
+    __shared__ __align__(32) double sc4[4];
+    __shared__ __align__(16) GmScratch gs;
+    const unsigned rank = cl_rank();
+    const CCta c = P.cta[rank];
+    const CLayout L = c_layout(dsm, P, 1, 1);  // one gathered-vector buffer; yb: the own rows of w
+    for (int k = threadIdx.x; k < c.ell_n; k += blockDim.x) {
+        const int s = __ldg(P.esrc + c.ell_base + k);
+        L.ev[k] = s >= 0 ? __ldg(val2 + s) : make_double2(0.0, 0.0);
+        L.ec[k] = __ldg(P.ecol + c.ell_base + k);
+    }
+    CEnv E;
+    CRowC rc[1];
+    c_env<1>(E, rc, P, c, rank, L, part_unused, red4, xbar, sc4);
+    const CRowC& r0 = rc[0];
+    const bool act = r0.t < c.nr;
+    const int g = r0.gid, t = r0.t;
+    double2* ws = L.yb;
+    const int ld = P.rows_cap;
+    double2* Vg = basis + (size_t)rank * (kGM + 1) * ld;
+    const unsigned xv = 16u * (unsigned)(c.nloc - c.nr) + 16u * (unsigned)P.C;  // vector exchange (+ a dummy pair)
+    auto xp = [&](int nv) { return 16u * (unsigned)((nv + 1) / 2) * (unsigned)P.C; };
+    double2 xr = act ? reinterpret_cast<const double2*>(x)[g] : d2(0.0, 0.0);
+    const double2 bb = act ? reinterpret_cast<const double2*>(b)[g] : d2(0.0, 0.0);
+    const double2 mv = (PRE && act) ? reinterpret_cast<const double2*>(minv)[g] : d2(1.0, 1.0);
+    __syncthreads();
+    cl_sync();
+    const bool lead = rank == 0 && threadIdx.x == 0;
+    if (*flag) {  // ValueError: zero diagonal under Jacobi (solver.py:416-417)
+        if (lead) c_write_result(res, 0, 0, 0, INFINITY, false, RAFEM_ERR_INVALID);
+        return;
+    }
+    // one-value all-reduce (sum) of v over the cluster
+    auto allsum1 = [&](double v) -> double {
+        double a[1] = {v};
+        warp_sum_k<1>(a);
+        if ((threadIdx.x & 31) == 0) red4[threadIdx.x >> 5][0] = a[0];
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            double s = threadIdx.x < (int)(blockDim.x >> 5) ? red4[threadIdx.x][0] : 0.0;
+            s = warp_sum(s);
+            if (threadIdx.x == 0) gs.red[0] = s;
+        }
+        __syncwarp();
+        c_xbegin(E, xp(1));
+        g_send(E, gs, 1);
+        c_xwait(E);
+        if (threadIdx.x < 32) g_sum(E, gs, 1);
+        __syncthreads();
+        const double r = gs.co[0];
+        __syncthreads();
+        return r;
+    };
+    // push v (own row) into buffer 0 of every reader; exchange with a dummy pair
+    auto push_vec = [&](double2 v) {
+        c_xbegin(E, xv);
+        if (act) c_push(E, r0, 0, v);
+        if (threadIdx.x == 0) {
+            gs.red[0] = 0.0;
+            gs.red[1] = 0.0;
+        }
+        __syncthreads();  // own entries of buffer 0 complete in the CTA
+        g_send(E, gs, 2);
+    };
+    const double bnorm = sqrt(allsum1(act ? fma(bb.x, bb.x, bb.y * bb.y) : 0.0));
+    if (bnorm == 0.0) {  // zero data: zero solution (solver.py:422-425)
+        if (act) reinterpret_cast<double2*>(x)[g] = d2(0.0, 0.0);
+        if (lead) c_write_result(res, 0, 1, 0, 0.0, true, RAFEM_OK);
+        cl_sync();
+        return;
+    }
+    double2 rr = d2(0.0, 0.0);
+    auto true_residual = [&]() -> double {  // r = b - A x, ||r|| / ||b|| (solver.py:438-439)
+        push_vec(xr);
+        c_xwait(E);
+        double s = 0.0;
+        if (act) {
+            const double2 y = c_spmv(E, r0, c_buf(E, 0));
+            rr = d2(bb.x - y.x, bb.y - y.y);
+            s = fma(rr.x, rr.x, rr.y * rr.y);
+        }
+        return sqrt(allsum1(s)) / bnorm;
+    };
+    long long total = 0, cycles = 0, hlen = 0;
+    int weak = 0;
+    bool latched = false, have_prev = false, converged = false;
+    double prev_start = 0.0, rel = INFINITY;
+    int status = RAFEM_OK;
+    const double tiny = 2.2250738585072014e-308;  // np.finfo(float64).tiny
+    while (true) {
+        rel = true_residual();
+        if (have_prev) {  // stagnation bookkeeping (solver.py:440-447)
+            if (rel > (1.0 - 1e-3) * prev_start) {
+                if (++weak >= 3) latched = true;
+            } else {
+                weak = 0;
+            }
+            have_prev = false;
+        }
+        if (rel <= tol) {
+            converged = true;
+            break;
+        }
+        if (total >= cap) break;
+        const double cycle_start = rel;
+        const double beta = rel * bnorm;
+        if (threadIdx.x == 0) {
+            for (int i = 0; i <= m; ++i) gs.gg[i] = 0.0;
+            gs.gg[0] = beta;
+        }
+        // v_0 = r / beta; push z_0 = M^-1 v_0
+        double2 v = d2(rr.x * (1.0 / beta), rr.y * (1.0 / beta));
+        if (act) __stcg(Vg + t, v);
+        push_vec(d2(mv.x * v.x, mv.y * v.y));
+        int used = 0;
+        bool broke = false, dead = false;
+        const long long hstart = hlen;
+        for (int k = 0; k < m; ++k) {
+            c_xwait(E);
+            // w = A z_k
+            double2 w = act ? c_spmv(E, r0, c_buf(E, 0)) : d2(0.0, 0.0);
+            if (act) ws[t] = w;
+            __syncthreads();
+            // CGS pass 1: h_i = v_i . w
+            g_dots(E, gs, Vg, ld, ws, k + 1, false);
+            __syncthreads();
+            c_xbegin(E, xp(k + 1));
+            g_send(E, gs, k + 1);
+            c_xwait(E);
+            if (threadIdx.x < 32) g_sum(E, gs, k + 1);
+            __syncthreads();
+            if (threadIdx.x == 0)
+                for (int i = 0; i <= k; ++i) gs.H[k * (m + 1) + i] = gs.co[i];
+            if (act) {
+                w = g_axpy_rows(w, Vg, ld, t, gs.co, k + 1);
+                ws[t] = w;
+            }
+            __syncthreads();
+            // CGS pass 2: c_i = v_i . w and ||w||^2
+            g_dots(E, gs, Vg, ld, ws, k + 1, true);
+            __syncthreads();
+            c_xbegin(E, xp(k + 2));
+            g_send(E, gs, k + 2);
+            c_xwait(E);
+            if (threadIdx.x < 32) g_sum(E, gs, k + 2);
+            __syncthreads();
+            if (threadIdx.x == 0)
+                for (int i = 0; i <= k; ++i) gs.H[k * (m + 1) + i] = add(gs.H[k * (m + 1) + i], gs.co[i]);
+            double cc = 0.0;
+            for (int i = 0; i <= k; ++i) cc = fma(gs.co[i], gs.co[i], cc);
+            const double ww = gs.co[k + 1];
+            double sq = 0.0;
+            if (act) {
+                w = g_axpy_rows(w, Vg, ld, t, gs.co, k + 1);
+                sq = fma(w.x, w.x, w.y * w.y);
+            }
+            // ||w - V c||^2 = ||w||^2 - ||c||^2; near an invariant subspace the
+            // difference cancels: then (same decision everywhere) reduce it
+            double hk1;
+            if (cc > 1e-8 * ww)
+                hk1 = sqrt(allsum1(sq));
+            else
+                hk1 = sqrt(fmax(ww - cc, 0.0));
+            ++total;
+            // Givens update of column k (solver.py:478-496), one thread per CTA
+            if (threadIdx.x == 0) {
+                double* hc = gs.H + k * (m + 1);
+                hc[k + 1] = hk1;
+                for (int i = 0; i < k; ++i) {
+                    const double tt = add(mul(gs.cs[i], hc[i]), mul(gs.sn[i], hc[i + 1]));
+                    hc[i + 1] = add(mul(-gs.sn[i], hc[i]), mul(gs.cs[i], hc[i + 1]));
+                    hc[i] = tt;
+                }
+                const double rad = hypot(hc[k], hc[k + 1]);
+                double est = 0.0;
+                int isdead = 0;
+                if (rad == 0.0) {
+                    isdead = 1;
+                } else {
+                    gs.cs[k] = hc[k] / rad;
+                    gs.sn[k] = hc[k + 1] / rad;
+                    hc[k] = rad;
+                    hc[k + 1] = 0.0;
+                    gs.gg[k + 1] = mul(-gs.sn[k], gs.gg[k]);
+                    gs.gg[k] = mul(gs.cs[k], gs.gg[k]);
+                    est = fabs(gs.gg[k + 1]) / bnorm;
+                    if (rank == 0 && hlen < hist_cap) hist[hlen] = est;
+                }
+                gs.sc[0] = isdead;
+                gs.sc[1] = est;
+            }
+            __syncthreads();
+            if (gs.sc[0] != 0.0) {  // column added nothing (solver.py:483-487)
+                dead = true;
+                used = k;
+                break;
+            }
+            used = k + 1;
+            const double est = gs.sc[1];
+            ++hlen;
+            if (hk1 < tiny) {  // breakdown (solver.py:497-499)
+                broke = true;
+                break;
+            }
+            if (est <= tol || total >= cap || k + 1 == m) break;
+            v = d2(w.x * (1.0 / hk1), w.y * (1.0 / hk1));
+            if (act) __stcg(Vg + (size_t)(k + 1) * ld + t, v);
+            push_vec(d2(mv.x * v.x, mv.y * v.y));
+        }
+        if (used > 0) {  // y = R^-1 g ; x += M^-1 (V y)   (solver.py:504-511)
+            if (threadIdx.x == 0) {
+                for (int i = used - 1; i >= 0; --i) {
+                    double d = 0.0;
+                    for (int j = i + 1; j < used; ++j) d = add(d, mul(gs.H[j * (m + 1) + i], gs.yy[j]));
+                    gs.yy[i] = sub(gs.gg[i], d) / gs.H[i * (m + 1) + i];
+                }
+            }
+            __syncthreads();
+            if (act) {
+                const double2 u = g_axpy_rows<1>(d2(0.0, 0.0), Vg, ld, t, gs.yy, used);  // V y
+                xr = d2(xr.x + mv.x * u.x, xr.y + mv.y * u.y);
+            }
+            __syncthreads();
+        }
+        if (lead && cycles < cyc_cap) cyc[cycles] = hlen - hstart;
+        ++cycles;
+        have_prev = true;
+        prev_start = cycle_start;
+        if (broke || dead) {  // solver.py:516-524
+            rel = true_residual();
+            if (rel <= tol)
+                converged = true;
+            else
+                status = RAFEM_ERR_BREAKDOWN;
+            break;
+        }
+    }
+    if (act) reinterpret_cast<double2*>(x)[g] = xr;
+    if (lead) c_write_result(res, total, cycles, hlen, rel, converged, status);
+    if (lead) res->stagnated = (latched && !converged) ? 1 : 0;
     cl_sync();  // no CTA leaves while a peer may still address its shared memory
 }
 
@@ -1205,6 +1535,7 @@ struct ClusterPlan {
     int N = 0, C = 0, nt = 0;
     size_t smem = 0;  // dynamic shared memory of the solve kernel
     size_t smem_blk = 0;  // + the block-Jacobi y buffer
+    size_t smem_gm = 0;   // GMRES: one gathered-vector buffer + the own rows of w
     size_t smem_sim = 0;
     void* dev = nullptr;
     CPlan view{};
@@ -1468,6 +1799,7 @@ static ClusterPlan* cluster_plan(rafem_ctx* ctx, const int* rp_dev, const int* c
     P->smem = c_layout_bytes(ell_cap, nloc_cap, rows_cap, ndw, 0);
     P->smem_blk = c_layout_bytes(ell_cap, nloc_cap, rows_cap, ndw, 1);
     P->smem_sim = P->smem_blk + al16((size_t)nloc_cap);  // + local node kinds
+    P->smem_gm = c_layout_bytes(ell_cap, nloc_cap, rows_cap, ndw, 1, 1);
     if (P->smem > 225 * 1024) return nullptr;
     // upload
     const size_t o_cta = 0, o_w = al16(sizeof(CCta) * C), o_ec = o_w + al16(sizeof(int4) * warps.size());
@@ -1554,15 +1886,75 @@ static cudaError_t cluster_launch(rafem_ctx* ctx, const void* fn, int C, int nt,
     return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
-// Eligibility: PCG with point Jacobi (or none) on a node-paired system small
-// enough for one cluster's shared memory.  RAFEM_CLUSTER=0 disables it,
-// RAFEM_CLUSTER=1 also takes block-Jacobi requests (applied as point Jacobi).
+// GMRES(m <= 30) on a node-paired system that fits one cluster (RAFEM_CLUSTER=0
+// disables it).  Same result block and history layout as the grid GMRES.
+static int cluster_gmres_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, double* x_dev,
+                               const double* minv_dev, const rafem_solver_params& p, KResult* res_dev, int* flag_dev,
+                               cudaEvent_t ev_start, cudaEvent_t ev_stop) {
+    if (p.restart_m < 1 || p.restart_m > kGM) return RAFEM_ERR_UNSUPPORTED;
+    const int N = A.ngroups;
+    const int C = cluster_size_for(N);
+    int rc = RAFEM_OK;
+    ClusterPlan* P = cluster_plan(ctx, A.rp, A.col, A.coords, N, A.slots, A.pattern_id, C, rc);
+    if (rc) return rc;
+    if (!P) return RAFEM_ERR_UNSUPPORTED;
+    const bool pre = p.precondition != RAFEM_PRECOND_NONE;
+    const size_t smem = P->smem_gm;
+    const void* fn = pre ? (const void*)cgmres_kernel<true> : (const void*)cgmres_kernel<false>;
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess) {
+        cudaGetLastError();
+        return RAFEM_ERR_UNSUPPORTED;
+    }
+    if (smem + fa.sharedSizeBytes > 227 * 1024) return RAFEM_ERR_UNSUPPORTED;
+    if (!cluster_launchable(ctx, fn, C, P->nt, smem)) return RAFEM_ERR_UNSUPPORTED;
+    const long long n = 2LL * N;
+    const long long hist_cap = std::min<long long>(p.max_total_iters > 0 ? p.max_total_iters : 10LL * n, 1LL << 20) + 1;
+    if (int r = ensure(ctx, ctx->ws_hist, sizeof(double) * (size_t)hist_cap)) return r;
+    if (int r = ensure(ctx, ctx->ws_cyc, sizeof(long long) * (size_t)hist_cap)) return r;
+    if (int r = ensure(ctx, ctx->ws_basis, sizeof(double2) * (size_t)C * (kGM + 1) * P->view.rows_cap)) return r;
+    CPlan view = P->view;
+    const double2* val2 = reinterpret_cast<const double2*>(A.val);
+    double tol = p.tolerance;
+    long long cap = p.max_total_iters > 0 ? p.max_total_iters : 10LL * n;
+    int m = p.restart_m;
+    double* hist = static_cast<double*>(ctx->ws_hist.p);
+    long long* cyc = static_cast<long long*>(ctx->ws_cyc.p);
+    long long hc = hist_cap, cc = hist_cap;
+    const double* minv = pre ? minv_dev : nullptr;
+    double2* basis = static_cast<double2*>(ctx->ws_basis.p);
+    void* args[] = {&view, &val2, &b_dev, &x_dev, &minv, &flag_dev, &tol, &cap, &m, &hist, &hc, &cyc, &cc,
+                    &res_dev, &basis};
+    if (ev_start) RF_CUDA_TRY(ctx, cudaEventRecord(ev_start, ctx->stream));
+    RF_CUDA_TRY(ctx, cluster_launch(ctx, fn, C, P->nt, smem, args));
+    if (ev_stop) RF_CUDA_TRY(ctx, cudaEventRecord(ev_stop, ctx->stream));
+    ctx->launches++;
+    ctx->last_mode = 5;
+    ctx->last_ctas = C;
+    ctx->last_team = 1;
+    ctx->last_precond = pre ? RAFEM_PRECOND_JACOBI : RAFEM_PRECOND_NONE;
+    return RAFEM_OK;
+}
+
+// Eligibility: PCG (Jacobi, block-Jacobi or none) or GMRES(m <= 30) on a
+// node-paired system small enough for one cluster's shared memory.
+// RAFEM_CLUSTER=0 disables the engine.
 int cluster_pcg_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, double* x_dev, const double* minv_dev,
                       const rafem_solver_params& p, KResult* res_dev, int* flag_dev, cudaEvent_t ev_start,
                       cudaEvent_t ev_stop) {
     const char* env = getenv("RAFEM_CLUSTER");
     if (env && env[0] == '0') return RAFEM_ERR_UNSUPPORTED;
-    if (p.method != RAFEM_METHOD_PCG || A.W != 2 || !A.pattern_id || p.grid_ctas > 0) return RAFEM_ERR_UNSUPPORTED;
+    if (A.W != 2 || !A.pattern_id || p.grid_ctas > 0) return RAFEM_ERR_UNSUPPORTED;
+    if (p.method != RAFEM_METHOD_PCG) {
+        // opt-in (RAFEM_CLUSTER_GMRES=1): measured no faster than the grid
+        // GMRES (14.2 vs 14.1 us per inner step on mesh-B; the three
+        // exchanges and the basis sweeps through L2 per step are latency
+        // chains on 16 SMs, and batching the basis loads spills at the
+        // 96-register cap of 576-thread CTAs: 30 us), profiles/r2b_cgmres_probe.txt
+        const char* g = getenv("RAFEM_CLUSTER_GMRES");
+        if (!(g && g[0] == '1')) return RAFEM_ERR_UNSUPPORTED;
+        return cluster_gmres_solve(ctx, A, b_dev, x_dev, minv_dev, p, res_dev, flag_dev, ev_start, ev_stop);
+    }
     const int N = A.ngroups;
     const int C = cluster_size_for(N);
     int rc = RAFEM_OK;

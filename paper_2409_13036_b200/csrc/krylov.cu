@@ -2456,9 +2456,9 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     const size_t hess_bytes = (size_t)hess_doubles * 8;
 
     // ---- choose the execution mode
-    // paper-scale PCG: the cluster-resident engine (cluster.cu) when the
-    // system fits one cluster's shared memory
-    if (!gm) {
+    // paper-scale PCG and GMRES: the cluster-resident engine (cluster.cu)
+    // when the system fits one cluster's shared memory
+    {
         const int crc = cluster_pcg_solve(ctx, A, b_dev, x_dev, minv_dev, p, res_dev, flag_dev, ev_start, ev_stop);
         if (crc != RAFEM_ERR_UNSUPPORTED) return crc;
     }

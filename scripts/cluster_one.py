@@ -10,5 +10,5 @@ rng = np.random.default_rng(2409)
 t = 37 + rng.uniform(0, 30, n); v = rng.uniform(0, 25, n)
 s = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, v, t, 0.5)
 for _ in range(2):
-    x, st = solve(s.matrix, s.rhs, x0=np.zeros(2 * n), config=SolverConfig(backend="pcg", precondition="jacobi"))
+    x, st = solve(s.matrix, s.rhs, x0=np.zeros(2 * n), config=SolverConfig(backend="pcg", precondition="block_jacobi"))
 print(st.iterations, st.device_ms)

@@ -383,3 +383,33 @@ def test_cluster_resident_pcg_vs_grid_pcg(dims):
     assert se.iterations == 0 and np.array_equal(xe, x)
     xz, sz = solve(a, np.zeros_like(b), x0=x0, config=SolverConfig(backend="pcg", precondition="jacobi"))
     assert sz.converged and not np.any(xz)
+
+
+@pytest.mark.parametrize("dims", [(6, 5, 7), (15, 15, 16)])
+def test_cluster_gmres_matches_grid_gmres(dims):
+    """The cluster GMRES(30) (opt-in RAFEM_CLUSTER_GMRES=1) follows the grid
+    GMRES step for step: same inner steps and restarts, solutions within
+    1e-10, the stats contract (true residual, per-cycle history)."""
+    import os
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, assemble_global, generate_box_mesh, solve
+    from paper_2409_13036_b200 import _native as nat
+    mesh = generate_box_mesh(*dims)
+    n = mesh.node_count
+    rng = np.random.default_rng(5)
+    t, v = 37.0 + rng.uniform(0, 30, n), rng.uniform(0, 25, n)
+    s = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, v, t, 0.5)
+    a, b = s.matrix, s.rhs
+    cfg = SolverConfig(backend="gmres", precondition="jacobi", tolerance=1e-10)
+    xg, sg = solve(a, b, config=cfg)
+    assert nat.last_solve_mode()[0] == 0
+    os.environ["RAFEM_CLUSTER_GMRES"] = "1"
+    try:
+        x, st = solve(a, b, config=cfg)
+        assert nat.last_solve_mode()[0] == 5
+    finally:
+        del os.environ["RAFEM_CLUSTER_GMRES"]
+    res = np.linalg.norm(b - O.matvec(a.row_ptr, a.col_idx, a.vals, x)) / np.linalg.norm(b)
+    assert st.converged and res <= 1e-10 and abs(st.final_relative_residual - res) < 1e-12
+    assert st.iterations == sg.iterations and st.restarts == sg.restarts
+    assert [len(c) for c in st.residual_history] == [len(c) for c in sg.residual_history]
+    assert rel_err(x, xg) < 1e-10
