@@ -178,6 +178,15 @@ int rafem_mesh_create(rafem_ctx* ctx, int64_t n_nodes, const double* nodes, int6
                       const double* alpha, const double* t_ref, const uint8_t* dof_kind,
                       rafem_mesh** out);
 void rafem_mesh_destroy(rafem_mesh* mesh);
+/* Bit-exact assembly mode: replace the device-computed element geometry with
+ * the reference's own (_basis_gradients, fem.py:229-240: np.linalg.det /
+ * np.linalg.inv of the edge matrix — LAPACK LU, which a device kernel does
+ * not reproduce to the last bit).  grad: n_tets x 4 x 3 basis gradients,
+ * vol: n_tets volumes, computed once per mesh on the host; the packed
+ * vol * grad_a . grad_b table (fem.py:280-282) is rebuilt on the device in
+ * np.einsum's summation order.  Every later assembly of this mesh is then
+ * bit-identical to assemble_global (fem.py:325-430). */
+int rafem_mesh_set_geometry(rafem_mesh* mesh, const double* grad, const double* vol);
 /* node-pattern size (slots); the dof CSR has 2*slots entries */
 int64_t rafem_mesh_slots(const rafem_mesh* mesh);
 /* stencil classes of the node pattern (built on first call): rows whose

@@ -15,7 +15,7 @@ CPU fallback.
 """
 
 from .assembly import (AssembledSystem, MaterialParams, PhysicsRangeError, RegionMaterial,
-                       SimConfig, assemble_global)
+                       SimConfig, assemble_global, set_exact_geometry)
 from .boxmesh import TetMesh, generate_box_mesh
 from .csr import CooMatrix, CsrMatrix, DeviceCsrMatrix, coo_to_csr, spmv
 from .krylov import (GmresBreakdownError, KrylovBreakdownError, SolveStats, SolverConfig,

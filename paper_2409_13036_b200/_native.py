@@ -90,6 +90,7 @@ _SIGS = {
     "rafem_matrix_solve": (i32, [vp, vp, vp, P(SolverParams), vp, P(SolveStatsC), vp, i64, vp, i64]),
     "rafem_mesh_create": (i32, [vp, i64, vp, i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, P(vp)]),
     "rafem_mesh_destroy": (None, [vp]),
+    "rafem_mesh_set_geometry": (i32, [vp, vp, vp]),
     "rafem_mesh_slots": (i64, [vp]),
     "rafem_mesh_stencil_classes": (i32, [vp]),
     "rafem_mesh_pattern": (i32, [vp, vp, vp]),

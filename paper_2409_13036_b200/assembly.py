@@ -12,6 +12,7 @@ four kernels, and the returned matrix stays in HBM.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import weakref
 from dataclasses import dataclass, field
 
@@ -112,6 +113,33 @@ def _dof_kinds(mesh):
     return kind
 
 
+_EXACT_GEOMETRY = os.environ.get("RAFEM_EXACT_GEOMETRY", "0") == "1"
+
+
+def set_exact_geometry(on: bool) -> None:
+    """Bit-exact assembly mode: device meshes created afterwards take the
+    reference's own element geometry (fem.py:229-240, np.linalg.det / inv,
+    computed once per mesh on the host and uploaded through
+    rafem_mesh_set_geometry); every assembly is then bit-identical to
+    assemble_global.  Off by default: the device geometry kernel agrees to
+    rtol 1e-12.  Also RAFEM_EXACT_GEOMETRY=1."""
+    global _EXACT_GEOMETRY
+    _EXACT_GEOMETRY = bool(on)
+
+
+def reference_geometry(nodes, tets):
+    """_basis_gradients (fem.py:229-240) for all tets: gradients (M, 4, 3)
+    and volumes (M,), the same numpy operations in the same order."""
+    corners = nodes[tets]
+    edges = corners[:, 1:, :] - corners[:, :1, :]
+    vol = np.linalg.det(edges) / 6.0
+    inv = np.linalg.inv(edges)
+    grads = np.empty((corners.shape[0], 4, 3))
+    grads[:, 1:, :] = np.transpose(inv, (0, 2, 1))
+    grads[:, 0, :] = -grads[:, 1:, :].sum(axis=1)
+    return grads, vol
+
+
 class DeviceMesh:
     """Mesh + symbolic pattern + geometry resident on the device."""
 
@@ -132,6 +160,13 @@ class DeviceMesh:
                                  C.byref(h))
         nat.check(rc, "mesh setup")
         self._adopt(h)
+        self.exact_geometry = False
+        if _EXACT_GEOMETRY and self.tet_count > 0:
+            grads, vol = reference_geometry(nodes, tets)
+            grads = np.ascontiguousarray(grads, dtype=np.float64)
+            vol = np.ascontiguousarray(vol, dtype=np.float64)
+            nat.check(L.rafem_mesh_set_geometry(h, nat.ptr(grads), nat.ptr(vol)), "mesh geometry")
+            self.exact_geometry = True
 
     def _adopt(self, h):
         L = nat.lib()
@@ -302,7 +337,7 @@ def _material_key(mesh, material):
 
 def device_mesh(mesh, material) -> DeviceMesh:
     """Cached device mesh for (mesh object, material values)."""
-    key = (id(mesh), _material_key(mesh, material))
+    key = (id(mesh), _material_key(mesh, material), _EXACT_GEOMETRY)
     hit = _MESH_CACHE.get(key)
     if hit is not None:
         ref, nodes_id, tets_id, dm = hit

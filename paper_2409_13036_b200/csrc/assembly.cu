@@ -301,6 +301,40 @@ __global__ void geometry_kernel(const double* nodes, const int* tets, int M, dou
         }
 }
 
+// base = vol * grad_a . grad_b from given gradients and volumes, the dot in
+// np.einsum("mid,mjd->mij")'s order ((d0 + d2) + d1; geometry_kernel's too)
+__global__ void base_from_grad_kernel(const double* grad, const double* vol_in, int M, double* base) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= M) return;
+    double g[4][3];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) g[a][d] = grad[12LL * e + 3 * a + d];
+    const double vol = vol_in[e];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = a; b < 4; ++b) {
+            const double dot = add(add(mul(g[a][0], g[b][0]), mul(g[a][2], g[b][2])), mul(g[a][1], g[b][1]));
+            base[10LL * e + sym_index(a, b)] = mul(vol, dot);
+        }
+}
+
+int mesh_set_geometry(rafem_mesh* m, const double* grad, const double* vol) {
+    rafem_ctx* ctx = m->ctx;
+    const int M = m->M;
+    if (M <= 0) return RAFEM_OK;
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(m->grad, grad, sizeof(double) * 12 * (size_t)M, cudaMemcpyHostToDevice,
+                                     ctx->stream));
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(m->vol, vol, sizeof(double) * (size_t)M, cudaMemcpyHostToDevice, ctx->stream));
+    base_from_grad_kernel<<<(M + 127) / 128, 128, 0, ctx->stream>>>(m->grad, m->vol, M, m->base);
+    ctx->launches++;
+    RF_CUDA_TRY(ctx, cudaGetLastError());
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return RAFEM_OK;
+}
+
 // ---------------------------------------------------------------------------
 // numeric fill (device functions in assembly_dev.cuh)
 

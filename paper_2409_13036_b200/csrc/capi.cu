@@ -487,6 +487,11 @@ int rafem_mesh_create(rafem_ctx* ctx, int64_t n_nodes, const double* nodes, int6
     return RAFEM_OK;
 }
 
+int rafem_mesh_set_geometry(rafem_mesh* m, const double* grad, const double* vol) {
+    if (!m || !grad || !vol) return RAFEM_ERR_INVALID;
+    return mesh_set_geometry(m, grad, vol);
+}
+
 void rafem_mesh_destroy(rafem_mesh* m) {
     if (!m) return;
     auto& pc = m->ctx->part_cache;  // partitions cached for this mesh's pattern

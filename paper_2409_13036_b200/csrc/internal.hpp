@@ -237,6 +237,7 @@ int vec_delta_launch(rafem_ctx* ctx, const double* xn, const double* xo, int n, 
 // assembly.cu
 int mesh_symbolic(rafem_mesh* m);
 int mesh_geometry(rafem_mesh* m);
+int mesh_set_geometry(rafem_mesh* m, const double* grad, const double* vol);  // host geometry (exact mode)
 int mesh_slot_lists(rafem_mesh* m);  // per-slot contributor lists (built on first use)
 int mesh_slot_positions(rafem_mesh* m);  // their inverse maps (fused simulation, built on first use)
 // stencil classes of the node pattern (built on first use; none when the

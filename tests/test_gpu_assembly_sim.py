@@ -414,3 +414,48 @@ def test_fused_element_fill_is_bitwise_the_two_kernel_fill(dims, monkeypatch):
             out.append((s.matrix.vals.copy(), s.rhs.copy(), s.voltage_row_scale))
     for a, b in zip(out[:2], out[2:]):
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
+
+
+@pytest.mark.parametrize("name", ["tet", "b333", "b435", "b666", "A"])
+def test_exact_geometry_assembly_is_bitwise_reference(name):
+    """Bit-exact assembly mode (set_exact_geometry / rafem_mesh_set_geometry,
+    SURVEY §8(c)2): with the reference's own element geometry the device
+    assemble_global equals the reference's output bit for bit — values and
+    rhs, with and without constraints / equilibration, hot and cold."""
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, assemble_global, set_exact_geometry
+    d = golden("assembly")
+    set_exact_geometry(True)
+    try:
+        mesh = mesh_for(name, d)
+        t, v, tp = d[f"{name}_t"], d[f"{name}_v"], d[f"{name}_tp"]
+        for tag, kw in (("full", {}), ("raw", dict(apply_constraints=False)),
+                        ("noeq", dict(equilibrate=False))):
+            s = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, v, tp, 0.5, **kw)
+            assert np.array_equal(s.matrix.row_ptr, d[f"{name}_{tag}_row_ptr"])
+            assert np.array_equal(s.matrix.col_idx, d[f"{name}_{tag}_col_idx"])
+            assert s.voltage_row_scale == float(d[f"{name}_{tag}_scale"])
+            assert np.array_equal(s.matrix.vals, d[f"{name}_{tag}_vals"]), tag
+            assert np.array_equal(s.rhs, d[f"{name}_{tag}_rhs"]), tag
+        cold = assemble_global(mesh, MaterialParams.default(), SimConfig(), np.full(mesh.node_count, 37.0),
+                               np.zeros(mesh.node_count), np.full(mesh.node_count, 37.0), 0.5)
+        assert np.array_equal(cold.matrix.vals, d[f"{name}_cold_vals"])
+        assert np.array_equal(cold.rhs, d[f"{name}_cold_rhs"])
+    finally:
+        set_exact_geometry(False)
+
+
+def test_exact_geometry_two_regions_bitwise():
+    from paper_2409_13036_b200 import (MaterialParams, RegionMaterial, SimConfig, assemble_global,
+                                       generate_box_mesh, set_exact_geometry)
+    d = golden("assembly")
+    set_exact_geometry(True)
+    try:
+        mesh = generate_box_mesh(4, 3, 5)
+        mesh.regions = d["reg2_regions"].copy()
+        mat = MaterialParams({0: RegionMaterial(), 1: RegionMaterial(k=0.9e-3, rho_c=2.5e-3,
+                                                                      sigma0=0.35e-3, alpha=0.01)})
+        s = assemble_global(mesh, mat, SimConfig(), d["reg2_t"], d["reg2_v"], d["reg2_t"], 0.25)
+        assert np.array_equal(s.matrix.vals, d["reg2_vals"])
+        assert np.array_equal(s.rhs, d["reg2_rhs"])
+    finally:
+        set_exact_geometry(False)

@@ -36,9 +36,9 @@ def c3_oracle_mesh():
 
 
 @pytest.mark.parametrize("iterate", ["cold", "hot"])
-@pytest.mark.parametrize("mesh_path", ["host", "device"])
+@pytest.mark.parametrize("mesh_path", ["host", "device", "host-exact"])
 def test_c3_assembly_vs_oracle(c3_oracle_mesh, iterate, mesh_path):
-    from paper_2409_13036_b200 import MaterialParams, SimConfig, assemble_global, generate_box_mesh
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, assemble_global, generate_box_mesh, set_exact_geometry
     from paper_2409_13036_b200.assembly import DeviceMesh
     om = c3_oracle_mesh
     n = om.nodes.shape[0]
@@ -48,10 +48,19 @@ def test_c3_assembly_vs_oracle(c3_oracle_mesh, iterate, mesh_path):
         t, v = _hot(n)
     tp = np.full(n, 37.0) if iterate == "cold" else t
     ref = O.assemble(om, {0: O.OMaterial()}, 25.0, 37.0, t, v, tp, 0.5)
-    if mesh_path == "host":
-        s = assemble_global(generate_box_mesh(*C3), MaterialParams.default(), SimConfig(), t, v, tp, 0.5)
-        row_ptr, col_idx, vals, rhs, scale = (s.matrix.row_ptr, s.matrix.col_idx, s.matrix.vals, s.rhs,
-                                              s.voltage_row_scale)
+    if mesh_path in ("host", "host-exact"):
+        set_exact_geometry(mesh_path == "host-exact")  # the reference's geometry: bit-exact assembly
+        try:
+            s = assemble_global(generate_box_mesh(*C3), MaterialParams.default(), SimConfig(), t, v, tp, 0.5)
+            row_ptr, col_idx, vals, rhs, scale = (s.matrix.row_ptr, s.matrix.col_idx, s.matrix.vals, s.rhs,
+                                                  s.voltage_row_scale)
+        finally:
+            set_exact_geometry(False)
+        if mesh_path == "host-exact":
+            assert np.array_equal(row_ptr, ref.row_ptr) and np.array_equal(col_idx, ref.col_idx)
+            assert scale == ref.scale
+            assert np.array_equal(vals, ref.vals) and np.array_equal(rhs, ref.rhs)
+            return
     else:
         # generate_box_mesh + symbolic phase on the device (rafem_mesh_create_box)
         import ctypes as C
