@@ -2269,6 +2269,9 @@ static int spmv_pipe_launch(rafem_ctx* ctx, const MatView& A, const double* x_de
     // per-tile bulk L2 prefetch of the tile's own x rows (RAFEM_XPF=1; off by
     // default — measured r2, cold L2: C3 36.9 -> 35.7 us, C4 401 -> 416 us
     // with the default 192 x 2 tiles; it helps only the narrower tiles)
+    // (a per-gather L2 prefetch of the next tile's columns — computable from
+    // the stencil classes before its matrix tile lands — measured slower at
+    // C3: 38.9 vs 37.5 us; profiles/r2b_spmv_x_prefetch_sweep.txt)
     const char* xe = getenv("RAFEM_XPF");
     int xpf = (xe && xe[0] == '1') ? 1 : 0;
     void* args[] = {&Av, &xp, &yp, &valcap, &bufbytes, &xpf};

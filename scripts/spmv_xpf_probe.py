@@ -30,7 +30,7 @@ def main():
     B = 16 * S + n + 4 * (n + 1) + 32 * n
     x = np.random.default_rng(1).standard_normal(2 * n)
     ys = {}
-    for cfg in ["", "128,4,1,2", "96,4,1,2", "128,3,1,2", "256,2,1,1", "64,4,1,3"]:
+    for cfg in ["", "128,3,1,2", "256,2,1,1", "192,3,1,1", "128,4,1,2"]:
         for xpf in ("0", "1"):
             os.environ["RAFEM_XPF"] = xpf
             if cfg:
