@@ -1846,9 +1846,33 @@ static int cluster_size_for(int N) {
     return C;
 }
 
+static bool cluster_launchable_uncached(rafem_ctx* ctx, const void* fn, int C, int nt, size_t smem);
+// The attribute calls and the occupancy query cost tens of microseconds; a
+// solve on the plug-in seam is ~100 us, so the answer is cached per
+// (kernel, cluster size, threads) and the attribute raised to the largest
+// shared memory asked so far.
 static bool cluster_launchable(rafem_ctx* ctx, const void* fn, int C, int nt, size_t smem) {
+    struct Key {
+        const void* fn;
+        int C, nt;
+        size_t smem;
+        bool ok;
+    };
+    static std::vector<Key> cache;
+    for (const Key& k : cache)
+        if (k.fn == fn && k.C == C && k.nt == nt && k.smem >= smem && k.ok) return true;
+    const bool ok = cluster_launchable_uncached(ctx, fn, C, nt, smem);
+    if (ok) cache.push_back({fn, C, nt, smem, ok});
+    return ok;
+}
+static bool cluster_launchable_uncached(rafem_ctx* ctx, const void* fn, int C, int nt, size_t smem) {
+    // the attribute never goes down: launches cached earlier may need more
+    static std::vector<std::pair<const void*, size_t>> maxset;
+    size_t smax = smem;
+    for (auto& e : maxset)
+        if (e.first == fn) smax = std::max(smax, e.second);
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
@@ -1867,6 +1891,13 @@ static bool cluster_launchable(rafem_ctx* ctx, const void* fn, int C, int nt, si
     int ncl = 0;
     const bool ok = cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) == cudaSuccess && ncl >= 1;
     cudaGetLastError();
+    bool found = false;
+    for (auto& e : maxset)
+        if (e.first == fn) {
+            e.second = smax;
+            found = true;
+        }
+    if (!found) maxset.push_back({fn, smax});
     return ok;
 }
 
