@@ -254,7 +254,7 @@ void rafem_ctx_destroy(rafem_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (DevBuf* b : {&ctx->ws_basis, &ctx->ws_vec, &ctx->ws_partial, &ctx->ws_hess, &ctx->ws_hist,
                       &ctx->ws_cyc, &ctx->ws_part, &ctx->ws_res, &ctx->ws_trace, &ctx->ws_flags, &ctx->ws_simout,
-                      &ctx->ws_diag})
+                      &ctx->ws_diag, &ctx->ws_gal})
         if (b->p) cudaFree(b->p);
     for (auto& e : ctx->part_cache) dfree(ctx, e.gpart);
     ctx->part_cache.clear();

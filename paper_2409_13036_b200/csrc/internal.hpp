@@ -105,6 +105,7 @@ struct rafem_ctx {
     rafem::DevBuf ws_flags;     // grid barrier / all-reduce slots
     rafem::DevBuf ws_simout;    // fused simulation summary
     rafem::DevBuf ws_diag;      // diagonal-sum partials of the assembly
+    rafem::DevBuf ws_gal;       // fused simulation: Galerkin-start ring of solution increments
     unsigned epoch = 0;         // per-launch flag epoch
     // device blocks of destroyed meshes / systems kept for reuse (a new mesh
     // of the same size then costs no cudaMalloc / cudaFree, which synchronise)

@@ -1085,7 +1085,7 @@ constexpr int kPipeRows = 128;  // max node rows per CTA (y and the owner vector
 template <bool PRE, class Mode, class R>
 RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, double bnorm, double* co, double* red,
                             int& par, const int* zflag = nullptr, const double* x0_gather = nullptr,
-                            const double* xold = nullptr, double* dmax = nullptr) {
+                            const double* xold = nullptr, double* dmax = nullptr, const double* r_pre = nullptr) {
     __shared__ double2 ybuf[kPipeRows];
     // owner-only recurrence vectors live in shared memory (indexed by the
     // global dof, offset by the CTA's first dof); u is mirrored to global
@@ -1245,12 +1245,10 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
             double v[3] = {0.0, 0.0, 0.0};
             const double* xg = x0_gather ? x0_gather : x;
             x0_gather = nullptr;
-            spmv_team<2>(rows, g0, g1, a.team, SrcPlain{xg}, [&](int g, const double* y) {
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    const int e = 2 * g + k;
+            if (r_pre) {  // the caller's exact r = b - A x of the start (no product here)
+                for (int e = lo + tid; e < hi; e += blockDim.x) {
                     const double be = a.b[e];
-                    const double re = sub(be, y[k]);
+                    const double re = r_pre[e];
                     r[e] = re;
                     if (!blk) {
                         const double ue = PRE ? mul(M(e), re) : re;
@@ -1260,7 +1258,25 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                     v[2] = add(v[2], mul(re, re));
                     if (with_b) v[0] = add(v[0], mul(be, be));
                 }
-            });
+                r_pre = nullptr;
+            } else {
+                spmv_team<2>(rows, g0, g1, a.team, SrcPlain{xg}, [&](int g, const double* y) {
+#pragma unroll
+                    for (int k = 0; k < 2; ++k) {
+                        const int e = 2 * g + k;
+                        const double be = a.b[e];
+                        const double re = sub(be, y[k]);
+                        r[e] = re;
+                        if (!blk) {
+                            const double ue = PRE ? mul(M(e), re) : re;
+                            u[e] = ue;
+                            ug[e] = ue;
+                        }
+                        v[2] = add(v[2], mul(re, re));
+                        if (with_b) v[0] = add(v[0], mul(be, be));
+                    }
+                });
+            }
             // later heads usually end the solve: their block step waits until
             // the true residual says the iteration continues
             if (blk && first_head) {
@@ -2764,6 +2780,7 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     if (smem + fa.sharedSizeBytes > 227 * 1024) return RAFEM_ERR_UNSUPPORTED;
     // room to stage each CTA's assembly index data (simulate_dev.cuh)
     int stage_fill = 0;
+    size_t gal_scratch_min = ~(size_t)0;  // doubles of contribution scratch on the smallest CTA
     if (mesh->slot_src && !(getenv("RAFEM_NO_STAGE_FILL") && getenv("RAFEM_NO_STAGE_FILL")[0] == '1')) {
         // per block: row, slot, incidence and contributor-list boundaries,
         // gathered on the device and copied once
@@ -2793,6 +2810,7 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
         }
         need = (need + 15) / 16 * 16;
         need2 = (need2 + 15) / 16 * 16;
+        for (int c = 0; c < G; ++c) gal_scratch_min = std::min(gal_scratch_min, 2 * (size_t)(hsp[c + 1] - hsp[c]));
         const char* nsc = getenv("RAFEM_NO_STAGE_CONTRIB");
         const char* nl = getenv("RAFEM_NO_LEAN_SIM");
         if (pipe && need2 + fa_lean.sharedSizeBytes <= 227 * 1024 && !(nsc && nsc[0] == '1') &&
@@ -2816,7 +2834,12 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     const long long n2 = 2LL * N;
     const long long ldv = (n2 + 31) / 32 * 32;
     if (int rc = ensure(ctx, ctx->ws_vec, sizeof(double) * (size_t)10 * ldv)) return rc;
-    if (int rc = ensure(ctx, ctx->ws_partial, sizeof(double) * (size_t)2 * 8 * G)) return rc;
+    // partials: two parity buffers of 8 x G, then the Galerkin start's
+    // nv (nv + 3) / 2 x G
+    if (int rc = ensure(ctx, ctx->ws_partial,
+                        sizeof(double) * ((size_t)(16 + kGalMax + kGalMax * (kGalMax + 1) / 2) * G +
+                                          kGalMax + kGalMax * (kGalMax + 1) / 2)))
+        return rc;
     if (int rc = ensure(ctx, ctx->ws_simout, sizeof(SimDevOut))) return rc;
     {
         const size_t fb = sizeof(unsigned long long) * (2 * 8 * (size_t)G + 8);
@@ -2879,6 +2902,21 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     {
         const char* nv = getenv("RAFEM_NO_VX0");
         S.vx0 = !(nv && nv[0] == '1');
+    }
+    {
+        // Galerkin solver start (pipelined PCG with staged contributions, whose
+        // scratch holds the (2k + 1) x 2 rows-per-CTA doubles it needs)
+        int K = 10;  // window (measured on the mesh-B run: 8 26.3, 10 23.1, 12 23.2, 14 23.6, 16 24.4 ms)
+        if (const char* ge = getenv("RAFEM_GALERKIN_K")) K = std::max(0, std::min(kGalMax, atoi(ge)));
+        if (!(stage_fill == 2 && fn == fn_lean) || !pipe) K = 0;
+        if (K > 0 && gal_scratch_min < (size_t)(2 * K + 1) * 2 * part.max_groups) K = 0;
+        if (K > 0) {
+            if (int rc = ensure(ctx, ctx->ws_gal, sizeof(double) * (size_t)(K + 1) * n2)) return rc;
+            S.gal_d = static_cast<double*>(ctx->ws_gal.p);
+            S.gal_xl = S.gal_d + (size_t)K * n2;
+        }
+        S.gal_k = K;
+        if (const char* gd = getenv("RAFEM_GAL_DBG")) S.gal_dbg = atoi(gd);
     }
     if (int rc = system_contrib(s)) return rc;
     S.contrib = reinterpret_cast<double2*>(s->contrib);

@@ -49,7 +49,232 @@ struct SimArgs {
     long long ptrace_cap;
     int stage_fill;            // contributor lists, incidences and dof kinds staged in smem
     int vx0;                   // pipelined PCG: first pass of a step starts from V extrapolated in time
+    // Galerkin solver start (pipelined PCG path): ring of the last gal_k
+    // increments between successive pass solutions (gal_k x n2) and the
+    // last solution (n2); gal_k == 0 disables it
+    double* gal_d;
+    double* gal_xl;
+    int gal_k;
+    int gal_dbg;  // cost study: 1 skip products, 2 skip dots, 4 skip gather, 8 skip Cholesky,
+                  // 16 only on a step's first pass
 };
+
+constexpr int kGalMax = 16;  // largest Galerkin window
+
+// Galerkin start of a pass's solve (the native loop's own choice of x0; the
+// plug-in seam keeps the reference's x0): with D the nv most recent
+// increments between successive pass solutions, x0 += D c where
+// (D^T A D) c = D^T (b - A x0) with this pass's A — the A-norm-closest
+// point of x0 + span(D) to the solution, so the Krylov solve starts
+// without the components the last passes already resolved.  Everything is
+// on the CTA's own rows and its shared-memory matrix slice: 1 + nv slice
+// products (x0 and the d_j, gathered from L2), nv (nv + 3) / 2 dots in one
+// reduction, a scaled pivot-thresholded Cholesky of the nv x nv system on
+// every CTA (identical bits everywhere: the reduction is fixed-order), the
+// update of x0 and a barrier.  CPU study (scripts/galerkin_x0_probe.py,
+// the 900 s mesh-B run, block-Jacobi PCG): 4,655 -> 2,997 (nv = 8) and
+// 2,223 (nv = 12) iterations with the same trajectory.
+// scr: shared memory for (2 nv + 1) x 2 nr doubles; gco: >= nv (nv + 3) / 2.
+template <class Mode, class R>
+RF_DEV void galerkin_start(const KArgs& a, const R& rows, Sync<Mode>& sy, const double* b,
+                                            const double* xsrc, double* x, const double* D, long long n2, int K,
+                                            int head, int nv, double* scr, double* P, double* gco,
+                                            int skip = 0) {
+    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int g0 = a.gpart[cta], g1 = a.gpart[cta + 1], lo = 2 * g0, nd = 2 * (g1 - g0);
+    double* sR = scr;                    // r0 = b - A x0 (own dofs)
+    double* sD = scr + nd;               // d_j (own dofs), j < nv
+    double* sAD = sD + (size_t)nv * nd;  // A d_j
+    auto dvec = [&](int j) { return D + (size_t)((head - 1 - j + 2 * K) % K) * n2; };  // most recent first
+    // products of the slice with x0 and the d_j, six sources per sweep (a
+    // team of lanes per row; a lane's slots and all their gathers issued
+    // before the first accumulation, so a sweep is one L2 round trip)
+    constexpr int NQ = 6, SL = 4;  // sources per sweep, slots per lane in flight
+    for (int q0 = -1; q0 < ((skip & 1) ? -1 : nv); q0 += NQ) {
+        const int nq = min(NQ, nv - q0);
+        const double2* src[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int j = q0 + q;
+            src[q] = reinterpret_cast<const double2*>(j < 0 ? xsrc : (j < nv ? dvec(j) : xsrc));
+        }
+        const int team = a.team, tl = tid & (team - 1), nteams = blockDim.x / team;
+        for (int gb = g0; gb < g1; gb += nteams) {
+            const int g = gb + tid / team;
+            double acc[2 * NQ];
+#pragma unroll
+            for (int k = 0; k < 2 * NQ; ++k) acc[k] = 0.0;
+            if (g < g1) {
+                const int s0 = rows.start(g), s1 = rows.start(g + 1);
+                for (int sb = s0 + tl; sb < s1; sb += SL * team) {
+                    int c[SL];
+                    double2 v[SL], xv[SL][NQ];
+#pragma unroll
+                    for (int u = 0; u < SL; ++u) {
+                        const int sl = sb + u * team;
+                        c[u] = sl < s1 ? rows.column(sl) : -1;
+                        v[u] = sl < s1 ? rows.value2(sl) : make_double2(0.0, 0.0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < SL; ++u)
+#pragma unroll
+                        for (int q = 0; q < NQ; ++q)
+                            if (c[u] >= 0 && q < nq) xv[u][q] = __ldca(src[q] + c[u]);
+#pragma unroll
+                    for (int u = 0; u < SL; ++u)
+#pragma unroll
+                        for (int q = 0; q < NQ; ++q)
+                            if (c[u] >= 0 && q < nq) {
+                                acc[2 * q] = fma(v[u].x, xv[u][q].x, acc[2 * q]);
+                                acc[2 * q + 1] = fma(v[u].y, xv[u][q].y, acc[2 * q + 1]);
+                            }
+                }
+            }
+            for (int o = team >> 1; o > 0; o >>= 1)
+#pragma unroll
+                for (int k = 0; k < 2 * NQ; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+            if (g < g1 && tl == 0) {
+                const int e = 2 * g - lo;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const int j = q0 + q;
+                    if (q >= nq) continue;
+                    if (j < 0) {
+                        sR[e] = sub(b[2 * g], acc[0]);
+                        sR[e + 1] = sub(b[2 * g + 1], acc[1]);
+                    } else {
+                        sAD[(size_t)j * nd + e] = acc[2 * q];
+                        sAD[(size_t)j * nd + e + 1] = acc[2 * q + 1];
+                    }
+                }
+            }
+        }
+    }
+    for (int q = tid; q < nv * nd; q += blockDim.x) {  // all the d_j rows at once
+        const int j = q / nd, e = q - j * nd;
+        sD[q] = __ldcg(dvec(j) + lo + e);
+    }
+    __syncthreads();
+    // coefficient c: g_i (c < nv), then M_ij (i <= j) row by row; a thread
+    // each, two fixed interleaved partial sums over the own dofs
+    const int nvals = nv + nv * (nv + 1) / 2;
+    for (int c = tid; c < ((skip & 2) ? 0 : nvals); c += blockDim.x) {
+        int i, j;
+        const double* u;
+        if (c < nv) {
+            i = c;
+            u = sR;
+        } else {
+            int q = c - nv;
+            i = 0;
+            while (q >= nv - i) {
+                q -= nv - i;
+                ++i;
+            }
+            j = i + q;
+            u = sAD + (size_t)j * nd;
+        }
+        // (shared-space loads: the scratch pointer arrives as a generic one)
+        const unsigned dis = smem_u32(sD + (size_t)i * nd), us = smem_u32(u);
+        double a0 = 0.0, a1 = 0.0;
+        int e = 0;
+        for (; e + 2 <= nd; e += 2) {
+            double d0, d1, u0, u1;
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(d0), "=d"(d1) : "r"(dis + 8u * e));
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(u0), "=d"(u1) : "r"(us + 8u * e));
+            a0 = fma(d0, u0, a0);
+            a1 = fma(d1, u1, a1);
+        }
+        if (e < nd) {
+            double d0, u0;
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(d0) : "r"(dis + 8u * e));
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(u0) : "r"(us + 8u * e));
+            a0 = fma(d0, u0, a0);
+        }
+        P[(long long)c * G + cta] = a0 + a1;
+    }
+    sy.barrier();
+    // two-level gather: CTA c folds coefficient c (c, c + G, ...) over the G
+    // partials in CTA order, a barrier, every CTA reads the nvals totals
+    double* T = P + (long long)nvals * G;
+    for (int c = cta; c < ((skip & 4) ? 0 : nvals); c += G)
+        if (warp == 0) {
+            const double s = reduce_partials_warp(P + (long long)c * G, G);
+            if (lane == 0) T[c] = s;
+        }
+    sy.barrier();
+    for (int c = tid; c < nvals; c += blockDim.x) gco[c] = __ldcg(T + c);
+    __syncthreads();
+    // scaled Cholesky with a pivot threshold (dependent directions drop out)
+    // and the two triangular solves, right-looking on warp 0 in shared memory
+    __shared__ double Ms[kGalMax][kGalMax + 1];
+    __shared__ double cf[kGalMax], sc[kGalMax], rl[kGalMax];
+    if (warp == 0 && !(skip & 8)) {
+        auto Mij = [&](int i, int j) {  // M packed after g in gco: row i holds j = i..nv-1
+            if (i > j) {
+                const int t = i;
+                i = j;
+                j = t;
+            }
+            return gco[nv + i * nv - (i * (i - 1)) / 2 + (j - i)];
+        };
+        if (lane < nv) {
+            const double m = Mij(lane, lane);
+            sc[lane] = m > 0.0 ? 1.0 / sqrt(m) : 0.0;
+        }
+        __syncwarp();
+        for (int q = lane; q < nv * nv; q += 32) {
+            const int i = q / nv, j = q - i * nv;
+            Ms[i][j] = Mij(i, j) * sc[i] * sc[j];
+        }
+        __syncwarp();
+        unsigned ac = 0;
+        for (int j = 0; j < nv; ++j) {
+            const double d = Ms[j][j];
+            const bool ok = sc[j] > 0.0 && d > 1e-10;
+            const double r = ok ? 1.0 / sqrt(d) : 0.0;  // 1 / L_jj
+            if (ok) ac |= 1u << j;
+            if (lane == j) rl[j] = r;
+            if (lane > j && lane < nv) Ms[lane][j] *= r;  // column j of L
+            __syncwarp();
+            {  // trailing lower triangle: lane = column, rows below it
+                const int col = j + 1 + lane;
+                if (col < nv) {
+                    const double lcj = Ms[col][j];
+                    for (int row = col; row < nv; ++row) Ms[row][col] = fma(-Ms[row][j], lcj, Ms[row][col]);
+                }
+            }
+            __syncwarp();
+        }
+        // L y = S g: lane i holds y_i; L^T z = y; c = S z
+        double y = lane < nv ? gco[lane] * sc[lane] : 0.0;
+        for (int j = 0; j < nv; ++j) {
+            const double yj = __shfl_sync(0xffffffffu, y, j) * rl[j];
+            if (lane == j) y = yj;
+            if (lane > j && lane < nv) y = fma(-Ms[lane][j], yj, y);
+        }
+        for (int j = nv - 1; j >= 0; --j) {
+            const double zj = __shfl_sync(0xffffffffu, y, j) * rl[j];
+            if (lane == j) y = zj;
+            if (lane < j) y = fma(-Ms[j][lane], zj, y);
+        }
+        if (lane < nv) cf[lane] = (ac >> lane & 1u) ? y * sc[lane] : 0.0;
+    }
+    __syncthreads();
+    // x0 += D c on the own rows and, exactly, r0 -= (A D) c: the solver's first
+    // head takes r from sR (no product, so no barrier for the new x here)
+    for (int e = tid; e < nd; e += blockDim.x) {
+        double v = xsrc[lo + e], rr = sR[e];
+        for (int j = 0; j < nv; ++j) {
+            v = fma(cf[j], sD[(size_t)j * nd + e], v);
+            rr = fma(-cf[j], sAD[(size_t)j * nd + e], rr);
+        }
+        x[lo + e] = v;
+        sR[e] = rr;
+    }
+    __syncthreads();
+}
 
 // Max over CTAs of one nonnegative value (exact, order independent).
 template <class Mode>
@@ -164,6 +389,7 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
     extern __shared__ __align__(16) double sval[];
     __shared__ double red[32 * 8];
     __shared__ double co[8];
+    __shared__ double gco[LEAN ? kGalMax + kGalMax * (kGalMax + 1) / 2 : 1];
     __shared__ FillScratch ws[LEAN ? 1 : NT / 32];
     __shared__ int zflag;
     const KArgs& a = S.k;
@@ -253,6 +479,8 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
 
     double t = 0.0, dt_state = p.dt_init, dt_prev = p.dt_init;
     long long step = 0, passes = 0, corr = 0, inner = 0, halv = 0, bad = -1;
+    int gal_n = 0, gal_head = 0;  // Galerkin ring: valid increments, next slot
+    bool gal_last = false;        // gal_xl holds the previous pass's solution
     long long asm_ns = 0, sol_ns = 0;
     int status = RAFEM_OK, failed_step = -1;
     double failed_dt = 0.0;
@@ -445,8 +673,34 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
                 kk.b = S.rhs;
                 kk.x = X(inew);
                 kk.res = nullptr;
-                o = pcg_pipe_core<PRE, GridMode>(kk, rows, sy, -1.0, co, red, par, &zflag, x0_new ? X(inew) : X(iit),
-                                                 X(iit), &hdelta);
+                bool gal = false;
+                if constexpr (LEAN) {
+                    if (S.gal_k > 0 && gal_n > 0 && cst && (it == 1 || !(S.gal_dbg & 16))) {
+                        // (X(inew) holds the start on every CTA's own rows; the
+                        // constraints' writes of the rhs are visible after the bar.sync)
+                        galerkin_start<GridMode>(kk, rows, sy, S.rhs, x0_new ? X(inew) : X(iit), X(inew), S.gal_d,
+                                                 n2, S.gal_k, gal_head, gal_n, reinterpret_cast<double*>(cst),
+                                                 a.partial + 16LL * G, gco, S.gal_dbg);
+                        gal = true;
+                    }
+                }
+                o = pcg_pipe_core<PRE, GridMode>(kk, rows, sy, -1.0, co, red, par, &zflag,
+                                                 x0_new ? X(inew) : X(iit), X(iit), &hdelta,
+                                                 gal ? reinterpret_cast<const double*>(cst) - 2LL * a.gpart[cta] : nullptr);
+                if (S.gal_k > 0 && o.status == RAFEM_OK && o.converged) {
+                    // the ring: d = x_new - (previous pass's solution), own rows
+                    double* dn = S.gal_d + (size_t)gal_head * n2;
+                    for (int e = lo + tid; e < hi; e += blockDim.x) {
+                        const double xn = X(inew)[e];
+                        if (gal_last) dn[e] = sub(xn, S.gal_xl[e]);
+                        S.gal_xl[e] = xn;
+                    }
+                    if (gal_last) {
+                        gal_head = (gal_head + 1) % S.gal_k;
+                        gal_n = gal_n < S.gal_k ? gal_n + 1 : S.gal_k;
+                    }
+                    gal_last = true;
+                }
                 if (o.status == RAFEM_ERR_INVALID) {  // ValueError: zero diagonal under Jacobi (solver.py:416-417)
                     status = RAFEM_ERR_INVALID;
                     abort_run = true;

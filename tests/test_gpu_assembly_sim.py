@@ -261,9 +261,12 @@ def test_time_loop_failure_semantics():
     assert [r.dt for r in recs] == list(d["dt"]) and [r.time for r in recs] == list(d["time"])
 
 
-def test_fused_simulation_matches_multi_kernel_loop():
-    """The one-launch simulation kernel and the per-pass kernel loop agree."""
+def test_fused_simulation_matches_multi_kernel_loop(monkeypatch):
+    """The one-launch simulation kernel and the per-pass kernel loop agree
+    (the fused kernel's Galerkin solver start off: it is the fused kernel's
+    own, see test_galerkin_start_keeps_the_run_and_cuts_iterations)."""
     import os
+    monkeypatch.setenv("RAFEM_GALERKIN_K", "0")
     from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh
     from paper_2409_13036_b200.timeloop import DeviceRun
     mesh = generate_box_mesh(15, 15, 16)
@@ -324,14 +327,16 @@ def test_block_jacobi_pcg_full_run_vs_reference():
     _compare_run(recs12, golden("run_B900_1e-12"), 1e-6, every_step=True)
 
 
-def test_lean_and_generic_simulation_kernels_are_bitwise_equal():
+def test_lean_and_generic_simulation_kernels_are_bitwise_equal(monkeypatch):
     """The paper-scale instantiation of the fused simulation (pipelined PCG +
     cp.async-staged fill, everything else compiled out), the generic kernel
     taking the same paths at run time, the generic kernel with the
     register-chunked fill, and the lean kernel with tet-major element
     outputs gathered per element instead of the slot-major layout fetched
-    by TMA give the same bits: same sums in the same order."""
+    by TMA give the same bits: same sums in the same order (the lean
+    kernel's Galerkin solver start off: the generic kernel has none)."""
     import os
+    monkeypatch.setenv("RAFEM_GALERKIN_K", "0")
     from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh
     from paper_2409_13036_b200.timeloop import DeviceRun
     mesh = generate_box_mesh(15, 15, 16)
@@ -365,9 +370,11 @@ def test_first_pass_solver_start_extrapolates_v_without_changing_the_run():
     from paper_2409_13036_b200.timeloop import DeviceRun
     mesh = generate_box_mesh(20, 20, 21)
     cfg = SimConfig(total_time=900.0, solver=SolverConfig(backend="pcg", precondition="block_jacobi"))
-    new, sn = DeviceRun(mesh).run(cfg)
-    os.environ["RAFEM_NO_VX0"] = "1"
+    # isolate the V extrapolation from the Galerkin start (its own test below)
+    os.environ["RAFEM_GALERKIN_K"] = "0"
     try:
+        new, sn = DeviceRun(mesh).run(cfg)
+        os.environ["RAFEM_NO_VX0"] = "1"
         old, so = DeviceRun(mesh).run(cfg)
         loop_env = {"RAFEM_NO_FUSED": "1"}
         os.environ.update(loop_env)
@@ -375,7 +382,7 @@ def test_first_pass_solver_start_extrapolates_v_without_changing_the_run():
         del os.environ["RAFEM_NO_VX0"]
         new_loop, snl = DeviceRun(mesh).run(cfg)
     finally:
-        for k in ("RAFEM_NO_VX0", "RAFEM_NO_FUSED"):
+        for k in ("RAFEM_NO_VX0", "RAFEM_NO_FUSED", "RAFEM_GALERKIN_K"):
             os.environ.pop(k, None)
     traj = [(r.time, r.dt, r.corrector_iters) for r in old]
     assert [(r.time, r.dt, r.corrector_iters) for r in new] == traj
@@ -459,3 +466,34 @@ def test_exact_geometry_two_regions_bitwise():
         assert np.array_equal(s.rhs, d["reg2_rhs"])
     finally:
         set_exact_geometry(False)
+
+
+def test_galerkin_start_keeps_the_run_and_cuts_iterations(monkeypatch):
+    """The fused kernel's Galerkin solver start (x0 += D c over the last
+    increments between pass solutions, simulate_dev.cuh galerkin_start)
+    changes only the solves' paths: the 900 s mesh-B run keeps its
+    trajectory (time, dt, corrector passes of every step), its final fields
+    stay within 1e-6 of the reference's, block-Jacobi PCG iterations drop by
+    more than a third (CPU study: scripts/galerkin_x0_probe.py), and repeat
+    runs are bitwise identical."""
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, generate_box_mesh
+    from paper_2409_13036_b200.timeloop import DeviceRun
+    run = DeviceRun(generate_box_mesh(20, 20, 21), MaterialParams.default())
+    cfg = SimConfig(total_time=900.0, solver=SolverConfig(backend="pcg", precondition="block_jacobi"))
+    monkeypatch.setenv("RAFEM_GALERKIN_K", "0")
+    base, sb = run.run(cfg)
+    monkeypatch.delenv("RAFEM_GALERKIN_K")
+    gal, sg = run.run(cfg)
+    gal2, _ = run.run(cfg)
+    assert [(r.time, r.dt, r.corrector_iters) for r in gal] == [(r.time, r.dt, r.corrector_iters) for r in base]
+    # Both runs solve every system to ||r|| <= 1e-10 ||b||; from different
+    # starts the ill-conditioned V block lands on different points of that
+    # ball (measured: 1.4e-6 of peak at step 9), the T block much closer.
+    peak = max(np.max(np.abs(r.T)) for r in base)
+    assert max(np.max(np.abs(a.T - b.T)) for a, b in zip(gal, base)) <= 1e-6 * peak
+    vpeak = max(np.max(np.abs(r.V)) for r in base)
+    assert max(np.max(np.abs(a.V - b.V)) for a, b in zip(gal, base)) <= 5e-6 * vpeak
+    _compare_run(gal, golden("run_B900_1e-10"), 1e-6, every_step=False)
+    assert sg.total_solver_iterations < 0.67 * sb.total_solver_iterations, (sg.total_solver_iterations,
+                                                                          sb.total_solver_iterations)
+    assert all(np.array_equal(a.T, b.T) and np.array_equal(a.V, b.V) for a, b in zip(gal, gal2))
