@@ -88,6 +88,7 @@ struct KArgs {
     unsigned long long* gbar;   // grid-barrier arrival counter (zeroed before each launch); null: cg grid sync
     long long vs_off;           // GMRES: own rows of the basis in dynamic smem at this double offset (0: global)
     int vs_ld;                  // its row stride (own dofs of the widest CTA)
+    int gm1r;                   // GMRES with the basis in smem: one-reduce Arnoldi (gmres_1r_body)
 };
 
 // Phase timestamps for diagnosis: slot k of iteration i at trace[i*8 + k].
@@ -372,6 +373,70 @@ RF_DEV void multidot_smem(const double* Vs, int ld, int nv, const double* w, int
     }
 }
 
+// One-reduce Arnoldi partials (gmres_1r_body): for j < k, v_j . u -> row j
+// and v_j . w -> row k + 1 + j; u . u -> row k and u . w -> row 2k + 1.
+// w == nullptr: the u rows only.  One warp per j, as multidot_smem.
+RF_DEV void multidot_pair_smem(const double* Vs, int ld, int k, const double* u, const double* w, int lo, int hi,
+                               double* P, int ldp) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = wid; j <= k; j += nw) {
+        const double* vj = j < k ? Vs + (long long)j * ld - lo : u;
+        double sa = 0.0, sb = 0.0;
+        if (w) {
+            for (int e = lo + lane; e < hi; e += 32) {
+                const double v = vj[e];
+                sa = add(sa, mul(v, u[e]));
+                sb = add(sb, mul(v, w[e]));
+            }
+            sb = warp_sum(sb);
+        } else {
+            for (int e = lo + lane; e < hi; e += 32) sa = add(sa, mul(vj[e], u[e]));
+        }
+        sa = warp_sum(sa);
+        if (lane == 0) {
+            double* pc = P + (long long)blockIdx.x * ldp;
+            pc[j] = sa;
+            if (w) pc[k + 1 + j] = sb;
+        }
+    }
+}
+
+// After a barrier: nv coefficients from CTA-major partials P[c * ldp + i]
+// into co[] on every CTA.  512 threads load at once (8 groups of
+// consecutive CTAs x 64 coefficients, a warp reading 32 adjacent
+// coefficients of one CTA), then each coefficient adds its 8 group sums
+// left to right: one L2 round trip for G <= 152, the same fixed order on
+// every CTA.  gs: 512 doubles of shared scratch.
+RF_DEV void gather_wide(const double* P, int ldp, int nv, int G, double* co, double* gs) {
+    constexpr int NG = 8, U = 19;
+    const int t = threadIdx.x, i0 = t & 63, grp = t >> 6;
+    const int per = (G + NG - 1) / NG;
+    for (int base = 0; base < nv; base += 64) {
+        const int i = base + i0;
+        double s = 0.0;
+        if (grp < NG && i < nv) {
+            const int c0 = grp * per, c1 = min(G, c0 + per);
+            for (int c = c0; c < c1; c += U) {
+                double v[U];
+#pragma unroll
+                for (int q = 0; q < U; ++q) v[q] = c + q < c1 ? __ldcg(P + (long long)(c + q) * ldp + i) : 0.0;
+#pragma unroll
+                for (int q = 0; q < U; ++q)
+                    if (c + q < c1) s = add(s, v[q]);
+            }
+        }
+        if (grp < NG) gs[t] = s;
+        __syncthreads();
+        if (t < 64 && base + t < nv) {
+            double acc = gs[t];
+#pragma unroll
+            for (int g = 1; g < NG; ++g) acc = add(acc, gs[g * 64 + t]);
+            co[base + t] = acc;
+        }
+        __syncthreads();
+    }
+}
+
 // Cluster mode: copy this CTA's slice of the matrix into shared memory
 // (16-byte vector loads; the slice is constant for the whole solve).
 template <int W>
@@ -601,8 +666,17 @@ RF_DEV double prologue(const KArgs& a, Sync<Mode>& sy, int lo, int hi, double* c
 // Arnoldi basis to working precision, but 3 barriers per step instead of
 // k + 2 dependent reductions.
 
+template <int W, bool PRE, class R>
+RF_DEV void gmres_1r_body(const KArgs& a, const R& rows, double* dyn);
+
 template <int W, bool PRE, class Mode, class R>
 RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
+    if constexpr (!Mode::kCluster) {
+        if (a.gm1r) {
+            gmres_1r_body<W, PRE>(a, rows, dyn);
+            return;
+        }
+    }
     __shared__ double red[32 * 8];
     __shared__ double sc[4];
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
@@ -825,6 +899,317 @@ RF_DEV void gmres_body(const KArgs& a, const R& rows, double* dyn) {
                 for (int i = 0; i < used; ++i) u = add(u, mul(Vs ? vrow(i)[e] : __ldca(vrow(i) + e), yy[i]));
                 if (PRE) u = mul(a.minv[e], u);
                 a.x[e] = add(a.x[e], u);
+            }
+        }
+        if (cta == 0 && tid == 0 && cycles < a.cyc_cap) a.cyc[cycles] = hlen - hstart;
+        ++cycles;
+        have_prev = true;
+        prev_start = cycle_start;
+        sy.barrier();  // x final everywhere before the next SpMV
+
+        if (broke || dead) {  // solver.py:516-524
+            rel = true_residual();
+            if (rel <= a.tol) {
+                converged = true;
+            } else {
+                status = RAFEM_ERR_BREAKDOWN;
+            }
+            break;
+        }
+    }
+    if (cta == 0 && tid == 0) write_result(a.res, total, cycles, hlen, rel, converged, latched && !converged, status);
+}
+
+// ---------------------------------------------------------------------------
+// GMRES(m) with a one-reduce Arnoldi step: classical Gram-Schmidt whose
+// second (reorthogonalising) pass over each basis vector is delayed into the
+// next step, so one fixed-order reduction serves both passes (the
+// low-synchronisation "DCGS2" Arnoldi).  Step k holds u_k, the candidate
+// for v_k after one projection against V_{k-1}, forms w_k = A M^-1 u_k and
+// reduces in ONE round
+//     a = V_{k-1}^T u_k,   u_k . u_k,   b = V_{k-1}^T w_k,   u_k . w_k.
+// With alpha = ||u_k - V_{k-1} a|| = sqrt(u.u - a.a) (an explicit norm
+// reduction when that difference cancels):
+//     v_k       = (u_k - V_{k-1} a) / alpha                (second pass)
+//     H[:, k-1] = first-pass coefficients + a,  H[k][k-1] = alpha
+//     u_{k+1}   = (w_k - V_{k-1} b - v_k g) / alpha,   g = (u.w - a.b) / alpha
+//     first pass of column k = ([b; g] - H[0:k+1, 0:k] a) / alpha
+// since A M^-1 v_k = (w_k - A M^-1 V_{k-1} a) / alpha and A M^-1 V_{k-1} =
+// V_k H.  Column k-1 becomes final — Givens rotation, residual estimate and
+// the reference's stop tests (solver.py:478-502) — one step after its SpMV,
+// so m columns cost m SpMVs, m + 1 reductions and m barriers (3m
+// synchronisations in gmres_body); on convergence one SpMV goes unused.
+// Grid mode with the basis rows in shared memory only.
+template <int W, bool PRE, class R>
+RF_DEV void gmres_1r_body(const KArgs& a, const R& rows, double* dyn) {
+    __shared__ double red[32 * 8];
+    __shared__ double sc[8];
+    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
+    const int g0 = a.gpart[cta], g1 = a.gpart[cta + 1];
+    const int lo = W * g0, hi = W * g1;
+    const int m = a.m;
+    const long long ld = m + 1;
+    double* H = dyn;  // rotated columns (back substitution), col-major ld x m
+    double* cs = H + ld * m;
+    double* sn = cs + m;
+    double* gg = sn + m;          // m + 1
+    double* yy = gg + m + 1;      // m
+    double* co = yy + m;          // 2m + 4
+    double* Hr = co + 2 * m + 4;  // raw Hessenberg columns, col-major ld x m
+    double* Hf = Hr + ld * m;     // first-pass coefficients of the open column (2 x ld, alternating)
+    double* gs = Hf + 2 * ld;     // 512: gather_wide scratch
+    const long long pstride = (long long)(2 * m + 4) * G;
+    int par = 0;
+    Sync<GridMode> sy{a};
+    double* const Vs = dyn + a.vs_off;
+    auto vrow = [&](int i) -> double* { return Vs + (long long)i * a.vs_ld - lo; };
+
+    const double bnorm = prologue<GridMode>(a, sy, lo, hi, co, red, par, pstride);
+    if (bnorm < 0.0) return;
+
+    auto true_residual = [&]() -> double {  // solver.py:438-439, 517-518
+        double v[1] = {0.0};
+        spmv_team<W>(rows, g0, g1, a.team, SrcPlain{a.x}, [&](int g, const double* y) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                const int e = W * g + w;
+                const double re = sub(a.b[e], y[w]);
+                a.r[e] = re;
+                v[0] = add(v[0], mul(re, re));
+            }
+        });
+        sy.template reduce<1>(v, 1, a.partial + par * pstride, co, red);
+        par ^= 1;
+        return sqrt(co[0]) / bnorm;
+    };
+
+    long long total = 0, cycles = 0, hlen = 0, nstep = 0;  // nstep: trace stamps
+    int weak = 0;
+    bool latched = false, have_prev = false, converged = false;
+    double prev_start = 0.0, rel = INFINITY;
+    int status = RAFEM_OK;
+    const double tiny = 2.2250738585072014e-308;  // np.finfo(float64).tiny
+
+    while (true) {
+        rel = true_residual();
+        if (have_prev) {  // stagnation bookkeeping (solver.py:440-447)
+            if (rel > (1.0 - 1e-3) * prev_start) {
+                if (++weak >= 3) latched = true;
+            } else {
+                weak = 0;
+            }
+            have_prev = false;
+        }
+        if (rel <= a.tol) {
+            converged = true;
+            break;
+        }
+        if (total >= a.cap) break;
+
+        const double cycle_start = rel;
+        const double beta = rel * bnorm;
+        if (tid == 0) {
+            for (int i = 0; i <= m; ++i) gg[i] = 0.0;
+            gg[0] = beta;
+        }
+        int used = 0;
+        bool broke = false, dead = false;
+        const long long hstart = hlen;
+        double alpha = beta;  // u_0 = r, v_0 = r / beta
+
+        for (int k = 0; k <= m; ++k) {
+            const double* u = k == 0 ? a.r : ((k & 1) ? a.w1 : a.w0);
+            double* wv = a.z;
+            const bool more = k < m;
+            stamp(a, nstep, 0);
+            if (more) {  // w_k = A (M^-1 u_k)   (solver.py:469-470)
+                spmv_team<W>(rows, g0, g1, a.team, SrcBasis<PRE>{u, 1.0, a.minv}, [&](int g, const double* y) {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) wv[W * g + w] = y[w];
+                });
+            }
+            __syncthreads();
+            stamp(a, nstep, 1);
+            double* P = a.partial + par * pstride;
+            multidot_pair_smem(Vs, a.vs_ld, k, u, more ? wv : nullptr, lo, hi, P, 2 * m + 4);
+            stamp(a, nstep, 2);
+            sy.barrier();
+            stamp(a, nstep, 3);
+            gather_wide(P, 2 * m + 4, more ? 2 * k + 2 : k + 1, G, co, gs);
+            __syncthreads();
+            par ^= 1;
+            if (k > 0) {  // alpha = ||u_k - V_{k-1} a||; identical decision on every CTA
+                double aa = 0.0;
+                for (int i = 0; i < k; ++i) aa = add(aa, mul(co[i], co[i]));
+                if (aa > 1e-8 * co[k]) {
+                    stamp(a, nstep, 7);
+                    double v[1] = {0.0};
+                    for (int e = lo + tid; e < hi; e += bd) {
+                        double s = 0.0;
+                        for (int i = 0; i < k; ++i) s = add(s, mul(co[i], vrow(i)[e]));
+                        const double d = sub(u[e], s);
+                        v[0] = add(v[0], mul(d, d));
+                    }
+                    sy.template reduce<1>(v, 1, a.partial + par * pstride, sc + 4, red);
+                    par ^= 1;
+                    alpha = sqrt(sc[4]);
+                } else {
+                    alpha = sqrt(fmax(sub(co[k], aa), 0.0));
+                }
+            }
+            stamp(a, nstep, 4);
+            // v_k (second pass) and u_{k+1} (first pass of the next vector)
+            // over the own rows; then, while the grid barrier that publishes
+            // u_{k+1} is in flight (split arrive / wait on the counter),
+            // warp 0 rotates column k-1 (Givens, solver.py:478-496) and warp 1
+            // stores column k-1's raw values and column k's first-pass
+            // coefficients.  The stop tests read warp 0's results after the
+            // wait (on convergence v_k / u_{k+1} go unused).
+            const int j = k - 1;
+            const double ialpha = 1.0 / alpha;
+            const int wid = tid >> 5, lane = tid & 31;
+            if (more) {
+                // four lanes per row, lane q taking basis rows i = q mod 4, and
+                // a quad butterfly ((q0 + q1) + (q2 + q3)); a . b rides along
+                double* un = ((k + 1) & 1) ? a.w1 : a.w0;
+                double* Vk = vrow(k);
+                const int q = tid & 3;
+                const int nrow = hi - lo;
+                for (int r0 = 0; r0 < nrow; r0 += bd >> 2) {
+                    const int r = r0 + (tid >> 2);
+                    const int e = lo + (r < nrow ? r : nrow - 1);
+                    double sa = 0.0, sb = 0.0, ab = 0.0;
+                    for (int i = q; i < k; i += 4) {
+                        const double vi = vrow(i)[e];
+                        const double ci = co[i], bi = co[k + 1 + i];
+                        sa = add(sa, mul(ci, vi));
+                        sb = add(sb, mul(bi, vi));
+                        ab = add(ab, mul(ci, bi));
+                    }
+                    sa = add(sa, __shfl_xor_sync(0xffffffffu, sa, 1));
+                    sb = add(sb, __shfl_xor_sync(0xffffffffu, sb, 1));
+                    ab = add(ab, __shfl_xor_sync(0xffffffffu, ab, 1));
+                    sa = add(sa, __shfl_xor_sync(0xffffffffu, sa, 2));
+                    sb = add(sb, __shfl_xor_sync(0xffffffffu, sb, 2));
+                    ab = add(ab, __shfl_xor_sync(0xffffffffu, ab, 2));
+                    if (q == 0 && r < nrow) {
+                        const double gam = mul(sub(co[2 * k + 1], ab), ialpha);
+                        const double vk = mul(sub(u[e], sa), ialpha);
+                        Vk[e] = vk;
+                        un[e] = mul(sub(sub(wv[e], sb), mul(vk, gam)), ialpha);
+                    }
+                }
+                __syncthreads();
+                ++sy.nbar;
+                if (tid == 0) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.gbar) : "memory");
+            }
+            stamp(a, nstep, 5);
+            if (wid == 0) {
+                if (k > 0 && lane == 0) {
+                    const double* __restrict__ hf = Hf + (j & 1) * ld;
+                    double* __restrict__ hc = H + (long long)j * ld;
+                    const double* __restrict__ cr = cs;
+                    const double* __restrict__ sr = sn;
+                    double hi = add(hf[0], co[0]);
+                    for (int i = 0; i < j; ++i) {
+                        const double hn = add(hf[i + 1], co[i + 1]);
+                        const double c = cr[i], sv = sr[i];
+                        hc[i] = add(mul(c, hi), mul(sv, hn));
+                        hi = add(mul(-sv, hi), mul(c, hn));
+                    }
+                    const double h1 = alpha;
+                    const double rad = hypot(hi, h1);
+                    double est = 0.0;
+                    int isdead = 0;
+                    if (rad == 0.0) {
+                        isdead = 1;
+                    } else {
+                        cs[j] = hi / rad;
+                        sn[j] = h1 / rad;
+                        hc[j] = rad;
+                        hc[j + 1] = 0.0;
+                        gg[j + 1] = mul(-sn[j], gg[j]);
+                        gg[j] = mul(cs[j], gg[j]);
+                        est = fabs(gg[j + 1]) / bnorm;
+                        if (cta == 0 && hlen < a.hist_cap) a.hist[hlen] = est;
+                    }
+                    sc[0] = isdead;
+                    sc[1] = est;
+                }
+            } else if (wid == 1) {
+                if (k > 0) {
+                    const double* hf = Hf + (j & 1) * ld;
+                    double* hr = Hr + (long long)j * ld;
+                    for (int i = lane; i <= k; i += 32) hr[i] = i < k ? add(hf[i], co[i]) : alpha;
+                    __syncwarp();
+                }
+                if (more) {
+                    double* hf = Hf + (k & 1) * ld;
+                    for (int i = lane; i <= k; i += 32) {
+                        double t = 0.0;
+                        for (int jj = i > 0 ? i - 1 : 0; jj < k; ++jj)
+                            t = add(t, mul(Hr[(long long)jj * ld + i], co[jj]));
+                        double bi;
+                        if (i < k) {
+                            bi = co[k + 1 + i];
+                        } else {  // g, summed as the sweep's quads do
+                            double ab4[4];
+                            for (int q = 0; q < 4; ++q) {
+                                ab4[q] = 0.0;
+                                for (int ii = q; ii < k; ii += 4) ab4[q] = add(ab4[q], mul(co[ii], co[k + 1 + ii]));
+                            }
+                            const double ab = add(add(ab4[0], ab4[1]), add(ab4[2], ab4[3]));
+                            bi = mul(sub(co[2 * k + 1], ab), ialpha);
+                        }
+                        hf[i] = mul(sub(bi, t), ialpha);
+                    }
+                }
+            }
+            if (more && tid == 0) {  // wait for every CTA's u_{k+1}
+                const unsigned long long target = sy.nbar * (unsigned long long)G;
+                long long spins = 0;
+                unsigned long long v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.gbar) : "memory");
+                    if (++spins > kSpinCap) asm volatile("trap;");
+                } while (v < target);
+            }
+            __syncthreads();
+            stamp(a, nstep, 6);
+            ++nstep;
+            if (k > 0) {
+                total += 1;
+                if (sc[0] != 0.0) {  // column added nothing (solver.py:483-487)
+                    dead = true;
+                    used = j;
+                    break;
+                }
+                used = j + 1;
+                const double est = sc[1];
+                ++hlen;
+                if (alpha < tiny) {  // breakdown (solver.py:497-499)
+                    broke = true;
+                    break;
+                }
+                if (est <= a.tol || total >= a.cap) break;
+            }
+            if (!more) break;
+        }
+
+        if (used > 0) {  // y = R^-1 g ; x += M^-1 (V y)   (solver.py:504-511)
+            if (tid == 0) {
+                for (int i = used - 1; i >= 0; --i) {
+                    double d = 0.0;
+                    for (int j = i + 1; j < used; ++j) d = add(d, mul(H[(long long)j * ld + i], yy[j]));
+                    yy[i] = sub(gg[i], d) / H[(long long)i * ld + i];
+                }
+            }
+            __syncthreads();
+            for (int e = lo + tid; e < hi; e += bd) {
+                double s = 0.0;
+                for (int i = 0; i < used; ++i) s = add(s, mul(vrow(i)[e], yy[i]));
+                if (PRE) s = mul(a.minv[e], s);
+                a.x[e] = add(a.x[e], s);
             }
         }
         if (cta == 0 && tid == 0 && cycles < a.cyc_cap) a.cyc[cycles] = hlen - hstart;
@@ -2471,7 +2856,9 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
         RF_CUDA_TRY(ctx, cudaMemsetAsync(x_dev, 0, sizeof(double) * n, ctx->stream));
     }
 
-    const long long hess_doubles = gm ? (long long)(m + 1) * m + 5LL * m + 4 : 0;
+    // rotated H, cs, sn, g, y, 2m + 4 reduction results, raw H, two
+    // first-pass columns and the gather scratch (gmres_1r_body)
+    const long long hess_doubles = gm ? 2LL * (m + 1) * m + 5LL * m + 5 + m + 2LL * (m + 1) + 512 : 0;
     const size_t hess_bytes = (size_t)hess_doubles * 8;
 
     // ---- choose the execution mode
@@ -2582,7 +2969,9 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
             hess_global = true;
         }
         fn = select_grid(gm, A.W, pre, ms);
-        if (smem > 48 * 1024)
+        // opt in whenever dynamic smem is used: without it static + dynamic
+        // must stay within 48 KB, which a dynamic size just under 48 KB breaks
+        if (smem > 0)
             RF_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ = 0;
         RF_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, KT, smem));
@@ -2596,7 +2985,7 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
         if (int rc = ensure(ctx, ctx->ws_basis, sizeof(double) * (size_t)(m + 1) * ldv)) return rc;
     }
     if (int rc = ensure(ctx, ctx->ws_vec, sizeof(double) * (size_t)10 * ldv)) return rc;
-    if (int rc = ensure(ctx, ctx->ws_partial, sizeof(double) * (size_t)2 * (std::max(m, 6) + 2) * G)) return rc;
+    if (int rc = ensure(ctx, ctx->ws_partial, sizeof(double) * (size_t)2 * (2 * std::max(m, 6) + 4) * G)) return rc;
     if (hess_global) {
         if (int rc = ensure(ctx, ctx->ws_hess, sizeof(double) * (size_t)hess_doubles * G)) return rc;
     }
@@ -2630,6 +3019,10 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     a.hess_smem = ((cluster || ms == 2) && gm) ? (hess_doubles + 1) / 2 * 2 : 0;  // keep the slice 16-B aligned
     a.vs_off = vs_off;
     a.vs_ld = vs_ld;
+    {
+        const char* c2 = getenv("RAFEM_GMRES_CGS2");  // the three-synchronisation CGS2 step
+        a.gm1r = (gm && vs_off && !cluster && threads == 512 && !(c2 && c2[0] == '1')) ? 1 : 0;
+    }
     a.m = m;
     a.tol = p.tolerance;
     a.cap = p.max_total_iters > 0 ? p.max_total_iters : 10LL * n;
@@ -2649,6 +3042,8 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
         a.flags = static_cast<unsigned long long*>(ctx->ws_flags.p);
         a.epoch = ctx->epoch;
         a.gbar = grid_counter(ctx, a.flags, G);
+        // the one-reduce GMRES splits its per-step barrier (arrive / wait) on the counter
+        if (!a.gbar && a.gm1r) a.gbar = a.flags + 2 * 8 * (size_t)std::max(G, 1);
         if (a.gbar) RF_CUDA_TRY(ctx, cudaMemsetAsync(a.gbar, 0, sizeof(unsigned long long), ctx->stream));
     }
     if (ctx->trace_on) {
