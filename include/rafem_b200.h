@@ -212,6 +212,12 @@ void rafem_system_destroy(rafem_system* sys);
 int rafem_assemble(rafem_system* sys, const double* t_iter, const double* v_iter,
                    const double* t_prev, const rafem_assemble_params* p, double* scale_out,
                    int64_t* bad_element);
+/* rafem_assemble that also returns the rhs (2N, host) from the same
+ * stream synchronisation (the plug-in seam reads it on every pass,
+ * fem.py:495); rhs_out may be NULL. */
+int rafem_assemble_rhs(rafem_system* sys, const double* t_iter, const double* v_iter,
+                       const double* t_prev, const rafem_assemble_params* p, double* scale_out,
+                       int64_t* bad_element, double* rhs_out);
 /* dof-order values (2*slots, CsrMatrix.vals order) and rhs (2N) to host */
 int rafem_system_download(rafem_system* sys, double* vals_out, double* rhs_out);
 /* solve the device-resident system; b == NULL uses the assembled rhs */

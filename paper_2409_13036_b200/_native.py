@@ -98,6 +98,7 @@ _SIGS = {
     "rafem_system_create": (i32, [vp, P(vp)]),
     "rafem_system_destroy": (None, [vp]),
     "rafem_assemble": (i32, [vp, vp, vp, vp, P(AssembleParams), P(f64), P(i64)]),
+    "rafem_assemble_rhs": (i32, [vp, vp, vp, vp, P(AssembleParams), P(f64), P(i64), vp]),
     "rafem_system_download": (i32, [vp, vp, vp]),
     "rafem_system_solve": (i32, [vp, vp, vp, P(SolverParams), vp, P(SolveStatsC), vp, i64, vp, i64]),
     "rafem_system_spmv": (i32, [vp, vp, vp]),

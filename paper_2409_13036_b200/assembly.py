@@ -399,8 +399,11 @@ def assemble_global(mesh, material, config, t_iter, v_iter, t_prev, dt, apply_co
     p.equilibrate = 1 if equilibrate else 0
     scale = C.c_double()
     bad = C.c_int64(-1)
-    rc = nat.lib().rafem_assemble(h.handle, nat.ptr(t_iter), nat.ptr(v_iter), nat.ptr(t_prev),
-                                  C.byref(p), C.byref(scale), C.byref(bad))
+    # the rhs comes back with the same stream synchronisation: every caller
+    # of assemble_global reads it (fem.py:495)
+    rhs = np.empty(2 * n)
+    rc = nat.lib().rafem_assemble_rhs(h.handle, nat.ptr(t_iter), nat.ptr(v_iter), nat.ptr(t_prev),
+                                      C.byref(p), C.byref(scale), C.byref(bad), nat.ptr(rhs))
     if rc == nat.ERR_PHYSICS:
         e = int(bad.value)
         tets = mesh.tets[e]
@@ -411,4 +414,5 @@ def assemble_global(mesh, material, config, t_iter, v_iter, t_prev, dt, apply_co
             f"sigma(T) = {sigma:.3g} S/mm <= 0 in element {e} (mean T {tbar:.3g})")
     nat.check(rc, "assemble")
     h.scale = float(scale.value)
+    h._rhs = rhs
     return AssembledSystem(h)

@@ -170,37 +170,83 @@ struct SysStatus {
 SysStatus* sys_status(rafem_system* s) { return reinterpret_cast<SysStatus*>(s->status); }
 
 // solve on a matrix view with host b/x0/x; shared by system and matrix paths
+// RAFEM_HOST_TIMING=1: per-phase host microseconds of each solve to stderr
+static double host_us() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 int solve_common(rafem_ctx* ctx, const MatView& A, double* b_dev, bool b_is_host, const double* b,
                  const double* x0, const rafem_solver_params* p, double* x_out, rafem_solve_stats* st,
                  double* hist, int64_t hist_cap, int64_t* cycle_lens, int64_t cycle_cap, double* minv,
                  double* xbuf, SysStatus* dstat) {
     const int n = A.ngroups * A.W;
+    static const bool timing = [] { const char* e = getenv("RAFEM_HOST_TIMING"); return e && e[0] == '1'; }();
+    const double t0 = timing ? host_us() : 0.0;
     if (int rc = check_params(ctx, p)) return rc;
-    if (b_is_host && b) {
-        if (int rc = upload(ctx, b_dev, b, sizeof(double) * n)) return rc;
+    // one pinned staging area and one stream synchronisation per solve:
+    // [b | x0 | x out | KResult | history head | cycle-length head]
+    constexpr long long kHistHead = 4096, kCycHead = 512;
+    const size_t nb = sizeof(double) * (size_t)n;
+    char* pin = static_cast<char*>(pinned(ctx, 3 * nb + sizeof(KResult) + 8 * (kHistHead + kCycHead)));
+    if (!pin) return rafem_fail(ctx, RAFEM_ERR_CUDA, "pinned staging allocation failed");
+    double* pb = reinterpret_cast<double*>(pin);
+    double* px0 = pb + n;
+    double* px = px0 + n;
+    KResult* pr = reinterpret_cast<KResult*>(px + n);
+    double* ph = reinterpret_cast<double*>(pr + 1);
+    long long* pc = reinterpret_cast<long long*>(ph + kHistHead);
+    if (b_is_host && b && n > 0) {
+        std::memcpy(pb, b, nb);
+        if (int rc = upload(ctx, b_dev, pb, nb)) return rc;
     }
     const double* x0_dev = nullptr;
     if (x0) {
-        if (int rc = upload(ctx, xbuf, x0, sizeof(double) * n)) return rc;
+        if (n > 0) {
+            std::memcpy(px0, x0, nb);
+            if (int rc = upload(ctx, xbuf, px0, nb)) return rc;
+        }
         x0_dev = xbuf;
     }
+    const double t1 = timing ? host_us() : 0.0;
     int* flag = &dstat->flag;
     if (p->precondition != RAFEM_PRECOND_NONE) {
         if (int rc = jacobi_minv(ctx, A, minv, flag)) return rc;
     } else {
         RF_CUDA_TRY(ctx, cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
     }
+    const double t2 = timing ? host_us() : 0.0;
     if (int rc = krylov_solve(ctx, A, b_dev, x0_dev, xbuf, minv, *p, &dstat->pass.solve, flag, ctx->ev0, ctx->ev1))
         return rc;
-    KResult r;
-    RF_CUDA_TRY(ctx, cudaMemcpyAsync(&r, &dstat->pass.solve, sizeof(r), cudaMemcpyDeviceToHost, ctx->stream));
-    RF_CUDA_TRY(ctx, cudaMemcpyAsync(x_out, xbuf, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    const double t3 = timing ? host_us() : 0.0;
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(pr, &dstat->pass.solve, sizeof(KResult), cudaMemcpyDeviceToHost, ctx->stream));
+    if (n > 0) RF_CUDA_TRY(ctx, cudaMemcpyAsync(px, xbuf, nb, cudaMemcpyDeviceToHost, ctx->stream));
+    // the heads of the residual history and the cycle lengths ride along
+    const long long hh = std::min<long long>(kHistHead, (long long)(ctx->ws_hist.bytes / sizeof(double)));
+    const long long ch = std::min<long long>(kCycHead, (long long)(ctx->ws_cyc.bytes / sizeof(long long)));
+    if (hist && hist_cap > 0 && hh > 0)
+        RF_CUDA_TRY(ctx, cudaMemcpyAsync(ph, ctx->ws_hist.p, sizeof(double) * hh, cudaMemcpyDeviceToHost, ctx->stream));
+    if (cycle_lens && cycle_cap > 0 && ch > 0)
+        RF_CUDA_TRY(ctx, cudaMemcpyAsync(pc, ctx->ws_cyc.p, sizeof(long long) * ch, cudaMemcpyDeviceToHost, ctx->stream));
+    const double t4 = timing ? host_us() : 0.0;
     RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    const double t5 = timing ? host_us() : 0.0;
+    const KResult r = *pr;
+    if (n > 0) std::memcpy(x_out, px, nb);
+    if (timing)
+        std::fprintf(stderr, "solve host us: uploads %.1f, jacobi %.1f, krylov_solve %.1f, d2h enqueue %.1f, sync %.1f\n",
+                     t1 - t0, t2 - t1, t3 - t2, t4 - t3, t5 - t4);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
     if (st) fill_stats(r, ms, st);
-    if (int rc = krylov_read_history(ctx, r, hist, hist_cap, reinterpret_cast<long long*>(cycle_lens), cycle_cap))
+    const long long nh = std::min<long long>(r.hist_len, hist ? hist_cap : 0);
+    const long long nc = std::min<long long>(r.cycles, cycle_lens ? cycle_cap : 0);
+    if (nh <= hh && nc <= ch) {
+        if (nh > 0) std::memcpy(hist, ph, sizeof(double) * nh);
+        if (nc > 0) std::memcpy(cycle_lens, pc, sizeof(long long) * nc);
+    } else if (int rc = krylov_read_history(ctx, r, hist, hist_cap, reinterpret_cast<long long*>(cycle_lens),
+                                            cycle_cap)) {
         return rc;
+    }
     if (r.status == RAFEM_ERR_INVALID)
         return rafem_fail(ctx, RAFEM_ERR_INVALID, "Jacobi preconditioning requires a zero-free diagonal");
     if (r.status == RAFEM_ERR_BREAKDOWN) {
@@ -576,12 +622,20 @@ void rafem_system_destroy(rafem_system* s) {
 
 int rafem_assemble(rafem_system* s, const double* t_iter, const double* v_iter, const double* t_prev,
                    const rafem_assemble_params* p, double* scale_out, int64_t* bad_element) {
+    return rafem_assemble_rhs(s, t_iter, v_iter, t_prev, p, scale_out, bad_element, nullptr);
+}
+
+int rafem_assemble_rhs(rafem_system* s, const double* t_iter, const double* v_iter, const double* t_prev,
+                       const rafem_assemble_params* p, double* scale_out, int64_t* bad_element, double* rhs_out) {
     if (!s || !p) return RAFEM_ERR_INVALID;
     rafem_mesh* m = s->mesh;
     rafem_ctx* ctx = m->ctx;
     if (!(p->dt > 0.0)) return rafem_fail(ctx, RAFEM_ERR_INVALID, "dt must be positive");
     const int N = m->N;
-    double* pin = static_cast<double*>(pinned(ctx, sizeof(double) * 3 * (size_t)std::max(N, 1)));
+    // pinned staging: [t_iter | v_iter | t_prev] in, [rhs (2N) | PassStatus] out
+    const size_t in_b = sizeof(double) * 3 * (size_t)std::max(N, 1);
+    const size_t rhs_b = sizeof(double) * 2 * (size_t)N;
+    double* pin = static_cast<double*>(pinned(ctx, in_b + rhs_b + sizeof(PassStatus)));
     if (!pin) return rafem_fail(ctx, RAFEM_ERR_CUDA, "pinned staging allocation failed");
     std::memcpy(pin, t_iter, sizeof(double) * N);
     std::memcpy(pin + N, v_iter, sizeof(double) * N);
@@ -591,9 +645,13 @@ int rafem_assemble(rafem_system* s, const double* t_iter, const double* v_iter, 
     if (int rc = assemble_launch(s, s->xin, 1, s->xin + N, 1, s->xin + 2 * (size_t)N, 1, *p, &ds->pass.scale,
                                  &ds->pass.bad_element))
         return rc;
-    PassStatus hs;
-    RF_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, &ds->pass, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+    double* prhs = pin + in_b / sizeof(double);
+    PassStatus* phs = reinterpret_cast<PassStatus*>(reinterpret_cast<char*>(pin) + in_b + rhs_b);
+    if (rhs_out && N > 0) RF_CUDA_TRY(ctx, cudaMemcpyAsync(prhs, s->rhs, rhs_b, cudaMemcpyDeviceToHost, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(phs, &ds->pass, sizeof(PassStatus), cudaMemcpyDeviceToHost, ctx->stream));
     RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    const PassStatus hs = *phs;
+    if (rhs_out && N > 0) std::memcpy(rhs_out, prhs, rhs_b);
     s->scale = hs.scale;
     if (scale_out) *scale_out = hs.scale;
     if (bad_element) *bad_element = hs.bad_element;

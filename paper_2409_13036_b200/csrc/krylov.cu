@@ -37,6 +37,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <chrono>
 #include <cstdlib>
 #include <vector>
 
@@ -2861,13 +2862,20 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     const long long hess_doubles = gm ? 2LL * (m + 1) * m + 5LL * m + 5 + m + 2LL * (m + 1) + 512 : 0;
     const size_t hess_bytes = (size_t)hess_doubles * 8;
 
+    static const bool timing = [] { const char* e = getenv("RAFEM_HOST_TIMING"); return e && e[0] == '1'; }();
+    auto now_us = [] {
+        return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
+    const double k0 = timing ? now_us() : 0.0;
     // ---- choose the execution mode
     // paper-scale PCG and GMRES: the cluster-resident engine (cluster.cu)
     // when the system fits one cluster's shared memory
     {
         const int crc = cluster_pcg_solve(ctx, A, b_dev, x_dev, minv_dev, p, res_dev, flag_dev, ev_start, ev_stop);
+        if (timing && crc != RAFEM_ERR_UNSUPPORTED) std::fprintf(stderr, "  cluster engine %.1f us\n", now_us() - k0);
         if (crc != RAFEM_ERR_UNSUPPORTED) return crc;
     }
+    const double k1 = timing ? now_us() : 0.0;
     const void* fn = nullptr;
     size_t smem = 0;
     bool cluster = false, hess_global = false;
@@ -2979,6 +2987,7 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
         if (G > occ * ctx->sm_count) return rafem_fail(ctx, RAFEM_ERR_INVALID, "grid_ctas exceeds co-resident CTAs");
     }
 
+    const double k2 = timing ? now_us() : 0.0;
     // ---- workspace
     const long long ldv = ((long long)n + 31) / 32 * 32;
     if (gm) {
@@ -3074,6 +3083,7 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
         ctx->last_precond = a.block ? RAFEM_PRECOND_BLOCK_JACOBI : (pre ? RAFEM_PRECOND_JACOBI : RAFEM_PRECOND_NONE);
     }
     if (cluster) smem = (size_t)a.hess_smem * 8 + part.max_slice;
+    const double k3 = timing ? now_us() : 0.0;
     void* args[] = {&a};
     void* sargs[] = {&a, &stream_buf, &stream_valcap};
     if (ev_start) RF_CUDA_TRY(ctx, cudaEventRecord(ev_start, ctx->stream));
@@ -3100,6 +3110,9 @@ int krylov_solve(rafem_ctx* ctx, const MatView& A, const double* b_dev, const do
     if (ev_stop) RF_CUDA_TRY(ctx, cudaEventRecord(ev_stop, ctx->stream));
     ctx->last_ctas = G;
     ctx->launches++;
+    if (timing)
+        std::fprintf(stderr, "  krylov_solve: cluster attempt %.1f, mode %.1f, workspace + args %.1f, launch %.1f us\n",
+                     k1 - k0, k2 - k1, k3 - k2, now_us() - k3);
     return RAFEM_OK;
 }
 
@@ -3301,7 +3314,7 @@ int simulate_fused(rafem_system* s, const rafem_sim_params* p, SimDevOut* out, d
     {
         // Galerkin solver start (pipelined PCG with staged contributions, whose
         // scratch holds the (2k + 1) x 2 rows-per-CTA doubles it needs)
-        int K = 10;  // window (measured on the mesh-B run: 8 26.3, 10 23.1, 12 23.2, 14 23.6, 16 24.4 ms)
+        int K = 14;  // window (mesh-B run, r2d: 10 22.34, 12 22.23, 14 22.00, 16 22.06 ms; r2c before the CTA-wide solve: 8 26.3, 10 23.1, 12 23.2, 14 23.6, 16 24.4)
         if (const char* ge = getenv("RAFEM_GALERKIN_K")) K = std::max(0, std::min(kGalMax, atoi(ge)));
         if (!(stage_fill == 2 && fn == fn_lean) || !pipe) K = 0;
         if (K > 0 && gal_scratch_min < (size_t)(2 * K + 1) * 2 * part.max_groups) K = 0;

@@ -69,7 +69,7 @@ constexpr int kGalMax = 16;  // largest Galerkin window
 // without the components the last passes already resolved.  Everything is
 // on the CTA's own rows and its shared-memory matrix slice: 1 + nv slice
 // products (x0 and the d_j, gathered from L2), nv (nv + 3) / 2 dots in one
-// reduction, a scaled pivot-thresholded Cholesky of the nv x nv system on
+// reduction, a scaled pivot-thresholded Gauss-Jordan solve of the nv x nv system on
 // every CTA (identical bits everywhere: the reduction is fixed-order), the
 // update of x0 and a barrier.  CPU study (scripts/galerkin_x0_probe.py,
 // the 900 s mesh-B run, block-Jacobi PCG): 4,655 -> 2,997 (nv = 8) and
@@ -87,6 +87,24 @@ RF_DEV void galerkin_start(const KArgs& a, const R& rows, Sync<Mode>& sy, const 
     double* sD = scr + nd;               // d_j (own dofs), j < nv
     double* sAD = sD + (size_t)nv * nd;  // A d_j
     auto dvec = [&](int j) { return D + (size_t)((head - 1 - j + 2 * K) % K) * n2; };  // most recent first
+    // RAFEM trace on: phase clocks of the last start (CTA 0) at trace[8 * 4000 + k]
+#define GAL_STAMP(k) \
+    if (a.trace && cta == 0 && tid == 0 && 8 * 4000 + (k) < a.trace_cap) a.trace[8 * 4000 + (k)] = clock64()
+    GAL_STAMP(0);
+    const long long gal_t0 = clock64();
+    // the d_j rows (own dofs) stream into shared memory while the products run
+    if (!(nd & 1)) {
+        const int h = nd >> 1;
+        for (int q = tid; q < nv * h; q += blockDim.x) {
+            const int j = q / h, e2 = q - j * h;
+            cp_async16(sD + (size_t)j * nd + 2 * e2, dvec(j) + lo + 2 * e2);
+        }
+    } else {
+        for (int q = tid; q < nv * nd; q += blockDim.x) {
+            const int j = q / nd, e = q - j * nd;
+            cp_async8(sD + q, dvec(j) + lo + e);
+        }
+    }
     // products of the slice with x0 and the d_j, six sources per sweep (a
     // team of lanes per row; a lane's slots and all their gathers issued
     // before the first accumulation, so a sweep is one L2 round trip)
@@ -151,23 +169,25 @@ RF_DEV void galerkin_start(const KArgs& a, const R& rows, Sync<Mode>& sy, const 
             }
         }
     }
-    for (int q = tid; q < nv * nd; q += blockDim.x) {  // all the d_j rows at once
-        const int j = q / nd, e = q - j * nd;
-        sD[q] = __ldcg(dvec(j) + lo + e);
-    }
+    GAL_STAMP(1);
+    cp_async_wait_all();
     __syncthreads();
-    // coefficient c: g_i (c < nv), then M_ij (i <= j) row by row; a thread
-    // each, two fixed interleaved partial sums over the own dofs
+    GAL_STAMP(2);
+    // coefficient c: g_i (c < nv), then M_ij (i <= j) row by row; four
+    // lanes each over quarters of the own dofs (two interleaved partial sums
+    // per lane), then ((q0 + q1) + (q2 + q3))
     const int nvals = nv + nv * (nv + 1) / 2;
-    for (int c = tid; c < ((skip & 2) ? 0 : nvals); c += blockDim.x) {
-        int i, j;
+    const int nq = ((nd >> 1) + 3) >> 2;  // dof pairs per quarter
+    for (int c0 = 0; c0 < ((skip & 2) ? 0 : nvals); c0 += blockDim.x >> 2) {
+        const int c = c0 + (tid >> 2), qd = tid & 3;
+        int i = 0, j;
         const double* u;
-        if (c < nv) {
-            i = c;
+        const int cc = c < nvals ? c : nvals - 1;  // the quad's shuffles need every lane
+        if (cc < nv) {
+            i = cc;
             u = sR;
         } else {
-            int q = c - nv;
-            i = 0;
+            int q = cc - nv;
             while (q >= nv - i) {
                 q -= nv - i;
                 ++i;
@@ -178,23 +198,29 @@ RF_DEV void galerkin_start(const KArgs& a, const R& rows, Sync<Mode>& sy, const 
         // (shared-space loads: the scratch pointer arrives as a generic one)
         const unsigned dis = smem_u32(sD + (size_t)i * nd), us = smem_u32(u);
         double a0 = 0.0, a1 = 0.0;
-        int e = 0;
-        for (; e + 2 <= nd; e += 2) {
+        const int e0 = 2 * qd * nq, e1 = min(nd & ~1, e0 + 2 * nq);
+        for (int e = e0; e < e1; e += 2) {
             double d0, d1, u0, u1;
             asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(d0), "=d"(d1) : "r"(dis + 8u * e));
             asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(u0), "=d"(u1) : "r"(us + 8u * e));
             a0 = fma(d0, u0, a0);
             a1 = fma(d1, u1, a1);
         }
-        if (e < nd) {
+        if (qd == 3 && (nd & 1)) {
             double d0, u0;
-            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(d0) : "r"(dis + 8u * e));
-            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(u0) : "r"(us + 8u * e));
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(d0) : "r"(dis + 8u * (nd - 1)));
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(u0) : "r"(us + 8u * (nd - 1)));
             a0 = fma(d0, u0, a0);
         }
-        P[(long long)c * G + cta] = a0 + a1;
+        double sq = a0 + a1;
+        sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+        sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+        if (qd == 0 && c < nvals) P[(long long)c * G + cta] = sq;
     }
+    GAL_STAMP(3);
+    if (a.trace && tid == 0 && 8 * 4002 + cta < a.trace_cap) a.trace[8 * 4002 + cta] = clock64() - gal_t0;
     sy.barrier();
+    GAL_STAMP(4);
     // two-level gather: CTA c folds coefficient c (c, c + G, ...) over the G
     // partials in CTA order, a barrier, every CTA reads the nvals totals
     double* T = P + (long long)nvals * G;
@@ -203,14 +229,22 @@ RF_DEV void galerkin_start(const KArgs& a, const R& rows, Sync<Mode>& sy, const 
             const double s = reduce_partials_warp(P + (long long)c * G, G);
             if (lane == 0) T[c] = s;
         }
+    GAL_STAMP(5);
     sy.barrier();
+    GAL_STAMP(6);
     for (int c = tid; c < nvals; c += blockDim.x) gco[c] = __ldcg(T + c);
     __syncthreads();
-    // scaled Cholesky with a pivot threshold (dependent directions drop out)
-    // and the two triangular solves, right-looking on warp 0 in shared memory
+    GAL_STAMP(7);
+    // the scaled system with a pivot threshold (dependent directions drop
+    // out), solved by Gauss-Jordan with the whole CTA: thread = entry (i, k)
+    // of the augmented matrix [S M S | S g], one barrier per pivot, the
+    // pivots being Cholesky's Schur complements; a pivot <= 1e-10 is
+    // skipped and its coefficient is 0, as a dropped Cholesky column gives.
+    // (On warp 0 alone the elimination's registers spilled next to the
+    // solver state: 8 us per start.)
     __shared__ double Ms[kGalMax][kGalMax + 1];
-    __shared__ double cf[kGalMax], sc[kGalMax], rl[kGalMax];
-    if (warp == 0 && !(skip & 8)) {
+    __shared__ double cf[kGalMax], sc[kGalMax];
+    if (!(skip & 8)) {
         auto Mij = [&](int i, int j) {  // M packed after g in gco: row i holds j = i..nv-1
             if (i > j) {
                 const int t = i;
@@ -219,49 +253,32 @@ RF_DEV void galerkin_start(const KArgs& a, const R& rows, Sync<Mode>& sy, const 
             }
             return gco[nv + i * nv - (i * (i - 1)) / 2 + (j - i)];
         };
-        if (lane < nv) {
-            const double m = Mij(lane, lane);
-            sc[lane] = m > 0.0 ? 1.0 / sqrt(m) : 0.0;
+        if (tid < nv) {
+            const double m = Mij(tid, tid);
+            sc[tid] = m > 0.0 ? rsqrt(m) : 0.0;
         }
-        __syncwarp();
-        for (int q = lane; q < nv * nv; q += 32) {
-            const int i = q / nv, j = q - i * nv;
-            Ms[i][j] = Mij(i, j) * sc[i] * sc[j];
-        }
-        __syncwarp();
+        __syncthreads();
+        const int w = nv + 1, ne = nv * w, bd = blockDim.x;
+        const int i0 = tid < ne ? tid / w : -1, k0 = tid < ne ? tid - i0 * w : -1;
+        const int i1 = tid + bd < ne ? (tid + bd) / w : -1, k1 = tid + bd < ne ? tid + bd - i1 * w : -1;
+        if (i0 >= 0) Ms[i0][k0] = k0 < nv ? Mij(i0, k0) * sc[i0] * sc[k0] : gco[i0] * sc[i0];
+        if (i1 >= 0) Ms[i1][k1] = k1 < nv ? Mij(i1, k1) * sc[i1] * sc[k1] : gco[i1] * sc[i1];
+        __syncthreads();
         unsigned ac = 0;
         for (int j = 0; j < nv; ++j) {
             const double d = Ms[j][j];
-            const bool ok = sc[j] > 0.0 && d > 1e-10;
-            const double r = ok ? 1.0 / sqrt(d) : 0.0;  // 1 / L_jj
-            if (ok) ac |= 1u << j;
-            if (lane == j) rl[j] = r;
-            if (lane > j && lane < nv) Ms[lane][j] *= r;  // column j of L
-            __syncwarp();
-            {  // trailing lower triangle: lane = column, rows below it
-                const int col = j + 1 + lane;
-                if (col < nv) {
-                    const double lcj = Ms[col][j];
-                    for (int row = col; row < nv; ++row) Ms[row][col] = fma(-Ms[row][j], lcj, Ms[row][col]);
-                }
+            if (sc[j] > 0.0 && d > 1e-10) {  // the same decision in every thread
+                ac |= 1u << j;
+                const double r = 1.0 / d;
+                if (i0 >= 0 && i0 != j && k0 > j) Ms[i0][k0] = fma(-Ms[i0][j] * r, Ms[j][k0], Ms[i0][k0]);
+                if (i1 >= 0 && i1 != j && k1 > j) Ms[i1][k1] = fma(-Ms[i1][j] * r, Ms[j][k1], Ms[i1][k1]);
             }
-            __syncwarp();
+            __syncthreads();
         }
-        // L y = S g: lane i holds y_i; L^T z = y; c = S z
-        double y = lane < nv ? gco[lane] * sc[lane] : 0.0;
-        for (int j = 0; j < nv; ++j) {
-            const double yj = __shfl_sync(0xffffffffu, y, j) * rl[j];
-            if (lane == j) y = yj;
-            if (lane > j && lane < nv) y = fma(-Ms[lane][j], yj, y);
-        }
-        for (int j = nv - 1; j >= 0; --j) {
-            const double zj = __shfl_sync(0xffffffffu, y, j) * rl[j];
-            if (lane == j) y = zj;
-            if (lane < j) y = fma(-Ms[j][lane], zj, y);
-        }
-        if (lane < nv) cf[lane] = (ac >> lane & 1u) ? y * sc[lane] : 0.0;
+        if (tid < nv) cf[tid] = (ac >> tid & 1u) ? Ms[tid][nv] / Ms[tid][tid] * sc[tid] : 0.0;
     }
     __syncthreads();
+    GAL_STAMP(8);
     // x0 += D c on the own rows and, exactly, r0 -= (A D) c: the solver's first
     // head takes r from sR (no product, so no barrier for the new x here)
     for (int e = tid; e < nd; e += blockDim.x) {
@@ -274,6 +291,8 @@ RF_DEV void galerkin_start(const KArgs& a, const R& rows, Sync<Mode>& sy, const 
         sR[e] = rr;
     }
     __syncthreads();
+    GAL_STAMP(9);
+#undef GAL_STAMP
 }
 
 // Max over CTAs of one nonnegative value (exact, order independent).
@@ -678,7 +697,10 @@ __global__ void __launch_bounds__(NT, 1) simulate_kernel(SimArgs S) {
                     if (S.gal_k > 0 && gal_n > 0 && cst && (it == 1 || !(S.gal_dbg & 16))) {
                         // (X(inew) holds the start on every CTA's own rows; the
                         // constraints' writes of the rhs are visible after the bar.sync)
-                        galerkin_start<GridMode>(kk, rows, sy, S.rhs, x0_new ? X(inew) : X(iit), X(inew), S.gal_d,
+                        KArgs kg = kk;  // the start's phase clocks (trace on) past the per-pass stamps
+                        kg.trace = S.ptrace;
+                        kg.trace_cap = S.ptrace ? (int)S.ptrace_cap : 0;
+                        galerkin_start<GridMode>(kg, rows, sy, S.rhs, x0_new ? X(inew) : X(iit), X(inew), S.gal_d,
                                                  n2, S.gal_k, gal_head, gal_n, reinterpret_cast<double*>(cst),
                                                  a.partial + 16LL * G, gco, S.gal_dbg);
                         gal = true;

@@ -163,14 +163,25 @@ def _params(cfg, method: int) -> nat.SolverParams:
     return p
 
 
+_HIST_BUF: list = [np.empty(0), np.empty(0, dtype=np.int64)]
+
+
+def _history_buffers(cap):
+    """Reused host buffers for the residual history and the cycle lengths
+    (their contents are copied into Python lists before a solve returns)."""
+    if _HIST_BUF[0].size < cap:
+        _HIST_BUF[0] = np.empty(cap)
+        _HIST_BUF[1] = np.empty(cap, dtype=np.int64)
+    return _HIST_BUF[0][:cap], _HIST_BUF[1][:cap]
+
+
 def _device_solve(a, b, x0, cfg, method):
     n = a.nrows
     x = np.empty(n)
     st = nat.SolveStatsC()
     cap = int(cfg.max_total_iters) if cfg.max_total_iters is not None else 10 * n
     hist_cap = min(cap, 1 << 20) + 1
-    hist = np.empty(hist_cap)
-    cyc = np.empty(hist_cap, dtype=np.int64)
+    hist, cyc = _history_buffers(hist_cap)
     p = _params(cfg, method)
     L = nat.lib()
     if isinstance(a, DeviceCsrMatrix):

@@ -14,13 +14,24 @@ L.rafem_set_trace(ctx, 0)
 tr = np.zeros(8 * 4096, dtype=np.int64)
 L.rafem_get_trace(ctx, tr.ctypes.data, tr.size)
 tr = tr.reshape(-1, 8)[: int(out.passes)].astype(float)
-ok = tr[:, 6] > 0
-print("passes", out.passes, "with galerkin", ok.sum())
-print("galerkin us: mean", np.mean((tr[ok, 6] - tr[ok, 4]) / 1e3), "median", np.median((tr[ok, 6] - tr[ok, 4]) / 1e3))
-print("pcg after galerkin us mean", np.mean((tr[ok, 5] - tr[ok, 6]) / 1e3), "its", tr[ok, 7].mean())
-print("pass total us mean", np.mean(np.diff(tr[:, 0])) / 1e3)
-d = tr_all = np.zeros(8 * 4096, dtype=np.int64)
+# per-pass stamps (globaltimer ns): 0 pass start, 1 after the first-pass
+# barrier, 2 element phase done, 3 fill + constraints done, 4 solve start,
+# 5 PCG done, 6 delta done; slot 7 = PCG iterations
+print("passes", out.passes, "PCG iterations", int(tr[:, 7].sum()))
+ph = ["barrier (first pass)", "element phase", "fill + constraints", "to solve start", "solve (Galerkin + PCG)",
+      "delta"]
+for k, nm in enumerate(ph):
+    print(f"  {nm:24s} {np.mean(tr[:, k + 1] - tr[:, k]) / 1e3:7.2f} us/pass")
+print(f"  {'pass total':24s} {np.mean(np.diff(tr[:, 0])) / 1e3:7.2f} us/pass, {tr[:, 7].mean():.2f} PCG its/pass")
+d = np.zeros(8 * 4096, dtype=np.int64)
 L.rafem_get_trace(ctx, d.ctypes.data, d.size)
-g = d[8 * 4000: 8 * 4000 + 8].astype(float)
-print("last galerkin phases (us): spmv", (g[1] - g[0]) / 1e3, "stage D", (g[2] - g[1]) / 1e3, "dots", (g[3] - g[2]) / 1e3,
-      "barrier", (g[4] - g[3]) / 1e3, "c0 loop entry", (g[6] - g[2]) / 1e3, "c0 dot done", (g[7] - g[2]) / 1e3, "gather", (g[5] - g[4]) / 1e3, "x", 0)
+g = d[8 * 4000: 8 * 4000 + 10].astype(float) / 1.965e3
+names = ["products (2 sweeps)", "stage D", "dots", "barrier", "fold", "barrier", "read totals",
+         "Cholesky + solves", "x0, r0 update"]
+print("last Galerkin start, CTA 0 (us):")
+for k, nm in enumerate(names):
+    print(f"  {nm:22s} {g[k + 1] - g[k]:6.2f}")
+print(f"  {'total':22s} {g[9] - g[0]:6.2f}")
+per = d[8 * 4002: 8 * 4002 + 148].astype(float) / 1.965e3
+print("per-CTA start -> dots done (us): min %.2f median %.2f max %.2f (cta %d)" % (per.min(), np.median(per), per.max(), per.argmax()))
+print("slowest CTAs:", np.argsort(per)[-8:], np.sort(per)[-8:].round(2))
