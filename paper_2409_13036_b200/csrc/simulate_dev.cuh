@@ -60,6 +60,12 @@ struct SimArgs {
 };
 
 constexpr int kGalMax = 16;  // largest Galerkin window
+#ifndef GAL_NQ
+#define GAL_NQ 3  // Galerkin products: sources per sweep (r2e sweep: 6x4 21.98 ms, 3x7 20.93, 5x5 22.05, 2x14 23.27 per run;
+#endif
+#ifndef GAL_SL
+#define GAL_SL 7  // Galerkin products: slots per lane in flight (3x7 is the one without spills in the lean kernel)
+#endif
 
 // Galerkin start of a pass's solve (the native loop's own choice of x0; the
 // plug-in seam keeps the reference's x0): with D the nv most recent
@@ -108,7 +114,7 @@ RF_DEV void galerkin_start(const KArgs& a, const R& rows, Sync<Mode>& sy, const 
     // products of the slice with x0 and the d_j, six sources per sweep (a
     // team of lanes per row; a lane's slots and all their gathers issued
     // before the first accumulation, so a sweep is one L2 round trip)
-    constexpr int NQ = 6, SL = 4;  // sources per sweep, slots per lane in flight
+    constexpr int NQ = GAL_NQ, SL = GAL_SL;  // sources per sweep, slots per lane in flight
     for (int q0 = -1; q0 < ((skip & 1) ? -1 : nv); q0 += NQ) {
         const int nq = min(NQ, nv - q0);
         const double2* src[NQ];

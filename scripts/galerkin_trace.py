@@ -26,7 +26,7 @@ print(f"  {'pass total':24s} {np.mean(np.diff(tr[:, 0])) / 1e3:7.2f} us/pass, {t
 d = np.zeros(8 * 4096, dtype=np.int64)
 L.rafem_get_trace(ctx, d.ctypes.data, d.size)
 g = d[8 * 4000: 8 * 4000 + 10].astype(float) / 1.965e3
-names = ["products (2 sweeps)", "stage D", "dots", "barrier", "fold", "barrier", "read totals",
+names = ["products", "stage D", "dots", "barrier", "fold", "barrier", "read totals",
          "Cholesky + solves", "x0, r0 update"]
 print("last Galerkin start, CTA 0 (us):")
 for k, nm in enumerate(names):
