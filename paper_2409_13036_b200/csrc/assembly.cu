@@ -417,6 +417,114 @@ __global__ void __launch_bounds__(256) fused_fill_half_kernel(AsmMesh m, double 
     if (i >= m.N) return;  // whole half-warps exit together
     fill_node_fused_half(i, m, rk, rrc, sig, load4, val2, rhs, diag_raw, ws[threadIdx.x >> 4]);
 }
+// The same half-warp fill as a persistent grid-stride loop with a software
+// pipeline across rows: while row i's element data are fetched and summed,
+// the incidence records of row i + s and the row / incidence pointers of
+// row i + 2s are already in flight, so each row exposes one dependent
+// round trip (the element data) instead of three.  Per row the arithmetic
+// and the walk are fill_node_fused_half's, so the values are bitwise equal.
+struct FillMeta {
+    int r0, deg, p0, ninc, dslot;
+};
+RF_DEV FillMeta fill_meta(const AsmMesh& m, int i) {
+    FillMeta t{0, 0, 0, 0, -1};
+    if (i < m.N) {
+        t.r0 = __ldg(m.rp + i);
+        t.deg = __ldg(m.rp + i + 1);  // end; made a count on use
+        t.p0 = __ldg(m.inc_ptr + i);
+        t.ninc = __ldg(m.inc_ptr + i + 1);
+        t.dslot = __ldg(m.diag + i);
+    }
+    return t;
+}
+__global__ void __launch_bounds__(256) fused_fill_half_pipe_kernel(AsmMesh m, double dt, const double* sig,
+                                                                   const double* load4, double2* val2, double* rhs,
+                                                                   double* diag_raw) {
+    __shared__ FillScratch wsa[16];
+    __shared__ double rk[kFillRegions], rrc[kFillRegions];
+    for (int r = threadIdx.x; r < m.nreg; r += blockDim.x) {
+        rk[r] = m.regtab[r];
+        rrc[r] = m.regtab[m.nreg + r] / dt;  // element_core's rcdt
+    }
+    __syncthreads();
+    FillScratch& ws = wsa[threadIdx.x >> 4];
+    const int lane = threadIdx.x & 31, hl = lane & 15;
+    const unsigned hmask = 0xffffu << (lane & 16);
+    const int s = (int)(((long long)gridDim.x * blockDim.x) >> 4);
+    int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 4);
+    // pipeline fill: meta of i and i + s, incidence records of i
+    FillMeta cur = fill_meta(m, i);
+    FillMeta nxt = fill_meta(m, i + s);
+    auto inc_load = [&](const FillMeta& t, unsigned& ea, unsigned& eb, unsigned& oa, unsigned& ob) {
+        const int n = t.ninc - t.p0;
+        ea = eb = oa = ob = 0;
+        if (hl < n) {
+            ea = __ldg(m.inc_ea + t.p0 + hl);
+            oa = __ldg(m.inc_slot + t.p0 + hl);
+        }
+        if (hl + 16 < n) {
+            eb = __ldg(m.inc_ea + t.p0 + hl + 16);
+            ob = __ldg(m.inc_slot + t.p0 + hl + 16);
+        }
+    };
+    unsigned ea, eb, oa, ob;
+    inc_load(cur, ea, eb, oa, ob);
+    for (; i < m.N; i += s) {
+        // in flight while this row is processed
+        const FillMeta nn = fill_meta(m, i + 2 * s);
+        unsigned ean, ebn, oan, obn;
+        inc_load(nxt, ean, ebn, oan, obn);
+        const int r0 = cur.r0, deg = cur.deg - cur.r0, ninc = cur.ninc - cur.p0, dslot = cur.dslot;
+        const bool ha = hl < ninc, hb = hl + 16 < ninc;
+        __syncwarp(hmask);  // the previous row's walk is done with ws
+        if (ha) ws.off[hl] = oa;
+        if (hb) ws.off[hl + 16] = ob;
+        RowLoads la, lb;
+        if (ha) row_loads(ea, m, sig, load4, la);
+        if (hb) row_loads(eb, m, sig, load4, lb);
+        if (ha) {
+            row_contrib(ea, la, rk, rrc, ws.c[hl]);
+            ws.ld[hl] = la.ld;
+        }
+        if (hb) {
+            row_contrib(eb, lb, rk, rrc, ws.c[hl + 16]);
+            ws.ld[hl + 16] = lb.ld;
+        }
+        __syncwarp(hmask);
+        double accV = 0.0, accT = 0.0, racc = 0.0;
+        const unsigned lrep = (unsigned)hl * 0x01010101u;
+#pragma unroll 4
+        for (int q = 0; q < ninc; ++q) {
+            const unsigned hit = __vcmpeq4(ws.off[q], lrep);
+            const double2 c = ws.c[q][(__ffs(hit | 0x80000000u) - 1) >> 3];
+            const double av = add(accV, c.x), at = add(accT, c.y);
+            accV = hit ? av : accV;
+            accT = hit ? at : accT;
+            racc = add(racc, ws.ld[q]);  // (used by lane 0 only)
+        }
+        if (hl < deg) {
+            val2[r0 + hl] = make_double2(accV, accT);
+            if (hl == dslot) {
+                diag_raw[2LL * i] = accV;
+                diag_raw[2LL * i + 1] = accT;
+            }
+        }
+        if (hl == 0) {
+            rhs[2LL * i] = 0.0;
+            rhs[2LL * i + 1] = racc;
+            if (dslot < 0) {
+                diag_raw[2LL * i] = 0.0;
+                diag_raw[2LL * i + 1] = 0.0;
+            }
+        }
+        cur = nxt;
+        nxt = nn;
+        ea = ean;
+        eb = ebn;
+        oa = oan;
+        ob = obn;
+    }
+}
 __global__ void __launch_bounds__(256) fused_fill_kernel(AsmMesh m, double dt, const double* sig, const double* load4,
                                                          double2* val2, double* rhs, double* diag_raw) {
     __shared__ FillScratch ws[8];
@@ -839,7 +947,20 @@ int assemble_fill_launch(rafem_system* s, const double* t_it, int ts, const doub
         }
         if (N > 0) {
             const char* hf = getenv("RAFEM_HALF_FILL");
-            if (m->maxdeg <= 16 && m->maxinc <= 32 && m->nreg <= kFillRegions && !(hf && hf[0] == '0')) {
+            const char* fp = getenv("RAFEM_FILL_PIPE");
+            if (m->maxdeg <= 16 && m->maxinc <= 32 && m->nreg <= kFillRegions && !(hf && hf[0] == '0') &&
+                !(fp && fp[0] == '0')) {
+                // persistent: the blocks that fit at once (whole waves), or fewer for small meshes
+                static int occ = 0;
+                if (!occ) {
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_fill_half_pipe_kernel, 256, 0);
+                    occ = std::max(occ, 1);
+                }
+                const long long need = ((long long)N * 16 + 255) / 256;
+                const long long blocks = std::min<long long>(need, (long long)occ * ctx->sm_count);
+                fused_fill_half_pipe_kernel<<<(unsigned)blocks, 256, 0, st>>>(am, dt, s->esig, s->eload, val2,
+                                                                              s->rhs, s->diagpart);
+            } else if (m->maxdeg <= 16 && m->maxinc <= 32 && m->nreg <= kFillRegions && !(hf && hf[0] == '0')) {
                 const long long blocks = ((long long)N * 16 + 255) / 256;
                 fused_fill_half_kernel<<<(unsigned)blocks, 256, 0, st>>>(am, dt, s->esig, s->eload, val2, s->rhs,
                                                                          s->diagpart);

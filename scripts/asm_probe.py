@@ -1,5 +1,7 @@
-"""Assembly A/B at benchmark sizes: fused element+fill (default) vs the
-element kernel + contributor-list fill (RAFEM_FUSED_FILL=0).  Times one
+"""Assembly A/B at benchmark sizes: fused element+fill with the pipelined
+half-warp fill (default) vs the same fill without the row pipeline
+(RAFEM_FILL_PIPE=0), the warp fill (RAFEM_HALF_FILL=0) and the element
+kernel + contributor-list fill (RAFEM_FUSED_FILL=0).  Times one
 device-field assembly (rafem_sl_assemble_partial + rafem_assemble_finish,
 incl. the diagonal-sum read-back) and checks the two paths bitwise.
 
@@ -33,10 +35,11 @@ def main():
     sums = np.zeros(2)
     bad = C.c_int64()
     out = {}
-    for mode, half in (("1", "1"), ("1", "0"), ("0", "1"), ("1", "1")):
+    for mode, half, pipe in (("1", "1", "1"), ("1", "1", "0"), ("1", "0", "1"), ("0", "1", "1"), ("1", "1", "1")):
         os.environ["RAFEM_FUSED_FILL"] = mode
         os.environ["RAFEM_HALF_FILL"] = half
-        mode = mode + half
+        os.environ["RAFEM_FILL_PIPE"] = pipe
+        mode = mode + half + pipe
         ts = []
         for _ in range(reps):
             torch.cuda.synchronize()
@@ -48,11 +51,11 @@ def main():
         vals = sh.h.download_vals()
         rhs = sh.h.rhs()
         out.setdefault(mode, (vals, rhs))
-        print(f"fused,half={mode}: {dims} N={dm.node_count} M={dm.tet_count}: assembly {1e3 * min(ts):.2f} ms "
+        print(f"fused,half,pipe={mode}: {dims} N={dm.node_count} M={dm.tet_count}: assembly {1e3 * min(ts):.2f} ms "
               f"(median {1e3 * sorted(ts)[len(ts) // 2]:.2f})", flush=True)
-    for k in ("10", "01"):
-        same = np.array_equal(out["11"][0], out[k][0]) and np.array_equal(out["11"][1], out[k][1])
-        print(f"fused half-warp == {k} (fused, half) bitwise:", same)
+    for k in ("110", "101", "011"):
+        same = np.array_equal(out["111"][0], out[k][0]) and np.array_equal(out["111"][1], out[k][1])
+        print(f"pipelined half-warp fill == {k} (fused, half, pipe) bitwise:", same)
 
 
 if __name__ == "__main__":
