@@ -379,22 +379,31 @@ RF_DEV void multidot_smem(const double* Vs, int ld, int nv, const double* w, int
 // w == nullptr: the u rows only.  One warp per j, as multidot_smem.
 RF_DEV void multidot_pair_smem(const double* Vs, int ld, int k, const double* u, const double* w, int lo, int hi,
                                double* P, int ldp) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int j = wid; j <= k; j += nw) {
+    // one half-warp per j (all k + 1 in one round for k < 32 at 512 threads),
+    // lanes striding the dofs, a fixed xor-butterfly over the 16 lanes
+    const int hl = threadIdx.x & 15, hw = threadIdx.x >> 4, nh = blockDim.x >> 4;
+    const int jend = ((k + 1 + nh - 1) / nh) * nh;  // whole rounds: every lane shuffles
+    for (int j = hw; j < jend; j += nh) {
+        const bool on = j <= k;
         const double* vj = j < k ? Vs + (long long)j * ld - lo : u;
         double sa = 0.0, sb = 0.0;
-        if (w) {
-            for (int e = lo + lane; e < hi; e += 32) {
-                const double v = vj[e];
-                sa = add(sa, mul(v, u[e]));
-                sb = add(sb, mul(v, w[e]));
+        if (on) {
+            if (w) {
+                for (int e = lo + hl; e < hi; e += 16) {
+                    const double v = vj[e];
+                    sa = add(sa, mul(v, u[e]));
+                    sb = add(sb, mul(v, w[e]));
+                }
+            } else {
+                for (int e = lo + hl; e < hi; e += 16) sa = add(sa, mul(vj[e], u[e]));
             }
-            sb = warp_sum(sb);
-        } else {
-            for (int e = lo + lane; e < hi; e += 32) sa = add(sa, mul(vj[e], u[e]));
         }
-        sa = warp_sum(sa);
-        if (lane == 0) {
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+            sa = add(sa, __shfl_xor_sync(0xffffffffu, sa, o));
+            sb = add(sb, __shfl_xor_sync(0xffffffffu, sb, o));
+        }
+        if (on && hl == 0) {
             double* pc = P + (long long)blockIdx.x * ldp;
             pc[j] = sa;
             if (w) pc[k + 1 + j] = sb;

@@ -123,7 +123,11 @@ RF_DEV void galerkin_start(const KArgs& a, const R& rows, Sync<Mode>& sy, const 
             const int j = q0 + q;
             src[q] = reinterpret_cast<const double2*>(j < 0 ? xsrc : (j < nv ? dvec(j) : xsrc));
         }
-        const int team = a.team, tl = tid & (team - 1), nteams = blockDim.x / team;
+        // its own team width: the largest with every row in one round (the
+        // solver's SpMV team is sized for two rows per thread group)
+        int team = 1;
+        while (team < 8 && (g1 - g0) * team * 2 <= (int)blockDim.x) team *= 2;
+        const int tl = tid & (team - 1), nteams = blockDim.x / team;
         for (int gb = g0; gb < g1; gb += nteams) {
             const int g = gb + tid / team;
             double acc[2 * NQ];

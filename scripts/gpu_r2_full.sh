@@ -14,5 +14,6 @@ PREC=block_jacobi timeout 900 ncu --set full --import-source on --clock-control 
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:spmv_tma -s 5 -c 1 -o gpurun_out/prof_spmv_c3 -f python scripts/c3_spmv.py >> gpurun_out/ncu_ll.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:"kp_spmv|kp_update" -s 10 -c 2 -o gpurun_out/prof_kp_c4 -f python scripts/kp_probe.py >> gpurun_out/ncu_ll.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:"fused_fill|element_scalars|constrain" -c 3 -o gpurun_out/prof_asm_c4 -f python scripts/asm_probe.py 200 200 200 1 >> gpurun_out/ncu_ll.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:gmres_grid -s 1 -c 1 -o gpurun_out/prof_gmres -f python scripts/gmres_trace.py >> gpurun_out/ncu_ll.log 2>&1
 fi
 echo done > gpurun_out/round_done.txt
