@@ -94,7 +94,8 @@ struct KArgs {
 
 // Phase timestamps for diagnosis: slot k of iteration i at trace[i*8 + k].
 RF_DEV void stamp(const KArgs& a, long long it, int k) {
-    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && it * 8 + k < a.trace_cap)
+    // (thread and block first: every other thread leaves without loading a.trace)
+    if (threadIdx.x == 0 && blockIdx.x == 0 && a.trace && it * 8 + k < a.trace_cap)
         a.trace[it * 8 + k] = clock64();
 }
 
@@ -1758,9 +1759,9 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
             sy.barrier();
         }
         // alpha_{i+1} = gn / (dn - beta gn / alpha_i), beta = gn / gamma, is
-        // evaluated as gn / (dn - (gn * ig) * gn) with ig = 1 / (gamma alpha_i)
-        // formed while the previous update streams: one division (not three
-        // plus a square root) between the gathered scalars and the update.
+        // evaluated as gn / (dn - (gn * ig) * gn) with ig = 1 / (gamma alpha_i):
+        // one division per iteration (not three plus a square root), all
+        // scalars from q = 1 / (gn den) (below).
         // The convergence test compares squared norms; the history keeps the
         // squared estimates and is rescaled once after the solve.
         double alpha = 0.0, ig = 0.0, igam = 0.0;
@@ -1801,13 +1802,12 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
             stamp(a, total, 1);
             par ^= 1;
             const double gn = co[0], dn = co[1];
-            double beta = 0.0;
+            double beta = 0.0, den = dn;
             if (first) {
                 if (!(gn > 0.0) || !(dn > 0.0) || !isfinite(gn) || !isfinite(dn)) {
                     status = RAFEM_ERR_BREAKDOWN;
                     break;
                 }
-                alpha = gn / dn;
             } else {
                 ++total;
                 const double rr = co[2];
@@ -1815,12 +1815,22 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                 ++hlen;
                 if (rr <= thr || total >= a.cap) break;
                 beta = gn * igam;
-                const double den = fma(-(gn * ig), gn, dn);
+                den = fma(-(gn * ig), gn, dn);
                 if (!(gn > 0.0) || !(den > 0.0) || !isfinite(den)) {
                     status = RAFEM_ERR_BREAKDOWN;
                     break;
                 }
-                alpha = gn / den;
+            }
+            // ONE division per iteration: with q = 1 / (gn den),
+            // alpha = gn / den = gn^2 q, 1 / gn = den q and 1 / (gn alpha) =
+            // den / gn^2 (the next iteration's beta and den).  Two more
+            // divisions after the update were 11.5 % of the simulation
+            // kernel's stall samples (ncu r2f, scripts/sass_line_stalls.py).
+            {
+                const double q = 1.0 / (gn * den);
+                alpha = (gn * gn) * q;
+                igam = den * q;
+                ig = (den * igam) * igam;
             }
             double* mn = mb(cur ^ 1);
             double v[3] = {0.0, 0.0, 0.0};
@@ -1860,9 +1870,6 @@ RF_DEV PcgOut pcg_pipe_core(const KArgs& a, const R& rows, Sync<Mode>& sy, doubl
                 v[2] = add(v[2], mul(rn, rn));
             }
             stamp(a, total, 7);
-            // 1 / gn and 1 / (gn alpha) are first needed by the next iteration
-            igam = 1.0 / gn;
-            ig = 1.0 / (gn * alpha);
             // the CTA's dot partials: groups of 4 lanes pre-combine theirs
             // (owner dofs sit on threads < 2 * kPipeRows), the 64 group sums
             // per value go through shared memory (`red`, 256 doubles, is not
