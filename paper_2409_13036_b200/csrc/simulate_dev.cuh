@@ -92,7 +92,11 @@ RF_DEV void galerkin_start(const KArgs& a, const R& rows, Sync<Mode>& sy, const 
     double* sR = scr;                    // r0 = b - A x0 (own dofs)
     double* sD = scr + nd;               // d_j (own dofs), j < nv
     double* sAD = sD + (size_t)nv * nd;  // A d_j
-    auto dvec = [&](int j) { return D + (size_t)((head - 1 - j + 2 * K) % K) * n2; };  // most recent first
+    // ring rows, most recent first (the modulo once per start, not per use)
+    __shared__ const double* sdrow[kGalMax];
+    if (tid < nv) sdrow[tid] = D + (size_t)((head - 1 - tid + 2 * K) % K) * n2;
+    __syncthreads();
+    auto dvec = [&](int j) { return sdrow[j]; };
     // RAFEM trace on: phase clocks of the last start (CTA 0) at trace[8 * 4000 + k]
 #define GAL_STAMP(k) \
     if (a.trace && cta == 0 && tid == 0 && 8 * 4000 + (k) < a.trace_cap) a.trace[8 * 4000 + (k)] = clock64()
@@ -101,15 +105,11 @@ RF_DEV void galerkin_start(const KArgs& a, const R& rows, Sync<Mode>& sy, const 
     // the d_j rows (own dofs) stream into shared memory while the products run
     if (!(nd & 1)) {
         const int h = nd >> 1;
-        for (int q = tid; q < nv * h; q += blockDim.x) {
-            const int j = q / h, e2 = q - j * h;
-            cp_async16(sD + (size_t)j * nd + 2 * e2, dvec(j) + lo + 2 * e2);
-        }
+        for (int j = 0; j < nv; ++j)
+            for (int e2 = tid; e2 < h; e2 += blockDim.x) cp_async16(sD + (size_t)j * nd + 2 * e2, dvec(j) + lo + 2 * e2);
     } else {
-        for (int q = tid; q < nv * nd; q += blockDim.x) {
-            const int j = q / nd, e = q - j * nd;
-            cp_async8(sD + q, dvec(j) + lo + e);
-        }
+        for (int j = 0; j < nv; ++j)
+            for (int e = tid; e < nd; e += blockDim.x) cp_async8(sD + (size_t)j * nd + e, dvec(j) + lo + e);
     }
     // products of the slice with x0 and the d_j, six sources per sweep (a
     // team of lanes per row; a lane's slots and all their gathers issued
