@@ -447,3 +447,33 @@ def test_one_reduce_gmres_matches_cgs2(dims, monkeypatch):
         h2 = np.concatenate([np.asarray(c) for c in s2.residual_history])
         assert np.all(np.abs(h1 - h2) <= 1e-5 * h2 + 1e-15)
         assert rel_err(x1, x2) < 1e-12
+
+
+@pytest.mark.parametrize("m,cap", [(1, 40), (2, 0), (5, 0), (30, 37)])
+def test_one_reduce_gmres_restart_lengths_and_cap(m, cap, monkeypatch):
+    """Short restart cycles (the column of step k is final one step later,
+    so m = 1 exercises a cycle of one SpMV and two reductions) and an
+    iteration cap that lands mid-cycle: the one-reduce step and the CGS2
+    step agree on inner steps, restarts, convergence and the solution."""
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, assemble_global, generate_box_mesh, solve
+    mesh = generate_box_mesh(6, 5, 7)
+    n = mesh.node_count
+    rng = np.random.default_rng(29 + m)
+    t, v = 37.0 + rng.uniform(0, 30, n), rng.uniform(0, 25, n)
+    s = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, v, t, 0.5)
+    a, b = s.matrix, s.rhs
+    kw = dict(backend="gmres", precondition="jacobi", tolerance=1e-10, restart_m=m)
+    if cap:
+        kw["max_total_iters"] = cap
+    cfg = SolverConfig(**kw)
+    x1, s1 = solve(a, b, config=cfg)
+    monkeypatch.setenv("RAFEM_GMRES_CGS2", "1")
+    x2, s2 = solve(a, b, config=cfg)
+    monkeypatch.delenv("RAFEM_GMRES_CGS2")
+    assert (s1.iterations, s1.restarts, s1.converged) == (s2.iterations, s2.restarts, s2.converged)
+    if cap:
+        assert s1.iterations == cap and not s1.converged
+    else:
+        res = np.linalg.norm(b - O.matvec(a.row_ptr, a.col_idx, a.vals, x1)) / np.linalg.norm(b)
+        assert s1.converged and res <= 1e-10
+    assert rel_err(x1, x2) < 1e-10
