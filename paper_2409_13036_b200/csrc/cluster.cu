@@ -509,7 +509,7 @@ RF_DEV CpcgOut cpcg_core(CEnv& E, const CRowC (&rc)[RPT], CRow (&R)[RPT], const 
             }
         c_publish<false>(E, v0, v1, v2, 0.0);
         int cur = hb;
-        double alpha = 0.0, ig = 0.0, igam = 0.0, dnm = 0.0;
+        double alpha = 0.0, ig = 0.0, igam = 0.0;
         bool first = true;
         const int hstart = hlen;
         const double thr = (E.tol * bnorm) * (E.tol * bnorm);
@@ -534,11 +534,15 @@ RF_DEV CpcgOut cpcg_core(CEnv& E, const CRowC (&rc)[RPT], CRow (&R)[RPT], const 
                 const double gn = co[0], dn = co[1];
                 double beta = 0.0;
                 int flag = 0;  // 1: leave for the head (converged estimate / cap), 2: breakdown
+                // one division: q = 1 / (gn den) gives alpha = gn^2 q, 1 / gn =
+                // den q and 1 / (gn alpha) = den / gn^2 for the next iteration
+                double den = dn;
+                bool go = false;
                 if (first) {
                     if (!(E.abl & 8) && (!(gn > 0.0) || !(dn > 0.0) || !isfinite(gn) || !isfinite(dn)))
                         flag = 2;
                     else
-                        alpha = gn / dn;
+                        go = true;
                 } else {
                     const double rr = co[2];
                     if (lead && E.hist && hlen < E.hist_cap) E.hist[hlen] = rr;
@@ -546,22 +550,23 @@ RF_DEV CpcgOut cpcg_core(CEnv& E, const CRowC (&rc)[RPT], CRow (&R)[RPT], const 
                         flag = 1;
                     } else {
                         beta = gn * igam;
-                        const double den = fma(-(gn * ig), gn, dn);
-                        if (!(E.abl & 8) && (!(gn > 0.0) || !(den > 0.0) || !isfinite(den))) {
+                        den = fma(-(gn * ig), gn, dn);
+                        if (!(E.abl & 8) && (!(gn > 0.0) || !(den > 0.0) || !isfinite(den)))
                             flag = 2;
-                        } else {
-                            alpha = gn / den;
-                            dnm = den;
-                        }
+                        else
+                            go = true;
                     }
+                }
+                if (go) {
+                    const double q = 1.0 / (gn * den);
+                    alpha = (gn * gn) * q;
+                    igam = den * q;
+                    ig = (den * igam) * igam;
                 }
                 if (threadIdx.x == 0) {
                     sts2(E.sc_s, make_double2(alpha, beta));
                     sts2(E.sc_s + 16u, make_double2((double)flag, 0.0));
                 }
-                // 1 / gn and 1 / (gn alpha) = den / gn^2 for the next iteration
-                igam = 1.0 / gn;
-                ig = (first ? dn : dnm) * igam * igam;
                 __syncwarp();
                 asm volatile("bar.arrive 1, %0;" ::"r"((int)blockDim.x) : "memory");
 #pragma unroll
