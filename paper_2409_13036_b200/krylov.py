@@ -257,10 +257,12 @@ def solve(a, b, x0=None, config=None, session=None, tracer=None, trace_step=-1,
             f"backend {backend!r} is a direct CPU solver outside the B200 path; "
             "use backend='gmres' (reference algorithm) or 'pcg'")
     t0 = time.perf_counter_ns()
-    if backend == "gmres":
-        x, stats = gmres(a, b, x0, config)
+    # b is checked above; gmres()/pcg() would check it a second time
+    x0 = _check_x0(x0, a.nrows)
+    if a.nrows == 0:
+        x, stats = np.zeros(0), SolveStats()
     else:
-        x, stats = pcg(a, b, x0, config)
+        x, stats = _device_solve(a, b, x0, config, nat.METHOD_GMRES if backend == "gmres" else nat.METHOD_PCG)
     stats.wall_ns = max(time.perf_counter_ns() - t0, 1)
     return x, stats
 
