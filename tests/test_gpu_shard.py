@@ -69,7 +69,7 @@ def test_single_shard_matches_assemble_global_and_persistent_pcg():
     assert st4.converged and not np.any(x4)
 
 
-def _shard_worker(rank, world, port, dims, out_dir):
+def _shard_worker(rank, world, port, dims, out_dir, tol=1e-10):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -89,7 +89,7 @@ def _shard_worker(rank, world, port, dims, out_dir):
         rp, gcol, vals = sh.owned_rows()
         x0 = np.empty(2 * n)
         x0[0::2], x0[1::2] = v, t
-        cfg = SolverConfig(backend="pcg", precondition="jacobi", tolerance=1e-10)
+        cfg = SolverConfig(backend="pcg", precondition="jacobi", tolerance=tol)
         x, st = sh.solve(x0=x0[2 * p.lo:2 * p.hi], config=cfg)
         np.savez(os.path.join(out_dir, f"s{rank}.npz"), x=x, lo=p.lo, hi=p.hi, it=st.iterations,
                  rel=st.final_relative_residual, conv=st.converged, scale=scale, rp=rp, gcol=gcol, vals=vals,
@@ -409,3 +409,41 @@ def test_ipc_data_plane_time_loop_is_bitwise_the_host_collectives(tmp_path):
     for pa, pb in zip(a, b):
         assert np.array_equal(pa["traj"], pb["traj"]) and int(pa["inner"]) == int(pb["inner"])
         assert np.array_equal(pa["T"], pb["T"]) and np.array_equal(pa["V"], pb["V"])
+
+
+def test_sharded_pcg_agrees_with_one_gpu_at_tight_tolerance(tmp_path):
+    """SURVEY §8(c)5's 1e-10 bar for multi-shard solves: at a 1e-13 relative
+    residual the 2-shard solve (ranks sharing the GPU, host-staged
+    collectives), the single-shard engine and the persistent one-GPU PCG
+    agree within 1e-10 of the solution's peak (at the default 1e-10 they
+    only can to ~1e-7: two solves to a 1e-10 residual from the same start)."""
+    import torch.multiprocessing as mp
+    from paper_2409_13036_b200 import MaterialParams, SimConfig, SolverConfig, assemble_global, generate_box_mesh, solve
+    from paper_2409_13036_b200.shard import ShardedSystem
+    dims, tol = (14, 9, 10), 1e-13
+    port = 29700 + (os.getpid() % 200)
+    mp.start_processes(_shard_worker, args=(2, port, dims, str(tmp_path), tol), nprocs=2, join=True,
+                       start_method="spawn")
+    mesh = generate_box_mesh(*dims)
+    n = mesh.node_count
+    t, v = _hot(n)
+    ref = assemble_global(mesh, MaterialParams.default(), SimConfig(), t, v, t, 0.5)
+    a = ref.matrix
+    x = np.empty(2 * n)
+    for r in range(2):
+        d = np.load(tmp_path / f"s{r}.npz")
+        x[2 * int(d["lo"]):2 * int(d["hi"])] = d["x"]
+        assert bool(d["conv"])
+    x0 = np.empty(2 * n)
+    x0[0::2], x0[1::2] = v, t
+    cfg = SolverConfig(backend="pcg", precondition="jacobi", tolerance=tol)
+    xp, sp = solve(a, ref.rhs, x0=x0, config=cfg)
+    assert sp.converged
+    sh = ShardedSystem(mesh, MaterialParams.default())
+    sh.assemble(t, v, t, 0.5, SimConfig())
+    x1, s1 = sh.solve(x0=x0, config=cfg)
+    assert s1.converged
+    peak = np.max(np.abs(xp))
+    assert np.max(np.abs(x - xp)) <= 1e-10 * peak
+    assert np.max(np.abs(x1 - xp)) <= 1e-10 * peak
+    assert np.max(np.abs(x - x1)) <= 1e-10 * peak
