@@ -114,9 +114,11 @@ def test_gmres_matches_dense_on_golden_systems():
         assert abs(st.final_relative_residual - res) < 1e-12
         if float(tol) <= 1e-10:
             assert rel_err(x, d[f"c{c}_x_dense"]) < 1e-8
-        # same algorithm: iteration counts track the reference's MGS run closely
-        it_ref = int(d[f"c{c}_stats"][0])
-        assert abs(st.iterations - it_ref) <= max(2, 0.1 * it_ref)
+        # same algorithm: inner steps and restarts equal the reference's MGS
+        # run on every golden case (one-reduce Arnoldi vs MGS: the same
+        # Krylov basis to working precision)
+        it_ref, rs_ref = int(d[f"c{c}_stats"][0]), int(d[f"c{c}_stats"][1])
+        assert (st.iterations, st.restarts) == (it_ref, rs_ref)
 
 
 @pytest.mark.parametrize("seed", [201, 202, 401])
