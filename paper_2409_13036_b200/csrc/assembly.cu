@@ -826,7 +826,8 @@ int mesh_stencil_classes(rafem_mesh* m) {
         const int i = rep[c], d = rp[i + 1] - rp[i];
         deg[c] = d;
         std::vector<int> cc(d);
-        RF_CUDA_TRY(ctx, cudaMemcpy(cc.data(), m->col + rp[i], sizeof(int) * d, cudaMemcpyDeviceToHost));
+        RF_CUDA_TRY(ctx, cudaMemcpyAsync(cc.data(), m->col + rp[i], sizeof(int) * d, cudaMemcpyDeviceToHost, ctx->stream));
+        RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
         for (int k = 0; k < d; ++k) off[(size_t)c * kClsWidth + k] = cc[k] - i;
     }
     uint8_t* dcls = nullptr;

@@ -47,6 +47,7 @@ cudaError_t dmalloc(rafem_ctx* ctx, void** p, size_t bytes) {
     if (it != ctx->free_blocks.end() && it->first <= 2 * bytes) {  // reuse a block of close size
         *p = it->second;
         ctx->cached_bytes -= it->first;
+        ctx->free_set.erase(it->second);
         ctx->free_blocks.erase(it);
         return cudaSuccess;
     }
@@ -67,6 +68,12 @@ void dfree(rafem_ctx* ctx, void* p) {
         cudaFree(p);
         return;
     }
+    if (!ctx->free_set.insert(p).second) {  // already free: a second release would alias two later blocks
+        if (ctx->double_frees++ == 0)
+            if (const char* dbg = getenv("RAFEM_DEBUG_ALLOC"))
+                if (dbg[0] == '1') std::fprintf(stderr, "rafem: double free of device block %p ignored\n", p);
+        return;
+    }
     ctx->free_blocks.emplace(it->second, p);
     ctx->cached_bytes += it->second;
     // keep at most 8 GiB cached
@@ -74,6 +81,7 @@ void dfree(rafem_ctx* ctx, void* p) {
         auto big = std::prev(ctx->free_blocks.end());
         cudaFree(big->second);
         ctx->block_size.erase(big->second);
+        ctx->free_set.erase(big->second);
         ctx->cached_bytes -= big->first;
         ctx->free_blocks.erase(big);
     }
@@ -86,6 +94,7 @@ void dcache_release(rafem_ctx* ctx) {
         ctx->block_size.erase(kv.second);
     }
     ctx->free_blocks.clear();
+    ctx->free_set.clear();
     ctx->cached_bytes = 0;
 }
 
@@ -354,7 +363,9 @@ int rafem_set_trace(rafem_ctx* ctx, int32_t on) {
 int64_t rafem_get_trace(rafem_ctx* ctx, int64_t* out, int64_t cap) {
     if (!ctx || !ctx->ws_trace.p) return 0;
     const int64_t n = std::min<int64_t>(cap, (int64_t)(ctx->ws_trace.bytes / sizeof(long long)));
-    if (cudaMemcpy(out, ctx->ws_trace.p, sizeof(long long) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+    if (cudaMemcpyAsync(out, ctx->ws_trace.p, sizeof(long long) * n, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+        return 0;
     return n;
 }
 
@@ -510,11 +521,14 @@ int rafem_mesh_create(rafem_ctx* ctx, int64_t n_nodes, const double* nodes, int6
     RF_MS(dmalloc(ctx, (void**)&m->region, sizeof(int) * M));
     RF_MS(dmalloc(ctx, (void**)&m->regtab, sizeof(double) * 5 * n_regions));
     RF_MS(dmalloc(ctx, (void**)&m->kind, 2 * N));
-    RF_MS(cudaMemcpy(m->nodes, nodes, sizeof(double) * 3 * n_nodes, cudaMemcpyHostToDevice));
-    RF_MS(cudaMemcpy(m->tets, t32.data(), sizeof(int) * 4 * n_tets, cudaMemcpyHostToDevice));
-    RF_MS(cudaMemcpy(m->region, reg.data(), sizeof(int) * n_tets, cudaMemcpyHostToDevice));
-    RF_MS(cudaMemcpy(m->regtab, tab.data(), sizeof(double) * 5 * n_regions, cudaMemcpyHostToDevice));
-    RF_MS(cudaMemcpy(m->kind, dof_kind, 2 * n_nodes, cudaMemcpyHostToDevice));
+    // every copy on the library stream (non-blocking: legacy-stream copies
+    // are not ordered with it); the host vectors live until the sync below
+    RF_MS(cudaMemcpyAsync(m->nodes, nodes, sizeof(double) * 3 * n_nodes, cudaMemcpyHostToDevice, ctx->stream));
+    RF_MS(cudaMemcpyAsync(m->tets, t32.data(), sizeof(int) * 4 * n_tets, cudaMemcpyHostToDevice, ctx->stream));
+    RF_MS(cudaMemcpyAsync(m->region, reg.data(), sizeof(int) * n_tets, cudaMemcpyHostToDevice, ctx->stream));
+    RF_MS(cudaMemcpyAsync(m->regtab, tab.data(), sizeof(double) * 5 * n_regions, cudaMemcpyHostToDevice, ctx->stream));
+    RF_MS(cudaMemcpyAsync(m->kind, dof_kind, 2 * n_nodes, cudaMemcpyHostToDevice, ctx->stream));
+    RF_MS(cudaStreamSynchronize(ctx->stream));
 #undef RF_MS
     if (int rc = mesh_symbolic(m)) {
         rafem_mesh_destroy(m);
@@ -580,9 +594,11 @@ int rafem_mesh_pattern(rafem_mesh* m, int64_t* node_row_ptr, int32_t* node_col) 
     if (!m) return RAFEM_ERR_INVALID;
     rafem_ctx* ctx = m->ctx;
     std::vector<int> rp(m->N + 1);
-    RF_CUDA_TRY(ctx, cudaMemcpy(rp.data(), m->rp, sizeof(int) * (m->N + 1), cudaMemcpyDeviceToHost));
+    RF_CUDA_TRY(ctx, cudaMemcpyAsync(rp.data(), m->rp, sizeof(int) * (m->N + 1), cudaMemcpyDeviceToHost, ctx->stream));
+    if (m->slots)
+        RF_CUDA_TRY(ctx, cudaMemcpyAsync(node_col, m->col, sizeof(int) * m->slots, cudaMemcpyDeviceToHost, ctx->stream));
+    RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     for (int i = 0; i <= m->N; ++i) node_row_ptr[i] = rp[i];
-    if (m->slots) RF_CUDA_TRY(ctx, cudaMemcpy(node_col, m->col, sizeof(int) * m->slots, cudaMemcpyDeviceToHost));
     return RAFEM_OK;
 }
 
@@ -604,7 +620,10 @@ int rafem_system_create(rafem_mesh* m, rafem_system** out) {
     RF_SS(dmalloc(ctx, (void**)&s->xin, sizeof(double) * (3 * N + 2 * S)));  // host inputs / dof expansion
     RF_SS(dmalloc(ctx, (void**)&s->status, 1024));
     RF_SS(dmalloc(ctx, (void**)&s->xs, sizeof(double) * 6 * 2 * N));
-    RF_SS(cudaMemset(s->status, 0, 1024));
+    // on the library stream: ctx->stream is non-blocking, so a legacy-stream
+    // cudaMemset could land after the first assembly's reset of the bad-element
+    // flag (seen as a spurious PhysicsRangeError with two processes on a GPU)
+    RF_SS(cudaMemsetAsync(s->status, 0, 1024, ctx->stream));
 #undef RF_SS
     *out = s;
     return RAFEM_OK;
@@ -1021,7 +1040,10 @@ int simulate_host_loop(rafem_system* s, const rafem_sim_params* p, rafem_sim_sum
     }
     RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
     // keep the final accepted state at the front of xs for callers
-    if (xacc != s->xs) RF_CUDA_TRY(ctx, cudaMemcpy(s->xs, xacc, sizeof(double) * n2, cudaMemcpyDeviceToDevice));
+    if (xacc != s->xs) {
+        RF_CUDA_TRY(ctx, cudaMemcpyAsync(s->xs, xacc, sizeof(double) * n2, cudaMemcpyDeviceToDevice, st));
+        RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    }
     out->accepted_steps = step;
     out->total_corrector_iters = total_corr;
     out->total_solver_iterations = total_inner;
@@ -1159,16 +1181,21 @@ int rafem_simulate(rafem_system* s, const rafem_sim_params* p, rafem_sim_summary
             if (nrec > 0) {
                 std::vector<double> ht(nrec), hd(nrec);
                 std::vector<int> hi(nrec);
-                RF_CUDA_TRY(ctx, cudaMemcpy(ht.data(), d_rt, sizeof(double) * nrec, cudaMemcpyDeviceToHost));
-                RF_CUDA_TRY(ctx, cudaMemcpy(hd.data(), d_rd, sizeof(double) * nrec, cudaMemcpyDeviceToHost));
-                RF_CUDA_TRY(ctx, cudaMemcpy(hi.data(), d_ri, sizeof(int) * nrec, cudaMemcpyDeviceToHost));
+                RF_CUDA_TRY(ctx, cudaMemcpyAsync(ht.data(), d_rt, sizeof(double) * nrec, cudaMemcpyDeviceToHost, ctx->stream));
+                RF_CUDA_TRY(ctx, cudaMemcpyAsync(hd.data(), d_rd, sizeof(double) * nrec, cudaMemcpyDeviceToHost, ctx->stream));
+                RF_CUDA_TRY(ctx, cudaMemcpyAsync(hi.data(), d_ri, sizeof(int) * nrec, cudaMemcpyDeviceToHost, ctx->stream));
+                RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
                 for (long long k = 0; k < nrec; ++k) {
                     if (rec_step) rec_step[k] = k;
                     if (rec_time) rec_time[k] = ht[k];
                     if (rec_dt) rec_dt[k] = hd[k];
                     if (rec_iters) rec_iters[k] = hi[k];
                 }
-                if (d_rx) RF_CUDA_TRY(ctx, cudaMemcpy(rec_x, d_rx, sizeof(double) * n2 * nrec, cudaMemcpyDeviceToHost));
+                if (d_rx) {
+                    RF_CUDA_TRY(ctx, cudaMemcpyAsync(rec_x, d_rx, sizeof(double) * n2 * nrec, cudaMemcpyDeviceToHost,
+                                                     ctx->stream));
+                    RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+                }
             }
             release();
             return fused_summary(ctx, so, t_wall, out);

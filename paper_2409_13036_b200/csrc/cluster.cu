@@ -1609,7 +1609,8 @@ static ClusterPlan* cluster_plan(rafem_ctx* ctx, const int* rp_dev, const int* c
                sort_rows = env_on("RAFEM_CL_SORT", true);
     if (coords_dev && use_rcb) {
         std::vector<double> X((size_t)3 * N);
-        e = cudaMemcpy(X.data(), coords_dev, sizeof(double) * 3 * (size_t)N, cudaMemcpyDeviceToHost);
+        e = cudaMemcpyAsync(X.data(), coords_dev, sizeof(double) * 3 * (size_t)N, cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
         if (e != cudaSuccess) {
             rc = rafem_fail_cuda(ctx, e, "cluster plan coordinates", __FILE__, __LINE__);
             return nullptr;

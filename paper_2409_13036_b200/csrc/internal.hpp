@@ -7,6 +7,7 @@
 #include <map>
 #include <string>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/rafem_b200.h"
@@ -110,6 +111,8 @@ struct rafem_ctx {
     // device blocks of destroyed meshes / systems kept for reuse (a new mesh
     // of the same size then costs no cudaMalloc / cudaFree, which synchronise)
     std::multimap<size_t, void*> free_blocks;
+    std::unordered_set<void*> free_set;  // blocks in free_blocks (a second dfree of one is ignored)
+    long long double_frees = 0;
     std::unordered_map<void*, size_t> block_size;
     size_t cached_bytes = 0;
     cudaStream_t side_stream = nullptr;  // record copies of rafem_simulate_stream
