@@ -2684,14 +2684,15 @@ static int spmv_pipe_launch(rafem_ctx* ctx, const MatView& A, const double* x_de
     MatView Av = A;
     const double* xp = x_dev;
     double* yp = y_dev;
-    // per-tile bulk L2 prefetch of the tile's own x rows (RAFEM_XPF=1; off by
-    // default — measured r2, cold L2: C3 36.9 -> 35.7 us, C4 401 -> 416 us
-    // with the default 192 x 2 tiles; it helps only the narrower tiles)
+    // per-tile bulk L2 prefetch of the tile's own x rows (default on;
+    // RAFEM_XPF=0 turns it off) — measured r2h, cold L2, 192 x 2 tiles, three
+    // runs: C3 36.9 -> 35.4-35.7 us, C4 400.4 -> 388.0-388.5 us (an earlier
+    // r2b sweep had C4 slower, 401 -> 416; profiles/r2h_spmv_xpf.txt)
     // (a per-gather L2 prefetch of the next tile's columns — computable from
     // the stencil classes before its matrix tile lands — measured slower at
     // C3: 38.9 vs 37.5 us; profiles/r2b_spmv_x_prefetch_sweep.txt)
     const char* xe = getenv("RAFEM_XPF");
-    int xpf = (xe && xe[0] == '1') ? 1 : 0;
+    int xpf = (xe && xe[0] == '0') ? 0 : 1;
     void* args[] = {&Av, &xp, &yp, &valcap, &bufbytes, &xpf};
     if (ctx->spmv_pdl) {
         cudaLaunchConfig_t lc{};
