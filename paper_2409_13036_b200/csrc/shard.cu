@@ -117,6 +117,7 @@ struct KPArgs {
     int bufbytes, valcap;  // TMA tile buffers
     const KPIpc* ipc;      // device-initiated halo / slots (null: the host's collectives)
     unsigned long long seq_wait, seq_push;  // sequence numbers of this launch's exchange
+    int xpf;               // SpMV: bulk L2 prefetch of each tile's own source rows (RAFEM_KP_XPF=0: off)
 };
 
 RF_DEV bool kp_stopped(const KPState& s) { return s.done || s.need_head; }
@@ -156,6 +157,10 @@ RF_DEV void kp_sweep(const KPArgs& a, const double2* __restrict__ src, unsigned 
         mbar_expect_tx(&bar[b], vb + cb);
         if (vb) tma_load_1d_hint(dst, a.A.val + 2LL * s0, vb, &bar[b], pol);
         if (cb) tma_load_1d_hint(dst + (size_t)a.valcap * 16, a.A.col + sa, cb, &bar[b], pol);
+        // the tile's own source rows into L2 ahead of its gathers (as the
+        // standalone SpMV does); L2 is the point of coherence, so a prefetch
+        // issued before the previous kernel's writes land stays correct
+        if (a.xpf && r1 > r0) prefetch_l2_bulk(src + r0, 16u * (unsigned)(r1 - r0));
     };
     if (threadIdx.x == 0)
         for (int i = 0; i < kKpStages && i < mine; ++i) issue(i);
@@ -704,6 +709,10 @@ int rafem_kp_create(rafem_system* sys, int64_t n_owned, int64_t n_ext, int32_t n
     a.rank = rank;
     a.bufbytes = bufbytes;
     a.valcap = KPT * m->maxdeg;
+    {
+        const char* xe = getenv("RAFEM_KP_XPF");
+        a.xpf = (xe && xe[0] == '0') ? 0 : 1;
+    }
     cudaEventCreate(&k->e0);
     cudaEventCreate(&k->e1);
     for (const void* fn : {(const void*)kp_head_kernel<true, false>, (const void*)kp_head_kernel<false, false>,
