@@ -822,13 +822,19 @@ int mesh_stencil_classes(rafem_mesh* m) {
     }
     const int ncls = (int)keys.size();
     std::vector<int> off((size_t)ncls * kClsWidth, 0), deg(ncls);
-    for (int c = 0; c < ncls; ++c) {
-        const int i = rep[c], d = rp[i + 1] - rp[i];
-        deg[c] = d;
-        std::vector<int> cc(d);
-        RF_CUDA_TRY(ctx, cudaMemcpyAsync(cc.data(), m->col + rp[i], sizeof(int) * d, cudaMemcpyDeviceToHost, ctx->stream));
-        RF_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-        for (int k = 0; k < d; ++k) off[(size_t)c * kClsWidth + k] = cc[k] - i;
+    {  // every class representative's columns in one pinned staging area, one synchronisation
+        int* pc = static_cast<int*>(pinned(ctx, sizeof(int) * (size_t)std::max(ncls, 1) * kClsWidth));
+        if (!pc) return rafem_fail(ctx, RAFEM_ERR_CUDA, "pinned staging allocation failed");
+        for (int c = 0; c < ncls; ++c) {
+            const int i = rep[c], d = rp[i + 1] - rp[i];
+            deg[c] = d;
+            if (d > 0)
+                RF_CUDA_TRY(ctx, cudaMemcpyAsync(pc + (size_t)c * kClsWidth, m->col + rp[i], sizeof(int) * d,
+                                                 cudaMemcpyDeviceToHost, st));
+        }
+        RF_CUDA_TRY(ctx, cudaStreamSynchronize(st));
+        for (int c = 0; c < ncls; ++c)
+            for (int k = 0; k < deg[c]; ++k) off[(size_t)c * kClsWidth + k] = pc[(size_t)c * kClsWidth + k] - rep[c];
     }
     uint8_t* dcls = nullptr;
     int* doff = nullptr;
