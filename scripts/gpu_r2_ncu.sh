@@ -10,7 +10,8 @@ PREC=block_jacobi timeout 900 ncu --set full --import-source on --clock-control 
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:gmres_grid -s 1 -c 1 -o /tmp/prof_gmres -f python scripts/gmres_trace.py >> gpurun_out/ncu_ll.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:spmv_tma -s 5 -c 1 -o /tmp/prof_spmv_c3 -f python scripts/c3_spmv.py >> gpurun_out/ncu_ll.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:"fused_fill|element_scalars|constrain" -c 3 -o /tmp/prof_asm_c4 -f python scripts/asm_probe.py 200 200 200 1 >> gpurun_out/ncu_ll.log 2>&1
-python scripts/ncu_summary.py $TAG gpurun_out/launches_bench.csv /tmp/prof_simulate.ncu-rep /tmp/prof_gmres.ncu-rep /tmp/prof_spmv_c3.ncu-rep /tmp/prof_asm_c4.ncu-rep >> gpurun_out/ncu_ll.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:"kp_spmv|kp_update" -s 10 -c 2 -o /tmp/prof_kp_c4 -f python scripts/kp_probe.py >> gpurun_out/ncu_ll.log 2>&1
+python scripts/ncu_summary.py $TAG gpurun_out/launches_bench.csv /tmp/prof_simulate.ncu-rep /tmp/prof_gmres.ncu-rep /tmp/prof_spmv_c3.ncu-rep /tmp/prof_asm_c4.ncu-rep /tmp/prof_kp_c4.ncu-rep >> gpurun_out/ncu_ll.log 2>&1
 cp profiles/${TAG}_* profiles/traffic.json gpurun_out/prof_txt/ 2>/dev/null
 ncu -i /tmp/prof_simulate.ncu-rep --page source --csv --print-source sass > /tmp/sim_src.csv 2>/dev/null
 ncu -i /tmp/prof_simulate.ncu-rep --page source --csv > gpurun_out/prof_txt/simulate_source_cuda.csv 2>/dev/null
